@@ -1,0 +1,137 @@
+/*
+ * f4b200.h — C ABI of the B200-native F4 hot path (libf4b200.so).
+ *
+ * The reference (arXiv 2601.06765, package `fpgb`) has no FFI: its boundary
+ * is the set of module-level Python functions that the F4 driver calls
+ * (pkg/src/fpgb/groebner.py:32-50, call site f4_step :253-311).  These entry
+ * points are what a binding of that boundary needs; the Python shim
+ * (paper_2601_06765_b200/_capi.py) binds them with ctypes and keeps the
+ * reference signatures.  Each function cites the reference interface it
+ * replaces.
+ *
+ * Conventions
+ *  - Every call returns F4B_OK (0) or an f4b_status code; the message of the
+ *    last failure is available from f4b_ctx_last_error().  Codes map 1:1 onto
+ *    the reference exception classes (pkg/src/fpgb/errors.py).
+ *  - Arrays named h_* / passed as `const T*` without "device" in the comment
+ *    are HOST pointers.  Device memory is owned by the context and obtained
+ *    through the registered allocator (the Python host registers one backed
+ *    by the PyTorch caching allocator); with a NULL allocator cudaMalloc is
+ *    used.
+ *  - All work is issued on the stream set with f4b_ctx_set_stream (default
+ *    stream 0).  One context per (device, ring); calls on one context are not
+ *    thread-safe.
+ *  - Inputs are never modified; every plan / echelon is a fresh object that
+ *    stays valid until freed (reference ownership rule).
+ */
+#ifndef F4B200_H
+#define F4B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum f4b_status {
+  F4B_OK = 0,
+  F4B_ERR_MISSING_KEY = 1,     /* MissingKeyError  (bulk.py:235-240)          */
+  F4B_ERR_SIZE_CAP = 2,        /* SizeCapError     (symbolic.py:359-363)      */
+  F4B_ERR_LANE_OVERFLOW = 3,   /* LaneOverflowError (monomials.py:142-147)    */
+  F4B_ERR_PROPERTY = 4,        /* PropertyViolationError (symbolic.py:214-215)*/
+  F4B_ERR_PRECONDITION = 5,    /* PreconditionError (sparselin.py:288-289)    */
+  F4B_ERR_CUDA = 6,            /* CUDA runtime / launch failure               */
+  F4B_ERR_OOM = 7,             /* device allocation failed                    */
+  F4B_ERR_PROBABILISTIC = 8    /* ProbabilisticFailureError                   */
+};
+
+enum f4b_order { F4B_GREVLEX = 0, F4B_DEGLEX = 1, F4B_LEX = 2 };
+enum f4b_closure { F4B_SUPPORT_ONLY = 0, F4B_ONE_STEP_REDUCTION = 1 };
+enum f4b_psge_mode { F4B_NEW_ONLY = 0, F4B_FULL_RREF = 1 };
+
+typedef void* (*f4b_alloc_fn)(size_t bytes, void* user);
+typedef void (*f4b_free_fn)(void* device_ptr, void* user);
+
+typedef struct f4b_ctx f4b_ctx;
+typedef struct f4b_plan f4b_plan;
+typedef struct f4b_echelon f4b_echelon;
+
+int f4b_abi_version(void);
+
+/* Context = FieldModulus + Ring on one device (fp.py:80-128, monomials.py:40-95). */
+int f4b_ctx_create(int device, uint32_t p, int n_vars, int order, f4b_alloc_fn alloc,
+                   f4b_free_fn dfree, void* user, f4b_ctx** out);
+int f4b_ctx_destroy(f4b_ctx* ctx);
+int f4b_ctx_set_stream(f4b_ctx* ctx, void* cuda_stream);
+const char* f4b_ctx_last_error(const f4b_ctx* ctx);
+
+/* Device-resident basis — replaces soa_pack / SoaPolySet
+ * (polynomials.py:243-299, groebner.py:143-146).  `exps` is [T][n_vars] u16,
+ * `coeffs` [T] standard residues, `lengths` [n_polys]; each polynomial's terms
+ * strictly descending in the term order, leading term first. */
+int f4b_basis_clear(f4b_ctx* ctx);
+int f4b_basis_append(f4b_ctx* ctx, int64_t n_polys, const int64_t* lengths,
+                     const uint16_t* exps, const uint32_t* coeffs);
+int f4b_basis_size(const f4b_ctx* ctx, int64_t* n_polys, int64_t* n_terms);
+
+typedef struct {
+  int64_t r, N, M, closure_rounds, n_closure_rows;
+  int64_t key_words, lane_bits;
+  int64_t dict_build_ns, row_assemble_ns; /* device time (CUDA events) */
+  int64_t sort_passes, kernel_launches;
+} f4b_plan_info;
+
+/* compile_batch (symbolic.py:293-388): rows in select_rows order
+ * (symbolic.py:166-201): row_basis[r], row_shift[r][n_vars].  closure is an
+ * f4b_closure; candidates (may be NULL = all basis polys) restricts the
+ * closure reducers (symbolic.py:228-235).  dict_cap mirrors DICT_CAP. */
+int f4b_compile_batch(f4b_ctx* ctx, int64_t n_rows, const int32_t* row_basis,
+                      const uint16_t* row_shift, int closure, const int32_t* candidates,
+                      int64_t n_candidates, int64_t dict_cap, f4b_plan** out);
+int f4b_plan_get_info(const f4b_plan* plan, f4b_plan_info* info);
+/* LayoutPlan arrays (symbolic.py:99-163) to host memory; any pointer may be NULL.
+ * dict_exps is [N][n_vars], columns in DESCENDING term order (column 0 is the
+ * greatest monomial); closure rows (appended after the input rows) report
+ * their basis index, shift and discovery round. */
+int f4b_plan_download(const f4b_plan* plan, int64_t* row_ptr, int64_t* col_ind, uint64_t* val,
+                      uint16_t* dict_exps, int32_t* closure_basis, uint16_t* closure_shift,
+                      int32_t* closure_round);
+int f4b_plan_free(f4b_plan* plan);
+
+typedef struct {
+  int64_t n_rows, n_cols, rank, zero_rows;
+  int64_t n_pivot_rows, n_nonpivot_rows;  /* pivot rows valid once full */
+  int64_t pivot_nnz, nonpivot_nnz;
+  int64_t full;                           /* 1 once pivot rows are computed */
+  int64_t numeric_ns, backsub_ns;         /* device time (CUDA events) */
+  int64_t dense_rows, dense_cols;         /* D' block shape */
+} f4b_echelon_info;
+
+/* psge_reduce (sparselin.py:281-369) on a compiled plan (no copy) or on a
+ * host CSR (csr_from_arrays, sparselin.py:80-90).  F4B_NEW_ONLY computes the
+ * rows with new leading columns (all the F4 driver consumes,
+ * groebner.py:285-287); F4B_FULL_RREF also back-reduces the pivot rows. */
+int f4b_psge_plan(f4b_ctx* ctx, const f4b_plan* plan, int mode, f4b_echelon** out);
+int f4b_psge_csr(f4b_ctx* ctx, int64_t n_rows, int64_t n_cols, const int64_t* row_ptr,
+                 const int64_t* col_ind, const uint64_t* val, int mode, f4b_echelon** out);
+int f4b_echelon_complete(f4b_ctx* ctx, f4b_echelon* ech); /* NEW_ONLY -> FULL_RREF */
+int f4b_echelon_get_info(const f4b_echelon* ech, f4b_echelon_info* info);
+/* which = 0: pivot rows, 1: nonpivot rows; rows ascending by lead column.
+ * leads[k], row_ptr[k+1], cols/vals concatenated (standard residues). */
+int f4b_echelon_download(const f4b_echelon* ech, int which, int64_t* leads, int64_t* row_ptr,
+                         int64_t* cols, uint64_t* vals);
+/* pivot_cols (ascending, rank entries) — available in both modes. */
+int f4b_echelon_pivot_cols(const f4b_echelon* ech, int64_t* cols);
+int f4b_echelon_free(f4b_echelon* ech);
+
+/* spmm (sparselin.py:142-173): Y = A X mod p; A host CSR (n_rows x n_cols),
+ * X host [n_cols][b], Y host [n_rows][b]; u64 standard residues. */
+int f4b_spmm(f4b_ctx* ctx, int64_t n_rows, int64_t n_cols, const int64_t* row_ptr,
+             const int64_t* col_ind, const uint64_t* val, const uint64_t* X, int64_t b,
+             uint64_t* Y);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* F4B200_H */

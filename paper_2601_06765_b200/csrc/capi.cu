@@ -1,0 +1,466 @@
+// C ABI of libf4b200.so (include/f4b200.h): context, device memory through
+// the registered allocator, the device-resident basis, and the thin wrappers
+// that translate C++ exceptions into f4b_status codes.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "common.cuh"
+#include "engine.h"
+
+struct f4b_ctx {
+  f4b::Ctx c;
+};
+
+namespace f4b {
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw Error{code, msg}; }
+
+void check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    fail(e == cudaErrorMemoryAllocation ? F4B_ERR_OOM : F4B_ERR_CUDA,
+         std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
+static void* raw_alloc(Ctx* c, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  void* p = nullptr;
+  if (c->alloc) {
+    p = c->alloc(bytes, c->user);
+    if (!p) fail(F4B_ERR_OOM, "device allocation of " + std::to_string(bytes) + " bytes failed");
+  } else {
+    check_cuda(cudaMalloc(&p, bytes), "cudaMalloc");
+  }
+  return p;
+}
+
+static void raw_free(Ctx* c, void* p) {
+  if (!p) return;
+  if (c->dfree) c->dfree(p, c->user);
+  else cudaFree(p);
+}
+
+void release(Ctx* c, DBuf& b) {
+  raw_free(c, b.p);
+  b.p = nullptr;
+  b.cap = 0;
+}
+
+void ensure(Ctx* c, DBuf& b, size_t bytes) {
+  if (bytes <= b.cap && b.p) return;
+  release(c, b);
+  size_t cap = std::max<size_t>(bytes + bytes / 4, 256);
+  cap = (cap + 255) & ~(size_t)255;
+  b.p = raw_alloc(c, cap);
+  b.cap = cap;
+}
+
+void ensure_keep(Ctx* c, DBuf& b, size_t bytes) {
+  if (bytes <= b.cap && b.p) return;
+  size_t cap = std::max<size_t>(bytes + bytes / 2, 256);
+  cap = (cap + 255) & ~(size_t)255;
+  void* np = raw_alloc(c, cap);
+  if (b.p && b.cap) check_cuda(cudaMemcpyAsync(np, b.p, b.cap, cudaMemcpyDeviceToDevice, c->stream), "grow copy");
+  raw_free(c, b.p);
+  b.p = np;
+  b.cap = cap;
+}
+
+uint32_t read_u32(Ctx* c, const uint32_t* dptr) {
+  check_cuda(cudaMemcpyAsync(c->h_stat, dptr, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream), "d2h u32");
+  check_cuda(cudaStreamSynchronize(c->stream), "sync");
+  return c->h_stat[0];
+}
+
+void memset_async(Ctx* c, void* p, int v, size_t bytes) { check_cuda(cudaMemsetAsync(p, v, bytes, c->stream), "memset"); }
+
+void plan_release(f4b_plan* pl) {
+  if (!pl) return;
+  Ctx* c = pl->ctx;
+  DBuf* bufs[] = {&pl->row_ptr, &pl->col_ind, &pl->val, &pl->dict, &pl->dict_exps, &pl->cl_basis, &pl->cl_shift, &pl->cl_round};
+  for (DBuf* b : bufs) release(c, *b);
+  delete pl;
+}
+
+// ---------------------------------------------------------------------------
+// SpMM (reference sparselin.py:142-173): Y = A X mod p, one warp per row.
+// ---------------------------------------------------------------------------
+__global__ void k_spmm(Fp fp, const u32* __restrict__ rp, const u32* __restrict__ col, const u32* __restrict__ val,
+                       long long r, const u32* __restrict__ X, int b, u32* __restrict__ Y) {
+  long long row = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x & 31;
+  if (row >= r) return;
+  const u32 s = rp[row], e = rp[row + 1];
+  for (int j = 0; j < b; ++j) {
+    unsigned long long acc = 0;  // sum of < 32 reduced products per lane fits 64 bits
+    for (u32 k = s + lane; k < e; k += 32) {
+      acc += fp.mul(__ldg(val + k), __ldg(X + (size_t)col[k] * b + j));
+      if (acc >= (1ull << 62)) acc %= fp.p;
+    }
+    acc %= fp.p;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      unsigned long long y = __shfl_xor_sync(0xffffffffu, acc, o);
+      acc = (acc + y) % fp.p;
+    }
+    if (lane == 0) Y[(size_t)row * b + j] = (u32)acc;
+  }
+}
+
+void spmm(Ctx* c, long long r, long long N, const int64_t* rp, const int64_t* col, const uint64_t* val,
+          const uint64_t* X, long long b, uint64_t* Y) {
+  const long long M = rp[r];
+  std::vector<u32> hrp(r + 1), hcol(std::max<long long>(M, 1)), hval(std::max<long long>(M, 1));
+  std::vector<u32> hx(std::max<long long>(N * b, 1)), hy(std::max<long long>(r * b, 1));
+  for (long long i = 0; i <= r; ++i) hrp[i] = (u32)rp[i];
+  for (long long k = 0; k < M; ++k) {
+    hcol[k] = (u32)col[k];
+    hval[k] = (u32)(val[k] % c->p);
+  }
+  for (long long k = 0; k < N * b; ++k) hx[k] = (u32)(X[k] % c->p);
+  DBuf drp, dcol, dval, dx, dy;
+  ensure(c, drp, hrp.size() * 4);
+  ensure(c, dcol, hcol.size() * 4);
+  ensure(c, dval, hval.size() * 4);
+  ensure(c, dx, hx.size() * 4);
+  ensure(c, dy, hy.size() * 4);
+  check_cuda(cudaMemcpyAsync(drp.p, hrp.data(), hrp.size() * 4, cudaMemcpyHostToDevice, c->stream), "h2d");
+  check_cuda(cudaMemcpyAsync(dcol.p, hcol.data(), hcol.size() * 4, cudaMemcpyHostToDevice, c->stream), "h2d");
+  check_cuda(cudaMemcpyAsync(dval.p, hval.data(), hval.size() * 4, cudaMemcpyHostToDevice, c->stream), "h2d");
+  check_cuda(cudaMemcpyAsync(dx.p, hx.data(), hx.size() * 4, cudaMemcpyHostToDevice, c->stream), "h2d");
+  Fp fp{c->p, c->pprime, c->r2};
+  if (r > 0 && b > 0) {
+    unsigned blocks = (unsigned)std::max<long long>(1, (r * 32 + 255) / 256);
+    k_spmm<<<blocks, 256, 0, c->stream>>>(fp, drp.as<u32>(), dcol.as<u32>(), dval.as<u32>(), r, dx.as<u32>(), (int)b,
+                                          dy.as<u32>());
+    check_cuda(cudaGetLastError(), "k_spmm");
+  }
+  check_cuda(cudaMemcpyAsync(hy.data(), dy.p, hy.size() * 4, cudaMemcpyDeviceToHost, c->stream), "d2h");
+  check_cuda(cudaStreamSynchronize(c->stream), "sync");
+  for (long long k = 0; k < r * b; ++k) Y[k] = hy[k];
+  release(c, drp);
+  release(c, dcol);
+  release(c, dval);
+  release(c, dx);
+  release(c, dy);
+}
+
+}  // namespace f4b
+
+using namespace f4b;
+
+#define API_BEGIN(ctxp) \
+  Ctx* _c = (ctxp);     \
+  try {
+#define API_END                                  \
+  }                                              \
+  catch (const Error& e) {                       \
+    if (_c) _c->last_error = e.msg;              \
+    return e.code;                               \
+  }                                              \
+  catch (const std::bad_alloc&) {                \
+    if (_c) _c->last_error = "host allocation";  \
+    return F4B_ERR_OOM;                          \
+  }                                              \
+  catch (...) {                                  \
+    if (_c) _c->last_error = "unknown failure";  \
+    return F4B_ERR_CUDA;                         \
+  }                                              \
+  return F4B_OK;
+
+extern "C" {
+
+int f4b_abi_version(void) { return 1; }
+
+int f4b_ctx_create(int device, uint32_t p, int n_vars, int order, f4b_alloc_fn alloc, f4b_free_fn dfree, void* user,
+                   f4b_ctx** out) {
+  if (!out) return F4B_ERR_PRECONDITION;
+  *out = nullptr;
+  if (p < 3 || p >= (1u << 31) || (p & 1u) == 0 || n_vars < 1 || n_vars > 32 || order < 0 || order > 2)
+    return F4B_ERR_PRECONDITION;
+  f4b_ctx* h = new (std::nothrow) f4b_ctx();
+  if (!h) return F4B_ERR_OOM;
+  Ctx* c = &h->c;
+  try {
+    check_cuda(cudaSetDevice(device), "cudaSetDevice");
+    c->device = device;
+    c->p = p;
+    c->n_vars = n_vars;
+    c->order = order;
+    c->alloc = alloc;
+    c->dfree = dfree;
+    c->user = user;
+    int sms = 0;
+    check_cuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "sm count");
+    c->num_sms = sms;
+    // Montgomery constants: p * p' = -1 mod 2^32, R^2 mod p
+    uint32_t x = 1;
+    for (int i = 0; i < 6; ++i) x = x * (2u - p * x);
+    c->pprime = (uint32_t)(0u - x);
+    c->r2 = (uint32_t)(((unsigned __int128)1 << 64) % p);
+    check_cuda(cudaMallocHost((void**)&c->h_stat, 64), "pinned");
+    c->basis.h_off.push_back(0);
+  } catch (const Error& e) {
+    delete h;
+    return e.code;
+  }
+  *out = h;
+  return F4B_OK;
+}
+
+int f4b_ctx_destroy(f4b_ctx* h) {
+  if (!h) return F4B_OK;
+  Ctx* c = &h->c;
+  cudaStreamSynchronize(c->stream);
+  DBuf* bufs[] = {&c->basis.exps, &c->basis.coeff, &c->basis.off, &c->basis.len, &c->basis.lmexp, &c->basis.ckey,
+                  &c->basis.maxe, &c->scan_tmp, &c->sort_a, &c->sort_b, &c->sort_hist, &c->flags, &c->errflag,
+                  &c->tmp_u32a, &c->tmp_u32b, &c->tmp_u32c, &c->rows_basis, &c->rows_delta, &c->rows_len,
+                  &c->rows_start, &c->keys_all, &c->vals_all, &c->dict_a, &c->dict_b, &c->front, &c->front_new,
+                  &c->uniq, &c->red, &c->lmpref, &c->cand_idx, &c->shift_in, &c->cl_basis, &c->cl_shift,
+                  &c->cl_round};
+  for (DBuf* b : bufs) release(c, *b);
+  if (c->h_stat) cudaFreeHost(c->h_stat);
+  delete h;
+  return F4B_OK;
+}
+
+int f4b_ctx_set_stream(f4b_ctx* h, void* stream) {
+  if (!h) return F4B_ERR_PRECONDITION;
+  h->c.stream = (cudaStream_t)stream;
+  return F4B_OK;
+}
+
+const char* f4b_ctx_last_error(const f4b_ctx* h) { return h ? h->c.last_error.c_str() : "null context"; }
+
+int f4b_basis_clear(f4b_ctx* h) {
+  if (!h) return F4B_ERR_PRECONDITION;
+  Basis& B = h->c.basis;
+  B.n_polys = 0;
+  B.n_terms = 0;
+  B.h_len.clear();
+  B.h_off.assign(1, 0);
+  B.h_lm.clear();
+  B.h_maxe.clear();
+  B.ckey_terms = 0;
+  B.ckey_lane_bits = -1;
+  return F4B_OK;
+}
+
+int f4b_basis_append(f4b_ctx* h, int64_t n_polys, const int64_t* lengths, const uint16_t* exps, const uint32_t* coeffs) {
+  if (!h) return F4B_ERR_PRECONDITION;
+  API_BEGIN(&h->c)
+  Ctx* c = _c;
+  Basis& B = c->basis;
+  const int n = c->n_vars;
+  if (n_polys < 0) fail(F4B_ERR_PRECONDITION, "negative polynomial count");
+  long long T = 0;
+  for (long long i = 0; i < n_polys; ++i) {
+    if (lengths[i] < 0) fail(F4B_ERR_PRECONDITION, "negative polynomial length");
+    T += lengths[i];
+  }
+  for (long long t = 0; t < T; ++t)
+    if (coeffs[t] == 0 || coeffs[t] >= c->p) fail(F4B_ERR_PROPERTY, "basis coefficient outside [1, p)");
+  const long long T0 = B.n_terms, P0 = B.n_polys, T1 = T0 + T, P1 = P0 + n_polys;
+  if (T1 >= (1ll << 31)) fail(F4B_ERR_SIZE_CAP, "basis has more than 2^31 terms");
+  // host mirrors
+  long long at = 0;
+  for (long long i = 0; i < n_polys; ++i) {
+    const long long L = lengths[i];
+    B.h_len.push_back(L);
+    B.h_off.push_back(B.h_off.back() + L);
+    for (int v = 0; v < n; ++v) {
+      uint16_t lm = L ? exps[(at)*n + v] : 0, mx = 0;
+      for (long long j = 0; j < L; ++j) mx = std::max<uint16_t>(mx, exps[(at + j) * n + v]);
+      B.h_lm.push_back(lm);
+      B.h_maxe.push_back(mx);
+    }
+    at += L;
+  }
+  // device streams (grow, preserving the existing basis)
+  ensure_keep(c, B.exps, (size_t)(T1 + 1) * n * sizeof(u16));
+  ensure_keep(c, B.coeff, (size_t)(T1 + 1) * sizeof(u32));
+  ensure_keep(c, B.off, (size_t)(P1 + 1) * sizeof(u32));
+  ensure_keep(c, B.len, (size_t)(P1 + 1) * sizeof(u32));
+  ensure_keep(c, B.lmexp, (size_t)(P1 + 1) * n * sizeof(u16));
+  ensure_keep(c, B.maxe, (size_t)(P1 + 1) * n * sizeof(u16));
+  std::vector<u32> hoff(n_polys + 1), hlen(std::max<long long>(n_polys, 1));
+  for (long long i = 0; i <= n_polys; ++i) hoff[i] = (u32)B.h_off[P0 + i];
+  for (long long i = 0; i < n_polys; ++i) hlen[i] = (u32)lengths[i];
+  if (T) {
+    check_cuda(cudaMemcpyAsync(B.exps.as<u16>() + T0 * n, exps, T * n * sizeof(u16), cudaMemcpyHostToDevice, c->stream),
+               "h2d exps");
+    check_cuda(cudaMemcpyAsync(B.coeff.as<u32>() + T0, coeffs, T * sizeof(u32), cudaMemcpyHostToDevice, c->stream),
+               "h2d coeff");
+  }
+  check_cuda(cudaMemcpyAsync(B.off.as<u32>() + P0, hoff.data(), (n_polys + 1) * sizeof(u32), cudaMemcpyHostToDevice,
+                             c->stream), "h2d off");
+  if (n_polys) {
+    check_cuda(cudaMemcpyAsync(B.len.as<u32>() + P0, hlen.data(), n_polys * sizeof(u32), cudaMemcpyHostToDevice, c->stream),
+               "h2d len");
+    check_cuda(cudaMemcpyAsync(B.lmexp.as<u16>() + P0 * n, B.h_lm.data() + P0 * n, n_polys * n * sizeof(u16),
+                               cudaMemcpyHostToDevice, c->stream), "h2d lm");
+    check_cuda(cudaMemcpyAsync(B.maxe.as<u16>() + P0 * n, B.h_maxe.data() + P0 * n, n_polys * n * sizeof(u16),
+                               cudaMemcpyHostToDevice, c->stream), "h2d maxe");
+  }
+  // the staging vectors die here: make the copies complete first
+  check_cuda(cudaStreamSynchronize(c->stream), "sync");
+  B.n_terms = T1;
+  B.n_polys = (int)P1;
+  API_END
+}
+
+int f4b_basis_size(const f4b_ctx* h, int64_t* n_polys, int64_t* n_terms) {
+  if (!h) return F4B_ERR_PRECONDITION;
+  if (n_polys) *n_polys = h->c.basis.n_polys;
+  if (n_terms) *n_terms = h->c.basis.n_terms;
+  return F4B_OK;
+}
+
+int f4b_compile_batch(f4b_ctx* h, int64_t n_rows, const int32_t* row_basis, const uint16_t* row_shift, int closure,
+                      const int32_t* candidates, int64_t n_candidates, int64_t dict_cap, f4b_plan** out) {
+  if (!h || !out) return F4B_ERR_PRECONDITION;
+  *out = nullptr;
+  f4b_plan* pl = new (std::nothrow) f4b_plan();
+  if (!pl) return F4B_ERR_OOM;
+  pl->ctx = &h->c;
+  API_BEGIN(&h->c)
+  try {
+    compile_batch(_c, n_rows, row_basis, row_shift, closure, candidates, n_candidates, dict_cap, pl);
+  } catch (...) {
+    plan_release(pl);
+    throw;
+  }
+  *out = pl;
+  API_END
+}
+
+int f4b_plan_get_info(const f4b_plan* pl, f4b_plan_info* info) {
+  if (!pl || !info) return F4B_ERR_PRECONDITION;
+  info->r = pl->r;
+  info->N = pl->N;
+  info->M = pl->M;
+  info->closure_rounds = pl->closure_rounds;
+  info->n_closure_rows = pl->r - pl->r0;
+  info->key_words = pl->KW;
+  info->lane_bits = pl->lane_bits;
+  info->dict_build_ns = pl->dict_ns;
+  info->row_assemble_ns = pl->asm_ns;
+  info->sort_passes = pl->sort_passes;
+  info->kernel_launches = pl->launches;
+  return F4B_OK;
+}
+
+int f4b_plan_download(const f4b_plan* pl, int64_t* row_ptr, int64_t* col_ind, uint64_t* val, uint16_t* dict_exps,
+                      int32_t* closure_basis, uint16_t* closure_shift, int32_t* closure_round) {
+  if (!pl) return F4B_ERR_PRECONDITION;
+  API_BEGIN(pl->ctx)
+  Ctx* c = _c;
+  const int n = c->n_vars;
+  const long long r = pl->r, M = pl->M, N = pl->N, ncl = pl->r - pl->r0;
+  std::vector<u32> tmp;
+  if (row_ptr) {
+    tmp.resize(r + 1);
+    check_cuda(cudaMemcpyAsync(tmp.data(), pl->row_ptr.p, (r + 1) * 4, cudaMemcpyDeviceToHost, c->stream), "d2h");
+    check_cuda(cudaStreamSynchronize(c->stream), "sync");
+    for (long long i = 0; i <= r; ++i) row_ptr[i] = tmp[i];
+  }
+  if (col_ind && M) {
+    tmp.resize(M);
+    check_cuda(cudaMemcpyAsync(tmp.data(), pl->col_ind.p, M * 4, cudaMemcpyDeviceToHost, c->stream), "d2h");
+    check_cuda(cudaStreamSynchronize(c->stream), "sync");
+    for (long long i = 0; i < M; ++i) col_ind[i] = tmp[i];
+  }
+  if (val && M) {
+    tmp.resize(M);
+    check_cuda(cudaMemcpyAsync(tmp.data(), pl->val.p, M * 4, cudaMemcpyDeviceToHost, c->stream), "d2h");
+    check_cuda(cudaStreamSynchronize(c->stream), "sync");
+    for (long long i = 0; i < M; ++i) val[i] = tmp[i];
+  }
+  if (dict_exps && N)
+    check_cuda(cudaMemcpyAsync(dict_exps, pl->dict_exps.p, N * n * sizeof(u16), cudaMemcpyDeviceToHost, c->stream), "d2h");
+  if (ncl) {
+    if (closure_basis)
+      check_cuda(cudaMemcpyAsync(closure_basis, pl->cl_basis.p, ncl * 4, cudaMemcpyDeviceToHost, c->stream), "d2h");
+    if (closure_shift)
+      check_cuda(cudaMemcpyAsync(closure_shift, pl->cl_shift.p, ncl * n * 2, cudaMemcpyDeviceToHost, c->stream), "d2h");
+    if (closure_round)
+      check_cuda(cudaMemcpyAsync(closure_round, pl->cl_round.p, ncl * 4, cudaMemcpyDeviceToHost, c->stream), "d2h");
+  }
+  check_cuda(cudaStreamSynchronize(c->stream), "sync");
+  API_END
+}
+
+int f4b_plan_free(f4b_plan* pl) {
+  plan_release(pl);
+  return F4B_OK;
+}
+
+int f4b_psge_plan(f4b_ctx* h, const f4b_plan* pl, int mode, f4b_echelon** out) {
+  if (!h || !pl || !out) return F4B_ERR_PRECONDITION;
+  *out = nullptr;
+  API_BEGIN(&h->c)
+  *out = psge_plan(_c, pl, mode);
+  API_END
+}
+
+int f4b_psge_csr(f4b_ctx* h, int64_t n_rows, int64_t n_cols, const int64_t* row_ptr, const int64_t* col_ind,
+                 const uint64_t* val, int mode, f4b_echelon** out) {
+  if (!h || !out) return F4B_ERR_PRECONDITION;
+  *out = nullptr;
+  API_BEGIN(&h->c)
+  *out = psge_csr(_c, n_rows, n_cols, row_ptr, col_ind, val, mode);
+  API_END
+}
+
+int f4b_echelon_complete(f4b_ctx* h, f4b_echelon* e) {
+  if (!h || !e) return F4B_ERR_PRECONDITION;
+  API_BEGIN(&h->c)
+  echelon_complete(_c, e);
+  API_END
+}
+
+int f4b_echelon_get_info(const f4b_echelon* e, f4b_echelon_info* info) {
+  if (!e || !info) return F4B_ERR_PRECONDITION;
+  echelon_info(e, info);
+  return F4B_OK;
+}
+
+int f4b_echelon_download(const f4b_echelon* e, int which, int64_t* leads, int64_t* row_ptr, int64_t* cols,
+                         uint64_t* vals) {
+  if (!e) return F4B_ERR_PRECONDITION;
+  try {
+    echelon_download(e, which, leads, row_ptr, cols, vals);
+  } catch (const Error& er) {
+    return er.code;
+  }
+  return F4B_OK;
+}
+
+int f4b_echelon_pivot_cols(const f4b_echelon* e, int64_t* cols) {
+  if (!e) return F4B_ERR_PRECONDITION;
+  try {
+    echelon_pivot_cols(e, cols);
+  } catch (const Error& er) {
+    return er.code;
+  }
+  return F4B_OK;
+}
+
+int f4b_echelon_free(f4b_echelon* e) {
+  echelon_release(e);
+  return F4B_OK;
+}
+
+int f4b_spmm(f4b_ctx* h, int64_t n_rows, int64_t n_cols, const int64_t* row_ptr, const int64_t* col_ind,
+             const uint64_t* val, const uint64_t* X, int64_t b, uint64_t* Y) {
+  if (!h) return F4B_ERR_PRECONDITION;
+  API_BEGIN(&h->c)
+  spmm(_c, n_rows, n_cols, row_ptr, col_ind, val, X, b, Y);
+  API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,874 @@
+// F_p elimination to the fully reduced row echelon form on the device.
+//
+// Replaces reference `psge_reduce` (pkg/src/fpgb/sparselin.py:281-369).  The
+// reduced echelon form of a matrix is unique, so any pivot schedule yields
+// the reference's bytes; this one is the Faugère–Lachartre split validated in
+// SURVEY.md §7.3(3):
+//
+//   E1  pivot per distinct leading column: fewest nonzeros, then lowest row
+//       index — the reference rule (sparselin.py:316), via a 64-bit atomicMin
+//       over (len << 32 | row).  A = pivot rows, C = the other nonzero rows.
+//   E2  every C row is swept left to right over the A columns with a dense
+//       F_p accumulator in shared memory (one CTA per row, warp-0 ballot scan
+//       for the next nonzero A column, block-parallel sparse AXPY with the
+//       normalized A row; Montgomery products in registers).  What remains
+//       lives on the non-A columns: the dense block D' (|C| x K).
+//   E3  D' forward elimination in one cooperative kernel (one grid barrier
+//       per column, pivot = lowest row index with a nonzero, pivot rows frozen
+//       once chosen), then a row-parallel back-substitution to RREF(D').
+//       RREF(D') rows are the rows with NEW leading columns — the
+//       `nonpivot_rows` the F4 driver harvests (groebner.py:285-287).
+//   E4  (full RREF only) every A row is swept over the A columns right of its
+//       lead, then reduced in one shot by RREF(D') and made monic — the
+//       reference's back-reduction (sparselin.py:337-349) done row-parallel.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <climits>
+#include <vector>
+
+#include "common.cuh"
+#include "engine.h"
+
+namespace cg = cooperative_groups;
+
+struct f4b_echelon {
+  f4b::Ctx* ctx = nullptr;
+  long long M = 0;
+  long long n_rows = 0, n_cols = 0, nA = 0, nC = 0, K = 0, rankD = 0, zero_rows = 0;
+  bool full = false;
+  int64_t numeric_ns = 0, backsub_ns = 0;
+  // input CSR (owned if uploaded from host)
+  f4b::DBuf own_rp, own_col, own_val;
+  const uint32_t *rp = nullptr, *col = nullptr, *val = nullptr;
+  // structure
+  f4b::DBuf prow;      // u32 [N] pivot row of each column or NONE
+  f4b::DBuf invl;      // u32 [N] inverse of the pivot row's lead coefficient
+  f4b::DBuf abits;     // u32 [(N+31)/32] A-column bitmap
+  f4b::DBuf acols;     // u32 [nA] A columns ascending
+  f4b::DBuf nonA;      // u32 [K] non-A columns ascending
+  f4b::DBuf Rd;        // u32 [rankD * K] RREF(D') rows (dense, non-A coordinates)
+  f4b::DBuf dpiv;      // u32 [rankD] D' pivot positions (non-A coordinates)
+  // outputs: pool + per-row slots
+  f4b::DBuf pool_col, pool_val;  // u32
+  f4b::DBuf a_off, a_len;        // u32 [nA] (pivot rows, ascending lead)
+  f4b::DBuf d_off, d_len;        // u32 [rankD] (nonpivot rows, ascending lead)
+  f4b::DBuf cursor;              // u64
+  size_t pool_cap = 0;
+  long long pivot_nnz = 0, nonpivot_nnz = 0;
+};
+
+namespace f4b {
+
+static constexpr u32 NONE = 0xFFFFFFFFu;
+static constexpr int SW_THREADS = 256;
+
+static inline unsigned nb(long long n, int t) { return (unsigned)std::max<long long>(1, (n + t - 1) / t); }
+
+// ---------------------------------------------------------------------------
+// E1: pivot selection and structure
+// ---------------------------------------------------------------------------
+__global__ void k_pivot_select(const u32* __restrict__ rp, const u32* __restrict__ col, long long r,
+                               unsigned long long* __restrict__ pk) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= r) return;
+  u32 s = rp[i], e = rp[i + 1];
+  if (e == s) return;
+  atomicMin(pk + col[s], ((unsigned long long)(e - s) << 32) | (unsigned long long)i);
+}
+
+__global__ void k_col_structure(Fp fp, const unsigned long long* __restrict__ pk, long long N, const u32* __restrict__ rp,
+                                const u32* __restrict__ val, u32* __restrict__ prow, u32* __restrict__ invl,
+                                uint8_t* __restrict__ isA, uint8_t* __restrict__ notA) {
+  long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= N) return;
+  unsigned long long k = pk[c];
+  bool a = k != ~0ull;
+  u32 row = a ? (u32)(k & 0xFFFFFFFFull) : NONE;
+  prow[c] = row;
+  invl[c] = a ? fp.inv(val[rp[row]]) : 0u;
+  isA[c] = a ? 1 : 0;
+  notA[c] = a ? 0 : 1;
+}
+
+__global__ void k_bits(const uint8_t* __restrict__ isA, long long N, u32* __restrict__ bits) {
+  long long w = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (w * 32 >= N) return;
+  u32 b = 0;
+  for (int j = 0; j < 32; ++j) {
+    long long c = w * 32 + j;
+    if (c < N && isA[c]) b |= 1u << j;
+  }
+  bits[w] = b;
+}
+
+__global__ void k_c_flags(const u32* __restrict__ rp, const u32* __restrict__ col, const u32* __restrict__ prow,
+                          long long r, uint8_t* __restrict__ flags) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= r) return;
+  u32 s = rp[i], e = rp[i + 1];
+  flags[i] = (e > s && prow[col[s]] != (u32)i) ? 1 : 0;
+}
+
+__global__ void k_compact_idx(const uint8_t* __restrict__ flags, const u32* __restrict__ pos, long long n,
+                              u32* __restrict__ out) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && flags[i]) out[pos[i]] = (u32)i;
+}
+
+// ---------------------------------------------------------------------------
+// Block helpers
+// ---------------------------------------------------------------------------
+F4B_DEV u32 block_sum(u32 v, u32* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  u32 t = 0;
+  if (threadIdx.x < 32) {
+    t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (threadIdx.x == 0) red[32] = t;
+  }
+  __syncthreads();
+  t = red[32];
+  __syncthreads();
+  return t;
+}
+
+// exclusive block scan of a 0/1 flag; returns prefix, total in *tot
+F4B_DEV u32 block_scan_flag(u32 f, u32* red, u32* tot) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned b = __ballot_sync(0xffffffffu, f);
+  u32 pre = __popc(b & lanemask_lt());
+  if (lane == 0) red[warp] = __popc(b);
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    u32 x = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0;
+    u32 y = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      u32 z = __shfl_up_sync(0xffffffffu, y, o);
+      if (threadIdx.x >= o) y += z;
+    }
+    red[threadIdx.x] = y - x;
+    if (threadIdx.x == 31) red[32] = y;
+  }
+  __syncthreads();
+  u32 res = red[warp] + pre;
+  *tot = red[32];
+  __syncthreads();
+  return res;
+}
+
+// Write the nonzeros of acc[lo, hi) (ascending) to the output pool.
+F4B_DEV void emit_row(const u32* acc, u32 lo, u32 hi, const u32* __restrict__ colmap, u32* __restrict__ pcol,
+                      u32* __restrict__ pval, size_t cap, unsigned long long* cursor, u32* slot_off, u32* slot_len,
+                      u32* err, u32* red, u32* sh) {
+  u32 cnt = 0;
+  for (u32 c = lo + threadIdx.x; c < hi; c += blockDim.x) cnt += acc[c] != 0;
+  cnt = block_sum(cnt, red);
+  if (threadIdx.x == 0) {
+    unsigned long long base = atomicAdd(cursor, (unsigned long long)cnt);
+    if (base + cnt > cap) {
+      atomicOr(err, (u32)DEVERR_CAPACITY);
+      sh[0] = NONE;
+    } else {
+      sh[0] = (u32)base;
+    }
+    *slot_off = (u32)base;
+    *slot_len = cnt;
+  }
+  __syncthreads();
+  u32 base = sh[0];
+  __syncthreads();
+  if (base == NONE) return;
+  for (u32 c0 = lo; c0 < hi; c0 += blockDim.x) {
+    u32 c = c0 + threadIdx.x;
+    u32 v = c < hi ? acc[c] : 0u;
+    u32 tot;
+    u32 p = block_scan_flag(v != 0, red, &tot);
+    if (v) {
+      pcol[base + p] = colmap ? colmap[c] : c;
+      pval[base + p] = v;
+    }
+    base += tot;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// E2 / E4: sparse sweep of a row over the A columns with a dense accumulator
+// ---------------------------------------------------------------------------
+// MODE 0: C rows  -> write the non-A part densely into Dp[slot][K]
+// MODE 1: A rows  -> sweep right of the lead, reduce by RREF(D'), make monic, emit
+template <int MODE>
+__global__ void __launch_bounds__(SW_THREADS) k_sweep(
+    Fp fp, const u32* __restrict__ rp, const u32* __restrict__ col, const u32* __restrict__ val, u32 N,
+    const u32* __restrict__ rows, u32 nrows, const u32* __restrict__ prow, const u32* __restrict__ invl,
+    const u32* __restrict__ abits_g, u32* __restrict__ gacc, u32* __restrict__ Dp, u32 K,
+    const u32* __restrict__ nonA, const u32* __restrict__ Rd, u32 rankD, const u32* __restrict__ dpiv,
+    u32* __restrict__ pcol, u32* __restrict__ pval, size_t cap, unsigned long long* cursor,
+    u32* __restrict__ s_off, u32* __restrict__ s_len, u32* __restrict__ err) {
+  extern __shared__ u32 smem[];
+  const u32 nwords = (N + 31) / 32;
+  u32* abits = smem;
+  u32* acc = gacc ? gacc + (size_t)blockIdx.x * N : smem + nwords;
+  __shared__ u32 red[33];
+  __shared__ u32 sh[4];
+  __shared__ u32 coef_n;
+  __shared__ u32 coef_k[256];
+  __shared__ u32 coef_v[256];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (u32 w = tid; w < nwords; w += blockDim.x) abits[w] = abits_g[w];
+  __syncthreads();
+  for (u32 rr = blockIdx.x; rr < nrows; rr += gridDim.x) {
+    const u32 i = rows[rr];
+    const u32 s = rp[i], e = rp[i + 1];
+    const u32 lead = col[s];
+    for (u32 c = lead + tid; c < N; c += blockDim.x) acc[c] = 0;
+    __syncthreads();
+    for (u32 k = s + tid; k < e; k += blockDim.x) acc[col[k]] = val[k];
+    __syncthreads();
+    u32 cur = MODE == 1 ? lead + 1 : lead;
+    while (true) {
+      if (warp == 0) {
+        u32 found = N;
+        for (u32 c0 = cur & ~31u; c0 < N; c0 += 32) {
+          u32 c = c0 + lane;
+          bool hit = c >= cur && c < N && acc[c] != 0 && ((abits[c >> 5] >> (c & 31)) & 1u);
+          unsigned b = __ballot_sync(0xffffffffu, hit);
+          if (b) {
+            found = c0 + __ffs(b) - 1;
+            break;
+          }
+        }
+        if (lane == 0) sh[0] = found;
+      }
+      __syncthreads();
+      const u32 c = sh[0];
+      if (c >= N) break;
+      const u32 j = prow[c];
+      const u32 f = fp.mul(acc[c], invl[c]);
+      const u32 fm = fp.to_mont(fp.neg(f));
+      const u32 js = rp[j] + 1, je = rp[j + 1];
+      for (u32 k = js + tid; k < je; k += blockDim.x) {
+        const u32 cc = col[k];
+        acc[cc] = fp.add(acc[cc], fp.mont_mul(fm, __ldg(val + k)));
+      }
+      if (tid == 0) acc[c] = 0;
+      __syncthreads();
+      cur = c + 1;
+    }
+    if (MODE == 0) {
+      u32* out = Dp + (size_t)rr * K;
+      for (u32 q = tid; q < K; q += blockDim.x) {
+        const u32 cc = nonA[q];
+        out[q] = cc >= lead ? acc[cc] : 0u;
+      }
+      __syncthreads();
+    } else {
+      // one-shot reduction by RREF(D'): coefficients at D' pivot columns
+      for (u32 k0 = 0; k0 < rankD; k0 += 256) {
+        if (tid == 0) coef_n = 0;
+        __syncthreads();
+        for (u32 k = k0 + tid; k < min(rankD, k0 + 256); k += blockDim.x) {
+          const u32 cc = nonA[dpiv[k]];
+          const u32 v = cc > lead ? acc[cc] : 0u;
+          if (v) {
+            u32 slot = atomicAdd(&coef_n, 1u);
+            coef_k[slot] = k;
+            coef_v[slot] = fp.to_mont(fp.neg(v));
+          }
+        }
+        __syncthreads();
+        const u32 nco = coef_n;
+        if (nco) {
+          for (u32 q = tid; q < K; q += blockDim.x) {
+            const u32 cc = nonA[q];
+            if (cc <= lead) continue;
+            u32 a = acc[cc];
+            for (u32 t = 0; t < nco; ++t) a = fp.add(a, fp.mont_mul(coef_v[t], __ldg(Rd + (size_t)coef_k[t] * K + q)));
+            acc[cc] = a;
+          }
+        }
+        __syncthreads();
+      }
+      // monic: the lead coefficient is untouched by the sweep
+      const u32 inv = invl[lead];
+      for (u32 c = lead + tid; c < N; c += blockDim.x) {
+        u32 v = acc[c];
+        if (v) acc[c] = fp.mul(v, inv);
+      }
+      __syncthreads();
+      emit_row(acc, lead, N, nullptr, pcol, pval, cap, cursor, s_off + rr, s_len + rr, err, red, sh + 1);
+      __syncthreads();
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// E3a: cooperative forward elimination of the dense block D' (R x K)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_dense_forward(Fp fp, u32* Dp, u32 R, u32 K, int* cand, uint8_t* used,
+                                                       u32* piv_of_col) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ int bmin[8];
+  __shared__ u32 s_inv;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const u32 G = gridDim.x;
+  const u32 lo = (u32)(((unsigned long long)R * blockIdx.x) / G);
+  const u32 hi = (u32)(((unsigned long long)R * (blockIdx.x + 1)) / G);
+  for (u32 c = 0; c < K; ++c) {
+    int m = INT_MAX;
+    for (u32 i = lo + tid; i < hi; i += blockDim.x)
+      if (!used[i] && Dp[(size_t)i * K + c] != 0) m = min(m, (int)i);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) bmin[warp] = m;
+    __syncthreads();
+    if (tid == 0) {
+      int mm = INT_MAX;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) mm = min(mm, bmin[w]);
+      if (mm != INT_MAX) atomicMin(cand + c, mm);
+    }
+    grid.sync();
+    const int pr = __ldcg(cand + c);
+    if (pr == INT_MAX) continue;
+    const u32* prow_p = Dp + (size_t)pr * K;
+    if (tid == 0) {
+      s_inv = fp.inv(__ldcg(prow_p + c));
+      if ((u32)pr >= lo && (u32)pr < hi) {
+        used[pr] = 1;
+        piv_of_col[c] = (u32)pr;
+      }
+    }
+    __syncthreads();
+    const u32 inv = s_inv;
+    // warp per own row, lanes over columns c..K-1
+    for (u32 i = lo + warp; i < hi; i += (blockDim.x >> 5)) {
+      if (used[i]) continue;
+      u32* row = Dp + (size_t)i * K;
+      const u32 f = row[c];
+      if (!f) continue;
+      const u32 fm = fp.to_mont(fp.neg(fp.mul(f, inv)));
+      for (u32 q = c + lane; q < K; q += 32) row[q] = fp.add(row[q], fp.mont_mul(fm, __ldcg(prow_p + q)));
+    }
+    __syncthreads();
+  }
+}
+
+// E3b: back-substitution -> RREF(D') rows (dense), one CTA per pivot.
+__global__ void __launch_bounds__(SW_THREADS) k_dense_back(Fp fp, const u32* __restrict__ Dp, u32 K,
+                                                            const u32* __restrict__ dpiv, const u32* __restrict__ dprow,
+                                                            u32 rankD, const u32* __restrict__ pbits_g,
+                                                            const u32* __restrict__ pinv, const u32* __restrict__ prow_of,
+                                                            u32* __restrict__ Rd) {
+  extern __shared__ u32 smem[];
+  const u32 nwords = (K + 31) / 32;
+  u32* pbits = smem;
+  u32* acc = smem + nwords;
+  __shared__ u32 sh[2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (u32 w = tid; w < nwords; w += blockDim.x) pbits[w] = pbits_g[w];
+  for (u32 k = blockIdx.x; k < rankD; k += gridDim.x) {
+    const u32 c0p = dpiv[k];
+    const u32* src = Dp + (size_t)dprow[k] * K;
+    for (u32 q = tid; q < K; q += blockDim.x) acc[q] = q >= c0p ? src[q] : 0u;
+    __syncthreads();
+    u32 cur = c0p + 1;
+    while (true) {
+      if (warp == 0) {
+        u32 found = K;
+        for (u32 b0 = cur & ~31u; b0 < K; b0 += 32) {
+          u32 q = b0 + lane;
+          bool hit = q >= cur && q < K && acc[q] != 0 && ((pbits[q >> 5] >> (q & 31)) & 1u);
+          unsigned b = __ballot_sync(0xffffffffu, hit);
+          if (b) {
+            found = b0 + __ffs(b) - 1;
+            break;
+          }
+        }
+        if (lane == 0) sh[0] = found;
+      }
+      __syncthreads();
+      const u32 q0 = sh[0];
+      if (q0 >= K) break;
+      const u32* prow_p = Dp + (size_t)prow_of[q0] * K;
+      const u32 fm = fp.to_mont(fp.neg(fp.mul(acc[q0], pinv[q0])));
+      for (u32 q = q0 + 1 + tid; q < K; q += blockDim.x) acc[q] = fp.add(acc[q], fp.mont_mul(fm, __ldg(prow_p + q)));
+      if (tid == 0) acc[q0] = 0;
+      __syncthreads();
+      cur = q0 + 1;
+    }
+    const u32 inv = fp.inv(acc[c0p]);
+    u32* out = Rd + (size_t)k * K;
+    for (u32 q = tid; q < K; q += blockDim.x) out[q] = acc[q] ? fp.mul(acc[q], inv) : 0u;
+    __syncthreads();
+  }
+}
+
+__global__ void k_fill_u32(u32* __restrict__ p, long long n, u32 v) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+__global__ void k_dense_pivots(const u32* __restrict__ piv_of_col, u32 K, uint8_t* __restrict__ flags) {
+  long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < K) flags[q] = piv_of_col[q] != NONE;
+}
+
+__global__ void k_dense_piv_info(Fp fp, const u32* __restrict__ Dp, u32 K, const u32* __restrict__ piv_of_col,
+                                 u32* __restrict__ pinv, const uint8_t* __restrict__ flags, const u32* __restrict__ pos,
+                                 u32* __restrict__ dpiv, u32* __restrict__ dprow) {
+  long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= K) return;
+  u32 pr = piv_of_col[q];
+  pinv[q] = pr != NONE ? fp.inv(Dp[(size_t)pr * K + q]) : 0u;
+  if (flags[q]) {
+    dpiv[pos[q]] = (u32)q;
+    dprow[pos[q]] = pr;
+  }
+}
+
+// E3c: emit RREF(D') rows as sparse rows over the global columns
+__global__ void __launch_bounds__(SW_THREADS) k_emit_dense(const u32* __restrict__ Rd, u32 K, u32 rankD,
+                                                            const u32* __restrict__ dpiv, const u32* __restrict__ nonA,
+                                                            u32* __restrict__ pcol, u32* __restrict__ pval, size_t cap,
+                                                            unsigned long long* cursor, u32* s_off, u32* s_len,
+                                                            u32* err) {
+  __shared__ u32 red[33];
+  __shared__ u32 sh[2];
+  for (u32 k = blockIdx.x; k < rankD; k += gridDim.x) {
+    emit_row(Rd + (size_t)k * K, dpiv[k], K, nonA, pcol, pval, cap, cursor, s_off + k, s_len + k, err, red, sh);
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host orchestration
+// ---------------------------------------------------------------------------
+static Fp make_fp(Ctx* c) {
+  Fp fp;
+  fp.p = c->p;
+  fp.pprime = c->pprime;
+  fp.r2 = c->r2;
+  return fp;
+}
+
+static size_t sweep_smem(u32 N, bool& global_acc) {
+  size_t need = (size_t)((N + 31) / 32) * 4 + (size_t)N * 4;
+  global_acc = need > 200 * 1024;
+  return global_acc ? (size_t)((N + 31) / 32) * 4 : need;
+}
+
+static int sweep_grid(Ctx* c, size_t smem, long long rows) {
+  int per_sm = (int)std::max<size_t>(1, std::min<size_t>(8, (220 * 1024) / std::max<size_t>(smem + 3072, 1)));
+  return (int)std::max<long long>(1, std::min<long long>(rows, (long long)c->num_sms * per_sm));
+}
+
+static void run_a_sweep(Ctx* c, f4b_echelon* E);
+
+static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
+  Fp fp = make_fp(c);
+  const long long r = E->n_rows, N = E->n_cols;
+  cudaEvent_t ev0, ev1;
+  check_cuda(cudaEventCreate(&ev0), "event");
+  check_cuda(cudaEventCreate(&ev1), "event");
+  check_cuda(cudaEventRecord(ev0, c->stream), "event");
+  ensure(c, c->errflag, 64);
+  u32* err = c->errflag.as<u32>();
+  check_cuda(cudaMemsetAsync(err, 0, 4, c->stream), "memset");
+  const long long Nn = std::max<long long>(N, 1);
+  // E1
+  DBuf pk;
+  ensure(c, pk, Nn * sizeof(unsigned long long));
+  check_cuda(cudaMemsetAsync(pk.p, 0xFF, Nn * sizeof(unsigned long long), c->stream), "memset pk");
+  if (r) {
+    k_pivot_select<<<nb(r, 256), 256, 0, c->stream>>>(E->rp, E->col, r, pk.as<unsigned long long>());
+    check_cuda(cudaGetLastError(), "k_pivot_select");
+  }
+  ensure(c, E->prow, Nn * sizeof(u32));
+  ensure(c, E->invl, Nn * sizeof(u32));
+  ensure(c, E->abits, (size_t)((Nn + 31) / 32 + 1) * sizeof(u32));
+  ensure(c, c->flags, (size_t)2 * Nn + 32);
+  uint8_t* isA = c->flags.as<uint8_t>();
+  uint8_t* notA = isA + Nn + 16;
+  if (N) {
+    k_col_structure<<<nb(N, 256), 256, 0, c->stream>>>(fp, pk.as<unsigned long long>(), N, E->rp, E->val,
+                                                        E->prow.as<u32>(), E->invl.as<u32>(), isA, notA);
+    check_cuda(cudaGetLastError(), "k_col_structure");
+    k_bits<<<nb((N + 31) / 32, 256), 256, 0, c->stream>>>(isA, N, E->abits.as<u32>());
+    check_cuda(cudaGetLastError(), "k_bits");
+  }
+  release(c, pk);
+  // A columns / non-A columns
+  ensure(c, c->tmp_u32a, (size_t)(Nn + 2) * sizeof(u32));
+  ensure(c, c->tmp_u32b, (size_t)(Nn + 2) * sizeof(u32));
+  exclusive_scan_flags(c, isA, c->tmp_u32a.as<u32>(), N);
+  exclusive_scan_flags(c, notA, c->tmp_u32b.as<u32>(), N);
+  E->nA = N ? read_u32(c, c->tmp_u32a.as<u32>() + N) : 0;
+  E->K = N - E->nA;
+  ensure(c, E->acols, (size_t)std::max<long long>(E->nA, 1) * sizeof(u32));
+  ensure(c, E->nonA, (size_t)std::max<long long>(E->K, 1) * sizeof(u32));
+  if (N) {
+    k_compact_idx<<<nb(N, 256), 256, 0, c->stream>>>(isA, c->tmp_u32a.as<u32>(), N, E->acols.as<u32>());
+    k_compact_idx<<<nb(N, 256), 256, 0, c->stream>>>(notA, c->tmp_u32b.as<u32>(), N, E->nonA.as<u32>());
+    check_cuda(cudaGetLastError(), "k_compact_idx");
+  }
+  // C rows
+  DBuf crows;
+  ensure(c, c->flags, (size_t)std::max<long long>(r, 1) + 32);
+  ensure(c, c->tmp_u32a, (size_t)(r + 2) * sizeof(u32));
+  if (r) {
+    k_c_flags<<<nb(r, 256), 256, 0, c->stream>>>(E->rp, E->col, E->prow.as<u32>(), r, c->flags.as<uint8_t>());
+    check_cuda(cudaGetLastError(), "k_c_flags");
+  }
+  exclusive_scan_flags(c, c->flags.as<uint8_t>(), c->tmp_u32a.as<u32>(), r);
+  E->nC = r ? read_u32(c, c->tmp_u32a.as<u32>() + r) : 0;
+  ensure(c, crows, (size_t)std::max<long long>(E->nC, 1) * sizeof(u32));
+  if (r) {
+    k_compact_idx<<<nb(r, 256), 256, 0, c->stream>>>(c->flags.as<uint8_t>(), c->tmp_u32a.as<u32>(), r, crows.as<u32>());
+    check_cuda(cudaGetLastError(), "k_compact_idx");
+  }
+  // E2: D' = C swept over the A columns
+  const long long R = E->nC, K = E->K;
+  DBuf Dp, gacc, cand, used, pofc;
+  E->rankD = 0;
+  if (R > 0 && K > 0) {
+    ensure(c, Dp, (size_t)R * K * sizeof(u32));
+    bool gl = false;
+    size_t smem = sweep_smem((u32)N, gl);
+    int grid = sweep_grid(c, smem, R);
+    if (gl) ensure(c, gacc, (size_t)grid * N * sizeof(u32));
+    static bool attr0 = false;
+    if (!attr0) {
+      check_cuda(cudaFuncSetAttribute(k_sweep<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 4096), "attr");
+      attr0 = true;
+    }
+    k_sweep<0><<<grid, SW_THREADS, smem, c->stream>>>(
+        fp, E->rp, E->col, E->val, (u32)N, crows.as<u32>(), (u32)R, E->prow.as<u32>(), E->invl.as<u32>(),
+        E->abits.as<u32>(), gl ? gacc.as<u32>() : nullptr, Dp.as<u32>(), (u32)K, E->nonA.as<u32>(), nullptr, 0, nullptr,
+        nullptr, nullptr, 0, nullptr, nullptr, nullptr, err);
+    check_cuda(cudaGetLastError(), "k_sweep<0>");
+    release(c, gacc);
+    // E3a: cooperative forward elimination
+    ensure(c, cand, (size_t)K * sizeof(int));
+    ensure(c, used, (size_t)R + 16);
+    ensure(c, pofc, (size_t)K * sizeof(u32));
+    k_fill_u32<<<nb(K, 256), 256, 0, c->stream>>>(cand.as<u32>(), K, (u32)INT_MAX);
+    check_cuda(cudaMemsetAsync(used.p, 0, R, c->stream), "memset");
+    k_fill_u32<<<nb(K, 256), 256, 0, c->stream>>>(pofc.as<u32>(), K, NONE);
+    check_cuda(cudaGetLastError(), "k_fill_u32");
+    int bps = 0;
+    check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_dense_forward, 256, 0), "occupancy");
+    int G = (int)std::min<long long>((long long)c->num_sms * std::max(1, std::min(bps, 2)), std::max<long long>(R, 1));
+    u32* dpp = Dp.as<u32>();
+    u32 Ru = (u32)R, Ku = (u32)K;
+    int* candp = cand.as<int>();
+    uint8_t* usedp = used.as<uint8_t>();
+    u32* pofcp = pofc.as<u32>();
+    void* args[] = {&fp, &dpp, &Ru, &Ku, &candp, &usedp, &pofcp};
+    check_cuda(cudaLaunchCooperativeKernel((void*)k_dense_forward, G, 256, args, 0, c->stream), "k_dense_forward");
+    // pivots of D'
+    ensure(c, c->flags, (size_t)K + 32);
+    ensure(c, c->tmp_u32a, (size_t)(K + 2) * sizeof(u32));
+    k_dense_pivots<<<nb(K, 256), 256, 0, c->stream>>>(pofc.as<u32>(), (u32)K, c->flags.as<uint8_t>());
+    exclusive_scan_flags(c, c->flags.as<uint8_t>(), c->tmp_u32a.as<u32>(), K);
+    E->rankD = read_u32(c, c->tmp_u32a.as<u32>() + K);
+    DBuf pinv, dprow, pbits;
+    ensure(c, pinv, (size_t)K * sizeof(u32));
+    ensure(c, E->dpiv, (size_t)std::max<long long>(E->rankD, 1) * sizeof(u32));
+    ensure(c, dprow, (size_t)std::max<long long>(E->rankD, 1) * sizeof(u32));
+    ensure(c, pbits, (size_t)((K + 31) / 32 + 1) * sizeof(u32));
+    k_dense_piv_info<<<nb(K, 256), 256, 0, c->stream>>>(fp, Dp.as<u32>(), (u32)K, pofc.as<u32>(), pinv.as<u32>(),
+                                                         c->flags.as<uint8_t>(), c->tmp_u32a.as<u32>(), E->dpiv.as<u32>(),
+                                                         dprow.as<u32>());
+    k_bits<<<nb((K + 31) / 32, 256), 256, 0, c->stream>>>(c->flags.as<uint8_t>(), K, pbits.as<u32>());
+    check_cuda(cudaGetLastError(), "k_dense_piv_info");
+    if (E->rankD) {
+      ensure(c, E->Rd, (size_t)E->rankD * K * sizeof(u32));
+      size_t smem2 = (size_t)((K + 31) / 32) * 4 + (size_t)K * 4;
+      if (smem2 > 200 * 1024) fail(F4B_ERR_SIZE_CAP, "dense block too wide for the device back-substitution");
+      static bool attr1 = false;
+      if (!attr1) {
+        check_cuda(cudaFuncSetAttribute(k_dense_back, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 4096),
+                   "attr");
+        attr1 = true;
+      }
+      int g2 = sweep_grid(c, smem2, E->rankD);
+      k_dense_back<<<g2, SW_THREADS, smem2, c->stream>>>(fp, Dp.as<u32>(), (u32)K, E->dpiv.as<u32>(), dprow.as<u32>(),
+                                                         (u32)E->rankD, pbits.as<u32>(), pinv.as<u32>(), pofc.as<u32>(),
+                                                         E->Rd.as<u32>());
+      check_cuda(cudaGetLastError(), "k_dense_back");
+    }
+    release(c, pinv);
+    release(c, dprow);
+    release(c, pbits);
+  }
+  release(c, Dp);
+  release(c, cand);
+  release(c, used);
+  release(c, pofc);
+  release(c, crows);
+  // E3c: emit the nonpivot rows (RREF(D'))
+  const long long rankD = E->rankD;
+  ensure(c, E->d_off, (size_t)std::max<long long>(rankD, 1) * sizeof(u32));
+  ensure(c, E->d_len, (size_t)std::max<long long>(rankD, 1) * sizeof(u32));
+  ensure(c, E->cursor, 16);
+  if (E->pool_cap == 0) {
+    E->pool_cap = (size_t)std::max<long long>(rankD * K + 2 * (long long)E->nA * 64 + 4096, 1 << 20);
+  }
+  for (int attempt = 0; attempt < 8; ++attempt) {
+    ensure(c, E->pool_col, E->pool_cap * sizeof(u32));
+    ensure(c, E->pool_val, E->pool_cap * sizeof(u32));
+    check_cuda(cudaMemsetAsync(E->cursor.p, 0, 8, c->stream), "memset");
+    check_cuda(cudaMemsetAsync(err, 0, 4, c->stream), "memset");
+    if (rankD) {
+      int g = (int)std::min<long long>(rankD, (long long)c->num_sms * 4);
+      k_emit_dense<<<g, SW_THREADS, 0, c->stream>>>(E->Rd.as<u32>(), (u32)K, (u32)rankD, E->dpiv.as<u32>(),
+                                                     E->nonA.as<u32>(), E->pool_col.as<u32>(), E->pool_val.as<u32>(),
+                                                     E->pool_cap, E->cursor.as<unsigned long long>(), E->d_off.as<u32>(),
+                                                     E->d_len.as<u32>(), err);
+      check_cuda(cudaGetLastError(), "k_emit_dense");
+    }
+    u32 e = read_u32(c, err);
+    if (!(e & DEVERR_CAPACITY)) break;
+    E->pool_cap *= 2;
+  }
+  unsigned long long used_pool = 0;
+  check_cuda(cudaMemcpyAsync(&used_pool, E->cursor.p, 8, cudaMemcpyDeviceToHost, c->stream), "d2h");
+  check_cuda(cudaStreamSynchronize(c->stream), "sync");
+  E->nonpivot_nnz = (long long)used_pool;
+  check_cuda(cudaEventRecord(ev1, c->stream), "event");
+  check_cuda(cudaEventSynchronize(ev1), "event sync");
+  float ms = 0;
+  cudaEventElapsedTime(&ms, ev0, ev1);
+  E->numeric_ns = (int64_t)(ms * 1e6);
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
+  E->zero_rows = r - (E->nA + rankD);
+  if (mode == F4B_FULL_RREF) run_a_sweep(c, E);
+}
+
+static void run_a_sweep(Ctx* c, f4b_echelon* E) {
+  if (E->full) return;
+  Fp fp = make_fp(c);
+  const long long N = E->n_cols, nA = E->nA, K = E->K;
+  cudaEvent_t ev0, ev1;
+  check_cuda(cudaEventCreate(&ev0), "event");
+  check_cuda(cudaEventCreate(&ev1), "event");
+  check_cuda(cudaEventRecord(ev0, c->stream), "event");
+  ensure(c, E->a_off, (size_t)std::max<long long>(nA, 1) * sizeof(u32));
+  ensure(c, E->a_len, (size_t)std::max<long long>(nA, 1) * sizeof(u32));
+  ensure(c, c->errflag, 64);
+  u32* err = c->errflag.as<u32>();
+  if (nA) {
+    DBuf arows, gacc;
+    ensure(c, arows, (size_t)nA * sizeof(u32));
+    // A rows in ascending lead-column order: arows[k] = prow[acols[k]]
+    std::vector<u32> h_acols(nA), h_prow(N);
+    check_cuda(cudaMemcpyAsync(h_acols.data(), E->acols.p, nA * sizeof(u32), cudaMemcpyDeviceToHost, c->stream), "d2h");
+    check_cuda(cudaMemcpyAsync(h_prow.data(), E->prow.p, N * sizeof(u32), cudaMemcpyDeviceToHost, c->stream), "d2h");
+    check_cuda(cudaStreamSynchronize(c->stream), "sync");
+    std::vector<u32> h_arows(nA);
+    for (long long k = 0; k < nA; ++k) h_arows[k] = h_prow[h_acols[k]];
+    check_cuda(cudaMemcpyAsync(arows.p, h_arows.data(), nA * sizeof(u32), cudaMemcpyHostToDevice, c->stream), "h2d");
+    bool gl = false;
+    size_t smem = sweep_smem((u32)N, gl);
+    int grid = sweep_grid(c, smem, nA);
+    if (gl) ensure(c, gacc, (size_t)grid * N * sizeof(u32));
+    static bool attr = false;
+    if (!attr) {
+      check_cuda(cudaFuncSetAttribute(k_sweep<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 4096), "attr");
+      attr = true;
+    }
+    size_t base_used = (size_t)E->nonpivot_nnz;
+    for (int attempt = 0; attempt < 8; ++attempt) {
+      size_t need = base_used + (size_t)std::max<long long>(2 * E->M, 1 << 20);
+      if (E->pool_cap < need) {
+        // grow, preserving the nonpivot rows already in the pool
+        E->pool_cap = std::max(need, 2 * E->pool_cap);
+        ensure_keep(c, E->pool_col, E->pool_cap * sizeof(u32));
+        ensure_keep(c, E->pool_val, E->pool_cap * sizeof(u32));
+      }
+      unsigned long long cur = base_used;
+      check_cuda(cudaMemcpyAsync(E->cursor.p, &cur, 8, cudaMemcpyHostToDevice, c->stream), "h2d");
+      check_cuda(cudaMemsetAsync(err, 0, 4, c->stream), "memset");
+      k_sweep<1><<<grid, SW_THREADS, smem, c->stream>>>(
+          fp, E->rp, E->col, E->val, (u32)N, arows.as<u32>(), (u32)nA, E->prow.as<u32>(), E->invl.as<u32>(),
+          E->abits.as<u32>(), gl ? gacc.as<u32>() : nullptr, nullptr, (u32)K, E->nonA.as<u32>(),
+          E->rankD ? E->Rd.as<u32>() : nullptr, (u32)E->rankD, E->rankD ? E->dpiv.as<u32>() : nullptr,
+          E->pool_col.as<u32>(), E->pool_val.as<u32>(), E->pool_cap, E->cursor.as<unsigned long long>(),
+          E->a_off.as<u32>(), E->a_len.as<u32>(), err);
+      check_cuda(cudaGetLastError(), "k_sweep<1>");
+      u32 e = read_u32(c, err);
+      if (!(e & DEVERR_CAPACITY)) break;
+      unsigned long long tot = 0;
+      check_cuda(cudaMemcpy(&tot, E->cursor.p, 8, cudaMemcpyDeviceToHost), "d2h");
+      E->pool_cap = std::max<size_t>(2 * E->pool_cap, (size_t)tot + 1024);
+      ensure_keep(c, E->pool_col, E->pool_cap * sizeof(u32));
+      ensure_keep(c, E->pool_val, E->pool_cap * sizeof(u32));
+    }
+    unsigned long long tot = 0;
+    check_cuda(cudaMemcpyAsync(&tot, E->cursor.p, 8, cudaMemcpyDeviceToHost, c->stream), "d2h");
+    check_cuda(cudaStreamSynchronize(c->stream), "sync");
+    E->pivot_nnz = (long long)tot - (long long)base_used;
+    release(c, arows);
+    release(c, gacc);
+  }
+  check_cuda(cudaEventRecord(ev1, c->stream), "event");
+  check_cuda(cudaEventSynchronize(ev1), "event sync");
+  float ms = 0;
+  cudaEventElapsedTime(&ms, ev0, ev1);
+  E->backsub_ns = (int64_t)(ms * 1e6);
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
+  E->full = true;
+}
+
+f4b_echelon* psge_plan(Ctx* c, const f4b_plan* pl, int mode) {
+  f4b_echelon* E = new f4b_echelon();
+  E->ctx = c;
+  E->n_rows = pl->r;
+  E->n_cols = pl->N;
+  E->M = pl->M;
+  E->rp = pl->row_ptr.as<u32>();
+  E->col = pl->col_ind.as<u32>();
+  E->val = pl->val.as<u32>();
+  try {
+    psge_run(c, E, mode);
+  } catch (...) {
+    echelon_release(E);
+    throw;
+  }
+  return E;
+}
+
+f4b_echelon* psge_csr(Ctx* c, long long r, long long N, const int64_t* rp, const int64_t* col, const uint64_t* val,
+                      int mode) {
+  f4b_echelon* E = new f4b_echelon();
+  E->ctx = c;
+  E->n_rows = r;
+  E->n_cols = N;
+  try {
+    long long M = rp[r];
+    E->M = M;
+    std::vector<u32> hrp(r + 1), hcol(std::max<long long>(M, 1)), hval(std::max<long long>(M, 1));
+    for (long long i = 0; i <= r; ++i) hrp[i] = (u32)rp[i];
+    for (long long k = 0; k < M; ++k) {
+      if (col[k] < 0 || col[k] >= N) fail(F4B_ERR_PROPERTY, "column out of range");
+      if (val[k] == 0 || val[k] >= c->p) fail(F4B_ERR_PROPERTY, "CSR values outside [1, p)");
+      hcol[k] = (u32)col[k];
+      hval[k] = (u32)val[k];
+    }
+    ensure(c, E->own_rp, (r + 1) * sizeof(u32));
+    ensure(c, E->own_col, hcol.size() * sizeof(u32));
+    ensure(c, E->own_val, hval.size() * sizeof(u32));
+    check_cuda(cudaMemcpyAsync(E->own_rp.p, hrp.data(), (r + 1) * sizeof(u32), cudaMemcpyHostToDevice, c->stream), "h2d");
+    check_cuda(cudaMemcpyAsync(E->own_col.p, hcol.data(), hcol.size() * sizeof(u32), cudaMemcpyHostToDevice, c->stream),
+               "h2d");
+    check_cuda(cudaMemcpyAsync(E->own_val.p, hval.data(), hval.size() * sizeof(u32), cudaMemcpyHostToDevice, c->stream),
+               "h2d");
+    E->rp = E->own_rp.as<u32>();
+    E->col = E->own_col.as<u32>();
+    E->val = E->own_val.as<u32>();
+    psge_run(c, E, mode);
+    check_cuda(cudaStreamSynchronize(c->stream), "sync");
+  } catch (...) {
+    echelon_release(E);
+    throw;
+  }
+  return E;
+}
+
+void echelon_complete(Ctx* c, f4b_echelon* E) { run_a_sweep(c, E); }
+
+void echelon_info(const f4b_echelon* E, f4b_echelon_info* info) {
+  info->n_rows = E->n_rows;
+  info->n_cols = E->n_cols;
+  info->rank = E->nA + E->rankD;
+  info->zero_rows = E->zero_rows;
+  info->n_pivot_rows = E->nA;
+  info->n_nonpivot_rows = E->rankD;
+  info->pivot_nnz = E->pivot_nnz;
+  info->nonpivot_nnz = E->nonpivot_nnz;
+  info->full = E->full ? 1 : 0;
+  info->numeric_ns = E->numeric_ns;
+  info->backsub_ns = E->backsub_ns;
+  info->dense_rows = E->nC;
+  info->dense_cols = E->K;
+}
+
+void echelon_download(const f4b_echelon* E, int which, int64_t* leads, int64_t* row_ptr, int64_t* cols,
+                      uint64_t* vals) {
+  Ctx* c = E->ctx;
+  const long long n = which == 0 ? E->nA : E->rankD;
+  if (which == 0 && !E->full) fail(F4B_ERR_PRECONDITION, "pivot rows not computed (NEW_ONLY echelon)");
+  std::vector<u32> off(n), len(n), lead(n);
+  if (n) {
+    const DBuf& o = which == 0 ? E->a_off : E->d_off;
+    const DBuf& l = which == 0 ? E->a_len : E->d_len;
+    check_cuda(cudaMemcpyAsync(off.data(), o.p, n * sizeof(u32), cudaMemcpyDeviceToHost, c->stream), "d2h");
+    check_cuda(cudaMemcpyAsync(len.data(), l.p, n * sizeof(u32), cudaMemcpyDeviceToHost, c->stream), "d2h");
+    if (which == 0) {
+      check_cuda(cudaMemcpyAsync(lead.data(), E->acols.p, n * sizeof(u32), cudaMemcpyDeviceToHost, c->stream), "d2h");
+    }
+  }
+  const long long used = E->nonpivot_nnz + (E->full ? E->pivot_nnz : 0);
+  std::vector<u32> pc(std::max<long long>(used, 1)), pv(std::max<long long>(used, 1));
+  if (used) {
+    check_cuda(cudaMemcpyAsync(pc.data(), E->pool_col.p, used * sizeof(u32), cudaMemcpyDeviceToHost, c->stream), "d2h");
+    check_cuda(cudaMemcpyAsync(pv.data(), E->pool_val.p, used * sizeof(u32), cudaMemcpyDeviceToHost, c->stream), "d2h");
+  }
+  check_cuda(cudaStreamSynchronize(c->stream), "sync");
+  long long at = 0;
+  if (row_ptr) row_ptr[0] = 0;
+  for (long long k = 0; k < n; ++k) {
+    if (leads) leads[k] = which == 0 ? (int64_t)lead[k] : (int64_t)pc[off[k]];
+    for (u32 t = 0; t < len[k]; ++t) {
+      if (cols) cols[at + t] = pc[off[k] + t];
+      if (vals) vals[at + t] = pv[off[k] + t];
+    }
+    at += len[k];
+    if (row_ptr) row_ptr[k + 1] = at;
+  }
+}
+
+// All pivot columns, ascending: A columns merged with the D' pivots.
+void echelon_pivot_cols(const f4b_echelon* E, int64_t* cols) {
+  Ctx* c = E->ctx;
+  std::vector<u32> a(std::max<long long>(E->nA, 1)), d(std::max<long long>(E->rankD, 1)),
+      nonA(std::max<long long>(E->K, 1));
+  if (E->nA) check_cuda(cudaMemcpyAsync(a.data(), E->acols.p, E->nA * 4, cudaMemcpyDeviceToHost, c->stream), "d2h");
+  if (E->rankD) {
+    check_cuda(cudaMemcpyAsync(d.data(), E->dpiv.p, E->rankD * 4, cudaMemcpyDeviceToHost, c->stream), "d2h");
+    check_cuda(cudaMemcpyAsync(nonA.data(), E->nonA.p, E->K * 4, cudaMemcpyDeviceToHost, c->stream), "d2h");
+  }
+  check_cuda(cudaStreamSynchronize(c->stream), "sync");
+  long long i = 0, j = 0, o = 0;
+  while (i < E->nA || j < E->rankD) {
+    long long x = i < E->nA ? (long long)a[i] : LLONG_MAX;
+    long long y = j < E->rankD ? (long long)nonA[d[j]] : LLONG_MAX;
+    if (x < y) {
+      cols[o++] = x;
+      ++i;
+    } else {
+      cols[o++] = y;
+      ++j;
+    }
+  }
+}
+
+void echelon_release(f4b_echelon* E) {
+  if (!E) return;
+  Ctx* c = E->ctx;
+  DBuf* bufs[] = {&E->own_rp, &E->own_col, &E->own_val, &E->prow,  &E->invl,     &E->abits,    &E->acols,
+                  &E->nonA,   &E->Rd,      &E->dpiv,    &E->pool_col, &E->pool_val, &E->a_off, &E->a_len,
+                  &E->d_off,  &E->d_len,   &E->cursor};
+  for (DBuf* b : bufs) release(c, *b);
+  delete E;
+}
+
+}  // namespace f4b

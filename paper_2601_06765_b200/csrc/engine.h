@@ -1,0 +1,139 @@
+// Internal (C++) interface between the translation units of libf4b200.so.
+// The public C ABI is include/f4b200.h.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+#include <cuda_runtime.h>
+
+#include "../../include/f4b200.h"
+
+namespace f4b {
+
+struct Ctx;
+
+// A device buffer obtained through the context allocator (torch caching
+// allocator when the Python host registers it, cudaMalloc otherwise).
+struct DBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  template <class T> T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+// Per-status error carrying a C-ABI code.
+struct Error {
+  int code;
+  std::string msg;
+};
+
+void ensure(Ctx* c, DBuf& b, size_t bytes);  // grow-only; contents not preserved
+void ensure_keep(Ctx* c, DBuf& b, size_t bytes);  // grow-only; contents preserved
+void release(Ctx* c, DBuf& b);
+void check_cuda(cudaError_t e, const char* what);  // throws Error{F4B_ERR_CUDA}
+[[noreturn]] void fail(int code, const std::string& msg);
+
+// Timing helper: CUDA events recorded on the context stream.
+struct EventPair {
+  cudaEvent_t a = nullptr, b = nullptr;
+};
+
+struct Basis {
+  int n_polys = 0;
+  long long n_terms = 0;
+  // host mirrors (small): lengths, offsets, LM exps, LM degrees, per-poly max exps
+  std::vector<int64_t> h_len, h_off;
+  std::vector<uint16_t> h_lm;    // n_polys * n_vars
+  std::vector<uint16_t> h_maxe;  // n_polys * n_vars
+  // device streams
+  DBuf exps;    // u16 [T * n]
+  DBuf coeff;   // u32 [T]
+  DBuf off;     // u32 [n_polys + 1]
+  DBuf len;     // u32 [n_polys]
+  DBuf lmexp;   // u16 [n_polys * n]
+  // cached device keys for the current key format
+  DBuf ckey;    // u64 [T * KW]
+  DBuf maxe;    // u16 [n_polys * n] per-polynomial max exponent per variable
+  int ckey_lane_bits = -1, ckey_words = 0;
+  long long ckey_terms = 0;  // terms already encoded in this format
+};
+
+struct Ctx {
+  int device = 0;
+  uint32_t p = 0;
+  int n_vars = 0;
+  int order = 0;
+  f4b_alloc_fn alloc = nullptr;
+  f4b_free_fn dfree = nullptr;
+  void* user = nullptr;
+  cudaStream_t stream = 0;
+  int num_sms = 148;
+  std::string last_error;
+  Basis basis;
+  // pinned host scratch for round counters
+  uint32_t* h_stat = nullptr;
+  // reusable device scratch
+  DBuf scan_tmp, sort_a, sort_b, sort_hist, flags, errflag, tmp_u32a, tmp_u32b, tmp_u32c;
+  // FBSP scratch (grow-only, reused across compile_batch calls)
+  DBuf rows_basis, rows_delta, rows_len, rows_start, keys_all, vals_all;
+  DBuf dict_a, dict_b, front, front_new, uniq, red, lmpref, cand_idx, shift_in;
+  DBuf cl_basis, cl_shift, cl_round;
+  uint32_t pprime = 0, r2 = 0;
+  long long launches = 0;  // kernel launches issued (for reporting)
+};
+
+// scan.cu: exclusive scan of n u32 values into out (n+1 entries; out[n] = total).
+void exclusive_scan_u32(Ctx* c, const uint32_t* in, uint32_t* out, long long n);
+// exclusive scan where in[i] = (flags[i] != 0)
+void exclusive_scan_flags(Ctx* c, const uint8_t* flags, uint32_t* out, long long n);
+
+// radix.cu: sort n keys (KW words each) ascending, only the low `bits` bits
+// vary.  Result lands in *result (one of the two ping-pong buffers).
+void radix_sort_keys(Ctx* c, int KW, const uint64_t* in, long long n, int bits, uint64_t** result);
+// unique over a sorted key array -> out (compacted); returns count (host sync).
+long long unique_keys(Ctx* c, int KW, const uint64_t* sorted, long long n, uint64_t* out);
+
+uint32_t read_u32(Ctx* c, const uint32_t* dptr);  // synchronous small D2H
+void memset_async(Ctx* c, void* p, int v, size_t bytes);
+
+}  // namespace f4b
+
+// ---------------------------------------------------------------------------
+// Opaque objects of the C ABI
+// ---------------------------------------------------------------------------
+struct f4b_plan {
+  f4b::Ctx* ctx = nullptr;
+  int KW = 1, lane_bits = 1;
+  long long r = 0, r0 = 0, N = 0, M = 0, closure_rounds = 0;
+  long long sort_passes = 0, launches = 0;
+  int64_t dict_ns = 0, asm_ns = 0;
+  f4b::DBuf row_ptr;    // u32 [r+1]
+  f4b::DBuf col_ind;    // u32 [M]
+  f4b::DBuf val;        // u32 [M]
+  f4b::DBuf dict;       // u64 [N*KW] ascending device keys
+  f4b::DBuf dict_exps;  // u16 [N*n] descending (column order)
+  f4b::DBuf cl_basis;   // i32 [r-r0]
+  f4b::DBuf cl_shift;   // u16 [(r-r0)*n]
+  f4b::DBuf cl_round;   // i32 [r-r0]
+};
+
+struct f4b_echelon;
+
+namespace f4b {
+void plan_release(f4b_plan* pl);
+}
+
+namespace f4b {
+void compile_batch(Ctx* c, long long r0, const int32_t* rb, const uint16_t* shift, int closure, const int32_t* cands,
+                   long long n_cands, long long dict_cap, f4b_plan* pl);
+f4b_echelon* psge_plan(Ctx* c, const f4b_plan* pl, int mode);
+f4b_echelon* psge_csr(Ctx* c, long long r, long long N, const int64_t* rp, const int64_t* col, const uint64_t* val,
+                      int mode);
+void echelon_complete(Ctx* c, f4b_echelon* E);
+void echelon_info(const f4b_echelon* E, f4b_echelon_info* info);
+void echelon_download(const f4b_echelon* E, int which, int64_t* leads, int64_t* row_ptr, int64_t* cols, uint64_t* vals);
+void echelon_release(f4b_echelon* E);
+void echelon_pivot_cols(const f4b_echelon* E, int64_t* cols);
+void spmm(Ctx* c, long long r, long long N, const int64_t* rp, const int64_t* col, const uint64_t* val,
+          const uint64_t* X, long long b, uint64_t* Y);
+}  // namespace f4b

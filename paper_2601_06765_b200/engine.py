@@ -1,0 +1,223 @@
+"""Device engine: one C-ABI context per (device, ring), the device-resident
+basis, and handles for device plans / echelon forms.
+
+The basis lives in HBM across F4 steps (SURVEY.md §1 "Boundaries in the
+build"): ``sync_basis`` appends only the polynomials the device has not seen
+(the F4 driver appends harvested rows directly), replacing the reference's
+full ``soa_pack`` every step (``groebner.py:143-146``).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import itertools
+import weakref
+
+import numpy as np
+
+from . import _capi
+from ._capi import EchelonInfo, PlanInfo, ptr
+from .errors import LaneOverflowError
+from .monomials import ORDER_CODE
+
+_EXP_MAX = 0xFFFF
+_ids = itertools.count(1)
+
+
+class DevicePlan:
+    """Handle of an ``f4b_plan`` (device CSR + dictionary + closure rows)."""
+
+    def __init__(self, engine, handle):
+        self.engine = engine
+        self.h = handle
+        info = PlanInfo()
+        engine.ctx.check(engine.lib.f4b_plan_get_info(handle, C.byref(info)), "plan info")
+        self.info = {k: int(getattr(info, k)) for k, _ in PlanInfo._fields_}
+        self._fin = weakref.finalize(self, engine.lib.f4b_plan_free, handle)
+
+    def download(self, arrays=True, dict_exps=True, closure=True):
+        e, n = self.engine, self.engine.n_vars
+        r, M, N, ncl = (self.info[k] for k in ("r", "M", "N", "n_closure_rows"))
+        out = {}
+        if arrays:
+            out["row_ptr"] = np.empty(r + 1, dtype=np.int64)
+            out["col_ind"] = np.empty(M, dtype=np.int64)
+            out["val"] = np.empty(M, dtype=np.uint64)
+        if dict_exps:
+            out["dict_exps"] = np.empty((N, n), dtype=np.uint16)
+        if closure:
+            out["cl_basis"] = np.empty(ncl, dtype=np.int32)
+            out["cl_shift"] = np.empty((ncl, n), dtype=np.uint16)
+            out["cl_round"] = np.empty(ncl, dtype=np.int32)
+        g = out.get
+        e.ctx.check(e.lib.f4b_plan_download(
+            self.h, ptr(g("row_ptr"), C.c_int64), ptr(g("col_ind"), C.c_int64), ptr(g("val"), C.c_uint64),
+            ptr(g("dict_exps"), C.c_uint16), ptr(g("cl_basis"), C.c_int32), ptr(g("cl_shift"), C.c_uint16),
+            ptr(g("cl_round"), C.c_int32)), "plan download")
+        return out
+
+
+class DeviceEchelon:
+    """Handle of an ``f4b_echelon``; pivot rows are computed on demand."""
+
+    def __init__(self, engine, handle, keepalive=None):
+        self.engine = engine
+        self.h = handle
+        self._keep = keepalive  # the plan whose CSR the echelon reads
+        self._fin = weakref.finalize(self, engine.lib.f4b_echelon_free, handle)
+
+    def info(self):
+        inf = EchelonInfo()
+        self.engine.lib.f4b_echelon_get_info(self.h, C.byref(inf))
+        return {k: int(getattr(inf, k)) for k, _ in EchelonInfo._fields_}
+
+    def complete(self):
+        self.engine.ctx.sync_stream()
+        self.engine.ctx.check(self.engine.lib.f4b_echelon_complete(self.engine.ctx.h, self.h), "echelon complete")
+
+    def pivot_cols(self):
+        inf = self.info()
+        out = np.empty(inf["rank"], dtype=np.int64)
+        self.engine.ctx.check(self.engine.lib.f4b_echelon_pivot_cols(self.h, ptr(out, C.c_int64)), "pivot cols")
+        return out
+
+    def rows(self, which: int):
+        """Return (leads, row_ptr, cols, vals) for pivot (0) or nonpivot (1) rows."""
+        inf = self.info()
+        if which == 0 and not inf["full"]:
+            self.complete()
+            inf = self.info()
+        n = inf["n_pivot_rows"] if which == 0 else inf["n_nonpivot_rows"]
+        nnz = inf["pivot_nnz"] if which == 0 else inf["nonpivot_nnz"]
+        leads = np.empty(n, dtype=np.int64)
+        rp = np.empty(n + 1, dtype=np.int64)
+        cols = np.empty(max(nnz, 1), dtype=np.int64)
+        vals = np.empty(max(nnz, 1), dtype=np.uint64)
+        self.engine.ctx.check(self.engine.lib.f4b_echelon_download(
+            self.h, which, ptr(leads, C.c_int64), ptr(rp, C.c_int64), ptr(cols, C.c_int64),
+            ptr(vals, C.c_uint64)), "echelon download")
+        return leads, rp, cols[:nnz], vals[:nnz]
+
+
+class Engine:
+    """Device engine for one ring on one GPU."""
+
+    _registry: dict = {}
+
+    @classmethod
+    def for_ring(cls, ring, device: int = 0) -> "Engine":
+        key = (device, ring.modulus.p, ring.n_vars, ring.order)
+        eng = cls._registry.get(key)
+        if eng is None:
+            eng = cls(ring.modulus.p, ring.n_vars, ring.order, device)
+            cls._registry[key] = eng
+        return eng
+
+    def __init__(self, p, n_vars, order, device=0):
+        self.ctx = _capi.Context(p, n_vars, ORDER_CODE[order], device)
+        self.lib = self.ctx.lib
+        self.p, self.n_vars, self.order, self.device = p, n_vars, order, device
+        self.uid = next(_ids)
+        self.generation = 0
+        # host mirror of the device basis: lengths + concatenated exps / coeffs
+        self._lens = np.zeros(0, dtype=np.int64)
+        self._exps = np.zeros((0, n_vars), dtype=np.uint16)
+        self._coeff = np.zeros(0, dtype=np.uint32)
+
+    # -- basis -------------------------------------------------------------
+    @property
+    def token(self):
+        return (self.uid, self.generation)
+
+    @property
+    def n_polys(self) -> int:
+        return len(self._lens)
+
+    def clear_basis(self):
+        self.ctx.check(self.lib.f4b_basis_clear(self.ctx.h), "basis clear")
+        self._lens = np.zeros(0, dtype=np.int64)
+        self._exps = np.zeros((0, self.n_vars), dtype=np.uint16)
+        self._coeff = np.zeros(0, dtype=np.uint32)
+        self.generation += 1
+
+    def append_polys(self, lengths, exps, coeffs):
+        lengths = np.ascontiguousarray(lengths, dtype=np.int64)
+        exps = np.asarray(exps)
+        if exps.size and (exps.min() < 0 or exps.max() > _EXP_MAX):
+            raise LaneOverflowError("exponent does not fit a 16-bit lane")
+        exps = np.ascontiguousarray(exps, dtype=np.uint16).reshape(-1, self.n_vars)
+        coeffs = np.ascontiguousarray(coeffs, dtype=np.uint32)
+        self.ctx.sync_stream()
+        self.ctx.check(self.lib.f4b_basis_append(self.ctx.h, len(lengths), ptr(lengths, C.c_int64),
+                                                 ptr(exps, C.c_uint16), ptr(coeffs, C.c_uint32)), "basis append")
+        self._lens = np.concatenate([self._lens, lengths])
+        self._exps = np.concatenate([self._exps, exps])
+        self._coeff = np.concatenate([self._coeff, coeffs])
+        self.generation += 1
+
+    def sync_basis(self, soa):
+        """Make the device basis equal to ``soa`` (a SoaPolySet)."""
+        if getattr(soa, "_f4b_token", None) == self.token:
+            return
+        n_dev = self.n_polys
+        T_dev = len(self._coeff)
+        same_prefix = (
+            len(soa) >= n_dev
+            and soa.total_terms() >= T_dev
+            and np.array_equal(soa.length[:n_dev], self._lens)
+            and np.array_equal(soa.coeff[:T_dev].astype(np.uint32), self._coeff)
+            and np.array_equal(soa.exps[:T_dev], self._exps)
+        )
+        if not same_prefix:
+            self.clear_basis()
+            n_dev, T_dev = 0, 0
+        if len(soa) > n_dev:
+            self.append_polys(soa.length[n_dev:], soa.exps[T_dev:], soa.coeff[T_dev:])
+        soa._f4b_token = self.token
+
+    # -- hot path ----------------------------------------------------------
+    def compile(self, row_basis, row_shift, closure: bool, candidates=None, dict_cap=10**6) -> DevicePlan:
+        rb = np.ascontiguousarray(row_basis, dtype=np.int32)
+        sh = np.asarray(row_shift)
+        if sh.size and (sh.min() < 0 or sh.max() > _EXP_MAX):
+            raise LaneOverflowError("shift exponent does not fit a 16-bit lane")
+        sh = np.ascontiguousarray(sh, dtype=np.uint16).reshape(len(rb), self.n_vars)
+        cand = None if candidates is None else np.ascontiguousarray(candidates, dtype=np.int32)
+        self.ctx.sync_stream()
+        h = C.c_void_p()
+        code = self.lib.f4b_compile_batch(
+            self.ctx.h, len(rb), ptr(rb, C.c_int32), ptr(sh, C.c_uint16), 1 if closure else 0,
+            ptr(cand, C.c_int32) if cand is not None else None, 0 if cand is None else len(cand),
+            int(dict_cap), C.byref(h))
+        self.ctx.check(code, "compile_batch")
+        return DevicePlan(self, h)
+
+    def psge_plan(self, plan: DevicePlan, full: bool) -> DeviceEchelon:
+        self.ctx.sync_stream()
+        h = C.c_void_p()
+        self.ctx.check(self.lib.f4b_psge_plan(self.ctx.h, plan.h, 1 if full else 0, C.byref(h)), "psge")
+        return DeviceEchelon(self, h, keepalive=plan)
+
+    def psge_csr(self, n_rows, n_cols, row_ptr, col_ind, val, full: bool) -> DeviceEchelon:
+        rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+        ci = np.ascontiguousarray(col_ind, dtype=np.int64)
+        va = np.ascontiguousarray(val, dtype=np.uint64)
+        self.ctx.sync_stream()
+        h = C.c_void_p()
+        self.ctx.check(self.lib.f4b_psge_csr(self.ctx.h, int(n_rows), int(n_cols), ptr(rp, C.c_int64),
+                                             ptr(ci, C.c_int64), ptr(va, C.c_uint64), 1 if full else 0,
+                                             C.byref(h)), "psge")
+        return DeviceEchelon(self, h)
+
+    def spmm(self, n_rows, n_cols, row_ptr, col_ind, val, X):
+        X = np.ascontiguousarray(X, dtype=np.uint64)
+        b = X.shape[1]
+        Y = np.zeros((n_rows, b), dtype=np.uint64)
+        rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+        ci = np.ascontiguousarray(col_ind, dtype=np.int64)
+        va = np.ascontiguousarray(val, dtype=np.uint64)
+        self.ctx.sync_stream()
+        self.ctx.check(self.lib.f4b_spmm(self.ctx.h, int(n_rows), int(n_cols), ptr(rp, C.c_int64),
+                                         ptr(ci, C.c_int64), ptr(va, C.c_uint64), ptr(X, C.c_uint64), b,
+                                         ptr(Y, C.c_uint64)), "spmm")
+        return Y

@@ -1,0 +1,435 @@
+"""F4 driver over the GPU hot path — drop-in for ``pkg/src/fpgb/groebner.py``.
+
+The host keeps the reference's pair logic bit for bit (Gebauer–Möller update
+:154-201, normal strategy :204-213, harvest order :285-290), vectorized over
+NumPy arrays of leading exponents; each F4 step calls the device
+``compile_batch`` -> ``psge_reduce`` and appends the harvested rows straight
+to the HBM-resident basis (no whole-basis re-pack per step).
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .bulk import ExecPolicy
+from .errors import NonterminationError, PreconditionError, PropertyViolationError
+from .fp import FieldModulus
+from .monomials import Ring, key_pack_vec, mon_div, mon_divides, mon_lcm
+from .polynomials import Poly, SoaPolySet, poly_add_scaled, poly_monic, poly_mul_mon
+from .sparselin import (EchelonResult, KernelBasis, KernelMode, csr_from_plan, dense_gauss, left_kernel,
+                        psge_reduce)
+from .symbolic import BatchSpec, Closure, LayoutPlan, PairTarget, compile_batch, row_lead_cols, select_rows
+
+MAX_STEPS_DEFAULT = 10_000
+
+
+@dataclass
+class Pair:
+    i: int
+    j: int
+    lcm: tuple
+    degree: int
+    key: tuple
+
+    def sort_tuple(self):
+        return (self.degree, self.key, self.i, self.j)
+
+
+@dataclass
+class BatchStats:
+    degree: int
+    r: int
+    N: int
+    M: int
+    nnz: int
+    rank: int
+    new_polys: int
+    zero_reductions: int
+    closure_rounds: int
+    timings_ns: dict
+
+
+class _HostBasis:
+    """Growable SoA copy of the basis (exps, coeffs, reference keys)."""
+
+    def __init__(self, ring: Ring):
+        self.ring = ring
+        n, W = ring.n_vars, ring.n_key_words
+        self.T = 0
+        self.exps = np.zeros((1024, n), dtype=np.int64)
+        self.coeff = np.zeros(1024, dtype=np.uint64)
+        self.keys = np.zeros((1024, W), dtype=np.uint64)
+        self.lengths: list = []
+        self.lm = np.zeros((64, n), dtype=np.int64)
+
+    def append(self, exps: np.ndarray, coeff: np.ndarray):
+        k = len(exps)
+        need = self.T + k
+        if need > len(self.coeff):
+            cap = max(need, 2 * len(self.coeff))
+            for name in ("exps", "coeff", "keys"):
+                old = getattr(self, name)
+                new = np.zeros((cap,) + old.shape[1:], dtype=old.dtype)
+                new[:self.T] = old[:self.T]
+                setattr(self, name, new)
+        self.exps[self.T:need] = exps
+        self.coeff[self.T:need] = coeff
+        if k:
+            self.keys[self.T:need] = key_pack_vec(exps, self.ring)
+        t = len(self.lengths)
+        if t >= len(self.lm):
+            grown = np.zeros((2 * len(self.lm), self.lm.shape[1]), dtype=np.int64)
+            grown[:t] = self.lm[:t]
+            self.lm = grown
+        self.lm[t] = exps[0] if k else 0
+        self.lengths.append(k)
+        self.T = need
+
+    def soa(self) -> SoaPolySet:
+        lengths = np.asarray(self.lengths, dtype=np.int64)
+        offset = np.zeros(len(lengths) + 1, dtype=np.int64)
+        np.cumsum(lengths, out=offset[1:])
+        return SoaPolySet(self.ring, self.keys[:self.T], self.coeff[:self.T], offset, lengths, self.exps[:self.T])
+
+
+class GroebnerState:
+    """Basis + pair queue.  ``pairs`` is a list of Pair (reference API) backed
+    by NumPy arrays for the vectorized criteria."""
+
+    def __init__(self, ring: Ring, basis=None, pairs=None):
+        self.ring = ring
+        self.basis: list = []
+        self.stats: list = []
+        self.zero_reductions = 0
+        self._hb = _HostBasis(ring)
+        self._soa = None
+        self._dev_token = None  # engine token matching len(basis) polys
+        self._dev_n = -1
+        n, W = ring.n_vars, ring.n_key_words
+        self._pi = np.zeros(0, np.int64)
+        self._pj = np.zeros(0, np.int64)
+        self._plcm = np.zeros((0, n), np.int64)
+        self._pdeg = np.zeros(0, np.int64)
+        self._pkey = np.zeros((0, W), np.uint64)
+        self._pairs_cache = []
+        for f in basis or []:
+            self._push_basis(f)
+        if pairs:
+            self.pairs = pairs
+
+    def _push_basis(self, f: Poly):
+        self.basis.append(f)
+        if f.terms:
+            ex = np.asarray([e for e, _ in f.terms], dtype=np.int64)
+            cf = np.asarray([c for _, c in f.terms], dtype=np.uint64)
+        else:
+            ex = np.zeros((0, self.ring.n_vars), np.int64)
+            cf = np.zeros(0, np.uint64)
+        self._hb.append(ex, cf)
+        self._soa = None
+
+    # -- pair queue as a list of Pair ------------------------------------------
+    @property
+    def pairs(self):
+        if self._pairs_cache is None:
+            self._pairs_cache = [
+                Pair(int(i), int(j), tuple(int(x) for x in l), int(d), tuple(int(w) for w in k))
+                for i, j, l, d, k in zip(self._pi.tolist(), self._pj.tolist(), self._plcm, self._pdeg.tolist(),
+                                         self._pkey)]
+        return self._pairs_cache
+
+    @pairs.setter
+    def pairs(self, plist):
+        plist = list(plist)
+        n, W = self.ring.n_vars, self.ring.n_key_words
+        self._pi = np.asarray([q.i for q in plist], dtype=np.int64)
+        self._pj = np.asarray([q.j for q in plist], dtype=np.int64)
+        self._plcm = np.asarray([q.lcm for q in plist], dtype=np.int64).reshape(len(plist), n)
+        self._pdeg = np.asarray([q.degree for q in plist], dtype=np.int64)
+        self._pkey = np.asarray([q.key for q in plist], dtype=np.uint64).reshape(len(plist), W)
+        self._pairs_cache = plist
+
+    def n_pairs(self) -> int:
+        return len(self._pi)
+
+    def soa(self) -> SoaPolySet:
+        if self._soa is None or len(self._soa) != len(self.basis):
+            self._soa = self._hb.soa()
+            if self._dev_n == len(self.basis) and self._dev_token is not None:
+                self._soa._f4b_token = self._dev_token
+        return self._soa
+
+
+def _make_pair(state: GroebnerState, i: int, j: int) -> Pair:
+    lcm = mon_lcm(state.basis[i].lm(), state.basis[j].lm())
+    return Pair(i, j, lcm, sum(lcm), state.ring.sort_key(lcm))
+
+
+def _minimal_mask(u: np.ndarray) -> np.ndarray:
+    """True for rows of ``u`` (distinct exponent vectors) not divisible by any
+    other row — processed by ascending degree against the minimal set."""
+    deg = u.sum(axis=1)
+    keep = np.zeros(len(u), dtype=bool)
+    mins = np.zeros((0, u.shape[1]), dtype=u.dtype)
+    for d in np.unique(deg):
+        idx = np.flatnonzero(deg == d)
+        blk = u[idx]
+        if len(mins):
+            dom = (blk[:, None, :] >= mins[None, :, :]).all(axis=2).any(axis=1)
+        else:
+            dom = np.zeros(len(idx), dtype=bool)
+        keep[idx[~dom]] = True
+        mins = np.concatenate([mins, blk[~dom]])
+    return keep
+
+
+def update_pairs(state: GroebnerState, new_poly: Poly) -> GroebnerState:
+    """Append a monic polynomial with Gebauer–Möller pruning (reference :154-201)."""
+    if new_poly.is_zero() or new_poly.lc() != 1:
+        raise PreconditionError("basis members must be monic and nonzero")
+    t = len(state.basis)
+    state._push_basis(new_poly)
+    lm_t = np.asarray(new_poly.lm(), dtype=np.int64)
+    L = state._hb.lm[:t]
+    ring = state.ring
+    # new pairs (i, t): chain criterion among themselves
+    lcm = np.maximum(L, lm_t[None, :])
+    if t:
+        uq, inv = np.unique(lcm, axis=0, return_inverse=True)
+        inv = inv.reshape(-1)
+        kept = _minimal_mask(uq)[inv]
+        kept_idx = np.flatnonzero(kept)
+        # one representative per lcm: the lowest partner index
+        _, first = np.unique(inv[kept_idx], return_index=True)
+        reps = np.sort(kept_idx[first])
+        # product criterion on the representative
+        coprime = (np.minimum(L[reps], lm_t[None, :]) == 0).all(axis=1)
+        surv = reps[~coprime]
+    else:
+        surv = np.zeros(0, dtype=np.int64)
+    # chain criterion against queued pairs
+    pl = state._plcm
+    if len(pl):
+        hit = (pl >= lm_t[None, :]).all(axis=1)
+        hit &= (np.maximum(L[state._pi], lm_t) != pl).any(axis=1)
+        hit &= (np.maximum(L[state._pj], lm_t) != pl).any(axis=1)
+        keep_old = ~hit
+    else:
+        keep_old = np.zeros(0, dtype=bool)
+    nl = lcm[surv]
+    pi = np.concatenate([state._pi[keep_old], surv])
+    pj = np.concatenate([state._pj[keep_old], np.full(len(surv), t, dtype=np.int64)])
+    plcm = np.concatenate([pl[keep_old], nl])
+    pdeg = np.concatenate([state._pdeg[keep_old], nl.sum(axis=1)])
+    pkey = np.concatenate([state._pkey[keep_old], key_pack_vec(nl, ring) if len(nl)
+                           else np.zeros((0, ring.n_key_words), np.uint64)])
+    order = np.lexsort((pj, pi) + tuple(pkey[:, w] for w in reversed(range(pkey.shape[1]))) + (pdeg,))
+    state._pi, state._pj, state._plcm = pi[order], pj[order], plcm[order]
+    state._pdeg, state._pkey = pdeg[order], pkey[order]
+    state._pairs_cache = None
+    return state
+
+
+def select_batch(state: GroebnerState):
+    """Normal strategy: all queued pairs of minimal lcm degree (reference :204-213)."""
+    if state.n_pairs() == 0:
+        raise PreconditionError("empty pair queue")
+    d = int(state._pdeg[0])
+    k = int(np.searchsorted(state._pdeg, d, side="right"))
+    targets = [PairTarget(tuple(int(x) for x in state._plcm[q]), q, int(state._pi[q]), int(state._pj[q]))
+               for q in range(k)]
+    for name in ("_pi", "_pj", "_plcm", "_pdeg", "_pkey"):
+        setattr(state, name, getattr(state, name)[k:])
+    state._pairs_cache = None
+    return BatchSpec(targets=targets, candidates=tuple(range(len(state.basis)))), d
+
+
+@dataclass
+class F4Config:
+    numeric: str = "psge"  # psge | dense | wiedemann
+    panel_width: int = 256
+    block_width: int = 4
+    seed: int = 0
+    workers: int = 1
+    max_steps: int = MAX_STEPS_DEFAULT
+    policy: ExecPolicy | None = None
+
+    def exec_policy(self) -> ExecPolicy:
+        return self.policy if self.policy is not None else ExecPolicy(self.workers)
+
+
+def _dense_echelon(plan: LayoutPlan, m: FieldModulus) -> EchelonResult:
+    """Dense-oracle stand-in (reference :238-250), small batches only."""
+    A = csr_from_plan(plan, m)
+    rank, rref, pivots = dense_gauss(A.to_dense(), m)
+    orig = set(row_lead_cols(plan).tolist())
+    piv, nonpiv = [], []
+    for k, col in enumerate(pivots):
+        cols = np.flatnonzero(rref[k]).astype(np.int64)
+        (piv if col in orig else nonpiv).append((col, cols, rref[k][cols]))
+    return EchelonResult(list(pivots), piv, nonpiv, A.n_rows - rank, rank, 0)
+
+
+def f4_step(state: GroebnerState, config: F4Config | None = None):
+    """One batch: select, compile (GPU), eliminate (GPU), harvest.
+
+    Returns (plan, echelon, kernel) like the reference (:253-311)."""
+    from .engine import Engine
+
+    config = config or F4Config()
+    ring = state.ring
+    spec, degree = select_batch(state)
+    basis_snapshot = list(state.basis)
+    soa = state.soa()
+    rows = select_rows(spec, soa)
+    plan = compile_batch(rows, soa, Closure.ONE_STEP_REDUCTION, config.exec_policy())
+    t0 = time.perf_counter_ns()
+    if config.numeric == "dense":
+        ech = _dense_echelon(plan, ring.modulus)
+    else:
+        ech = psge_reduce(csr_from_plan(plan, ring.modulus), config.panel_width)
+    leads, rp, cols, vals = ech.nonpivot_arrays()
+    numeric_ns = time.perf_counter_ns() - t0
+    kernel = None
+    if config.numeric == "wiedemann":
+        A = csr_from_plan(plan, ring.modulus)
+        kernel = left_kernel(A, count=max(1, A.n_rows), seed=config.seed)
+        rep = verify_kernel_syzygy(plan, basis_snapshot, kernel)
+        if not rep.ok:
+            raise PropertyViolationError(f"kernel syzygy violation: {rep.detail}")
+    # harvest: RREF rows are monic with terms descending (columns ascending);
+    # key(LM) ascending == lead column descending (reference :285-290)
+    exps_all = plan.dict_exps().astype(np.int64)
+    new_ex, new_cf, new_len = [], [], []
+    for k in range(len(leads) - 1, -1, -1):
+        c = cols[rp[k]:rp[k + 1]]
+        ex = exps_all[c]
+        cf = vals[rp[k]:rp[k + 1]]
+        update_pairs(state, Poly(ring, tuple(zip(map(tuple, ex.tolist()), cf.tolist()))))
+        new_ex.append(ex)
+        new_cf.append(cf)
+        new_len.append(len(c))
+    # keep the device basis in lockstep (no re-upload of the whole basis)
+    eng = Engine.for_ring(ring)
+    if getattr(soa, "_f4b_token", None) == eng.token and new_len:
+        eng.append_polys(np.asarray(new_len), np.concatenate(new_ex), np.concatenate(new_cf))
+    if getattr(soa, "_f4b_token", None) is not None and soa._f4b_token[0] == eng.uid:
+        state._dev_token, state._dev_n = eng.token, len(state.basis)
+    state.zero_reductions += ech.zero_row_count
+    dt = plan.timings_ns
+    state.stats.append(BatchStats(
+        degree=degree, r=plan.counters.r, N=plan.counters.N, M=plan.counters.M, nnz=plan.counters.nnz,
+        rank=ech.rank, new_polys=len(new_len), zero_reductions=ech.zero_row_count,
+        closure_rounds=plan.counters.closure_rounds,
+        timings_ns={"dict_build": dt.get("dict_build_ns", 0), "row_assemble": dt.get("row_assemble_ns", 0),
+                    "numeric_core": numeric_ns, "fill_generated": ech.fill_generated,
+                    **{f"device_{k}": v for k, v in ech.timings().items()}}))
+    return plan, ech, kernel
+
+
+def spoly(f: Poly, g: Poly) -> Poly:
+    if f.is_zero() or g.is_zero():
+        raise PreconditionError("S-polynomial of a zero polynomial")
+    p = f.ring.modulus.p
+    L = mon_lcm(f.lm(), g.lm())
+    a = poly_mul_mon(mon_div(L, f.lm()), f)
+    b = poly_mul_mon(mon_div(L, g.lm()), g)
+    ia, ib = pow(f.lc(), p - 2, p), pow(g.lc(), p - 2, p)
+    left = Poly(f.ring, tuple((e, c * ia % p) for e, c in a.terms))
+    return poly_add_scaled(left, (p - ib) % p, b)
+
+
+def normal_form(f: Poly, basis: list) -> Poly:
+    """Full remainder; reducer = smallest LM first, then lowest index
+    (reference :70-105, the closure rule of compile_batch)."""
+    live = [g for g in basis if not g.is_zero()]
+    if f.is_zero() or not live:
+        return f
+    ring = f.ring
+    p = ring.modulus.p
+    table = sorted(range(len(live)), key=lambda i: (ring.sort_key(live[i].lm()), i))
+    lms = [(live[i].lm(), i) for i in table]
+    work, out = f, []
+    while not work.is_zero():
+        lead, lc = work.terms[0]
+        hit = next((i for lm, i in lms if mon_divides(lm, lead)), None)
+        if hit is None:
+            out.append((lead, lc))
+            work = Poly(ring, work.terms[1:])
+            continue
+        g = live[hit]
+        coef = lc * pow(g.lc(), p - 2, p) % p
+        work = poly_add_scaled(work, p - coef, poly_mul_mon(mon_div(lead, g.lm()), g))
+    return Poly(ring, tuple(out))
+
+
+def reduce_basis(polys: list, ring: Ring) -> list:
+    """Canonical reduced basis: minimal, tail-reduced, monic, sorted by lead
+    descending (reference :314-332).  Host-side; see DESIGN.md §next."""
+    work = sorted((poly_monic(f) for f in polys if not f.is_zero()), key=lambda f: ring.sort_key(f.lm()))
+    minimal = []
+    for f in work:
+        if not any(mon_divides(g.lm(), f.lm()) for g in minimal):
+            minimal.append(f)
+    changed = True
+    while changed:
+        changed = False
+        for i in range(len(minimal)):
+            r = normal_form(minimal[i], minimal[:i] + minimal[i + 1:])
+            if r.terms != minimal[i].terms:
+                minimal[i] = poly_monic(r)
+                changed = True
+    minimal.sort(key=lambda f: ring.sort_key(f.lm()), reverse=True)
+    return minimal
+
+
+def f4_groebner(system: list, ring: Ring, config: F4Config | None = None) -> list:
+    """Reduced Gröbner basis via the GPU F4 driver (reference :335-350)."""
+    config = config or F4Config()
+    if any(f.is_zero() for f in system):
+        raise PreconditionError("zero polynomial in input system")
+    state = GroebnerState(ring)
+    for f in system:
+        update_pairs(state, poly_monic(f))
+    steps = 0
+    while state.n_pairs():
+        if steps >= config.max_steps:
+            raise NonterminationError(f"f4 exceeded {config.max_steps} batches")
+        f4_step(state, config)
+        steps += 1
+    return reduce_basis(state.basis, ring)
+
+
+@dataclass
+class GroebnerReport:
+    ok: bool
+    detail: str = ""
+    witness: tuple | None = None
+
+
+def is_groebner(G: list, ring: Ring) -> GroebnerReport:
+    live = [g for g in G if not g.is_zero()]
+    for a in range(len(live)):
+        for b in range(a + 1, len(live)):
+            if not normal_form(spoly(live[a], live[b]), live).is_zero():
+                return GroebnerReport(False, f"S-poly of members {a},{b} does not reduce to zero", (a, b))
+    return GroebnerReport(True)
+
+
+def verify_kernel_syzygy(plan: LayoutPlan, basis: list, kernel: KernelBasis) -> GroebnerReport:
+    """Exact recombination sum_i v_i (t_i g_{k_i}) == 0 (reference :409-428)."""
+    ring = plan.ring
+    for n, v in enumerate(kernel.vectors):
+        if len(v) != plan.n_rows:
+            return GroebnerReport(False, f"kernel vector {n} has wrong length")
+        total = Poly(ring)
+        for i, row in enumerate(plan.row_meta):
+            c = int(v[i])
+            if c:
+                total = poly_add_scaled(total, c, poly_mul_mon(row.shift, basis[row.basis_index]))
+        if not total.is_zero():
+            return GroebnerReport(False, f"kernel vector {n} recombines to {total}")
+    return GroebnerReport(True)
