@@ -1,0 +1,382 @@
+"""Benchmark: Macaulay nnz/s assembled + F_p reduction s/F4 step on cyclic-8 / F_32003.
+
+Workload (BASELINE.json metric config, fits one GPU): every F4 batch of the
+cyclic-8 / F_32003 grevlex run.  Setup runs the full F4 computation once on
+the GPU (bit-exact with the reference) and captures each batch's row list and
+basis prefix; the device basis (final, HBM-resident) then serves all batches
+(closure candidates restricted to the batch's basis prefix, which reproduces
+the live plans exactly).
+
+One bench *step* = all 38 batches of the run through compile_batch ->
+psge_reduce (new-row mode, what the F4 driver consumes).  L2 is flushed
+(a 256 MiB write) before every batch, outside the CUDA-event intervals.
+
+  value      = sum(M) / sum(t_sym): nnz assembled per second, t_sym = device
+               time of compile_batch (CUDA events inside the engine), inputs
+               resident in HBM.
+  e2e        = the same metric through the public Python API / C ABI with
+               host buffers: each batch uploads its basis + rows (fresh device
+               basis) and downloads the assembled LayoutPlan arrays.
+  reduction  = F_p reduction seconds per F4 step (psge, device time).
+
+--impl reference times the CPU oracle (a NumPy restatement of the reference
+fpgb algorithm, tests pin it byte-for-byte) on a bounded sample: cyclic-8
+steps restored from committed reference snapshots.
+"""
+
+from __future__ import annotations
+
+import argparse
+import gzip
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Macaulay nnz/s assembled + F_p reduction s/F4 step (cyclic-8, 1-8 GPU)"
+UNIT = "nnz/s"
+WORKLOAD = "cyclic-8 over F_32003, grevlex, all 38 F4 batches (compile_batch + psge_reduce)"
+CPU_SAMPLE_STEPS = (5, 6, 7)
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            pk = json.load(fh)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle on reference snapshots
+# ---------------------------------------------------------------------------
+def cpu_sample(steps=CPU_SAMPLE_STEPS):
+    import oracle
+    from paper_2601_06765_b200.groebner import GroebnerState, Pair, _make_pair, select_batch
+    from paper_2601_06765_b200.symbolic import select_rows
+    from paper_2601_06765_b200.systems import parse_system
+
+    path = os.path.join(ROOT, "tests", "golden", "cyclic8_p32003.snap.json.gz")
+    if not os.path.exists(path):
+        return {"M": 0, "t_sym": 0.0, "t_num": 0.0, "steps": []}
+    with gzip.open(path, "rt") as fh:
+        snaps = json.load(fh)["snapshots"]
+    tot_M = tot_sym = tot_num = 0.0
+    done = []
+    for k in steps:
+        snap = snaps.get(str(k))
+        if snap is None:
+            continue
+        ring, basis = parse_system(snap["basis"])
+        st = GroebnerState(ring)
+        for f in basis:
+            st._push_basis(f)
+        st.pairs = sorted([_make_pair(st, i, j) for i, j in snap["pairs"]], key=Pair.sort_tuple)
+        spec, _ = select_batch(st)
+        soa = st.soa()
+        rows = [(r.shift, r.basis_index, r.role.value, r.provenance) for r in select_rows(spec, soa)]
+        t0 = time.perf_counter()
+        plan = oracle.compile_batch_arrays(rows, (soa.exps, soa.coeff, soa.offset, soa.length), ring.order)
+        t1 = time.perf_counter()
+        oracle.psge_arrays(len(plan["row_ptr"]) - 1, plan["counters"]["N"], plan["row_ptr"], plan["col_ind"],
+                           plan["val"], ring.modulus.p)
+        t2 = time.perf_counter()
+        tot_M += plan["counters"]["M"]
+        tot_sym += t1 - t0
+        tot_num += t2 - t1
+        done.append(k)
+    return {"M": tot_M, "t_sym": tot_sym, "t_num": tot_num, "steps": done}
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    for _ in range(args.warmup):
+        cpu_sample()
+    tM = tS = tN = 0.0
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        s = cpu_sample()
+        tM += s["M"]
+        tS += s["t_sym"]
+        tN += s["t_num"]
+    wall = time.perf_counter() - t0
+    value = tM / tS
+    sample = (f"cyclic-8/F_32003 F4 steps {list(CPU_SAMPLE_STEPS)} restored from reference snapshots; "
+              "NumPy oracle port of fpgb compile_batch + psge_reduce, single-threaded")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * wall / max(1, args.steps),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32 residues mod p",
+        "data": "synthetic (generated cyclic-8 system)",
+        "config": {"workload": WORKLOAD + " [CPU sample]", "sample_steps": list(CPU_SAMPLE_STEPS)},
+        "reduction_s_per_f4_step": tN / (args.steps * len(CPU_SAMPLE_STEPS)),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU workload capture
+# ---------------------------------------------------------------------------
+def capture_workload():
+    from paper_2601_06765_b200.groebner import GroebnerState, f4_step, update_pairs
+    from paper_2601_06765_b200.polynomials import poly_monic
+    from paper_2601_06765_b200.systems import gen_cyclic
+
+    ring, polys = gen_cyclic(8, 32003)
+    st = GroebnerState(ring)
+    for f in polys:
+        update_pairs(st, poly_monic(f))
+    batches = []
+
+    def cap(rows, soa, plan):
+        n = ring.n_vars
+        batches.append({
+            "rows": rows,
+            "rb": np.fromiter((r.basis_index for r in rows), dtype=np.int64, count=len(rows)),
+            "sh": np.asarray([r.shift for r in rows], dtype=np.int64).reshape(len(rows), n),
+            "n_basis": len(soa), "n_terms": soa.total_terms(),
+            "r": plan.counters.r, "N": plan.counters.N, "M": plan.counters.M,
+        })
+
+    t0 = time.perf_counter()
+    while st.n_pairs():
+        f4_step(st, _capture=cap)
+    return ring, st, batches, time.perf_counter() - t0
+
+
+class ClockSampler:
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = [], [], set()
+        try:
+            for line in open(self.path):
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) < 7:
+                    continue
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+                for nm, flag in zip(names, parts[3:7]):
+                    if flag.lower().startswith("active"):
+                        reasons.add(nm)
+            os.unlink(self.path)
+        except Exception:
+            pass
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# algorithmic bytes per kernel: totals per batch
+def kernel_bytes(name, b, KW):
+    M, N, r = b["M"], b["N"], b["r"]
+    key = 8 * KW
+    if name.startswith("k_join"):
+        return M * key + 4 * M + N * key
+    if name.startswith("k_fill"):
+        return 2 * M * (key + 4)
+    return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=1)
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2601_06765_b200.engine import Engine
+    from paper_2601_06765_b200.sparselin import csr_from_plan, psge_reduce
+    from paper_2601_06765_b200.symbolic import compile_batch
+
+    ring, st, batches, setup_s = capture_workload()
+    eng = Engine.for_ring(ring, local)
+    total_M = sum(b["M"] for b in batches)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def replay_step(record):
+        ts = tn = 0
+        for b in batches:
+            flush.fill_(1)
+            plan = eng.compile(b["rb"], b["sh"], True, list(range(b["n_basis"])))
+            ech = eng.psge_plan(plan, full=False)
+            inf = ech.info()
+            ts += plan.info["dict_build_ns"] + plan.info["row_assemble_ns"]
+            tn += inf["numeric_ns"]
+            if record is not None:
+                record.append((b, plan.info, inf))
+        return ts, tn
+
+    for _ in range(args.warmup):
+        replay_step(None)
+    # timed region
+    eng.profile(True)
+    _, launches0 = eng.profile_read()
+    records = []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        w0 = time.perf_counter()
+        t_sym = t_num = 0
+        for _ in range(args.steps):
+            a, c = replay_step(records)
+            t_sym += a
+            t_num += c
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - w0
+    if world > 1:
+        dist.barrier()
+    kprof, launches1 = eng.profile_read()
+    eng.profile(False)
+    t_tot_ns = float(t_sym + t_num)
+    if world > 1:
+        t = torch.tensor([t_tot_ns, float(t_sym)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_tot_ns, t_sym = float(t[0]), float(t[1])
+    ms_per_step = t_tot_ns / 1e6 / args.steps
+    value = world * total_M * args.steps / (t_sym / 1e9)
+    red_s = t_num / 1e9 / (args.steps * len(batches))
+
+    # roofline: the dominant kernel with an algorithmic byte model
+    peak, peak_src = _peaks()
+    KW = records[0][1]["key_words"] if records else 1
+    ranked = sorted(kprof.items(), key=lambda kv: -kv[1][1])
+    roof = None
+    for name, (cnt, ns) in ranked:
+        tot_bytes = 0
+        ok = True
+        for b, pinfo, _ in records:
+            kb = kernel_bytes(name, b, pinfo["key_words"])
+            if kb is None:
+                ok = False
+                break
+            tot_bytes += kb
+        if ok and ns > 0:
+            ach = tot_bytes / (ns * 1e-9) / 1e9
+            roof = {"bound": "hbm", "kernel": name, "achieved": ach, "peak": peak, "unit": "GB/s",
+                    "frac": ach / peak, "traffic": None, "launches": cnt, "avg_launch_us": ns / cnt / 1e3,
+                    "peak_source": peak_src, "share_of_step": ns / max(1.0, sum(v[1] for v in kprof.values()))}
+            break
+    # symbolic (FBSP) effective roofline, B_sym per SURVEY.md §8(d)
+    W = ring.n_key_words
+    B_sym = sum(b["M"] * (8 * W + 4) + 8 * b["M"] + 4 * (b["r"] + 1) + b["N"] * 8 * W for b in batches)
+    sym_frac = (B_sym * args.steps / (t_sym / 1e9) / 1e9) / peak
+
+    # e2e: public API, host buffers in and out, fresh device basis per batch
+    e2e = None
+    if args.e2e_steps > 0:
+        from paper_2601_06765_b200.groebner import _HostBasis
+
+        final = st.soa()
+        h2d = d2h = 0
+        e_sym = 0.0
+        e_M = 0
+        for _ in range(args.e2e_steps):
+            for b in batches:
+                nb_, nt = b["n_basis"], b["n_terms"]
+                from paper_2601_06765_b200.polynomials import SoaPolySet
+
+                soa = SoaPolySet(ring, final.mon_key[:nt], final.coeff[:nt], final.offset[:nb_ + 1],
+                                 final.length[:nb_], final.exps[:nt])
+                eng.clear_basis()
+                flush.fill_(1)
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                plan = compile_batch(b["rows"], soa)
+                rp, ci, va = plan.row_ptr, plan.col_ind, plan.val
+                dk = plan.dict_keys
+                t1 = time.perf_counter()
+                e_sym += t1 - t0
+                e_M += b["M"]
+                h2d += nt * (2 * ring.n_vars + 4) + (nb_ + 1) * 8 + len(b["rows"]) * (4 + 2 * ring.n_vars)
+                d2h += plan.counters.M * 8 + (plan.counters.r + 1) * 4 + plan.counters.N * 2 * ring.n_vars
+        e2e = {"value": world * e_M / e_sym, "unit": UNIT, "h2d_bytes_per_step": h2d // args.e2e_steps,
+               "d2h_bytes_per_step": d2h // args.e2e_steps,
+               "note": "per batch: basis + rows H2D (pageable), compile_batch, LayoutPlan arrays D2H; wall clock"}
+        eng.clear_basis()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        s = cpu_sample()
+        if s["t_sym"] > 0:
+            cpu = {"value": s["M"] / s["t_sym"], "unit": UNIT, "cores": 1, "kind": "port",
+                   "sample": f"cyclic-8 F4 steps {s['steps']} from reference snapshots, NumPy oracle port, "
+                             f"compile {s['t_sym']:.2f}s + psge {s['t_num']:.2f}s"}
+    if rank == 0:
+        kernels = {k: {"launches": v[0], "ms": round(v[1] / 1e6, 3)} for k, v in ranked[:12]}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u32 residues mod p (u64 monomial keys)",
+            "data": "synthetic (generated cyclic-8 system, deterministic)",
+            "config": {"workload": WORKLOAD, "batches": len(batches), "sum_M_per_step": total_M,
+                       "parallelism": "replicas" if world > 1 else "single",
+                       "l2": "flushed (256 MiB write) before every batch"},
+            "reduction_s_per_f4_step": red_s,
+            "symbolic_roofline": {"B_sym_bytes_per_step": B_sym, "frac": sym_frac, "peak": peak},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
+            "gpu_launches": launches1 - launches0, "wall_ms_per_step": 1000 * wall / args.steps,
+            "setup_s": round(setup_s, 2), "kernels_top": kernels,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -65,6 +65,11 @@ int f4b_ctx_create(int device, uint32_t p, int n_vars, int order, f4b_alloc_fn a
 int f4b_ctx_destroy(f4b_ctx* ctx);
 int f4b_ctx_set_stream(f4b_ctx* ctx, void* cuda_stream);
 const char* f4b_ctx_last_error(const f4b_ctx* ctx);
+/* Instrumentation: when enabled, every kernel launch is bracketed by CUDA
+ * events on the context stream; profile_read resolves them into lines
+ * "kernel launches total_ns" and reports the total launch count. */
+int f4b_ctx_profile(f4b_ctx* ctx, int enable);
+int f4b_ctx_profile_read(f4b_ctx* ctx, char* buf, int64_t buflen, int64_t* total_launches);
 
 /* Device-resident basis — replaces soa_pack / SoaPolySet
  * (polynomials.py:243-299, groebner.py:143-146).  `exps` is [T][n_vars] u16,

@@ -78,6 +78,47 @@ uint32_t read_u32(Ctx* c, const uint32_t* dptr) {
 
 void memset_async(Ctx* c, void* p, int v, size_t bytes) { check_cuda(cudaMemsetAsync(p, v, bytes, c->stream), "memset"); }
 
+ProfScope::ProfScope(Ctx* c_, const char* n) : c(c_), name(n) {
+  ++c->launches;
+  ++c->total_launches;
+  if (!c->prof) return;
+  if (c->ev_used + 2 > c->ev_pool.size()) {
+    size_t grow = std::max<size_t>(256, c->ev_pool.size());
+    for (size_t i = 0; i < grow; ++i) {
+      cudaEvent_t e;
+      check_cuda(cudaEventCreate(&e), "event pool");
+      c->ev_pool.push_back(e);
+    }
+  }
+  e0 = c->ev_used++;
+  check_cuda(cudaEventRecord(c->ev_pool[e0], c->stream), "event record");
+}
+
+ProfScope::~ProfScope() {
+  if (!c->prof) return;
+  size_t e1 = c->ev_used++;
+  cudaEventRecord(c->ev_pool[e1], c->stream);
+  c->pending.push_back({name, e0, e1});
+}
+
+static void prof_resolve(Ctx* c) {
+  if (c->pending.empty()) return;
+  check_cuda(cudaStreamSynchronize(c->stream), "sync");
+  for (const auto& p : c->pending) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, c->ev_pool[p.e0], c->ev_pool[p.e1]);
+    auto it = std::find_if(c->prof_acc.begin(), c->prof_acc.end(), [&](const auto& kv) { return kv.first == p.name; });
+    if (it == c->prof_acc.end()) {
+      c->prof_acc.push_back({p.name, {0.0, 0}});
+      it = c->prof_acc.end() - 1;
+    }
+    it->second.first += ms;
+    it->second.second += 1;
+  }
+  c->pending.clear();
+  c->ev_used = 0;
+}
+
 void plan_release(f4b_plan* pl) {
   if (!pl) return;
   Ctx* c = pl->ctx;
@@ -135,7 +176,7 @@ void spmm(Ctx* c, long long r, long long N, const int64_t* rp, const int64_t* co
   Fp fp{c->p, c->pprime, c->r2};
   if (r > 0 && b > 0) {
     unsigned blocks = (unsigned)std::max<long long>(1, (r * 32 + 255) / 256);
-    k_spmm<<<blocks, 256, 0, c->stream>>>(fp, drp.as<u32>(), dcol.as<u32>(), dval.as<u32>(), r, dx.as<u32>(), (int)b,
+    F4B_LAUNCH(c, k_spmm, blocks, 256, 0, fp, drp.as<u32>(), dcol.as<u32>(), dval.as<u32>(), r, dx.as<u32>(), (int)b,
                                           dy.as<u32>());
     check_cuda(cudaGetLastError(), "k_spmm");
   }
@@ -224,6 +265,7 @@ int f4b_ctx_destroy(f4b_ctx* h) {
                   &c->cl_round};
   for (DBuf* b : bufs) release(c, *b);
   if (c->h_stat) cudaFreeHost(c->h_stat);
+  for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   delete h;
   return F4B_OK;
 }
@@ -231,6 +273,42 @@ int f4b_ctx_destroy(f4b_ctx* h) {
 int f4b_ctx_set_stream(f4b_ctx* h, void* stream) {
   if (!h) return F4B_ERR_PRECONDITION;
   h->c.stream = (cudaStream_t)stream;
+  return F4B_OK;
+}
+
+int f4b_ctx_profile(f4b_ctx* h, int enable) {
+  if (!h) return F4B_ERR_PRECONDITION;
+  Ctx* _c = &h->c;
+  try {
+    prof_resolve(_c);
+  } catch (const Error& e) {
+    return e.code;
+  }
+  _c->prof_acc.clear();
+  _c->prof = enable != 0;
+  return F4B_OK;
+}
+
+int f4b_ctx_profile_read(f4b_ctx* h, char* buf, int64_t buflen, int64_t* total_launches) {
+  if (!h) return F4B_ERR_PRECONDITION;
+  Ctx* _c = &h->c;
+  try {
+    prof_resolve(_c);
+  } catch (const Error& e) {
+    return e.code;
+  }
+  if (total_launches) *total_launches = _c->total_launches;
+  std::string out;
+  for (const auto& kv : _c->prof_acc) {
+    char line[256];
+    snprintf(line, sizeof line, "%s %lld %.0f\n", kv.first.c_str(), kv.second.second, kv.second.first * 1e6);
+    out += line;
+  }
+  if (buf && buflen > 0) {
+    size_t n = std::min<size_t>(out.size(), (size_t)buflen - 1);
+    memcpy(buf, out.data(), n);
+    buf[n] = 0;
+  }
   return F4B_OK;
 }
 

@@ -364,11 +364,11 @@ __global__ void __launch_bounds__(SW_THREADS) k_dense_back(Fp fp, const u32* __r
                                                             const u32* __restrict__ dpiv, const u32* __restrict__ dprow,
                                                             u32 rankD, const u32* __restrict__ pbits_g,
                                                             const u32* __restrict__ pinv, const u32* __restrict__ prow_of,
-                                                            u32* __restrict__ Rd) {
+                                                            u32* __restrict__ Rd, u32* __restrict__ gacc) {
   extern __shared__ u32 smem[];
   const u32 nwords = (K + 31) / 32;
   u32* pbits = smem;
-  u32* acc = smem + nwords;
+  u32* acc = gacc ? gacc + (size_t)blockIdx.x * K : smem + nwords;
   __shared__ u32 sh[2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (u32 w = tid; w < nwords; w += blockDim.x) pbits[w] = pbits_g[w];
@@ -486,7 +486,7 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
   ensure(c, pk, Nn * sizeof(unsigned long long));
   check_cuda(cudaMemsetAsync(pk.p, 0xFF, Nn * sizeof(unsigned long long), c->stream), "memset pk");
   if (r) {
-    k_pivot_select<<<nb(r, 256), 256, 0, c->stream>>>(E->rp, E->col, r, pk.as<unsigned long long>());
+    F4B_LAUNCH(c, k_pivot_select, nb(r, 256), 256, 0, E->rp, E->col, r, pk.as<unsigned long long>());
     check_cuda(cudaGetLastError(), "k_pivot_select");
   }
   ensure(c, E->prow, Nn * sizeof(u32));
@@ -496,10 +496,10 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
   uint8_t* isA = c->flags.as<uint8_t>();
   uint8_t* notA = isA + Nn + 16;
   if (N) {
-    k_col_structure<<<nb(N, 256), 256, 0, c->stream>>>(fp, pk.as<unsigned long long>(), N, E->rp, E->val,
+    F4B_LAUNCH(c, k_col_structure, nb(N, 256), 256, 0, fp, pk.as<unsigned long long>(), N, E->rp, E->val,
                                                         E->prow.as<u32>(), E->invl.as<u32>(), isA, notA);
     check_cuda(cudaGetLastError(), "k_col_structure");
-    k_bits<<<nb((N + 31) / 32, 256), 256, 0, c->stream>>>(isA, N, E->abits.as<u32>());
+    F4B_LAUNCH(c, k_bits, nb((N + 31) / 32, 256), 256, 0, isA, N, E->abits.as<u32>());
     check_cuda(cudaGetLastError(), "k_bits");
   }
   release(c, pk);
@@ -513,8 +513,8 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
   ensure(c, E->acols, (size_t)std::max<long long>(E->nA, 1) * sizeof(u32));
   ensure(c, E->nonA, (size_t)std::max<long long>(E->K, 1) * sizeof(u32));
   if (N) {
-    k_compact_idx<<<nb(N, 256), 256, 0, c->stream>>>(isA, c->tmp_u32a.as<u32>(), N, E->acols.as<u32>());
-    k_compact_idx<<<nb(N, 256), 256, 0, c->stream>>>(notA, c->tmp_u32b.as<u32>(), N, E->nonA.as<u32>());
+    F4B_LAUNCH(c, k_compact_idx, nb(N, 256), 256, 0, isA, c->tmp_u32a.as<u32>(), N, E->acols.as<u32>());
+    F4B_LAUNCH(c, k_compact_idx, nb(N, 256), 256, 0, notA, c->tmp_u32b.as<u32>(), N, E->nonA.as<u32>());
     check_cuda(cudaGetLastError(), "k_compact_idx");
   }
   // C rows
@@ -522,14 +522,14 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
   ensure(c, c->flags, (size_t)std::max<long long>(r, 1) + 32);
   ensure(c, c->tmp_u32a, (size_t)(r + 2) * sizeof(u32));
   if (r) {
-    k_c_flags<<<nb(r, 256), 256, 0, c->stream>>>(E->rp, E->col, E->prow.as<u32>(), r, c->flags.as<uint8_t>());
+    F4B_LAUNCH(c, k_c_flags, nb(r, 256), 256, 0, E->rp, E->col, E->prow.as<u32>(), r, c->flags.as<uint8_t>());
     check_cuda(cudaGetLastError(), "k_c_flags");
   }
   exclusive_scan_flags(c, c->flags.as<uint8_t>(), c->tmp_u32a.as<u32>(), r);
   E->nC = r ? read_u32(c, c->tmp_u32a.as<u32>() + r) : 0;
   ensure(c, crows, (size_t)std::max<long long>(E->nC, 1) * sizeof(u32));
   if (r) {
-    k_compact_idx<<<nb(r, 256), 256, 0, c->stream>>>(c->flags.as<uint8_t>(), c->tmp_u32a.as<u32>(), r, crows.as<u32>());
+    F4B_LAUNCH(c, k_compact_idx, nb(r, 256), 256, 0, c->flags.as<uint8_t>(), c->tmp_u32a.as<u32>(), r, crows.as<u32>());
     check_cuda(cudaGetLastError(), "k_compact_idx");
   }
   // E2: D' = C swept over the A columns
@@ -547,7 +547,7 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
       check_cuda(cudaFuncSetAttribute(k_sweep<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 4096), "attr");
       attr0 = true;
     }
-    k_sweep<0><<<grid, SW_THREADS, smem, c->stream>>>(
+    F4B_LAUNCH(c, k_sweep<0>, grid, SW_THREADS, smem, 
         fp, E->rp, E->col, E->val, (u32)N, crows.as<u32>(), (u32)R, E->prow.as<u32>(), E->invl.as<u32>(),
         E->abits.as<u32>(), gl ? gacc.as<u32>() : nullptr, Dp.as<u32>(), (u32)K, E->nonA.as<u32>(), nullptr, 0, nullptr,
         nullptr, nullptr, 0, nullptr, nullptr, nullptr, err);
@@ -557,9 +557,9 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
     ensure(c, cand, (size_t)K * sizeof(int));
     ensure(c, used, (size_t)R + 16);
     ensure(c, pofc, (size_t)K * sizeof(u32));
-    k_fill_u32<<<nb(K, 256), 256, 0, c->stream>>>(cand.as<u32>(), K, (u32)INT_MAX);
+    F4B_LAUNCH(c, k_fill_u32, nb(K, 256), 256, 0, cand.as<u32>(), K, (u32)INT_MAX);
     check_cuda(cudaMemsetAsync(used.p, 0, R, c->stream), "memset");
-    k_fill_u32<<<nb(K, 256), 256, 0, c->stream>>>(pofc.as<u32>(), K, NONE);
+    F4B_LAUNCH(c, k_fill_u32, nb(K, 256), 256, 0, pofc.as<u32>(), K, NONE);
     check_cuda(cudaGetLastError(), "k_fill_u32");
     int bps = 0;
     check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_dense_forward, 256, 0), "occupancy");
@@ -570,11 +570,14 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
     uint8_t* usedp = used.as<uint8_t>();
     u32* pofcp = pofc.as<u32>();
     void* args[] = {&fp, &dpp, &Ru, &Ku, &candp, &usedp, &pofcp};
-    check_cuda(cudaLaunchCooperativeKernel((void*)k_dense_forward, G, 256, args, 0, c->stream), "k_dense_forward");
+    {
+      ProfScope ps(c, "k_dense_forward");
+      check_cuda(cudaLaunchCooperativeKernel((void*)k_dense_forward, G, 256, args, 0, c->stream), "k_dense_forward");
+    }
     // pivots of D'
     ensure(c, c->flags, (size_t)K + 32);
     ensure(c, c->tmp_u32a, (size_t)(K + 2) * sizeof(u32));
-    k_dense_pivots<<<nb(K, 256), 256, 0, c->stream>>>(pofc.as<u32>(), (u32)K, c->flags.as<uint8_t>());
+    F4B_LAUNCH(c, k_dense_pivots, nb(K, 256), 256, 0, pofc.as<u32>(), (u32)K, c->flags.as<uint8_t>());
     exclusive_scan_flags(c, c->flags.as<uint8_t>(), c->tmp_u32a.as<u32>(), K);
     E->rankD = read_u32(c, c->tmp_u32a.as<u32>() + K);
     DBuf pinv, dprow, pbits;
@@ -582,15 +585,17 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
     ensure(c, E->dpiv, (size_t)std::max<long long>(E->rankD, 1) * sizeof(u32));
     ensure(c, dprow, (size_t)std::max<long long>(E->rankD, 1) * sizeof(u32));
     ensure(c, pbits, (size_t)((K + 31) / 32 + 1) * sizeof(u32));
-    k_dense_piv_info<<<nb(K, 256), 256, 0, c->stream>>>(fp, Dp.as<u32>(), (u32)K, pofc.as<u32>(), pinv.as<u32>(),
+    F4B_LAUNCH(c, k_dense_piv_info, nb(K, 256), 256, 0, fp, Dp.as<u32>(), (u32)K, pofc.as<u32>(), pinv.as<u32>(),
                                                          c->flags.as<uint8_t>(), c->tmp_u32a.as<u32>(), E->dpiv.as<u32>(),
                                                          dprow.as<u32>());
-    k_bits<<<nb((K + 31) / 32, 256), 256, 0, c->stream>>>(c->flags.as<uint8_t>(), K, pbits.as<u32>());
+    F4B_LAUNCH(c, k_bits, nb((K + 31) / 32, 256), 256, 0, c->flags.as<uint8_t>(), K, pbits.as<u32>());
     check_cuda(cudaGetLastError(), "k_dense_piv_info");
     if (E->rankD) {
       ensure(c, E->Rd, (size_t)E->rankD * K * sizeof(u32));
       size_t smem2 = (size_t)((K + 31) / 32) * 4 + (size_t)K * 4;
-      if (smem2 > 200 * 1024) fail(F4B_ERR_SIZE_CAP, "dense block too wide for the device back-substitution");
+      DBuf gacc2;
+      const bool gl2 = smem2 > 200 * 1024;  // accumulator in HBM for very wide blocks
+      if (gl2) smem2 = (size_t)((K + 31) / 32) * 4;
       static bool attr1 = false;
       if (!attr1) {
         check_cuda(cudaFuncSetAttribute(k_dense_back, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 4096),
@@ -598,10 +603,11 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
         attr1 = true;
       }
       int g2 = sweep_grid(c, smem2, E->rankD);
-      k_dense_back<<<g2, SW_THREADS, smem2, c->stream>>>(fp, Dp.as<u32>(), (u32)K, E->dpiv.as<u32>(), dprow.as<u32>(),
-                                                         (u32)E->rankD, pbits.as<u32>(), pinv.as<u32>(), pofc.as<u32>(),
-                                                         E->Rd.as<u32>());
-      check_cuda(cudaGetLastError(), "k_dense_back");
+      if (gl2) ensure(c, gacc2, (size_t)g2 * K * sizeof(u32));
+      F4B_LAUNCH(c, k_dense_back, g2, SW_THREADS, smem2, fp, Dp.as<u32>(), (u32)K, E->dpiv.as<u32>(), dprow.as<u32>(),
+                 (u32)E->rankD, pbits.as<u32>(), pinv.as<u32>(), pofc.as<u32>(), E->Rd.as<u32>(),
+                 gl2 ? gacc2.as<u32>() : nullptr);
+      release(c, gacc2);
     }
     release(c, pinv);
     release(c, dprow);
@@ -627,7 +633,7 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
     check_cuda(cudaMemsetAsync(err, 0, 4, c->stream), "memset");
     if (rankD) {
       int g = (int)std::min<long long>(rankD, (long long)c->num_sms * 4);
-      k_emit_dense<<<g, SW_THREADS, 0, c->stream>>>(E->Rd.as<u32>(), (u32)K, (u32)rankD, E->dpiv.as<u32>(),
+      F4B_LAUNCH(c, k_emit_dense, g, SW_THREADS, 0, E->Rd.as<u32>(), (u32)K, (u32)rankD, E->dpiv.as<u32>(),
                                                      E->nonA.as<u32>(), E->pool_col.as<u32>(), E->pool_val.as<u32>(),
                                                      E->pool_cap, E->cursor.as<unsigned long long>(), E->d_off.as<u32>(),
                                                      E->d_len.as<u32>(), err);
@@ -696,7 +702,7 @@ static void run_a_sweep(Ctx* c, f4b_echelon* E) {
       unsigned long long cur = base_used;
       check_cuda(cudaMemcpyAsync(E->cursor.p, &cur, 8, cudaMemcpyHostToDevice, c->stream), "h2d");
       check_cuda(cudaMemsetAsync(err, 0, 4, c->stream), "memset");
-      k_sweep<1><<<grid, SW_THREADS, smem, c->stream>>>(
+      F4B_LAUNCH(c, k_sweep<1>, grid, SW_THREADS, smem, 
           fp, E->rp, E->col, E->val, (u32)N, arows.as<u32>(), (u32)nA, E->prow.as<u32>(), E->invl.as<u32>(),
           E->abits.as<u32>(), gl ? gacc.as<u32>() : nullptr, nullptr, (u32)K, E->nonA.as<u32>(),
           E->rankD ? E->Rd.as<u32>() : nullptr, (u32)E->rankD, E->rankD ? E->dpiv.as<u32>() : nullptr,

@@ -79,8 +79,35 @@ struct Ctx {
   DBuf dict_a, dict_b, front, front_new, uniq, red, lmpref, cand_idx, shift_in;
   DBuf cl_basis, cl_shift, cl_round;
   uint32_t pprime = 0, r2 = 0;
-  long long launches = 0;  // kernel launches issued (for reporting)
+  long long launches = 0;        // kernel launches issued (reset per compile call)
+  long long total_launches = 0;  // monotonically increasing
+  // optional per-kernel CUDA-event timing (f4b_ctx_profile)
+  bool prof = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  struct Pending {
+    const char* name;
+    size_t e0, e1;
+  };
+  std::vector<Pending> pending;
+  std::vector<std::pair<std::string, std::pair<double, long long>>> prof_acc;
 };
+
+// RAII scope: records CUDA events around one launch when profiling is on.
+struct ProfScope {
+  Ctx* c;
+  const char* name;
+  size_t e0 = 0;
+  ProfScope(Ctx* c_, const char* n);
+  ~ProfScope();
+};
+
+#define F4B_LAUNCH(c, kern, grid, block, smem, ...)                   \
+  do {                                                                \
+    ::f4b::ProfScope _f4b_ps((c), #kern);                             \
+    kern<<<(grid), (block), (smem), (c)->stream>>>(__VA_ARGS__);      \
+    ::f4b::check_cuda(cudaGetLastError(), #kern);                     \
+  } while (0)
 
 // scan.cu: exclusive scan of n u32 values into out (n+1 entries; out[n] = total).
 void exclusive_scan_u32(Ctx* c, const uint32_t* in, uint32_t* out, long long n);

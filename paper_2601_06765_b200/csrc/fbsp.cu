@@ -227,10 +227,8 @@ __global__ void k_dict_exps(KeyFmt f, const u64* __restrict__ dict, u32 N, u16* 
 // ---------------------------------------------------------------------------
 static inline unsigned nblk(long long n, int t) { return (unsigned)std::max<long long>(1, (n + t - 1) / t); }
 
-#define LAUNCH_CHECK(name)                       \
-  do {                                           \
-    check_cuda(cudaGetLastError(), name);        \
-    ++c->launches;                               \
+#define LAUNCH_CHECK(name) \
+  do {                     \
   } while (0)
 
 // Term-order comparison of exponent vectors (reference monomials.py:107-128).
@@ -264,7 +262,7 @@ static void encode_basis(Ctx* c, const KeyFmt& f) {
   if (B.ckey_terms == B.n_terms) return;
   ensure_keep(c, B.ckey, (size_t)(B.n_terms + 1) * KW * sizeof(u64));
   long long t0 = B.ckey_terms, t1 = B.n_terms;
-  k_encode_basis<KW><<<nblk(t1 - t0, 256), 256, 0, c->stream>>>(f, B.exps.as<u16>(), t0, t1, B.ckey.as<u64>());
+  F4B_LAUNCH(c, k_encode_basis<KW>, nblk(t1 - t0, 256), 256, 0, f, B.exps.as<u16>(), t0, t1, B.ckey.as<u64>());
   LAUNCH_CHECK("k_encode_basis");
   B.ckey_terms = t1;
 }
@@ -306,13 +304,13 @@ static void compile_t(Ctx* c, const KeyFmt& f, long long r0, const int32_t* h_rb
   check_cuda(cudaMemcpyAsync(c->shift_in.p, h_shift, r0 * n * sizeof(u16), cudaMemcpyHostToDevice, c->stream), "h2d shifts");
   check_cuda(cudaMemcpyAsync(c->rows_start.p, h_start.data(), (r0 + 1) * sizeof(u32), cudaMemcpyHostToDevice, c->stream),
              "h2d starts");
-  k_rows0<KW><<<nblk(r0, 256), 256, 0, c->stream>>>(f, r0, c->rows_basis.as<int>(), c->shift_in.as<u16>(),
+  F4B_LAUNCH(c, k_rows0<KW>, nblk(r0, 256), 256, 0, f, r0, c->rows_basis.as<int>(), c->shift_in.as<u16>(),
                                                      B.len.as<u32>(), c->rows_delta.as<u64>(), c->rows_len.as<u32>());
   LAUNCH_CHECK("k_rows0");
   long long mcap = std::max<long long>(M + M / 2 + 4096, 1 << 16);
   ensure(c, c->keys_all, mcap * KW * sizeof(u64));
   ensure(c, c->vals_all, mcap * sizeof(u32));
-  k_fill<KW><<<nblk(r0 * 32, 256), 256, 0, c->stream>>>(0, r0, c->rows_basis.as<int>(), c->rows_delta.as<u64>(),
+  F4B_LAUNCH(c, k_fill<KW>, nblk(r0 * 32, 256), 256, 0, 0, r0, c->rows_basis.as<int>(), c->rows_delta.as<u64>(),
                                                          c->rows_start.as<u32>(), B.off.as<u32>(), B.ckey.as<u64>(),
                                                          B.coeff.as<u32>(), c->keys_all.as<u64>(), c->vals_all.as<u32>());
   LAUNCH_CHECK("k_fill");
@@ -336,15 +334,15 @@ static void compile_t(Ctx* c, const KeyFmt& f, long long r0, const int32_t* h_rb
     ensure(c, c->tmp_u32c, (size_t)N + 16);  // done flags (u8)
     uint8_t* done = c->tmp_u32c.as<uint8_t>();
     check_cuda(cudaMemsetAsync(done, 0, N, c->stream), "memset done");
-    k_mark_leads<KW><<<nblk(r0, 256), 256, 0, c->stream>>>(r0, c->rows_start.as<u32>(), c->keys_all.as<u64>(), dict,
+    F4B_LAUNCH(c, k_mark_leads<KW>, nblk(r0, 256), 256, 0, r0, c->rows_start.as<u32>(), c->keys_all.as<u64>(), dict,
                                                             (u32)N, done);
     LAUNCH_CHECK("k_mark_leads");
     uint8_t* flags = c->flags.as<uint8_t>();
-    k_not_flags<<<nblk(N, 256), 256, 0, c->stream>>>(done, N, flags);
+    F4B_LAUNCH(c, k_not_flags, nblk(N, 256), 256, 0, done, N, flags);
     LAUNCH_CHECK("k_not_flags");
     u32* pos = c->tmp_u32b.as<u32>();
     exclusive_scan_flags(c, flags, pos, N);
-    k_compact<KW><<<nblk(N, 256), 256, 0, c->stream>>>(dict, N, flags, pos, c->front.as<u64>());
+    F4B_LAUNCH(c, k_compact<KW>, nblk(N, 256), 256, 0, dict, N, flags, pos, c->front.as<u64>());
     LAUNCH_CHECK("k_compact");
     long long nf = read_u32(c, pos + N);
 
@@ -376,14 +374,14 @@ static void compile_t(Ctx* c, const KeyFmt& f, long long r0, const int32_t* h_rb
     while (nf > 0 && nc > 0) {
       // closure search over the frontier
       ensure(c, c->red, (size_t)nf * sizeof(int));
-      k_closure_search<KW><<<nblk(nf * 32, 256), 256, 0, c->stream>>>(f, c->front.as<u64>(), nf, c->lmpref.as<u32>(),
+      F4B_LAUNCH(c, k_closure_search<KW>, nblk(nf * 32, 256), 256, 0, f, c->front.as<u64>(), nf, c->lmpref.as<u32>(),
                                                                         c->cand_idx.as<int>(), nc, nw, c->red.as<int>());
       LAUNCH_CHECK("k_closure_search");
       ensure(c, c->flags, (size_t)nf + 16);
       ensure(c, c->tmp_u32b, (size_t)(nf + 2) * sizeof(u32));
       flags = c->flags.as<uint8_t>();
       pos = c->tmp_u32b.as<u32>();
-      k_red_flags<<<nblk(nf, 256), 256, 0, c->stream>>>(c->red.as<int>(), nf, flags);
+      F4B_LAUNCH(c, k_red_flags, nblk(nf, 256), 256, 0, c->red.as<int>(), nf, flags);
       LAUNCH_CHECK("k_red_flags");
       exclusive_scan_flags(c, flags, pos, nf);
       long long R = read_u32(c, pos + nf);
@@ -403,7 +401,7 @@ static void compile_t(Ctx* c, const KeyFmt& f, long long r0, const int32_t* h_rb
         ensure_keep(c, c->cl_shift, clcap * n * sizeof(u16));
         ensure_keep(c, c->cl_round, clcap * sizeof(int));
       }
-      k_new_rows<KW><<<nblk(nf, 256), 256, 0, c->stream>>>(
+      F4B_LAUNCH(c, k_new_rows<KW>, nblk(nf, 256), 256, 0, 
           f, c->front.as<u64>(), nf, c->red.as<int>(), pos, r, n_cl, B.off.as<u32>(), B.len.as<u32>(), B.ckey.as<u64>(),
           B.lmexp.as<u16>(), B.maxe.as<u16>(), (int)rounds, c->rows_basis.as<int>(), c->rows_delta.as<u64>(),
           c->rows_len.as<u32>(), c->cl_basis.as<int>(), c->cl_shift.as<u16>(), c->cl_round.as<int>(), err);
@@ -411,7 +409,7 @@ static void compile_t(Ctx* c, const KeyFmt& f, long long r0, const int32_t* h_rb
       // offsets of the new rows continue after M
       ensure(c, c->tmp_u32a, (size_t)(R + 2) * sizeof(u32));
       exclusive_scan_u32(c, c->rows_len.as<u32>() + r, c->tmp_u32a.as<u32>(), R);
-      k_offsets<<<nblk(R + 1, 256), 256, 0, c->stream>>>(c->tmp_u32a.as<u32>(), R, (u32)M, c->rows_start.as<u32>() + r);
+      F4B_LAUNCH(c, k_offsets, nblk(R + 1, 256), 256, 0, c->tmp_u32a.as<u32>(), R, (u32)M, c->rows_start.as<u32>() + r);
       LAUNCH_CHECK("k_offsets");
       long long Mk = read_u32(c, c->tmp_u32a.as<u32>() + R);
       if (M + Mk >= (1ll << 31)) fail(F4B_ERR_SIZE_CAP, "batch has more than 2^31 terms");
@@ -420,7 +418,7 @@ static void compile_t(Ctx* c, const KeyFmt& f, long long r0, const int32_t* h_rb
         ensure_keep(c, c->keys_all, mcap * KW * sizeof(u64));
         ensure_keep(c, c->vals_all, mcap * sizeof(u32));
       }
-      k_fill<KW><<<nblk(R * 32, 256), 256, 0, c->stream>>>(r, r + R, c->rows_basis.as<int>(), c->rows_delta.as<u64>(),
+      F4B_LAUNCH(c, k_fill<KW>, nblk(R * 32, 256), 256, 0, r, r + R, c->rows_basis.as<int>(), c->rows_delta.as<u64>(),
                                                             c->rows_start.as<u32>(), B.off.as<u32>(), B.ckey.as<u64>(),
                                                             B.coeff.as<u32>(), c->keys_all.as<u64>(), c->vals_all.as<u32>());
       LAUNCH_CHECK("k_fill");
@@ -435,10 +433,10 @@ static void compile_t(Ctx* c, const KeyFmt& f, long long r0, const int32_t* h_rb
       ensure(c, c->front_new, (size_t)(nu + 1) * KW * sizeof(u64));
       flags = c->flags.as<uint8_t>();
       pos = c->tmp_u32b.as<u32>();
-      k_absent_flags<KW><<<nblk(nu, 256), 256, 0, c->stream>>>(c->uniq.as<u64>(), nu, dict, (u32)N, flags);
+      F4B_LAUNCH(c, k_absent_flags<KW>, nblk(nu, 256), 256, 0, c->uniq.as<u64>(), nu, dict, (u32)N, flags);
       LAUNCH_CHECK("k_absent_flags");
       exclusive_scan_flags(c, flags, pos, nu);
-      k_compact<KW><<<nblk(nu, 256), 256, 0, c->stream>>>(c->uniq.as<u64>(), nu, flags, pos, c->front_new.as<u64>());
+      F4B_LAUNCH(c, k_compact<KW>, nblk(nu, 256), 256, 0, c->uniq.as<u64>(), nu, flags, pos, c->front_new.as<u64>());
       LAUNCH_CHECK("k_compact");
       long long nnew = read_u32(c, pos + nu);
       // merged dictionary (symbolic.py:281-290)
@@ -448,7 +446,7 @@ static void compile_t(Ctx* c, const KeyFmt& f, long long r0, const int32_t* h_rb
       (void)other;
       ensure(c, obuf, (size_t)(N + nnew + 1) * KW * sizeof(u64));
       if (nnew) {
-        k_merge_corank<KW><<<nblk(N + nnew, 256), 256, 0, c->stream>>>(cbuf.as<u64>(), (u32)N, c->front_new.as<u64>(),
+        F4B_LAUNCH(c, k_merge_corank<KW>, nblk(N + nnew, 256), 256, 0, cbuf.as<u64>(), (u32)N, c->front_new.as<u64>(),
                                                                         (u32)nnew, obuf.as<u64>());
         LAUNCH_CHECK("k_merge_corank");
         dict = obuf.as<u64>();
@@ -507,12 +505,12 @@ static void compile_t(Ctx* c, const KeyFmt& f, long long r0, const int32_t* h_rb
       attr_set[KW] = true;
     }
     int blocks = (int)std::min<long long>(nblk(M, 512), (long long)c->num_sms * (use_smem ? 1 : 4));
-    k_join<KW><<<blocks, 512, smem, c->stream>>>(c->keys_all.as<u64>(), M, pl->dict.as<u64>(), (u32)N, use_smem,
+    F4B_LAUNCH(c, k_join<KW>, blocks, 512, smem, c->keys_all.as<u64>(), M, pl->dict.as<u64>(), (u32)N, use_smem,
                                                  pl->col_ind.as<u32>(), err);
     LAUNCH_CHECK("k_join");
   }
   if (N) {
-    k_dict_exps<KW><<<nblk(N, 256), 256, 0, c->stream>>>(f, pl->dict.as<u64>(), (u32)N, pl->dict_exps.as<u16>());
+    F4B_LAUNCH(c, k_dict_exps<KW>, nblk(N, 256), 256, 0, f, pl->dict.as<u64>(), (u32)N, pl->dict_exps.as<u16>());
     LAUNCH_CHECK("k_dict_exps");
   }
   check_cuda(cudaEventRecord(ev2, c->stream), "event record");

@@ -118,10 +118,10 @@ static void radix_sort_t(Ctx* c, const u64* in, long long n, int bits, u64** res
   const u64* src = in;
   int which = 0;
   for (int b = 0; b < bits; b += 8) {
-    k_radix_count<KW><<<tiles, RS_THREADS, 0, c->stream>>>(src, n, b, hist, tiles);
+    F4B_LAUNCH(c, k_radix_count<KW>, tiles, RS_THREADS, 0, src, n, b, hist, tiles);
     check_cuda(cudaGetLastError(), "k_radix_count");
     exclusive_scan_u32(c, hist, offs, (long long)256 * tiles);
-    k_radix_scatter<KW><<<tiles, RS_THREADS, 0, c->stream>>>(src, bufs[which], n, b, offs, tiles);
+    F4B_LAUNCH(c, k_radix_scatter<KW>, tiles, RS_THREADS, 0, src, bufs[which], n, b, offs, tiles);
     check_cuda(cudaGetLastError(), "k_radix_scatter");
     src = bufs[which];
     which ^= 1;
@@ -168,10 +168,10 @@ static long long unique_t(Ctx* c, const u64* sorted, long long n, u64* out) {
   u32* pos = c->tmp_u32a.as<u32>();
   const int T = 256;
   unsigned blocks = (unsigned)((n + T - 1) / T);
-  k_head_flags<KW><<<blocks, T, 0, c->stream>>>(sorted, n, flags);
+  F4B_LAUNCH(c, k_head_flags<KW>, blocks, T, 0, sorted, n, flags);
   check_cuda(cudaGetLastError(), "k_head_flags");
   exclusive_scan_flags(c, flags, pos, n);
-  k_compact_keys<KW><<<blocks, T, 0, c->stream>>>(sorted, n, flags, pos, out);
+  F4B_LAUNCH(c, k_compact_keys<KW>, blocks, T, 0, sorted, n, flags, pos, out);
   check_cuda(cudaGetLastError(), "k_compact_keys");
   return (long long)read_u32(c, pos + n);
 }

@@ -86,16 +86,16 @@ template <class Load>
 static void scan_level(Ctx* c, Load ld, u32* out, long long n, u32* scratch) {
   long long tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
   if (tiles <= 1) {
-    k_tile_scan<Load><<<1, SCAN_THREADS, 0, c->stream>>>(ld, n, nullptr, out);
+    F4B_LAUNCH(c, k_tile_scan<Load>, 1, SCAN_THREADS, 0, ld, n, nullptr, out);
     check_cuda(cudaGetLastError(), "k_tile_scan");
     return;
   }
   u32* sums = scratch;
   u32* prefix = scratch + tiles + 1;
-  k_tile_sums<Load><<<(unsigned)tiles, SCAN_THREADS, 0, c->stream>>>(ld, n, sums);
+  F4B_LAUNCH(c, k_tile_sums<Load>, (unsigned)tiles, SCAN_THREADS, 0, ld, n, sums);
   check_cuda(cudaGetLastError(), "k_tile_sums");
   scan_level<LoadU32>(c, LoadU32{sums}, prefix, tiles, prefix + tiles + 1);
-  k_tile_scan<Load><<<(unsigned)tiles, SCAN_THREADS, 0, c->stream>>>(ld, n, prefix, out);
+  F4B_LAUNCH(c, k_tile_scan<Load>, (unsigned)tiles, SCAN_THREADS, 0, ld, n, prefix, out);
   check_cuda(cudaGetLastError(), "k_tile_scan");
 }
 

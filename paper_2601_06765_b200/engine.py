@@ -124,6 +124,22 @@ class Engine:
         self._exps = np.zeros((0, n_vars), dtype=np.uint16)
         self._coeff = np.zeros(0, dtype=np.uint32)
 
+    # -- instrumentation -----------------------------------------------------
+    def profile(self, enable: bool):
+        """Bracket every kernel launch with CUDA events (f4b_ctx_profile)."""
+        self.ctx.check(self.lib.f4b_ctx_profile(self.ctx.h, 1 if enable else 0), "profile")
+
+    def profile_read(self):
+        """-> ({kernel: (launches, total_ns)}, total launches since context creation)."""
+        buf = C.create_string_buffer(1 << 16)
+        tot = np.zeros(1, dtype=np.int64)
+        self.ctx.check(self.lib.f4b_ctx_profile_read(self.ctx.h, buf, len(buf), ptr(tot, C.c_int64)), "profile read")
+        out = {}
+        for line in buf.value.decode().splitlines():
+            name, cnt, ns = line.rsplit(" ", 2)
+            out[name] = (int(cnt), float(ns))
+        return out, int(tot[0])
+
     # -- basis -------------------------------------------------------------
     @property
     def token(self):

@@ -273,7 +273,7 @@ def _dense_echelon(plan: LayoutPlan, m: FieldModulus) -> EchelonResult:
     return EchelonResult(list(pivots), piv, nonpiv, A.n_rows - rank, rank, 0)
 
 
-def f4_step(state: GroebnerState, config: F4Config | None = None):
+def f4_step(state: GroebnerState, config: F4Config | None = None, _capture=None):
     """One batch: select, compile (GPU), eliminate (GPU), harvest.
 
     Returns (plan, echelon, kernel) like the reference (:253-311)."""
@@ -286,6 +286,8 @@ def f4_step(state: GroebnerState, config: F4Config | None = None):
     soa = state.soa()
     rows = select_rows(spec, soa)
     plan = compile_batch(rows, soa, Closure.ONE_STEP_REDUCTION, config.exec_policy())
+    if _capture is not None:
+        _capture(rows, soa, plan)
     t0 = time.perf_counter_ns()
     if config.numeric == "dense":
         ech = _dense_echelon(plan, ring.modulus)

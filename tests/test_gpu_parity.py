@@ -1,0 +1,290 @@
+"""GPU parity: the CUDA path (through the Python API over the C ABI) against
+the CPU oracle on seeded inputs and against the reference's golden digests.
+
+Tolerance: none — everything is exact integer arithmetic mod p, so every
+comparison is byte equality (plan_to_text / RREF digests / arrays)."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import load_golden, load_snapshots, state_from_snapshot
+from paper_2601_06765_b200 import errors
+from paper_2601_06765_b200.fp import FieldModulus
+from paper_2601_06765_b200.groebner import GroebnerState, f4_groebner, f4_step, select_batch, update_pairs
+from paper_2601_06765_b200.monomials import Ring, mon_key_pack
+from paper_2601_06765_b200.polynomials import poly_monic, poly_parse, soa_pack, poly_normalize
+from paper_2601_06765_b200.sparselin import (CsrMatrix, KernelMode, csr_from_arrays, csr_from_dense, csr_from_plan,
+                                             left_kernel, psge_reduce, spmm, spmv, wiedemann_solve)
+from paper_2601_06765_b200.symbolic import (BatchSpec, Closure, PairTarget, Row, RowRole, compile_batch, plan_digest,
+                                            plan_to_text, select_rows)
+from paper_2601_06765_b200.systems import format_system, gen_cyclic, gen_katsura
+
+pytestmark = pytest.mark.gpu
+
+M7 = FieldModulus(7)
+R2 = Ring(["x", "y"], "grevlex", M7)
+
+
+def _oracle_plan(rows, soa, closure=True):
+    return oracle.compile_batch_arrays([(r.shift, r.basis_index, r.role.value, r.provenance) for r in rows],
+                                       (soa.exps, soa.coeff, soa.offset, soa.length), soa.ring.order, closure=closure)
+
+
+def _check_plan(plan, rows, soa, closure=True):
+    ring = soa.ring
+    ref = _oracle_plan(rows, soa, closure)
+    assert plan_to_text(plan) == oracle.plan_text(ref, ring.modulus.p, ring.order, ring.var_names)
+    return ref
+
+
+def _rref_digest(ech):
+    return oracle.rref_sha256(ech.pivot_rows, ech.nonpivot_rows)
+
+
+# ---------------------------------------------------------------------------
+# compile_batch: worked examples and edge cases (reference tests/test_symbolic.py)
+# ---------------------------------------------------------------------------
+def test_compile_worked_example(cuda):
+    soa = soa_pack([poly_parse("x^2 - y", R2), poly_parse("x*y - 1", R2)], R2)
+    rows = select_rows(BatchSpec([PairTarget((2, 1), 0, 0, 1)], (0, 1)), soa)
+    plan = compile_batch(rows, soa, Closure.SUPPORT_ONLY)
+    assert [tuple(k) for k in plan.dict_keys.tolist()] == [mon_key_pack(m, R2) for m in [(2, 1), (0, 2), (1, 0)]]
+    assert plan.row_ptr.tolist() == [0, 2, 4] and plan.col_ind.tolist() == [0, 1, 0, 2]
+    assert plan.val.tolist() == [1, 6, 1, 6]
+    plan.validate()
+    ech = psge_reduce(csr_from_plan(plan, M7), panel_width=2)
+    assert ech.rank == 2 and ech.pivot_cols == [0, 1]
+    lead, cols, vals = ech.nonpivot_rows[0]
+    assert lead == 1 and cols.tolist() == [1, 2] and vals.tolist() == [1, 6]
+
+
+def test_compile_closure_examples(cuda):
+    soa = soa_pack([poly_parse(t, R2) for t in ("x^2 - y", "x*y - 1", "y^2 - 1")], R2)
+    rows = select_rows(BatchSpec([PairTarget((2, 1), 0, 0, 1)], (0, 1)), soa)
+    plan = compile_batch(rows, soa, Closure.ONE_STEP_REDUCTION)
+    assert [r.role for r in plan.row_meta] == [RowRole.SPOLY_HALF, RowRole.SPOLY_HALF, RowRole.REDUCER]
+    assert plan.row_meta[2].shift == (0, 0) and plan.row_meta[2].basis_index == 2
+    assert plan.counters.closure_rounds == 1
+    _check_plan(plan, rows, soa)
+    rx = Ring(["x"], "grevlex", M7)
+    gb = soa_pack([poly_parse("x - 1", rx)], rx)
+    seed = [Row((2,), 0, RowRole.SPOLY_HALF, 0)]
+    plan = compile_batch(seed, gb, Closure.ONE_STEP_REDUCTION)
+    assert [r.shift for r in plan.row_meta] == [(2,), (1,), (0,)]
+    assert [tuple(k) for k in plan.dict_keys.tolist()] == [mon_key_pack((e,), rx) for e in (3, 2, 1, 0)]
+
+
+def test_compile_edge_cases(cuda):
+    soa = soa_pack([poly_parse("x^2 - y", R2), poly_parse("x*y - 1", R2)], R2)
+    empty = compile_batch([], soa)
+    assert empty.row_ptr.tolist() == [0] and empty.counters.N == 0 and empty.dict_keys.shape == (0, R2.n_key_words)
+    with pytest.raises(errors.LaneOverflowError):
+        compile_batch([Row((65535, 0), 0, RowRole.SPOLY_HALF, 0)], soa)
+    zsoa = soa_pack([poly_parse("x - 1", R2), poly_parse("0", R2)], R2)
+    with pytest.raises(errors.PropertyViolationError):
+        compile_batch([Row((0, 1), 1, RowRole.SPOLY_HALF, 0)], zsoa)
+    import paper_2601_06765_b200.symbolic as sym
+
+    rx = Ring(["x"], "grevlex", M7)
+    gb = soa_pack([poly_parse("x - 1", rx)], rx)
+    old = sym.DICT_CAP
+    sym.DICT_CAP = 10
+    try:
+        with pytest.raises(errors.SizeCapError):
+            compile_batch([Row((50,), 0, RowRole.SPOLY_HALF, 0)], gb, Closure.ONE_STEP_REDUCTION)
+    finally:
+        sym.DICT_CAP = old
+
+
+def _random_poly(rng, ring, max_exp, terms):
+    ts = [(tuple(int(x) for x in rng.integers(0, max_exp + 1, ring.n_vars)), int(rng.integers(1, ring.modulus.p)))
+          for _ in range(terms)]
+    return poly_monic(poly_normalize(ts, ring))
+
+
+@pytest.mark.parametrize("order,n,max_exp,p", [("grevlex", 2, 3, 7), ("grevlex", 5, 4, 32003),
+                                               ("deglex", 4, 3, 101), ("lex", 3, 3, 65521),
+                                               ("lex", 6, 2, 101), ("grevlex", 9, 2, 2147483629),
+                                               ("grevlex", 3, 40, 32003)])
+def test_compile_random_against_oracle(cuda, order, n, max_exp, p):
+    ring = Ring([f"v{i}" for i in range(n)], order, FieldModulus(p))
+    rng = np.random.default_rng(n * 1000 + max_exp)
+    for trial in range(6):
+        polys = []
+        while len(polys) < 5:
+            f = _random_poly(rng, ring, max_exp, int(rng.integers(1, 12)))
+            if not f.is_zero():
+                polys.append(f)
+        soa = soa_pack(polys, ring)
+        rows = sorted({Row(tuple(int(x) for x in rng.integers(0, 3, n)), int(rng.integers(0, 5)),
+                           RowRole.SPOLY_HALF, int(rng.integers(0, 4))) for _ in range(int(rng.integers(1, 9)))},
+                      key=lambda r: (r.provenance, mon_key_pack(r.shift, ring), r.basis_index))
+        for closure in (Closure.SUPPORT_ONLY, Closure.ONE_STEP_REDUCTION):
+            plan = compile_batch(rows, soa, closure)
+            _check_plan(plan, rows, soa, closure is Closure.ONE_STEP_REDUCTION)
+
+
+# ---------------------------------------------------------------------------
+# psge_reduce against the oracle (reference tests/test_sparselin.py)
+# ---------------------------------------------------------------------------
+def _random_sparse(rng, r, c, density, p):
+    mat = (rng.random((r, c)) < density) * rng.integers(1, p, (r, c), dtype=np.int64)
+    return mat.astype(np.uint64)
+
+
+def _oracle_rref(mat, p):
+    A = csr_from_dense(mat, FieldModulus(p))
+    e = oracle.psge_arrays(A.n_rows, A.n_cols, A.row_ptr, A.col_ind, A.val, p)
+    return e, oracle.rref_sha256(e["pivot_rows"], e["nonpivot_rows"])
+
+
+@pytest.mark.parametrize("p", [7, 101, 32003, 65521, 2147483629])
+@pytest.mark.parametrize("density", [0.01, 0.05, 0.2, 0.6])
+def test_psge_random_against_oracle(cuda, p, density):
+    m = FieldModulus(p)
+    rng = np.random.default_rng(p % 997 + int(density * 1000))
+    for _ in range(5):
+        r, c = (int(x) for x in rng.integers(5, 90, 2))
+        mat = _random_sparse(rng, r, c, density, p)
+        if rng.random() < 0.5:  # duplicate rows -> zero reductions
+            mat[rng.integers(0, r, r // 3)] = mat[rng.integers(0, r, r // 3)]
+        e, want = _oracle_rref(mat, p)
+        ech = psge_reduce(csr_from_dense(mat, m), panel_width=int(rng.integers(1, 17)))
+        assert ech.rank == e["rank"] and ech.zero_row_count == e["zero_row_count"]
+        assert ech.pivot_cols == e["pivot_cols"]
+        assert _rref_digest(ech) == want
+
+
+def test_psge_zero_and_empty(cuda):
+    A = CsrMatrix(3, 4, np.zeros(4, np.int64), np.zeros(0, np.int64), np.zeros(0, np.uint64), M7)
+    res = psge_reduce(A)
+    assert res.rank == 0 and res.zero_row_count == 3 and res.pivot_cols == []
+    with pytest.raises(errors.PreconditionError):
+        psge_reduce(A, panel_width=0)
+    res = psge_reduce(csr_from_dense(np.array([[1, 2, 0], [0, 1, 3], [0, 0, 1]], dtype=np.uint64), M7))
+    assert res.rank == 3 and res.pivot_cols == [0, 1, 2] and res.zero_row_count == 0
+
+
+def test_psge_wide_matrix_global_accumulator(cuda):
+    # N beyond the shared-memory accumulator (200 KB) exercises the HBM path
+    p = 32003
+    rng = np.random.default_rng(5)
+    r, c = 120, 60000
+    rows, cols, vals = [], [], []
+    for i in range(r):
+        k = rng.choice(c, 40, replace=False)
+        k.sort()
+        rows += [i] * 40
+        cols += k.tolist()
+        vals += rng.integers(1, p, 40).tolist()
+    rp = np.zeros(r + 1, np.int64)
+    np.cumsum(np.bincount(rows, minlength=r), out=rp[1:])
+    A = csr_from_arrays(r, c, rp, np.asarray(cols), np.asarray(vals, dtype=np.uint64), FieldModulus(p))
+    e = oracle.psge_arrays(r, c, A.row_ptr, A.col_ind, A.val, p)
+    ech = psge_reduce(A)
+    assert _rref_digest(ech) == oracle.rref_sha256(e["pivot_rows"], e["nonpivot_rows"])
+
+
+# ---------------------------------------------------------------------------
+# whole F4 runs against the reference's per-step digests
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("name,gen,args", [("cyclic5_p32003", gen_cyclic, (5, 32003)),
+                                           ("cyclic6_p32003", gen_cyclic, (6, 32003)),
+                                           ("katsura5_p32003", gen_katsura, (5, 32003)),
+                                           ("katsura6_p32003", gen_katsura, (6, 32003)),
+                                           ("katsura8_p32003", gen_katsura, (8, 32003)),
+                                           ("cyclic7_p65521", gen_cyclic, (7, 65521))])
+def test_f4_steps_match_reference(cuda, name, gen, args):
+    gold = load_golden(name)
+    ring, polys = gen(*args)
+    st = GroebnerState(ring)
+    for f in polys:
+        update_pairs(st, poly_monic(f))
+    k = 0
+    while st.n_pairs():
+        plan, ech, _ = f4_step(st)
+        g = gold["steps"][k]
+        assert (plan.counters.r, plan.counters.N, plan.counters.M, plan.counters.closure_rounds) == \
+            (g["r"], g["N"], g["M"], g["closure_rounds"]), f"step {k}"
+        assert plan_digest(plan) == g["plan_sha256"], f"plan step {k}"
+        assert _rref_digest(ech) == g["rref_sha256"], f"rref step {k}"
+        k += 1
+    assert k == len(gold["steps"])
+    from paper_2601_06765_b200.groebner import reduce_basis
+
+    text = format_system(ring, reduce_basis(st.basis, ring))
+    assert hashlib.sha256(text.encode()).hexdigest() == gold["final_sha256"]
+
+
+def test_f4_groebner_entry_point(cuda):
+    ring, polys = gen_cyclic(6, 32003)
+    gb = f4_groebner(polys, ring)
+    assert hashlib.sha256(format_system(ring, gb).encode()).hexdigest() == \
+        load_golden("cyclic6_p32003")["final_sha256"]
+
+
+@pytest.mark.parametrize("name", ["cyclic8_p32003", "katsura11_p32003", "mq16x32_p31", "cyclic7_p65521"])
+def test_large_step_replay(cuda, name):
+    """Full-size steps replayed from reference snapshots (north-star configs)."""
+    snaps = load_snapshots(name)
+    if not snaps:
+        pytest.skip(f"no snapshots for {name}")
+    gold = load_golden(name)
+    for k, snap in sorted(snaps.items()):
+        if k >= len(gold["steps"]):
+            continue
+        ring, st = state_from_snapshot(snap)
+        spec, _ = select_batch(st)
+        soa = st.soa()
+        rows = select_rows(spec, soa)
+        plan = compile_batch(rows, soa, Closure.ONE_STEP_REDUCTION)
+        assert plan_digest(plan) == gold["steps"][k]["plan_sha256"], f"plan step {k}"
+        ech = psge_reduce(csr_from_plan(plan, ring.modulus))
+        assert _rref_digest(ech) == gold["steps"][k]["rref_sha256"], f"rref step {k}"
+
+
+# ---------------------------------------------------------------------------
+# SpMM / Wiedemann / left kernel (reference tests/test_sparselin.py:100-306)
+# ---------------------------------------------------------------------------
+def test_spmm_matches_numpy(cuda):
+    for p in (101, 32003, 2147483629):
+        m = FieldModulus(p)
+        rng = np.random.default_rng(p % 1000)
+        mat = _random_sparse(rng, 70, 50, 0.2, p)
+        X = rng.integers(0, p, (50, 4), dtype=np.uint64)
+        want = np.zeros((70, 4), dtype=object)
+        for i in range(70):
+            for j in range(4):
+                want[i, j] = sum(int(a) * int(b) for a, b in zip(mat[i], X[:, j])) % p
+        got = spmm(csr_from_dense(mat, m), X)
+        assert np.array_equal(got.astype(object), want)
+        assert np.array_equal(spmv(csr_from_dense(mat, m), X[:, 0]).astype(object), want[:, 0])
+
+
+def test_left_kernel_small(cuda):
+    kb = left_kernel(csr_from_dense(np.array([[1, 2, 3], [1, 2, 3]], dtype=np.uint64), M7), count=4, seed=0)
+    assert kb.side == "left" and kb.dimension_found == 1
+    v = kb.vectors[0]
+    assert (int(v[0]) + int(v[1])) % 7 == 0 and v[0] != 0
+    kb = left_kernel(csr_from_dense(np.array([[1, 0, 0], [0, 1, 0]], dtype=np.uint64), M7), count=4, seed=0)
+    assert kb.dimension_found == 0
+
+
+def test_wiedemann_nullity(cuda):
+    m = FieldModulus(2147483629)
+    rng = np.random.default_rng(31415)
+    n, rank = 40, 34
+    Lf = rng.integers(0, m.p, (n, rank), dtype=np.uint64)
+    Rf = rng.integers(0, m.p, (rank, n), dtype=np.uint64)
+    mat = np.array([[sum(int(Lf[i, k]) * int(Rf[k, j]) for k in range(rank)) % m.p for j in range(n)]
+                    for i in range(n)], dtype=np.uint64)
+    A = csr_from_dense(mat, m)
+    kb = wiedemann_solve(A, KernelMode.RIGHT_KERNEL, seed=0)
+    assert kb.dimension_found == n - psge_reduce(A).rank
+    for v in kb.vectors:
+        assert (spmv(A, v) == 0).all()
+    eye = csr_from_dense(np.eye(3, dtype=np.uint64), FieldModulus(101))
+    assert wiedemann_solve(eye, KernelMode.MINPOLY, seed=11) == [100, 1]

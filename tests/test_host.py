@@ -1,0 +1,186 @@
+"""Host-side logic (CPU suite): C-ABI surface, data model, keys, pair logic,
+generators, and a whole F4 run driven by the host glue with the oracle as
+the per-step engine (checked against the reference's final-basis digest)."""
+
+import hashlib
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import ROOT, load_golden
+from paper_2601_06765_b200 import errors
+from paper_2601_06765_b200.fp import FieldModulus
+from paper_2601_06765_b200.groebner import (GroebnerState, Pair, _minimal_mask, reduce_basis, select_batch,
+                                            update_pairs)
+from paper_2601_06765_b200.monomials import (DeviceKeyFormat, Ring, key_pack_vec, key_unpack_vec, mon_compare,
+                                             mon_key_pack)
+from paper_2601_06765_b200.polynomials import Poly, poly_format, poly_monic, poly_parse
+from paper_2601_06765_b200.symbolic import Closure, select_rows
+from paper_2601_06765_b200.systems import format_system, gen_cyclic, gen_katsura, gen_random_quadratic, parse_system
+
+M7 = FieldModulus(7)
+R2 = Ring(["x", "y"], "grevlex", M7)
+
+
+# ---------------------------------------------------------------------------
+# C ABI
+# ---------------------------------------------------------------------------
+def test_library_exports_every_header_symbol(built_lib):
+    header = open(f"{ROOT}/include/f4b200.h").read()
+    names = set(re.findall(r"\b(f4b_[a-z_0-9]+)\s*\(", header)) - {"f4b_alloc_fn", "f4b_free_fn"}
+    assert len(names) >= 20
+    for name in sorted(names):
+        assert hasattr(built_lib, name), name
+    assert built_lib.f4b_abi_version() == 1
+
+
+def test_status_codes_map_to_reference_exceptions():
+    for code, exc in [(1, errors.MissingKeyError), (2, errors.SizeCapError), (3, errors.LaneOverflowError),
+                      (4, errors.PropertyViolationError), (5, errors.PreconditionError), (6, errors.DeviceError)]:
+        with pytest.raises(exc):
+            errors.raise_for_code(code, "x")
+
+
+def test_engine_refuses_without_gpu():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2601_06765_b200.symbolic import compile_batch
+    from paper_2601_06765_b200.polynomials import soa_pack
+    from paper_2601_06765_b200.symbolic import Row, RowRole
+
+    soa = soa_pack([poly_parse("x - 1", R2)], R2)
+    with pytest.raises(errors.DeviceError):
+        compile_batch([Row((1, 0), 0, RowRole.SPOLY_HALF, 0)], soa)
+
+
+# ---------------------------------------------------------------------------
+# data model
+# ---------------------------------------------------------------------------
+def test_parse_and_format_examples():
+    assert poly_parse("x^2*y + 3*x - 1", R2).terms == (((2, 1), 1), ((1, 0), 3), ((0, 0), 6))
+    assert poly_parse("0", R2).is_zero() and poly_parse("7", R2).is_zero()
+    assert poly_parse("-3", R2).terms == (((0, 0), 4),)
+    assert poly_format(poly_parse("x*y - 1", R2)) == "x*y + 6"
+    with pytest.raises(errors.PolyParseError):
+        poly_parse("x + z", R2)
+    with pytest.raises(errors.PolyParseError):
+        poly_parse("x^70000", R2)
+
+
+def test_generators_match_reference_texts():
+    assert [poly_format(f) for f in gen_cyclic(2, 7)[1]] == ["x0 + x1", "x0*x1 + 6"]
+    assert [poly_format(f) for f in gen_cyclic(3, 7)[1]] == ["x0 + x1 + x2", "x0*x1 + x0*x2 + x1*x2",
+                                                            "x0*x1*x2 + 6"]
+    assert [poly_format(f) for f in gen_katsura(1, 101)[1]] == ["x0 + 2*x1 + 100", "x0^2 + 2*x1^2 + 100*x0"]
+    ring, polys = gen_random_quadratic(3, 2, 0.5, 7, 101)
+    r2, p2 = parse_system(format_system(ring, polys))
+    assert [f.terms for f in p2] == [f.terms for f in polys]
+
+
+@pytest.mark.parametrize("order", ["grevlex", "deglex", "lex"])
+@pytest.mark.parametrize("n", [1, 3, 8, 12])
+def test_reference_keys_refine_the_order(order, n):
+    ring = Ring([f"v{i}" for i in range(n)], order, M7)
+    rng = np.random.default_rng(n)
+    a = rng.integers(0, 6, (400, n))
+    b = rng.integers(0, 6, (400, n))
+    ka, kb = key_pack_vec(a, ring), key_pack_vec(b, ring)
+    assert np.array_equal(key_unpack_vec(ka, ring), a)
+    for i in range(400):
+        want = mon_compare(tuple(a[i]), tuple(b[i]), ring)
+        ta, tb = tuple(int(w) for w in ka[i]), tuple(int(w) for w in kb[i])
+        assert (ta > tb) - (ta < tb) == want
+        assert ta == mon_key_pack(tuple(int(x) for x in a[i]), ring)
+
+
+@pytest.mark.parametrize("order", ["grevlex", "deglex", "lex"])
+@pytest.mark.parametrize("n,D", [(5, 7), (8, 15), (12, 7), (16, 4), (9, 31)])
+def test_device_key_order_isomorphic_and_shift_additive(order, n, D):
+    ring = Ring([f"v{i}" for i in range(n)], order, M7)
+    fmt = DeviceKeyFormat(ring, D)
+    rng = np.random.default_rng(D * 100 + n)
+    mons = [tuple(int(x) for x in rng.multinomial(int(rng.integers(0, D + 1)), [1.0 / n] * n))
+            for _ in range(300)]
+    dk = [fmt.pack_int(m) for m in mons]
+    rk = [mon_key_pack(m, ring) for m in mons]
+    for i in range(0, 300, 3):
+        for j in range(1, 300, 7):
+            assert (dk[i] < dk[j]) == (rk[i] < rk[j]) and (dk[i] == dk[j]) == (mons[i] == mons[j])
+    one = fmt.pack_int((0,) * n)
+    for i in range(0, 300, 5):
+        t, m = mons[i], mons[(i * 7 + 1) % 300]
+        tm = tuple(a + b for a, b in zip(t, m))
+        if sum(tm) <= D:
+            assert fmt.pack_int(tm) == fmt.pack_int(m) + fmt.pack_int(t) - one
+
+
+# ---------------------------------------------------------------------------
+# pair logic
+# ---------------------------------------------------------------------------
+def test_update_pairs_product_and_chain_criteria():
+    st = GroebnerState(R2)
+    update_pairs(st, poly_parse("x + 6", R2))
+    update_pairs(st, poly_parse("y + 6", R2))
+    assert st.pairs == []
+    r3 = Ring(["x", "y", "z"], "grevlex", M7)
+    st = GroebnerState(r3)
+    update_pairs(st, poly_parse("x^2*z + y", r3))
+    update_pairs(st, poly_parse("y^2*z + x", r3))
+    assert [(q.i, q.j) for q in st.pairs] == [(0, 1)]
+    update_pairs(st, poly_parse("x*y*z + 1", r3))
+    assert [(q.i, q.j) for q in st.pairs] == [(1, 2), (0, 2)]
+    with pytest.raises(errors.PreconditionError):
+        update_pairs(st, poly_parse("2*x + 1", r3))
+
+
+def test_minimal_mask():
+    u = np.array([[1, 0], [2, 0], [0, 1], [1, 1], [0, 3]])
+    assert _minimal_mask(u).tolist() == [True, False, True, False, False]
+
+
+def test_select_batch_groups_minimal_degree():
+    st = GroebnerState(R2)
+    st.basis = [poly_parse("x^2", R2)] * 4
+    k = R2.sort_key
+    st.pairs = sorted([Pair(0, 1, (2, 1), 3, k((2, 1))), Pair(1, 2, (1, 2), 3, k((1, 2))),
+                       Pair(2, 3, (4, 1), 5, k((4, 1)))], key=Pair.sort_tuple)
+    spec, d = select_batch(st)
+    assert d == 3 and len(spec.targets) == 2 and len(st.pairs) == 1
+    with pytest.raises(errors.PreconditionError):
+        select_batch(st)
+        select_batch(st)
+
+
+# ---------------------------------------------------------------------------
+# whole F4 run: host glue + oracle per step == reference final basis
+# ---------------------------------------------------------------------------
+def _f4_with_oracle(ring, polys):
+    st = GroebnerState(ring)
+    for f in polys:
+        update_pairs(st, poly_monic(f))
+    while st.n_pairs():
+        spec, _ = select_batch(st)
+        soa = st.soa()
+        rows = select_rows(spec, soa)
+        plan = oracle.compile_batch_arrays([(r.shift, r.basis_index, r.role.value, r.provenance) for r in rows],
+                                           (soa.exps, soa.coeff, soa.offset, soa.length), ring.order)
+        e = oracle.psge_arrays(len(plan["row_ptr"]) - 1, plan["counters"]["N"], plan["row_ptr"],
+                               plan["col_ind"], plan["val"], ring.modulus.p)
+        dexp = oracle.fbsp.ref_unkeys(plan["dict_keys"], ring.n_vars, ring.order)
+        new = [Poly(ring, tuple((tuple(int(x) for x in dexp[c]), int(v)) for c, v in zip(cols, vals)))
+               for _, cols, vals in e["nonpivot_rows"]]
+        for f in sorted(new, key=lambda f: ring.sort_key(f.lm())):
+            update_pairs(st, f)
+    return reduce_basis(st.basis, ring)
+
+
+@pytest.mark.parametrize("name,gen,args", [("cyclic5_p32003", gen_cyclic, (5, 32003)),
+                                           ("katsura5_p32003", gen_katsura, (5, 32003))])
+def test_host_f4_loop_with_oracle_matches_reference(name, gen, args):
+    ring, polys = gen(*args)
+    gb = _f4_with_oracle(ring, polys)
+    assert hashlib.sha256(format_system(ring, gb).encode()).hexdigest() == load_golden(name)["final_sha256"]
