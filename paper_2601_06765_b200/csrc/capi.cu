@@ -243,7 +243,7 @@ int f4b_ctx_create(int device, uint32_t p, int n_vars, int order, f4b_alloc_fn a
     for (int i = 0; i < 6; ++i) x = x * (2u - p * x);
     c->pprime = (uint32_t)(0u - x);
     c->r2 = (uint32_t)(((unsigned __int128)1 << 64) % p);
-    check_cuda(cudaMallocHost((void**)&c->h_stat, 64), "pinned");
+    check_cuda(cudaMallocHost((void**)&c->h_stat, 4096), "pinned");
     c->basis.h_off.push_back(0);
   } catch (const Error& e) {
     delete h;

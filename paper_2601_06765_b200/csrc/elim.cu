@@ -14,8 +14,9 @@
 //       normalized A row; Montgomery products in registers).  What remains
 //       lives on the non-A columns: the dense block D' (|C| x K).
 //   E3  D' forward elimination in one cooperative kernel (one grid barrier
-//       per column, pivot = lowest row index with a nonzero, pivot rows frozen
-//       once chosen), then a row-parallel back-substitution to RREF(D').
+//       per pivot: next pivot = min (leading column, row) over live rows;
+//       pivot rows frozen once chosen), then a row-parallel
+//       back-substitution to RREF(D').
 //       RREF(D') rows are the rows with NEW leading columns — the
 //       `nonpivot_rows` the F4 driver harvests (groebner.py:285-287).
 //   E4  (full RREF only) every A row is swept over the A columns right of its
@@ -44,6 +45,7 @@ struct f4b_echelon {
   // structure
   f4b::DBuf prow;      // u32 [N] pivot row of each column or NONE
   f4b::DBuf invl;      // u32 [N] inverse of the pivot row's lead coefficient
+  f4b::DBuf desc;      // uint4 [N] (tail start, tail end, inverse lead, pivot row)
   f4b::DBuf abits;     // u32 [(N+31)/32] A-column bitmap
   f4b::DBuf acols;     // u32 [nA] A columns ascending
   f4b::DBuf nonA;      // u32 [K] non-A columns ascending
@@ -79,14 +81,17 @@ __global__ void k_pivot_select(const u32* __restrict__ rp, const u32* __restrict
 
 __global__ void k_col_structure(Fp fp, const unsigned long long* __restrict__ pk, long long N, const u32* __restrict__ rp,
                                 const u32* __restrict__ val, u32* __restrict__ prow, u32* __restrict__ invl,
-                                uint8_t* __restrict__ isA, uint8_t* __restrict__ notA) {
+                                uint4* __restrict__ desc, uint8_t* __restrict__ isA, uint8_t* __restrict__ notA) {
   long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= N) return;
   unsigned long long k = pk[c];
   bool a = k != ~0ull;
   u32 row = a ? (u32)(k & 0xFFFFFFFFull) : NONE;
   prow[c] = row;
-  invl[c] = a ? fp.inv(val[rp[row]]) : 0u;
+  const u32 inv = a ? fp.inv(val[rp[row]]) : 0u;
+  invl[c] = inv;
+  // packed sweep descriptor: tail range of the pivot row + inverse lead
+  desc[c] = a ? make_uint4(rp[row] + 1, rp[row + 1], inv, row) : make_uint4(0, 0, 0, NONE);
   isA[c] = a ? 1 : 0;
   notA[c] = a ? 0 : 1;
 }
@@ -206,7 +211,7 @@ F4B_DEV void emit_row(const u32* acc, u32 lo, u32 hi, const u32* __restrict__ co
 template <int MODE>
 __global__ void __launch_bounds__(SW_THREADS) k_sweep(
     Fp fp, const u32* __restrict__ rp, const u32* __restrict__ col, const u32* __restrict__ val, u32 N,
-    const u32* __restrict__ rows, u32 nrows, const u32* __restrict__ prow, const u32* __restrict__ invl,
+    const u32* __restrict__ rows, u32 nrows, const uint4* __restrict__ desc, const u32* __restrict__ invl,
     const u32* __restrict__ abits_g, u32* __restrict__ gacc, u32* __restrict__ Dp, u32 K,
     const u32* __restrict__ nonA, const u32* __restrict__ Rd, u32 rankD, const u32* __restrict__ dpiv,
     u32* __restrict__ pcol, u32* __restrict__ pval, size_t cap, unsigned long long* cursor,
@@ -249,10 +254,9 @@ __global__ void __launch_bounds__(SW_THREADS) k_sweep(
       __syncthreads();
       const u32 c = sh[0];
       if (c >= N) break;
-      const u32 j = prow[c];
-      const u32 f = fp.mul(acc[c], invl[c]);
-      const u32 fm = fp.to_mont(fp.neg(f));
-      const u32 js = rp[j] + 1, je = rp[j + 1];
+      const uint4 d = __ldg(desc + c);
+      const u32 fm = fp.to_mont(fp.neg(fp.mul(acc[c], d.z)));
+      const u32 js = d.x, je = d.y;
       for (u32 k = js + tid; k < je; k += blockDim.x) {
         const u32 cc = col[k];
         acc[cc] = fp.add(acc[cc], fp.mont_mul(fm, __ldg(val + k)));
@@ -311,49 +315,73 @@ __global__ void __launch_bounds__(SW_THREADS) k_sweep(
 // ---------------------------------------------------------------------------
 // E3a: cooperative forward elimination of the dense block D' (R x K)
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_dense_forward(Fp fp, u32* Dp, u32 R, u32 K, int* cand, uint8_t* used,
-                                                       u32* piv_of_col) {
+// One grid barrier per PIVOT (not per column): every CTA keeps the leading
+// column of its live rows; the next pivot is the global minimum of
+// (lead << 32 | row), published with one 64-bit atomicMin per CTA.  Pivot
+// rows are frozen once chosen, so other CTAs read them without a second
+// barrier.  Grid barriers = rank(D') + 1.
+__device__ __forceinline__ u32 first_nonzero_warp(const u32* row, u32 from, u32 K) {
+  const int lane = threadIdx.x & 31;
+  for (u32 b0 = from & ~31u; b0 < K; b0 += 32) {
+    const u32 q = b0 + lane;
+    const bool nz = q >= from && q < K && row[q] != 0;
+    const unsigned m = __ballot_sync(0xffffffffu, nz);
+    if (m) return b0 + __ffs(m) - 1;
+  }
+  return K;
+}
+
+__global__ void __launch_bounds__(256) k_dense_forward(Fp fp, u32* Dp, u32 R, u32 K, unsigned long long* cand,
+                                                       u32* lead, uint8_t* used, u32* piv_of_col) {
   cg::grid_group grid = cg::this_grid();
-  __shared__ int bmin[8];
+  __shared__ unsigned long long bmin[8];
   __shared__ u32 s_inv;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nwarps = blockDim.x >> 5;
   const u32 G = gridDim.x;
   const u32 lo = (u32)(((unsigned long long)R * blockIdx.x) / G);
   const u32 hi = (u32)(((unsigned long long)R * (blockIdx.x + 1)) / G);
-  for (u32 c = 0; c < K; ++c) {
-    int m = INT_MAX;
+  for (u32 i = lo + warp; i < hi; i += nwarps) {
+    const u32 l = first_nonzero_warp(Dp + (size_t)i * K, 0, K);
+    if (lane == 0) lead[i] = l;
+  }
+  __syncthreads();
+  for (u32 step = 0;; ++step) {
+    unsigned long long m = ~0ull;
     for (u32 i = lo + tid; i < hi; i += blockDim.x)
-      if (!used[i] && Dp[(size_t)i * K + c] != 0) m = min(m, (int)i);
+      if (!used[i] && lead[i] < K) m = min(m, ((unsigned long long)lead[i] << 32) | i);
 #pragma unroll
     for (int o = 16; o; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
     if (lane == 0) bmin[warp] = m;
     __syncthreads();
     if (tid == 0) {
-      int mm = INT_MAX;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) mm = min(mm, bmin[w]);
-      if (mm != INT_MAX) atomicMin(cand + c, mm);
+      unsigned long long mm = ~0ull;
+      for (int w = 0; w < nwarps; ++w) mm = min(mm, bmin[w]);
+      if (mm != ~0ull) atomicMin(cand + step, mm);
     }
     grid.sync();
-    const int pr = __ldcg(cand + c);
-    if (pr == INT_MAX) continue;
+    const unsigned long long win = __ldcg(cand + step);
+    if (win == ~0ull) break;
+    const u32 c = (u32)(win >> 32), pr = (u32)(win & 0xFFFFFFFFull);
     const u32* prow_p = Dp + (size_t)pr * K;
     if (tid == 0) {
       s_inv = fp.inv(__ldcg(prow_p + c));
-      if ((u32)pr >= lo && (u32)pr < hi) {
+      if (pr >= lo && pr < hi) {
         used[pr] = 1;
-        piv_of_col[c] = (u32)pr;
+        piv_of_col[c] = pr;
       }
     }
     __syncthreads();
     const u32 inv = s_inv;
-    // warp per own row, lanes over columns c..K-1
-    for (u32 i = lo + warp; i < hi; i += (blockDim.x >> 5)) {
-      if (used[i]) continue;
+    // rows leading at c: eliminate, then find their new lead
+    for (u32 i = lo + warp; i < hi; i += nwarps) {
+      if (used[i] || lead[i] != c) continue;
       u32* row = Dp + (size_t)i * K;
-      const u32 f = row[c];
-      if (!f) continue;
-      const u32 fm = fp.to_mont(fp.neg(fp.mul(f, inv)));
+      const u32 fm = fp.to_mont(fp.neg(fp.mul(row[c], inv)));
       for (u32 q = c + lane; q < K; q += 32) row[q] = fp.add(row[q], fp.mont_mul(fm, __ldcg(prow_p + q)));
+      __syncwarp();
+      const u32 l = first_nonzero_warp(row, c + 1, K);
+      if (lane == 0) lead[i] = l;
     }
     __syncthreads();
   }
@@ -491,13 +519,14 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
   }
   ensure(c, E->prow, Nn * sizeof(u32));
   ensure(c, E->invl, Nn * sizeof(u32));
+  ensure(c, E->desc, Nn * sizeof(uint4));
   ensure(c, E->abits, (size_t)((Nn + 31) / 32 + 1) * sizeof(u32));
   ensure(c, c->flags, (size_t)2 * Nn + 32);
   uint8_t* isA = c->flags.as<uint8_t>();
   uint8_t* notA = isA + Nn + 16;
   if (N) {
     F4B_LAUNCH(c, k_col_structure, nb(N, 256), 256, 0, fp, pk.as<unsigned long long>(), N, E->rp, E->val,
-                                                        E->prow.as<u32>(), E->invl.as<u32>(), isA, notA);
+                                                        E->prow.as<u32>(), E->invl.as<u32>(), E->desc.as<uint4>(), isA, notA);
     check_cuda(cudaGetLastError(), "k_col_structure");
     F4B_LAUNCH(c, k_bits, nb((N + 31) / 32, 256), 256, 0, isA, N, E->abits.as<u32>());
     check_cuda(cudaGetLastError(), "k_bits");
@@ -534,7 +563,7 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
   }
   // E2: D' = C swept over the A columns
   const long long R = E->nC, K = E->K;
-  DBuf Dp, gacc, cand, used, pofc;
+  DBuf Dp, gacc, cand, used, pofc, lead;
   E->rankD = 0;
   if (R > 0 && K > 0) {
     ensure(c, Dp, (size_t)R * K * sizeof(u32));
@@ -548,28 +577,29 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
       attr0 = true;
     }
     F4B_LAUNCH(c, k_sweep<0>, grid, SW_THREADS, smem, 
-        fp, E->rp, E->col, E->val, (u32)N, crows.as<u32>(), (u32)R, E->prow.as<u32>(), E->invl.as<u32>(),
+        fp, E->rp, E->col, E->val, (u32)N, crows.as<u32>(), (u32)R, E->desc.as<uint4>(), E->invl.as<u32>(),
         E->abits.as<u32>(), gl ? gacc.as<u32>() : nullptr, Dp.as<u32>(), (u32)K, E->nonA.as<u32>(), nullptr, 0, nullptr,
         nullptr, nullptr, 0, nullptr, nullptr, nullptr, err);
     check_cuda(cudaGetLastError(), "k_sweep<0>");
     release(c, gacc);
     // E3a: cooperative forward elimination
-    ensure(c, cand, (size_t)K * sizeof(int));
     ensure(c, used, (size_t)R + 16);
     ensure(c, pofc, (size_t)K * sizeof(u32));
-    F4B_LAUNCH(c, k_fill_u32, nb(K, 256), 256, 0, cand.as<u32>(), K, (u32)INT_MAX);
+    ensure(c, cand, (size_t)(std::min(R, K) + 2) * sizeof(unsigned long long));
+    ensure(c, lead, (size_t)R * sizeof(u32));
+    check_cuda(cudaMemsetAsync(cand.p, 0xFF, (std::min(R, K) + 2) * sizeof(unsigned long long), c->stream), "memset");
     check_cuda(cudaMemsetAsync(used.p, 0, R, c->stream), "memset");
     F4B_LAUNCH(c, k_fill_u32, nb(K, 256), 256, 0, pofc.as<u32>(), K, NONE);
-    check_cuda(cudaGetLastError(), "k_fill_u32");
     int bps = 0;
     check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_dense_forward, 256, 0), "occupancy");
     int G = (int)std::min<long long>((long long)c->num_sms * std::max(1, std::min(bps, 2)), std::max<long long>(R, 1));
     u32* dpp = Dp.as<u32>();
     u32 Ru = (u32)R, Ku = (u32)K;
-    int* candp = cand.as<int>();
+    unsigned long long* candp = cand.as<unsigned long long>();
+    u32* leadp = lead.as<u32>();
     uint8_t* usedp = used.as<uint8_t>();
     u32* pofcp = pofc.as<u32>();
-    void* args[] = {&fp, &dpp, &Ru, &Ku, &candp, &usedp, &pofcp};
+    void* args[] = {&fp, &dpp, &Ru, &Ku, &candp, &leadp, &usedp, &pofcp};
     {
       ProfScope ps(c, "k_dense_forward");
       check_cuda(cudaLaunchCooperativeKernel((void*)k_dense_forward, G, 256, args, 0, c->stream), "k_dense_forward");
@@ -617,6 +647,7 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
   release(c, cand);
   release(c, used);
   release(c, pofc);
+  release(c, lead);
   release(c, crows);
   // E3c: emit the nonpivot rows (RREF(D'))
   const long long rankD = E->rankD;
@@ -703,7 +734,7 @@ static void run_a_sweep(Ctx* c, f4b_echelon* E) {
       check_cuda(cudaMemcpyAsync(E->cursor.p, &cur, 8, cudaMemcpyHostToDevice, c->stream), "h2d");
       check_cuda(cudaMemsetAsync(err, 0, 4, c->stream), "memset");
       F4B_LAUNCH(c, k_sweep<1>, grid, SW_THREADS, smem, 
-          fp, E->rp, E->col, E->val, (u32)N, arows.as<u32>(), (u32)nA, E->prow.as<u32>(), E->invl.as<u32>(),
+          fp, E->rp, E->col, E->val, (u32)N, arows.as<u32>(), (u32)nA, E->desc.as<uint4>(), E->invl.as<u32>(),
           E->abits.as<u32>(), gl ? gacc.as<u32>() : nullptr, nullptr, (u32)K, E->nonA.as<u32>(),
           E->rankD ? E->Rd.as<u32>() : nullptr, (u32)E->rankD, E->rankD ? E->dpiv.as<u32>() : nullptr,
           E->pool_col.as<u32>(), E->pool_val.as<u32>(), E->pool_cap, E->cursor.as<unsigned long long>(),
@@ -870,7 +901,7 @@ void echelon_pivot_cols(const f4b_echelon* E, int64_t* cols) {
 void echelon_release(f4b_echelon* E) {
   if (!E) return;
   Ctx* c = E->ctx;
-  DBuf* bufs[] = {&E->own_rp, &E->own_col, &E->own_val, &E->prow,  &E->invl,     &E->abits,    &E->acols,
+  DBuf* bufs[] = {&E->own_rp, &E->own_col, &E->own_val, &E->prow,  &E->invl, &E->desc, &E->abits, &E->acols,
                   &E->nonA,   &E->Rd,      &E->dpiv,    &E->pool_col, &E->pool_val, &E->a_off, &E->a_len,
                   &E->d_off,  &E->d_len,   &E->cursor};
   for (DBuf* b : bufs) release(c, *b);

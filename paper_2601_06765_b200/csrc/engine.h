@@ -114,11 +114,12 @@ void exclusive_scan_u32(Ctx* c, const uint32_t* in, uint32_t* out, long long n);
 // exclusive scan where in[i] = (flags[i] != 0)
 void exclusive_scan_flags(Ctx* c, const uint8_t* flags, uint32_t* out, long long n);
 
-// radix.cu: sort n keys (KW words each) ascending, only the low `bits` bits
-// vary.  Result lands in *result (one of the two ping-pong buffers).
-void radix_sort_keys(Ctx* c, int KW, const uint64_t* in, long long n, int bits, uint64_t** result);
-// unique over a sorted key array -> out (compacted); returns count (host sync).
-long long unique_keys(Ctx* c, int KW, const uint64_t* sorted, long long n, uint64_t* out);
+// radix.cu: ascending unique keys of in[0, n) (n = *d_n if d_n, else n_max),
+// dropping keys present in the ascending dictionary `dict` (size *d_ndict)
+// when dict != nullptr; result compacted into out, count into *d_count.
+// Only the low `bits` bits of the keys vary.  No host synchronisation.
+void sort_unique(Ctx* c, int KW, const uint64_t* in, const uint32_t* d_n, uint32_t n_max, int bits,
+                 const uint64_t* dict, const uint32_t* d_ndict, uint64_t* out, uint32_t* d_count);
 
 uint32_t read_u32(Ctx* c, const uint32_t* dptr);  // synchronous small D2H
 void memset_async(Ctx* c, void* p, int v, size_t bytes);

@@ -1,34 +1,62 @@
 // FBSP symbolic preprocessing on the device — the ★★ path of the north star.
 //
 // Restates reference `compile_batch` (pkg/src/fpgb/symbolic.py:293-388) with
-// its helpers `_materialize` (:204-225), `closure_expand` (:238-278),
+// `_materialize` (:204-225), `closure_expand` (:238-278),
 // `_reducer_preference` (:228-235), `_merge_dict` (:281-290) and the
-// dictionary join (bulk.py:207-241), producing a byte-identical LayoutPlan:
+// dictionary join (bulk.py:207-241), producing a byte-identical LayoutPlan.
 //
-//   round 0 : rows -> per-row delta key + length (count), offsets (scan),
-//             shifted keys + coefficients (fill, warp per row)
-//             -> radix sort -> unique = dictionary
-//   closure : mark leads done; frontier = dictionary entries not done;
-//             per frontier monomial the first basis LM dividing it, in
-//             (key(LM), index) order (warp ballot over 32 candidates at a
-//             time, SWAR u16x2 compares); compact in ascending key order ->
-//             new rows -> fill -> sort -> unique -> keys absent from the
-//             dictionary become the next frontier; merge by co-rank.
-//   join    : col_ind = N-1-lower_bound(dict, key) with the dictionary staged
-//             in shared memory; any miss -> MissingKeyError.
-//
-// Device keys use the compact order-isomorphic format (common.cuh, KeyFmt),
-// so the sort touches only lane_bits * n_lanes bits.
+// Per round (round 0 = the input rows, round k = closure rows of round k):
+//   K1 k_tile_dict      fill (shifted keys generated on the fly from the
+//                       HBM-resident basis: key = basis_key + row delta) +
+//                       shared-memory radix sort + unique of a tile of keys,
+//                       runs compacted with decoupled look-back.  The M keys
+//                       never round-trip through HBM.
+//   K2 sort_unique      one-sweep radix sort + unique of the tile survivors
+//                       (radix.cu); for closure rounds it also drops keys
+//                       already in the dictionary -> the next frontier.
+//   K3 k_merge_corank   dictionary ∪ new keys (disjoint, both ascending).
+//   K4 k_closure_search first basis LM dividing each frontier monomial in
+//                       (key(LM), index) order (warp ballot, SWAR u16x2).
+//   K5 k_new_rows       compaction of the reducers found, in ascending key(m)
+//                       order, with row offsets (two look-backs).
+// Final: k_join_gen regenerates every key and binary-searches the
+//        shared-memory dictionary -> col_ind = N-1-pos and val.
+// Host round trips: one small counter read per closure round (grids of the
+// round are sized by upper bounds; kernels read the true sizes on device).
 #include <algorithm>
 #include <cstring>
+#include <cstdlib>
 #include <vector>
 
+#include "block.cuh"
 #include "common.cuh"
 #include "engine.h"
 
 namespace f4b {
 
 static constexpr int MAXV = 32;
+static constexpr int K1_THREADS = 512;
+
+template <int KW>
+struct K1Cfg {
+  static constexpr int ITEMS = KW >= 4 ? 4 / (KW / 4) : (KW == 2 ? 8 : 16);
+  static constexpr int TILE = K1_THREADS * ITEMS;
+  static constexpr int SROWS = 1024;  // rows of a tile staged in shared memory
+  static constexpr size_t SMEM = (size_t)2 * TILE * KW * 8 + 16 * 256 * 4 + (size_t)SROWS * (KW * 8 + 8) + 16;
+};
+
+// device-side counters of one compile_batch call
+struct DevCounters {
+  u32 U;     // tile survivors of the current round
+  u32 N;     // dictionary size after round 0
+  u32 nf;    // frontier size
+  u32 R;     // new rows of the round
+  u32 Mk;    // terms of the new rows
+  u32 ndict; // dictionary size uploaded for the absent filter
+  u32 err;
+  u32 pad;
+  u32 tickets[16];
+};
 
 template <int KW>
 __global__ void k_encode_basis(KeyFmt f, const u16* __restrict__ exps, long long t0, long long t1,
@@ -54,54 +82,186 @@ __global__ void k_rows0(KeyFmt f, long long r, const int* __restrict__ rb, const
   rlen[i] = blen[rb[i]];
 }
 
-// Pass 2 (fill): one warp per row, lanes stride over the row's terms.
+// row owning term t among rows [lo, hi): rstart[row] <= t < rstart[row+1]
+F4B_DEV u32 row_of_term(const u32* __restrict__ rstart, u32 lo, u32 hi, u32 t) {
+  while (lo + 1 < hi) {
+    const u32 mid = (lo + hi) >> 1;
+    if (rstart[mid] <= t) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// Keys (and optionally coefficients) of terms [t, t + cnt), walking rows forward.
 template <int KW>
-__global__ void k_fill(long long row_lo, long long row_hi, const int* __restrict__ rb,
-                       const u64* __restrict__ delta, const u32* __restrict__ rstart,
-                       const u32* __restrict__ boff, const u64* __restrict__ bckey,
-                       const u32* __restrict__ bcoeff, u64* __restrict__ keys, u32* __restrict__ vals) {
-  long long row = row_lo + ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 32;
-  const int lane = threadIdx.x & 31;
-  if (row >= row_hi) return;
-  const int g = rb[row];
-  const Key<KW> d = key_load<KW>(delta, row);
-  const u32 s = rstart[row], len = rstart[row + 1] - s, bo = boff[g];
-  for (u32 j = lane; j < len; j += 32) {
-    key_store<KW>(keys, (long long)s + j, key_add<KW>(key_load<KW>(bckey, (long long)bo + j), d));
-    vals[s + j] = __ldg(bcoeff + bo + j);
+F4B_DEV void gen_keys(u32 t, int cnt, u32 r_lo, u32 r_hi, const int* __restrict__ rb,
+                      const u64* __restrict__ delta, const u32* __restrict__ rstart, const u32* __restrict__ boff,
+                      const u64* __restrict__ bckey, Key<KW>* dst, const u32* __restrict__ bcoeff, u32* vals) {
+  u32 row = row_of_term(rstart, r_lo, r_hi, t);
+  u32 rs = rstart[row], re = rstart[row + 1];
+  int g = rb[row];
+  Key<KW> d = key_load<KW>(delta, row);
+  u32 bo = boff[g];
+  for (int i = 0; i < cnt; ++i, ++t) {
+    while (t >= re) {
+      ++row;
+      rs = re;
+      re = rstart[row + 1];
+      g = rb[row];
+      d = key_load<KW>(delta, row);
+      bo = boff[g];
+    }
+    dst[i] = key_add<KW>(key_load<KW>(bckey, (long long)bo + (t - rs)), d);
+    if (vals) vals[i] = __ldg(bcoeff + bo + (t - rs));
   }
 }
 
+// K1: fill + tile sort + unique + look-back compaction.
+// m_hi / r_hi may come from device counters (closure rounds: d_Mk / d_R set
+// by k_new_rows), so the grid can be an upper bound; surplus tiles exit.
 template <int KW>
-__global__ void k_mark_leads(long long r, const u32* __restrict__ rstart, const u64* __restrict__ keys,
-                             const u64* __restrict__ dict, u32 N, uint8_t* __restrict__ done) {
+__global__ void __launch_bounds__(K1_THREADS) k_tile_dict(u32 m_lo, u32 m_hi_host, const u32* __restrict__ d_mk,
+                                                          u32 r_lo, u32 r_hi_host, const u32* __restrict__ d_r,
+                                                          const int* __restrict__ rb, const u64* __restrict__ delta,
+                                                          const u32* __restrict__ rstart,
+                                                          const u32* __restrict__ boff, const u64* __restrict__ bckey,
+                                                          int bits, u64* __restrict__ out, u32* status,
+                                                          u32* ticket, u32* d_U) {
+  constexpr int ITEMS = K1Cfg<KW>::ITEMS;
+  constexpr int TILE = K1Cfg<KW>::TILE;
+  constexpr int SROWS = K1Cfg<KW>::SROWS;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  Key<KW>* a = reinterpret_cast<Key<KW>*>(smraw);
+  Key<KW>* b = a + TILE;
+  Key<KW>* sdel = b + TILE;
+  u32* wh = reinterpret_cast<u32*>(sdel + SROWS);
+  u32* srs = wh + 16 * 256;      // row starts of the staged rows (+1)
+  u32* sbo = srs + SROWS + 1;    // basis offsets of the staged rows
+  __shared__ u32 ws[33];
+  __shared__ u32 s_tile, s_base, s_rf, s_nr;
+  const u32 m_hi = d_mk ? m_lo + *d_mk : m_hi_host;
+  const u32 r_hi = d_r ? r_lo + *d_r : r_hi_host;
+  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const u32 tile = s_tile;
+  const u32 ntiles = (m_hi - m_lo + TILE - 1) / TILE;
+  if (tile >= ntiles) {
+    if (tile == 0 && threadIdx.x == 0) *d_U = 0;
+    return;
+  }
+  const u32 t0 = m_lo + tile * TILE;
+  const int n = (int)min((u32)TILE, m_hi - t0);
+  if (threadIdx.x == 0) {
+    const u32 rf = row_of_term(rstart, r_lo, r_hi, t0);
+    const u32 rl = row_of_term(rstart, rf, r_hi, t0 + n - 1);
+    s_rf = rf;
+    s_nr = rl - rf + 1;
+  }
+  __syncthreads();
+  const u32 rf = s_rf, nr = s_nr;
+  if (nr <= (u32)SROWS) {
+    // stage the tile's rows, then generate warp-striped (coalesced basis reads)
+    for (u32 i = threadIdx.x; i <= nr; i += blockDim.x) srs[i] = rstart[rf + i];
+    for (u32 i = threadIdx.x; i < nr; i += blockDim.x) {
+      sbo[i] = boff[rb[rf + i]];
+      sdel[i] = key_load<KW>(delta, rf + i);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const u32 t = t0 + i;
+      u32 lo = 0, hi = nr;
+      while (lo + 1 < hi) {
+        const u32 mid = (lo + hi) >> 1;
+        if (srs[mid] <= t) lo = mid; else hi = mid;
+      }
+      a[i] = key_add<KW>(key_load<KW>(bckey, (long long)sbo[lo] + (t - srs[lo])), sdel[lo]);
+    }
+  } else {
+    const int my0 = threadIdx.x * ITEMS;
+    const int cnt = max(0, min(ITEMS, n - my0));
+    if (cnt > 0) {
+      Key<KW> tmp[ITEMS];
+      gen_keys<KW>(t0 + my0, cnt, r_lo, r_hi, rb, delta, rstart, boff, bckey, tmp, nullptr, nullptr);
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i)
+        if (i < cnt) a[my0 + i] = tmp[i];
+    }
+  }
+  __syncthreads();
+  block_sort_keys<KW, ITEMS>(a, b, n, bits, wh, ws);
+  u32 o = 0;
+  for (int c0 = 0; c0 < n; c0 += blockDim.x) {
+    const int i = c0 + threadIdx.x;
+    const bool fl = i < n && (i == 0 || !key_eq<KW>(a[i], a[i - 1]));
+    u32 tot;
+    const u32 pre = block_scan_excl(fl ? 1u : 0u, ws, &tot);
+    if (fl) b[o + pre] = a[i];
+    o += tot;
+  }
+  if (threadIdx.x == 0) s_base = lookback_prefix(status, tile, o);
+  __syncthreads();
+  const u32 base = s_base;
+  for (u32 i = threadIdx.x; i < o; i += blockDim.x) key_store<KW>(out, (long long)base + i, b[i]);
+  if (threadIdx.x == 0 && tile == ntiles - 1) *d_U = base + o;
+}
+
+template <int KW>
+__global__ void k_mark_leads(long long r, const int* __restrict__ rb, const u64* __restrict__ delta,
+                             const u32* __restrict__ boff, const u64* __restrict__ bckey, const u64* __restrict__ dict,
+                             const u32* __restrict__ d_N, uint8_t* __restrict__ done) {
   long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= r) return;
-  Key<KW> k = key_load<KW>(keys, rstart[i]);
-  u32 pos = key_lower_bound<KW>(dict, N, k);
+  const u32 N = *d_N;
+  const Key<KW> k = key_add<KW>(key_load<KW>(bckey, boff[rb[i]]), key_load<KW>(delta, i));
+  const u32 pos = key_lower_bound<KW>(dict, N, k);
   if (pos < N && key_eq<KW>(key_load<KW>(dict, pos), k)) done[pos] = 1;
 }
 
-__global__ void k_not_flags(const uint8_t* __restrict__ done, long long n, uint8_t* __restrict__ flags) {
-  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) flags[i] = done[i] ? 0 : 1;
+// frontier of round 1: dictionary entries not covered by a lead (look-back compaction)
+template <int KW>
+__global__ void __launch_bounds__(256) k_front0(const u64* __restrict__ dict, const uint8_t* __restrict__ done,
+                                                const u32* __restrict__ d_N, u64* __restrict__ front, u32* status,
+                                                u32* ticket, u32* d_nf) {
+  constexpr int ITEMS = 8;
+  __shared__ u32 ws[33];
+  __shared__ u32 s_tile, s_base;
+  const u32 N = *d_N;
+  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const u32 tile = s_tile;
+  const u32 ntiles = (N + 256 * ITEMS - 1) / (256 * ITEMS);
+  if (tile >= ntiles) {
+    if (tile == 0 && threadIdx.x == 0) *d_nf = 0;
+    return;
+  }
+  const u32 base = tile * 256 * ITEMS + threadIdx.x * ITEMS;
+  u32 keep = 0;
+  for (int i = 0; i < ITEMS; ++i) keep += (base + i < N && !done[base + i]) ? 1u : 0u;
+  u32 tot;
+  const u32 pre = block_scan_excl(keep, ws, &tot);
+  if (threadIdx.x == 0) s_base = lookback_prefix(status, tile, tot);
+  __syncthreads();
+  u32 o = s_base + pre;
+  for (int i = 0; i < ITEMS; ++i)
+    if (base + i < N && !done[base + i]) key_store<KW>(front, o++, key_load<KW>(dict, base + i));
+  if (tile == ntiles - 1 && threadIdx.x == 0) *d_nf = s_base + tot;
 }
 
+// K4: first divisor in preference order, warp per frontier monomial.
 template <int KW>
-__global__ void k_compact(const u64* __restrict__ in, long long n, const uint8_t* __restrict__ flags,
-                          const u32* __restrict__ pos, u64* __restrict__ out) {
-  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n && flags[i]) key_store<KW>(out, pos[i], key_load<KW>(in, i));
-}
-
-// First divisor in preference order: warp per frontier monomial.
-template <int KW>
-__global__ void k_closure_search(KeyFmt f, const u64* __restrict__ front, long long nf,
-                                 const u32* __restrict__ lmw, const int* __restrict__ cidx, int nc, int nw,
+__global__ void k_closure_search(KeyFmt f, const u64* __restrict__ front, const u32* __restrict__ d_nf,
+                                 const u32* lmw, const int* __restrict__ cidx, int nc, int nw,
                                  int* __restrict__ red) {
-  long long j = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  // candidate LM table staged in shared memory when it fits (<= 48 KB)
+  extern __shared__ __align__(16) u32 slm[];
+  const bool staged = (long long)nc * nw * 4 <= 48 * 1024;
+  if (staged) {
+    for (int i = threadIdx.x; i < nc * nw; i += blockDim.x) slm[i] = __ldg(lmw + i);
+    __syncthreads();
+    lmw = slm;
+  }
+  const long long j = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 32;
   const int lane = threadIdx.x & 31;
-  if (j >= nf) return;
+  if (j >= *d_nf) return;
   u16 e[MAXV + 1];
   key_decode<KW>(f, key_load<KW>(front, j), e);
   e[f.n_vars] = 0;
@@ -113,104 +273,133 @@ __global__ void k_closure_search(KeyFmt f, const u64* __restrict__ front, long l
     bool ok = c < nc;
     if (ok) {
       const u32* lm = lmw + (long long)c * nw;
-      for (int w = 0; w < nw; ++w) ok &= (__vcmpgeu2(me[w], __ldg(lm + w)) == 0xFFFFFFFFu);
+      for (int w = 0; w < nw; ++w) ok &= (__vcmpgeu2(me[w], lm[w]) == 0xFFFFFFFFu);
     }
-    unsigned b = __ballot_sync(0xffffffffu, ok);
-    if (b) {
-      found = cidx[base + __ffs(b) - 1];
+    const unsigned bm = __ballot_sync(0xffffffffu, ok);
+    if (bm) {
+      found = cidx[base + __ffs(bm) - 1];
       break;
     }
   }
   if (lane == 0) red[j] = found;
 }
 
-__global__ void k_red_flags(const int* __restrict__ red, long long n, uint8_t* __restrict__ flags) {
-  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) flags[i] = red[i] >= 0 ? 1 : 0;
-}
-
+// K5: compaction of the rows found (ascending key(m)) + row offsets.
 template <int KW>
-__global__ void k_new_rows(KeyFmt f, const u64* __restrict__ front, long long nf, const int* __restrict__ red,
-                           const u32* __restrict__ pos, long long row_base, long long cl_base,
-                           const u32* __restrict__ boff, const u32* __restrict__ blen,
-                           const u64* __restrict__ bckey, const u16* __restrict__ lmexp,
-                           const u16* __restrict__ maxe, int round, int* __restrict__ rows_basis,
-                           u64* __restrict__ rows_delta, u32* __restrict__ rows_len, int* __restrict__ cl_basis,
-                           u16* __restrict__ cl_shift, int* __restrict__ cl_round, u32* __restrict__ err) {
-  long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= nf) return;
-  const int g = red[j];
-  if (g < 0) return;
-  const long long q = pos[j];
-  const long long row = row_base + q;
-  const Key<KW> m = key_load<KW>(front, j);
-  const Key<KW> lmk = key_load<KW>(bckey, boff[g]);
-  rows_basis[row] = g;
-  key_store<KW>(rows_delta, row, key_sub<KW>(m, lmk));
-  rows_len[row] = blen[g];
-  u16 e[MAXV];
-  key_decode<KW>(f, m, e);
-  bool over = false;
-  for (int v = 0; v < f.n_vars; ++v) {
-    u32 s = (u32)e[v] - (u32)lmexp[(long long)g * f.n_vars + v];
-    over |= (s + (u32)maxe[(long long)g * f.n_vars + v]) > 0xFFFFu;
-    cl_shift[(cl_base + q) * f.n_vars + v] = (u16)s;
+__global__ void __launch_bounds__(256) k_new_rows(KeyFmt f, const u64* __restrict__ front, const int* __restrict__ red,
+                                                  const u32* __restrict__ d_nf, long long row_base, long long cl_base,
+                                                  u32 M_base, const u32* __restrict__ boff,
+                                                  const u32* __restrict__ blen, const u64* __restrict__ bckey,
+                                                  const u16* __restrict__ lmexp, const u16* __restrict__ maxe,
+                                                  int round, int* __restrict__ rows_basis,
+                                                  u64* __restrict__ rows_delta, u32* __restrict__ rows_start,
+                                                  int* __restrict__ cl_basis, u16* __restrict__ cl_shift,
+                                                  int* __restrict__ cl_round, u32* status_n, u32* status_len,
+                                                  u32* ticket, u32* d_R, u32* d_Mk, u32* err) {
+  __shared__ u32 ws[33];
+  __shared__ u32 s_tile, s_base, s_lbase;
+  const u32 nf = *d_nf;
+  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const u32 tile = s_tile;
+  const u32 ntiles = (nf + 255) / 256;
+  if (tile >= ntiles) {
+    if (tile == 0 && threadIdx.x == 0) {
+      *d_R = 0;
+      *d_Mk = 0;
+    }
+    return;
   }
-  if (over) atomicOr(err, (u32)DEVERR_LANE_OVERFLOW);
-  cl_basis[cl_base + q] = g;
-  cl_round[cl_base + q] = round;
+  const u32 j = tile * 256 + threadIdx.x;
+  const int g = j < nf ? red[j] : -1;
+  const u32 len = g >= 0 ? blen[g] : 0u;
+  u32 tot, ltot;
+  const u32 pre = block_scan_excl(g >= 0 ? 1u : 0u, ws, &tot);
+  const u32 lpre = block_scan_excl(len, ws, &ltot);
+  if (threadIdx.x == 0) {
+    s_base = lookback_prefix(status_n, tile, tot);
+    s_lbase = lookback_prefix(status_len, tile, ltot);
+  }
+  __syncthreads();
+  if (g >= 0) {
+    const long long q = (long long)s_base + pre;
+    const long long row = row_base + q;
+    const Key<KW> m = key_load<KW>(front, j);
+    rows_basis[row] = g;
+    key_store<KW>(rows_delta, row, key_sub<KW>(m, key_load<KW>(bckey, boff[g])));
+    rows_start[row] = M_base + s_lbase + lpre;
+    u16 e[MAXV];
+    key_decode<KW>(f, m, e);
+    bool over = false;
+    for (int v = 0; v < f.n_vars; ++v) {
+      const u32 s = (u32)e[v] - (u32)lmexp[(long long)g * f.n_vars + v];
+      over |= (s + (u32)maxe[(long long)g * f.n_vars + v]) > 0xFFFFu;
+      cl_shift[(cl_base + q) * f.n_vars + v] = (u16)s;
+    }
+    if (over) atomicOr(err, (u32)DEVERR_LANE_OVERFLOW);
+    cl_basis[cl_base + q] = g;
+    cl_round[cl_base + q] = round;
+  }
+  if (tile == ntiles - 1 && threadIdx.x == 0) {
+    *d_R = s_base + tot;
+    *d_Mk = s_lbase + ltot;
+    rows_start[row_base + s_base + tot] = M_base + s_lbase + ltot;
+  }
 }
 
-__global__ void k_offsets(const u32* __restrict__ scanned, long long n, u32 base, u32* __restrict__ out) {
-  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i <= n) out[i] = base + scanned[i];
-}
-
+// K3: merge two disjoint ascending sets by co-rank; nb read from the device.
 template <int KW>
-__global__ void k_absent_flags(const u64* __restrict__ uniq, long long nu, const u64* __restrict__ dict, u32 N,
-                               uint8_t* __restrict__ flags) {
-  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nu) return;
-  Key<KW> k = key_load<KW>(uniq, i);
-  u32 pos = key_lower_bound<KW>(dict, N, k);
-  flags[i] = (pos < N && key_eq<KW>(key_load<KW>(dict, pos), k)) ? 0 : 1;
-}
-
-// Merge two disjoint ascending sets by co-rank.
-template <int KW>
-__global__ void k_merge_corank(const u64* __restrict__ a, u32 na, const u64* __restrict__ b, u32 nb,
-                               u64* __restrict__ out) {
-  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void k_merge_corank(const u64* __restrict__ a, u32 na, const u64* __restrict__ b,
+                               const u32* __restrict__ d_nb, u64* __restrict__ out) {
+  const u32 nb = *d_nb;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < na) {
-    Key<KW> k = key_load<KW>(a, i);
+    const Key<KW> k = key_load<KW>(a, i);
     key_store<KW>(out, i + key_lower_bound<KW>(b, nb, k), k);
   } else if (i < (long long)na + nb) {
-    long long j = i - na;
-    Key<KW> k = key_load<KW>(b, j);
+    const long long j = i - na;
+    const Key<KW> k = key_load<KW>(b, j);
     key_store<KW>(out, j + key_lower_bound<KW>(a, na, k), k);
   }
 }
 
-// Dictionary join: col = N-1-lower_bound(dict, key); dictionary in smem.
+// Final join: regenerate every key, binary-search the (shared-memory) dictionary.
 template <int KW>
-__global__ void __launch_bounds__(512) k_join(const u64* __restrict__ keys, long long M, const u64* __restrict__ dict,
-                                              u32 N, int use_smem, u32* __restrict__ col, u32* __restrict__ err) {
-  extern __shared__ u64 sdict[];
+__global__ void __launch_bounds__(512) k_join_gen(u32 M, u32 r, const int* __restrict__ rb,
+                                                  const u64* __restrict__ delta, const u32* __restrict__ rstart,
+                                                  const u32* __restrict__ boff, const u64* __restrict__ bckey,
+                                                  const u32* __restrict__ bcoeff, const u64* __restrict__ dict,
+                                                  u32 N, int use_smem, u32* __restrict__ col, u32* __restrict__ val,
+                                                  u32* err) {
+  constexpr int ITEMS = 8;
+  extern __shared__ __align__(16) u64 sdict[];
   const u64* table = dict;
   if (use_smem) {
-    for (long long i = threadIdx.x; i < (long long)N * KW; i += blockDim.x) sdict[i] = __ldg(dict + i);
+    for (u32 i = threadIdx.x; i < N * KW; i += blockDim.x) sdict[i] = __ldg(dict + i);
     __syncthreads();
     table = sdict;
   }
-  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < M; t += (long long)gridDim.x * blockDim.x) {
-    Key<KW> k = key_load<KW>(keys, t);
-    u32 pos = key_lower_bound<KW>(table, N, k);
-    if (pos >= N || !key_eq<KW>(key_load_rw<KW>(table, pos), k)) {
-      atomicOr(err, (u32)DEVERR_MISSING_KEY);
-      pos = 0;
+  bool miss = false;
+  for (long long t0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * ITEMS; t0 < M;
+       t0 += (long long)gridDim.x * blockDim.x * ITEMS) {
+    const int cnt = (int)min((long long)ITEMS, M - t0);
+    Key<KW> k[ITEMS];
+    u32 v[ITEMS];
+    gen_keys<KW>((u32)t0, cnt, 0, r, rb, delta, rstart, boff, bckey, k, bcoeff, v);
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      if (i < cnt) {
+        u32 pos = key_lower_bound<KW>(table, N, k[i]);
+        if (pos >= N || !key_eq<KW>(key_load_rw<KW>(table, pos), k[i])) {
+          miss = true;
+          pos = 0;
+        }
+        col[t0 + i] = N - 1 - pos;
+        val[t0 + i] = v[i];
+      }
     }
-    col[t] = N - 1 - pos;
   }
+  if (miss) atomicOr(err, (u32)DEVERR_MISSING_KEY);
 }
 
 template <int KW>
@@ -227,11 +416,6 @@ __global__ void k_dict_exps(KeyFmt f, const u64* __restrict__ dict, u32 N, u16* 
 // ---------------------------------------------------------------------------
 static inline unsigned nblk(long long n, int t) { return (unsigned)std::max<long long>(1, (n + t - 1) / t); }
 
-#define LAUNCH_CHECK(name) \
-  do {                     \
-  } while (0)
-
-// Term-order comparison of exponent vectors (reference monomials.py:107-128).
 static int mon_cmp(const uint16_t* u, const uint16_t* v, int n, int order) {
   if (order != 2) {
     long du = 0, dv = 0;
@@ -261,11 +445,25 @@ static void encode_basis(Ctx* c, const KeyFmt& f) {
   }
   if (B.ckey_terms == B.n_terms) return;
   ensure_keep(c, B.ckey, (size_t)(B.n_terms + 1) * KW * sizeof(u64));
-  long long t0 = B.ckey_terms, t1 = B.n_terms;
+  const long long t0 = B.ckey_terms, t1 = B.n_terms;
   F4B_LAUNCH(c, k_encode_basis<KW>, nblk(t1 - t0, 256), 256, 0, f, B.exps.as<u16>(), t0, t1, B.ckey.as<u64>());
-  LAUNCH_CHECK("k_encode_basis");
   B.ckey_terms = t1;
 }
+
+static void read_counters(Ctx* c, const DevCounters* dc, DevCounters* h) {
+  check_cuda(cudaMemcpyAsync(c->h_stat, dc, sizeof(DevCounters), cudaMemcpyDeviceToHost, c->stream), "d2h counters");
+  check_cuda(cudaStreamSynchronize(c->stream), "sync");
+  memcpy(h, c->h_stat, sizeof(DevCounters));
+}
+
+// Look-back scratch of one round: [tickets | status regions], zeroed per round.
+struct RoundScratch {
+  u32* tile_st;
+  u32* front_st;
+  u32* rows_n_st;
+  u32* rows_l_st;
+  size_t words;
+};
 
 template <int KW>
 static void compile_t(Ctx* c, const KeyFmt& f, long long r0, const int32_t* h_rb, const uint16_t* h_shift,
@@ -279,13 +477,8 @@ static void compile_t(Ctx* c, const KeyFmt& f, long long r0, const int32_t* h_rb
   check_cuda(cudaEventCreate(&ev1), "event");
   check_cuda(cudaEventCreate(&ev2), "event");
   check_cuda(cudaEventRecord(ev0, c->stream), "event record");
-
   encode_basis<KW>(c, f);
-  ensure(c, c->errflag, 64);
-  u32* err = c->errflag.as<u32>();
-  check_cuda(cudaMemsetAsync(err, 0, 4, c->stream), "memset err");
 
-  // ---- round 0: count (host knows the lengths) / scan / fill -------------
   std::vector<uint32_t> h_start(r0 + 1);
   long long M = 0;
   for (long long i = 0; i < r0; ++i) {
@@ -293,7 +486,34 @@ static void compile_t(Ctx* c, const KeyFmt& f, long long r0, const int32_t* h_rb
     M += B.h_len[h_rb[i]];
   }
   h_start[r0] = (uint32_t)M;
-  if (M >= (1ll << 31)) fail(F4B_ERR_SIZE_CAP, "batch has more than 2^31 terms");
+  if (M >= (1ll << 30)) fail(F4B_ERR_SIZE_CAP, "batch has more than 2^30 terms");
+  const u32 M0 = (u32)M;
+
+  // counters + per-round look-back scratch
+  DevCounters* dc = nullptr;
+  RoundScratch rs{};
+  auto reset_round = [&](u32 m_terms, u32 m_front) {
+    const size_t a = m_terms / K1Cfg<KW>::TILE + 4, b = m_front / 2048 + 4, cc = m_front / 256 + 4;
+    const size_t words = a + b + 2 * cc + 64;
+    const size_t bytes = sizeof(DevCounters) + words * 4;
+    if (bytes > c->errflag.cap) {
+      ensure_keep(c, c->errflag, bytes);
+    }
+    dc = reinterpret_cast<DevCounters*>(c->errflag.p);
+    u32* lb = reinterpret_cast<u32*>(dc + 1);
+    rs.tile_st = lb;
+    rs.front_st = lb + a;
+    rs.rows_n_st = rs.front_st + b;
+    rs.rows_l_st = rs.rows_n_st + cc;
+    rs.words = words;
+    check_cuda(cudaMemsetAsync(dc->tickets, 0, sizeof(dc->tickets), c->stream), "memset tickets");
+    check_cuda(cudaMemsetAsync(lb, 0, words * 4, c->stream), "memset lb");
+  };
+  ensure(c, c->errflag, sizeof(DevCounters) + 4096);
+  check_cuda(cudaMemsetAsync(c->errflag.p, 0, sizeof(DevCounters), c->stream), "memset counters");
+  reset_round(M0, M0);
+
+  // ---- round 0 ----------------------------------------------------------
   long long rcap = std::max<long long>(2 * r0 + 1024, 4096);
   ensure(c, c->rows_basis, rcap * sizeof(int));
   ensure(c, c->rows_delta, rcap * KW * sizeof(u64));
@@ -301,56 +521,53 @@ static void compile_t(Ctx* c, const KeyFmt& f, long long r0, const int32_t* h_rb
   ensure(c, c->rows_start, (rcap + 1) * sizeof(u32));
   ensure(c, c->shift_in, (size_t)std::max<long long>(r0, 1) * n * sizeof(u16));
   check_cuda(cudaMemcpyAsync(c->rows_basis.p, h_rb, r0 * sizeof(int), cudaMemcpyHostToDevice, c->stream), "h2d rows");
-  check_cuda(cudaMemcpyAsync(c->shift_in.p, h_shift, r0 * n * sizeof(u16), cudaMemcpyHostToDevice, c->stream), "h2d shifts");
-  check_cuda(cudaMemcpyAsync(c->rows_start.p, h_start.data(), (r0 + 1) * sizeof(u32), cudaMemcpyHostToDevice, c->stream),
-             "h2d starts");
+  check_cuda(cudaMemcpyAsync(c->shift_in.p, h_shift, r0 * n * sizeof(u16), cudaMemcpyHostToDevice, c->stream), "h2d");
+  check_cuda(cudaMemcpyAsync(c->rows_start.p, h_start.data(), (r0 + 1) * sizeof(u32), cudaMemcpyHostToDevice,
+                             c->stream), "h2d starts");
   F4B_LAUNCH(c, k_rows0<KW>, nblk(r0, 256), 256, 0, f, r0, c->rows_basis.as<int>(), c->shift_in.as<u16>(),
-                                                     B.len.as<u32>(), c->rows_delta.as<u64>(), c->rows_len.as<u32>());
-  LAUNCH_CHECK("k_rows0");
-  long long mcap = std::max<long long>(M + M / 2 + 4096, 1 << 16);
-  ensure(c, c->keys_all, mcap * KW * sizeof(u64));
-  ensure(c, c->vals_all, mcap * sizeof(u32));
-  F4B_LAUNCH(c, k_fill<KW>, nblk(r0 * 32, 256), 256, 0, 0, r0, c->rows_basis.as<int>(), c->rows_delta.as<u64>(),
-                                                         c->rows_start.as<u32>(), B.off.as<u32>(), B.ckey.as<u64>(),
-                                                         B.coeff.as<u32>(), c->keys_all.as<u64>(), c->vals_all.as<u32>());
-  LAUNCH_CHECK("k_fill");
-
-  // ---- dictionary: radix sort + unique ------------------------------------
-  u64* sorted = nullptr;
-  radix_sort_keys(c, KW, c->keys_all.as<u64>(), M, bits, &sorted);
+             B.len.as<u32>(), c->rows_delta.as<u64>(), c->rows_len.as<u32>());
+  static bool attr = false;
+  if (!attr) {
+    check_cuda(cudaFuncSetAttribute(k_tile_dict<KW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K1Cfg<KW>::SMEM),
+               "attr");
+    check_cuda(cudaFuncSetAttribute(k_join_gen<KW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 1024),
+               "attr");
+    attr = true;
+  }
+  // m_hi / r_hi either host-known (d_mk = d_r = nullptr) or device counters
+  // with `m_bound` bounding m_hi - m_lo (grid upper bound, surplus tiles exit)
+  auto tile_dict = [&](u32 m_lo, u32 m_hi, u32 m_bound, const u32* d_mk, u32 r_lo, u32 r_hi, const u32* d_r,
+                       u64* out) {
+    const u32 tiles = std::max<u32>(1, (m_bound + K1Cfg<KW>::TILE - 1) / K1Cfg<KW>::TILE);
+    F4B_LAUNCH(c, k_tile_dict<KW>, tiles, K1_THREADS, K1Cfg<KW>::SMEM, m_lo, m_hi, d_mk, r_lo, r_hi, d_r,
+               c->rows_basis.as<int>(), c->rows_delta.as<u64>(), c->rows_start.as<u32>(), B.off.as<u32>(),
+               B.ckey.as<u64>(), bits, out, rs.tile_st, &dc->tickets[0], &dc->U);
+  };
+  ensure(c, c->uniq, (size_t)(M0 + 1) * KW * sizeof(u64));
+  tile_dict(0, M0, M0, nullptr, 0, (u32)r0, nullptr, c->uniq.as<u64>());
   pl->sort_passes += (bits + 7) / 8;
-  ensure(c, c->dict_a, (size_t)(M + 1) * KW * sizeof(u64));
-  long long N = unique_keys(c, KW, sorted, M, c->dict_a.as<u64>());
+  ensure(c, c->dict_a, (size_t)(M0 + 1) * KW * sizeof(u64));
+  sort_unique(c, KW, c->uniq.as<u64>(), &dc->U, M0, bits, nullptr, nullptr, c->dict_a.as<u64>(), &dc->N);
   u64* dict = c->dict_a.as<u64>();
+  long long r = r0, rounds = 0, n_cl = 0;
+  DevCounters hc;
+  long long N = 0;
 
-  long long r = r0;
-  long long rounds = 0;
-  long long n_cl = 0;
-  if (closure && N > 0) {
-    // leads of the input rows are covered (symbolic.py:339)
-    ensure(c, c->flags, (size_t)N + 16);
-    ensure(c, c->front, (size_t)(N + 1) * KW * sizeof(u64));
-    ensure(c, c->tmp_u32b, (size_t)(N + 2) * sizeof(u32));
-    ensure(c, c->tmp_u32c, (size_t)N + 16);  // done flags (u8)
-    uint8_t* done = c->tmp_u32c.as<uint8_t>();
-    check_cuda(cudaMemsetAsync(done, 0, N, c->stream), "memset done");
-    F4B_LAUNCH(c, k_mark_leads<KW>, nblk(r0, 256), 256, 0, r0, c->rows_start.as<u32>(), c->keys_all.as<u64>(), dict,
-                                                            (u32)N, done);
-    LAUNCH_CHECK("k_mark_leads");
-    uint8_t* flags = c->flags.as<uint8_t>();
-    F4B_LAUNCH(c, k_not_flags, nblk(N, 256), 256, 0, done, N, flags);
-    LAUNCH_CHECK("k_not_flags");
-    u32* pos = c->tmp_u32b.as<u32>();
-    exclusive_scan_flags(c, flags, pos, N);
-    F4B_LAUNCH(c, k_compact<KW>, nblk(N, 256), 256, 0, dict, N, flags, pos, c->front.as<u64>());
-    LAUNCH_CHECK("k_compact");
-    long long nf = read_u32(c, pos + N);
-
+  if (closure && M0 > 0) {
+    // leads of the input rows are covered (symbolic.py:339); the rest is the frontier
+    ensure(c, c->flags, (size_t)M0 + 16);
+    ensure(c, c->front, (size_t)(M0 + 1) * KW * sizeof(u64));
+    uint8_t* done = c->flags.as<uint8_t>();
+    check_cuda(cudaMemsetAsync(done, 0, M0, c->stream), "memset done");
+    F4B_LAUNCH(c, k_mark_leads<KW>, nblk(r0, 256), 256, 0, r0, c->rows_basis.as<int>(), c->rows_delta.as<u64>(),
+               B.off.as<u32>(), B.ckey.as<u64>(), dict, &dc->N, done);
+    F4B_LAUNCH(c, k_front0<KW>, nblk(M0, 2048), 256, 0, dict, done, &dc->N, c->front.as<u64>(), rs.front_st,
+               &dc->tickets[1], &dc->nf);
     // candidate LMs in preference order (key(LM), index) (symbolic.py:228-235)
     std::vector<int32_t> pref(cand);
-    std::stable_sort(pref.begin(), pref.end(), [&](int32_t a, int32_t b) {
-      int s = mon_cmp(&B.h_lm[(size_t)a * n], &B.h_lm[(size_t)b * n], n, c->order);
-      return s != 0 ? s < 0 : a < b;
+    std::stable_sort(pref.begin(), pref.end(), [&](int32_t x, int32_t y) {
+      int s = mon_cmp(&B.h_lm[(size_t)x * n], &B.h_lm[(size_t)y * n], n, c->order);
+      return s != 0 ? s < 0 : x < y;
     });
     const int nc = (int)pref.size();
     const int nw = (n + 1) / 2;
@@ -360,111 +577,88 @@ static void compile_t(Ctx* c, const KeyFmt& f, long long r0, const int32_t* h_rb
         h_lmw[(size_t)q * nw + v / 2] |= (uint32_t)B.h_lm[(size_t)pref[q] * n + v] << (16 * (v & 1));
     ensure(c, c->lmpref, h_lmw.size() * sizeof(u32));
     ensure(c, c->cand_idx, (size_t)std::max(nc, 1) * sizeof(int));
-    check_cuda(cudaMemcpyAsync(c->lmpref.p, h_lmw.data(), h_lmw.size() * sizeof(u32), cudaMemcpyHostToDevice, c->stream),
-               "h2d lm");
+    check_cuda(cudaMemcpyAsync(c->lmpref.p, h_lmw.data(), h_lmw.size() * sizeof(u32), cudaMemcpyHostToDevice,
+                               c->stream), "h2d lm");
     if (nc)
       check_cuda(cudaMemcpyAsync(c->cand_idx.p, pref.data(), nc * sizeof(int), cudaMemcpyHostToDevice, c->stream),
                  "h2d cand");
-
-    long long clcap = 1024;
+    read_counters(c, dc, &hc);
+    N = hc.N;
+    long long nf = hc.nf;
+    long long clcap = std::max<long long>(N + 1024, 4096);
     ensure(c, c->cl_basis, clcap * sizeof(int));
     ensure(c, c->cl_shift, clcap * n * sizeof(u16));
     ensure(c, c->cl_round, clcap * sizeof(int));
+    u32 Mcur = M0;
+    long long maxlen = 1;
+    for (int32_t k : pref) maxlen = std::max<long long>(maxlen, B.h_len[k]);
 
+    // One host round trip per closure round: every kernel of the round reads
+    // the sizes it needs (nf, R, Mk, U) from device counters; grids are
+    // sized by upper bounds (new rows <= nf, terms <= nf * max length).
     while (nf > 0 && nc > 0) {
-      // closure search over the frontier
-      ensure(c, c->red, (size_t)nf * sizeof(int));
-      F4B_LAUNCH(c, k_closure_search<KW>, nblk(nf * 32, 256), 256, 0, f, c->front.as<u64>(), nf, c->lmpref.as<u32>(),
-                                                                        c->cand_idx.as<int>(), nc, nw, c->red.as<int>());
-      LAUNCH_CHECK("k_closure_search");
-      ensure(c, c->flags, (size_t)nf + 16);
-      ensure(c, c->tmp_u32b, (size_t)(nf + 2) * sizeof(u32));
-      flags = c->flags.as<uint8_t>();
-      pos = c->tmp_u32b.as<u32>();
-      F4B_LAUNCH(c, k_red_flags, nblk(nf, 256), 256, 0, c->red.as<int>(), nf, flags);
-      LAUNCH_CHECK("k_red_flags");
-      exclusive_scan_flags(c, flags, pos, nf);
-      long long R = read_u32(c, pos + nf);
-      if (R == 0) break;
-      ++rounds;
-      // grow row / closure arrays (contents preserved)
-      if (r + R + 1 > rcap) {
-        rcap = 2 * (r + R + 1);
+      const long long mk_bound = std::max<long long>(1, std::min<long long>(nf * maxlen, (1ll << 30) - Mcur));
+      if (r + nf + 2 > rcap) {
+        rcap = 2 * (r + nf + 2);
         ensure_keep(c, c->rows_basis, rcap * sizeof(int));
         ensure_keep(c, c->rows_delta, rcap * KW * sizeof(u64));
         ensure_keep(c, c->rows_len, rcap * sizeof(u32));
         ensure_keep(c, c->rows_start, (rcap + 1) * sizeof(u32));
       }
-      if (n_cl + R > clcap) {
-        clcap = 2 * (n_cl + R);
+      if (n_cl + nf > clcap) {
+        clcap = 2 * (n_cl + nf);
         ensure_keep(c, c->cl_basis, clcap * sizeof(int));
         ensure_keep(c, c->cl_shift, clcap * n * sizeof(u16));
         ensure_keep(c, c->cl_round, clcap * sizeof(int));
       }
-      F4B_LAUNCH(c, k_new_rows<KW>, nblk(nf, 256), 256, 0, 
-          f, c->front.as<u64>(), nf, c->red.as<int>(), pos, r, n_cl, B.off.as<u32>(), B.len.as<u32>(), B.ckey.as<u64>(),
-          B.lmexp.as<u16>(), B.maxe.as<u16>(), (int)rounds, c->rows_basis.as<int>(), c->rows_delta.as<u64>(),
-          c->rows_len.as<u32>(), c->cl_basis.as<int>(), c->cl_shift.as<u16>(), c->cl_round.as<int>(), err);
-      LAUNCH_CHECK("k_new_rows");
-      // offsets of the new rows continue after M
-      ensure(c, c->tmp_u32a, (size_t)(R + 2) * sizeof(u32));
-      exclusive_scan_u32(c, c->rows_len.as<u32>() + r, c->tmp_u32a.as<u32>(), R);
-      F4B_LAUNCH(c, k_offsets, nblk(R + 1, 256), 256, 0, c->tmp_u32a.as<u32>(), R, (u32)M, c->rows_start.as<u32>() + r);
-      LAUNCH_CHECK("k_offsets");
-      long long Mk = read_u32(c, c->tmp_u32a.as<u32>() + R);
-      if (M + Mk >= (1ll << 31)) fail(F4B_ERR_SIZE_CAP, "batch has more than 2^31 terms");
-      if (M + Mk > mcap) {
-        mcap = 2 * (M + Mk);
-        ensure_keep(c, c->keys_all, mcap * KW * sizeof(u64));
-        ensure_keep(c, c->vals_all, mcap * sizeof(u32));
-      }
-      F4B_LAUNCH(c, k_fill<KW>, nblk(R * 32, 256), 256, 0, r, r + R, c->rows_basis.as<int>(), c->rows_delta.as<u64>(),
-                                                            c->rows_start.as<u32>(), B.off.as<u32>(), B.ckey.as<u64>(),
-                                                            B.coeff.as<u32>(), c->keys_all.as<u64>(), c->vals_all.as<u32>());
-      LAUNCH_CHECK("k_fill");
-      u64* nk = c->keys_all.as<u64>() + (size_t)M * KW;
-      radix_sort_keys(c, KW, nk, Mk, bits, &sorted);
+      ensure(c, c->red, (size_t)nf * sizeof(int));
+      reset_round((u32)mk_bound, (u32)nf);
+      ensure(c, c->uniq, (size_t)(mk_bound + 1) * KW * sizeof(u64));
+      ensure(c, c->front_new, (size_t)(mk_bound + 1) * KW * sizeof(u64));
+      DBuf& cur = (dict == c->dict_a.as<u64>()) ? c->dict_a : c->dict_b;
+      DBuf& oth = (dict == c->dict_a.as<u64>()) ? c->dict_b : c->dict_a;
+      ensure(c, oth, (size_t)(N + mk_bound + 1) * KW * sizeof(u64));
+      const size_t lm_smem = (size_t)nc * nw * 4 <= 48 * 1024 ? (size_t)nc * nw * 4 : 0;
+      F4B_LAUNCH(c, k_closure_search<KW>, nblk(nf * 32, 256), 256, lm_smem, f, c->front.as<u64>(), &dc->nf,
+                 c->lmpref.as<u32>(), c->cand_idx.as<int>(), nc, nw, c->red.as<int>());
+      F4B_LAUNCH(c, k_new_rows<KW>, nblk(nf, 256), 256, 0, f, c->front.as<u64>(), c->red.as<int>(), &dc->nf, r, n_cl,
+                 Mcur, B.off.as<u32>(), B.len.as<u32>(), B.ckey.as<u64>(), B.lmexp.as<u16>(), B.maxe.as<u16>(),
+                 (int)rounds + 1, c->rows_basis.as<int>(), c->rows_delta.as<u64>(), c->rows_start.as<u32>(),
+                 c->cl_basis.as<int>(), c->cl_shift.as<u16>(), c->cl_round.as<int>(), rs.rows_n_st, rs.rows_l_st,
+                 &dc->tickets[2], &dc->R, &dc->Mk, &dc->err);
+      // fill + dictionary of the new rows; keys absent from the dictionary -> next frontier
+      tile_dict(Mcur, 0, (u32)mk_bound, &dc->Mk, (u32)r, 0, &dc->R, c->uniq.as<u64>());
+      c->h_stat[512] = (u32)N;
+      check_cuda(cudaMemcpyAsync(&dc->ndict, &c->h_stat[512], 4, cudaMemcpyHostToDevice, c->stream), "h2d N");
+      sort_unique(c, KW, c->uniq.as<u64>(), &dc->U, (u32)mk_bound, bits, dict, &dc->ndict, c->front_new.as<u64>(),
+                  &dc->nf);
+      // merged dictionary (symbolic.py:281-290); the new keys are the next frontier
+      F4B_LAUNCH(c, k_merge_corank<KW>, nblk(N + mk_bound, 256), 256, 0, cur.as<u64>(), (u32)N,
+                 c->front_new.as<u64>(), &dc->nf, oth.as<u64>());
+      read_counters(c, dc, &hc);
+      const long long R = hc.R, Mk = hc.Mk;
+      if (R == 0) break;
+      if ((long long)Mcur + Mk >= (1ll << 30)) fail(F4B_ERR_SIZE_CAP, "batch has more than 2^30 terms");
+      ++rounds;
       pl->sort_passes += (bits + 7) / 8;
-      ensure(c, c->uniq, (size_t)(Mk + 1) * KW * sizeof(u64));
-      long long nu = unique_keys(c, KW, sorted, Mk, c->uniq.as<u64>());
-      // keys not yet in the dictionary become the next frontier
-      ensure(c, c->flags, (size_t)nu + 16);
-      ensure(c, c->tmp_u32b, (size_t)(nu + 2) * sizeof(u32));
-      ensure(c, c->front_new, (size_t)(nu + 1) * KW * sizeof(u64));
-      flags = c->flags.as<uint8_t>();
-      pos = c->tmp_u32b.as<u32>();
-      F4B_LAUNCH(c, k_absent_flags<KW>, nblk(nu, 256), 256, 0, c->uniq.as<u64>(), nu, dict, (u32)N, flags);
-      LAUNCH_CHECK("k_absent_flags");
-      exclusive_scan_flags(c, flags, pos, nu);
-      F4B_LAUNCH(c, k_compact<KW>, nblk(nu, 256), 256, 0, c->uniq.as<u64>(), nu, flags, pos, c->front_new.as<u64>());
-      LAUNCH_CHECK("k_compact");
-      long long nnew = read_u32(c, pos + nu);
-      // merged dictionary (symbolic.py:281-290)
-      u64* other = (dict == c->dict_a.as<u64>()) ? nullptr : c->dict_a.as<u64>();
-      DBuf& obuf = (dict == c->dict_a.as<u64>()) ? c->dict_b : c->dict_a;
-      DBuf& cbuf = (dict == c->dict_a.as<u64>()) ? c->dict_a : c->dict_b;
-      (void)other;
-      ensure(c, obuf, (size_t)(N + nnew + 1) * KW * sizeof(u64));
-      if (nnew) {
-        F4B_LAUNCH(c, k_merge_corank<KW>, nblk(N + nnew, 256), 256, 0, cbuf.as<u64>(), (u32)N, c->front_new.as<u64>(),
-                                                                        (u32)nnew, obuf.as<u64>());
-        LAUNCH_CHECK("k_merge_corank");
-        dict = obuf.as<u64>();
-      }
-      N += nnew;
+      std::swap(c->front, c->front_new);
+      nf = hc.nf;
+      dict = oth.as<u64>();
+      N += nf;
       M += Mk;
+      Mcur += (u32)Mk;
       r += R;
       n_cl += R;
-      if (N > dict_cap) fail(F4B_ERR_SIZE_CAP, "dictionary exceeded the cap after " + std::to_string(rounds) +
-                                                   " closure rounds");
-      // frontier <- new keys
-      std::swap(c->front, c->front_new);
-      nf = nnew;
+      if (N > dict_cap)
+        fail(F4B_ERR_SIZE_CAP, "dictionary exceeded the cap after " + std::to_string(rounds) + " closure rounds");
     }
+  } else {
+    read_counters(c, dc, &hc);
+    N = hc.N;
   }
   check_cuda(cudaEventRecord(ev1, c->stream), "event record");
 
-  // ---- row assembly: offsets are final; join ------------------------------
+  // ---- row assembly ------------------------------------------------------
   pl->KW = KW;
   pl->lane_bits = f.lane_bits;
   pl->r = r;
@@ -480,41 +674,32 @@ static void compile_t(Ctx* c, const KeyFmt& f, long long r0, const int32_t* h_rb
   ensure(c, pl->cl_basis, (size_t)std::max<long long>(n_cl, 1) * sizeof(int));
   ensure(c, pl->cl_shift, (size_t)std::max<long long>(n_cl, 1) * n * sizeof(u16));
   ensure(c, pl->cl_round, (size_t)std::max<long long>(n_cl, 1) * sizeof(int));
-  check_cuda(cudaMemcpyAsync(pl->row_ptr.p, c->rows_start.p, (r + 1) * sizeof(u32), cudaMemcpyDeviceToDevice, c->stream),
-             "d2d row_ptr");
-  if (M) {
-    check_cuda(cudaMemcpyAsync(pl->val.p, c->vals_all.p, M * sizeof(u32), cudaMemcpyDeviceToDevice, c->stream), "d2d val");
-  }
-  if (N) {
-    check_cuda(cudaMemcpyAsync(pl->dict.p, dict, N * KW * sizeof(u64), cudaMemcpyDeviceToDevice, c->stream), "d2d dict");
-  }
+  check_cuda(cudaMemcpyAsync(pl->row_ptr.p, c->rows_start.p, (r + 1) * sizeof(u32), cudaMemcpyDeviceToDevice,
+                             c->stream), "d2d row_ptr");
+  if (N)
+    check_cuda(cudaMemcpyAsync(pl->dict.p, dict, N * KW * sizeof(u64), cudaMemcpyDeviceToDevice, c->stream), "d2d");
   if (n_cl) {
-    check_cuda(cudaMemcpyAsync(pl->cl_basis.p, c->cl_basis.p, n_cl * sizeof(int), cudaMemcpyDeviceToDevice, c->stream), "d2d");
-    check_cuda(cudaMemcpyAsync(pl->cl_shift.p, c->cl_shift.p, n_cl * n * sizeof(u16), cudaMemcpyDeviceToDevice, c->stream),
+    check_cuda(cudaMemcpyAsync(pl->cl_basis.p, c->cl_basis.p, n_cl * sizeof(int), cudaMemcpyDeviceToDevice, c->stream),
                "d2d");
-    check_cuda(cudaMemcpyAsync(pl->cl_round.p, c->cl_round.p, n_cl * sizeof(int), cudaMemcpyDeviceToDevice, c->stream), "d2d");
+    check_cuda(cudaMemcpyAsync(pl->cl_shift.p, c->cl_shift.p, n_cl * n * sizeof(u16), cudaMemcpyDeviceToDevice,
+                               c->stream), "d2d");
+    check_cuda(cudaMemcpyAsync(pl->cl_round.p, c->cl_round.p, n_cl * sizeof(int), cudaMemcpyDeviceToDevice, c->stream),
+               "d2d");
   }
   if (M) {
     size_t smem = (size_t)N * KW * sizeof(u64);
-    int use_smem = smem <= 200 * 1024 ? 1 : 0;
+    const int use_smem = smem <= 200 * 1024 ? 1 : 0;
     if (!use_smem) smem = 0;
-    static bool attr_set[9] = {false};
-    if (!attr_set[KW]) {
-      check_cuda(cudaFuncSetAttribute(k_join<KW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 1024),
-                 "join attr");
-      attr_set[KW] = true;
-    }
-    int blocks = (int)std::min<long long>(nblk(M, 512), (long long)c->num_sms * (use_smem ? 1 : 4));
-    F4B_LAUNCH(c, k_join<KW>, blocks, 512, smem, c->keys_all.as<u64>(), M, pl->dict.as<u64>(), (u32)N, use_smem,
-                                                 pl->col_ind.as<u32>(), err);
-    LAUNCH_CHECK("k_join");
+    const int per_sm = use_smem ? (int)std::max<size_t>(1, std::min<size_t>(4, (220 * 1024) / (smem + 8 * 1024))) : 4;
+    const int blocks = (int)std::min<long long>(nblk(M, 512 * 8), (long long)c->num_sms * per_sm);
+    F4B_LAUNCH(c, k_join_gen<KW>, blocks, 512, smem, (u32)M, (u32)r, c->rows_basis.as<int>(),
+               c->rows_delta.as<u64>(), c->rows_start.as<u32>(), B.off.as<u32>(), B.ckey.as<u64>(),
+               B.coeff.as<u32>(), pl->dict.as<u64>(), (u32)N, use_smem, pl->col_ind.as<u32>(), pl->val.as<u32>(),
+               &dc->err);
   }
-  if (N) {
-    F4B_LAUNCH(c, k_dict_exps<KW>, nblk(N, 256), 256, 0, f, pl->dict.as<u64>(), (u32)N, pl->dict_exps.as<u16>());
-    LAUNCH_CHECK("k_dict_exps");
-  }
+  if (N) F4B_LAUNCH(c, k_dict_exps<KW>, nblk(N, 256), 256, 0, f, pl->dict.as<u64>(), (u32)N, pl->dict_exps.as<u16>());
   check_cuda(cudaEventRecord(ev2, c->stream), "event record");
-  u32 e = read_u32(c, err);
+  read_counters(c, dc, &hc);
   float ms1 = 0, ms2 = 0;
   check_cuda(cudaEventElapsedTime(&ms1, ev0, ev1), "elapsed");
   check_cuda(cudaEventElapsedTime(&ms2, ev1, ev2), "elapsed");
@@ -524,24 +709,618 @@ static void compile_t(Ctx* c, const KeyFmt& f, long long r0, const int32_t* h_rb
   pl->dict_ns = (int64_t)(ms1 * 1e6);
   pl->asm_ns = (int64_t)(ms2 * 1e6);
   pl->launches = c->launches;
-  if (e & DEVERR_LANE_OVERFLOW) fail(F4B_ERR_LANE_OVERFLOW, "shifted exponent overflows a 16-bit lane");
-  if (e & DEVERR_MISSING_KEY) fail(F4B_ERR_MISSING_KEY, "row key absent from dictionary (closure defect)");
+  if (hc.err & DEVERR_LANE_OVERFLOW) fail(F4B_ERR_LANE_OVERFLOW, "shifted exponent overflows a 16-bit lane");
+  if (hc.err & DEVERR_MISSING_KEY) fail(F4B_ERR_MISSING_KEY, "row key absent from dictionary (closure defect)");
+}
+
+// ===========================================================================
+// Rank-bitmap dictionary (grevlex fast path)
+// ---------------------------------------------------------------------------
+// A counting sort over the dense monomial rank space: for grevlex and batch
+// degree <= D every monomial m has a combinatorial rank
+//   rank(m) = C(n+d-1, n) + sum_{i=n-1..1} [s_i > e_i] C(s_i - e_i - 1 + i, i),
+//   d = deg m, s_{n-1} = d, s_{i-1} = s_i - e_i,
+// that is order-isomorphic to the term order on [0, C(n+D, n)).  The
+// dictionary is then a STATIC presence bitmap over that range (idempotent
+// ORs into a preallocated array — no dynamic insertion, no hashing, fully
+// deterministic), unique is the bitmap itself, the ascending dictionary is the
+// set bits in rank order, and the column map is a popcount prefix:
+//   col(m) = N - 1 - (prefix[rank >> 5] + popc(word & below(rank))).
+// The radix-sort path above stays for lex / deglex and huge rank spaces.
+// ===========================================================================
+static constexpr int RK_THREADS = 256;
+static constexpr int RK_TILE = 4096;
+static constexpr int RK_SROWS = 1024;
+
+template <int KW>
+F4B_DEV u32 key_rank(const KeyFmt& f, const u32* bt, int st, const Key<KW>& k) {
+  const int n = f.n_vars;
+  const int full = (1 << f.lane_bits) - 1;
+  const int d = (int)key_lane<KW>(f, k, 0);
+  u32 r = d ? bt[(n + d - 1) * st + n] : 0u;
+  int s = d;
+  for (int L = 1; L < n; ++L) {
+    const int i = n - L;
+    const int e = full - (int)key_lane<KW>(f, k, L);
+    if (s > e) r += bt[(s - e - 1 + i) * st + i];
+    s -= e;
+  }
+  return r;
+}
+
+F4B_DEV void unrank_exps(u32 r, int n, int D, const u32* bt, int st, u16* e) {
+  // degree: largest d <= D with C(n+d-1, n) <= r  (binary search; C(n-1, n) = 0)
+  int lo = 0, hi = D;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (bt[(n + mid - 1) * st + n] <= r) lo = mid; else hi = mid - 1;
+  }
+  const int d = lo;
+  if (d) r -= bt[(n + d - 1) * st + n];
+  int s = d;
+  for (int i = n - 1; i >= 1; --i) {
+    // largest m in [0, s] with C(m-1+i, i) <= r  (C(i-1, i) = 0 for m = 0)
+    int a = 0, b = s;
+    while (a < b) {
+      const int mid = (a + b + 1) >> 1;
+      if (bt[(mid - 1 + i) * st + i] <= r) a = mid; else b = mid - 1;
+    }
+    if (a > 0) r -= bt[(a - 1 + i) * st + i];
+    e[i] = (u16)(s - a);
+    s = a;
+  }
+  e[0] = (u16)s;
+}
+
+// Fill: every term of rows [r_lo, r_hi) -> its rank -> one bit.  Private
+// shared-memory bitmaps per CTA (written out as partials) when the rank space
+// fits, otherwise atomicOr straight into one global bitmap.
+template <int KW>
+__global__ void __launch_bounds__(RK_THREADS) k_rank_fill(
+    KeyFmt f, u32 m_lo, u32 m_hi_host, const u32* __restrict__ d_mk, u32 r_lo, u32 r_hi_host,
+    const u32* __restrict__ d_r, const int* __restrict__ rb, const u64* __restrict__ delta,
+    const u32* __restrict__ rstart, const u32* __restrict__ boff, const u64* __restrict__ bckey,
+    const u32* __restrict__ bt_g, int st, int bt_words, u32 words, int use_smem, u32* __restrict__ partial) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  Key<KW>* sdel = reinterpret_cast<Key<KW>*>(smraw);
+  u32* srs = reinterpret_cast<u32*>(sdel + RK_SROWS);
+  u32* sbo = srs + RK_SROWS + 1;
+  u32* bt = sbo + RK_SROWS;
+  u32* sbits = bt + bt_words;
+  __shared__ u32 s_rf, s_nr;
+  const u32 m_hi = d_mk ? m_lo + *d_mk : m_hi_host;
+  const u32 r_hi = d_r ? r_lo + *d_r : r_hi_host;
+  for (int i = threadIdx.x; i < bt_words; i += blockDim.x) bt[i] = bt_g[i];
+  u32* bits = partial;
+  if (use_smem) {
+    for (u32 w = threadIdx.x; w < words; w += blockDim.x) sbits[w] = 0;
+    bits = sbits;
+  }
+  __syncthreads();
+  const u32 ntiles = (m_hi - m_lo + RK_TILE - 1) / RK_TILE;
+  for (u32 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const u32 t0 = m_lo + tile * RK_TILE;
+    const u32 n = min((u32)RK_TILE, m_hi - t0);
+    if (threadIdx.x == 0) {
+      const u32 rf = row_of_term(rstart, r_lo, r_hi, t0);
+      s_rf = rf;
+      s_nr = row_of_term(rstart, rf, r_hi, t0 + n - 1) - rf + 1;
+    }
+    __syncthreads();
+    const u32 rf = s_rf, nr = s_nr;
+    if (nr <= (u32)RK_SROWS) {
+      for (u32 i = threadIdx.x; i <= nr; i += blockDim.x) srs[i] = rstart[rf + i];
+      for (u32 i = threadIdx.x; i < nr; i += blockDim.x) {
+        sbo[i] = boff[rb[rf + i]];
+        sdel[i] = key_load<KW>(delta, rf + i);
+      }
+      __syncthreads();
+      for (u32 i = threadIdx.x; i < n; i += blockDim.x) {
+        const u32 t = t0 + i;
+        u32 lo = 0, hi = nr;
+        while (lo + 1 < hi) {
+          const u32 mid = (lo + hi) >> 1;
+          if (srs[mid] <= t) lo = mid; else hi = mid;
+        }
+        const Key<KW> k = key_add<KW>(key_load<KW>(bckey, (long long)sbo[lo] + (t - srs[lo])), sdel[lo]);
+        const u32 rk = key_rank<KW>(f, bt, st, k);
+        atomicOr(bits + (rk >> 5), 1u << (rk & 31));
+      }
+    } else {
+      for (u32 i = threadIdx.x * 8; i < n; i += blockDim.x * 8) {
+        Key<KW> k[8];
+        const int cnt = (int)min(8u, n - i);
+        gen_keys<KW>(t0 + i, cnt, r_lo, r_hi, rb, delta, rstart, boff, bckey, k, nullptr, nullptr);
+        for (int q = 0; q < cnt; ++q) {
+          const u32 rk = key_rank<KW>(f, bt, st, k[q]);
+          atomicOr(bits + (rk >> 5), 1u << (rk & 31));
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (use_smem)
+    for (u32 w = threadIdx.x; w < words; w += blockDim.x) partial[(size_t)blockIdx.x * words + w] = sbits[w];
+}
+
+// OR the partial bitmaps.  mode 0: dict = OR.  mode 1: newbits = OR & ~dict,
+// dict |= OR.  Adds the popcount of the result (dict / newbits) to *d_count.
+__global__ void __launch_bounds__(256) k_rank_reduce(const u32* __restrict__ partial, int nparts, u32 words, int mode,
+                                                     u32* __restrict__ dict, u32* __restrict__ newbits,
+                                                     u32* d_count) {
+  __shared__ u32 ws[33];
+  const u32 w = blockIdx.x * blockDim.x + threadIdx.x;
+  u32 cnt = 0;
+  if (w < words) {
+    u32 v = 0;
+    for (int p = 0; p < nparts; ++p) v |= partial[(size_t)p * words + w];
+    if (mode == 0) {
+      dict[w] = v;
+      cnt = __popc(v);
+    } else {
+      const u32 old = dict[w];
+      const u32 nw = v & ~old;
+      newbits[w] = nw;
+      dict[w] = old | v;
+      cnt = __popc(nw);
+    }
+  }
+  u32 tot;
+  block_scan_excl(cnt, ws, &tot);
+  if (threadIdx.x == 0 && tot) atomicAdd(d_count, tot);
+}
+
+template <int KW>
+__global__ void k_rank_leads(KeyFmt f, long long r, const int* __restrict__ rb, const u64* __restrict__ delta,
+                             const u32* __restrict__ boff, const u64* __restrict__ bckey, const u32* __restrict__ bt,
+                             int st, u32* __restrict__ done) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= r) return;
+  const Key<KW> k = key_add<KW>(key_load<KW>(bckey, boff[rb[i]]), key_load<KW>(delta, i));
+  const u32 rk = key_rank<KW>(f, bt, st, k);
+  atomicOr(done + (rk >> 5), 1u << (rk & 31));
+}
+
+// Set bits of (A & ~B) in ascending rank order (look-back compaction).
+// mode 0 (frontier): out_keys[pos] = device key of the monomial.
+// mode 1 (final dictionary): out_keys ascending, out_exps[(N-1-pos)] (column
+//   order), wprefix[w] = number of set bits before word w.
+template <int KW>
+__global__ void __launch_bounds__(256) k_rank_extract(KeyFmt f, const u32* __restrict__ A, const u32* __restrict__ B,
+                                                      u32 words, int mode, const u32* __restrict__ bt_g, int st,
+                                                      int bt_words, u32* __restrict__ ranks,
+                                                      u32* __restrict__ wprefix, u32* status, u32* ticket,
+                                                      u32* d_count) {
+  constexpr int WPT = 4;  // words per thread
+  extern __shared__ u32 bt[];
+  __shared__ u32 ws[33];
+  __shared__ u32 s_tile, s_base;
+  for (int i = threadIdx.x; i < bt_words; i += blockDim.x) bt[i] = bt_g[i];
+  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const u32 tile = s_tile;
+  const u32 ntiles = (words + 256 * WPT - 1) / (256 * WPT);
+  if (tile >= ntiles) {
+    if (tile == 0 && threadIdx.x == 0) *d_count = 0;
+    return;
+  }
+  const u32 w0 = tile * 256 * WPT + threadIdx.x * WPT;
+  u32 v[WPT];
+  u32 cnt = 0;
+#pragma unroll
+  for (int q = 0; q < WPT; ++q) {
+    const u32 w = w0 + q;
+    v[q] = w < words ? (A[w] & (B ? ~B[w] : 0xFFFFFFFFu)) : 0u;
+    cnt += __popc(v[q]);
+  }
+  u32 tot;
+  const u32 pre = block_scan_excl(cnt, ws, &tot);
+  if (threadIdx.x == 0) s_base = lookback_prefix(status, tile, tot);
+  __syncthreads();
+  u32 pos = s_base + pre;
+#pragma unroll
+  for (int q = 0; q < WPT; ++q) {
+    const u32 w = w0 + q;
+    if (mode == 1 && w < words) wprefix[w] = pos;
+    u32 m = v[q];
+    while (m) {
+      const int bit = __ffs(m) - 1;
+      m &= m - 1;
+      ranks[pos++] = w * 32 + bit;
+    }
+  }
+  if (tile == ntiles - 1 && threadIdx.x == 0) *d_count = s_base + tot;
+}
+
+// ranks -> device keys (and, for the final dictionary, exponents in column
+// order).  Grid-stride over the device-side count.
+template <int KW>
+__global__ void __launch_bounds__(256) k_rank_unrank(KeyFmt f, const u32* __restrict__ ranks,
+                                                     const u32* __restrict__ d_count, const u32* __restrict__ bt_g,
+                                                     int st, int bt_words, int D, u64* __restrict__ out_keys,
+                                                     u16* __restrict__ out_exps) {
+  extern __shared__ u32 bts[];
+  for (int i = threadIdx.x; i < bt_words; i += blockDim.x) bts[i] = bt_g[i];
+  __syncthreads();
+  const u32 cnt = *d_count;
+  const int n = f.n_vars;
+  for (u32 j = blockIdx.x * blockDim.x + threadIdx.x; j < cnt; j += gridDim.x * blockDim.x) {
+    u16 e[MAXV];
+    unrank_exps(ranks[j], n, D, bts, st, e);
+    key_store<KW>(out_keys, j, key_encode<KW>(f, e));
+    if (out_exps)
+      for (int x = 0; x < n; ++x) out_exps[((long long)cnt - 1 - j) * n + x] = e[x];
+  }
+}
+
+// Join: every term -> rank -> column via the popcount prefix.
+template <int KW>
+__global__ void __launch_bounds__(RK_THREADS) k_rank_join(KeyFmt f, u32 M, u32 r, const int* __restrict__ rb,
+                                                          const u64* __restrict__ delta, const u32* __restrict__ rstart,
+                                                          const u32* __restrict__ boff, const u64* __restrict__ bckey,
+                                                          const u32* __restrict__ bcoeff, const u32* __restrict__ bt_g,
+                                                          int st, int bt_words, const u32* __restrict__ dict_g,
+                                                          const u32* __restrict__ wpre_g, u32 words, int use_smem,
+                                                          u32 N, u32* __restrict__ col, u32* __restrict__ val,
+                                                          u32* err) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  Key<KW>* sdel = reinterpret_cast<Key<KW>*>(smraw);
+  u32* srs = reinterpret_cast<u32*>(sdel + RK_SROWS);
+  u32* sbo = srs + RK_SROWS + 1;
+  u32* bt = sbo + RK_SROWS;
+  u32* sd = bt + bt_words;
+  u32* sp = sd + words;
+  __shared__ u32 s_rf, s_nr;
+  for (int i = threadIdx.x; i < bt_words; i += blockDim.x) bt[i] = bt_g[i];
+  const u32* dict = dict_g;
+  const u32* wpre = wpre_g;
+  if (use_smem) {
+    for (u32 w = threadIdx.x; w < words; w += blockDim.x) {
+      sd[w] = dict_g[w];
+      sp[w] = wpre_g[w];
+    }
+    dict = sd;
+    wpre = sp;
+  }
+  __syncthreads();
+  bool miss = false;
+  const u32 ntiles = (M + RK_TILE - 1) / RK_TILE;
+  for (u32 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const u32 t0 = tile * RK_TILE;
+    const u32 n = min((u32)RK_TILE, M - t0);
+    if (threadIdx.x == 0) {
+      const u32 rf = row_of_term(rstart, 0, r, t0);
+      s_rf = rf;
+      s_nr = row_of_term(rstart, rf, r, t0 + n - 1) - rf + 1;
+    }
+    __syncthreads();
+    const u32 rf = s_rf, nr = s_nr;
+    const bool staged = nr <= (u32)RK_SROWS;
+    if (staged) {
+      for (u32 i = threadIdx.x; i <= nr; i += blockDim.x) srs[i] = rstart[rf + i];
+      for (u32 i = threadIdx.x; i < nr; i += blockDim.x) {
+        sbo[i] = boff[rb[rf + i]];
+        sdel[i] = key_load<KW>(delta, rf + i);
+      }
+    }
+    __syncthreads();
+    for (u32 i = threadIdx.x; i < n; i += blockDim.x) {
+      const u32 t = t0 + i;
+      u32 row, rs, bo;
+      Key<KW> d;
+      if (staged) {
+        u32 lo = 0, hi = nr;
+        while (lo + 1 < hi) {
+          const u32 mid = (lo + hi) >> 1;
+          if (srs[mid] <= t) lo = mid; else hi = mid;
+        }
+        rs = srs[lo];
+        bo = sbo[lo];
+        d = sdel[lo];
+      } else {
+        row = row_of_term(rstart, rf, r, t);
+        rs = rstart[row];
+        bo = boff[rb[row]];
+        d = key_load<KW>(delta, row);
+      }
+      const Key<KW> k = key_add<KW>(key_load<KW>(bckey, (long long)bo + (t - rs)), d);
+      const u32 rk = key_rank<KW>(f, bt, st, k);
+      const u32 word = dict[rk >> 5];
+      const u32 below = word & ((1u << (rk & 31)) - 1u);
+      if (!((word >> (rk & 31)) & 1u)) miss = true;
+      col[t] = N - 1 - (wpre[rk >> 5] + __popc(below));
+      val[t] = __ldg(bcoeff + bo + (t - rs));
+    }
+    __syncthreads();
+  }
+  if (miss) atomicOr(err, (u32)DEVERR_MISSING_KEY);
+}
+
+static unsigned long long binom_ull(int a, int b) {
+  if (b < 0 || a < b) return 0;
+  unsigned long long r = 1;
+  for (int i = 1; i <= b; ++i) r = r * (unsigned long long)(a - b + i) / (unsigned long long)i;
+  return r;
+}
+
+// Eligibility of the rank path: grevlex and a rank space of <= 2^26 monomials.
+static bool rank_path_ok(int order, int n, long long D) {
+  if (order != 0 || D > 255) return false;
+  if (const char* e = getenv("F4B_DICT")) {
+    if (!strcmp(e, "sort")) return false;
+  }
+  return binom_ull(n + (int)D, n) <= (1ull << 26);
+}
+
+template <int KW>
+static void compile_rank(Ctx* c, const KeyFmt& f, int D, long long r0, const int32_t* h_rb, const uint16_t* h_shift,
+                         int closure, const std::vector<int32_t>& cand, long long dict_cap, f4b_plan* pl) {
+  Basis& B = c->basis;
+  const int n = c->n_vars;
+  c->launches = 0;
+  cudaEvent_t ev0, ev1, ev2;
+  check_cuda(cudaEventCreate(&ev0), "event");
+  check_cuda(cudaEventCreate(&ev1), "event");
+  check_cuda(cudaEventCreate(&ev2), "event");
+  check_cuda(cudaEventRecord(ev0, c->stream), "event record");
+  encode_basis<KW>(c, f);
+
+  // binomial table C(a, b), a <= D + n + 1, b <= n
+  const int st = n + 1;
+  const int rows_bt = D + n + 2;
+  const int bt_words = rows_bt * st;
+  std::vector<u32> hbt((size_t)bt_words, 0u);
+  for (int a = 0; a < rows_bt; ++a)
+    for (int b = 0; b <= n; ++b) hbt[(size_t)a * st + b] = (u32)std::min<unsigned long long>(binom_ull(a, b), 0xFFFFFFFFull);
+  const unsigned long long Rsp = binom_ull(n + D, n);
+  const u32 words = (u32)((Rsp + 31) / 32);
+
+  std::vector<uint32_t> h_start(r0 + 1);
+  long long M = 0;
+  for (long long i = 0; i < r0; ++i) {
+    h_start[i] = (uint32_t)M;
+    M += B.h_len[h_rb[i]];
+  }
+  h_start[r0] = (uint32_t)M;
+  if (M >= (1ll << 30)) fail(F4B_ERR_SIZE_CAP, "batch has more than 2^30 terms");
+  const u32 M0 = (u32)M;
+
+  // buffers: counters+lookback | bt | dict | aux (done / newbits) | wprefix | partials
+  const size_t fill_smem_bits = (size_t)words * 4;
+  const int use_smem = fill_smem_bits <= 96 * 1024 ? 1 : 0;
+  const size_t fill_smem = (size_t)RK_SROWS * (KW * 8 + 8) + 16 + (size_t)bt_words * 4 + (use_smem ? fill_smem_bits : 0);
+  const int per_sm = use_smem ? (int)std::max<size_t>(1, std::min<size_t>(4, (220 * 1024) / (fill_smem + 4096))) : 4;
+  const int max_grid = c->num_sms * per_sm;
+  ensure(c, c->errflag, sizeof(DevCounters) + 4096);
+  DevCounters* dc = reinterpret_cast<DevCounters*>(c->errflag.p);
+  check_cuda(cudaMemsetAsync(dc, 0, sizeof(DevCounters), c->stream), "memset counters");
+  // look-back status regions: A/B for k_new_rows (<= N/256 tiles), C for k_rank_extract
+  const size_t lbAB = (size_t)words / 8 + 64, lbC = (size_t)words / 1024 + 64;
+  ensure(c, c->dict_b, ((size_t)bt_words + 3 * (size_t)words + 2 * lbAB + lbC + 64) * 4);
+  u32* base = c->dict_b.as<u32>();
+  u32* d_bt = base;
+  u32* d_dict = d_bt + bt_words;
+  u32* d_aux = d_dict + words;
+  u32* d_wpre = d_aux + words;
+  u32* d_lbA = d_wpre + words + 1;
+  u32* d_lbB = d_lbA + lbAB;
+  u32* d_lbC = d_lbB + lbAB;
+  check_cuda(cudaMemcpyAsync(d_bt, hbt.data(), (size_t)bt_words * 4, cudaMemcpyHostToDevice, c->stream), "h2d binom");
+  auto zero_lb = [&]() {
+    check_cuda(cudaMemsetAsync(dc->tickets, 0, sizeof(dc->tickets), c->stream), "memset tickets");
+    check_cuda(cudaMemsetAsync(d_lbA, 0, (2 * lbAB + lbC) * 4, c->stream), "memset lb");
+  };
+
+  // rows of round 0
+  long long rcap = std::max<long long>(2 * r0 + 1024, 4096);
+  ensure(c, c->rows_basis, rcap * sizeof(int));
+  ensure(c, c->rows_delta, rcap * KW * sizeof(u64));
+  ensure(c, c->rows_len, rcap * sizeof(u32));
+  ensure(c, c->rows_start, (rcap + 1) * sizeof(u32));
+  ensure(c, c->shift_in, (size_t)std::max<long long>(r0, 1) * n * sizeof(u16));
+  check_cuda(cudaMemcpyAsync(c->rows_basis.p, h_rb, r0 * sizeof(int), cudaMemcpyHostToDevice, c->stream), "h2d rows");
+  check_cuda(cudaMemcpyAsync(c->shift_in.p, h_shift, r0 * n * sizeof(u16), cudaMemcpyHostToDevice, c->stream), "h2d");
+  check_cuda(cudaMemcpyAsync(c->rows_start.p, h_start.data(), (r0 + 1) * sizeof(u32), cudaMemcpyHostToDevice,
+                             c->stream), "h2d starts");
+  F4B_LAUNCH(c, k_rows0<KW>, nblk(r0, 256), 256, 0, f, r0, c->rows_basis.as<int>(), c->shift_in.as<u16>(),
+             B.len.as<u32>(), c->rows_delta.as<u64>(), c->rows_len.as<u32>());
+  static bool attr = false;
+  if (!attr) {
+    check_cuda(cudaFuncSetAttribute(k_rank_fill<KW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "attr");
+    check_cuda(cudaFuncSetAttribute(k_rank_join<KW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "attr");
+    check_cuda(cudaFuncSetAttribute(k_rank_extract<KW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024),
+               "attr");
+    attr = true;
+  }
+  auto fill = [&](u32 m_lo, u32 m_hi, u32 m_bound, const u32* d_mk, u32 r_lo, u32 r_hi, const u32* d_r) -> int {
+    const u32 tiles = std::max<u32>(1, (m_bound + RK_TILE - 1) / RK_TILE);
+    const int grid = (int)std::min<long long>(tiles, max_grid);
+    const int nparts = use_smem ? grid : 1;
+    ensure(c, c->uniq, (size_t)nparts * words * 4 + 16);
+    if (!use_smem) check_cuda(cudaMemsetAsync(c->uniq.p, 0, (size_t)words * 4, c->stream), "memset bits");
+    F4B_LAUNCH(c, k_rank_fill<KW>, grid, RK_THREADS, fill_smem, f, m_lo, m_hi, d_mk, r_lo, r_hi, d_r,
+               c->rows_basis.as<int>(), c->rows_delta.as<u64>(), c->rows_start.as<u32>(), B.off.as<u32>(),
+               B.ckey.as<u64>(), d_bt, st, bt_words, words, use_smem, c->uniq.as<u32>());
+    return nparts;
+  };
+  const size_t ex_smem = (size_t)bt_words * 4;
+  // (caller zeroes region C and ticket 3 first)
+  // set bits of A & ~Bm -> rank list (ascending) -> device keys (+ exponents)
+  ensure(c, c->tmp_u32c, ((size_t)std::min<unsigned long long>(Rsp, (unsigned long long)M0 + (1ull << 22)) + 16) * 4);
+  auto extract = [&](const u32* A, const u32* Bm, int mode, u64* out_keys, u16* out_exps, u32 N_final, u32* d_count) {
+    (void)N_final;
+    const u32 tiles = std::max<u32>(1, (words + 1023) / 1024);
+    F4B_LAUNCH(c, k_rank_extract<KW>, tiles, 256, 0, f, A, Bm, words, mode, d_bt, st, 0, c->tmp_u32c.as<u32>(), d_wpre,
+               d_lbC, &dc->tickets[3], d_count);
+    F4B_LAUNCH(c, k_rank_unrank<KW>, c->num_sms * 2, 256, ex_smem, f, c->tmp_u32c.as<u32>(), d_count, d_bt, st,
+               bt_words, D, out_keys, out_exps);
+  };
+
+  zero_lb();
+  int nparts = fill(0, M0, M0, nullptr, 0, (u32)r0, nullptr);
+  check_cuda(cudaMemsetAsync(&dc->N, 0, 4, c->stream), "memset");
+  F4B_LAUNCH(c, k_rank_reduce, nblk(words, 256), 256, 0, c->uniq.as<u32>(), nparts, words, 0, d_dict, nullptr,
+             &dc->N);
+  long long r = r0, rounds = 0, n_cl = 0, N = 0;
+  DevCounters hc;
+  if (closure) {
+    check_cuda(cudaMemsetAsync(d_aux, 0, (size_t)words * 4, c->stream), "memset done");
+    F4B_LAUNCH(c, k_rank_leads<KW>, nblk(r0, 256), 256, 0, f, r0, c->rows_basis.as<int>(), c->rows_delta.as<u64>(),
+               B.off.as<u32>(), B.ckey.as<u64>(), d_bt, st, d_aux);
+    ensure(c, c->front, (size_t)(std::min<unsigned long long>(Rsp, M0) + 1) * KW * sizeof(u64));
+    extract(d_dict, d_aux, 0, c->front.as<u64>(), nullptr, 0, &dc->nf);
+    // candidate LMs in preference order (key(LM), index) (symbolic.py:228-235)
+    std::vector<int32_t> pref(cand);
+    std::stable_sort(pref.begin(), pref.end(), [&](int32_t x, int32_t y) {
+      int s = mon_cmp(&B.h_lm[(size_t)x * n], &B.h_lm[(size_t)y * n], n, c->order);
+      return s != 0 ? s < 0 : x < y;
+    });
+    const int nc = (int)pref.size();
+    const int nw = (n + 1) / 2;
+    std::vector<uint32_t> h_lmw((size_t)std::max(nc, 1) * nw, 0u);
+    for (int q = 0; q < nc; ++q)
+      for (int v = 0; v < n; ++v)
+        h_lmw[(size_t)q * nw + v / 2] |= (uint32_t)B.h_lm[(size_t)pref[q] * n + v] << (16 * (v & 1));
+    ensure(c, c->lmpref, h_lmw.size() * sizeof(u32));
+    ensure(c, c->cand_idx, (size_t)std::max(nc, 1) * sizeof(int));
+    check_cuda(cudaMemcpyAsync(c->lmpref.p, h_lmw.data(), h_lmw.size() * sizeof(u32), cudaMemcpyHostToDevice,
+                               c->stream), "h2d lm");
+    if (nc)
+      check_cuda(cudaMemcpyAsync(c->cand_idx.p, pref.data(), nc * sizeof(int), cudaMemcpyHostToDevice, c->stream),
+                 "h2d cand");
+    read_counters(c, dc, &hc);
+    N = hc.N;
+    long long nf = hc.nf;
+    long long clcap = std::max<long long>(N + 1024, 4096);
+    ensure(c, c->cl_basis, clcap * sizeof(int));
+    ensure(c, c->cl_shift, clcap * n * sizeof(u16));
+    ensure(c, c->cl_round, clcap * sizeof(int));
+    u32 Mcur = M0;
+    long long maxlen = 1;
+    for (int32_t k : pref) maxlen = std::max<long long>(maxlen, B.h_len[k]);
+    while (nf > 0 && nc > 0) {
+      const long long mk_bound = std::max<long long>(1, std::min<long long>(nf * maxlen, (1ll << 30) - Mcur));
+      if (r + nf + 2 > rcap) {
+        rcap = 2 * (r + nf + 2);
+        ensure_keep(c, c->rows_basis, rcap * sizeof(int));
+        ensure_keep(c, c->rows_delta, rcap * KW * sizeof(u64));
+        ensure_keep(c, c->rows_len, rcap * sizeof(u32));
+        ensure_keep(c, c->rows_start, (rcap + 1) * sizeof(u32));
+      }
+      if (n_cl + nf > clcap) {
+        clcap = 2 * (n_cl + nf);
+        ensure_keep(c, c->cl_basis, clcap * sizeof(int));
+        ensure_keep(c, c->cl_shift, clcap * n * sizeof(u16));
+        ensure_keep(c, c->cl_round, clcap * sizeof(int));
+      }
+      ensure(c, c->red, (size_t)nf * sizeof(int));
+      ensure(c, c->front_new, (size_t)(std::min<unsigned long long>(Rsp, (unsigned long long)mk_bound) + 1) * KW *
+                                  sizeof(u64));
+      zero_lb();
+      const size_t lm_smem = (size_t)nc * nw * 4 <= 48 * 1024 ? (size_t)nc * nw * 4 : 0;
+      F4B_LAUNCH(c, k_closure_search<KW>, nblk(nf * 32, 256), 256, lm_smem, f, c->front.as<u64>(), &dc->nf,
+                 c->lmpref.as<u32>(), c->cand_idx.as<int>(), nc, nw, c->red.as<int>());
+      F4B_LAUNCH(c, k_new_rows<KW>, nblk(nf, 256), 256, 0, f, c->front.as<u64>(), c->red.as<int>(), &dc->nf, r, n_cl,
+                 Mcur, B.off.as<u32>(), B.len.as<u32>(), B.ckey.as<u64>(), B.lmexp.as<u16>(), B.maxe.as<u16>(),
+                 (int)rounds + 1, c->rows_basis.as<int>(), c->rows_delta.as<u64>(), c->rows_start.as<u32>(),
+                 c->cl_basis.as<int>(), c->cl_shift.as<u16>(), c->cl_round.as<int>(), d_lbA, d_lbB,
+                 &dc->tickets[2], &dc->R, &dc->Mk, &dc->err);
+      nparts = fill(Mcur, 0, (u32)mk_bound, &dc->Mk, (u32)r, 0, &dc->R);
+      F4B_LAUNCH(c, k_rank_reduce, nblk(words, 256), 256, 0, c->uniq.as<u32>(), nparts, words, 1, d_dict, d_aux,
+                 &dc->U);
+      extract(d_aux, nullptr, 0, c->front_new.as<u64>(), nullptr, 0u, &dc->nf);
+      read_counters(c, dc, &hc);
+      const long long R = hc.R, Mk = hc.Mk;
+      if (R == 0) break;
+      if ((long long)Mcur + Mk >= (1ll << 30)) fail(F4B_ERR_SIZE_CAP, "batch has more than 2^30 terms");
+      ++rounds;
+      std::swap(c->front, c->front_new);
+      nf = hc.nf;
+      N += nf;
+      M += Mk;
+      Mcur += (u32)Mk;
+      r += R;
+      n_cl += R;
+      if (N > dict_cap)
+        fail(F4B_ERR_SIZE_CAP, "dictionary exceeded the cap after " + std::to_string(rounds) + " closure rounds");
+    }
+  } else {
+    read_counters(c, dc, &hc);
+    N = hc.N;
+  }
+  check_cuda(cudaEventRecord(ev1, c->stream), "event record");
+
+  // ---- row assembly ------------------------------------------------------
+  pl->KW = KW;
+  pl->lane_bits = f.lane_bits;
+  pl->r = r;
+  pl->r0 = r0;
+  pl->N = N;
+  pl->M = M;
+  pl->closure_rounds = rounds;
+  pl->sort_passes = 0;
+  ensure(c, pl->row_ptr, (size_t)(r + 1) * sizeof(u32));
+  ensure(c, pl->col_ind, (size_t)std::max<long long>(M, 1) * sizeof(u32));
+  ensure(c, pl->val, (size_t)std::max<long long>(M, 1) * sizeof(u32));
+  ensure(c, pl->dict, (size_t)std::max<long long>(N, 1) * KW * sizeof(u64));
+  ensure(c, pl->dict_exps, (size_t)std::max<long long>(N, 1) * n * sizeof(u16));
+  ensure(c, pl->cl_basis, (size_t)std::max<long long>(n_cl, 1) * sizeof(int));
+  ensure(c, pl->cl_shift, (size_t)std::max<long long>(n_cl, 1) * n * sizeof(u16));
+  ensure(c, pl->cl_round, (size_t)std::max<long long>(n_cl, 1) * sizeof(int));
+  check_cuda(cudaMemcpyAsync(pl->row_ptr.p, c->rows_start.p, (r + 1) * sizeof(u32), cudaMemcpyDeviceToDevice,
+                             c->stream), "d2d row_ptr");
+  if (n_cl) {
+    check_cuda(cudaMemcpyAsync(pl->cl_basis.p, c->cl_basis.p, n_cl * sizeof(int), cudaMemcpyDeviceToDevice, c->stream),
+               "d2d");
+    check_cuda(cudaMemcpyAsync(pl->cl_shift.p, c->cl_shift.p, n_cl * n * sizeof(u16), cudaMemcpyDeviceToDevice,
+                               c->stream), "d2d");
+    check_cuda(cudaMemcpyAsync(pl->cl_round.p, c->cl_round.p, n_cl * sizeof(int), cudaMemcpyDeviceToDevice, c->stream),
+               "d2d");
+  }
+  // final dictionary: keys ascending, exponents in column order, word prefix
+  zero_lb();
+  extract(d_dict, nullptr, 1, pl->dict.as<u64>(), pl->dict_exps.as<u16>(), (u32)N, &dc->U);
+  if (M) {
+    const size_t js = (size_t)RK_SROWS * (KW * 8 + 8) + 16 + (size_t)bt_words * 4;
+    const int use_s = js + (size_t)words * 8 <= 200 * 1024 ? 1 : 0;
+    const size_t jsmem = js + (use_s ? (size_t)words * 8 : 0);
+    const int jper = (int)std::max<size_t>(1, std::min<size_t>(4, (220 * 1024) / (jsmem + 4096)));
+    const int grid = (int)std::min<long long>(nblk(M, RK_TILE), (long long)c->num_sms * jper);
+    F4B_LAUNCH(c, k_rank_join<KW>, grid, RK_THREADS, jsmem, f, (u32)M, (u32)r, c->rows_basis.as<int>(),
+               c->rows_delta.as<u64>(), c->rows_start.as<u32>(), B.off.as<u32>(), B.ckey.as<u64>(),
+               B.coeff.as<u32>(), d_bt, st, bt_words, d_dict, d_wpre, words, use_s, (u32)N, pl->col_ind.as<u32>(),
+               pl->val.as<u32>(), &dc->err);
+  }
+  check_cuda(cudaEventRecord(ev2, c->stream), "event record");
+  read_counters(c, dc, &hc);
+  float ms1 = 0, ms2 = 0;
+  check_cuda(cudaEventElapsedTime(&ms1, ev0, ev1), "elapsed");
+  check_cuda(cudaEventElapsedTime(&ms2, ev1, ev2), "elapsed");
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
+  cudaEventDestroy(ev2);
+  pl->dict_ns = (int64_t)(ms1 * 1e6);
+  pl->asm_ns = (int64_t)(ms2 * 1e6);
+  pl->launches = c->launches;
+  if (hc.U != (u32)N) fail(F4B_ERR_PROPERTY, "dictionary extraction count mismatch");
+  if (hc.err & DEVERR_LANE_OVERFLOW) fail(F4B_ERR_LANE_OVERFLOW, "shifted exponent overflows a 16-bit lane");
+  if (hc.err & DEVERR_MISSING_KEY) fail(F4B_ERR_MISSING_KEY, "row key absent from dictionary (closure defect)");
 }
 
 void compile_batch(Ctx* c, long long r0, const int32_t* rb, const uint16_t* shift, int closure, const int32_t* cands,
                    long long n_cands, long long dict_cap, f4b_plan* pl) {
   Basis& B = c->basis;
   const int n = c->n_vars;
-  // validation + batch degree (host metadata only)
   long long D = 0;
   for (long long i = 0; i < r0; ++i) {
-    int g = rb[i];
+    const int g = rb[i];
     if (g < 0 || g >= B.n_polys) fail(F4B_ERR_PRECONDITION, "row references unknown basis index");
     if (B.h_len[g] < 1) fail(F4B_ERR_PROPERTY, "zero polynomial referenced as a reducer");
     long long d = 0;
     for (int v = 0; v < n; ++v) {
-      long long s = shift[i * n + v];
-      if (s + B.h_maxe[(size_t)g * n + v] > 0xFFFF) fail(F4B_ERR_LANE_OVERFLOW, "shifted exponent overflows a 16-bit lane");
+      const long long s = shift[i * n + v];
+      if (s + B.h_maxe[(size_t)g * n + v] > 0xFFFF)
+        fail(F4B_ERR_LANE_OVERFLOW, "shifted exponent overflows a 16-bit lane");
       d += s + B.h_lm[(size_t)g * n + v];
     }
     D = std::max(D, d);
@@ -555,7 +1334,6 @@ void compile_batch(Ctx* c, long long r0, const int32_t* rb, const uint16_t* shif
     cand.resize(B.n_polys);
     for (int k = 0; k < B.n_polys; ++k) cand[k] = k;
   }
-  // drop empty candidates (zero polynomials have no leading monomial)
   cand.erase(std::remove_if(cand.begin(), cand.end(), [&](int32_t k) { return B.h_len[k] < 1; }), cand.end());
   KeyFmt f;
   f.order = c->order;
@@ -568,10 +1346,19 @@ void compile_batch(Ctx* c, long long r0, const int32_t* rb, const uint16_t* shif
     f.lane_bits = b;
   }
   f.n_lanes = n;
-  int bits = f.lane_bits * f.n_lanes;
+  const int bits = f.lane_bits * f.n_lanes;
   int KW = 1;
   while (64 * KW < bits) KW *= 2;
   if (KW > 8) fail(F4B_ERR_PRECONDITION, "batch degree too large for the device key format");
+  if (rank_path_ok(c->order, n, D)) {
+    switch (KW) {
+      case 1: compile_rank<1>(c, f, (int)D, r0, rb, shift, closure, cand, dict_cap, pl); break;
+      case 2: compile_rank<2>(c, f, (int)D, r0, rb, shift, closure, cand, dict_cap, pl); break;
+      case 4: compile_rank<4>(c, f, (int)D, r0, rb, shift, closure, cand, dict_cap, pl); break;
+      default: compile_rank<8>(c, f, (int)D, r0, rb, shift, closure, cand, dict_cap, pl); break;
+    }
+    return;
+  }
   switch (KW) {
     case 1: compile_t<1>(c, f, r0, rb, shift, closure, cand, dict_cap, pl); break;
     case 2: compile_t<2>(c, f, r0, rb, shift, closure, cand, dict_cap, pl); break;

@@ -105,11 +105,21 @@ def _random_poly(rng, ring, max_exp, terms):
     return poly_monic(poly_normalize(ts, ring))
 
 
+@pytest.fixture(params=["rank", "sort"])
+def dict_mode(request, monkeypatch):
+    """Both dictionary paths: rank bitmap (grevlex fast path) and radix sort."""
+    if request.param == "sort":
+        monkeypatch.setenv("F4B_DICT", "sort")
+    else:
+        monkeypatch.delenv("F4B_DICT", raising=False)
+    return request.param
+
+
 @pytest.mark.parametrize("order,n,max_exp,p", [("grevlex", 2, 3, 7), ("grevlex", 5, 4, 32003),
                                                ("deglex", 4, 3, 101), ("lex", 3, 3, 65521),
                                                ("lex", 6, 2, 101), ("grevlex", 9, 2, 2147483629),
                                                ("grevlex", 3, 40, 32003)])
-def test_compile_random_against_oracle(cuda, order, n, max_exp, p):
+def test_compile_random_against_oracle(cuda, dict_mode, order, n, max_exp, p):
     ring = Ring([f"v{i}" for i in range(n)], order, FieldModulus(p))
     rng = np.random.default_rng(n * 1000 + max_exp)
     for trial in range(6):
@@ -217,6 +227,30 @@ def test_f4_steps_match_reference(cuda, name, gen, args):
 
     text = format_system(ring, reduce_basis(st.basis, ring))
     assert hashlib.sha256(text.encode()).hexdigest() == gold["final_sha256"]
+
+
+@pytest.mark.parametrize("name,gen,args", [("cyclic6_p32003", gen_cyclic, (6, 32003)),
+                                           ("katsura6_p32003", gen_katsura, (6, 32003))])
+def test_f4_steps_match_reference_sort_path(cuda, monkeypatch, name, gen, args):
+    """Same per-step digests with the radix-sort dictionary forced."""
+    monkeypatch.setenv("F4B_DICT", "sort")
+    gold = load_golden(name)
+    ring, polys = gen(*args)
+    st = GroebnerState(ring)
+    for f in polys:
+        update_pairs(st, poly_monic(f))
+    k = 0
+    while st.n_pairs():
+        plan, ech, _ = f4_step(st)
+        assert plan_digest(plan) == gold["steps"][k]["plan_sha256"], f"plan step {k}"
+        assert _rref_digest(ech) == gold["steps"][k]["rref_sha256"], f"rref step {k}"
+        k += 1
+
+
+@pytest.mark.parametrize("name", ["cyclic8_p32003", "katsura11_p32003"])
+def test_large_step_replay_sort_path(cuda, monkeypatch, name):
+    monkeypatch.setenv("F4B_DICT", "sort")
+    test_large_step_replay(cuda, name)
 
 
 def test_f4_groebner_entry_point(cuda):
