@@ -47,6 +47,22 @@ WORKLOAD = "cyclic-8 over F_32003, grevlex, all 38 F4 batches (compile_batch + p
 CPU_SAMPLE_STEPS = (5, 6, 7)
 
 
+def _traffic_from_profiles():
+    """DRAM bytes per launch (dram__bytes_read + write) from the committed
+    `ncu --set full` summary (profiles/*/traffic.json), keyed by kernel."""
+    out = {}
+    pdir = os.path.join(ROOT, "profiles")
+    for sub in sorted(os.listdir(pdir)) if os.path.isdir(pdir) else []:
+        path = os.path.join(pdir, sub, "traffic.json")
+        if os.path.exists(path):
+            try:
+                with open(path) as fh:
+                    out.update(json.load(fh))
+            except Exception:
+                pass
+    return out
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -205,14 +221,53 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-# algorithmic bytes per kernel: totals per batch
-def kernel_bytes(name, b, KW):
-    M, N, r = b["M"], b["N"], b["r"]
-    key = 8 * KW
-    if name.startswith("k_join"):
-        return M * key + 4 * M + N * key
-    if name.startswith("k_fill"):
-        return 2 * M * (key + 4)
+# Algorithmic (compulsory) bytes per kernel per batch — DESIGN.md §4.
+#   k_rank_join / k_join_gen : read every term's source key + coefficient,
+#                              write col_ind + val            M(8KW+4) + 8M
+#   k_rank_fill / k_tile_dict: read every term's source key   M * 8KW
+#   k_sweep<0>               : read the C and A rows once, write D'
+#                              8M + 4|C|K
+#   k_dense_forward          : read + write D' once           8|C|K
+SYMBOLIC = ("k_rank_", "k_tile_dict", "k_join_gen", "k_os_", "k_small_sort", "k_unique_absent", "k_closure",
+            "k_new_rows", "k_merge_corank", "k_rows0", "k_encode_basis", "k_mark_leads", "k_front0", "k_dict_exps")
+
+
+def kernel_bytes(name, b, pinfo, einfo):
+    M = b["M"]
+    KW = pinfo["key_words"]
+    C, K = einfo["dense_rows"], einfo["dense_cols"]
+    if name.startswith(("k_rank_join", "k_join_gen")):
+        return M * (8 * KW + 4) + 8 * M
+    if name.startswith(("k_rank_fill", "k_tile_dict")):
+        return M * 8 * KW
+    if name == "k_sweep<0>":
+        return 8 * M + 4 * C * K
+    if name == "k_dense_forward":
+        return 8 * C * K
+    return None
+
+
+def roofline_for(kprof, records, peak, peak_src, want):
+    """Roofline of the most expensive kernel accepted by `want` (with a byte model)."""
+    total = max(1.0, sum(v[1] for v in kprof.values()))
+    for name, (cnt, ns) in sorted(kprof.items(), key=lambda kv: -kv[1][1]):
+        if not want(name) or ns <= 0:
+            continue
+        tot = 0
+        for b, pinfo, einfo in records:
+            kb = kernel_bytes(name, b, pinfo, einfo)
+            if kb is None:
+                tot = None
+                break
+            tot += kb
+        if tot is None:
+            return {"bound": "latency", "kernel": name, "achieved": None, "peak": peak, "unit": "GB/s", "frac": None,
+                    "traffic": None, "launches": cnt, "avg_launch_us": ns / cnt / 1e3, "share_of_step": ns / total,
+                    "note": "no algorithmic byte model (schedule-dependent work)"}
+        ach = tot / (ns * 1e-9) / 1e9
+        return {"bound": "hbm", "kernel": name, "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                "traffic": None, "launches": cnt, "avg_launch_us": ns / cnt / 1e3, "peak_source": peak_src,
+                "share_of_step": ns / total, "algorithmic_bytes_per_launch": tot / cnt}
     return None
 
 
@@ -294,24 +349,13 @@ def main():
 
     # roofline: the dominant kernel with an algorithmic byte model
     peak, peak_src = _peaks()
-    KW = records[0][1]["key_words"] if records else 1
     ranked = sorted(kprof.items(), key=lambda kv: -kv[1][1])
-    roof = None
-    for name, (cnt, ns) in ranked:
-        tot_bytes = 0
-        ok = True
-        for b, pinfo, _ in records:
-            kb = kernel_bytes(name, b, pinfo["key_words"])
-            if kb is None:
-                ok = False
-                break
-            tot_bytes += kb
-        if ok and ns > 0:
-            ach = tot_bytes / (ns * 1e-9) / 1e9
-            roof = {"bound": "hbm", "kernel": name, "achieved": ach, "peak": peak, "unit": "GB/s",
-                    "frac": ach / peak, "traffic": None, "launches": cnt, "avg_launch_us": ns / cnt / 1e3,
-                    "peak_source": peak_src, "share_of_step": ns / max(1.0, sum(v[1] for v in kprof.values()))}
-            break
+    roof = roofline_for(kprof, records, peak, peak_src, lambda nm: True)
+    roof_sym = roofline_for(kprof, records, peak, peak_src, lambda nm: nm.startswith(SYMBOLIC))
+    traffic = _traffic_from_profiles()
+    for rf in (roof, roof_sym):
+        if rf and rf.get("kernel") in traffic:
+            rf["traffic"] = traffic[rf["kernel"]]
     # symbolic (FBSP) effective roofline, B_sym per SURVEY.md §8(d)
     W = ring.n_key_words
     B_sym = sum(b["M"] * (8 * W + 4) + 8 * b["M"] + 4 * (b["r"] + 1) + b["N"] * 8 * W for b in batches)
@@ -369,7 +413,8 @@ def main():
                        "l2": "flushed (256 MiB write) before every batch"},
             "reduction_s_per_f4_step": red_s,
             "symbolic_roofline": {"B_sym_bytes_per_step": B_sym, "frac": sym_frac, "peak": peak},
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
+            "roofline": roof, "roofline_symbolic": roof_sym, "cpu_baseline": cpu, "e2e": e2e,
+            "clocks": clk.summary(),
             "gpu_launches": launches1 - launches0, "wall_ms_per_step": 1000 * wall / args.steps,
             "setup_s": round(setup_s, 2), "kernels_top": kernels,
         }

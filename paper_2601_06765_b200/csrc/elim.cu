@@ -26,6 +26,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -169,7 +170,8 @@ F4B_DEV u32 block_scan_flag(u32 f, u32* red, u32* tot) {
 }
 
 // Write the nonzeros of acc[lo, hi) (ascending) to the output pool.
-F4B_DEV void emit_row(const u32* acc, u32 lo, u32 hi, const u32* __restrict__ colmap, u32* __restrict__ pcol,
+template <typename T>
+F4B_DEV void emit_row(const T* acc, u32 lo, u32 hi, const u32* __restrict__ colmap, u32* __restrict__ pcol,
                       u32* __restrict__ pval, size_t cap, unsigned long long* cursor, u32* slot_off, u32* slot_len,
                       u32* err, u32* red, u32* sh) {
   u32 cnt = 0;
@@ -208,24 +210,32 @@ F4B_DEV void emit_row(const u32* acc, u32 lo, u32 hi, const u32* __restrict__ co
 // ---------------------------------------------------------------------------
 // MODE 0: C rows  -> write the non-A part densely into Dp[slot][K]
 // MODE 1: A rows  -> sweep right of the lead, reduce by RREF(D'), make monic, emit
-template <int MODE>
+// T: accumulator lane type (u16 when p < 2^16: half the shared memory, so
+// more rows in flight and more L1 left for descriptor / pivot-row hits).
+//
+// One barrier per pivot: every warp scans for the next pivot itself (same
+// data -> same answer) and takes the multiplier from its own ballot.  The
+// scan reads columns >= cur only, while the update of pivot c writes
+// columns > c only, so a warp still scanning can never see a different
+// pivot; acc[c] is zeroed after the barrier, when no scan reads it.
+template <int MODE, typename T>
 __global__ void __launch_bounds__(SW_THREADS) k_sweep(
     Fp fp, const u32* __restrict__ rp, const u32* __restrict__ col, const u32* __restrict__ val, u32 N,
     const u32* __restrict__ rows, u32 nrows, const uint4* __restrict__ desc, const u32* __restrict__ invl,
-    const u32* __restrict__ abits_g, u32* __restrict__ gacc, u32* __restrict__ Dp, u32 K,
+    const u32* __restrict__ abits_g, T* __restrict__ gacc, u32* __restrict__ Dp, u32 K,
     const u32* __restrict__ nonA, const u32* __restrict__ Rd, u32 rankD, const u32* __restrict__ dpiv,
     u32* __restrict__ pcol, u32* __restrict__ pval, size_t cap, unsigned long long* cursor,
     u32* __restrict__ s_off, u32* __restrict__ s_len, u32* __restrict__ err) {
   extern __shared__ u32 smem[];
   const u32 nwords = (N + 31) / 32;
   u32* abits = smem;
-  u32* acc = gacc ? gacc + (size_t)blockIdx.x * N : smem + nwords;
+  T* acc = gacc ? gacc + (size_t)blockIdx.x * N : reinterpret_cast<T*>(smem + nwords);
   __shared__ u32 red[33];
   __shared__ u32 sh[4];
   __shared__ u32 coef_n;
   __shared__ u32 coef_k[256];
   __shared__ u32 coef_v[256];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31;
   for (u32 w = tid; w < nwords; w += blockDim.x) abits[w] = abits_g[w];
   __syncthreads();
   for (u32 rr = blockIdx.x; rr < nrows; rr += gridDim.x) {
@@ -234,42 +244,49 @@ __global__ void __launch_bounds__(SW_THREADS) k_sweep(
     const u32 lead = col[s];
     for (u32 c = lead + tid; c < N; c += blockDim.x) acc[c] = 0;
     __syncthreads();
-    for (u32 k = s + tid; k < e; k += blockDim.x) acc[col[k]] = val[k];
+    for (u32 k = s + tid; k < e; k += blockDim.x) acc[col[k]] = (T)val[k];
     __syncthreads();
-    u32 cur = MODE == 1 ? lead + 1 : lead;
-    while (true) {
-      if (warp == 0) {
-        u32 found = N;
-        for (u32 c0 = cur & ~31u; c0 < N; c0 += 32) {
-          u32 c = c0 + lane;
-          bool hit = c >= cur && c < N && acc[c] != 0 && ((abits[c >> 5] >> (c & 31)) & 1u);
-          unsigned b = __ballot_sync(0xffffffffu, hit);
-          if (b) {
-            found = c0 + __ffs(b) - 1;
-            break;
-          }
+    // per-warp scan: next pivot column >= from, and acc at it (warp-uniform)
+    auto scan = [&](u32 from, u32& value) -> u32 {
+      for (u32 c0 = from & ~31u; c0 < N; c0 += 32) {
+        const u32 cc = c0 + lane;
+        const u32 v = (cc >= from && cc < N) ? (u32)acc[cc] : 0u;
+        const bool hit = v != 0 && ((abits[cc >> 5] >> (cc & 31)) & 1u);
+        const unsigned b = __ballot_sync(0xffffffffu, hit);
+        if (b) {
+          const int src = __ffs(b) - 1;
+          value = __shfl_sync(0xffffffffu, v, src);
+          return c0 + src;
         }
-        if (lane == 0) sh[0] = found;
       }
-      __syncthreads();
-      const u32 c = sh[0];
-      if (c >= N) break;
+      return N;
+    };
+    u32 av = 0;
+    u32 c = scan(MODE == 1 ? lead + 1 : lead, av);
+    while (c < N) {
       const uint4 d = __ldg(desc + c);
-      const u32 fm = fp.to_mont(fp.neg(fp.mul(acc[c], d.z)));
-      const u32 js = d.x, je = d.y;
-      for (u32 k = js + tid; k < je; k += blockDim.x) {
-        const u32 cc = col[k];
-        acc[cc] = fp.add(acc[cc], fp.mont_mul(fm, __ldg(val + k)));
+      const u32 fm = fp.to_mont(fp.neg(fp.mul(av, d.z)));
+      u32 k = d.x + tid;
+      for (; k + blockDim.x < d.y; k += 2 * blockDim.x) {
+        const u32 c0 = __ldg(col + k), c1 = __ldg(col + k + blockDim.x);
+        const u32 v0 = __ldg(val + k), v1 = __ldg(val + k + blockDim.x);
+        acc[c0] = (T)fp.add((u32)acc[c0], fp.mont_mul(fm, v0));
+        acc[c1] = (T)fp.add((u32)acc[c1], fp.mont_mul(fm, v1));
       }
-      if (tid == 0) acc[c] = 0;
+      if (k < d.y) {
+        const u32 cc = __ldg(col + k);
+        acc[cc] = (T)fp.add((u32)acc[cc], fp.mont_mul(fm, __ldg(val + k)));
+      }
       __syncthreads();
-      cur = c + 1;
+      if (tid == 0) acc[c] = 0;
+      c = scan(c + 1, av);
     }
+    __syncthreads();
     if (MODE == 0) {
       u32* out = Dp + (size_t)rr * K;
       for (u32 q = tid; q < K; q += blockDim.x) {
         const u32 cc = nonA[q];
-        out[q] = cc >= lead ? acc[cc] : 0u;
+        out[q] = cc >= lead ? (u32)acc[cc] : 0u;
       }
       __syncthreads();
     } else {
@@ -279,7 +296,7 @@ __global__ void __launch_bounds__(SW_THREADS) k_sweep(
         __syncthreads();
         for (u32 k = k0 + tid; k < min(rankD, k0 + 256); k += blockDim.x) {
           const u32 cc = nonA[dpiv[k]];
-          const u32 v = cc > lead ? acc[cc] : 0u;
+          const u32 v = cc > lead ? (u32)acc[cc] : 0u;
           if (v) {
             u32 slot = atomicAdd(&coef_n, 1u);
             coef_k[slot] = k;
@@ -292,21 +309,21 @@ __global__ void __launch_bounds__(SW_THREADS) k_sweep(
           for (u32 q = tid; q < K; q += blockDim.x) {
             const u32 cc = nonA[q];
             if (cc <= lead) continue;
-            u32 a = acc[cc];
+            u32 a = (u32)acc[cc];
             for (u32 t = 0; t < nco; ++t) a = fp.add(a, fp.mont_mul(coef_v[t], __ldg(Rd + (size_t)coef_k[t] * K + q)));
-            acc[cc] = a;
+            acc[cc] = (T)a;
           }
         }
         __syncthreads();
       }
       // monic: the lead coefficient is untouched by the sweep
       const u32 inv = invl[lead];
-      for (u32 c = lead + tid; c < N; c += blockDim.x) {
-        u32 v = acc[c];
-        if (v) acc[c] = fp.mul(v, inv);
+      for (u32 c2 = lead + tid; c2 < N; c2 += blockDim.x) {
+        const u32 v = (u32)acc[c2];
+        if (v) acc[c2] = (T)fp.mul(v, inv);
       }
       __syncthreads();
-      emit_row(acc, lead, N, nullptr, pcol, pval, cap, cursor, s_off + rr, s_len + rr, err, red, sh + 1);
+      emit_row<T>(acc, lead, N, nullptr, pcol, pval, cap, cursor, s_off + rr, s_len + rr, err, red, sh + 1);
       __syncthreads();
     }
   }
@@ -320,6 +337,26 @@ __global__ void __launch_bounds__(SW_THREADS) k_sweep(
 // (lead << 32 | row), published with one 64-bit atomicMin per CTA.  Pivot
 // rows are frozen once chosen, so other CTAs read them without a second
 // barrier.  Grid barriers = rank(D') + 1.
+// row[q] += fm * prow[q] for q = q0, q0+32, ... < K — 8 independent L2 loads in
+// flight per lane (the pivot row lives in L2; the un-pipelined loop was
+// latency bound).
+__device__ __forceinline__ void row_axpy8(const Fp& fp, u32* row, const u32* prow, u32 fm, u32 q0, u32 K) {
+  for (u32 qb = q0; qb < K; qb += 32 * 8) {
+    u32 pv[8], rv[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const u32 q = qb + 32 * j;
+      pv[j] = q < K ? __ldcg(prow + q) : 0u;
+      rv[j] = q < K ? row[q] : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const u32 q = qb + 32 * j;
+      if (q < K) row[q] = fp.add(rv[j], fp.mont_mul(fm, pv[j]));
+    }
+  }
+}
+
 __device__ __forceinline__ u32 first_nonzero_warp(const u32* row, u32 from, u32 K) {
   const int lane = threadIdx.x & 31;
   for (u32 b0 = from & ~31u; b0 < K; b0 += 32) {
@@ -378,13 +415,76 @@ __global__ void __launch_bounds__(256) k_dense_forward(Fp fp, u32* Dp, u32 R, u3
       if (used[i] || lead[i] != c) continue;
       u32* row = Dp + (size_t)i * K;
       const u32 fm = fp.to_mont(fp.neg(fp.mul(row[c], inv)));
-      for (u32 q = c + lane; q < K; q += 32) row[q] = fp.add(row[q], fp.mont_mul(fm, __ldcg(prow_p + q)));
+      row_axpy8(fp, row, prow_p, fm, c + lane, K);
       __syncwarp();
       const u32 l = first_nonzero_warp(row, c + 1, K);
       if (lane == 0) lead[i] = l;
     }
     __syncthreads();
   }
+}
+
+// E3a' (small D'): the same pivot-to-pivot elimination inside ONE thread-block
+// cluster: candidates are exchanged through distributed shared memory and the
+// per-pivot barrier is a cluster barrier (hardware, ~sub-µs) instead of a
+// grid-wide one.  Slots are double-buffered by step parity, so one barrier
+// per pivot suffices; pivot rows are frozen, read with ld.global.cg.
+__global__ void __launch_bounds__(1024) k_dense_forward_cluster(Fp fp, u32* Dp, u32 R, u32 K, u32* lead,
+                                                               uint8_t* used, u32* piv_of_col) {
+  cg::cluster_group cl = cg::this_cluster();
+  __shared__ unsigned long long slot[2];
+  __shared__ unsigned long long wmin[32];
+  __shared__ u32 s_inv;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const u32 cs = cl.num_blocks(), me = cl.block_rank();
+  const u32 lo = (u32)(((unsigned long long)R * me) / cs);
+  const u32 hi = (u32)(((unsigned long long)R * (me + 1)) / cs);
+  for (u32 i = lo + warp; i < hi; i += nwarps) {
+    const u32 l = first_nonzero_warp(Dp + (size_t)i * K, 0, K);
+    if (lane == 0) lead[i] = l;
+  }
+  __syncthreads();
+  for (u32 step = 0;; ++step) {
+    const int par = step & 1;
+    unsigned long long m = ~0ull;
+    for (u32 i = lo + tid; i < hi; i += blockDim.x)
+      if (!used[i] && lead[i] < K) m = min(m, ((unsigned long long)lead[i] << 32) | i);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) wmin[warp] = m;
+    __syncthreads();
+    if (tid == 0) {
+      unsigned long long mm = ~0ull;
+      for (int w = 0; w < nwarps; ++w) mm = min(mm, wmin[w]);
+      slot[par] = mm;
+    }
+    cl.sync();
+    unsigned long long win = ~0ull;
+    for (u32 rk = 0; rk < cs; ++rk) win = min(win, *cl.map_shared_rank(&slot[par], rk));
+    if (win == ~0ull) break;
+    const u32 c = (u32)(win >> 32), pr = (u32)(win & 0xFFFFFFFFull);
+    const u32* prow_p = Dp + (size_t)pr * K;
+    if (tid == 0) {
+      s_inv = fp.inv(__ldcg(prow_p + c));
+      if (pr >= lo && pr < hi) {
+        used[pr] = 1;
+        piv_of_col[c] = pr;
+      }
+    }
+    __syncthreads();
+    const u32 inv = s_inv;
+    for (u32 i = lo + warp; i < hi; i += nwarps) {
+      if (used[i] || lead[i] != c) continue;
+      u32* row = Dp + (size_t)i * K;
+      const u32 fm = fp.to_mont(fp.neg(fp.mul(row[c], inv)));
+      row_axpy8(fp, row, prow_p, fm, c + lane, K);
+      __syncwarp();
+      const u32 l = first_nonzero_warp(row, c + 1, K);
+      if (lane == 0) lead[i] = l;
+    }
+    __syncthreads();
+  }
+  cl.sync();  // keep every CTA's shared slots alive until all have read them
 }
 
 // E3b: back-substitution -> RREF(D') rows (dense), one CTA per pivot.
@@ -485,15 +585,48 @@ static Fp make_fp(Ctx* c) {
   return fp;
 }
 
-static size_t sweep_smem(u32 N, bool& global_acc) {
-  size_t need = (size_t)((N + 31) / 32) * 4 + (size_t)N * 4;
-  global_acc = need > 200 * 1024;
-  return global_acc ? (size_t)((N + 31) / 32) * 4 : need;
-}
-
 static int sweep_grid(Ctx* c, size_t smem, long long rows) {
   int per_sm = (int)std::max<size_t>(1, std::min<size_t>(8, (220 * 1024) / std::max<size_t>(smem + 3072, 1)));
   return (int)std::max<long long>(1, std::min<long long>(rows, (long long)c->num_sms * per_sm));
+}
+
+// k_sweep<MODE, T>: u16 accumulators when p < 2^16 and the row fits shared
+// memory, u32 in shared memory otherwise, u32 in HBM for very wide matrices.
+template <int MODE>
+static void launch_sweep(Ctx* c, const Fp& fp, f4b_echelon* E, const u32* rows, u32 nrows, u32* Dp, u32 K,
+                         const u32* Rd, u32 rankD, const u32* dpiv, u32* pcol, u32* pval, size_t cap,
+                         unsigned long long* cursor, u32* s_off, u32* s_len, u32* err) {
+  const u32 N = (u32)E->n_cols;
+  const size_t bitmap = (size_t)((N + 31) / 32) * 4;
+  const bool small_p = c->p < 65536u;
+  const size_t acc_b = (((size_t)N * (small_p ? 2 : 4)) + 15) & ~(size_t)15;
+  const bool gl = bitmap + acc_b > 200 * 1024;
+  const size_t smem = gl ? bitmap : bitmap + acc_b;
+  const int grid = sweep_grid(c, smem, nrows);
+  static bool attr = false;
+  if (!attr) {
+    check_cuda(cudaFuncSetAttribute(k_sweep<MODE, u32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 4096),
+               "attr");
+    check_cuda(cudaFuncSetAttribute(k_sweep<MODE, uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    200 * 1024 + 4096), "attr");
+    attr = true;
+  }
+  if (gl) {
+    DBuf gacc;
+    ensure(c, gacc, (size_t)grid * N * sizeof(u32));
+    F4B_LAUNCH(c, (k_sweep<MODE, u32>), grid, SW_THREADS, smem, fp, E->rp, E->col, E->val, N, rows, nrows,
+               E->desc.as<uint4>(), E->invl.as<u32>(), E->abits.as<u32>(), gacc.as<u32>(), Dp, K, E->nonA.as<u32>(),
+               Rd, rankD, dpiv, pcol, pval, cap, cursor, s_off, s_len, err);
+    release(c, gacc);
+  } else if (small_p) {
+    F4B_LAUNCH(c, (k_sweep<MODE, uint16_t>), grid, SW_THREADS, smem, fp, E->rp, E->col, E->val, N, rows, nrows,
+               E->desc.as<uint4>(), E->invl.as<u32>(), E->abits.as<u32>(), (uint16_t*)nullptr, Dp, K,
+               E->nonA.as<u32>(), Rd, rankD, dpiv, pcol, pval, cap, cursor, s_off, s_len, err);
+  } else {
+    F4B_LAUNCH(c, (k_sweep<MODE, u32>), grid, SW_THREADS, smem, fp, E->rp, E->col, E->val, N, rows, nrows,
+               E->desc.as<uint4>(), E->invl.as<u32>(), E->abits.as<u32>(), (u32*)nullptr, Dp, K, E->nonA.as<u32>(),
+               Rd, rankD, dpiv, pcol, pval, cap, cursor, s_off, s_len, err);
+  }
 }
 
 static void run_a_sweep(Ctx* c, f4b_echelon* E);
@@ -567,21 +700,8 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
   E->rankD = 0;
   if (R > 0 && K > 0) {
     ensure(c, Dp, (size_t)R * K * sizeof(u32));
-    bool gl = false;
-    size_t smem = sweep_smem((u32)N, gl);
-    int grid = sweep_grid(c, smem, R);
-    if (gl) ensure(c, gacc, (size_t)grid * N * sizeof(u32));
-    static bool attr0 = false;
-    if (!attr0) {
-      check_cuda(cudaFuncSetAttribute(k_sweep<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 4096), "attr");
-      attr0 = true;
-    }
-    F4B_LAUNCH(c, k_sweep<0>, grid, SW_THREADS, smem, 
-        fp, E->rp, E->col, E->val, (u32)N, crows.as<u32>(), (u32)R, E->desc.as<uint4>(), E->invl.as<u32>(),
-        E->abits.as<u32>(), gl ? gacc.as<u32>() : nullptr, Dp.as<u32>(), (u32)K, E->nonA.as<u32>(), nullptr, 0, nullptr,
-        nullptr, nullptr, 0, nullptr, nullptr, nullptr, err);
-    check_cuda(cudaGetLastError(), "k_sweep<0>");
-    release(c, gacc);
+    launch_sweep<0>(c, fp, E, crows.as<u32>(), (u32)R, Dp.as<u32>(), (u32)K, nullptr, 0, nullptr, nullptr, nullptr, 0,
+                    nullptr, nullptr, nullptr, err);
     // E3a: cooperative forward elimination
     ensure(c, used, (size_t)R + 16);
     ensure(c, pofc, (size_t)K * sizeof(u32));
@@ -600,7 +720,42 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
     uint8_t* usedp = used.as<uint8_t>();
     u32* pofcp = pofc.as<u32>();
     void* args[] = {&fp, &dpp, &Ru, &Ku, &candp, &leadp, &usedp, &pofcp};
-    {
+    // Grid-wide cooperative kernel by default.  The 16-CTA cluster variant
+    // (F4B_DENSE_CLUSTER=1) has cheaper barriers but measured slower on the
+    // cyclic-8 batches (profiles/r01/NOTES.md): per-pivot work, not the
+    // barrier, dominates once the loads are pipelined.
+    bool done_cluster = false;
+    if (R <= 16384 && (long long)R * K <= (64ll << 20) && getenv("F4B_DENSE_CLUSTER")) {
+      static int cl_ok = -1;
+      if (cl_ok < 0) {
+        cl_ok = cudaFuncSetAttribute(k_dense_forward_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+                cudaSuccess;
+        cudaGetLastError();
+      }
+      for (int csz : {16, 8}) {
+        if (csz == 16 && !cl_ok) continue;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(csz);
+        cfg.blockDim = dim3(1024);
+        cfg.dynamicSmemBytes = 0;
+        cfg.stream = c->stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = csz;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        ProfScope ps(c, "k_dense_forward");
+        cudaError_t e = cudaLaunchKernelEx(&cfg, k_dense_forward_cluster, fp, dpp, Ru, Ku, leadp, usedp, pofcp);
+        if (e == cudaSuccess) {
+          done_cluster = true;
+          break;
+        }
+        cudaGetLastError();
+      }
+    }
+    if (!done_cluster) {
       ProfScope ps(c, "k_dense_forward");
       check_cuda(cudaLaunchCooperativeKernel((void*)k_dense_forward, G, 256, args, 0, c->stream), "k_dense_forward");
     }
@@ -712,15 +867,6 @@ static void run_a_sweep(Ctx* c, f4b_echelon* E) {
     std::vector<u32> h_arows(nA);
     for (long long k = 0; k < nA; ++k) h_arows[k] = h_prow[h_acols[k]];
     check_cuda(cudaMemcpyAsync(arows.p, h_arows.data(), nA * sizeof(u32), cudaMemcpyHostToDevice, c->stream), "h2d");
-    bool gl = false;
-    size_t smem = sweep_smem((u32)N, gl);
-    int grid = sweep_grid(c, smem, nA);
-    if (gl) ensure(c, gacc, (size_t)grid * N * sizeof(u32));
-    static bool attr = false;
-    if (!attr) {
-      check_cuda(cudaFuncSetAttribute(k_sweep<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 4096), "attr");
-      attr = true;
-    }
     size_t base_used = (size_t)E->nonpivot_nnz;
     for (int attempt = 0; attempt < 8; ++attempt) {
       size_t need = base_used + (size_t)std::max<long long>(2 * E->M, 1 << 20);
@@ -733,13 +879,10 @@ static void run_a_sweep(Ctx* c, f4b_echelon* E) {
       unsigned long long cur = base_used;
       check_cuda(cudaMemcpyAsync(E->cursor.p, &cur, 8, cudaMemcpyHostToDevice, c->stream), "h2d");
       check_cuda(cudaMemsetAsync(err, 0, 4, c->stream), "memset");
-      F4B_LAUNCH(c, k_sweep<1>, grid, SW_THREADS, smem, 
-          fp, E->rp, E->col, E->val, (u32)N, arows.as<u32>(), (u32)nA, E->desc.as<uint4>(), E->invl.as<u32>(),
-          E->abits.as<u32>(), gl ? gacc.as<u32>() : nullptr, nullptr, (u32)K, E->nonA.as<u32>(),
-          E->rankD ? E->Rd.as<u32>() : nullptr, (u32)E->rankD, E->rankD ? E->dpiv.as<u32>() : nullptr,
-          E->pool_col.as<u32>(), E->pool_val.as<u32>(), E->pool_cap, E->cursor.as<unsigned long long>(),
-          E->a_off.as<u32>(), E->a_len.as<u32>(), err);
-      check_cuda(cudaGetLastError(), "k_sweep<1>");
+      launch_sweep<1>(c, fp, E, arows.as<u32>(), (u32)nA, nullptr, (u32)K, E->rankD ? E->Rd.as<u32>() : nullptr,
+                      (u32)E->rankD, E->rankD ? E->dpiv.as<u32>() : nullptr, E->pool_col.as<u32>(),
+                      E->pool_val.as<u32>(), E->pool_cap, E->cursor.as<unsigned long long>(), E->a_off.as<u32>(),
+                      E->a_len.as<u32>(), err);
       u32 e = read_u32(c, err);
       if (!(e & DEVERR_CAPACITY)) break;
       unsigned long long tot = 0;
