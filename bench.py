@@ -173,28 +173,41 @@ def capture_workload():
 
 
 class ClockSampler:
+    """nvidia-smi sampling (100 ms) started before the timed region; only the
+    samples whose timestamps fall inside [t_begin, t_end] are summarised."""
+
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
     def __init__(self, device):
         self.device = device
         self.proc = None
         self.path = None
+        self.t_begin = self.t_end = None
 
-    def __enter__(self):
+    def start(self):
         fd, self.path = tempfile.mkstemp(suffix=".csv")
         os.close(fd)
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device),
-                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
+        time.sleep(1.0)  # nvidia-smi needs a moment before its first sample
         return self
 
-    def __exit__(self, *exc):
+    def begin(self):
+        self.t_begin = time.time()
+
+    def end(self):
+        self.t_end = time.time()
+
+    def stop(self):
         if self.proc is not None:
+            time.sleep(0.25)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
@@ -202,23 +215,37 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
+        import datetime
+
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        sm, mx, reasons = [], [], set()
+        rows = []
         try:
             for line in open(self.path):
                 parts = [x.strip() for x in line.split(",")]
-                if len(parts) < 7:
+                if len(parts) < 8:
                     continue
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
-                for nm, flag in zip(names, parts[3:7]):
-                    if flag.lower().startswith("active"):
-                        reasons.add(nm)
+                try:
+                    ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                except ValueError:
+                    continue
+                rows.append((ts, float(parts[1]), float(parts[2]), parts[4:8]))
             os.unlink(self.path)
         except Exception:
             pass
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        inside = [r for r in rows if self.t_begin is not None and self.t_begin - 0.05 <= r[0] <= self.t_end + 0.05]
+        note = "samples inside the timed region"
+        if not inside and rows and self.t_begin is not None:
+            # timed region shorter than the sampling period: nearest samples
+            inside = sorted(rows, key=lambda r: abs(r[0] - 0.5 * (self.t_begin + self.t_end)))[:2]
+            note = "timed region shorter than the sampling period: nearest samples"
+        reasons = set()
+        for r in inside:
+            for nm, flag in zip(names, r[3]):
+                if flag.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median([r[1] for r in inside]) if inside else None,
+                "sm_max_mhz": max(r[2] for r in inside) if inside else None, "reasons": sorted(reasons),
+                "samples": len(inside), "note": note}
 
 
 # Algorithmic (compulsory) bytes per kernel per batch — DESIGN.md §4.
@@ -274,7 +301,7 @@ def roofline_for(kprof, records, peak, peak_src, want):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -316,6 +343,7 @@ def main():
                 record.append((b, plan.info, inf))
         return ts, tn
 
+    clk = ClockSampler(local).start()
     for _ in range(args.warmup):
         replay_step(None)
     # timed region
@@ -325,15 +353,17 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        w0 = time.perf_counter()
-        t_sym = t_num = 0
-        for _ in range(args.steps):
-            a, c = replay_step(records)
-            t_sym += a
-            t_num += c
-        torch.cuda.synchronize()
-        wall = time.perf_counter() - w0
+    clk.begin()
+    w0 = time.perf_counter()
+    t_sym = t_num = 0
+    for _ in range(args.steps):
+        a, c = replay_step(records)
+        t_sym += a
+        t_num += c
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - w0
+    clk.end()
+    clk.stop()
     if world > 1:
         dist.barrier()
     kprof, launches1 = eng.profile_read()

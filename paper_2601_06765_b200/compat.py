@@ -1,0 +1,45 @@
+"""Drop-in shim for an existing `fpgb` installation (SURVEY.md §8b option ii).
+
+    import fpgb
+    from paper_2601_06765_b200 import compat
+    compat.install(fpgb)          # fpgb.groebner now runs the hot path on the GPU
+
+`f4_step` (reference groebner.py:253-311) resolves `compile_batch`,
+`csr_from_plan` and `psge_reduce` from the `fpgb.groebner` module namespace
+(imported at groebner.py:32-50), so rebinding those three names routes every
+F4 step of `f4_groebner`, `run_pipeline` and `verify_instance` through the
+CUDA engine.  The GPU functions accept the reference's own objects by duck
+typing (rows with .shift/.basis_index/.role/.provenance, a SoaPolySet with
+.ring/.exps/.coeff/.length/.offset) and return objects with the attributes
+the reference reads (LayoutPlan .counters/.timings_ns/.dict_keys/.row_meta,
+EchelonResult .nonpivot_rows/.pivot_rows/.rank/.zero_row_count/
+.fill_generated).  `uninstall(fpgb)` restores the originals.
+"""
+
+from __future__ import annotations
+
+from . import sparselin, symbolic
+
+_SAVED: dict = {}
+PATCHED = ("compile_batch", "csr_from_plan", "psge_reduce")
+
+
+def _ring_adapter(ring):
+    """The device engine only needs p, n_vars, order and the key width."""
+    return ring
+
+
+def install(fpgb_pkg) -> None:
+    g = fpgb_pkg.groebner
+    for name in PATCHED:
+        _SAVED.setdefault(name, getattr(g, name))
+    g.compile_batch = symbolic.compile_batch
+    g.csr_from_plan = sparselin.csr_from_plan
+    g.psge_reduce = sparselin.psge_reduce
+
+
+def uninstall(fpgb_pkg) -> None:
+    g = fpgb_pkg.groebner
+    for name, fn in _SAVED.items():
+        setattr(g, name, fn)
+    _SAVED.clear()

@@ -229,7 +229,9 @@ def compile_batch(rows, basis: SoaPolySet, closure: Closure = Closure.ONE_STEP_R
     if rb.min() < 0 or rb.max() >= len(basis):
         raise IndexError("row references a basis index out of range")
     sh = np.asarray([r.shift for r in rows], dtype=np.int64).reshape(len(rows), n)
-    dev = eng.compile(rb, sh, closure is Closure.ONE_STEP_REDUCTION,
+    # compare by value: callers may pass the reference's own Closure enum
+    one_step = getattr(closure, "value", closure) == Closure.ONE_STEP_REDUCTION.value
+    dev = eng.compile(rb, sh, one_step,
                       None if candidates is None else list(candidates), DICT_CAP)
     info = dev.info
     M = info["M"]

@@ -184,3 +184,19 @@ def test_host_f4_loop_with_oracle_matches_reference(name, gen, args):
     ring, polys = gen(*args)
     gb = _f4_with_oracle(ring, polys)
     assert hashlib.sha256(format_system(ring, gb).encode()).hexdigest() == load_golden(name)["final_sha256"]
+
+
+def test_compat_shim_rebinds_reference_names():
+    """compat.install rebinds fpgb.groebner's hot-path names (uses a stand-in
+    module object: the reference itself is not needed)."""
+    import types
+
+    from paper_2601_06765_b200 import compat, sparselin, symbolic
+
+    g = types.SimpleNamespace(compile_batch=1, csr_from_plan=2, psge_reduce=3)
+    fake = types.SimpleNamespace(groebner=g)
+    compat.install(fake)
+    assert g.compile_batch is symbolic.compile_batch and g.psge_reduce is sparselin.psge_reduce
+    assert g.csr_from_plan is sparselin.csr_from_plan
+    compat.uninstall(fake)
+    assert (g.compile_batch, g.csr_from_plan, g.psge_reduce) == (1, 2, 3)
