@@ -953,6 +953,190 @@ __global__ void __launch_bounds__(256) k_rank_unrank(KeyFmt f, const u32* __rest
   }
 }
 
+// Fused round tail: OR the fill partials (mode 0: dict = OR, frontier = dict &
+// ~done; mode 1: frontier = OR & ~dict, dict |= OR), then emit the frontier
+// monomials in ascending rank order (look-back over word tiles) as device
+// keys, unranked cooperatively by the whole CTA.  Replaces reduce + extract +
+// unrank (three launches) per round.
+static constexpr int RX_WPT = 4;
+static constexpr int RX_LIST = 4096;
+template <int KW>
+__global__ void __launch_bounds__(256) k_rank_round(KeyFmt f, const u32* __restrict__ partial, int nparts, u32 words,
+                                                    int mode, u32* __restrict__ dict, const u32* __restrict__ done,
+                                                    const u32* __restrict__ bt_g, int st, int bt_words, int D,
+                                                    u64* __restrict__ front, u32* status, u32* ticket, u32* d_nf,
+                                                    u32* d_ndict) {
+  extern __shared__ __align__(16) u32 rsm[];
+  u32* bt = rsm;
+  u32* list = rsm + bt_words;
+  __shared__ u32 ws[33];
+  __shared__ u32 s_tile, s_base;
+  for (int i = threadIdx.x; i < bt_words; i += blockDim.x) bt[i] = bt_g[i];
+  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const u32 tile = s_tile;
+  const u32 ntiles = (words + 256 * RX_WPT - 1) / (256 * RX_WPT);
+  if (tile >= ntiles) return;
+  const u32 w0 = tile * 256 * RX_WPT + threadIdx.x * RX_WPT;
+  u32 x[RX_WPT];
+  u32 cnt = 0, dcnt = 0;
+#pragma unroll
+  for (int q = 0; q < RX_WPT; ++q) {
+    const u32 w = w0 + q;
+    x[q] = 0;
+    if (w < words) {
+      u32 v = 0;
+      for (int pp = 0; pp < nparts; ++pp) v |= partial[(size_t)pp * words + w];
+      if (mode == 0) {
+        dict[w] = v;
+        dcnt += __popc(v);
+        x[q] = v & ~done[w];
+      } else {
+        const u32 old = dict[w];
+        x[q] = v & ~old;
+        dict[w] = old | v;
+        dcnt += __popc(x[q]);
+      }
+      cnt += __popc(x[q]);
+    }
+  }
+  u32 tot, dtot;
+  const u32 pre = block_scan_excl(cnt, ws, &tot);
+  block_scan_excl(dcnt, ws, &dtot);
+  if (threadIdx.x == 0) {
+    s_base = lookback_prefix(status, tile, tot);
+    if (dtot) atomicAdd(d_ndict, dtot);
+  }
+  __syncthreads();
+  const u32 base = s_base;
+  // unrank the tile's frontier monomials: ranks staged in shared memory
+  for (u32 done_cnt = 0; done_cnt < tot; done_cnt += RX_LIST) {
+    u32 p = pre;
+#pragma unroll
+    for (int q = 0; q < RX_WPT; ++q) {
+      u32 m = x[q];
+      while (m) {
+        const int bit = __ffs(m) - 1;
+        m &= m - 1;
+        if (p >= done_cnt && p < done_cnt + RX_LIST) list[p - done_cnt] = (w0 + q) * 32 + bit;
+        ++p;
+      }
+    }
+    __syncthreads();
+    const u32 chunk = min((u32)RX_LIST, tot - done_cnt);
+    for (u32 j = threadIdx.x; j < chunk; j += blockDim.x) {
+      u16 e[MAXV];
+      unrank_exps(list[j], f.n_vars, D, bt, st, e);
+      key_store<KW>(front, (long long)base + done_cnt + j, key_encode<KW>(f, e));
+    }
+    __syncthreads();
+  }
+  if (tile == ntiles - 1 && threadIdx.x == 0) *d_nf = base + tot;
+}
+
+// Fused closure round: first LM divisor per frontier monomial (warp per
+// monomial, SWAR u16x2 over the shared-memory LM table) and compaction of the
+// reducer rows in ascending key(m) with their row offsets (two look-backs).
+static constexpr int CR_TILE = 64;
+template <int KW>
+__global__ void __launch_bounds__(256) k_closure_rows(KeyFmt f, const u64* __restrict__ front,
+                                                      const u32* __restrict__ d_nf, const u32* lmw_g,
+                                                      const int* __restrict__ cidx, int nc, int nw, int stage_lm,
+                                                      long long row_base, long long cl_base, u32 M_base,
+                                                      const u32* __restrict__ boff, const u32* __restrict__ blen,
+                                                      const u64* __restrict__ bckey, const u16* __restrict__ lmexp,
+                                                      const u16* __restrict__ maxe, int round,
+                                                      int* __restrict__ rows_basis, u64* __restrict__ rows_delta,
+                                                      u32* __restrict__ rows_start, int* __restrict__ cl_basis,
+                                                      u16* __restrict__ cl_shift, int* __restrict__ cl_round,
+                                                      u32* status_n, u32* status_len, u32* ticket, u32* d_R, u32* d_Mk,
+                                                      u32* err) {
+  extern __shared__ __align__(16) u32 slm[];
+  __shared__ int sred[CR_TILE];
+  __shared__ u32 ws[33];
+  __shared__ u32 s_tile, s_base, s_lbase;
+  const u32* lmw = lmw_g;
+  if (stage_lm) {
+    for (int i = threadIdx.x; i < nc * nw; i += blockDim.x) slm[i] = __ldg(lmw_g + i);
+    lmw = slm;
+  }
+  const u32 nf = *d_nf;
+  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const u32 tile = s_tile;
+  const u32 ntiles = (nf + CR_TILE - 1) / CR_TILE;
+  if (tile >= ntiles) {
+    if (tile == 0 && threadIdx.x == 0) {
+      *d_R = 0;
+      *d_Mk = 0;
+    }
+    return;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int t = warp; t < CR_TILE; t += 8) {
+    const u32 j = tile * CR_TILE + t;
+    int found = -1;
+    if (j < nf) {
+      u16 e[MAXV + 1];
+      key_decode<KW>(f, key_load<KW>(front, j), e);
+      e[f.n_vars] = 0;
+      u32 me[MAXV / 2];
+      for (int w = 0; w < nw; ++w) me[w] = (u32)e[2 * w] | ((u32)e[2 * w + 1] << 16);
+      for (int b0 = 0; b0 < nc; b0 += 32) {
+        const int cc = b0 + lane;
+        bool ok = cc < nc;
+        if (ok) {
+          const u32* lm = lmw + (long long)cc * nw;
+          for (int w = 0; w < nw; ++w) ok &= (__vcmpgeu2(me[w], lm[w]) == 0xFFFFFFFFu);
+        }
+        const unsigned bm = __ballot_sync(0xffffffffu, ok);
+        if (bm) {
+          found = cidx[b0 + __ffs(bm) - 1];
+          break;
+        }
+      }
+    }
+    if (lane == 0) sred[t] = found;
+  }
+  __syncthreads();
+  const int t = threadIdx.x;
+  const u32 j = tile * CR_TILE + t;
+  const int g = (t < CR_TILE && j < nf) ? sred[t] : -1;
+  const u32 len = g >= 0 ? blen[g] : 0u;
+  u32 tot, ltot;
+  const u32 pre = block_scan_excl(g >= 0 ? 1u : 0u, ws, &tot);
+  const u32 lpre = block_scan_excl(len, ws, &ltot);
+  if (threadIdx.x == 0) {
+    s_base = lookback_prefix(status_n, tile, tot);
+    s_lbase = lookback_prefix(status_len, tile, ltot);
+  }
+  __syncthreads();
+  if (g >= 0) {
+    const long long q = (long long)s_base + pre;
+    const long long row = row_base + q;
+    const Key<KW> m = key_load<KW>(front, j);
+    rows_basis[row] = g;
+    key_store<KW>(rows_delta, row, key_sub<KW>(m, key_load<KW>(bckey, boff[g])));
+    rows_start[row] = M_base + s_lbase + lpre;
+    u16 e[MAXV];
+    key_decode<KW>(f, m, e);
+    bool over = false;
+    for (int v = 0; v < f.n_vars; ++v) {
+      const u32 s = (u32)e[v] - (u32)lmexp[(long long)g * f.n_vars + v];
+      over |= (s + (u32)maxe[(long long)g * f.n_vars + v]) > 0xFFFFu;
+      cl_shift[(cl_base + q) * f.n_vars + v] = (u16)s;
+    }
+    if (over) atomicOr(err, (u32)DEVERR_LANE_OVERFLOW);
+    cl_basis[cl_base + q] = g;
+    cl_round[cl_base + q] = round;
+  }
+  if (tile == ntiles - 1 && threadIdx.x == 0) {
+    *d_R = s_base + tot;
+    *d_Mk = s_lbase + ltot;
+    rows_start[row_base + s_base + tot] = M_base + s_lbase + ltot;
+  }
+}
+
 // Join: every term -> rank -> column via the popcount prefix.
 template <int KW>
 __global__ void __launch_bounds__(RK_THREADS) k_rank_join(KeyFmt f, u32 M, u32 r, const int* __restrict__ rb,
@@ -1095,7 +1279,7 @@ static void compile_rank(Ctx* c, const KeyFmt& f, int D, long long r0, const int
   DevCounters* dc = reinterpret_cast<DevCounters*>(c->errflag.p);
   check_cuda(cudaMemsetAsync(dc, 0, sizeof(DevCounters), c->stream), "memset counters");
   // look-back status regions: A/B for k_new_rows (<= N/256 tiles), C for k_rank_extract
-  const size_t lbAB = (size_t)words / 8 + 64, lbC = (size_t)words / 1024 + 64;
+  const size_t lbAB = (size_t)words / 2 + 64, lbC = (size_t)words / 1024 + 64;
   ensure(c, c->dict_b, ((size_t)bt_words + 3 * (size_t)words + 2 * lbAB + lbC + 64) * 4);
   u32* base = c->dict_b.as<u32>();
   u32* d_bt = base;
@@ -1130,6 +1314,8 @@ static void compile_rank(Ctx* c, const KeyFmt& f, int D, long long r0, const int
     check_cuda(cudaFuncSetAttribute(k_rank_join<KW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "attr");
     check_cuda(cudaFuncSetAttribute(k_rank_extract<KW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024),
                "attr");
+    check_cuda(cudaFuncSetAttribute(k_rank_round<KW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024),
+               "attr");
     attr = true;
   }
   auto fill = [&](u32 m_lo, u32 m_hi, u32 m_bound, const u32* d_mk, u32 r_lo, u32 r_hi, const u32* d_r) -> int {
@@ -1157,18 +1343,22 @@ static void compile_rank(Ctx* c, const KeyFmt& f, int D, long long r0, const int
   };
 
   zero_lb();
-  int nparts = fill(0, M0, M0, nullptr, 0, (u32)r0, nullptr);
   check_cuda(cudaMemsetAsync(&dc->N, 0, 4, c->stream), "memset");
-  F4B_LAUNCH(c, k_rank_reduce, nblk(words, 256), 256, 0, c->uniq.as<u32>(), nparts, words, 0, d_dict, nullptr,
-             &dc->N);
+  // leads of the input rows are covered (symbolic.py:339): "done" bitmap
+  check_cuda(cudaMemsetAsync(d_aux, closure ? 0 : 0xFF, (size_t)words * 4, c->stream), "memset done");
+  if (closure)
+    F4B_LAUNCH(c, k_rank_leads<KW>, nblk(r0, 256), 256, 0, f, r0, c->rows_basis.as<int>(), c->rows_delta.as<u64>(),
+               B.off.as<u32>(), B.ckey.as<u64>(), d_bt, st, d_aux);
+  int nparts = fill(0, M0, M0, nullptr, 0, (u32)r0, nullptr);
+  ensure(c, c->front, (size_t)(std::min<unsigned long long>(Rsp, M0) + 1) * KW * sizeof(u64));
+  const size_t rr_smem = ((size_t)bt_words + RX_LIST) * 4;
+  const u32 rr_tiles = std::max<u32>(1, (words + 256 * RX_WPT - 1) / (256 * RX_WPT));
+  // dictionary (= OR of the partials), its size, and the round-1 frontier
+  F4B_LAUNCH(c, k_rank_round<KW>, rr_tiles, 256, rr_smem, f, c->uniq.as<u32>(), nparts, words, 0, d_dict, d_aux, d_bt,
+             st, bt_words, D, c->front.as<u64>(), d_lbC, &dc->tickets[3], &dc->nf, &dc->N);
   long long r = r0, rounds = 0, n_cl = 0, N = 0;
   DevCounters hc;
   if (closure) {
-    check_cuda(cudaMemsetAsync(d_aux, 0, (size_t)words * 4, c->stream), "memset done");
-    F4B_LAUNCH(c, k_rank_leads<KW>, nblk(r0, 256), 256, 0, f, r0, c->rows_basis.as<int>(), c->rows_delta.as<u64>(),
-               B.off.as<u32>(), B.ckey.as<u64>(), d_bt, st, d_aux);
-    ensure(c, c->front, (size_t)(std::min<unsigned long long>(Rsp, M0) + 1) * KW * sizeof(u64));
-    extract(d_dict, d_aux, 0, c->front.as<u64>(), nullptr, 0, &dc->nf);
     // candidate LMs in preference order (key(LM), index) (symbolic.py:228-235)
     std::vector<int32_t> pref(cand);
     std::stable_sort(pref.begin(), pref.end(), [&](int32_t x, int32_t y) {
@@ -1217,18 +1407,16 @@ static void compile_rank(Ctx* c, const KeyFmt& f, int D, long long r0, const int
       ensure(c, c->front_new, (size_t)(std::min<unsigned long long>(Rsp, (unsigned long long)mk_bound) + 1) * KW *
                                   sizeof(u64));
       zero_lb();
-      const size_t lm_smem = (size_t)nc * nw * 4 <= 48 * 1024 ? (size_t)nc * nw * 4 : 0;
-      F4B_LAUNCH(c, k_closure_search<KW>, nblk(nf * 32, 256), 256, lm_smem, f, c->front.as<u64>(), &dc->nf,
-                 c->lmpref.as<u32>(), c->cand_idx.as<int>(), nc, nw, c->red.as<int>());
-      F4B_LAUNCH(c, k_new_rows<KW>, nblk(nf, 256), 256, 0, f, c->front.as<u64>(), c->red.as<int>(), &dc->nf, r, n_cl,
-                 Mcur, B.off.as<u32>(), B.len.as<u32>(), B.ckey.as<u64>(), B.lmexp.as<u16>(), B.maxe.as<u16>(),
-                 (int)rounds + 1, c->rows_basis.as<int>(), c->rows_delta.as<u64>(), c->rows_start.as<u32>(),
-                 c->cl_basis.as<int>(), c->cl_shift.as<u16>(), c->cl_round.as<int>(), d_lbA, d_lbB,
-                 &dc->tickets[2], &dc->R, &dc->Mk, &dc->err);
+      const int stage_lm = (size_t)nc * nw * 4 <= 48 * 1024 ? 1 : 0;
+      F4B_LAUNCH(c, k_closure_rows<KW>, std::max<long long>(1, (nf + CR_TILE - 1) / CR_TILE), 256,
+                 stage_lm ? (size_t)nc * nw * 4 : 0, f, c->front.as<u64>(), &dc->nf, c->lmpref.as<u32>(),
+                 c->cand_idx.as<int>(), nc, nw, stage_lm, r, n_cl, Mcur, B.off.as<u32>(), B.len.as<u32>(),
+                 B.ckey.as<u64>(), B.lmexp.as<u16>(), B.maxe.as<u16>(), (int)rounds + 1, c->rows_basis.as<int>(),
+                 c->rows_delta.as<u64>(), c->rows_start.as<u32>(), c->cl_basis.as<int>(), c->cl_shift.as<u16>(),
+                 c->cl_round.as<int>(), d_lbA, d_lbB, &dc->tickets[2], &dc->R, &dc->Mk, &dc->err);
       nparts = fill(Mcur, 0, (u32)mk_bound, &dc->Mk, (u32)r, 0, &dc->R);
-      F4B_LAUNCH(c, k_rank_reduce, nblk(words, 256), 256, 0, c->uniq.as<u32>(), nparts, words, 1, d_dict, d_aux,
-                 &dc->U);
-      extract(d_aux, nullptr, 0, c->front_new.as<u64>(), nullptr, 0u, &dc->nf);
+      F4B_LAUNCH(c, k_rank_round<KW>, rr_tiles, 256, rr_smem, f, c->uniq.as<u32>(), nparts, words, 1, d_dict, nullptr,
+                 d_bt, st, bt_words, D, c->front_new.as<u64>(), d_lbC, &dc->tickets[3], &dc->nf, &dc->N);
       read_counters(c, dc, &hc);
       const long long R = hc.R, Mk = hc.Mk;
       if (R == 0) break;
