@@ -111,6 +111,8 @@ typedef struct {
   int64_t full;                           /* 1 once pivot rows are computed */
   int64_t numeric_ns, backsub_ns;         /* device time (CUDA events) */
   int64_t dense_rows, dense_cols;         /* D' block shape */
+  int64_t sweep_pivots;                   /* pivot-row applications in the C-row sweep */
+  int64_t sweep_tail_nnz;                 /* pivot-row tail entries those applications read */
 } f4b_echelon_info;
 
 /* psge_reduce (sparselin.py:281-369) on a compiled plan (no copy) or on a

@@ -43,7 +43,8 @@ class PlanInfo(C.Structure):
 class EchelonInfo(C.Structure):
     _fields_ = [(k, C.c_int64) for k in (
         "n_rows", "n_cols", "rank", "zero_rows", "n_pivot_rows", "n_nonpivot_rows",
-        "pivot_nnz", "nonpivot_nnz", "full", "numeric_ns", "backsub_ns", "dense_rows", "dense_cols")]
+        "pivot_nnz", "nonpivot_nnz", "full", "numeric_ns", "backsub_ns", "dense_rows", "dense_cols",
+        "sweep_pivots", "sweep_tail_nnz")]
 
 
 # name -> (restype, argtypes)

@@ -215,7 +215,7 @@ using namespace f4b;
 
 extern "C" {
 
-int f4b_abi_version(void) { return 1; }
+int f4b_abi_version(void) { return 2; }
 
 int f4b_ctx_create(int device, uint32_t p, int n_vars, int order, f4b_alloc_fn alloc, f4b_free_fn dfree, void* user,
                    f4b_ctx** out) {

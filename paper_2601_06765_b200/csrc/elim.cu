@@ -57,6 +57,8 @@ struct f4b_echelon {
   f4b::DBuf a_off, a_len;        // u32 [nA] (pivot rows, ascending lead)
   f4b::DBuf d_off, d_len;        // u32 [rankD] (nonpivot rows, ascending lead)
   f4b::DBuf cursor;              // u64
+  f4b::DBuf stats;               // u64 [2] sweep work counters
+  unsigned long long sweep_pivots = 0, sweep_tail_nnz = 0;
   size_t pool_cap = 0;
   long long pivot_nnz = 0, nonpivot_nnz = 0;
 };
@@ -225,10 +227,11 @@ __global__ void __launch_bounds__(SW_THREADS) k_sweep(
     const u32* __restrict__ abits_g, T* __restrict__ gacc, u32* __restrict__ Dp, u32 K,
     const u32* __restrict__ nonA, const u32* __restrict__ Rd, u32 rankD, const u32* __restrict__ dpiv,
     u32* __restrict__ pcol, u32* __restrict__ pval, size_t cap, unsigned long long* cursor,
-    u32* __restrict__ s_off, u32* __restrict__ s_len, u32* __restrict__ err) {
+    u32* __restrict__ s_off, u32* __restrict__ s_len, u32* __restrict__ err, unsigned long long* __restrict__ stats) {
   extern __shared__ u32 smem[];
   const u32 nwords = (N + 31) / 32;
   u32* abits = smem;
+  unsigned long long n_piv = 0, n_tail = 0;  // work counters (thread 0)
   T* acc = gacc ? gacc + (size_t)blockIdx.x * N : reinterpret_cast<T*>(smem + nwords);
   __shared__ u32 red[33];
   __shared__ u32 sh[4];
@@ -266,6 +269,10 @@ __global__ void __launch_bounds__(SW_THREADS) k_sweep(
     while (c < N) {
       const uint4 d = __ldg(desc + c);
       const u32 fm = fp.to_mont(fp.neg(fp.mul(av, d.z)));
+      if (tid == 0) {
+        ++n_piv;
+        n_tail += d.y - d.x;
+      }
       u32 k = d.x + tid;
       for (; k + blockDim.x < d.y; k += 2 * blockDim.x) {
         const u32 c0 = __ldg(col + k), c1 = __ldg(col + k + blockDim.x);
@@ -326,6 +333,10 @@ __global__ void __launch_bounds__(SW_THREADS) k_sweep(
       emit_row<T>(acc, lead, N, nullptr, pcol, pval, cap, cursor, s_off + rr, s_len + rr, err, red, sh + 1);
       __syncthreads();
     }
+  }
+  if (stats && tid == 0 && n_piv) {
+    atomicAdd(stats, n_piv);
+    atomicAdd(stats + 1, n_tail);
   }
 }
 
@@ -595,7 +606,8 @@ static int sweep_grid(Ctx* c, size_t smem, long long rows) {
 template <int MODE>
 static void launch_sweep(Ctx* c, const Fp& fp, f4b_echelon* E, const u32* rows, u32 nrows, u32* Dp, u32 K,
                          const u32* Rd, u32 rankD, const u32* dpiv, u32* pcol, u32* pval, size_t cap,
-                         unsigned long long* cursor, u32* s_off, u32* s_len, u32* err) {
+                         unsigned long long* cursor, u32* s_off, u32* s_len, u32* err,
+                         unsigned long long* stats = nullptr) {
   const u32 N = (u32)E->n_cols;
   const size_t bitmap = (size_t)((N + 31) / 32) * 4;
   const bool small_p = c->p < 65536u;
@@ -616,16 +628,16 @@ static void launch_sweep(Ctx* c, const Fp& fp, f4b_echelon* E, const u32* rows, 
     ensure(c, gacc, (size_t)grid * N * sizeof(u32));
     F4B_LAUNCH(c, (k_sweep<MODE, u32>), grid, SW_THREADS, smem, fp, E->rp, E->col, E->val, N, rows, nrows,
                E->desc.as<uint4>(), E->invl.as<u32>(), E->abits.as<u32>(), gacc.as<u32>(), Dp, K, E->nonA.as<u32>(),
-               Rd, rankD, dpiv, pcol, pval, cap, cursor, s_off, s_len, err);
+               Rd, rankD, dpiv, pcol, pval, cap, cursor, s_off, s_len, err, stats);
     release(c, gacc);
   } else if (small_p) {
     F4B_LAUNCH(c, (k_sweep<MODE, uint16_t>), grid, SW_THREADS, smem, fp, E->rp, E->col, E->val, N, rows, nrows,
                E->desc.as<uint4>(), E->invl.as<u32>(), E->abits.as<u32>(), (uint16_t*)nullptr, Dp, K,
-               E->nonA.as<u32>(), Rd, rankD, dpiv, pcol, pval, cap, cursor, s_off, s_len, err);
+               E->nonA.as<u32>(), Rd, rankD, dpiv, pcol, pval, cap, cursor, s_off, s_len, err, stats);
   } else {
     F4B_LAUNCH(c, (k_sweep<MODE, u32>), grid, SW_THREADS, smem, fp, E->rp, E->col, E->val, N, rows, nrows,
                E->desc.as<uint4>(), E->invl.as<u32>(), E->abits.as<u32>(), (u32*)nullptr, Dp, K, E->nonA.as<u32>(),
-               Rd, rankD, dpiv, pcol, pval, cap, cursor, s_off, s_len, err);
+               Rd, rankD, dpiv, pcol, pval, cap, cursor, s_off, s_len, err, stats);
   }
 }
 
@@ -700,8 +712,10 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
   E->rankD = 0;
   if (R > 0 && K > 0) {
     ensure(c, Dp, (size_t)R * K * sizeof(u32));
+    ensure(c, E->stats, 16);
+    check_cuda(cudaMemsetAsync(E->stats.p, 0, 16, c->stream), "memset");
     launch_sweep<0>(c, fp, E, crows.as<u32>(), (u32)R, Dp.as<u32>(), (u32)K, nullptr, 0, nullptr, nullptr, nullptr, 0,
-                    nullptr, nullptr, nullptr, err);
+                    nullptr, nullptr, nullptr, err, E->stats.as<unsigned long long>());
     // E3a: cooperative forward elimination
     ensure(c, used, (size_t)R + 16);
     ensure(c, pofc, (size_t)K * sizeof(u32));
@@ -829,9 +843,12 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
     if (!(e & DEVERR_CAPACITY)) break;
     E->pool_cap *= 2;
   }
-  unsigned long long used_pool = 0;
+  unsigned long long used_pool = 0, st2[2] = {0, 0};
   check_cuda(cudaMemcpyAsync(&used_pool, E->cursor.p, 8, cudaMemcpyDeviceToHost, c->stream), "d2h");
+  if (E->stats.p) check_cuda(cudaMemcpyAsync(st2, E->stats.p, 16, cudaMemcpyDeviceToHost, c->stream), "d2h");
   check_cuda(cudaStreamSynchronize(c->stream), "sync");
+  E->sweep_pivots = st2[0];
+  E->sweep_tail_nnz = st2[1];
   E->nonpivot_nnz = (long long)used_pool;
   check_cuda(cudaEventRecord(ev1, c->stream), "event");
   check_cuda(cudaEventSynchronize(ev1), "event sync");
@@ -979,6 +996,8 @@ void echelon_info(const f4b_echelon* E, f4b_echelon_info* info) {
   info->backsub_ns = E->backsub_ns;
   info->dense_rows = E->nC;
   info->dense_cols = E->K;
+  info->sweep_pivots = (int64_t)E->sweep_pivots;
+  info->sweep_tail_nnz = (int64_t)E->sweep_tail_nnz;
 }
 
 void echelon_download(const f4b_echelon* E, int which, int64_t* leads, int64_t* row_ptr, int64_t* cols,
@@ -1046,7 +1065,7 @@ void echelon_release(f4b_echelon* E) {
   Ctx* c = E->ctx;
   DBuf* bufs[] = {&E->own_rp, &E->own_col, &E->own_val, &E->prow,  &E->invl, &E->desc, &E->abits, &E->acols,
                   &E->nonA,   &E->Rd,      &E->dpiv,    &E->pool_col, &E->pool_val, &E->a_off, &E->a_len,
-                  &E->d_off,  &E->d_len,   &E->cursor};
+                  &E->d_off,  &E->d_len,   &E->cursor, &E->stats};
   for (DBuf* b : bufs) release(c, *b);
   delete E;
 }

@@ -77,7 +77,8 @@ struct Ctx {
   // FBSP scratch (grow-only, reused across compile_batch calls)
   DBuf rows_basis, rows_delta, rows_len, rows_start, keys_all, vals_all;
   DBuf dict_a, dict_b, front, front_new, uniq, red, lmpref, cand_idx, shift_in;
-  DBuf cl_basis, cl_shift, cl_round;
+  DBuf cl_basis, cl_shift, cl_round, loop_scratch;
+  long long closure_cap_hint = 0;  // frontier / closure-row capacity of the persistent loop
   uint32_t pprime = 0, r2 = 0;
   long long launches = 0;        // kernel launches issued (reset per compile call)
   long long total_launches = 0;  // monotonically increasing

@@ -23,7 +23,10 @@
 //        shared-memory dictionary -> col_ind = N-1-pos and val.
 // Host round trips: one small counter read per closure round (grids of the
 // round are sized by upper bounds; kernels read the true sizes on device).
+#include <cooperative_groups.h>
+
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <cstdlib>
 #include <vector>
@@ -774,13 +777,16 @@ F4B_DEV void unrank_exps(u32 r, int n, int D, const u32* bt, int st, u16* e) {
 
 // Fill: every term of rows [r_lo, r_hi) -> its rank -> one bit.  Private
 // shared-memory bitmaps per CTA (written out as partials) when the rank space
-// fits, otherwise atomicOr straight into one global bitmap.
+// fits, otherwise atomicOr straight into one global bitmap.  Closure rounds
+// pass `known` (the dictionary so far): only absent monomials are ORed into
+// the global new-bits map, so a round costs O(Mk) instead of O(grid * words).
 template <int KW>
 __global__ void __launch_bounds__(RK_THREADS) k_rank_fill(
     KeyFmt f, u32 m_lo, u32 m_hi_host, const u32* __restrict__ d_mk, u32 r_lo, u32 r_hi_host,
     const u32* __restrict__ d_r, const int* __restrict__ rb, const u64* __restrict__ delta,
     const u32* __restrict__ rstart, const u32* __restrict__ boff, const u64* __restrict__ bckey,
-    const u32* __restrict__ bt_g, int st, int bt_words, u32 words, int use_smem, u32* __restrict__ partial) {
+    const u32* __restrict__ bt_g, int st, int bt_words, u32 words, int use_smem, u32* __restrict__ partial,
+    const u32* __restrict__ known) {
   extern __shared__ __align__(16) unsigned char smraw[];
   Key<KW>* sdel = reinterpret_cast<Key<KW>*>(smraw);
   u32* srs = reinterpret_cast<u32*>(sdel + RK_SROWS);
@@ -824,7 +830,7 @@ __global__ void __launch_bounds__(RK_THREADS) k_rank_fill(
         }
         const Key<KW> k = key_add<KW>(key_load<KW>(bckey, (long long)sbo[lo] + (t - srs[lo])), sdel[lo]);
         const u32 rk = key_rank<KW>(f, bt, st, k);
-        atomicOr(bits + (rk >> 5), 1u << (rk & 31));
+        if (!known || !((__ldg(known + (rk >> 5)) >> (rk & 31)) & 1u)) atomicOr(bits + (rk >> 5), 1u << (rk & 31));
       }
     } else {
       for (u32 i = threadIdx.x * 8; i < n; i += blockDim.x * 8) {
@@ -833,14 +839,18 @@ __global__ void __launch_bounds__(RK_THREADS) k_rank_fill(
         gen_keys<KW>(t0 + i, cnt, r_lo, r_hi, rb, delta, rstart, boff, bckey, k, nullptr, nullptr);
         for (int q = 0; q < cnt; ++q) {
           const u32 rk = key_rank<KW>(f, bt, st, k[q]);
-          atomicOr(bits + (rk >> 5), 1u << (rk & 31));
+          if (!known || !((__ldg(known + (rk >> 5)) >> (rk & 31)) & 1u)) atomicOr(bits + (rk >> 5), 1u << (rk & 31));
         }
       }
     }
     __syncthreads();
   }
+  // merge the private map: OR only words that add bits (most are already in)
   if (use_smem)
-    for (u32 w = threadIdx.x; w < words; w += blockDim.x) partial[(size_t)blockIdx.x * words + w] = sbits[w];
+    for (u32 w = threadIdx.x; w < words; w += blockDim.x) {
+      const u32 v = sbits[w];
+      if (v && (v & ~__ldcg(partial + w))) atomicOr(partial + w, v);
+    }
 }
 
 // OR the partial bitmaps.  mode 0: dict = OR.  mode 1: newbits = OR & ~dict,
@@ -958,7 +968,7 @@ __global__ void __launch_bounds__(256) k_rank_unrank(KeyFmt f, const u32* __rest
 // monomials in ascending rank order (look-back over word tiles) as device
 // keys, unranked cooperatively by the whole CTA.  Replaces reduce + extract +
 // unrank (three launches) per round.
-static constexpr int RX_WPT = 4;
+static constexpr int RX_WPT = 1;
 static constexpr int RX_LIST = 4096;
 template <int KW>
 __global__ void __launch_bounds__(256) k_rank_round(KeyFmt f, const u32* __restrict__ partial, int nparts, u32 words,
@@ -1137,6 +1147,343 @@ __global__ void __launch_bounds__(256) k_closure_rows(KeyFmt f, const u64* __res
   }
 }
 
+// ---------------------------------------------------------------------------
+// Persistent closure loop (cooperative launch): every closure round of
+// symbolic.py:250-290 in ONE kernel, grid barriers between the phases, no
+// host round trip per round.  Per round:
+//   A  reducer search, warp per frontier monomial; per-tile (rows, terms)
+//      counts                                                   | grid.sync
+//   B  totals + tile bases (every CTA scans the tile counts), rows written
+//      in frontier order, and their terms ranked straight away by the CTA
+//      that wrote them: absent monomials ORed into `newbits`    | grid.sync
+//   D1 per-CTA word chunk popcounts                             | grid.sync
+//   D2 chunk bases; set bits -> next frontier (ascending rank = ascending
+//      key), dict |= newbits, newbits = 0                       | grid.sync
+// Every CTA derives the same loop state (R, Mk, nf) from the same global
+// counts, so all exits are grid-uniform.  Capacity overflows stop the loop
+// with a flag; the host grows the buffers and recompiles.
+// ---------------------------------------------------------------------------
+struct LoopOut {
+  u32 r, n_cl, M, N, rounds, nf, flags, sel;
+};
+enum : u32 { LOOP_OVERFLOW = 1u, LOOP_SIZE_CAP = 2u, LOOP_DICT_CAP = 4u };
+
+struct LoopArgs {
+  KeyFmt f;
+  int D, st, bt_words;
+  u32 words;
+  const u32* bt;
+  u32* dict;
+  u32* newbits;
+  u64* front0;
+  u64* front1;
+  u32 front_cap;
+  int* red;
+  u32* tilecnt;
+  u32* chunkcnt;
+  const u32* lmw;
+  const int* cidx;
+  int nc, nw, stage_lm;
+  const u32* boff;
+  const u32* blen;
+  const u64* bckey;
+  const u16* lmexp;
+  const u16* maxe;
+  int* rows_basis;
+  u64* rows_delta;
+  u32* rows_start;
+  long long rows_cap;
+  int* cl_basis;
+  u16* cl_shift;
+  int* cl_round;
+  long long cl_cap;
+  long long r0;
+  u32 M0, maxlen;
+  long long dict_cap;
+  const u32* d_nf0;
+  const u32* d_N0;
+  u32* err;
+  LoopOut* out;
+  unsigned long long* trace;  // optional: [round][5] %globaltimer stamps + nf (F4B_LOOP_TRACE)
+};
+
+F4B_DEV unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+static constexpr int CL_THREADS = 256;
+static constexpr int CL_LIST = 2048;
+
+F4B_DEV u32 block_sum_u32(u32 v, u32* ws) {
+  u32 tot;
+  block_scan_excl(v, ws, &tot);
+  return tot;
+}
+
+template <int KW>
+__global__ void __launch_bounds__(CL_THREADS) k_closure_loop(const LoopArgs a) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) u32 csm[];
+  u32* bt = csm;
+  u32* list = csm + a.bt_words;             // CL_LIST ranks (D2)
+  u32* slm = list + CL_LIST;                // LM table (optional)
+  __shared__ u32 ws[33];
+  __shared__ u32 s_wn[CL_THREADS / 32], s_wl[CL_THREADS / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NWARP = CL_THREADS / 32;
+  const int n = a.f.n_vars;
+  for (int i = tid; i < a.bt_words; i += blockDim.x) bt[i] = a.bt[i];
+  const u32* lmw = a.lmw;
+  if (a.stage_lm) {
+    for (int i = tid; i < a.nc * a.nw; i += blockDim.x) slm[i] = __ldg(a.lmw + i);
+    lmw = slm;
+  }
+  __syncthreads();
+  u32 nf = __ldcg(a.d_nf0), N = __ldcg(a.d_N0);
+  long long r = a.r0, n_cl = 0;
+  u32 Mcur = a.M0, rounds = 0, flags = 0;
+  int sel = 0;
+  const u32 G = gridDim.x, W = G * NWARP, gw = blockIdx.x * NWARP + warp;
+  const u32 CH = (a.maxlen + 31) / 32;  // 32-term chunks per row (upper bound)
+  const u32 cw = (((a.words + G - 1) / G) + 31) & ~31u;
+  const u32 w_lo = min(a.words, blockIdx.x * cw), w_hi = min(a.words, w_lo + cw);
+  while (nf > 0 && a.nc > 0) {
+    const u64* front = sel ? a.front1 : a.front0;
+    u64* fnext = sel ? a.front0 : a.front1;
+    const bool tr = a.trace && blockIdx.x == 0 && tid == 0 && rounds < 64;
+    if (tr) {
+      a.trace[rounds * 6] = gtimer();
+      a.trace[rounds * 6 + 5] = nf;
+    }
+    // ---- A: first LM divisor in preference order (symbolic.py:228-235),
+    // warp per monomial over contiguous per-warp ranges; per-warp counts.
+    const u32 per = (nf + W - 1) / W;
+    const u32 j0 = min(nf, gw * per), j1 = min(nf, j0 + per);
+    {
+      u32 cn = 0, cl = 0;
+      for (u32 j = j0; j < j1; ++j) {
+        int found = -1;
+        u16 e[MAXV + 1];
+        key_decode<KW>(a.f, key_load<KW>(front, j), e);
+        e[n] = 0;
+        u32 me[MAXV / 2];
+        for (int w = 0; w < a.nw; ++w) me[w] = (u32)e[2 * w] | ((u32)e[2 * w + 1] << 16);
+        for (int b0 = 0; b0 < a.nc; b0 += 32) {
+          const int cc = b0 + lane;
+          bool ok = cc < a.nc;
+          if (ok) {
+            const u32* lm = lmw + (long long)cc * a.nw;
+            for (int w = 0; w < a.nw; ++w) ok &= (__vcmpgeu2(me[w], lm[w]) == 0xFFFFFFFFu);
+          }
+          const unsigned bm = __ballot_sync(0xffffffffu, ok);
+          if (bm) {
+            found = __ldg(a.cidx + b0 + __ffs(bm) - 1);
+            break;
+          }
+        }
+        if (lane == 0) a.red[j] = found;
+        if (found >= 0) {
+          ++cn;
+          cl += __ldg(a.blen + found);
+        }
+      }
+      if (lane == 0) {
+        a.tilecnt[2 * gw] = cn;
+        a.tilecnt[2 * gw + 1] = cl;
+      }
+    }
+    grid.sync();
+    if (tr) a.trace[rounds * 6 + 1] = gtimer();
+    // ---- totals and this warp's row / term bases
+    u32 R, Mk, bn, bl;
+    {
+      u32 tn = 0, tl = 0, pn = 0, pl = 0;
+      const u32 mine = blockIdx.x * NWARP;
+      for (u32 w = tid; w < W; w += blockDim.x) {
+        const u32 vn = __ldcg(a.tilecnt + 2 * w), vl = __ldcg(a.tilecnt + 2 * w + 1);
+        tn += vn;
+        tl += vl;
+        if (w < mine) {
+          pn += vn;
+          pl += vl;
+        }
+        if (w >= mine && w < mine + NWARP) {
+          s_wn[w - mine] = vn;
+          s_wl[w - mine] = vl;
+        }
+      }
+      R = block_sum_u32(tn, ws);
+      Mk = block_sum_u32(tl, ws);
+      bn = block_sum_u32(pn, ws);
+      bl = block_sum_u32(pl, ws);
+      for (int q = 0; q < warp; ++q) {
+        bn += s_wn[q];
+        bl += s_wl[q];
+      }
+    }
+    if (R == 0) break;
+    if (r + R + 1 > a.rows_cap || n_cl + R > a.cl_cap) {
+      flags |= LOOP_OVERFLOW;
+      break;
+    }
+    if ((unsigned long long)Mcur + Mk >= (1ull << 30)) {
+      flags |= LOOP_SIZE_CAP;
+      break;
+    }
+    if (blockIdx.x == 0 && tid == 0) a.rows_start[r + R] = Mcur + Mk;
+    // ---- B: the warp's rows, in frontier order
+    for (u32 jb = j0; jb < j1; jb += 32) {
+      const u32 j = jb + lane;
+      const int g = j < j1 ? __ldcg(a.red + j) : -1;
+      const u32 len = g >= 0 ? __ldg(a.blen + g) : 0u;
+      const unsigned bm = __ballot_sync(0xffffffffu, g >= 0);
+      u32 lp = len;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const u32 y = __shfl_up_sync(0xffffffffu, lp, o);
+        if (lane >= o) lp += y;
+      }
+      const u32 ltot = __shfl_sync(0xffffffffu, lp, 31);
+      if (g >= 0) {
+        const long long q = (long long)bn + __popc(bm & lanemask_lt());
+        const long long row = r + q;
+        const Key<KW> m = key_load<KW>(front, j);
+        a.rows_basis[row] = g;
+        key_store<KW>(a.rows_delta, row, key_sub<KW>(m, key_load<KW>(a.bckey, __ldg(a.boff + g))));
+        a.rows_start[row] = Mcur + bl + lp - len;
+        u16 e[MAXV];
+        key_decode<KW>(a.f, m, e);
+        bool over = false;
+        for (int v = 0; v < n; ++v) {
+          const u32 s = (u32)e[v] - (u32)a.lmexp[(long long)g * n + v];
+          over |= (s + (u32)a.maxe[(long long)g * n + v]) > 0xFFFFu;
+          a.cl_shift[(n_cl + q) * n + v] = (u16)s;
+        }
+        if (over) atomicOr(a.err, (u32)DEVERR_LANE_OVERFLOW);
+        a.cl_basis[n_cl + q] = g;
+        a.cl_round[n_cl + q] = (int)rounds + 1;
+      }
+      bn += __popc(bm);
+      bl += ltot;
+    }
+    // ---- C: every term of the new rows -> rank; absent monomials into
+    // newbits.  Items (frontier entry, 32-term chunk) over all warps of the
+    // grid.  The dictionary test is only a filter (a stale hit just costs an
+    // extra atomic; D masks with the dictionary), so it may use the L1 path.
+    for (u32 it = gw; it < nf * CH; it += W) {
+      const u32 j = it / CH, ch = it - j * CH;
+      const int g = __ldcg(a.red + j);
+      if (g < 0) continue;
+      const u32 len = __ldg(a.blen + g);
+      if (ch * 32 >= len) continue;
+      const u32 off = __ldg(a.boff + g);
+      const Key<KW> dl = key_sub<KW>(key_load<KW>(front, j), key_load<KW>(a.bckey, off));
+      const u32 t = ch * 32 + lane;
+      if (t < len) {
+        const Key<KW> kk = key_add<KW>(key_load<KW>(a.bckey, (long long)off + t), dl);
+        const u32 rk = key_rank<KW>(a.f, bt, a.st, kk);
+        const u32 bit = 1u << (rk & 31);
+        if (!(__ldg(a.dict + (rk >> 5)) & bit)) atomicOr(a.newbits + (rk >> 5), bit);
+      }
+    }
+    grid.sync();
+    if (tr) a.trace[rounds * 6 + 2] = gtimer();
+    // ---- D1: popcount of the CTA's word chunk (new = newbits & ~dict)
+    {
+      u32 cnt = 0;
+      for (u32 w = w_lo + tid; w < w_hi; w += blockDim.x) cnt += __popc(__ldcg(a.newbits + w) & ~__ldcg(a.dict + w));
+      cnt = block_sum_u32(cnt, ws);
+      if (tid == 0) a.chunkcnt[blockIdx.x] = cnt;
+    }
+    grid.sync();
+    if (tr) a.trace[rounds * 6 + 3] = gtimer();
+    // ---- D2: next frontier (ascending rank), dictionary update
+    u32 base, total;
+    {
+      u32 sb = 0, st = 0;
+      for (u32 b = tid; b < G; b += blockDim.x) {
+        const u32 v = __ldcg(a.chunkcnt + b);
+        st += v;
+        if (b < blockIdx.x) sb += v;
+      }
+      base = block_sum_u32(sb, ws);
+      total = block_sum_u32(st, ws);
+    }
+    if (total > a.front_cap) {
+      flags |= LOOP_OVERFLOW;
+      break;
+    }
+    for (u32 w0 = w_lo; w0 < w_hi; w0 += blockDim.x) {
+      const u32 w = w0 + tid;
+      u32 x = 0;
+      if (w < w_hi) {
+        const u32 nb = __ldcg(a.newbits + w);
+        if (nb) {
+          const u32 d = __ldcg(a.dict + w);
+          x = nb & ~d;
+          a.dict[w] = d | nb;
+          a.newbits[w] = 0;
+        }
+      }
+      u32 tt;
+      const u32 pre = block_scan_excl(__popc(x), ws, &tt);
+      if (tt <= (u32)CL_LIST) {
+        u32 p = pre, m = x;
+        while (m) {
+          const int b = __ffs(m) - 1;
+          m &= m - 1;
+          list[p++] = w * 32 + b;
+        }
+        __syncthreads();
+        for (u32 q = tid; q < tt; q += blockDim.x) {
+          u16 e[MAXV];
+          unrank_exps(list[q], n, a.D, bt, a.st, e);
+          key_store<KW>(fnext, base + q, key_encode<KW>(a.f, e));
+        }
+        __syncthreads();
+      } else {
+        u32 p = base + pre, m = x;
+        while (m) {
+          const int b = __ffs(m) - 1;
+          m &= m - 1;
+          u16 e[MAXV];
+          unrank_exps(w * 32 + b, n, a.D, bt, a.st, e);
+          key_store<KW>(fnext, p++, key_encode<KW>(a.f, e));
+        }
+      }
+      base += tt;
+    }
+    r += R;
+    n_cl += R;
+    Mcur += Mk;
+    ++rounds;
+    nf = total;
+    N += total;
+    sel ^= 1;
+    if ((long long)N > a.dict_cap) {
+      flags |= LOOP_DICT_CAP;
+      break;
+    }
+    grid.sync();
+    if (tr) a.trace[(rounds - 1) * 6 + 4] = gtimer();
+  }
+  if (blockIdx.x == 0 && tid == 0) {
+    LoopOut o;
+    o.r = (u32)r;
+    o.n_cl = (u32)n_cl;
+    o.M = Mcur;
+    o.N = N;
+    o.rounds = rounds;
+    o.nf = nf;
+    o.flags = flags;
+    o.sel = (u32)sel;
+    *a.out = o;
+  }
+}
+
 // Join: every term -> rank -> column via the popcount prefix.
 template <int KW>
 __global__ void __launch_bounds__(RK_THREADS) k_rank_join(KeyFmt f, u32 M, u32 r, const int* __restrict__ rb,
@@ -1279,7 +1626,7 @@ static void compile_rank(Ctx* c, const KeyFmt& f, int D, long long r0, const int
   DevCounters* dc = reinterpret_cast<DevCounters*>(c->errflag.p);
   check_cuda(cudaMemsetAsync(dc, 0, sizeof(DevCounters), c->stream), "memset counters");
   // look-back status regions: A/B for k_new_rows (<= N/256 tiles), C for k_rank_extract
-  const size_t lbAB = (size_t)words / 2 + 64, lbC = (size_t)words / 1024 + 64;
+  const size_t lbAB = (size_t)words / 2 + 64, lbC = (size_t)words / 256 + 64;
   ensure(c, c->dict_b, ((size_t)bt_words + 3 * (size_t)words + 2 * lbAB + lbC + 64) * 4);
   u32* base = c->dict_b.as<u32>();
   u32* d_bt = base;
@@ -1318,15 +1665,20 @@ static void compile_rank(Ctx* c, const KeyFmt& f, int D, long long r0, const int
                "attr");
     attr = true;
   }
-  auto fill = [&](u32 m_lo, u32 m_hi, u32 m_bound, const u32* d_mk, u32 r_lo, u32 r_hi, const u32* d_r) -> int {
+  // known == nullptr: round 0 (private partials when they fit);
+  // known == dict: closure round, absent monomials only, one global map.
+  auto fill = [&](u32 m_lo, u32 m_hi, u32 m_bound, const u32* d_mk, u32 r_lo, u32 r_hi, const u32* d_r,
+                  const u32* known) -> int {
+    const int sm = known ? 0 : use_smem;
     const u32 tiles = std::max<u32>(1, (m_bound + RK_TILE - 1) / RK_TILE);
-    const int grid = (int)std::min<long long>(tiles, max_grid);
-    const int nparts = use_smem ? grid : 1;
-    ensure(c, c->uniq, (size_t)nparts * words * 4 + 16);
-    if (!use_smem) check_cuda(cudaMemsetAsync(c->uniq.p, 0, (size_t)words * 4, c->stream), "memset bits");
-    F4B_LAUNCH(c, k_rank_fill<KW>, grid, RK_THREADS, fill_smem, f, m_lo, m_hi, d_mk, r_lo, r_hi, d_r,
-               c->rows_basis.as<int>(), c->rows_delta.as<u64>(), c->rows_start.as<u32>(), B.off.as<u32>(),
-               B.ckey.as<u64>(), d_bt, st, bt_words, words, use_smem, c->uniq.as<u32>());
+    const int grid = (int)std::min<long long>(tiles, sm ? std::min(max_grid, 2 * c->num_sms) : 4 * c->num_sms);
+    const int nparts = 1;
+    ensure(c, c->uniq, (size_t)words * 4 + 16);
+    check_cuda(cudaMemsetAsync(c->uniq.p, 0, (size_t)words * 4, c->stream), "memset bits");
+    F4B_LAUNCH(c, k_rank_fill<KW>, grid, RK_THREADS, sm ? fill_smem : fill_smem - (use_smem ? fill_smem_bits : 0), f,
+               m_lo, m_hi, d_mk, r_lo, r_hi, d_r, c->rows_basis.as<int>(), c->rows_delta.as<u64>(),
+               c->rows_start.as<u32>(), B.off.as<u32>(), B.ckey.as<u64>(), d_bt, st, bt_words, words, sm,
+               c->uniq.as<u32>(), known);
     return nparts;
   };
   const size_t ex_smem = (size_t)bt_words * 4;
@@ -1349,7 +1701,7 @@ static void compile_rank(Ctx* c, const KeyFmt& f, int D, long long r0, const int
   if (closure)
     F4B_LAUNCH(c, k_rank_leads<KW>, nblk(r0, 256), 256, 0, f, r0, c->rows_basis.as<int>(), c->rows_delta.as<u64>(),
                B.off.as<u32>(), B.ckey.as<u64>(), d_bt, st, d_aux);
-  int nparts = fill(0, M0, M0, nullptr, 0, (u32)r0, nullptr);
+  int nparts = fill(0, M0, M0, nullptr, 0, (u32)r0, nullptr, nullptr);
   ensure(c, c->front, (size_t)(std::min<unsigned long long>(Rsp, M0) + 1) * KW * sizeof(u64));
   const size_t rr_smem = ((size_t)bt_words + RX_LIST) * 4;
   const u32 rr_tiles = std::max<u32>(1, (words + 256 * RX_WPT - 1) / (256 * RX_WPT));
@@ -1378,6 +1730,133 @@ static void compile_rank(Ctx* c, const KeyFmt& f, int D, long long r0, const int
     if (nc)
       check_cuda(cudaMemcpyAsync(c->cand_idx.p, pref.data(), nc * sizeof(int), cudaMemcpyHostToDevice, c->stream),
                  "h2d cand");
+    if (!getenv("F4B_CLOSURE_ROUNDS")) {
+      // persistent closure loop: one cooperative launch for every round
+      const long long cap = (long long)std::min<unsigned long long>(
+          Rsp + 1, (unsigned long long)std::max<long long>({1ll << 16, c->closure_cap_hint, 2 * r0}));
+      const long long rows_cap = r0 + cap + 1;
+      if (rows_cap > rcap) {
+        rcap = rows_cap;
+        ensure_keep(c, c->rows_basis, rcap * sizeof(int));
+        ensure_keep(c, c->rows_delta, rcap * KW * sizeof(u64));
+        ensure_keep(c, c->rows_len, rcap * sizeof(u32));
+        ensure_keep(c, c->rows_start, (rcap + 1) * sizeof(u32));
+      }
+      ensure(c, c->cl_basis, cap * sizeof(int));
+      ensure(c, c->cl_shift, cap * n * sizeof(u16));
+      ensure(c, c->cl_round, cap * sizeof(int));
+      ensure_keep(c, c->front, (size_t)(std::max<unsigned long long>(cap, std::min<unsigned long long>(Rsp, M0) + 1)) *
+                                   KW * sizeof(u64));
+      ensure(c, c->front_new, (size_t)cap * KW * sizeof(u64));
+      ensure(c, c->red, (size_t)cap * sizeof(int));
+      const int stage_lm = (size_t)nc * nw * 4 <= 48 * 1024 ? 1 : 0;
+      const size_t lsm = ((size_t)bt_words + CL_LIST) * 4 + (stage_lm ? (size_t)nc * nw * 4 : 0);
+      static bool lattr = false;
+      if (!lattr) {
+        check_cuda(cudaFuncSetAttribute(k_closure_loop<KW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024),
+                   "attr");
+        lattr = true;
+      }
+      int bps = 0;
+      check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_closure_loop<KW>, CL_THREADS, lsm), "occupancy");
+      static const int bps_max = getenv("F4B_LOOP_BPS") ? atoi(getenv("F4B_LOOP_BPS")) : 2;
+      const int G = c->num_sms * std::max(1, std::min(bps, bps_max));
+      const size_t ntile_cap = (size_t)G * (CL_THREADS / 32);
+      ensure(c, c->loop_scratch, (2 * ntile_cap + G + 16) * sizeof(u32));
+      LoopOut* d_out = reinterpret_cast<LoopOut*>(dc + 1);
+      check_cuda(cudaMemsetAsync(d_aux, 0, (size_t)words * 4, c->stream), "memset newbits");
+      LoopArgs la;
+      la.f = f;
+      la.D = D;
+      la.st = st;
+      la.bt_words = bt_words;
+      la.words = words;
+      la.bt = d_bt;
+      la.dict = d_dict;
+      la.newbits = d_aux;
+      la.front0 = c->front.as<u64>();
+      la.front1 = c->front_new.as<u64>();
+      la.front_cap = (u32)cap;
+      la.red = c->red.as<int>();
+      la.tilecnt = c->loop_scratch.as<u32>();
+      la.chunkcnt = la.tilecnt + 2 * ntile_cap;
+      la.lmw = c->lmpref.as<u32>();
+      la.cidx = c->cand_idx.as<int>();
+      la.nc = nc;
+      la.nw = nw;
+      la.stage_lm = stage_lm;
+      la.boff = B.off.as<u32>();
+      la.blen = B.len.as<u32>();
+      la.bckey = B.ckey.as<u64>();
+      la.lmexp = B.lmexp.as<u16>();
+      la.maxe = B.maxe.as<u16>();
+      la.rows_basis = c->rows_basis.as<int>();
+      la.rows_delta = c->rows_delta.as<u64>();
+      la.rows_start = c->rows_start.as<u32>();
+      la.rows_cap = rcap;
+      la.cl_basis = c->cl_basis.as<int>();
+      la.cl_shift = c->cl_shift.as<u16>();
+      la.cl_round = c->cl_round.as<int>();
+      la.cl_cap = cap;
+      la.r0 = r0;
+      la.M0 = M0;
+      u32 maxlen_c = 1;
+      for (int32_t k : pref) maxlen_c = std::max<u32>(maxlen_c, (u32)B.h_len[k]);
+      la.maxlen = maxlen_c;
+      la.dict_cap = dict_cap;
+      la.d_nf0 = &dc->nf;
+      la.d_N0 = &dc->N;
+      la.err = &dc->err;
+      la.out = d_out;
+      static const bool trace_on = getenv("F4B_LOOP_TRACE") != nullptr;
+      DBuf trb;
+      la.trace = nullptr;
+      if (trace_on) {
+        ensure(c, trb, 64 * 6 * 8);
+        check_cuda(cudaMemsetAsync(trb.p, 0, 64 * 6 * 8, c->stream), "memset");
+        la.trace = trb.as<unsigned long long>();
+      }
+      {
+        void* args[] = {&la};
+        ProfScope ps(c, "k_closure_loop");
+        check_cuda(cudaLaunchCooperativeKernel((void*)k_closure_loop<KW>, G, CL_THREADS, args, lsm, c->stream),
+                   "k_closure_loop");
+      }
+      LoopOut ho;
+      check_cuda(cudaMemcpyAsync(c->h_stat, d_out, sizeof(LoopOut), cudaMemcpyDeviceToHost, c->stream), "d2h");
+      check_cuda(cudaStreamSynchronize(c->stream), "sync");
+      memcpy(&ho, c->h_stat, sizeof(LoopOut));
+      if (trace_on) {
+        std::vector<unsigned long long> ht(64 * 6);
+        check_cuda(cudaMemcpy(ht.data(), trb.p, ht.size() * 8, cudaMemcpyDeviceToHost), "d2h");
+        fprintf(stderr, "[loop] G=%d nc=%d rounds=%u N=%u\n", G, nc, ho.rounds, ho.N);
+        for (u32 q = 0; q < std::min<u32>(ho.rounds + 1, 64); ++q) {
+          const unsigned long long* t = &ht[q * 6];
+          if (!t[0]) break;
+          fprintf(stderr, "[loop]  round %u nf=%llu A=%.1fus B=%.1fus D1=%.1fus D2=%.1fus\n", q, t[5],
+                  t[1] ? (t[1] - t[0]) / 1e3 : 0.0, t[2] ? (t[2] - t[1]) / 1e3 : 0.0, t[3] ? (t[3] - t[2]) / 1e3 : 0.0,
+                  t[4] ? (t[4] - t[3]) / 1e3 : 0.0);
+        }
+        release(c, trb);
+      }
+      if (ho.flags & LOOP_OVERFLOW) {
+        // frontier / closure rows outgrew the buffers: grow and recompile
+        c->closure_cap_hint = std::max<long long>(4 * cap, c->closure_cap_hint);
+        cudaEventDestroy(ev0);
+        cudaEventDestroy(ev1);
+        cudaEventDestroy(ev2);
+        compile_rank<KW>(c, f, D, r0, h_rb, h_shift, closure, cand, dict_cap, pl);
+        return;
+      }
+      if (ho.flags & LOOP_SIZE_CAP) fail(F4B_ERR_SIZE_CAP, "batch has more than 2^30 terms");
+      if (ho.flags & LOOP_DICT_CAP)
+        fail(F4B_ERR_SIZE_CAP, "dictionary exceeded the cap after " + std::to_string(ho.rounds) + " closure rounds");
+      r = ho.r;
+      n_cl = ho.n_cl;
+      M = ho.M;
+      N = ho.N;
+      rounds = ho.rounds;
+    } else {
     read_counters(c, dc, &hc);
     N = hc.N;
     long long nf = hc.nf;
@@ -1414,7 +1893,7 @@ static void compile_rank(Ctx* c, const KeyFmt& f, int D, long long r0, const int
                  B.ckey.as<u64>(), B.lmexp.as<u16>(), B.maxe.as<u16>(), (int)rounds + 1, c->rows_basis.as<int>(),
                  c->rows_delta.as<u64>(), c->rows_start.as<u32>(), c->cl_basis.as<int>(), c->cl_shift.as<u16>(),
                  c->cl_round.as<int>(), d_lbA, d_lbB, &dc->tickets[2], &dc->R, &dc->Mk, &dc->err);
-      nparts = fill(Mcur, 0, (u32)mk_bound, &dc->Mk, (u32)r, 0, &dc->R);
+      nparts = fill(Mcur, 0, (u32)mk_bound, &dc->Mk, (u32)r, 0, &dc->R, d_dict);
       F4B_LAUNCH(c, k_rank_round<KW>, rr_tiles, 256, rr_smem, f, c->uniq.as<u32>(), nparts, words, 1, d_dict, nullptr,
                  d_bt, st, bt_words, D, c->front_new.as<u64>(), d_lbC, &dc->tickets[3], &dc->nf, &dc->N);
       read_counters(c, dc, &hc);
@@ -1431,6 +1910,7 @@ static void compile_rank(Ctx* c, const KeyFmt& f, int D, long long r0, const int
       n_cl += R;
       if (N > dict_cap)
         fail(F4B_ERR_SIZE_CAP, "dictionary exceeded the cap after " + std::to_string(rounds) + " closure rounds");
+    }
     }
   } else {
     read_counters(c, dc, &hc);

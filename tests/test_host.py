@@ -33,7 +33,7 @@ def test_library_exports_every_header_symbol(built_lib):
     assert len(names) >= 20
     for name in sorted(names):
         assert hasattr(built_lib, name), name
-    assert built_lib.f4b_abi_version() == 1
+    assert built_lib.f4b_abi_version() == 2
 
 
 def test_status_codes_map_to_reference_exceptions():

@@ -57,6 +57,7 @@ def main():
             "dict_ms": plan.info["dict_build_ns"] / 1e6, "join_ms": plan.info["row_assemble_ns"] / 1e6,
             "elim_ms": inf["numeric_ns"] / 1e6, "backsub_ms": inf["backsub_ns"] / 1e6,
             "C": inf["dense_rows"], "K": inf["dense_cols"], "rank": inf["rank"],
+            "pivots": inf["sweep_pivots"], "tail_nnz": inf["sweep_tail_nnz"],
             "launches_sym": plan.info["kernel_launches"], "kernel_ms_total": round(ksum, 3),
             "top": {k: [v[0], round(v[1] / 1e6, 3)] for k, v in top}}), flush=True)
 
