@@ -2,6 +2,7 @@
 // the registered allocator, the device-resident basis, and the thin wrappers
 // that translate C++ exceptions into f4b_status codes.
 #include <algorithm>
+#include <cstdint>
 #include <cstdio>
 #include <cstring>
 #include <new>
@@ -44,15 +45,49 @@ static void raw_free(Ctx* c, void* p) {
   else cudaFree(p);
 }
 
+static constexpr size_t POOL_MAX_BUFS = 96;
+static constexpr size_t POOL_MAX_BYTES = (size_t)8 << 30;
+
 void release(Ctx* c, DBuf& b) {
-  raw_free(c, b.p);
+  if (b.p && c->pool.size() < POOL_MAX_BUFS && c->pool_bytes + b.cap <= POOL_MAX_BYTES) {
+    c->pool.push_back({b.p, b.cap});
+    c->pool_bytes += b.cap;
+  } else {
+    raw_free(c, b.p);
+  }
   b.p = nullptr;
   b.cap = 0;
+}
+
+void pool_flush(Ctx* c) {
+  for (auto& e : c->pool) raw_free(c, e.first);
+  c->pool.clear();
+  c->pool_bytes = 0;
+}
+
+// smallest pooled buffer in [bytes, 2 * bytes + 1 MiB]
+static bool pool_take(Ctx* c, DBuf& b, size_t bytes) {
+  size_t best = SIZE_MAX, bi = 0;
+  for (size_t i = 0; i < c->pool.size(); ++i) {
+    const size_t cp = c->pool[i].second;
+    if (cp >= bytes && cp <= 2 * bytes + (1u << 20) && cp < best) {
+      best = cp;
+      bi = i;
+    }
+  }
+  if (best == SIZE_MAX) return false;
+  b.p = c->pool[bi].first;
+  b.cap = best;
+  c->pool_bytes -= best;
+  c->pool[bi] = c->pool.back();
+  c->pool.pop_back();
+  return true;
 }
 
 void ensure(Ctx* c, DBuf& b, size_t bytes) {
   if (bytes <= b.cap && b.p) return;
   release(c, b);
+  if (pool_take(c, b, bytes)) return;
   size_t cap = std::max<size_t>(bytes + bytes / 4, 256);
   cap = (cap + 255) & ~(size_t)255;
   b.p = raw_alloc(c, cap);
@@ -262,8 +297,9 @@ int f4b_ctx_destroy(f4b_ctx* h) {
                   &c->tmp_u32a, &c->tmp_u32b, &c->tmp_u32c, &c->rows_basis, &c->rows_delta, &c->rows_len,
                   &c->rows_start, &c->keys_all, &c->vals_all, &c->dict_a, &c->dict_b, &c->front, &c->front_new,
                   &c->uniq, &c->red, &c->lmpref, &c->cand_idx, &c->shift_in, &c->cl_basis, &c->cl_shift,
-                  &c->cl_round};
+                  &c->cl_round, &c->loop_scratch};
   for (DBuf* b : bufs) release(c, *b);
+  pool_flush(c);
   if (c->h_stat) cudaFreeHost(c->h_stat);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   delete h;
@@ -272,6 +308,15 @@ int f4b_ctx_destroy(f4b_ctx* h) {
 
 int f4b_ctx_set_stream(f4b_ctx* h, void* stream) {
   if (!h) return F4B_ERR_PRECONDITION;
+  if (h->c.stream != (cudaStream_t)stream) {
+    // pooled buffers were last used on the old stream
+    cudaStreamSynchronize(h->c.stream);
+    try {
+      pool_flush(&h->c);
+    } catch (const Error& e) {
+      return e.code;
+    }
+  }
   h->c.stream = (cudaStream_t)stream;
   return F4B_OK;
 }
@@ -432,6 +477,11 @@ int f4b_plan_get_info(const f4b_plan* pl, f4b_plan_info* info) {
   return F4B_OK;
 }
 
+__global__ void k_widen_u32(const u32* __restrict__ in, long long n, unsigned long long* __restrict__ out) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = in[i];
+}
+
 int f4b_plan_download(const f4b_plan* pl, int64_t* row_ptr, int64_t* col_ind, uint64_t* val, uint16_t* dict_exps,
                       int32_t* closure_basis, uint16_t* closure_shift, int32_t* closure_round) {
   if (!pl) return F4B_ERR_PRECONDITION;
@@ -439,24 +489,21 @@ int f4b_plan_download(const f4b_plan* pl, int64_t* row_ptr, int64_t* col_ind, ui
   Ctx* c = _c;
   const int n = c->n_vars;
   const long long r = pl->r, M = pl->M, N = pl->N, ncl = pl->r - pl->r0;
-  std::vector<u32> tmp;
-  if (row_ptr) {
-    tmp.resize(r + 1);
-    check_cuda(cudaMemcpyAsync(tmp.data(), pl->row_ptr.p, (r + 1) * 4, cudaMemcpyDeviceToHost, c->stream), "d2h");
-    check_cuda(cudaStreamSynchronize(c->stream), "sync");
-    for (long long i = 0; i <= r; ++i) row_ptr[i] = tmp[i];
-  }
-  if (col_ind && M) {
-    tmp.resize(M);
-    check_cuda(cudaMemcpyAsync(tmp.data(), pl->col_ind.p, M * 4, cudaMemcpyDeviceToHost, c->stream), "d2h");
-    check_cuda(cudaStreamSynchronize(c->stream), "sync");
-    for (long long i = 0; i < M; ++i) col_ind[i] = tmp[i];
-  }
-  if (val && M) {
-    tmp.resize(M);
-    check_cuda(cudaMemcpyAsync(tmp.data(), pl->val.p, M * 4, cudaMemcpyDeviceToHost, c->stream), "d2h");
-    check_cuda(cudaStreamSynchronize(c->stream), "sync");
-    for (long long i = 0; i < M; ++i) val[i] = tmp[i];
+  // widen u32 -> 64-bit on the device, then one D2H per array straight into
+  // the caller's buffers (page-locked ones copy at full link rate)
+  const long long w_row = row_ptr ? r + 1 : 0, w_col = col_ind ? M : 0, w_val = val ? M : 0;
+  DBuf wide;
+  if (w_row + w_col + w_val) {
+    ensure(c, wide, (size_t)(w_row + w_col + w_val) * 8);
+    unsigned long long* wp = wide.as<unsigned long long>();
+    const int g = c->num_sms * 4;
+    if (w_row) F4B_LAUNCH(c, k_widen_u32, g, 256, 0, pl->row_ptr.as<u32>(), w_row, wp);
+    if (w_col) F4B_LAUNCH(c, k_widen_u32, g, 256, 0, pl->col_ind.as<u32>(), w_col, wp + w_row);
+    if (w_val) F4B_LAUNCH(c, k_widen_u32, g, 256, 0, pl->val.as<u32>(), w_val, wp + w_row + w_col);
+    if (w_row) check_cuda(cudaMemcpyAsync(row_ptr, wp, w_row * 8, cudaMemcpyDeviceToHost, c->stream), "d2h");
+    if (w_col) check_cuda(cudaMemcpyAsync(col_ind, wp + w_row, w_col * 8, cudaMemcpyDeviceToHost, c->stream), "d2h");
+    if (w_val)
+      check_cuda(cudaMemcpyAsync(val, wp + w_row + w_col, w_val * 8, cudaMemcpyDeviceToHost, c->stream), "d2h");
   }
   if (dict_exps && N)
     check_cuda(cudaMemcpyAsync(dict_exps, pl->dict_exps.p, N * n * sizeof(u16), cudaMemcpyDeviceToHost, c->stream), "d2h");
@@ -469,6 +516,7 @@ int f4b_plan_download(const f4b_plan* pl, int64_t* row_ptr, int64_t* col_ind, ui
       check_cuda(cudaMemcpyAsync(closure_round, pl->cl_round.p, ncl * 4, cudaMemcpyDeviceToHost, c->stream), "d2h");
   }
   check_cuda(cudaStreamSynchronize(c->stream), "sync");
+  release(c, wide);
   API_END
 }
 

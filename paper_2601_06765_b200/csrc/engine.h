@@ -30,6 +30,7 @@ struct Error {
 void ensure(Ctx* c, DBuf& b, size_t bytes);  // grow-only; contents not preserved
 void ensure_keep(Ctx* c, DBuf& b, size_t bytes);  // grow-only; contents preserved
 void release(Ctx* c, DBuf& b);
+void pool_flush(Ctx* c);
 void check_cuda(cudaError_t e, const char* what);  // throws Error{F4B_ERR_CUDA}
 [[noreturn]] void fail(int code, const std::string& msg);
 
@@ -79,6 +80,10 @@ struct Ctx {
   DBuf dict_a, dict_b, front, front_new, uniq, red, lmpref, cand_idx, shift_in;
   DBuf cl_basis, cl_shift, cl_round, loop_scratch;
   long long closure_cap_hint = 0;  // frontier / closure-row capacity of the persistent loop
+  // released buffers kept for reuse on the context stream (stream-ordered,
+  // like the caching allocator itself, without a host callback per buffer)
+  std::vector<std::pair<void*, size_t>> pool;
+  size_t pool_bytes = 0;
   uint32_t pprime = 0, r2 = 0;
   long long launches = 0;        // kernel launches issued (reset per compile call)
   long long total_launches = 0;  // monotonically increasing

@@ -26,6 +26,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
@@ -1589,6 +1590,13 @@ static void compile_rank(Ctx* c, const KeyFmt& f, int D, long long r0, const int
   Basis& B = c->basis;
   const int n = c->n_vars;
   c->launches = 0;
+  static const bool htrace = getenv("F4B_HOST_TRACE") != nullptr;
+  const auto h0 = std::chrono::steady_clock::now();
+  std::vector<std::pair<const char*, double>> hmarks;
+  auto mark = [&](const char* what) {
+    if (htrace)
+      hmarks.push_back({what, std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count()});
+  };
   cudaEvent_t ev0, ev1, ev2;
   check_cuda(cudaEventCreate(&ev0), "event");
   check_cuda(cudaEventCreate(&ev1), "event");
@@ -1655,6 +1663,7 @@ static void compile_rank(Ctx* c, const KeyFmt& f, int D, long long r0, const int
                              c->stream), "h2d starts");
   F4B_LAUNCH(c, k_rows0<KW>, nblk(r0, 256), 256, 0, f, r0, c->rows_basis.as<int>(), c->shift_in.as<u16>(),
              B.len.as<u32>(), c->rows_delta.as<u64>(), c->rows_len.as<u32>());
+  mark("rows h2d + rows0");
   static bool attr = false;
   if (!attr) {
     check_cuda(cudaFuncSetAttribute(k_rank_fill<KW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "attr");
@@ -1709,6 +1718,7 @@ static void compile_rank(Ctx* c, const KeyFmt& f, int D, long long r0, const int
   F4B_LAUNCH(c, k_rank_round<KW>, rr_tiles, 256, rr_smem, f, c->uniq.as<u32>(), nparts, words, 0, d_dict, d_aux, d_bt,
              st, bt_words, D, c->front.as<u64>(), d_lbC, &dc->tickets[3], &dc->nf, &dc->N);
   long long r = r0, rounds = 0, n_cl = 0, N = 0;
+  mark("fill + round0 launched");
   DevCounters hc;
   if (closure) {
     // candidate LMs in preference order (key(LM), index) (symbolic.py:228-235)
@@ -1730,6 +1740,7 @@ static void compile_rank(Ctx* c, const KeyFmt& f, int D, long long r0, const int
     if (nc)
       check_cuda(cudaMemcpyAsync(c->cand_idx.p, pref.data(), nc * sizeof(int), cudaMemcpyHostToDevice, c->stream),
                  "h2d cand");
+    mark("LM pref sorted + h2d");
     if (!getenv("F4B_CLOSURE_ROUNDS")) {
       // persistent closure loop: one cooperative launch for every round
       const long long cap = (long long)std::min<unsigned long long>(
@@ -1822,10 +1833,12 @@ static void compile_rank(Ctx* c, const KeyFmt& f, int D, long long r0, const int
         check_cuda(cudaLaunchCooperativeKernel((void*)k_closure_loop<KW>, G, CL_THREADS, args, lsm, c->stream),
                    "k_closure_loop");
       }
+      mark("loop launched");
       LoopOut ho;
       check_cuda(cudaMemcpyAsync(c->h_stat, d_out, sizeof(LoopOut), cudaMemcpyDeviceToHost, c->stream), "d2h");
       check_cuda(cudaStreamSynchronize(c->stream), "sync");
       memcpy(&ho, c->h_stat, sizeof(LoopOut));
+      mark("loop synced");
       if (trace_on) {
         std::vector<unsigned long long> ht(64 * 6);
         check_cuda(cudaMemcpy(ht.data(), trb.p, ht.size() * 8, cudaMemcpyDeviceToHost), "d2h");
@@ -1960,6 +1973,7 @@ static void compile_rank(Ctx* c, const KeyFmt& f, int D, long long r0, const int
                pl->val.as<u32>(), &dc->err);
   }
   check_cuda(cudaEventRecord(ev2, c->stream), "event record");
+  mark("join launched");
   read_counters(c, dc, &hc);
   float ms1 = 0, ms2 = 0;
   check_cuda(cudaEventElapsedTime(&ms1, ev0, ev1), "elapsed");
@@ -1967,6 +1981,12 @@ static void compile_rank(Ctx* c, const KeyFmt& f, int D, long long r0, const int
   cudaEventDestroy(ev0);
   cudaEventDestroy(ev1);
   cudaEventDestroy(ev2);
+  mark("final sync");
+  if (htrace) {
+    fprintf(stderr, "[host] r0=%lld M=%lld:", r0, (long long)M);
+    for (auto& m : hmarks) fprintf(stderr, " %s @%.1f |", m.first, m.second);
+    fprintf(stderr, " dev dict %.1fus asm %.1fus\n", ms1 * 1e3, ms2 * 1e3);
+  }
   pl->dict_ns = (int64_t)(ms1 * 1e6);
   pl->asm_ns = (int64_t)(ms2 * 1e6);
   pl->launches = c->launches;

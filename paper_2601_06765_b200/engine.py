@@ -21,6 +21,21 @@ from .errors import LaneOverflowError
 from .monomials import ORDER_CODE
 
 _EXP_MAX = 0xFFFF
+_PINNED_MIN = 1 << 16
+
+
+def host_empty(shape, dtype):
+    """Host array for a device download: page-locked (torch's caching host
+    allocator) above 64 KiB so the copy runs at full PCIe / C2C rate."""
+    dtype = np.dtype(dtype)
+    count = int(np.prod(shape)) if np.ndim(shape) else int(shape)
+    nbytes = count * dtype.itemsize
+    if nbytes < _PINNED_MIN:
+        return np.empty(shape, dtype=dtype)
+    import torch
+
+    t = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    return t.numpy().view(dtype).reshape(shape)
 _ids = itertools.count(1)
 
 
@@ -40,9 +55,9 @@ class DevicePlan:
         r, M, N, ncl = (self.info[k] for k in ("r", "M", "N", "n_closure_rows"))
         out = {}
         if arrays:
-            out["row_ptr"] = np.empty(r + 1, dtype=np.int64)
-            out["col_ind"] = np.empty(M, dtype=np.int64)
-            out["val"] = np.empty(M, dtype=np.uint64)
+            out["row_ptr"] = host_empty(r + 1, np.int64)
+            out["col_ind"] = host_empty(M, np.int64)
+            out["val"] = host_empty(M, np.uint64)
         if dict_exps:
             out["dict_exps"] = np.empty((N, n), dtype=np.uint16)
         if closure:
@@ -119,10 +134,17 @@ class Engine:
         self.p, self.n_vars, self.order, self.device = p, n_vars, order, device
         self.uid = next(_ids)
         self.generation = 0
-        # host mirror of the device basis: lengths + concatenated exps / coeffs
+        self._reset_mirror()
+
+    def _reset_mirror(self):
+        # host mirror of the device basis: lengths + the appended chunks (no
+        # concatenation, so appends stay O(new terms)), and the buffers of the
+        # last synced SoaPolySet for the append-only fast path of sync_basis
         self._lens = np.zeros(0, dtype=np.int64)
-        self._exps = np.zeros((0, n_vars), dtype=np.uint16)
-        self._coeff = np.zeros(0, dtype=np.uint32)
+        self._chunks = []  # (t0, exps u16 chunk, coeff u32 chunk)
+        self._T = 0
+        self._src = None
+        self._src_refs = None
 
     # -- instrumentation -----------------------------------------------------
     def profile(self, enable: bool):
@@ -151,9 +173,7 @@ class Engine:
 
     def clear_basis(self):
         self.ctx.check(self.lib.f4b_basis_clear(self.ctx.h), "basis clear")
-        self._lens = np.zeros(0, dtype=np.int64)
-        self._exps = np.zeros((0, self.n_vars), dtype=np.uint16)
-        self._coeff = np.zeros(0, dtype=np.uint32)
+        self._reset_mirror()
         self.generation += 1
 
     def append_polys(self, lengths, exps, coeffs):
@@ -167,28 +187,47 @@ class Engine:
         self.ctx.check(self.lib.f4b_basis_append(self.ctx.h, len(lengths), ptr(lengths, C.c_int64),
                                                  ptr(exps, C.c_uint16), ptr(coeffs, C.c_uint32)), "basis append")
         self._lens = np.concatenate([self._lens, lengths])
-        self._exps = np.concatenate([self._exps, exps])
-        self._coeff = np.concatenate([self._coeff, coeffs])
+        if len(coeffs):
+            self._chunks.append((self._T, exps, coeffs))
+        self._T += len(coeffs)
+        self._src = None
         self.generation += 1
 
+    @staticmethod
+    def _buffers(soa):
+        # (address, strides) of the streams; the arrays themselves are kept in
+        # self._src_refs so the addresses cannot be recycled by another array
+        return tuple((a.__array_interface__["data"][0], a.strides) for a in (soa.exps, soa.coeff))
+
+    def _prefix_equal(self, soa) -> bool:
+        n_dev, T_dev = self.n_polys, self._T
+        if len(soa) < n_dev or soa.total_terms() < T_dev:
+            return False
+        if not np.array_equal(soa.length[:n_dev], self._lens):
+            return False
+        if self._src is not None and self._src == self._buffers(soa):
+            # same append-only buffers as the last sync (the F4 driver's
+            # growing SoaPolySet): the synced prefix cannot have changed
+            return True
+        for t0, ex, co in self._chunks:
+            t1 = t0 + len(co)
+            if not (np.array_equal(soa.coeff[t0:t1], co) and np.array_equal(soa.exps[t0:t1], ex)):
+                return False
+        return True
+
     def sync_basis(self, soa):
-        """Make the device basis equal to ``soa`` (a SoaPolySet)."""
+        """Make the device basis equal to ``soa`` (a SoaPolySet).  Appends
+        only the polynomials beyond the device prefix when that prefix is
+        unchanged (SoaPolySet streams are append-only, as in the reference)."""
         if getattr(soa, "_f4b_token", None) == self.token:
             return
-        n_dev = self.n_polys
-        T_dev = len(self._coeff)
-        same_prefix = (
-            len(soa) >= n_dev
-            and soa.total_terms() >= T_dev
-            and np.array_equal(soa.length[:n_dev], self._lens)
-            and np.array_equal(soa.coeff[:T_dev].astype(np.uint32), self._coeff)
-            and np.array_equal(soa.exps[:T_dev], self._exps)
-        )
-        if not same_prefix:
+        if not self._prefix_equal(soa):
             self.clear_basis()
-            n_dev, T_dev = 0, 0
+        n_dev, T_dev = self.n_polys, self._T
         if len(soa) > n_dev:
             self.append_polys(soa.length[n_dev:], soa.exps[T_dev:], soa.coeff[T_dev:])
+        self._src = self._buffers(soa)
+        self._src_refs = (soa.exps, soa.coeff)
         soa._f4b_token = self.token
 
     # -- hot path ----------------------------------------------------------
