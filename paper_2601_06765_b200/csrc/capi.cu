@@ -297,9 +297,10 @@ int f4b_ctx_destroy(f4b_ctx* h) {
                   &c->tmp_u32a, &c->tmp_u32b, &c->tmp_u32c, &c->rows_basis, &c->rows_delta, &c->rows_len,
                   &c->rows_start, &c->keys_all, &c->vals_all, &c->dict_a, &c->dict_b, &c->front, &c->front_new,
                   &c->uniq, &c->red, &c->lmpref, &c->cand_idx, &c->shift_in, &c->cl_basis, &c->cl_shift,
-                  &c->cl_round, &c->loop_scratch};
+                  &c->cl_round, &c->loop_scratch, &c->dstage, &c->maps, &c->dwp, &c->fcnt};
   for (DBuf* b : bufs) release(c, *b);
   pool_flush(c);
+  if (c->h_stage) cudaFreeHost(c->h_stage);
   if (c->h_stat) cudaFreeHost(c->h_stat);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   delete h;
@@ -370,6 +371,8 @@ int f4b_basis_clear(f4b_ctx* h) {
   B.h_maxe.clear();
   B.ckey_terms = 0;
   B.ckey_lane_bits = -1;
+  B.lm_order.clear();
+  B.lm_sorted = 0;
   return F4B_OK;
 }
 

@@ -107,6 +107,26 @@ F4B_DEV Key<KW> key_load(const u64* __restrict__ base, long long i) {
 }
 
 // Plain (non-__ldg) load for buffers written earlier in the same kernel.
+// L2-coherent load (ld.global.cg) for keys written earlier in the SAME
+// launch by other CTAs (persistent kernels): never served from a stale L1 line.
+template <int KW>
+F4B_DEV Key<KW> key_load_cg(const u64* base, long long i) {
+  Key<KW> k;
+  if constexpr (KW % 2 == 0) {
+    const ulonglong2* p = reinterpret_cast<const ulonglong2*>(base + i * KW);
+#pragma unroll
+    for (int j = 0; j < KW / 2; ++j) {
+      const ulonglong2 v = __ldcg(p + j);
+      k.w[2 * j] = v.x;
+      k.w[2 * j + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < KW; ++j) k.w[j] = __ldcg(base + i * KW + j);
+  }
+  return k;
+}
+
 template <int KW>
 F4B_DEV Key<KW> key_load_rw(const u64* base, long long i) {
   Key<KW> k;

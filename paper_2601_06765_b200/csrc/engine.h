@@ -57,6 +57,10 @@ struct Basis {
   DBuf maxe;    // u16 [n_polys * n] per-polynomial max exponent per variable
   int ckey_lane_bits = -1, ckey_words = 0;
   long long ckey_terms = 0;  // terms already encoded in this format
+  // nonzero polynomials sorted by (key(LM), index): the closure preference
+  // order (symbolic.py:228-235), extended incrementally on append
+  std::vector<int32_t> lm_order;
+  int lm_sorted = 0;  // polynomials [0, lm_sorted) are merged into lm_order
 };
 
 struct Ctx {
@@ -80,6 +84,18 @@ struct Ctx {
   DBuf dict_a, dict_b, front, front_new, uniq, red, lmpref, cand_idx, shift_in;
   DBuf cl_basis, cl_shift, cl_round, loop_scratch;
   long long closure_cap_hint = 0;  // frontier / closure-row capacity of the persistent loop
+  long long m_cap_hint = 0, n_cap_hint = 0;  // plan capacities of the fused FBSP kernel
+  void* h_stage = nullptr;                   // page-locked H2D staging (grow-only)
+  size_t h_stage_cap = 0;
+  DBuf dstage;
+  // k_fbsp presence maps + chunk counters: zero between calls; the first
+  // maps_clean bytes of `maps` are known to be zero
+  DBuf maps, dwp;
+  size_t maps_clean = 0;
+  DBuf fcnt;          // two sets of 4G chunk counters (alternating per call)
+  int fcnt_G = 0, fcnt_parity = 0;
+  int fbsp_bps = -1;
+  size_t fbsp_bps_smem = 0;
   // released buffers kept for reuse on the context stream (stream-ordered,
   // like the caching allocator itself, without a host callback per buffer)
   std::vector<std::pair<void*, size_t>> pool;

@@ -439,6 +439,41 @@ static int mon_cmp(const uint16_t* u, const uint16_t* v, int n, int order) {
   return 0;
 }
 
+// Candidates in preference order (key(LM), index).  The whole basis order is
+// kept sorted incrementally (sort the appended polynomials, merge), so a call
+// costs O(#polys) instead of a comparison sort of the candidate set.
+static std::vector<int32_t> preference_order(Ctx* c, const std::vector<int32_t>& cand) {
+  Basis& B = c->basis;
+  const int n = c->n_vars;
+  auto less = [&](int32_t x, int32_t y) {
+    const int sgn = mon_cmp(&B.h_lm[(size_t)x * n], &B.h_lm[(size_t)y * n], n, c->order);
+    return sgn != 0 ? sgn < 0 : x < y;
+  };
+  if (B.lm_sorted < B.n_polys) {
+    const size_t mid = B.lm_order.size();
+    for (int k = B.lm_sorted; k < B.n_polys; ++k)
+      if (B.h_len[k] >= 1) B.lm_order.push_back(k);
+    std::sort(B.lm_order.begin() + mid, B.lm_order.end(), less);
+    std::inplace_merge(B.lm_order.begin(), B.lm_order.begin() + mid, B.lm_order.end(), less);
+    B.lm_sorted = B.n_polys;
+  }
+  std::vector<int32_t> out;
+  out.reserve(cand.size());
+  bool prefix = true;  // candidates == [0, k): the common case
+  for (size_t i = 0; i < cand.size() && prefix; ++i) prefix = cand[i] == (int32_t)i;
+  if (prefix) {
+    const int32_t k = (int32_t)cand.size();
+    for (int32_t x : B.lm_order)
+      if (x < k) out.push_back(x);
+  } else {
+    std::vector<char> in((size_t)B.n_polys, 0);
+    for (int32_t x : cand) in[(size_t)x] = 1;
+    for (int32_t x : B.lm_order)
+      if (in[(size_t)x]) out.push_back(x);
+  }
+  return out;
+}
+
 template <int KW>
 static void encode_basis(Ctx* c, const KeyFmt& f) {
   Basis& B = c->basis;
@@ -1166,6 +1201,7 @@ __global__ void __launch_bounds__(256) k_closure_rows(KeyFmt f, const u64* __res
 // ---------------------------------------------------------------------------
 struct LoopOut {
   u32 r, n_cl, M, N, rounds, nf, flags, sel;
+  unsigned long long t_start, t_epi, t_end;  // %globaltimer (fused kernel)
 };
 enum : u32 { LOOP_OVERFLOW = 1u, LOOP_SIZE_CAP = 2u, LOOP_DICT_CAP = 4u };
 
@@ -1206,6 +1242,20 @@ struct LoopArgs {
   u32* err;
   LoopOut* out;
   unsigned long long* trace;  // optional: [round][5] %globaltimer stamps + nf (F4B_LOOP_TRACE)
+  // full pipeline (compile_rank_fused): round 0 before the loop, the final
+  // dictionary and the join after it
+  int full, closure;
+  const int* rb_in;
+  const u32* start_in;
+  const u16* shift_in;
+  const u32* bcoeff;
+  u32* done;
+  u64* dict_out;
+  u16* dict_exps;
+  uint2* dwp;
+  u32* col;
+  u32* val;
+  u32 N_cap, M_cap;
 };
 
 F4B_DEV unsigned long long gtimer() {
@@ -1243,7 +1293,7 @@ __global__ void __launch_bounds__(CL_THREADS) k_closure_loop(const LoopArgs a) {
     lmw = slm;
   }
   __syncthreads();
-  u32 nf = __ldcg(a.d_nf0), N = __ldcg(a.d_N0);
+  u32 nf = a.full ? 0u : __ldcg(a.d_nf0), N = a.full ? 0u : __ldcg(a.d_N0);
   long long r = a.r0, n_cl = 0;
   u32 Mcur = a.M0, rounds = 0, flags = 0;
   int sel = 0;
@@ -1251,6 +1301,130 @@ __global__ void __launch_bounds__(CL_THREADS) k_closure_loop(const LoopArgs a) {
   const u32 CH = (a.maxlen + 31) / 32;  // 32-term chunks per row (upper bound)
   const u32 cw = (((a.words + G - 1) / G) + 31) & ~31u;
   const u32 w_lo = min(a.words, blockIdx.x * cw), w_hi = min(a.words, w_lo + cw);
+  // emit the set bits of x(w) over this CTA's word chunk, ascending, from
+  // position `base`: keys to out_keys[pos]; with out_exps also exponents to
+  // out_exps[N_all - 1 - pos] (column order) and the word prefix to dwp
+  auto emit_chunk = [&](auto getx, u32 base, u64* out_keys, u16* out_exps, u32 N_all) {
+    for (u32 w0 = w_lo; w0 < w_hi; w0 += blockDim.x) {
+      const u32 w = w0 + tid;
+      const u32 x = w < w_hi ? getx(w) : 0u;
+      u32 tt;
+      const u32 pre = block_scan_excl(__popc(x), ws, &tt);
+      if (out_exps && w < w_hi) a.dwp[w] = make_uint2(x, base + pre);
+      auto put = [&](u32 pos, u32 rk) {
+        u16 e[MAXV];
+        unrank_exps(rk, n, a.D, bt, a.st, e);
+        key_store<KW>(out_keys, pos, key_encode<KW>(a.f, e));
+        if (out_exps)
+          for (int v = 0; v < n; ++v) out_exps[((long long)N_all - 1 - pos) * n + v] = e[v];
+      };
+      if (tt <= (u32)CL_LIST) {
+        u32 p = pre, m = x;
+        while (m) {
+          const int b = __ffs(m) - 1;
+          m &= m - 1;
+          list[p++] = w * 32 + b;
+        }
+        __syncthreads();
+        for (u32 q = tid; q < tt; q += blockDim.x) put(base + q, list[q]);
+        __syncthreads();
+      } else {
+        u32 p = base + pre, m = x;
+        while (m) {
+          const int b = __ffs(m) - 1;
+          m &= m - 1;
+          put(p++, w * 32 + b);
+        }
+      }
+      base += tt;
+    }
+  };
+  // exclusive base of this CTA and the grand total of per-CTA counts cnt[0, G)
+  auto chunk_bases = [&](const u32* cnt, u32& base, u32& total) {
+    u32 sb = 0, st = 0;
+    for (u32 b = tid; b < G; b += blockDim.x) {
+      const u32 v = __ldcg(cnt + b);
+      st += v;
+      if (b < blockIdx.x) sb += v;
+    }
+    base = block_sum_u32(sb, ws);
+    total = block_sum_u32(st, ws);
+  };
+  unsigned long long t_start = 0, t_epi = 0;
+  if (blockIdx.x == 0 && tid == 0) t_start = gtimer();
+  if (a.full) {
+    const long long gt = (long long)blockIdx.x * blockDim.x + tid, GT = (long long)G * blockDim.x;
+    // P0: clear the maps; shift deltas key(t) - key(1) of the input rows
+    for (long long w = gt; w < a.words; w += GT) {
+      a.dict[w] = 0;
+      a.done[w] = 0;
+      a.newbits[w] = 0;
+    }
+    for (long long i = gt; i <= a.r0; i += GT) {
+      a.rows_start[i] = a.start_in[i];
+      if (i == a.r0) break;
+      a.rows_basis[i] = a.rb_in[i];
+      u16 e[MAXV], z[MAXV];
+      for (int v = 0; v < n; ++v) {
+        e[v] = a.shift_in[i * n + v];
+        z[v] = 0;
+      }
+      key_store<KW>(a.rows_delta, i, key_sub<KW>(key_encode<KW>(a.f, e), key_encode<KW>(a.f, z)));
+    }
+    grid.sync();
+    if (a.trace && blockIdx.x == 0 && tid == 0) a.trace[384] = gtimer();
+    // P1: leads of the input rows are covered (symbolic.py:339); every term
+    // of the input rows -> its dictionary bit (a stale L1 read of the map
+    // only costs a redundant atomic)
+    if (a.closure)
+      for (long long i = gt; i < a.r0; i += GT) {
+        const int g = __ldcg(a.rows_basis + i);
+        const Key<KW> k = key_add<KW>(key_load<KW>(a.bckey, __ldg(a.boff + g)), key_load_cg<KW>(a.rows_delta, i));
+        const u32 rk = key_rank<KW>(a.f, bt, a.st, k);
+        atomicOr(a.done + (rk >> 5), 1u << (rk & 31));
+      }
+    for (long long i = gw; i < a.r0; i += W) {
+      const int g = __ldcg(a.rows_basis + i);
+      const u32 off = __ldg(a.boff + g), len = __ldg(a.blen + g);
+      const Key<KW> dl = key_load_cg<KW>(a.rows_delta, i);
+      for (u32 t = lane; t < len; t += 32) {
+        const Key<KW> kk = key_add<KW>(key_load<KW>(a.bckey, (long long)off + t), dl);
+        const u32 rk = key_rank<KW>(a.f, bt, a.st, kk);
+        const u32 bit = 1u << (rk & 31);
+        if (!(a.dict[rk >> 5] & bit)) atomicOr(a.dict + (rk >> 5), bit);
+      }
+    }
+    grid.sync();
+    if (a.trace && blockIdx.x == 0 && tid == 0) a.trace[385] = gtimer();
+    // P2: dictionary size and the round-1 frontier dict & ~done (ascending)
+    {
+      u32 cf = 0, cd = 0;
+      for (u32 w = w_lo + tid; w < w_hi; w += blockDim.x) {
+        const u32 d = __ldcg(a.dict + w);
+        cd += __popc(d);
+        if (a.closure) cf += __popc(d & ~__ldcg(a.done + w));
+      }
+      cf = block_sum_u32(cf, ws);
+      cd = block_sum_u32(cd, ws);
+      if (tid == 0) {
+        a.chunkcnt[blockIdx.x] = cf;
+        a.chunkcnt[G + blockIdx.x] = cd;
+      }
+    }
+    grid.sync();
+    u32 base, dummy;
+    chunk_bases(a.chunkcnt, base, nf);
+    chunk_bases(a.chunkcnt + G, dummy, N);
+    if (nf > a.front_cap) {
+      flags |= LOOP_OVERFLOW;
+      nf = 0;
+    } else if (a.closure && nf) {
+      emit_chunk([&](u32 w) { return __ldcg(a.dict + w) & ~__ldcg(a.done + w); }, base, a.front0, nullptr, 0u);
+    }
+    if (!a.closure) nf = 0;
+    grid.sync();
+    if (a.trace && blockIdx.x == 0 && tid == 0) a.trace[386] = gtimer();
+  }
   while (nf > 0 && a.nc > 0) {
     const u64* front = sel ? a.front1 : a.front0;
     u64* fnext = sel ? a.front0 : a.front1;
@@ -1268,7 +1442,7 @@ __global__ void __launch_bounds__(CL_THREADS) k_closure_loop(const LoopArgs a) {
       for (u32 j = j0; j < j1; ++j) {
         int found = -1;
         u16 e[MAXV + 1];
-        key_decode<KW>(a.f, key_load<KW>(front, j), e);
+        key_decode<KW>(a.f, key_load_cg<KW>(front, j), e);
         e[n] = 0;
         u32 me[MAXV / 2];
         for (int w = 0; w < a.nw; ++w) me[w] = (u32)e[2 * w] | ((u32)e[2 * w + 1] << 16);
@@ -1351,7 +1525,7 @@ __global__ void __launch_bounds__(CL_THREADS) k_closure_loop(const LoopArgs a) {
       if (g >= 0) {
         const long long q = (long long)bn + __popc(bm & lanemask_lt());
         const long long row = r + q;
-        const Key<KW> m = key_load<KW>(front, j);
+        const Key<KW> m = key_load_cg<KW>(front, j);
         a.rows_basis[row] = g;
         key_store<KW>(a.rows_delta, row, key_sub<KW>(m, key_load<KW>(a.bckey, __ldg(a.boff + g))));
         a.rows_start[row] = Mcur + bl + lp - len;
@@ -1381,7 +1555,7 @@ __global__ void __launch_bounds__(CL_THREADS) k_closure_loop(const LoopArgs a) {
       const u32 len = __ldg(a.blen + g);
       if (ch * 32 >= len) continue;
       const u32 off = __ldg(a.boff + g);
-      const Key<KW> dl = key_sub<KW>(key_load<KW>(front, j), key_load<KW>(a.bckey, off));
+      const Key<KW> dl = key_sub<KW>(key_load_cg<KW>(front, j), key_load<KW>(a.bckey, off));
       const u32 t = ch * 32 + lane;
       if (t < len) {
         const Key<KW> kk = key_add<KW>(key_load<KW>(a.bckey, (long long)off + t), dl);
@@ -1471,6 +1645,45 @@ __global__ void __launch_bounds__(CL_THREADS) k_closure_loop(const LoopArgs a) {
     grid.sync();
     if (tr) a.trace[(rounds - 1) * 6 + 4] = gtimer();
   }
+  if (blockIdx.x == 0 && tid == 0) t_epi = gtimer();
+  if (a.full && !flags) {
+    if (N > a.N_cap || Mcur > a.M_cap || r + 1 > a.rows_cap) {
+      flags |= LOOP_OVERFLOW;
+    } else {
+      // P3: final dictionary: keys ascending, exponents in column order
+      // (descending), word prefix for the column map
+      {
+        u32 cd = 0;
+        for (u32 w = w_lo + tid; w < w_hi; w += blockDim.x) cd += __popc(__ldcg(a.dict + w));
+        cd = block_sum_u32(cd, ws);
+        if (tid == 0) a.chunkcnt[blockIdx.x] = cd;
+      }
+      grid.sync();
+      u32 base, tot;
+      chunk_bases(a.chunkcnt, base, tot);
+      emit_chunk([&](u32 w) { return __ldcg(a.dict + w); }, base, a.dict_out, a.dict_exps, N);
+      grid.sync();
+      if (a.trace && blockIdx.x == 0 && tid == 0) a.trace[387] = gtimer();
+      // P4: join (symbolic.py:360-388): every term -> rank -> column
+      //   col = N - 1 - (prefix[rank >> 5] + popc(word & below(rank)))
+      bool miss = false;
+      for (long long i = gw; i < r; i += W) {
+        const int g = __ldcg(a.rows_basis + i);
+        const u32 off = __ldg(a.boff + g), len = __ldg(a.blen + g);
+        const u32 rs = __ldcg(a.rows_start + i);
+        const Key<KW> dl = key_load_cg<KW>(a.rows_delta, i);
+        for (u32 t = lane; t < len; t += 32) {
+          const Key<KW> kk = key_add<KW>(key_load<KW>(a.bckey, (long long)off + t), dl);
+          const u32 rk = key_rank<KW>(a.f, bt, a.st, kk);
+          const uint2 dw = __ldcg(a.dwp + (rk >> 5));
+          if (!((dw.x >> (rk & 31)) & 1u)) miss = true;
+          a.col[rs + t] = N - 1 - (dw.y + __popc(dw.x & ((1u << (rk & 31)) - 1u)));
+          a.val[rs + t] = __ldg(a.bcoeff + off + t);
+        }
+      }
+      if (miss) atomicOr(a.err, (u32)DEVERR_MISSING_KEY);
+    }
+  }
   if (blockIdx.x == 0 && tid == 0) {
     LoopOut o;
     o.r = (u32)r;
@@ -1481,6 +1694,586 @@ __global__ void __launch_bounds__(CL_THREADS) k_closure_loop(const LoopArgs a) {
     o.nf = nf;
     o.flags = flags;
     o.sel = (u32)sel;
+    o.t_start = t_start;
+    o.t_epi = t_epi;
+    o.t_end = gtimer();
+    *a.out = o;
+  }
+}
+
+// ===========================================================================
+// k_fbsp: the whole rank-path compile_batch (symbolic.py:293-388) in ONE
+// cooperative launch.  Grid barriers:
+//   P1  input rows: shift deltas, row table, lead bits, dictionary bits
+//       (first setter of a bit counts it for the owning word chunk)   | sync
+//   P2  round-1 frontier = dict & ~done: chunk counts | sync | emit  | sync
+//   per closure round (2 barriers):
+//     AC  reducer search (symbolic.py:228-235) and, in the same warps,
+//         ranking of the reducer rows' terms: absent monomials into
+//         newbits, first setters counted per word chunk              | sync
+//     BD  row bases -> rows written in frontier order; chunk bases ->
+//         next frontier (ascending rank = ascending key), dict |= new | sync
+//   P3  final dictionary: keys ascending, exponents in column order, word
+//       prefix for the column map                                     | sync
+//   P4  join: every term -> rank -> column (symbolic.py:360-388)      | sync
+// The presence maps and the per-chunk counters are zero on entry and left
+// zero on exit (the host clears them after an aborted run).  All exits are
+// grid-uniform: every CTA derives the loop state from the same counters.
+// ===========================================================================
+struct FbspArgs {
+  KeyFmt f;
+  int D, st, bt_words, closure, nc, nw, stage_lm;
+  unsigned long long prefetch_terms;  // basis terms to pull into L2 up front (0 = none)
+  u32 words, maxlen, front_cap, N_cap, M_cap, M0;
+  long long r0, rows_cap, cl_cap, dict_cap;
+  const u32* bt;
+  const int* rb_in;
+  const u32* start_in;
+  const u16* shift_in;
+  const u32* lmw;
+  const int* cidx;
+  const u32* boff;
+  const u32* blen;
+  const u64* bckey;
+  const u32* bcoeff;
+  const u16* lmexp;
+  const u16* maxe;
+  u32* dict;
+  u32* done;
+  u32* newbits;
+  uint2* dwp;
+  u64* front0;
+  u64* front1;
+  int* red;
+  u32* tilecnt;  // [2 * warps]
+  u32* cnt;      // [4 * G] this call: new-bit counts (two parities), dictionary and lead counts per chunk
+  u32* cnt_next; // [4 * G] the next call's set, cleared here
+  int* rows_basis;
+  u64* rows_delta;
+  u32* rows_start;
+  int* cl_basis;
+  u16* cl_shift;
+  int* cl_round;
+  u64* dict_out;
+  u16* dict_exps;
+  u32* col;
+  u32* val;
+  u32* err;
+  LoopOut* out;
+  unsigned long long* trace;
+};
+
+template <int KW>
+__global__ void __launch_bounds__(CL_THREADS) k_fbsp(const FbspArgs a) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) u32 csm[];
+  u32* bt = csm;
+  u32* list = csm + ((a.bt_words + 3) & ~3);  // 16-byte aligned
+  u32* slm = list + CL_LIST;
+  __shared__ u32 ws[33];
+  __shared__ u32 s_wn[CL_THREADS / 32], s_wl[CL_THREADS / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NWARP = CL_THREADS / 32;
+  constexpr int U = KW <= 2 ? 4 : 2;  // 32-term chunks in flight per warp
+  const int n = a.f.n_vars;
+  const u32 G = gridDim.x, W = G * NWARP, gw = blockIdx.x * NWARP + warp;
+  // pull the basis keys / coefficients into L2 (one 128-byte line per
+  // thread-step): the per-warp chains below then start from L2, not HBM
+  if (a.prefetch_terms) {
+    const char* kp = reinterpret_cast<const char*>(a.bckey);
+    const char* cp = reinterpret_cast<const char*>(a.bcoeff);
+    const unsigned long long kb_ = a.prefetch_terms * KW * 8, cb_ = a.prefetch_terms * 4;
+    const unsigned long long gt = (unsigned long long)blockIdx.x * blockDim.x + tid, GT = (unsigned long long)G * blockDim.x;
+    for (unsigned long long o = gt * 128; o < kb_; o += GT * 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(kp + o));
+    for (unsigned long long o = gt * 128; o < cb_; o += GT * 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(cp + o));
+  }
+  // stage the binomial and LM tables (16-byte loads, all in flight)
+  for (int i = tid; i < a.bt_words; i += blockDim.x) bt[i] = a.bt[i];
+  const u32* lmw = a.lmw;
+  if (a.stage_lm) {
+    const int nv = (a.nc * a.nw) >> 2;
+    const uint4* src = reinterpret_cast<const uint4*>(a.lmw);
+    uint4* dst = reinterpret_cast<uint4*>(slm);
+    int i = tid;
+    for (; i + 3 * (int)blockDim.x < nv; i += 4 * blockDim.x) {
+      const uint4 v0 = src[i], v1 = src[i + blockDim.x], v2 = src[i + 2 * blockDim.x], v3 = src[i + 3 * blockDim.x];
+      dst[i] = v0;
+      dst[i + blockDim.x] = v1;
+      dst[i + 2 * blockDim.x] = v2;
+      dst[i + 3 * blockDim.x] = v3;
+    }
+    for (; i < nv; i += blockDim.x) dst[i] = src[i];
+    for (int w = (nv << 2) + tid; w < a.nc * a.nw; w += blockDim.x) slm[w] = a.lmw[w];
+    lmw = slm;
+  }
+  // the next call's counters are idle now: clear them
+  if (tid < 4) a.cnt_next[tid * G + blockIdx.x] = 0;
+  __syncthreads();
+  const u32 CH = max(1u, (a.maxlen + 31) / 32);
+  const u32 cw = (((a.words + G - 1) / G) + 31) & ~31u;
+  const u32 w_lo = min(a.words, blockIdx.x * cw), w_hi = min(a.words, w_lo + cw);
+  u32* cnt_a = a.cnt;
+  u32* cnt_b = a.cnt + G;
+  u32* dcount = a.cnt + 2 * G;
+  u32* lcount = a.cnt + 3 * G;
+  const bool t0th = blockIdx.x == 0 && tid == 0;
+  unsigned long long t_start = t0th ? gtimer() : 0ull, t_epi = 0;
+  auto stamp = [&](int slot) {
+    if (a.trace && t0th) a.trace[slot] = gtimer();
+  };
+  // exclusive base of this CTA and the total over per-CTA values v(b)
+  auto cta_bases = [&](auto v, u32& base, u32& total) {
+    u32 sb = 0, stt = 0;
+    for (u32 b = tid; b < G; b += blockDim.x) {
+      const u32 x = v(b);
+      stt += x;
+      if (b < blockIdx.x) sb += x;
+    }
+    base = block_sum_u32(sb, ws);
+    total = block_sum_u32(stt, ws);
+  };
+  // k warps per item (k = W / n_items clamped to [1, kmax]); each group of k
+  // warps owns a contiguous item range; `sub` is the warp's rank in it
+  auto groups_of = [&](u32 nitems, u32 kmax, u32& k, u32& i0, u32& i1, u32& sub) {
+    k = nitems >= W ? 1u : max(1u, min(W / max(nitems, 1u), kmax));
+    const u32 ng = W / k, g = gw / k;
+    sub = gw - g * k;
+    const u32 per = (nitems + ng - 1) / ng;
+    i0 = g < ng ? min(nitems, g * per) : nitems;
+    i1 = g < ng ? min(nitems, i0 + per) : nitems;
+  };
+  // set bits of getx(w) over this CTA's chunk, ascending from `base`: keys to
+  // out_keys[pos]; with out_exps also exponents to out_exps[N_all-1-pos]
+  // (column order) and the word prefix to dwp
+  auto emit_chunk = [&](auto getx, u32 base, u64* out_keys, u16* out_exps, u32 N_all) {
+    for (u32 w0 = w_lo; w0 < w_hi; w0 += blockDim.x) {
+      const u32 w = w0 + tid;
+      const u32 x = w < w_hi ? getx(w) : 0u;
+      u32 tt;
+      const u32 pre = block_scan_excl(__popc(x), ws, &tt);
+      if (out_exps && w < w_hi) a.dwp[w] = make_uint2(x, base + pre);
+      auto put = [&](u32 pos, u32 rk) {
+        u16 e[MAXV];
+        unrank_exps(rk, n, a.D, bt, a.st, e);
+        key_store<KW>(out_keys, pos, key_encode<KW>(a.f, e));
+        if (out_exps)
+          for (int v = 0; v < n; ++v) out_exps[((long long)N_all - 1 - pos) * n + v] = e[v];
+      };
+      if (tt <= (u32)CL_LIST) {
+        u32 p = pre, m = x;
+        while (m) {
+          const int b = __ffs(m) - 1;
+          m &= m - 1;
+          list[p++] = w * 32 + b;
+        }
+        __syncthreads();
+        for (u32 q = tid; q < tt; q += blockDim.x) put(base + q, list[q]);
+        __syncthreads();
+      } else {
+        u32 p = base + pre, m = x;
+        while (m) {
+          const int b = __ffs(m) - 1;
+          m &= m - 1;
+          put(p++, w * 32 + b);
+        }
+      }
+      base += tt;
+    }
+  };
+  // ranks of terms [0, len) of the basis polynomial at `off` times the shift
+  // `dl`, chunks sub, sub + k, ... with U chunks in flight per lane
+  auto rank_chunks = [&](u32 off, u32 len, const Key<KW>& dl, u32 sub, u32 k, u32 c, u32* tt, u32* rk) {
+    Key<KW> kk[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      tt[q] = (c + q * k) * 32 + lane;
+      if (tt[q] < len) kk[q] = key_load<KW>(a.bckey, (long long)off + tt[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < U; ++q)
+      if (tt[q] < len) rk[q] = key_rank<KW>(a.f, bt, a.st, key_add<KW>(kk[q], dl));
+  };
+  // Balanced term ranges: terms [t_begin, t_end) of rows [row_lo, row_hi)
+  // (row i owns [rs(i), rs(i) + len_i), rs ascending).  Warp gw takes the
+  // contiguous range [a0, a1) of T terms, finds its first row with a 32-ary
+  // warp search, then walks rows: body(i, rs_i, from, to).
+  auto term_ranges = [&](u32 row_lo, u32 row_hi, u32 t_begin, u32 t_end, auto rs_of, auto body) {
+    if (t_end <= t_begin || row_hi <= row_lo) return;
+    const u32 T = (((t_end - t_begin) + W - 1) / W + 31) & ~31u;
+    const unsigned long long a0l = (unsigned long long)t_begin + (unsigned long long)gw * T;
+    if (a0l >= t_end) return;
+    const u32 a0 = (u32)a0l, a1 = min(t_end, a0 + T);
+    u32 lo = row_lo, hi = row_hi;  // rs(lo) <= a0 < rs(hi)
+    while (hi - lo > 1) {
+      const u32 step = (hi - lo + 31) / 32;
+      const u32 pr = lo + step * (lane + 1);
+      const bool le = pr < hi && rs_of(pr) <= a0;
+      const u32 c = __popc(__ballot_sync(0xffffffffu, le));
+      lo += step * c;
+      hi = min(hi, lo + step);
+    }
+    for (u32 i = lo; i < row_hi; ++i) {
+      const u32 rsi = rs_of(i);
+      if (rsi >= a1) break;
+      body(i, rsi, max(a0, rsi), a1);
+    }
+  };
+
+  // ---- P1: input rows: shift deltas, row table, lead bits, dictionary bits
+  // (balanced term ranges; the first setter of a bit counts it for the
+  // owning word chunk; the warp owning a row's first term writes its entry)
+  term_ranges(0u, (u32)a.r0, 0u, a.M0, [&](u32 i) { return a.start_in[i]; }, [&](u32 i, u32 rsi, u32 from, u32 to) {
+    const int g = a.rb_in[i];
+    u16 e[MAXV], z[MAXV];
+    for (int v = 0; v < n; ++v) {
+      e[v] = a.shift_in[(long long)i * n + v];
+      z[v] = 0;
+    }
+    const Key<KW> dl = key_sub<KW>(key_encode<KW>(a.f, e), key_encode<KW>(a.f, z));
+    const u32 off = __ldg(a.boff + g), len = __ldg(a.blen + g);
+    if (from == rsi && lane == 0) {
+      a.rows_basis[i] = g;
+      key_store<KW>(a.rows_delta, i, dl);
+      a.rows_start[i] = rsi;
+      if (a.closure) {
+        // leads of the input rows are covered (symbolic.py:339)
+        const u32 rk = key_rank<KW>(a.f, bt, a.st, key_add<KW>(key_load<KW>(a.bckey, off), dl));
+        const u32 bit = 1u << (rk & 31);
+        if (!(atomicOr(a.done + (rk >> 5), bit) & bit)) atomicAdd(lcount + (rk >> 5) / cw, 1u);
+      }
+    }
+    const u32 t_lo = from - rsi, t_hi = min(len, to - rsi);
+    for (u32 tb = t_lo; tb < t_hi; tb += 32 * U) {
+      u32 tt[U], rk[U], dw[U];
+      Key<KW> kk[U];
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        tt[q] = tb + q * 32 + lane;
+        if (tt[q] < t_hi) kk[q] = key_load<KW>(a.bckey, (long long)off + tt[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < U; ++q)
+        if (tt[q] < t_hi) rk[q] = key_rank<KW>(a.f, bt, a.st, key_add<KW>(kk[q], dl));
+#pragma unroll
+      for (int q = 0; q < U; ++q) dw[q] = tt[q] < t_hi ? __ldcg(a.dict + (rk[q] >> 5)) : 0xFFFFFFFFu;  // L2 filter
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        if (tt[q] >= t_hi) continue;
+        const u32 w = rk[q] >> 5, bit = 1u << (rk[q] & 31);
+        if (!(dw[q] & bit) && !(atomicOr(a.dict + w, bit) & bit)) atomicAdd(dcount + w / cw, 1u);
+      }
+    }
+  });
+  if (t0th) a.rows_start[a.r0] = a.start_in[a.r0];
+  grid.sync();
+  stamp(384);
+  // ---- P2: dictionary size, round-1 frontier = dict & ~done (every lead is
+  // a dictionary monomial, so the chunk counts are dcount - lcount)
+  u32 nf = 0, N = 0, flags = 0, rounds = 0;
+  {
+    u32 base, dummy;
+    cta_bases([&](u32 b) { return __ldcg(dcount + b); }, dummy, N);
+    if (a.closure) {
+      cta_bases([&](u32 b) { return __ldcg(dcount + b) - __ldcg(lcount + b); }, base, nf);
+      if (nf > a.front_cap) {
+        flags |= LOOP_OVERFLOW;
+      } else {
+        emit_chunk([&](u32 w) {
+          const u32 d = __ldcg(a.dict + w), dn = __ldcg(a.done + w);
+          if (dn) a.done[w] = 0;
+          return d & ~dn;
+        }, base, a.front0, nullptr, 0u);
+      }
+      grid.sync();
+    }
+  }
+  stamp(385);
+  // ---- closure rounds ------------------------------------------------------
+  long long r = a.r0, n_cl = 0;
+  u32 Mcur = a.M0;
+  int sel = 0;
+  while (!flags && nf > 0 && a.nc > 0) {
+    const u64* front = sel ? a.front1 : a.front0;
+    u64* fnext = sel ? a.front0 : a.front1;
+    u32* cur = (rounds & 1) ? cnt_b : cnt_a;
+    u32* nxt = (rounds & 1) ? cnt_a : cnt_b;
+    const bool tr = a.trace && t0th && rounds < 64;
+    if (tr) {
+      a.trace[rounds * 6] = gtimer();
+      a.trace[rounds * 6 + 5] = nf;
+    }
+    // big rounds (nf >= W): search only here, the reducer rows' terms are
+    // ranked after the rows are written, over balanced term ranges (two more
+    // barriers); small rounds rank inside the search groups
+    const bool big = nf >= W;
+    u32 k, j0, j1, sub;
+    groups_of(nf, big ? 1u : CH, k, j0, j1, sub);
+    const bool leader = sub == 0;
+    // ---- AC: reducer search (every warp of the group) + ranking of the
+    // reducer row's terms (chunks split across the group)
+    {
+      u32 cn = 0, cl = 0;
+      for (u32 j = j0; j < j1; ++j) {
+        const Key<KW> m = key_load_cg<KW>(front, j);
+        int found = -1;
+        u16 e[MAXV + 1];
+        key_decode<KW>(a.f, m, e);
+        e[n] = 0;
+        u32 me[MAXV / 2];
+        for (int w = 0; w < a.nw; ++w) me[w] = (u32)e[2 * w] | ((u32)e[2 * w + 1] << 16);
+        for (int b0 = 0; b0 < a.nc; b0 += 32) {
+          const int cc = b0 + lane;
+          bool ok = cc < a.nc;
+          if (ok) {
+            const u32* lm = lmw + (long long)cc * a.nw;
+            for (int w = 0; w < a.nw; ++w) ok &= (__vcmpgeu2(me[w], lm[w]) == 0xFFFFFFFFu);
+          }
+          const unsigned bm = __ballot_sync(0xffffffffu, ok);
+          if (bm) {
+            found = a.cidx[b0 + __ffs(bm) - 1];
+            break;
+          }
+        }
+        if (leader) {
+          if (lane == 0) a.red[j] = found;
+          if (found >= 0) {
+            ++cn;
+            cl += __ldg(a.blen + found);
+          }
+        }
+        if (found < 0 || big) continue;
+        const u32 off = __ldg(a.boff + found), len = __ldg(a.blen + found);
+        const Key<KW> dl = key_sub<KW>(m, key_load<KW>(a.bckey, off));
+        for (u32 c = sub; c * 32 < len; c += U * k) {
+          u32 tt[U], rk[U], dw[U];
+          rank_chunks(off, len, dl, sub, k, c, tt, rk);
+#pragma unroll
+          for (int q = 0; q < U; ++q)
+            dw[q] = tt[q] < len ? (__ldcg(a.dict + (rk[q] >> 5)) | __ldcg(a.newbits + (rk[q] >> 5))) : 0xFFFFFFFFu;
+#pragma unroll
+          for (int q = 0; q < U; ++q) {
+            if (tt[q] >= len) continue;
+            const u32 w = rk[q] >> 5, bit = 1u << (rk[q] & 31);
+            if (!(dw[q] & bit) && !(atomicOr(a.newbits + w, bit) & bit)) atomicAdd(cur + w / cw, 1u);
+          }
+        }
+      }
+      if (lane == 0) {
+        s_wn[warp] = cn;
+        s_wl[warp] = cl;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        u32 sn = 0, sl = 0;
+        for (int q = 0; q < NWARP; ++q) {
+          sn += s_wn[q];
+          sl += s_wl[q];
+        }
+        a.tilecnt[2 * blockIdx.x] = sn;
+        a.tilecnt[2 * blockIdx.x + 1] = sl;
+      }
+    }
+    grid.sync();
+    if (tr) a.trace[rounds * 6 + 1] = gtimer();
+    // ---- BD: totals, this warp's row / term bases
+    u32 R, Mk, bn, bl;
+    {
+      u32 tn = 0, tl = 0, pn = 0, pl = 0;
+      for (u32 b = tid; b < G; b += blockDim.x) {
+        const uint2 v = __ldcg(reinterpret_cast<const uint2*>(a.tilecnt) + b);
+        tn += v.x;
+        tl += v.y;
+        if (b < blockIdx.x) {
+          pn += v.x;
+          pl += v.y;
+        }
+      }
+      R = block_sum_u32(tn, ws);
+      Mk = block_sum_u32(tl, ws);
+      bn = block_sum_u32(pn, ws);
+      bl = block_sum_u32(pl, ws);
+      for (int q = 0; q < warp; ++q) {
+        bn += s_wn[q];
+        bl += s_wl[q];
+      }
+    }
+    if (R == 0) break;
+    if (r + R + 1 > a.rows_cap || n_cl + R > a.cl_cap) {
+      flags |= LOOP_OVERFLOW;
+      break;
+    }
+    if ((unsigned long long)Mcur + Mk >= (1ull << 30)) {
+      flags |= LOOP_SIZE_CAP;
+      break;
+    }
+    if (t0th) a.rows_start[r + R] = Mcur + Mk;
+    // B: the group's rows, in frontier order (leader warp)
+    if (leader) {
+      for (u32 jb = j0; jb < j1; jb += 32) {
+        const u32 j = jb + lane;
+        const int g = j < j1 ? __ldcg(a.red + j) : -1;
+        const u32 len = g >= 0 ? __ldg(a.blen + g) : 0u;
+        const unsigned bm = __ballot_sync(0xffffffffu, g >= 0);
+        u32 lp = len;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const u32 y = __shfl_up_sync(0xffffffffu, lp, o);
+          if (lane >= o) lp += y;
+        }
+        const u32 ltot = __shfl_sync(0xffffffffu, lp, 31);
+        if (g >= 0) {
+          const long long q = (long long)bn + __popc(bm & lanemask_lt());
+          const long long row = r + q;
+          const Key<KW> m = key_load_cg<KW>(front, j);
+          a.rows_basis[row] = g;
+          key_store<KW>(a.rows_delta, row, key_sub<KW>(m, key_load<KW>(a.bckey, __ldg(a.boff + g))));
+          a.rows_start[row] = Mcur + bl + lp - len;
+          u16 e[MAXV];
+          key_decode<KW>(a.f, m, e);
+          bool over = false;
+          for (int v = 0; v < n; ++v) {
+            const u32 sft = (u32)e[v] - (u32)a.lmexp[(long long)g * n + v];
+            over |= (sft + (u32)a.maxe[(long long)g * n + v]) > 0xFFFFu;
+            a.cl_shift[(n_cl + q) * n + v] = (u16)sft;
+          }
+          if (over) atomicOr(a.err, (u32)DEVERR_LANE_OVERFLOW);
+          a.cl_basis[n_cl + q] = g;
+          a.cl_round[n_cl + q] = (int)rounds + 1;
+        }
+        bn += __popc(bm);
+        bl += ltot;
+      }
+    }
+    if (big) {
+      grid.sync();
+      if (tr) a.trace[rounds * 6 + 2] = gtimer();
+      // C: the new rows' terms -> rank -> absent monomials into newbits
+      term_ranges((u32)r, (u32)(r + R), Mcur, Mcur + Mk, [&](u32 i) { return __ldcg(a.rows_start + i); },
+                  [&](u32 i, u32 rsi, u32 from, u32 to) {
+        const int g = __ldcg(a.rows_basis + i);
+        const u32 off = __ldg(a.boff + g), len = __ldg(a.blen + g);
+        const Key<KW> dl = key_load_cg<KW>(a.rows_delta, i);
+        const u32 t_lo = from - rsi, t_hi = min(len, to - rsi);
+        for (u32 tb = t_lo; tb < t_hi; tb += 32 * U) {
+          u32 tt[U], rk[U], dw[U];
+          Key<KW> kk[U];
+#pragma unroll
+          for (int q = 0; q < U; ++q) {
+            tt[q] = tb + q * 32 + lane;
+            if (tt[q] < t_hi) kk[q] = key_load<KW>(a.bckey, (long long)off + tt[q]);
+          }
+#pragma unroll
+          for (int q = 0; q < U; ++q)
+            if (tt[q] < t_hi) rk[q] = key_rank<KW>(a.f, bt, a.st, key_add<KW>(kk[q], dl));
+#pragma unroll
+          for (int q = 0; q < U; ++q)
+            dw[q] = tt[q] < t_hi ? (__ldcg(a.dict + (rk[q] >> 5)) | __ldcg(a.newbits + (rk[q] >> 5))) : 0xFFFFFFFFu;
+#pragma unroll
+          for (int q = 0; q < U; ++q) {
+            if (tt[q] >= t_hi) continue;
+            const u32 w = rk[q] >> 5, bit = 1u << (rk[q] & 31);
+            if (!(dw[q] & bit) && !(atomicOr(a.newbits + w, bit) & bit)) atomicAdd(cur + w / cw, 1u);
+          }
+        }
+      });
+      grid.sync();
+      if (tr) a.trace[rounds * 6 + 3] = gtimer();
+    }
+    u32 base, total;
+    cta_bases([&](u32 b) { return __ldcg(cur + b); }, base, total);
+    if (total > a.front_cap) {
+      flags |= LOOP_OVERFLOW;
+      break;
+    }
+    // D: next frontier from this CTA's chunk; dict |= newbits; newbits = 0
+    emit_chunk([&](u32 w) {
+      const u32 nb = __ldcg(a.newbits + w);
+      if (!nb) return 0u;
+      const u32 d = __ldcg(a.dict + w);
+      a.dict[w] = d | nb;
+      a.newbits[w] = 0;
+      return nb & ~d;
+    }, base, fnext, nullptr, 0u);
+    if (tid == 0) {
+      dcount[blockIdx.x] += __ldcg(cur + blockIdx.x);
+      nxt[blockIdx.x] = 0;
+    }
+    r += R;
+    n_cl += R;
+    Mcur += Mk;
+    ++rounds;
+    nf = total;
+    N += total;
+    sel ^= 1;
+    if ((long long)N > a.dict_cap) flags |= LOOP_DICT_CAP;
+    grid.sync();
+    if (tr) a.trace[(rounds - 1) * 6 + 4] = gtimer();
+  }
+  if (t0th) t_epi = gtimer();
+  if (!flags && (N > a.N_cap || Mcur > a.M_cap || r + 1 > a.rows_cap)) flags |= LOOP_OVERFLOW;
+  if (!flags) {
+    // ---- P3: final dictionary (the map is cleared behind us)
+    u32 base, tot;
+    cta_bases([&](u32 b) { return __ldcg(dcount + b); }, base, tot);
+    emit_chunk([&](u32 w) {
+      const u32 d = __ldcg(a.dict + w);
+      if (d) a.dict[w] = 0;
+      return d;
+    }, base, a.dict_out, a.dict_exps, N);
+    grid.sync();
+    stamp(387);
+    // ---- P4: join: col = N - 1 - (prefix[rank >> 5] + popc(word & below))
+    bool miss = false;
+    term_ranges(0u, (u32)r, 0u, Mcur, [&](u32 i) { return __ldcg(a.rows_start + i); },
+                [&](u32 i, u32 rsi, u32 from, u32 to) {
+      const int g = __ldcg(a.rows_basis + i);
+      const u32 off = __ldg(a.boff + g), len = __ldg(a.blen + g);
+      const Key<KW> dl = key_load_cg<KW>(a.rows_delta, i);
+      const u32 t_lo = from - rsi, t_hi = min(len, to - rsi);
+      for (u32 tb = t_lo; tb < t_hi; tb += 32 * U) {
+        u32 tt[U], rk[U], cf[U];
+        uint2 dw[U];
+        Key<KW> kk[U];
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+          tt[q] = tb + q * 32 + lane;
+          if (tt[q] < t_hi) {
+            kk[q] = key_load<KW>(a.bckey, (long long)off + tt[q]);
+            cf[q] = __ldg(a.bcoeff + off + tt[q]);
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < U; ++q)
+          if (tt[q] < t_hi) rk[q] = key_rank<KW>(a.f, bt, a.st, key_add<KW>(kk[q], dl));
+#pragma unroll
+        for (int q = 0; q < U; ++q)
+          if (tt[q] < t_hi) dw[q] = __ldcg(a.dwp + (rk[q] >> 5));
+#pragma unroll
+        for (int q = 0; q < U; ++q)
+          if (tt[q] < t_hi) {
+            const u32 sh = rk[q] & 31;
+            if (!((dw[q].x >> sh) & 1u)) miss = true;
+            a.col[rsi + tt[q]] = N - 1 - (dw[q].y + __popc(dw[q].x & ((1u << sh) - 1u)));
+            a.val[rsi + tt[q]] = cf[q];
+          }
+      }
+    });
+    if (miss) atomicOr(a.err, (u32)DEVERR_MISSING_KEY);
+  }
+  if (t0th) {
+    LoopOut o;
+    o.r = (u32)r;
+    o.n_cl = (u32)n_cl;
+    o.M = Mcur;
+    o.N = N;
+    o.rounds = rounds;
+    o.nf = nf;
+    o.flags = flags;
+    o.sel = (u32)sel;
+    o.t_start = t_start;
+    o.t_epi = t_epi;
+    o.t_end = gtimer();
     *a.out = o;
   }
 }
@@ -1582,6 +2375,298 @@ static bool rank_path_ok(int order, int n, long long D) {
     if (!strcmp(e, "sort")) return false;
   }
   return binom_ull(n + (int)D, n) <= (1ull << 26);
+}
+
+// ===========================================================================
+// Fused rank-path compile: ONE cooperative launch runs round 0, every closure
+// round, the final dictionary and the join (k_closure_loop with full = 1);
+// the host packs its inputs into one page-locked upload and reads the
+// counters back once.  Plan buffers are sized from capacity hints; an
+// overflow (flagged by the kernel) grows the hints and recompiles.
+// ===========================================================================
+template <int KW>
+static void compile_rank_fused(Ctx* c, const KeyFmt& f, int D, long long r0, const int32_t* h_rb,
+                               const uint16_t* h_shift, int closure, const std::vector<int32_t>& cand,
+                               long long dict_cap, f4b_plan* pl) {
+  Basis& B = c->basis;
+  const int n = c->n_vars;
+  c->launches = 0;
+  static const bool htrace = getenv("F4B_HOST_TRACE") != nullptr;
+  const auto h0 = std::chrono::steady_clock::now();
+  std::vector<std::pair<const char*, double>> hmarks;
+  auto mark = [&](const char* what) {
+    if (htrace)
+      hmarks.push_back({what, std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count()});
+  };
+  cudaEvent_t ev0, ev1;
+  check_cuda(cudaEventCreate(&ev0), "event");
+  check_cuda(cudaEventCreate(&ev1), "event");
+  check_cuda(cudaEventRecord(ev0, c->stream), "event record");
+  encode_basis<KW>(c, f);
+
+  const int st = n + 1;
+  const int rows_bt = D + n + 2;
+  const int bt_words = rows_bt * st;
+  const unsigned long long Rsp = binom_ull(n + D, n);
+  const u32 words = (u32)((Rsp + 31) / 32);
+
+  long long M = 0;
+  for (long long i = 0; i < r0; ++i) M += B.h_len[h_rb[i]];
+  if (M >= (1ll << 30)) fail(F4B_ERR_SIZE_CAP, "batch has more than 2^30 terms");
+  const u32 M0 = (u32)M;
+
+  // candidate LMs in preference order (key(LM), index) (symbolic.py:228-235)
+  std::vector<int32_t> pref;
+  if (closure) pref = preference_order(c, cand);
+  mark("pref sort");
+  const int nc = closure ? (int)pref.size() : 0;
+  const int nw = (n + 1) / 2;
+  u32 maxlen = 1;
+  for (int32_t k : pref) maxlen = std::max<u32>(maxlen, (u32)B.h_len[k]);
+
+  // one page-locked staging block: binomials | rb | row starts | shifts | LM table | candidate ids
+  auto al = [](size_t x) { return (x + 15) & ~(size_t)15; };
+  const size_t o_bt = 0, o_rb = o_bt + al((size_t)bt_words * 4), o_st = o_rb + al((size_t)r0 * 4),
+               o_sh = o_st + al((size_t)(r0 + 1) * 4), o_lm = o_sh + al((size_t)r0 * n * 2),
+               o_ci = o_lm + al((size_t)std::max(nc, 1) * nw * 4), stage_bytes = o_ci + al((size_t)std::max(nc, 1) * 4);
+  if (c->h_stage_cap < stage_bytes) {
+    if (c->h_stage) cudaFreeHost(c->h_stage);
+    c->h_stage = nullptr;
+    c->h_stage_cap = 0;
+    const size_t cap = std::max<size_t>(stage_bytes + stage_bytes / 2, 1 << 20);
+    check_cuda(cudaHostAlloc(&c->h_stage, cap, cudaHostAllocDefault), "cudaHostAlloc stage");
+    c->h_stage_cap = cap;
+  }
+  unsigned char* hs = static_cast<unsigned char*>(c->h_stage);
+  {
+    u32* hbt = reinterpret_cast<u32*>(hs + o_bt);
+    for (int x = 0; x < rows_bt; ++x)
+      for (int y = 0; y <= n; ++y) hbt[(size_t)x * st + y] = (u32)std::min<unsigned long long>(binom_ull(x, y), 0xFFFFFFFFull);
+    memcpy(hs + o_rb, h_rb, (size_t)r0 * 4);
+    u32* hst = reinterpret_cast<u32*>(hs + o_st);
+    u32 acc = 0;
+    for (long long i = 0; i < r0; ++i) {
+      hst[i] = acc;
+      acc += (u32)B.h_len[h_rb[i]];
+    }
+    hst[r0] = acc;
+    memcpy(hs + o_sh, h_shift, (size_t)r0 * n * 2);
+    u32* hlm = reinterpret_cast<u32*>(hs + o_lm);
+    memset(hlm, 0, (size_t)std::max(nc, 1) * nw * 4);
+    for (int q = 0; q < nc; ++q)
+      for (int v = 0; v < n; ++v) hlm[(size_t)q * nw + v / 2] |= (u32)B.h_lm[(size_t)pref[q] * n + v] << (16 * (v & 1));
+    if (nc) memcpy(hs + o_ci, pref.data(), (size_t)nc * 4);
+  }
+  ensure(c, c->dstage, stage_bytes);
+  check_cuda(cudaMemcpyAsync(c->dstage.p, hs, stage_bytes, cudaMemcpyHostToDevice, c->stream), "h2d stage");
+  unsigned char* ds = c->dstage.as<unsigned char>();
+  mark("stage packed + h2d");
+
+  // capacities
+  const long long cap = (long long)std::min<unsigned long long>(
+      Rsp + 1, (unsigned long long)std::max<long long>({1ll << 16, c->closure_cap_hint, 2 * r0}));
+  const long long rows_cap = r0 + (closure ? cap : 0) + 1;
+  const long long M_cap = std::min<long long>((1ll << 30) + 1, std::max<long long>({3ll * M0 + (1 << 16), c->m_cap_hint}));
+  const long long N_cap = (long long)std::min<unsigned long long>(
+      Rsp + 1, (unsigned long long)std::max<long long>({1ll << 16, c->n_cap_hint}));
+  ensure(c, c->rows_basis, rows_cap * sizeof(int));
+  ensure(c, c->rows_delta, rows_cap * KW * sizeof(u64));
+  ensure(c, pl->row_ptr, (size_t)(rows_cap + 1) * sizeof(u32));
+  ensure(c, pl->col_ind, (size_t)M_cap * sizeof(u32));
+  ensure(c, pl->val, (size_t)M_cap * sizeof(u32));
+  ensure(c, pl->dict, (size_t)N_cap * KW * sizeof(u64));
+  ensure(c, pl->dict_exps, (size_t)N_cap * n * sizeof(u16));
+  const long long clc = closure ? cap : 1;
+  ensure(c, pl->cl_basis, clc * sizeof(int));
+  ensure(c, pl->cl_shift, clc * n * sizeof(u16));
+  ensure(c, pl->cl_round, clc * sizeof(int));
+  ensure(c, c->front, (size_t)cap * KW * sizeof(u64));
+  ensure(c, c->front_new, (size_t)cap * KW * sizeof(u64));
+  ensure(c, c->red, (size_t)cap * sizeof(int));
+  ensure(c, c->errflag, sizeof(DevCounters) + 4096);
+  DevCounters* dc = reinterpret_cast<DevCounters*>(c->errflag.p);
+  LoopOut* d_out = reinterpret_cast<LoopOut*>(dc + 1);
+  check_cuda(cudaMemsetAsync(dc, 0, sizeof(DevCounters), c->stream), "memset counters");
+
+  const int stage_lm = (size_t)nc * nw * 4 <= 48 * 1024 ? 1 : 0;
+  const size_t lsm = ((size_t)((bt_words + 3) & ~3) + CL_LIST) * 4 + (stage_lm ? (size_t)nc * nw * 4 : 0);
+  static bool lattr = false;
+  if (!lattr) {
+    check_cuda(cudaFuncSetAttribute(k_fbsp<KW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024), "attr");
+    lattr = true;
+  }
+  static int bps_cached = -1;
+  static size_t bps_smem = 0;
+  if (bps_cached < 0 || bps_smem != lsm) {
+    check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps_cached, k_fbsp<KW>, CL_THREADS, lsm), "occupancy");
+    bps_smem = lsm;
+  }
+  static const int bps_max = getenv("F4B_LOOP_BPS") ? atoi(getenv("F4B_LOOP_BPS")) : 2;
+  const int G = c->num_sms * std::max(1, std::min(bps_cached, bps_max));
+  const size_t W = (size_t)G * (CL_THREADS / 32);
+  ensure(c, c->loop_scratch, (2 * W + 16) * sizeof(u32));
+  // presence maps dict | done | newbits: zero on entry (kept zero by the
+  // kernel; cleared here after growth or an aborted run)
+  const size_t maps_bytes = ((size_t)3 * words + 64) * 4;
+  if (c->maps.cap < maps_bytes) c->maps_clean = 0;
+  ensure(c, c->maps, maps_bytes);
+  if (c->maps_clean < maps_bytes) {
+    check_cuda(cudaMemsetAsync(c->maps.p, 0, c->maps.cap, c->stream), "memset maps");
+    c->maps_clean = c->maps.cap;
+  }
+  u32* d_dict = c->maps.as<u32>();
+  u32* d_done = d_dict + words;
+  u32* d_new = d_done + words;
+  // chunk counters: set `parity` for this call (zero), the other set is
+  // cleared by the kernel for the next call
+  if (c->fcnt_G != G || !c->fcnt.p) {
+    ensure(c, c->fcnt, (size_t)8 * G * sizeof(u32));
+    check_cuda(cudaMemsetAsync(c->fcnt.p, 0, (size_t)8 * G * sizeof(u32), c->stream), "memset counters");
+    c->fcnt_G = G;
+    c->fcnt_parity = 0;
+  }
+  u32* d_cnt = c->fcnt.as<u32>() + (size_t)4 * G * c->fcnt_parity;
+  u32* d_cnt_next = c->fcnt.as<u32>() + (size_t)4 * G * (1 - c->fcnt_parity);
+  c->fcnt_parity ^= 1;
+  ensure(c, c->dwp, (size_t)(words + 1) * sizeof(uint2));
+
+  FbspArgs fa;
+  memset(&fa, 0, sizeof(fa));
+  fa.f = f;
+  fa.D = D;
+  fa.st = st;
+  fa.bt_words = bt_words;
+  fa.closure = closure;
+  fa.nc = nc;
+  fa.nw = nw;
+  fa.stage_lm = stage_lm;
+  {
+    // L2 prefetch of the basis streams when they fit comfortably (126 MB L2)
+    const unsigned long long bytes = (unsigned long long)B.n_terms * (KW * 8 + 4);
+    fa.prefetch_terms = bytes <= (48ull << 20) && !getenv("F4B_NO_PREFETCH") ? (unsigned long long)B.n_terms : 0ull;
+  }
+  fa.words = words;
+  fa.maxlen = maxlen;
+  fa.front_cap = (u32)cap;
+  fa.N_cap = (u32)std::min<long long>(N_cap, 0xFFFFFFFFll);
+  fa.M_cap = (u32)std::min<long long>(M_cap, 0xFFFFFFFFll);
+  fa.M0 = M0;
+  fa.r0 = r0;
+  fa.rows_cap = rows_cap;
+  fa.cl_cap = clc;
+  fa.dict_cap = dict_cap;
+  fa.bt = reinterpret_cast<const u32*>(ds + o_bt);
+  fa.rb_in = reinterpret_cast<const int*>(ds + o_rb);
+  fa.start_in = reinterpret_cast<const u32*>(ds + o_st);
+  fa.shift_in = reinterpret_cast<const u16*>(ds + o_sh);
+  fa.lmw = reinterpret_cast<const u32*>(ds + o_lm);
+  fa.cidx = reinterpret_cast<const int*>(ds + o_ci);
+  fa.boff = B.off.as<u32>();
+  fa.blen = B.len.as<u32>();
+  fa.bckey = B.ckey.as<u64>();
+  fa.bcoeff = B.coeff.as<u32>();
+  fa.lmexp = B.lmexp.as<u16>();
+  fa.maxe = B.maxe.as<u16>();
+  fa.dict = d_dict;
+  fa.done = d_done;
+  fa.newbits = d_new;
+  fa.dwp = c->dwp.as<uint2>();
+  fa.front0 = c->front.as<u64>();
+  fa.front1 = c->front_new.as<u64>();
+  fa.red = c->red.as<int>();
+  fa.tilecnt = c->loop_scratch.as<u32>();
+  fa.cnt = d_cnt;
+  fa.cnt_next = d_cnt_next;
+  fa.rows_basis = c->rows_basis.as<int>();
+  fa.rows_delta = c->rows_delta.as<u64>();
+  fa.rows_start = pl->row_ptr.as<u32>();
+  fa.cl_basis = pl->cl_basis.as<int>();
+  fa.cl_shift = pl->cl_shift.as<u16>();
+  fa.cl_round = pl->cl_round.as<int>();
+  fa.dict_out = pl->dict.as<u64>();
+  fa.dict_exps = pl->dict_exps.as<u16>();
+  fa.col = pl->col_ind.as<u32>();
+  fa.val = pl->val.as<u32>();
+  fa.err = &dc->err;
+  fa.out = d_out;
+  static const bool trace_on = getenv("F4B_LOOP_TRACE") != nullptr;
+  DBuf trb;
+  if (trace_on) {
+    ensure(c, trb, 400 * 8);
+    check_cuda(cudaMemsetAsync(trb.p, 0, 400 * 8, c->stream), "memset");
+    fa.trace = trb.as<unsigned long long>();
+  }
+  {
+    void* args[] = {&fa};
+    ProfScope ps(c, "k_fbsp");
+    check_cuda(cudaLaunchCooperativeKernel((void*)k_fbsp<KW>, G, CL_THREADS, args, lsm, c->stream), "k_fbsp");
+  }
+  mark("launched");
+  check_cuda(cudaEventRecord(ev1, c->stream), "event record");
+  check_cuda(cudaMemcpyAsync(c->h_stat, dc, sizeof(DevCounters) + sizeof(LoopOut), cudaMemcpyDeviceToHost, c->stream),
+             "d2h");
+  check_cuda(cudaStreamSynchronize(c->stream), "sync");
+  mark("synced");
+  if (htrace) {
+    fprintf(stderr, "[host] r0=%lld M0=%u:", r0, M0);
+    for (auto& m : hmarks) fprintf(stderr, " %s @%.1f |", m.first, m.second);
+    fprintf(stderr, "\n");
+  }
+  DevCounters hc;
+  LoopOut ho;
+  memcpy(&hc, c->h_stat, sizeof(DevCounters));
+  memcpy(&ho, reinterpret_cast<unsigned char*>(c->h_stat) + sizeof(DevCounters), sizeof(LoopOut));
+  if (trace_on) {
+    std::vector<unsigned long long> ht(400);
+    check_cuda(cudaMemcpy(ht.data(), trb.p, ht.size() * 8, cudaMemcpyDeviceToHost), "d2h");
+    auto us = [&](unsigned long long a1, unsigned long long b1) { return a1 && b1 ? (b1 - a1) / 1e3 : -1.0; };
+    fprintf(stderr, "[fused] G=%d nc=%d r0=%lld M0=%u rounds=%u N=%u M=%u | P1 %.1f P2 %.1f | loop %.1f | P3 %.1f P4 %.1f us\n",
+            G, nc, r0, M0, ho.rounds, ho.N, ho.M, us(ho.t_start, ht[384]), us(ht[384], ht[385]),
+            us(ht[385], ho.t_epi), us(ho.t_epi, ht[387]), us(ht[387], ho.t_end));
+    for (u32 q = 0; q < std::min<u32>(ho.rounds + 1, 64); ++q) {
+      const unsigned long long* t = &ht[q * 6];
+      if (!t[0]) break;
+      fprintf(stderr, "[fused]  rnd %u nf=%llu AC=%.1fus BD=%.1fus (B %.1f C %.1f)\n", q, t[5], us(t[0], t[1]),
+              us(t[1], t[4]), us(t[1], t[2]), us(t[2], t[3]));
+    }
+    release(c, trb);
+  }
+  float ms = 0;
+  check_cuda(cudaEventElapsedTime(&ms, ev0, ev1), "elapsed");
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
+  if (ho.flags) {
+    // aborted run: maps and counters may be dirty
+    c->maps_clean = 0;
+    c->fcnt_G = 0;
+  }
+  if (ho.flags & LOOP_OVERFLOW) {
+    c->closure_cap_hint = std::max<long long>(4 * cap, c->closure_cap_hint);
+    c->m_cap_hint = std::max<long long>(c->m_cap_hint, std::max<long long>(2 * M_cap, (long long)ho.M + ho.M / 4));
+    c->n_cap_hint = std::max<long long>(c->n_cap_hint, std::max<long long>(2 * N_cap, (long long)ho.N + ho.N / 4));
+    compile_rank_fused<KW>(c, f, D, r0, h_rb, h_shift, closure, cand, dict_cap, pl);
+    return;
+  }
+  if (ho.flags & LOOP_SIZE_CAP) fail(F4B_ERR_SIZE_CAP, "batch has more than 2^30 terms");
+  if (ho.flags & LOOP_DICT_CAP)
+    fail(F4B_ERR_SIZE_CAP, "dictionary exceeded the cap after " + std::to_string(ho.rounds) + " closure rounds");
+  if (hc.err & DEVERR_LANE_OVERFLOW) fail(F4B_ERR_LANE_OVERFLOW, "shifted exponent overflows a 16-bit lane");
+  if (hc.err & DEVERR_MISSING_KEY) fail(F4B_ERR_MISSING_KEY, "row key absent from dictionary (closure defect)");
+  // remember the sizes so later batches rarely overflow
+  c->m_cap_hint = std::max<long long>(c->m_cap_hint, (long long)ho.M + ho.M / 4);
+  c->n_cap_hint = std::max<long long>(c->n_cap_hint, (long long)ho.N + ho.N / 4);
+  pl->KW = KW;
+  pl->lane_bits = f.lane_bits;
+  pl->r = ho.r;
+  pl->r0 = r0;
+  pl->N = ho.N;
+  pl->M = ho.M;
+  pl->closure_rounds = ho.rounds;
+  pl->sort_passes = 0;
+  const double asm_ns = ho.t_end > ho.t_epi ? (double)(ho.t_end - ho.t_epi) : 0.0;
+  pl->asm_ns = (int64_t)asm_ns;
+  pl->dict_ns = (int64_t)std::max(0.0, ms * 1e6 - asm_ns);
+  pl->launches = c->launches;
 }
 
 template <int KW>
@@ -1777,6 +2862,7 @@ static void compile_rank(Ctx* c, const KeyFmt& f, int D, long long r0, const int
       LoopOut* d_out = reinterpret_cast<LoopOut*>(dc + 1);
       check_cuda(cudaMemsetAsync(d_aux, 0, (size_t)words * 4, c->stream), "memset newbits");
       LoopArgs la;
+      memset(&la, 0, sizeof(la));
       la.f = f;
       la.D = D;
       la.st = st;
@@ -2039,11 +3125,22 @@ void compile_batch(Ctx* c, long long r0, const int32_t* rb, const uint16_t* shif
   while (64 * KW < bits) KW *= 2;
   if (KW > 8) fail(F4B_ERR_PRECONDITION, "batch degree too large for the device key format");
   if (rank_path_ok(c->order, n, D)) {
-    switch (KW) {
-      case 1: compile_rank<1>(c, f, (int)D, r0, rb, shift, closure, cand, dict_cap, pl); break;
-      case 2: compile_rank<2>(c, f, (int)D, r0, rb, shift, closure, cand, dict_cap, pl); break;
-      case 4: compile_rank<4>(c, f, (int)D, r0, rb, shift, closure, cand, dict_cap, pl); break;
-      default: compile_rank<8>(c, f, (int)D, r0, rb, shift, closure, cand, dict_cap, pl); break;
+    // F4B_FBSP=multi: the multi-launch pipeline (kept as a cross-check)
+    static const bool multi = getenv("F4B_FBSP") && !strcmp(getenv("F4B_FBSP"), "multi");
+    if (multi) {
+      switch (KW) {
+        case 1: compile_rank<1>(c, f, (int)D, r0, rb, shift, closure, cand, dict_cap, pl); break;
+        case 2: compile_rank<2>(c, f, (int)D, r0, rb, shift, closure, cand, dict_cap, pl); break;
+        case 4: compile_rank<4>(c, f, (int)D, r0, rb, shift, closure, cand, dict_cap, pl); break;
+        default: compile_rank<8>(c, f, (int)D, r0, rb, shift, closure, cand, dict_cap, pl); break;
+      }
+    } else {
+      switch (KW) {
+        case 1: compile_rank_fused<1>(c, f, (int)D, r0, rb, shift, closure, cand, dict_cap, pl); break;
+        case 2: compile_rank_fused<2>(c, f, (int)D, r0, rb, shift, closure, cand, dict_cap, pl); break;
+        case 4: compile_rank_fused<4>(c, f, (int)D, r0, rb, shift, closure, cand, dict_cap, pl); break;
+        default: compile_rank_fused<8>(c, f, (int)D, r0, rb, shift, closure, cand, dict_cap, pl); break;
+      }
     }
     return;
   }
