@@ -248,27 +248,38 @@ class ClockSampler:
                 "samples": len(inside), "note": note}
 
 
-# Algorithmic (compulsory) bytes per kernel per batch — DESIGN.md §4.
-#   k_rank_join / k_join_gen : read every term's source key + coefficient,
-#                              write col_ind + val            M(8KW+4) + 8M
-#   k_rank_fill / k_tile_dict: read every term's source key   M * 8KW
-#   k_sweep<0>               : read the C and A rows once, write D'
-#                              8M + 4|C|K
-#   k_dense_forward          : read + write D' once           8|C|K
-SYMBOLIC = ("k_rank_", "k_tile_dict", "k_join_gen", "k_os_", "k_small_sort", "k_unique_absent", "k_closure",
-            "k_new_rows", "k_merge_corank", "k_rows0", "k_encode_basis", "k_mark_leads", "k_front0", "k_dict_exps")
+# Algorithmic bytes per kernel per batch — DESIGN.md §4.
+#   k_fbsp (whole compile_batch) : B_sym of SURVEY.md §8(d): every term's
+#                                  source key + coefficient in, col_ind + val
+#                                  out, row_ptr, the dictionary
+#                                  M(8W+4) + 8M + 4(r+1) + 8W N
+#   k_sweep<0> (C rows by A)     : every pivot-row application streams the
+#                                  pivot tail (u32 col + u32 val) and its
+#                                  16-byte descriptor; the C rows are read
+#                                  and D' is written once
+#                                  8 tail_nnz + 16 pivots + 8 nnz(C) + 4|C|K
+#                                  (pivot rows are reused across C rows, so
+#                                  this stream is L2-served, not HBM)
+#   k_dense_forward              : read + write D' once       8|C|K
+SYMBOLIC = ("k_fbsp", "k_rank_", "k_tile_dict", "k_join_gen", "k_os_", "k_small_sort", "k_unique_absent",
+            "k_closure", "k_new_rows", "k_merge_corank", "k_rows0", "k_encode_basis", "k_mark_leads", "k_front0",
+            "k_dict_exps")
 
 
 def kernel_bytes(name, b, pinfo, einfo):
     M = b["M"]
     KW = pinfo["key_words"]
     C, K = einfo["dense_rows"], einfo["dense_cols"]
+    if name.startswith("k_fbsp"):
+        return M * (8 * KW + 4) + 8 * M + 4 * (b["r"] + 1) + 8 * KW * b["N"]
     if name.startswith(("k_rank_join", "k_join_gen")):
         return M * (8 * KW + 4) + 8 * M
     if name.startswith(("k_rank_fill", "k_tile_dict")):
         return M * 8 * KW
-    if name == "k_sweep<0>":
-        return 8 * M + 4 * C * K
+    if "k_sweep<0" in name or "k_sweep<MODE" in name:
+        # C-row share of the nonzeros: |C| rows of mean length M / r
+        c_nnz = int(C * M / max(1, b["r"]))
+        return 8 * einfo["sweep_tail_nnz"] + 16 * einfo["sweep_pivots"] + 8 * c_nnz + 4 * C * K
     if name == "k_dense_forward":
         return 8 * C * K
     return None
@@ -292,9 +303,13 @@ def roofline_for(kprof, records, peak, peak_src, want):
                     "traffic": None, "launches": cnt, "avg_launch_us": ns / cnt / 1e3, "share_of_step": ns / total,
                     "note": "no algorithmic byte model (schedule-dependent work)"}
         ach = tot / (ns * 1e-9) / 1e9
-        return {"bound": "hbm", "kernel": name, "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                "traffic": None, "launches": cnt, "avg_launch_us": ns / cnt / 1e3, "peak_source": peak_src,
-                "share_of_step": ns / total, "algorithmic_bytes_per_launch": tot / cnt}
+        out = {"bound": "hbm", "kernel": name, "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+               "traffic": None, "launches": cnt, "avg_launch_us": ns / cnt / 1e3, "peak_source": peak_src,
+               "share_of_step": ns / total, "algorithmic_bytes_per_launch": tot / cnt}
+        if "k_sweep" in name:
+            out["note"] = ("pivot-row stream is L2-resident (rows reused by every C row); "
+                           "latency-bound: one CTA barrier per pivot application")
+        return out
     return None
 
 
