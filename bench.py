@@ -276,7 +276,7 @@ def kernel_bytes(name, b, pinfo, einfo):
         return M * (8 * KW + 4) + 8 * M
     if name.startswith(("k_rank_fill", "k_tile_dict")):
         return M * 8 * KW
-    if "k_sweep<0" in name or "k_sweep<MODE" in name:
+    if "k_sweep" in name:
         # C-row share of the nonzeros: |C| rows of mean length M / r
         c_nnz = int(C * M / max(1, b["r"]))
         return 8 * einfo["sweep_tail_nnz"] + 16 * einfo["sweep_pivots"] + 8 * c_nnz + 4 * C * K

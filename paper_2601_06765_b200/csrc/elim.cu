@@ -27,6 +27,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "common.cuh"
@@ -49,6 +50,7 @@ struct f4b_echelon {
   f4b::DBuf desc;      // uint4 [N] (tail start, tail end, inverse lead, pivot row)
   f4b::DBuf abits;     // u32 [(N+31)/32] A-column bitmap
   f4b::DBuf acols;     // u32 [nA] A columns ascending
+  f4b::DBuf apos;      // u32 [N] index of each A column in acols
   f4b::DBuf nonA;      // u32 [K] non-A columns ascending
   f4b::DBuf Rd;        // u32 [rankD * K] RREF(D') rows (dense, non-A coordinates)
   f4b::DBuf dpiv;      // u32 [rankD] D' pivot positions (non-A coordinates)
@@ -341,6 +343,242 @@ __global__ void __launch_bounds__(SW_THREADS) k_sweep(
 }
 
 // ---------------------------------------------------------------------------
+// E2, blocked: one CTA per C row, pivots taken 32 A-columns at a time.
+// The sequential dependency between pivots only runs through the A columns,
+// so for a window of BW consecutive A columns (starting at the first nonzero
+// one) the multipliers come from a BW x BW unit-triangular solve in one warp
+// (the pivot rows' in-window entries staged densely in shared memory), and
+// the rest of every active pivot tail is applied afterwards by the whole CTA
+// at once (shared-memory atomicAdd into a lazily reduced u32 accumulator: each
+// product is < p, a column receives at most nA of them, and p * nA < 2^32 is
+// checked on the host).  Three CTA barriers per window instead of one per
+// pivot application.  Same multipliers as the column-by-column sweep, so the
+// D' row is bit-identical.
+// ---------------------------------------------------------------------------
+static constexpr int BW = 32;
+__global__ void __launch_bounds__(256) k_sweep_blk(Fp fp, u32 mu, const u32* __restrict__ rp,
+                                                   const u32* __restrict__ col, const u32* __restrict__ val, u32 N,
+                                                   const u32* __restrict__ rows, u32 nrows,
+                                                   const uint4* __restrict__ desc, const u32* __restrict__ abits_g,
+                                                   const u32* __restrict__ acols, const u32* __restrict__ apos,
+                                                   u32 nA, u32* __restrict__ Dp, u32 K, const u32* __restrict__ nonA,
+                                                   unsigned long long* __restrict__ stats) {
+  extern __shared__ __align__(16) u32 smem[];
+  constexpr int NWARP = 8;
+  const u32 nwords = (N + 31) / 32;
+  u32* abits = smem;
+  u32* acc = smem + ((nwords + 3) & ~3u);
+  __shared__ u32 s_cw[NWARP][BW];  // window columns (a per-warp copy)
+  __shared__ uint4 s_dw[BW];       // window pivot descriptors
+  __shared__ u32 s_P[BW][BW + 1];  // in-window entries of the window pivots
+  __shared__ u32 s_m[BW];          // multipliers (Montgomery form)
+  __shared__ u32 s_act[BW];
+  __shared__ u32 s_nact;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const u32 p = fp.p;
+  auto red = [&](u32 v) -> u32 {  // v mod p for v < 2^32 (Barrett, mu = floor(2^32 / p))
+    const u32 r = v - __umulhi(v, mu) * p;
+    return r >= p ? r - p : r;
+  };
+  for (u32 w = tid; w < nwords; w += blockDim.x) abits[w] = abits_g[w];
+  for (u32 q = tid; q < BW * (BW + 1); q += blockDim.x) (&s_P[0][0])[q] = 0;
+  __syncthreads();
+  unsigned long long n_piv = 0, n_tail = 0;
+  for (u32 rr = blockIdx.x; rr < nrows; rr += gridDim.x) {
+    const u32 i = rows[rr];
+    const u32 s = rp[i], e = rp[i + 1];
+    const u32 lead = col[s];
+    for (u32 c = lead + tid; c < N; c += blockDim.x) acc[c] = 0;
+    __syncthreads();
+    for (u32 k = s + tid; k < e; k += blockDim.x) acc[col[k]] = val[k];
+    __syncthreads();
+    u32 from = lead;
+    while (true) {
+      // (1) every warp: window start = first nonzero A column >= from, the
+      // BW A columns from there (same data, same answer in every warp)
+      u32 c = N;
+      for (u32 c0 = from & ~31u; c0 < N; c0 += 32) {
+        const u32 cc = c0 + lane;
+        const bool hit = cc >= from && cc < N && ((abits[cc >> 5] >> (cc & 31)) & 1u) && red(acc[cc]) != 0;
+        const unsigned b = __ballot_sync(0xffffffffu, hit);
+        if (b) {
+          c = c0 + __ffs(b) - 1;
+          break;
+        }
+      }
+      if (c >= N) break;
+      const u32 a0 = __ldg(apos + c);
+      const u32 nw = min((u32)BW, nA - a0);
+      const u32 cw = (u32)lane < nw ? __ldg(acols + a0 + lane) : 0xFFFFFFFFu;
+      s_cw[warp][lane] = cw;
+      const u32 clast = __shfl_sync(0xffffffffu, cw, nw - 1);
+      __syncwarp();
+      // (2) stage the in-window entries P[t][u] of the window pivots
+      for (u32 t = warp; t < nw; t += NWARP) {
+        const uint4 d = __ldg(desc + s_cw[warp][t]);
+        if (lane == 0) s_dw[t] = d;
+        for (u32 k0 = d.x; k0 < d.y; k0 += 32) {
+          const u32 k = k0 + lane;
+          const u32 cc = k < d.y ? __ldg(col + k) : 0xFFFFFFFFu;
+          if (cc <= clast && ((abits[cc >> 5] >> (cc & 31)) & 1u)) {
+            u32 lo = 0, hi = nw;  // position of cc among the window columns
+            while (lo + 1 < hi) {
+              const u32 mid = (lo + hi) >> 1;
+              if (s_cw[warp][mid] <= cc) lo = mid; else hi = mid;
+            }
+            s_P[t][lo] = __ldg(val + k);
+          }
+          if (__shfl_sync(0xffffffffu, cc, 31) > clast) break;
+        }
+      }
+      __syncthreads();
+      // (3) warp 0: unit-triangular solve; lane u holds the value of column u
+      if (warp == 0) {
+        u32 v = (u32)lane < nw ? red(acc[cw]) : 0u;
+        const u32 inv = (u32)lane < nw ? s_dw[lane].z : 0u;
+        u32 nact = 0;
+        for (u32 t = 0; t < nw; ++t) {
+          const u32 vt = __shfl_sync(0xffffffffu, v, t);
+          const u32 it = __shfl_sync(0xffffffffu, inv, t);
+          u32 m = 0;
+          if (vt) {
+            m = fp.to_mont(fp.neg(fp.mul(vt, it)));
+            if ((u32)lane > t) v = fp.add(v, fp.mont_mul(m, s_P[t][lane]));
+            if (lane == 0) s_act[nact] = t;
+            ++nact;
+          }
+          if (lane == 0) s_m[t] = m;
+        }
+        if (lane == 0) s_nact = nact;
+      }
+      __syncthreads();
+      // (4) the rest of every active tail: columns right of the window and
+      // the non-A columns inside it; P rows cleared for the next window
+      const u32 nact = s_nact;
+      if (tid == 0) {
+        n_piv += nact;
+        for (u32 q = 0; q < nact; ++q) n_tail += s_dw[s_act[q]].y - s_dw[s_act[q]].x;
+      }
+      for (u32 t = warp; t < nw; t += NWARP) s_P[t][lane] = 0;
+      for (u32 q = warp; q < nact; q += NWARP) {
+        const u32 t = s_act[q];
+        const uint4 d = s_dw[t];
+        const u32 m = s_m[t];
+        for (u32 k0 = d.x; k0 < d.y; k0 += 32 * 4) {
+          u32 cc[4], vv[4];
+#pragma unroll
+          for (int z = 0; z < 4; ++z) {
+            const u32 k = k0 + z * 32 + lane;
+            cc[z] = k < d.y ? __ldg(col + k) : N;
+            vv[z] = k < d.y ? __ldg(val + k) : 0u;
+          }
+#pragma unroll
+          for (int z = 0; z < 4; ++z) {
+            const u32 cz = cc[z];
+            if (cz < N && (cz > clast || !((abits[cz >> 5] >> (cz & 31)) & 1u)))
+              atomicAdd(acc + cz, fp.mont_mul(m, vv[z]));
+          }
+        }
+      }
+      __syncthreads();
+      from = clast + 1;
+    }
+    u32* out = Dp + (size_t)rr * K;
+    for (u32 q = tid; q < K; q += blockDim.x) {
+      const u32 cc = nonA[q];
+      out[q] = cc >= lead ? red(acc[cc]) : 0u;
+    }
+    __syncthreads();
+  }
+  if (stats && tid == 0 && n_piv) {
+    atomicAdd(stats, n_piv);
+    atomicAdd(stats + 1, n_tail);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// E2, warp per row: one warp sweeps one C row with its own shared-memory
+// accumulator, so a pivot application needs no CTA barrier (only __syncwarp).
+// The pivot tail is loaded SWW_UNR entries per lane at a time — all loads in
+// flight before the read-modify-writes (tail columns are distinct, so lanes
+// never collide).  Same pivot order and arithmetic as k_sweep<0>: the D' row
+// is bit-identical.
+// ---------------------------------------------------------------------------
+static constexpr int SWW_UNR = 8;
+template <typename T>
+__global__ void __launch_bounds__(128) k_sweep_warp(Fp fp, const u32* __restrict__ rp, const u32* __restrict__ col,
+                                                    const u32* __restrict__ val, u32 N, const u32* __restrict__ rows,
+                                                    u32 nrows, const uint4* __restrict__ desc,
+                                                    const u32* __restrict__ abits_g, u32* __restrict__ Dp, u32 K,
+                                                    const u32* __restrict__ nonA, unsigned long long* __restrict__ stats) {
+  extern __shared__ __align__(16) u32 smem[];
+  const u32 nwords = (N + 31) / 32;
+  u32* abits = smem;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpc = blockDim.x >> 5;
+  T* acc = reinterpret_cast<T*>(smem + ((nwords + 3) & ~3u)) + (size_t)warp * ((N + 7) & ~7u);
+  for (u32 w = threadIdx.x; w < nwords; w += blockDim.x) abits[w] = abits_g[w];
+  __syncthreads();
+  unsigned long long n_piv = 0, n_tail = 0;
+  for (u32 rr = blockIdx.x * wpc + warp; rr < nrows; rr += gridDim.x * wpc) {
+    const u32 i = rows[rr];
+    const u32 s = rp[i], e = rp[i + 1];
+    const u32 lead = col[s];
+    for (u32 c = lead + lane; c < N; c += 32) acc[c] = 0;
+    __syncwarp();
+    for (u32 k = s + lane; k < e; k += 32) acc[col[k]] = (T)val[k];
+    __syncwarp();
+    u32 from = lead;
+    while (true) {
+      // next nonzero A column >= from (warp ballot over 32 columns)
+      u32 c = N, av = 0;
+      for (u32 c0 = from & ~31u; c0 < N; c0 += 32) {
+        const u32 cc = c0 + lane;
+        const u32 v = (cc >= from && cc < N) ? (u32)acc[cc] : 0u;
+        const bool hit = v != 0 && ((abits[cc >> 5] >> (cc & 31)) & 1u);
+        const unsigned b = __ballot_sync(0xffffffffu, hit);
+        if (b) {
+          const int src = __ffs(b) - 1;
+          av = __shfl_sync(0xffffffffu, v, src);
+          c = c0 + src;
+          break;
+        }
+      }
+      if (c >= N) break;
+      const uint4 d = __ldg(desc + c);
+      const u32 fm = fp.to_mont(fp.neg(fp.mul(av, d.z)));
+      ++n_piv;
+      n_tail += d.y - d.x;
+      for (u32 k0 = d.x; k0 < d.y; k0 += 32 * SWW_UNR) {
+        u32 cc[SWW_UNR], vv[SWW_UNR];
+#pragma unroll
+        for (int q = 0; q < SWW_UNR; ++q) {
+          const u32 k = k0 + q * 32 + lane;
+          cc[q] = k < d.y ? __ldg(col + k) : N;
+          vv[q] = k < d.y ? __ldg(val + k) : 0u;
+        }
+#pragma unroll
+        for (int q = 0; q < SWW_UNR; ++q)
+          if (cc[q] < N) acc[cc[q]] = (T)fp.add((u32)acc[cc[q]], fp.mont_mul(fm, vv[q]));
+      }
+      __syncwarp();
+      // acc[c] is cancelled by construction (never read again: later tails
+      // start right of their leads and D' reads non-A columns only)
+      from = c + 1;
+    }
+    u32* out = Dp + (size_t)rr * K;
+    for (u32 q = lane; q < K; q += 32) {
+      const u32 cc = nonA[q];
+      out[q] = cc >= lead ? (u32)acc[cc] : 0u;
+    }
+    __syncwarp();
+  }
+  if (stats && lane == 0 && n_piv) {
+    atomicAdd(stats, n_piv);
+    atomicAdd(stats + 1, n_tail);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // E3a: cooperative forward elimination of the dense block D' (R x K)
 // ---------------------------------------------------------------------------
 // One grid barrier per PIVOT (not per column): every CTA keeps the leading
@@ -609,6 +847,58 @@ static void launch_sweep(Ctx* c, const Fp& fp, f4b_echelon* E, const u32* rows, 
                          unsigned long long* cursor, u32* s_off, u32* s_len, u32* err,
                          unsigned long long* stats = nullptr) {
   const u32 N = (u32)E->n_cols;
+  static const char* sweep_env = getenv("F4B_SWEEP");
+  static const bool cta_sweep = sweep_env && !strcmp(sweep_env, "cta");
+  static const bool warp_sweep = sweep_env && !strcmp(sweep_env, "warp");
+  if (MODE == 0 && !cta_sweep && !warp_sweep) {
+    // blocked sweep: lazily reduced u32 accumulator needs p * (nA + 1) < 2^32
+    const size_t bitmap = (size_t)((((N + 31) / 32) + 3) & ~3u) * 4;
+    const size_t smem = bitmap + (size_t)N * 4;
+    if ((unsigned long long)c->p * (unsigned long long)(E->nA + 1) < (1ull << 32) && smem <= 180 * 1024) {
+      static bool battr = false;
+      if (!battr) {
+        check_cuda(cudaFuncSetAttribute(k_sweep_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
+                   "attr");
+        battr = true;
+      }
+      const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(8, (220 * 1024) / (smem + 8 * 1024)));
+      const int grid = (int)std::max<long long>(1, std::min<long long>(nrows, (long long)c->num_sms * per_sm));
+      const u32 mu = (u32)((1ull << 32) / c->p);
+      F4B_LAUNCH(c, k_sweep_blk, grid, 256, smem, fp, mu, E->rp, E->col, E->val, N, rows, nrows, E->desc.as<uint4>(),
+                 E->abits.as<u32>(), E->acols.as<u32>(), E->apos.as<u32>(), (u32)E->nA, Dp, K, E->nonA.as<u32>(),
+                 stats);
+      return;
+    }
+  }
+  if (MODE == 0 && warp_sweep) {
+    // warp per C row; warps per CTA from the accumulator footprint
+    const bool small_p = c->p < 65536u;
+    const size_t tb = small_p ? 2 : 4;
+    const size_t bitmap = (size_t)((((N + 31) / 32) + 3) & ~3u) * 4;
+    const size_t per_warp = (size_t)((N + 7) & ~7u) * tb;
+    if (bitmap + per_warp <= 200 * 1024) {
+      const int wpc = (int)std::max<size_t>(1, std::min<size_t>(4, (200 * 1024 - bitmap) / per_warp));
+      const size_t smem = bitmap + per_warp * wpc;
+      const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(16 / wpc, (220 * 1024) / (smem + 1024)));
+      const int grid = (int)std::max<long long>(
+          1, std::min<long long>((nrows + wpc - 1) / wpc, (long long)c->num_sms * per_sm));
+      static bool wattr = false;
+      if (!wattr) {
+        check_cuda(cudaFuncSetAttribute(k_sweep_warp<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        200 * 1024 + 4096), "attr");
+        check_cuda(cudaFuncSetAttribute(k_sweep_warp<u32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        200 * 1024 + 4096), "attr");
+        wattr = true;
+      }
+      if (small_p)
+        F4B_LAUNCH(c, k_sweep_warp<uint16_t>, grid, 32 * wpc, smem, fp, E->rp, E->col, E->val, N, rows, nrows,
+                   E->desc.as<uint4>(), E->abits.as<u32>(), Dp, K, E->nonA.as<u32>(), stats);
+      else
+        F4B_LAUNCH(c, k_sweep_warp<u32>, grid, 32 * wpc, smem, fp, E->rp, E->col, E->val, N, rows, nrows,
+                   E->desc.as<uint4>(), E->abits.as<u32>(), Dp, K, E->nonA.as<u32>(), stats);
+      return;
+    }
+  }
   const size_t bitmap = (size_t)((N + 31) / 32) * 4;
   const bool small_p = c->p < 65536u;
   const size_t acc_b = (((size_t)N * (small_p ? 2 : 4)) + 15) & ~(size_t)15;
@@ -682,6 +972,10 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
   ensure(c, c->tmp_u32b, (size_t)(Nn + 2) * sizeof(u32));
   exclusive_scan_flags(c, isA, c->tmp_u32a.as<u32>(), N);
   exclusive_scan_flags(c, notA, c->tmp_u32b.as<u32>(), N);
+  ensure(c, E->apos, (size_t)Nn * sizeof(u32));
+  if (N)
+    check_cuda(cudaMemcpyAsync(E->apos.p, c->tmp_u32a.p, (size_t)N * sizeof(u32), cudaMemcpyDeviceToDevice, c->stream),
+               "d2d apos");
   E->nA = N ? read_u32(c, c->tmp_u32a.as<u32>() + N) : 0;
   E->K = N - E->nA;
   ensure(c, E->acols, (size_t)std::max<long long>(E->nA, 1) * sizeof(u32));
@@ -1065,7 +1359,7 @@ void echelon_release(f4b_echelon* E) {
   Ctx* c = E->ctx;
   DBuf* bufs[] = {&E->own_rp, &E->own_col, &E->own_val, &E->prow,  &E->invl, &E->desc, &E->abits, &E->acols,
                   &E->nonA,   &E->Rd,      &E->dpiv,    &E->pool_col, &E->pool_val, &E->a_off, &E->a_len,
-                  &E->d_off,  &E->d_len,   &E->cursor, &E->stats};
+                  &E->d_off,  &E->d_len,   &E->cursor, &E->stats, &E->apos};
   for (DBuf* b : bufs) release(c, *b);
   delete E;
 }
