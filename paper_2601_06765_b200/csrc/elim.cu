@@ -673,6 +673,70 @@ __global__ void __launch_bounds__(256) k_dense_forward(Fp fp, u32* Dp, u32 R, u3
   }
 }
 
+// E3a (rounds): every live row whose leading column has no pivot claims it
+// (lowest row index wins, one atomicMin per row) and computes the inverse of
+// its own lead; then every other live row is reduced by the pivot of its
+// leading column, again and again, until its lead is a pivot-less column or
+// the row is zero.  Pivot rows are frozen once claimed.  All distinct leads
+// are claimed in the same round, so the grid barriers are 2 x rounds instead
+// of 1 per pivot; any echelon basis has the same RREF (k_dense_back).
+// Warp per row (rows stay with their warp for the whole kernel).
+__global__ void __launch_bounds__(256) k_dense_rounds(Fp fp, u32* Dp, u32 R, u32 K, u32* __restrict__ piv_of_col,
+                                                      u32* __restrict__ rinv, u32* __restrict__ active) {
+  cg::grid_group grid = cg::this_grid();
+  const int lane = threadIdx.x & 31;
+  const u32 W = gridDim.x * (blockDim.x >> 5);
+  const u32 gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  constexpr int RPW = 4;  // rows per warp kept in registers
+  u32 lead[RPW];
+  bool piv[RPW];
+#pragma unroll
+  for (int q = 0; q < RPW; ++q) {
+    const u32 i = gw + q * W;
+    lead[q] = i < R ? first_nonzero_warp(Dp + (size_t)i * K, 0, K) : K;
+    piv[q] = false;
+  }
+  for (u32 round = 0;; ++round) {
+    // A: claim pivot-less leading columns; inverse of the own lead
+#pragma unroll
+    for (int q = 0; q < RPW; ++q) {
+      const u32 i = gw + q * W;
+      if (i >= R || piv[q] || lead[q] >= K) continue;
+      if (lane == 0) {
+        rinv[i] = fp.inv(Dp[(size_t)i * K + lead[q]]);
+        if (__ldcg(piv_of_col + lead[q]) == NONE) atomicMin(piv_of_col + lead[q], i);
+      }
+    }
+    grid.sync();
+    // C: reduce until the lead is pivot-less (or the row is zero)
+    u32 live = 0;
+#pragma unroll
+    for (int q = 0; q < RPW; ++q) {
+      const u32 i = gw + q * W;
+      if (i >= R || piv[q] || lead[q] >= K) continue;
+      u32* row = Dp + (size_t)i * K;
+      u32 c = lead[q];
+      u32 pr = __ldcg(piv_of_col + c);
+      if (pr == i) {
+        piv[q] = true;
+        continue;
+      }
+      while (c < K && pr != NONE) {
+        const u32 fm = fp.to_mont(fp.neg(fp.mul(row[c], __ldcg(rinv + pr))));
+        row_axpy8(fp, row, Dp + (size_t)pr * K, fm, c + lane, K);
+        __syncwarp();
+        c = first_nonzero_warp(row, c + 1, K);
+        pr = c < K ? __ldcg(piv_of_col + c) : NONE;
+      }
+      lead[q] = c;
+      live += c < K;
+    }
+    if (lane == 0 && live) atomicAdd(active + round, live);
+    grid.sync();
+    if (__ldcg(active + round) == 0) break;
+  }
+}
+
 // E3a' (small D'): the same pivot-to-pivot elimination inside ONE thread-block
 // cluster: candidates are exchanged through distributed shared memory and the
 // per-pivot barrier is a cluster barrier (hardware, ~sub-µs) instead of a
@@ -1061,6 +1125,32 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
           break;
         }
         cudaGetLastError();
+      }
+    }
+    // F4B_DENSE=rounds: claim-all-leads rounds (2 grid barriers per round
+    // instead of 1 per pivot) — measured slower on cyclic-8 (a row reduced by
+    // many pivots becomes one warp's serial chain), kept as an option
+    static const bool rounds = getenv("F4B_DENSE") && !strcmp(getenv("F4B_DENSE"), "rounds");
+    if (!done_cluster && rounds) {
+      int bpr = 0;
+      check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpr, k_dense_rounds, 256, 0), "occupancy");
+      const int GR = c->num_sms * std::max(1, std::min(bpr, 2));
+      if ((long long)R <= 4ll * GR * 8) {
+        DBuf rinv, active;
+        ensure(c, rinv, (size_t)R * sizeof(u32));
+        ensure(c, active, (size_t)(K + 2) * sizeof(u32));
+        check_cuda(cudaMemsetAsync(active.p, 0, (size_t)(K + 2) * sizeof(u32), c->stream), "memset");
+        u32* rinvp = rinv.as<u32>();
+        u32* actp = active.as<u32>();
+        void* args2[] = {&fp, &dpp, &Ru, &Ku, &pofcp, &rinvp, &actp};
+        {
+          ProfScope ps(c, "k_dense_rounds");
+          check_cuda(cudaLaunchCooperativeKernel((void*)k_dense_rounds, GR, 256, args2, 0, c->stream),
+                     "k_dense_rounds");
+        }
+        release(c, rinv);
+        release(c, active);
+        done_cluster = true;
       }
     }
     if (!done_cluster) {
