@@ -445,11 +445,14 @@ def main():
                 rp, ci, va = plan.row_ptr, plan.col_ind, plan.val
                 dk = plan.dict_keys
                 e_M += b["M"]
-                # bytes moved: new basis terms (u16 exps + u32 coeff) and polys
-                # (offset, length, LM, max exps), rows (basis index + shift);
-                # back: row_ptr / col_ind / val (64-bit) + dictionary exponents
-                h2d += (nt - prev_nt) * (2 * n + 4) + (nb_ - prev_nb) * (8 + 4 * n) + len(b["rows"]) * (4 + 2 * n)
-                d2h += (plan.counters.r + 1) * 8 + plan.counters.M * 16 + plan.counters.N * 2 * n
+                # bytes moved: new basis terms as the reference streams them
+                # (int64 exps + uint64 coeff, narrowed on the device), their
+                # lengths + offsets, back their LM / max exponents; rows (basis
+                # index + shift); back: row_ptr / col_ind / val (64-bit) and
+                # dict_keys (reference key words)
+                h2d += (nt - prev_nt) * (8 * n + 8) + (nb_ - prev_nb) * 16 + len(b["rows"]) * (4 + 2 * n)
+                d2h += ((nb_ - prev_nb) * 4 * n + (plan.counters.r + 1) * 8 + plan.counters.M * 16
+                        + plan.counters.N * 8 * ring.n_key_words)
                 prev_nt, prev_nb = nt, nb_
                 del rp, ci, va, dk, plan
             torch.cuda.synchronize()

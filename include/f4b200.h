@@ -78,6 +78,13 @@ int f4b_ctx_profile_read(f4b_ctx* ctx, char* buf, int64_t buflen, int64_t* total
 int f4b_basis_clear(f4b_ctx* ctx);
 int f4b_basis_append(f4b_ctx* ctx, int64_t n_polys, const int64_t* lengths,
                      const uint16_t* exps, const uint32_t* coeffs);
+/* Same, for the reference's own SoaPolySet streams (soa_pack,
+ * polynomials.py:248-262): exps [T][n_vars] int64, coeffs [T] uint64.  The
+ * narrowing, the range checks (0 <= e <= 0xFFFF -> F4B_ERR_LANE_OVERFLOW,
+ * 1 <= c < p -> F4B_ERR_PROPERTY) and the per-polynomial LM / maximum
+ * exponents run on the device; page-locked host buffers copy at full rate. */
+int f4b_basis_append_wide(f4b_ctx* ctx, int64_t n_polys, const int64_t* lengths,
+                          const int64_t* exps, const uint64_t* coeffs);
 int f4b_basis_size(const f4b_ctx* ctx, int64_t* n_polys, int64_t* n_terms);
 
 typedef struct {
@@ -102,6 +109,10 @@ int f4b_plan_get_info(const f4b_plan* plan, f4b_plan_info* info);
 int f4b_plan_download(const f4b_plan* plan, int64_t* row_ptr, int64_t* col_ind, uint64_t* val,
                       uint16_t* dict_exps, int32_t* closure_basis, uint16_t* closure_shift,
                       int32_t* closure_round);
+/* LayoutPlan.dict_keys (symbolic.py:99-163): reference keys
+ * (monomials.py:131-148; big-endian u64 words, W = ceil((32 [graded] +
+ * 16 n_vars) / 64)) in column order (descending), [N][W], built on the device. */
+int f4b_plan_download_ref_keys(const f4b_plan* plan, uint64_t* keys);
 int f4b_plan_free(f4b_plan* plan);
 
 typedef struct {

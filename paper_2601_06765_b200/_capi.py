@@ -59,11 +59,13 @@ SIGNATURES = {
     "f4b_ctx_profile_read": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int64, i64p]),
     "f4b_basis_clear": (C.c_int, [C.c_void_p]),
     "f4b_basis_append": (C.c_int, [C.c_void_p, C.c_int64, i64p, u16p, u32p]),
+    "f4b_basis_append_wide": (C.c_int, [C.c_void_p, C.c_int64, i64p, i64p, u64p]),
     "f4b_basis_size": (C.c_int, [C.c_void_p, i64p, i64p]),
     "f4b_compile_batch": (C.c_int, [C.c_void_p, C.c_int64, i32p, u16p, C.c_int, i32p, C.c_int64, C.c_int64,
                                     C.POINTER(C.c_void_p)]),
     "f4b_plan_get_info": (C.c_int, [C.c_void_p, C.POINTER(PlanInfo)]),
     "f4b_plan_download": (C.c_int, [C.c_void_p, i64p, i64p, u64p, u16p, i32p, u16p, i32p]),
+    "f4b_plan_download_ref_keys": (C.c_int, [C.c_void_p, u64p]),
     "f4b_plan_free": (C.c_int, [C.c_void_p]),
     "f4b_psge_plan": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]),
     "f4b_psge_csr": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, i64p, i64p, u64p, C.c_int,

@@ -439,6 +439,125 @@ int f4b_basis_append(f4b_ctx* h, int64_t n_polys, const int64_t* lengths, const 
   API_END
 }
 
+__global__ void k_narrow_terms(const int64_t* __restrict__ e64, const uint64_t* __restrict__ c64, long long T, int n,
+                               uint32_t p, uint16_t* __restrict__ e16, uint32_t* __restrict__ c32,
+                               uint32_t* __restrict__ bad) {
+  uint32_t flags = 0;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < T; t += (long long)gridDim.x * blockDim.x) {
+    for (int v = 0; v < n; ++v) {
+      const int64_t x = e64[t * n + v];
+      if (x < 0 || x > 0xFFFF) flags |= 1u;
+      e16[t * n + v] = (uint16_t)x;
+    }
+    const uint64_t cc = c64[t];
+    if (cc == 0 || cc >= p) flags |= 2u;
+    c32[t] = (uint32_t)cc;
+  }
+  if (flags) atomicOr(bad, flags);
+}
+
+// per polynomial (warp each): offset, length, LM exponents, max exponent per variable
+__global__ void k_poly_meta(const uint16_t* __restrict__ e16, const int64_t* __restrict__ lens, long long P,
+                            long long T0, int n, uint32_t* __restrict__ off, uint32_t* __restrict__ len,
+                            uint16_t* __restrict__ lmexp, uint16_t* __restrict__ maxe,
+                            const long long* __restrict__ pre) {
+  const long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x & 31;
+  if (i >= P) return;
+  const long long s = pre[i], L = lens[i];
+  if (lane == 0) {
+    off[i] = (uint32_t)(T0 + s);
+    len[i] = (uint32_t)L;
+  }
+  for (int v = 0; v < n; ++v) {
+    uint32_t mx = 0;
+    for (long long j = lane; j < L; j += 32) mx = max(mx, (uint32_t)e16[(s + j) * n + v]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) {
+      maxe[i * n + v] = (uint16_t)mx;
+      lmexp[i * n + v] = L ? e16[s * n + v] : (uint16_t)0;
+    }
+  }
+}
+
+int f4b_basis_append_wide(f4b_ctx* h, int64_t n_polys, const int64_t* lengths, const int64_t* exps,
+                          const uint64_t* coeffs) {
+  if (!h) return F4B_ERR_PRECONDITION;
+  API_BEGIN(&h->c)
+  Ctx* c = _c;
+  Basis& B = c->basis;
+  const int n = c->n_vars;
+  if (n_polys < 0) fail(F4B_ERR_PRECONDITION, "negative polynomial count");
+  std::vector<long long> pre((size_t)n_polys + 1, 0);
+  for (long long i = 0; i < n_polys; ++i) {
+    if (lengths[i] < 0) fail(F4B_ERR_PRECONDITION, "negative polynomial length");
+    pre[i + 1] = pre[i] + lengths[i];
+  }
+  const long long T = pre[n_polys];
+  const long long T0 = B.n_terms, P0 = B.n_polys, T1 = T0 + T, P1 = P0 + n_polys;
+  if (T1 >= (1ll << 31)) fail(F4B_ERR_SIZE_CAP, "basis has more than 2^31 terms");
+  ensure_keep(c, B.exps, (size_t)(T1 + 1) * n * sizeof(u16));
+  ensure_keep(c, B.coeff, (size_t)(T1 + 1) * sizeof(u32));
+  ensure_keep(c, B.off, (size_t)(P1 + 1) * sizeof(u32));
+  ensure_keep(c, B.len, (size_t)(P1 + 1) * sizeof(u32));
+  ensure_keep(c, B.lmexp, (size_t)(P1 + 1) * n * sizeof(u16));
+  ensure_keep(c, B.maxe, (size_t)(P1 + 1) * n * sizeof(u16));
+  // raw streams -> device staging -> narrowed basis streams
+  DBuf raw;
+  const size_t b_e = (size_t)T * n * 8, b_c = (size_t)T * 8, b_l = (size_t)std::max<long long>(n_polys, 1) * 8,
+               b_p = (size_t)(n_polys + 1) * 8;
+  ensure(c, raw, b_e + b_c + b_l + b_p + 64);
+  unsigned char* rp = raw.as<unsigned char>();
+  int64_t* d_e = reinterpret_cast<int64_t*>(rp);
+  uint64_t* d_c = reinterpret_cast<uint64_t*>(rp + b_e);
+  int64_t* d_l = reinterpret_cast<int64_t*>(rp + b_e + b_c);
+  long long* d_p = reinterpret_cast<long long*>(rp + b_e + b_c + b_l);
+  uint32_t* d_bad = reinterpret_cast<uint32_t*>(rp + b_e + b_c + b_l + b_p);
+  check_cuda(cudaMemsetAsync(d_bad, 0, 4, c->stream), "memset");
+  if (T) {
+    check_cuda(cudaMemcpyAsync(d_e, exps, b_e, cudaMemcpyHostToDevice, c->stream), "h2d exps");
+    check_cuda(cudaMemcpyAsync(d_c, coeffs, b_c, cudaMemcpyHostToDevice, c->stream), "h2d coeffs");
+  }
+  if (n_polys) {
+    check_cuda(cudaMemcpyAsync(d_l, lengths, (size_t)n_polys * 8, cudaMemcpyHostToDevice, c->stream), "h2d lens");
+    check_cuda(cudaMemcpyAsync(d_p, pre.data(), b_p, cudaMemcpyHostToDevice, c->stream), "h2d pre");
+  }
+  if (T) {
+    const int g = (int)std::min<long long>((T + 255) / 256, (long long)c->num_sms * 8);
+    F4B_LAUNCH(c, k_narrow_terms, g, 256, 0, d_e, d_c, T, n, c->p, B.exps.as<u16>() + T0 * n, B.coeff.as<u32>() + T0,
+               d_bad);
+  }
+  std::vector<uint16_t> hlm((size_t)std::max<long long>(n_polys, 1) * n), hmx((size_t)std::max<long long>(n_polys, 1) * n);
+  if (n_polys) {
+    F4B_LAUNCH(c, k_poly_meta, (int)((n_polys * 32 + 255) / 256), 256, 0, B.exps.as<u16>() + T0 * n, d_l, n_polys, T0,
+               n, B.off.as<u32>() + P0, B.len.as<u32>() + P0, B.lmexp.as<u16>() + P0 * n,
+               B.maxe.as<u16>() + P0 * n, d_p);
+    check_cuda(cudaMemcpyAsync(hlm.data(), B.lmexp.as<u16>() + P0 * n, (size_t)n_polys * n * 2, cudaMemcpyDeviceToHost,
+                               c->stream), "d2h lm");
+    check_cuda(cudaMemcpyAsync(hmx.data(), B.maxe.as<u16>() + P0 * n, (size_t)n_polys * n * 2, cudaMemcpyDeviceToHost,
+                               c->stream), "d2h maxe");
+  }
+  // the basis end offset (off[P1]) for kernels reading off[i + 1]
+  const u32 tail_off = (u32)T1;
+  check_cuda(cudaMemcpyAsync(B.off.as<u32>() + P1, &tail_off, 4, cudaMemcpyHostToDevice, c->stream), "h2d off");
+  uint32_t bad = 0;
+  check_cuda(cudaMemcpyAsync(&bad, d_bad, 4, cudaMemcpyDeviceToHost, c->stream), "d2h");
+  check_cuda(cudaStreamSynchronize(c->stream), "sync");
+  release(c, raw);
+  if (bad & 1u) fail(F4B_ERR_LANE_OVERFLOW, "exponent does not fit a 16-bit lane");
+  if (bad & 2u) fail(F4B_ERR_PROPERTY, "basis coefficient outside [1, p)");
+  for (long long i = 0; i < n_polys; ++i) {
+    B.h_len.push_back(lengths[i]);
+    B.h_off.push_back(B.h_off.back() + lengths[i]);
+  }
+  B.h_lm.insert(B.h_lm.end(), hlm.begin(), hlm.begin() + (size_t)n_polys * n);
+  B.h_maxe.insert(B.h_maxe.end(), hmx.begin(), hmx.begin() + (size_t)n_polys * n);
+  B.n_terms = T1;
+  B.n_polys = (int)P1;
+  API_END
+}
+
 int f4b_basis_size(const f4b_ctx* h, int64_t* n_polys, int64_t* n_terms) {
   if (!h) return F4B_ERR_PRECONDITION;
   if (n_polys) *n_polys = h->c.basis.n_polys;
@@ -520,6 +639,47 @@ int f4b_plan_download(const f4b_plan* pl, int64_t* row_ptr, int64_t* col_ind, ui
   }
   check_cuda(cudaStreamSynchronize(c->stream), "sync");
   release(c, wide);
+  API_END
+}
+
+// reference keys (monomials.py:131-148) from the plan's column-order exponents
+__global__ void k_ref_keys(const uint16_t* __restrict__ ex, long long N, int n, int order, int W,
+                           unsigned long long* __restrict__ out) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  const uint16_t* e = ex + i * n;
+  const int head = order == 2 ? 0 : 32;
+  unsigned long long w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (order != 2) {
+    unsigned long long d = 0;
+    for (int v = 0; v < n; ++v) d += e[v];
+    w[0] |= d << 32;
+  }
+  for (int l = 0; l < n; ++l) {
+    const unsigned long long lane = order == 0 ? (unsigned long long)(0xFFFFu - e[n - 1 - l]) : (unsigned long long)e[l];
+    const int off = head + 16 * l;
+    w[off / 64] |= lane << (64 - (off % 64) - 16);
+  }
+  for (int q = 0; q < W; ++q) out[i * W + q] = w[q];
+}
+
+int f4b_plan_download_ref_keys(const f4b_plan* pl, uint64_t* keys) {
+  if (!pl) return F4B_ERR_PRECONDITION;
+  API_BEGIN(pl->ctx)
+  Ctx* c = _c;
+  const int n = c->n_vars;
+  const int W = ((c->order == 2 ? 0 : 32) + 16 * n + 63) / 64;
+  if (W > 8) fail(F4B_ERR_PRECONDITION, "reference key wider than 8 words");
+  const long long N = pl->N;
+  if (N) {
+    DBuf kb;
+    ensure(c, kb, (size_t)N * W * 8);
+    F4B_LAUNCH(c, k_ref_keys, (int)((N + 255) / 256), 256, 0, pl->dict_exps.as<uint16_t>(), N, n, c->order, W,
+               kb.as<unsigned long long>());
+    check_cuda(cudaMemcpyAsync(keys, kb.p, (size_t)N * W * 8, cudaMemcpyDeviceToHost, c->stream), "d2h keys");
+    check_cuda(cudaStreamSynchronize(c->stream), "sync");
+    release(c, kb);
+  }
   API_END
 }
 

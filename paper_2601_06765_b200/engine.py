@@ -50,6 +50,14 @@ class DevicePlan:
         self.info = {k: int(getattr(info, k)) for k, _ in PlanInfo._fields_}
         self._fin = weakref.finalize(self, engine.lib.f4b_plan_free, handle)
 
+    def download_ref_keys(self, n_key_words):
+        """LayoutPlan.dict_keys built on the device (reference key format)."""
+        out = host_empty((self.info["N"], n_key_words), np.uint64)
+        if self.info["N"]:
+            self.engine.ctx.check(self.engine.lib.f4b_plan_download_ref_keys(self.h, ptr(out, C.c_uint64)),
+                                  "plan keys")
+        return out
+
     def download(self, arrays=True, dict_exps=True, closure=True):
         e, n = self.engine, self.engine.n_vars
         r, M, N, ncl = (self.info[k] for k in ("r", "M", "N", "n_closure_rows"))
@@ -179,6 +187,22 @@ class Engine:
     def append_polys(self, lengths, exps, coeffs):
         lengths = np.ascontiguousarray(lengths, dtype=np.int64)
         exps = np.asarray(exps)
+        coeffs = np.asarray(coeffs)
+        if (exps.dtype == np.int64 and coeffs.dtype == np.uint64 and exps.ndim == 2
+                and exps.flags.c_contiguous and coeffs.flags.c_contiguous):
+            # the reference's SoaPolySet streams as they are: narrowing, range
+            # checks and per-polynomial metadata on the device
+            self.ctx.sync_stream()
+            self.ctx.check(self.lib.f4b_basis_append_wide(self.ctx.h, len(lengths), ptr(lengths, C.c_int64),
+                                                          ptr(exps, C.c_int64), ptr(coeffs, C.c_uint64)),
+                           "basis append")
+            self._lens = np.concatenate([self._lens, lengths])
+            if len(coeffs):
+                self._chunks.append((self._T, exps, coeffs))
+            self._T += len(coeffs)
+            self._src = None
+            self.generation += 1
+            return
         if exps.size and (exps.min() < 0 or exps.max() > _EXP_MAX):
             raise LaneOverflowError("exponent does not fit a 16-bit lane")
         exps = np.ascontiguousarray(exps, dtype=np.uint16).reshape(-1, self.n_vars)

@@ -107,8 +107,7 @@ class LayoutPlan:
             for k in ("row_ptr", "col_ind", "val"):
                 self._host[k] = got[k]
         elif name == "dict_keys":
-            self._host["dict_keys"] = (key_pack_vec(self.dict_exps().astype(np.int64), self.ring)
-                                       if dev.info["N"] else np.zeros((0, self.ring.n_key_words), np.uint64))
+            self._host["dict_keys"] = dev.download_ref_keys(self.ring.n_key_words)
         elif name == "row_meta":
             got = dev.download(arrays=False, dict_exps=False, closure=True)
             extra = tuple(

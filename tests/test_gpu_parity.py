@@ -322,3 +322,40 @@ def test_wiedemann_nullity(cuda):
         assert (spmv(A, v) == 0).all()
     eye = csr_from_dense(np.eye(3, dtype=np.uint64), FieldModulus(101))
     assert wiedemann_solve(eye, KernelMode.MINPOLY, seed=11) == [100, 1]
+
+
+def test_basis_append_wide_matches_narrow(cuda):
+    """f4b_basis_append_wide (reference int64 / uint64 streams, narrowed and
+    checked on the device) == f4b_basis_append (host-narrowed u16 / u32)."""
+    from paper_2601_06765_b200.engine import Engine
+
+    rng = np.random.default_rng(7)
+    ring = Ring(["a", "b", "c", "d"], "grevlex", FieldModulus(32003))
+    polys = [_random_poly(rng, ring, 5, 12) for _ in range(9)]
+    soa = soa_pack(polys, ring)
+    rows = [Row(tuple(int(x) for x in rng.integers(0, 3, 4)), int(k), RowRole.SPOLY_HALF, 0) for k in range(9)]
+    eng = Engine.for_ring(ring)
+    eng.clear_basis()
+    eng.append_polys(soa.length, soa.exps, soa.coeff)  # int64 / uint64 -> wide path
+    plan_w = eng.compile(np.array([r.basis_index for r in rows]), np.array([r.shift for r in rows]), True)
+    dw = plan_w.download()
+    eng.clear_basis()
+    eng.append_polys(soa.length, soa.exps.astype(np.uint16), soa.coeff.astype(np.uint32))  # narrow path
+    plan_n = eng.compile(np.array([r.basis_index for r in rows]), np.array([r.shift for r in rows]), True)
+    dn = plan_n.download()
+    for k in dw:
+        assert np.array_equal(dw[k], dn[k]), k
+    keys = plan_w.download_ref_keys(ring.n_key_words)
+    from paper_2601_06765_b200.monomials import key_pack_vec
+
+    assert np.array_equal(keys, key_pack_vec(dw["dict_exps"].astype(np.int64), ring))
+    eng.clear_basis()
+    bad = soa.exps.copy()
+    bad[3, 1] = 70000
+    with pytest.raises(errors.LaneOverflowError):
+        eng.append_polys(soa.length, bad, soa.coeff)
+    badc = soa.coeff.copy()
+    badc[5] = 0
+    with pytest.raises(errors.PropertyViolationError):
+        eng.append_polys(soa.length, soa.exps, badc)
+    eng.clear_basis()

@@ -25,41 +25,39 @@ def main():
     ring, st, batches, _ = bench.capture_workload()
     eng = Engine.for_ring(ring)
     final = st.soa()
-    acc = {"clear": 0.0, "upload": 0.0, "compile": 0.0, "rowptr": 0.0, "colval": 0.0, "dict": 0.0}
+    acc = {}
     M = 0
-    for rep in range(2):
-        for k in acc:
-            acc[k] = 0.0
+    import cProfile
+    import pstats
+
+    prof = cProfile.Profile()
+    for rep in range(3):
+        acc = {k: 0.0 for k in ("compile", "rowptr_col_val", "dict_keys")}
         M = 0
+        eng.clear_basis()
+        if rep == 2:
+            prof.enable()
         for b in batches:
             nb_, nt = b["n_basis"], b["n_terms"]
             soa = SoaPolySet(ring, final.mon_key[:nt], final.coeff[:nt], final.offset[:nb_ + 1],
                              final.length[:nb_], final.exps[:nt])
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            eng.clear_basis()
-            t1 = time.perf_counter()
-            eng.sync_basis(soa)
-            torch.cuda.synchronize()
             t2 = time.perf_counter()
             plan = compile_batch(b["rows"], soa)
             t3 = time.perf_counter()
-            rp = plan.row_ptr
-            t4 = time.perf_counter()
-            ci, va = plan.col_ind, plan.val
+            rp, ci, va = plan.row_ptr, plan.col_ind, plan.val
             t5 = time.perf_counter()
             dk = plan.dict_keys
             t6 = time.perf_counter()
-            acc["clear"] += t1 - t0
-            acc["upload"] += t2 - t1
             acc["compile"] += t3 - t2
-            acc["rowptr"] += t4 - t3
-            acc["colval"] += t5 - t4
-            acc["dict"] += t6 - t5
+            acc["rowptr_col_val"] += t5 - t3
+            acc["dict_keys"] += t6 - t5
             M += b["M"]
             del rp, ci, va, dk
+        if rep == 2:
+            prof.disable()
     tot = sum(acc.values())
     print({k: round(v * 1e3, 2) for k, v in acc.items()}, "total_ms", round(tot * 1e3, 2), "nnz/s", M / tot)
+    pstats.Stats(prof).sort_stats("cumulative").print_stats(25)
 
 
 if __name__ == "__main__":
