@@ -365,23 +365,25 @@ __global__ void __launch_bounds__(256) k_sweep_blk(Fp fp, u32 mu, const u32* __r
                                                    unsigned long long* __restrict__ stats) {
   extern __shared__ __align__(16) u32 smem[];
   constexpr int NWARP = 8;
+  constexpr u32 PENDING = 0xFFFFFFFFu;
   const u32 nwords = (N + 31) / 32;
   u32* abits = smem;
   u32* acc = smem + ((nwords + 3) & ~3u);
   __shared__ u32 s_cw[NWARP][BW];  // window columns (a per-warp copy)
   __shared__ uint4 s_dw[BW];       // window pivot descriptors
+  __shared__ u32 s_X[BW];          // inverse leads times R^2 (Montgomery)
   __shared__ u32 s_P[BW][BW + 1];  // in-window entries of the window pivots
-  __shared__ u32 s_m[BW];          // multipliers (Montgomery form)
-  __shared__ u32 s_act[BW];
-  __shared__ u32 s_nact;
+  __shared__ u32 s_m[BW];          // multipliers (Montgomery), PENDING until solved
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const u32 p = fp.p;
   auto red = [&](u32 v) -> u32 {  // v mod p for v < 2^32 (Barrett, mu = floor(2^32 / p))
     const u32 r = v - __umulhi(v, mu) * p;
     return r >= p ? r - p : r;
   };
+  volatile u32* vm = s_m;
   for (u32 w = tid; w < nwords; w += blockDim.x) abits[w] = abits_g[w];
   for (u32 q = tid; q < BW * (BW + 1); q += blockDim.x) (&s_P[0][0])[q] = 0;
+  if (tid < BW) s_m[tid] = PENDING;
   __syncthreads();
   unsigned long long n_piv = 0, n_tail = 0;
   for (u32 rr = blockIdx.x; rr < nrows; rr += gridDim.x) {
@@ -413,10 +415,14 @@ __global__ void __launch_bounds__(256) k_sweep_blk(Fp fp, u32 mu, const u32* __r
       s_cw[warp][lane] = cw;
       const u32 clast = __shfl_sync(0xffffffffu, cw, nw - 1);
       __syncwarp();
-      // (2) stage the in-window entries P[t][u] of the window pivots
+      // (2) stage the in-window entries P[t][u] of the window pivots (rows of
+      // P were cleared by the same warp after their last use)
       for (u32 t = warp; t < nw; t += NWARP) {
         const uint4 d = __ldg(desc + s_cw[warp][t]);
-        if (lane == 0) s_dw[t] = d;
+        if (lane == 0) {
+          s_dw[t] = d;
+          s_X[t] = fp.to_mont(fp.to_mont(d.z));
+        }
         for (u32 k0 = d.x; k0 < d.y; k0 += 32) {
           const u32 k = k0 + lane;
           const u32 cc = k < d.y ? __ldg(col + k) : 0xFFFFFFFFu;
@@ -432,55 +438,51 @@ __global__ void __launch_bounds__(256) k_sweep_blk(Fp fp, u32 mu, const u32* __r
         }
       }
       __syncthreads();
-      // (3) warp 0: unit-triangular solve; lane u holds the value of column u
       if (warp == 0) {
+        // (3) unit-triangular solve; lane u holds the value of column u; each
+        // multiplier is published as soon as it is known
         u32 v = (u32)lane < nw ? red(acc[cw]) : 0u;
-        const u32 inv = (u32)lane < nw ? s_dw[lane].z : 0u;
-        u32 nact = 0;
         for (u32 t = 0; t < nw; ++t) {
           const u32 vt = __shfl_sync(0xffffffffu, v, t);
-          const u32 it = __shfl_sync(0xffffffffu, inv, t);
           u32 m = 0;
           if (vt) {
-            m = fp.to_mont(fp.neg(fp.mul(vt, it)));
+            m = fp.mont_mul(p - vt, s_X[t]);  // -(v_t / lead_t), Montgomery form
             if ((u32)lane > t) v = fp.add(v, fp.mont_mul(m, s_P[t][lane]));
-            if (lane == 0) s_act[nact] = t;
-            ++nact;
           }
-          if (lane == 0) s_m[t] = m;
+          if (lane == 0) vm[t] = m;
         }
-        if (lane == 0) s_nact = nact;
+      } else {
+        // (4) meanwhile: the rest of each published tail — columns right of
+        // the window and the non-A columns inside it
+        for (u32 t = warp - 1; t < nw; t += NWARP - 1) {
+          u32 m;
+          while ((m = vm[t]) == PENDING) {
+          }
+          if (!m) continue;
+          const uint4 d = s_dw[t];
+          ++n_piv;
+          n_tail += d.y - d.x;
+          for (u32 k0 = d.x; k0 < d.y; k0 += 32 * 4) {
+            u32 cc[4], vv[4];
+#pragma unroll
+            for (int z = 0; z < 4; ++z) {
+              const u32 k = k0 + z * 32 + lane;
+              cc[z] = k < d.y ? __ldg(col + k) : N;
+              vv[z] = k < d.y ? __ldg(val + k) : 0u;
+            }
+#pragma unroll
+            for (int z = 0; z < 4; ++z) {
+              const u32 cz = cc[z];
+              if (cz < N && (cz > clast || !((abits[cz >> 5] >> (cz & 31)) & 1u)))
+                atomicAdd(acc + cz, fp.mont_mul(m, vv[z]));
+            }
+          }
+        }
       }
       __syncthreads();
-      // (4) the rest of every active tail: columns right of the window and
-      // the non-A columns inside it; P rows cleared for the next window
-      const u32 nact = s_nact;
-      if (tid == 0) {
-        n_piv += nact;
-        for (u32 q = 0; q < nact; ++q) n_tail += s_dw[s_act[q]].y - s_dw[s_act[q]].x;
-      }
+      // clear the window state: P rows (by their staging warp), multipliers
       for (u32 t = warp; t < nw; t += NWARP) s_P[t][lane] = 0;
-      for (u32 q = warp; q < nact; q += NWARP) {
-        const u32 t = s_act[q];
-        const uint4 d = s_dw[t];
-        const u32 m = s_m[t];
-        for (u32 k0 = d.x; k0 < d.y; k0 += 32 * 4) {
-          u32 cc[4], vv[4];
-#pragma unroll
-          for (int z = 0; z < 4; ++z) {
-            const u32 k = k0 + z * 32 + lane;
-            cc[z] = k < d.y ? __ldg(col + k) : N;
-            vv[z] = k < d.y ? __ldg(val + k) : 0u;
-          }
-#pragma unroll
-          for (int z = 0; z < 4; ++z) {
-            const u32 cz = cc[z];
-            if (cz < N && (cz > clast || !((abits[cz >> 5] >> (cz & 31)) & 1u)))
-              atomicAdd(acc + cz, fp.mont_mul(m, vv[z]));
-          }
-        }
-      }
-      __syncthreads();
+      if (tid < BW) s_m[tid] = PENDING;
       from = clast + 1;
     }
     u32* out = Dp + (size_t)rr * K;
@@ -490,7 +492,7 @@ __global__ void __launch_bounds__(256) k_sweep_blk(Fp fp, u32 mu, const u32* __r
     }
     __syncthreads();
   }
-  if (stats && tid == 0 && n_piv) {
+  if (stats && lane == 0 && n_piv) {
     atomicAdd(stats, n_piv);
     atomicAdd(stats + 1, n_tail);
   }
