@@ -307,8 +307,8 @@ def roofline_for(kprof, records, peak, peak_src, want):
                "traffic": None, "launches": cnt, "avg_launch_us": ns / cnt / 1e3, "peak_source": peak_src,
                "share_of_step": ns / total, "algorithmic_bytes_per_launch": tot / cnt}
         if "k_sweep" in name:
-            out["note"] = ("pivot-row stream is L2-resident (rows reused by every C row); "
-                           "latency-bound: one CTA barrier per pivot application")
+            out["note"] = ("pivot-row stream is L2-resident (rows reused by every C row); blocked sweep: "
+                           "3 CTA barriers per 32-A-column window, shared-atomic tail application")
         return out
     return None
 

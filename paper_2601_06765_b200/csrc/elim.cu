@@ -675,6 +675,109 @@ __global__ void __launch_bounds__(256) k_dense_forward(Fp fp, u32* Dp, u32 R, u3
   }
 }
 
+// E3a (CTA-cooperative rows): the per-pivot schedule of k_dense_forward, but
+// each row update is done by the whole CTA (K / 256 elements per thread, all
+// loads in flight) and the row's new leading column comes out of the update
+// itself (per-thread first nonzero, block min) — the per-pivot critical path
+// is one grid barrier + one pivot-row round trip instead of a warp-serial
+// sweep over K.  Row state (lead, used) lives in shared memory.
+static constexpr int DF_MAXROWS = 64;
+__global__ void __launch_bounds__(256) k_dense_forward_cta(Fp fp, u32* Dp, u32 R, u32 K, unsigned long long* cand,
+                                                           u32* piv_of_col) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ u32 s_lead[DF_MAXROWS];
+  __shared__ uint8_t s_used[DF_MAXROWS];
+  __shared__ u32 s_red[8];
+  __shared__ u32 s_inv;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const u32 G = gridDim.x;
+  const u32 lo = (u32)(((unsigned long long)R * blockIdx.x) / G);
+  const u32 hi = (u32)(((unsigned long long)R * (blockIdx.x + 1)) / G);
+  const u32 nr = hi - lo;
+  // first nonzero of row i at or after `from`, by the whole CTA
+  auto block_first = [&](const u32* row, u32 from) -> u32 {
+    u32 f = K;
+    for (u32 q = from + tid; q < K; q += blockDim.x)
+      if (row[q]) {
+        f = q;
+        break;
+      }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) f = min(f, __shfl_xor_sync(0xffffffffu, f, o));
+    if (lane == 0) s_red[warp] = f;
+    __syncthreads();
+    u32 m = K;
+    for (int w = 0; w < 8; ++w) m = min(m, s_red[w]);
+    __syncthreads();
+    return m;
+  };
+  for (u32 r = 0; r < nr; ++r) {
+    const u32 l = block_first(Dp + (size_t)(lo + r) * K, 0);
+    if (tid == 0) {
+      s_lead[r] = l;
+      s_used[r] = 0;
+    }
+  }
+  __syncthreads();
+  for (u32 step = 0;; ++step) {
+    if (tid == 0) {
+      unsigned long long m = ~0ull;
+      for (u32 r = 0; r < nr; ++r)
+        if (!s_used[r] && s_lead[r] < K) m = min(m, ((unsigned long long)s_lead[r] << 32) | (lo + r));
+      if (m != ~0ull) atomicMin(cand + step, m);
+    }
+    grid.sync();
+    const unsigned long long win = __ldcg(cand + step);
+    if (win == ~0ull) break;
+    const u32 c = (u32)(win >> 32), pr = (u32)(win & 0xFFFFFFFFull);
+    const u32* prow_p = Dp + (size_t)pr * K;
+    if (tid == 0) {
+      s_inv = fp.inv(__ldcg(prow_p + c));
+      if (pr >= lo && pr < hi) {
+        s_used[pr - lo] = 1;
+        piv_of_col[c] = pr;
+      }
+    }
+    __syncthreads();
+    const u32 inv = s_inv;
+    for (u32 r = 0; r < nr; ++r) {
+      if (s_used[r] || s_lead[r] != c) continue;
+      u32* row = Dp + (size_t)(lo + r) * K;
+      const u32 fm = fp.to_mont(fp.neg(fp.mul(row[c], inv)));
+      // row[q] += fm * prow[q] for q >= c; track this thread's first nonzero > c
+      u32 f = K;
+      for (u32 qb = c + tid; qb < K; qb += blockDim.x * 8) {
+        u32 pv[8], rv[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const u32 q = qb + blockDim.x * j;
+          pv[j] = q < K ? __ldcg(prow_p + q) : 0u;
+          rv[j] = q < K ? row[q] : 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const u32 q = qb + blockDim.x * j;
+          if (q < K) {
+            const u32 nv = fp.add(rv[j], fp.mont_mul(fm, pv[j]));
+            row[q] = nv;
+            if (nv && q > c && q < f) f = q;
+          }
+        }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) f = min(f, __shfl_xor_sync(0xffffffffu, f, o));
+      if (lane == 0) s_red[warp] = f;
+      __syncthreads();
+      if (tid == 0) {
+        u32 m = K;
+        for (int w = 0; w < 8; ++w) m = min(m, s_red[w]);
+        s_lead[r] = m;
+      }
+      __syncthreads();
+    }
+  }
+}
+
 // E3a (rounds): every live row whose leading column has no pivot claims it
 // (lowest row index wins, one atomicMin per row) and computes the inverse of
 // its own lead; then every other live row is reduced by the pivot of its
@@ -1128,6 +1231,23 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
         }
         cudaGetLastError();
       }
+    }
+    // default: CTA-cooperative per-pivot kernel when every CTA's row range fits
+    // its shared row state
+    static const bool dense_warp = getenv("F4B_DENSE") && !strcmp(getenv("F4B_DENSE"), "warp");
+    int bpc = 0;
+    check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpc, k_dense_forward_cta, 256, 0), "occupancy");
+    static const int dcta = getenv("F4B_DENSE_CTAS") ? atoi(getenv("F4B_DENSE_CTAS")) : 4;
+    const int GC = (int)std::min<long long>((long long)c->num_sms * std::max(1, std::min(bpc, dcta)),
+                                            std::max<long long>(R, 1));
+    // narrow D' blocks keep the warp-per-row kernel (a CTA per 459-wide row
+    // update idles most of its threads)
+    if (!done_cluster && !dense_warp && K >= 1024 && (long long)R <= (long long)GC * DF_MAXROWS) {
+      void* args3[] = {&fp, &dpp, &Ru, &Ku, &candp, &pofcp};
+      ProfScope ps(c, "k_dense_forward_cta");
+      check_cuda(cudaLaunchCooperativeKernel((void*)k_dense_forward_cta, GC, 256, args3, 0, c->stream),
+                 "k_dense_forward_cta");
+      done_cluster = true;
     }
     // F4B_DENSE=rounds: claim-all-leads rounds (2 grid barriers per round
     // instead of 1 per pivot) — measured slower on cyclic-8 (a row reduced by
