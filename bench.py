@@ -341,6 +341,22 @@ def main():
     from paper_2601_06765_b200.symbolic import compile_batch
 
     ring, st, batches, setup_s = capture_workload()
+    # the whole run also ends with the device interreduction (§8f.1); report
+    # both next to the reference's own timings of the same run (golden file)
+    from paper_2601_06765_b200.groebner import reduce_basis_device
+
+    t0 = time.perf_counter()
+    gb = reduce_basis_device(st.basis, ring)
+    reduce_s = time.perf_counter() - t0
+    full_run = {"system": "cyclic-8 / F_32003", "f4_loop_s": round(setup_s, 3), "reduce_basis_s": round(reduce_s, 3),
+                "gb_size": len(gb)}
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "cyclic8_p32003.json")) as fh:
+            g = json.load(fh)
+        full_run.update(reference_f4_loop_s=g["f4_loop_s"], reference_reduce_basis_s=g["reduce_basis_s"],
+                        reference_gb_size=g["gb_size"])
+    except Exception:
+        pass
     eng = Engine.for_ring(ring, local)
     total_M = sum(b["M"] for b in batches)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -485,7 +501,7 @@ def main():
             "roofline": roof, "roofline_symbolic": roof_sym, "cpu_baseline": cpu, "e2e": e2e,
             "clocks": clk.summary(),
             "gpu_launches": launches1 - launches0, "wall_ms_per_step": 1000 * wall / args.steps,
-            "setup_s": round(setup_s, 2), "kernels_top": kernels,
+            "setup_s": round(setup_s, 2), "full_run": full_run, "kernels_top": kernels,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

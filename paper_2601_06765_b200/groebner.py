@@ -388,6 +388,47 @@ def reduce_basis(polys: list, ring: Ring) -> list:
     return minimal
 
 
+def _minimal_monic(polys: list, ring: Ring) -> list:
+    work = sorted((poly_monic(f) for f in polys if not f.is_zero()), key=lambda f: ring.sort_key(f.lm()))
+    minimal = []
+    for f in work:
+        if not any(mon_divides(g.lm(), f.lm()) for g in minimal):
+            minimal.append(f)
+    return minimal
+
+
+def reduce_basis_device(polys: list, ring: Ring) -> list:
+    """Final interreduction of a Gröbner basis as ONE extra Macaulay matrix on
+    the GPU: the minimal basis (same selection as
+    reduce_basis, reference :314-332) as shift-0 rows, closed under one-step
+    reduction by compile_batch, then the fully reduced echelon form.  With all
+    reducers of every non-leading monomial present, the RREF row led by LM(g)
+    has no other term divisible by a leading monomial: it is the reduced basis
+    element for g — the unique reduced Gröbner basis the reference's
+    normal-form loop converges to (for a Gröbner basis input)."""
+    from .polynomials import soa_pack
+    from .symbolic import Row, RowRole
+
+    minimal = _minimal_monic(polys, ring)
+    if not minimal:
+        return []
+    soa = soa_pack(minimal, ring)
+    zero = (0,) * ring.n_vars
+    rows = [Row(zero, k, RowRole.SPOLY_HALF, 0) for k in range(len(minimal))]
+    plan = compile_batch(rows, soa, Closure.ONE_STEP_REDUCTION)
+    ech = psge_reduce(csr_from_plan(plan, ring.modulus))
+    ex = plan.dict_exps()
+    rp, ci = plan.row_ptr, plan.col_ind
+    lead_cols = {int(ci[rp[k]]) for k in range(len(minimal))}
+    out = []
+    for lead, cols, vals in ech.pivot_rows:
+        if lead in lead_cols:
+            out.append(Poly(ring, tuple((tuple(int(x) for x in ex[c]), int(v)) for c, v in zip(cols.tolist(),
+                                                                                          vals.tolist()))))
+    out.sort(key=lambda f: ring.sort_key(f.lm()), reverse=True)
+    return out
+
+
 def f4_groebner(system: list, ring: Ring, config: F4Config | None = None) -> list:
     """Reduced Gröbner basis via the GPU F4 driver (reference :335-350)."""
     config = config or F4Config()
@@ -402,7 +443,7 @@ def f4_groebner(system: list, ring: Ring, config: F4Config | None = None) -> lis
             raise NonterminationError(f"f4 exceeded {config.max_steps} batches")
         f4_step(state, config)
         steps += 1
-    return reduce_basis(state.basis, ring)
+    return reduce_basis_device(state.basis, ring)
 
 
 @dataclass
