@@ -149,6 +149,26 @@ int f4b_spmm(f4b_ctx* ctx, int64_t n_rows, int64_t n_cols, const int64_t* row_pt
              const int64_t* col_ind, const uint64_t* val, const uint64_t* X, int64_t b,
              uint64_t* Y);
 
+/* Device-resident black-box operator for Block Wiedemann (sparselin.py:450-548):
+ * B = A (square, normal = 0) or B = AᵀA (normal = 1, Aᵀ built once).  The CSR
+ * stays in HBM across applications; vectors are host [dim][b] u64 residues. */
+typedef struct f4b_op f4b_op;
+int f4b_op_create(f4b_ctx* ctx, int64_t n_rows, int64_t n_cols, const int64_t* row_ptr,
+                  const int64_t* col_ind, const uint64_t* val, int normal, f4b_op** out);
+int f4b_op_free(f4b_op* op);
+/* Y = B X */
+int f4b_op_apply(f4b_op* op, const uint64_t* X, int64_t b, uint64_t* Y);
+/* seqs[k][j] = sum_i U[i][j] (B^k V)[i][j] mod p for k < steps (the Krylov
+ * projections, sparselin.py:408-412), all applications on the device */
+int f4b_op_krylov(f4b_op* op, const uint64_t* U, const uint64_t* V, int64_t b, int64_t steps,
+                  uint64_t* seqs);
+/* out = sum_i g[i] B^i v, Horner from g[len-1] (sparselin.py:425-429) */
+int f4b_op_horner(f4b_op* op, const uint64_t* g, int64_t len, const uint64_t* v, uint64_t* out);
+/* acc = v; repeat up to max_steps: nxt = B acc, stop before nxt == 0, acc = nxt
+ * (sparselin.py:430-434); *taken = applications kept */
+int f4b_op_power_until_zero(f4b_op* op, const uint64_t* v, int64_t max_steps, uint64_t* out,
+                            int64_t* taken);
+
 #ifdef __cplusplus
 }
 #endif

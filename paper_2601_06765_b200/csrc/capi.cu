@@ -15,6 +15,8 @@ struct f4b_ctx {
   f4b::Ctx c;
 };
 
+f4b::Ctx* f4b_ctx_of(f4b_ctx* h) { return &h->c; }
+
 namespace f4b {
 
 [[noreturn]] void fail(int code, const std::string& msg) { throw Error{code, msg}; }

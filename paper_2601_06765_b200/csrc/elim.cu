@@ -1003,6 +1003,8 @@ static Fp make_fp(Ctx* c) {
   return fp;
 }
 
+Fp make_fp_pub(Ctx* c) { return make_fp(c); }
+
 static int sweep_grid(Ctx* c, size_t smem, long long rows) {
   int per_sm = (int)std::max<size_t>(1, std::min<size_t>(8, (220 * 1024) / std::max<size_t>(smem + 3072, 1)));
   return (int)std::max<long long>(1, std::min<long long>(rows, (long long)c->num_sms * per_sm));

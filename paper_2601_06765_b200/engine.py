@@ -80,6 +80,54 @@ class DevicePlan:
         return out
 
 
+class DeviceOperator:
+    """Handle of an ``f4b_op``: the CSR stays in HBM across applications."""
+
+    def __init__(self, engine, handle, dim):
+        self.engine = engine
+        self.h = handle
+        self.dim = dim
+        self._fin = weakref.finalize(self, engine.lib.f4b_op_free, handle)
+
+    def _chk(self, code, what):
+        self.engine.ctx.check(code, what)
+
+    def apply(self, X):
+        X = np.ascontiguousarray(X, dtype=np.uint64)
+        vec = X.ndim == 1
+        X2 = X.reshape(self.dim, -1)
+        Y = np.empty_like(X2)
+        self._chk(self.engine.lib.f4b_op_apply(self.h, ptr(X2, C.c_uint64), X2.shape[1], ptr(Y, C.c_uint64)),
+                  "operator apply")
+        return Y[:, 0] if vec else Y
+
+    def krylov(self, U, V, steps):
+        U = np.ascontiguousarray(U, dtype=np.uint64)
+        V = np.ascontiguousarray(V, dtype=np.uint64)
+        b = V.shape[1]
+        seqs = np.empty((steps, b), dtype=np.uint64)
+        self._chk(self.engine.lib.f4b_op_krylov(self.h, ptr(U, C.c_uint64), ptr(V, C.c_uint64), b, int(steps),
+                                                ptr(seqs, C.c_uint64)), "operator krylov")
+        return seqs
+
+    def horner(self, g, v):
+        g = np.ascontiguousarray(g, dtype=np.uint64)
+        v = np.ascontiguousarray(v, dtype=np.uint64).reshape(-1)
+        out = np.empty(self.dim, dtype=np.uint64)
+        self._chk(self.engine.lib.f4b_op_horner(self.h, ptr(g, C.c_uint64), len(g), ptr(v, C.c_uint64),
+                                                ptr(out, C.c_uint64)), "operator horner")
+        return out
+
+    def power_until_zero(self, v, max_steps):
+        v = np.ascontiguousarray(v, dtype=np.uint64).reshape(-1)
+        out = np.empty(self.dim, dtype=np.uint64)
+        taken = np.zeros(1, dtype=np.int64)
+        self._chk(self.engine.lib.f4b_op_power_until_zero(self.h, ptr(v, C.c_uint64), int(max_steps),
+                                                          ptr(out, C.c_uint64), ptr(taken, C.c_int64)),
+                  "operator power")
+        return out, int(taken[0])
+
+
 class DeviceEchelon:
     """Handle of an ``f4b_echelon``; pivot rows are computed on demand."""
 
@@ -287,6 +335,18 @@ class Engine:
                                              ptr(ci, C.c_int64), ptr(va, C.c_uint64), 1 if full else 0,
                                              C.byref(h)), "psge")
         return DeviceEchelon(self, h)
+
+    def operator(self, n_rows, n_cols, row_ptr, col_ind, val, normal: bool) -> "DeviceOperator":
+        """Resident black-box operator B = A (square) or AᵀA (normal) for Wiedemann."""
+        rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+        ci = np.ascontiguousarray(col_ind, dtype=np.int64)
+        va = np.ascontiguousarray(val, dtype=np.uint64)
+        h = C.c_void_p()
+        self.ctx.sync_stream()
+        self.ctx.check(self.lib.f4b_op_create(self.ctx.h, int(n_rows), int(n_cols), ptr(rp, C.c_int64),
+                                              ptr(ci, C.c_int64), ptr(va, C.c_uint64), 1 if normal else 0,
+                                              C.byref(h)), "operator")
+        return DeviceOperator(self, h, int(n_cols))
 
     def spmm(self, n_rows, n_cols, row_ptr, col_ind, val, X):
         X = np.ascontiguousarray(X, dtype=np.uint64)

@@ -392,3 +392,39 @@ def test_full_run_final_basis_matches_reference(cuda, name, gen, args):
     ref = load_golden(name)
     assert len(gb) == ref["gb_size"]
     assert hashlib.sha256(format_system(ring, gb).encode()).hexdigest() == ref["final_sha256"]
+
+
+@pytest.mark.parametrize("shape", [(37, 37), (53, 29)])
+def test_resident_operator_matches_numpy(cuda, shape):
+    """f4b_op_*: Krylov projections, Horner evaluation and the power loop of
+    wiedemann_solve (reference sparselin.py:408-434) against the NumPy loop."""
+    from paper_2601_06765_b200.sparselin import _engine_for, csr_transpose, spmm
+
+    p = 65521
+    m = FieldModulus(p)
+    rng = np.random.default_rng(3)
+    r, c = shape
+    dense = rng.integers(0, p, (r, c), dtype=np.uint64) * (rng.random((r, c)) < 0.2)
+    A = csr_from_dense(dense, m)
+    normal = r != c
+    op = _engine_for(m).operator(A.n_rows, A.n_cols, A.row_ptr, A.col_ind, A.val, normal)
+    P = np.uint64(p)
+    At = csr_transpose(A) if normal else None
+    apply_b = (lambda X: spmm(At, spmm(A, X))) if normal else (lambda X: spmm(A, X))
+    b = 3
+    V = rng.integers(0, p, (c, b), dtype=np.uint64)
+    U = rng.integers(0, p, (c, b), dtype=np.uint64)
+    steps = 12
+    ref = np.empty((steps, b), dtype=np.uint64)
+    W = V.copy()
+    for k in range(steps):
+        ref[k] = ((U * W) % P).sum(axis=0, dtype=np.uint64) % P
+        W = apply_b(W)
+    assert np.array_equal(op.krylov(U, V, steps), ref)
+    g = rng.integers(0, p, 6, dtype=np.uint64)
+    v = V[:, :1]
+    acc = g[-1] * v % P
+    for cc in g[:-1][::-1].tolist():
+        acc = (apply_b(acc) + np.uint64(cc) * v) % P
+    assert np.array_equal(op.horner(g, V[:, 0]), acc[:, 0])
+    assert np.array_equal(op.apply(V), apply_b(V))
