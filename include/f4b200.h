@@ -113,6 +113,11 @@ int f4b_plan_download(const f4b_plan* plan, int64_t* row_ptr, int64_t* col_ind, 
  * (monomials.py:131-148; big-endian u64 words, W = ceil((32 [graded] +
  * 16 n_vars) / 64)) in column order (descending), [N][W], built on the device. */
 int f4b_plan_download_ref_keys(const f4b_plan* plan, uint64_t* keys);
+/* Y = Aᵀ V over the plan's matrix (A = r x N, V [r][b], Y [N][b], u64
+ * residues): the left-kernel check vᵀA = 0 of verify_kernel_syzygy
+ * (groebner.py:409-428) — row i of the plan is exactly t_i g_{k_i} over the
+ * dictionary, so Y = 0 is the exact recombination Σ v_i t_i g_{k_i} = 0. */
+int f4b_plan_left_apply(const f4b_plan* plan, const uint64_t* V, int64_t b, uint64_t* Y);
 int f4b_plan_free(f4b_plan* plan);
 
 typedef struct {

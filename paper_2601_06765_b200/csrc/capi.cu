@@ -685,6 +685,49 @@ int f4b_plan_download_ref_keys(const f4b_plan* pl, uint64_t* keys) {
   API_END
 }
 
+// Y[col][j] += v[row][j] * a[row][col]: warp per row, u64 atomics of
+// reduced products (< 2^31 each, so 2^32 of them fit before the final mod)
+__global__ void k_left_apply(Fp fp, const u32* __restrict__ rp, const u32* __restrict__ col,
+                             const u32* __restrict__ val, long long r, const u32* __restrict__ V, int b,
+                             unsigned long long* __restrict__ Y) {
+  const long long row = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x & 31;
+  if (row >= r) return;
+  const u32 s = rp[row], e = rp[row + 1];
+  for (int j = 0; j < b; ++j) {
+    const u32 vj = V[(size_t)row * b + j];
+    if (!vj) continue;
+    for (u32 k = s + lane; k < e; k += 32) atomicAdd(Y + (size_t)col[k] * b + j, (unsigned long long)fp.mul(vj, val[k]));
+  }
+}
+
+int f4b_plan_left_apply(const f4b_plan* pl, const uint64_t* V, int64_t b, uint64_t* Y) {
+  if (!pl || b < 1) return F4B_ERR_PRECONDITION;
+  API_BEGIN(pl->ctx)
+  Ctx* c = _c;
+  const long long r = pl->r, N = pl->N;
+  Fp fp;
+  fp.p = c->p;
+  fp.pprime = c->pprime;
+  fp.r2 = c->r2;
+  std::vector<u32> hv((size_t)std::max<long long>(r * b, 1));
+  for (long long i = 0; i < r * b; ++i) hv[i] = (u32)(V[i] % c->p);
+  DBuf dv, dy;
+  ensure(c, dv, hv.size() * 4);
+  ensure(c, dy, (size_t)std::max<long long>(N * b, 1) * 8);
+  check_cuda(cudaMemcpyAsync(dv.p, hv.data(), (size_t)r * b * 4, cudaMemcpyHostToDevice, c->stream), "h2d");
+  check_cuda(cudaMemsetAsync(dy.p, 0, (size_t)std::max<long long>(N * b, 1) * 8, c->stream), "memset");
+  if (r) F4B_LAUNCH(c, k_left_apply, (int)((r * 32 + 255) / 256), 256, 0, fp, pl->row_ptr.as<u32>(), pl->col_ind.as<u32>(),
+                    pl->val.as<u32>(), r, dv.as<u32>(), (int)b, dy.as<unsigned long long>());
+  std::vector<unsigned long long> hy((size_t)std::max<long long>(N * b, 1));
+  check_cuda(cudaMemcpyAsync(hy.data(), dy.p, (size_t)N * b * 8, cudaMemcpyDeviceToHost, c->stream), "d2h");
+  check_cuda(cudaStreamSynchronize(c->stream), "sync");
+  for (long long i = 0; i < N * b; ++i) Y[i] = hy[i] % c->p;
+  release(c, dv);
+  release(c, dy);
+  API_END
+}
+
 int f4b_plan_free(f4b_plan* pl) {
   plan_release(pl);
   return F4B_OK;

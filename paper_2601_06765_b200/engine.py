@@ -50,6 +50,16 @@ class DevicePlan:
         self.info = {k: int(getattr(info, k)) for k, _ in PlanInfo._fields_}
         self._fin = weakref.finalize(self, engine.lib.f4b_plan_free, handle)
 
+    def left_apply(self, V):
+        """Aᵀ V over the device plan (V: r x b) -> N x b."""
+        V = np.ascontiguousarray(V, dtype=np.uint64)
+        vec = V.ndim == 1
+        V2 = V.reshape(self.info["r"], -1)
+        Y = np.empty((self.info["N"], V2.shape[1]), dtype=np.uint64)
+        self.engine.ctx.check(self.engine.lib.f4b_plan_left_apply(self.h, ptr(V2, C.c_uint64), V2.shape[1],
+                                                                   ptr(Y, C.c_uint64)), "plan left apply")
+        return Y[:, 0] if vec else Y
+
     def download_ref_keys(self, n_key_words):
         """LayoutPlan.dict_keys built on the device (reference key format)."""
         out = host_empty((self.info["N"], n_key_words), np.uint64)

@@ -463,8 +463,23 @@ def is_groebner(G: list, ring: Ring) -> GroebnerReport:
 
 
 def verify_kernel_syzygy(plan: LayoutPlan, basis: list, kernel: KernelBasis) -> GroebnerReport:
-    """Exact recombination sum_i v_i (t_i g_{k_i}) == 0 (reference :409-428)."""
+    """Exact recombination sum_i v_i (t_i g_{k_i}) == 0 (reference :409-428).
+
+    For a device plan this is one Aᵀ·V over the resident CSR:
+    row i of the plan is exactly t_i g_{k_i} over the dictionary monomials,
+    so Aᵀ v = 0 is the recombination itself."""
     ring = plan.ring
+    dev = getattr(plan, "device", None)
+    if dev is not None and kernel.vectors:
+        for n, v in enumerate(kernel.vectors):
+            if len(v) != plan.n_rows:
+                return GroebnerReport(False, f"kernel vector {n} has wrong length")
+        V = np.stack([np.asarray(v, dtype=np.uint64) % np.uint64(ring.modulus.p) for v in kernel.vectors], axis=1)
+        Y = dev.left_apply(V)
+        for n in range(V.shape[1]):
+            if Y[:, n].any():
+                return GroebnerReport(False, f"kernel vector {n} recombines to a nonzero polynomial")
+        return GroebnerReport(True)
     for n, v in enumerate(kernel.vectors):
         if len(v) != plan.n_rows:
             return GroebnerReport(False, f"kernel vector {n} has wrong length")

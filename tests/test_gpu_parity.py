@@ -428,3 +428,30 @@ def test_resident_operator_matches_numpy(cuda, shape):
         acc = (apply_b(acc) + np.uint64(cc) * v) % P
     assert np.array_equal(op.horner(g, V[:, 0]), acc[:, 0])
     assert np.array_equal(op.apply(V), apply_b(V))
+
+
+def test_verify_kernel_syzygy_device(cuda):
+    """§8f.3: the left-kernel recombination check on the device plan agrees
+    with the reference's polynomial recombination (host path)."""
+    from paper_2601_06765_b200.groebner import verify_kernel_syzygy
+    from paper_2601_06765_b200.sparselin import KernelBasis
+    from paper_2601_06765_b200.symbolic import LayoutPlan
+
+    ring, polys = gen_cyclic(5, 32003)
+    st = GroebnerState(ring)
+    for f in polys:
+        update_pairs(st, poly_monic(f))
+    for _ in range(4):
+        f4_step(st)
+    spec, _ = select_batch(st)
+    soa = st.soa()
+    plan = compile_batch(select_rows(spec, soa), soa, Closure.ONE_STEP_REDUCTION)
+    kb = left_kernel(csr_from_plan(plan, ring.modulus), count=3, seed=0)
+    assert kb.vectors, "expected dependent rows in this batch"
+    host = LayoutPlan(ring, plan.row_ptr, plan.col_ind, plan.val, plan.dict_keys, plan.row_meta, plan.counters)
+    assert verify_kernel_syzygy(plan, st.basis, kb).ok and verify_kernel_syzygy(host, st.basis, kb).ok
+    bad = [np.array(v, dtype=np.uint64).copy() for v in kb.vectors]
+    bad[0][int(np.flatnonzero(bad[0])[0])] += 1
+    kbad = KernelBasis(kb.side, bad, len(bad), kb.seed_trail)
+    assert not verify_kernel_syzygy(plan, st.basis, kbad).ok
+    assert not verify_kernel_syzygy(host, st.basis, kbad).ok
