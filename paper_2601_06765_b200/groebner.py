@@ -186,6 +186,24 @@ def _minimal_mask(u: np.ndarray) -> np.ndarray:
     return keep
 
 
+def _unique_rows(a: np.ndarray):
+    """np.unique(a, axis=0, return_inverse=True) for small non-negative
+    exponent rows: rows packed into one int64 (most significant = column 0,
+    so numeric order = lexicographic row order) when they fit, which replaces
+    the structured-dtype sort by a plain integer sort."""
+    if len(a):
+        mx = int(a.max())
+        bits = max(1, mx.bit_length())
+        if int(a.min()) >= 0 and bits * a.shape[1] <= 62:
+            key = np.zeros(len(a), dtype=np.int64)
+            for j in range(a.shape[1]):
+                key = (key << bits) | a[:, j]
+            _, idx, inv = np.unique(key, return_index=True, return_inverse=True)
+            return a[idx], inv.reshape(-1)
+    uq, inv = np.unique(a, axis=0, return_inverse=True)
+    return uq, inv.reshape(-1)
+
+
 def update_pairs(state: GroebnerState, new_poly: Poly) -> GroebnerState:
     """Append a monic polynomial with Gebauer–Möller pruning (reference :154-201)."""
     if new_poly.is_zero() or new_poly.lc() != 1:
@@ -198,8 +216,7 @@ def update_pairs(state: GroebnerState, new_poly: Poly) -> GroebnerState:
     # new pairs (i, t): chain criterion among themselves
     lcm = np.maximum(L, lm_t[None, :])
     if t:
-        uq, inv = np.unique(lcm, axis=0, return_inverse=True)
-        inv = inv.reshape(-1)
+        uq, inv = _unique_rows(lcm)
         kept = _minimal_mask(uq)[inv]
         kept_idx = np.flatnonzero(kept)
         # one representative per lcm: the lowest partner index
