@@ -358,6 +358,7 @@ def main():
     except Exception:
         pass
     eng = Engine.for_ring(ring, local)
+    eng.sync_basis(st.soa())  # the interreduction above replaced the device basis
     total_M = sum(b["M"] for b in batches)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 

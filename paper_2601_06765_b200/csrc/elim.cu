@@ -30,6 +30,7 @@
 #include <cstring>
 #include <vector>
 
+#include "block.cuh"
 #include "common.cuh"
 #include "engine.h"
 
@@ -124,6 +125,136 @@ __global__ void k_compact_idx(const uint8_t* __restrict__ flags, const u32* __re
                               u32* __restrict__ out) {
   long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n && flags[i]) out[pos[i]] = (u32)i;
+}
+
+// ---------------------------------------------------------------------------
+// E1 fused (one cooperative launch): pivot selection, column structure, the
+// A-column bitmap, A / non-A column lists (ascending), A-column positions and
+// the C-row list — the work of k_pivot_select, k_col_structure, k_bits, two
+// flag scans, three compactions and k_c_flags, with 4 grid barriers and one
+// host read of (nA, nC) instead of two.
+// ---------------------------------------------------------------------------
+struct PrepOut {
+  u32 nA, nC;
+};
+__global__ void __launch_bounds__(256) k_psge_prep(Fp fp, const u32* __restrict__ rp, const u32* __restrict__ col,
+                                                   const u32* __restrict__ val, u32 r, u32 N,
+                                                   unsigned long long* __restrict__ pk, u32* __restrict__ prow,
+                                                   u32* __restrict__ invl, uint4* __restrict__ desc,
+                                                   u32* __restrict__ abits, u32* __restrict__ acols,
+                                                   u32* __restrict__ apos, u32* __restrict__ nonA,
+                                                   u32* __restrict__ crows, u32* __restrict__ cnt, PrepOut* out) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ u32 ws[33];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const u32 G = gridDim.x;
+  const long long gt = (long long)blockIdx.x * blockDim.x + tid, GT = (long long)G * blockDim.x;
+  // contiguous, 32-aligned column chunks and row chunks per CTA
+  const u32 cw = (((N + G - 1) / G) + 31) & ~31u;
+  const u32 c_lo = min(N, blockIdx.x * cw), c_hi = min(N, c_lo + cw);
+  const u32 rw = (r + G - 1) / G;
+  const u32 r_lo = min(r, blockIdx.x * rw), r_hi = min(r, r_lo + rw);
+  auto bsum = [&](u32 v) -> u32 {
+    u32 t;
+    block_scan_excl(v, ws, &t);
+    return t;
+  };
+  for (long long c = gt; c < N; c += GT) pk[c] = ~0ull;
+  grid.sync();
+  // P1: pivot per distinct lead: fewest nonzeros, then lowest row (sparselin.py:316)
+  for (long long i = gt; i < r; i += GT) {
+    const u32 s = rp[i], e = rp[i + 1];
+    if (e > s) atomicMin(pk + col[s], ((unsigned long long)(e - s) << 32) | (unsigned long long)i);
+  }
+  grid.sync();
+  // P2: column structure over this CTA's chunk; A-column bitmap by warp ballot
+  {
+    u32 na = 0;
+    for (u32 c0 = c_lo; c0 < c_hi; c0 += blockDim.x) {
+      const u32 c = c0 + tid;
+      bool a = false;
+      if (c < c_hi) {
+        const unsigned long long k = __ldcg(pk + c);
+        a = k != ~0ull;
+        const u32 row = a ? (u32)(k & 0xFFFFFFFFull) : NONE;
+        const u32 inv = a ? fp.inv(val[rp[row]]) : 0u;
+        prow[c] = row;
+        invl[c] = inv;
+        desc[c] = a ? make_uint4(rp[row] + 1, rp[row + 1], inv, row) : make_uint4(0, 0, 0, NONE);
+      }
+      const unsigned bm = __ballot_sync(0xffffffffu, a);
+      if (lane == 0 && c < c_hi) abits[c >> 5] = bm;
+      na += a;
+    }
+    na = bsum(na);
+    if (tid == 0) cnt[blockIdx.x] = na;
+  }
+  grid.sync();
+  // P3: column positions; C-row flags counted per row chunk
+  u32 baseA = 0, nA = 0;
+  {
+    u32 sb = 0, st = 0;
+    for (u32 b = tid; b < G; b += blockDim.x) {
+      const u32 v = __ldcg(cnt + b);
+      st += v;
+      if (b < blockIdx.x) sb += v;
+    }
+    baseA = bsum(sb);
+    nA = bsum(st);
+  }
+  for (u32 c0 = c_lo; c0 < c_hi; c0 += blockDim.x) {
+    const u32 c = c0 + tid;
+    const bool a = c < c_hi && __ldcg(prow + c) != NONE;
+    u32 tt;
+    const u32 pre = block_scan_excl(a ? 1u : 0u, ws, &tt);
+    if (c < c_hi) {
+      const u32 pa = baseA + pre;  // A columns before c
+      if (a) {
+        acols[pa] = c;
+        apos[c] = pa;
+      } else {
+        nonA[c - pa] = c;
+      }
+    }
+    baseA += tt;
+  }
+  u32 nc = 0;
+  for (u32 i = r_lo + tid; i < r_hi; i += blockDim.x) {
+    const u32 s = rp[i], e = rp[i + 1];
+    nc += (e > s && __ldcg(prow + col[s]) != i);
+  }
+  nc = bsum(nc);
+  grid.sync();  // everyone has read cnt[] (column counts) before it is reused
+  if (tid == 0) cnt[blockIdx.x] = nc;
+  grid.sync();
+  // P4: C rows, ascending
+  u32 baseC = 0, nC = 0;
+  {
+    u32 sb = 0, st = 0;
+    for (u32 b = tid; b < G; b += blockDim.x) {
+      const u32 v = __ldcg(cnt + b);
+      st += v;
+      if (b < blockIdx.x) sb += v;
+    }
+    baseC = bsum(sb);
+    nC = bsum(st);
+  }
+  for (u32 i0 = r_lo; i0 < r_hi; i0 += blockDim.x) {
+    const u32 i = i0 + tid;
+    bool isc = false;
+    if (i < r_hi) {
+      const u32 s = rp[i], e = rp[i + 1];
+      isc = e > s && __ldcg(prow + col[s]) != i;
+    }
+    u32 tt;
+    const u32 pre = block_scan_excl(isc ? 1u : 0u, ws, &tt);
+    if (isc) crows[baseC + pre] = i;
+    baseC += tt;
+  }
+  if (blockIdx.x == 0 && tid == 0) {
+    out->nA = nA;
+    out->nC = nC;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1115,62 +1246,53 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
   u32* err = c->errflag.as<u32>();
   check_cuda(cudaMemsetAsync(err, 0, 4, c->stream), "memset");
   const long long Nn = std::max<long long>(N, 1);
-  // E1
-  DBuf pk;
+  // E1: one cooperative launch (k_psge_prep) and one read of (nA, nC)
+  DBuf pk, crows, pcnt;
   ensure(c, pk, Nn * sizeof(unsigned long long));
-  check_cuda(cudaMemsetAsync(pk.p, 0xFF, Nn * sizeof(unsigned long long), c->stream), "memset pk");
-  if (r) {
-    F4B_LAUNCH(c, k_pivot_select, nb(r, 256), 256, 0, E->rp, E->col, r, pk.as<unsigned long long>());
-    check_cuda(cudaGetLastError(), "k_pivot_select");
-  }
   ensure(c, E->prow, Nn * sizeof(u32));
   ensure(c, E->invl, Nn * sizeof(u32));
   ensure(c, E->desc, Nn * sizeof(uint4));
   ensure(c, E->abits, (size_t)((Nn + 31) / 32 + 1) * sizeof(u32));
-  ensure(c, c->flags, (size_t)2 * Nn + 32);
-  uint8_t* isA = c->flags.as<uint8_t>();
-  uint8_t* notA = isA + Nn + 16;
-  if (N) {
-    F4B_LAUNCH(c, k_col_structure, nb(N, 256), 256, 0, fp, pk.as<unsigned long long>(), N, E->rp, E->val,
-                                                        E->prow.as<u32>(), E->invl.as<u32>(), E->desc.as<uint4>(), isA, notA);
-    check_cuda(cudaGetLastError(), "k_col_structure");
-    F4B_LAUNCH(c, k_bits, nb((N + 31) / 32, 256), 256, 0, isA, N, E->abits.as<u32>());
-    check_cuda(cudaGetLastError(), "k_bits");
+  ensure(c, E->acols, (size_t)Nn * sizeof(u32));
+  ensure(c, E->nonA, (size_t)Nn * sizeof(u32));
+  ensure(c, E->apos, (size_t)Nn * sizeof(u32));
+  ensure(c, crows, (size_t)std::max<long long>(r, 1) * sizeof(u32));
+  {
+    static int bpp = -1;
+    if (bpp < 0) check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpp, k_psge_prep, 256, 0), "occupancy");
+    const int GP = c->num_sms * std::max(1, std::min(bpp, 2));
+    ensure(c, pcnt, (size_t)GP * sizeof(u32) + sizeof(PrepOut) + 16);
+    PrepOut* d_out = reinterpret_cast<PrepOut*>(pcnt.as<u32>() + GP);
+    u32 ru = (u32)r, Nu = (u32)N;
+    unsigned long long* pkp = pk.as<unsigned long long>();
+    u32* prowp = E->prow.as<u32>();
+    u32* invlp = E->invl.as<u32>();
+    uint4* descp = E->desc.as<uint4>();
+    u32* abitsp = E->abits.as<u32>();
+    u32* acolsp = E->acols.as<u32>();
+    u32* aposp = E->apos.as<u32>();
+    u32* nonAp = E->nonA.as<u32>();
+    u32* crowsp = crows.as<u32>();
+    u32* cntp = pcnt.as<u32>();
+    const u32* rpp = E->rp;
+    const u32* colp = E->col;
+    const u32* valp = E->val;
+    void* args[] = {&fp, &rpp, &colp, &valp, &ru, &Nu, &pkp, &prowp, &invlp, &descp, &abitsp, &acolsp, &aposp,
+                    &nonAp, &crowsp, &cntp, &d_out};
+    {
+      ProfScope ps(c, "k_psge_prep");
+      check_cuda(cudaLaunchCooperativeKernel((void*)k_psge_prep, GP, 256, args, 0, c->stream), "k_psge_prep");
+    }
+    PrepOut ho;
+    check_cuda(cudaMemcpyAsync(c->h_stat, d_out, sizeof(PrepOut), cudaMemcpyDeviceToHost, c->stream), "d2h");
+    check_cuda(cudaStreamSynchronize(c->stream), "sync");
+    memcpy(&ho, c->h_stat, sizeof(PrepOut));
+    E->nA = ho.nA;
+    E->K = N - E->nA;
+    E->nC = ho.nC;
   }
   release(c, pk);
-  // A columns / non-A columns
-  ensure(c, c->tmp_u32a, (size_t)(Nn + 2) * sizeof(u32));
-  ensure(c, c->tmp_u32b, (size_t)(Nn + 2) * sizeof(u32));
-  exclusive_scan_flags(c, isA, c->tmp_u32a.as<u32>(), N);
-  exclusive_scan_flags(c, notA, c->tmp_u32b.as<u32>(), N);
-  ensure(c, E->apos, (size_t)Nn * sizeof(u32));
-  if (N)
-    check_cuda(cudaMemcpyAsync(E->apos.p, c->tmp_u32a.p, (size_t)N * sizeof(u32), cudaMemcpyDeviceToDevice, c->stream),
-               "d2d apos");
-  E->nA = N ? read_u32(c, c->tmp_u32a.as<u32>() + N) : 0;
-  E->K = N - E->nA;
-  ensure(c, E->acols, (size_t)std::max<long long>(E->nA, 1) * sizeof(u32));
-  ensure(c, E->nonA, (size_t)std::max<long long>(E->K, 1) * sizeof(u32));
-  if (N) {
-    F4B_LAUNCH(c, k_compact_idx, nb(N, 256), 256, 0, isA, c->tmp_u32a.as<u32>(), N, E->acols.as<u32>());
-    F4B_LAUNCH(c, k_compact_idx, nb(N, 256), 256, 0, notA, c->tmp_u32b.as<u32>(), N, E->nonA.as<u32>());
-    check_cuda(cudaGetLastError(), "k_compact_idx");
-  }
-  // C rows
-  DBuf crows;
-  ensure(c, c->flags, (size_t)std::max<long long>(r, 1) + 32);
-  ensure(c, c->tmp_u32a, (size_t)(r + 2) * sizeof(u32));
-  if (r) {
-    F4B_LAUNCH(c, k_c_flags, nb(r, 256), 256, 0, E->rp, E->col, E->prow.as<u32>(), r, c->flags.as<uint8_t>());
-    check_cuda(cudaGetLastError(), "k_c_flags");
-  }
-  exclusive_scan_flags(c, c->flags.as<uint8_t>(), c->tmp_u32a.as<u32>(), r);
-  E->nC = r ? read_u32(c, c->tmp_u32a.as<u32>() + r) : 0;
-  ensure(c, crows, (size_t)std::max<long long>(E->nC, 1) * sizeof(u32));
-  if (r) {
-    F4B_LAUNCH(c, k_compact_idx, nb(r, 256), 256, 0, c->flags.as<uint8_t>(), c->tmp_u32a.as<u32>(), r, crows.as<u32>());
-    check_cuda(cudaGetLastError(), "k_compact_idx");
-  }
+  release(c, pcnt);
   // E2: D' = C swept over the A columns
   const long long R = E->nC, K = E->K;
   DBuf Dp, gacc, cand, used, pofc, lead;
