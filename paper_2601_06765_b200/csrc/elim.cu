@@ -28,6 +28,7 @@
 #include <climits>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include "block.cuh"
@@ -630,6 +631,341 @@ __global__ void __launch_bounds__(256) k_sweep_blk(Fp fp, u32 mu, const u32* __r
 }
 
 // ---------------------------------------------------------------------------
+// E2, fixed windows with precomputed block inverses.
+//
+// The A columns are cut into FIXED windows of 32 consecutive A columns
+// (acols[32j .. 32j+32)).  Inside window j the pivot rows form an upper
+// triangular block T_j (diagonal = lead coefficients, above it the pivot
+// rows' entries at the window's A columns).  Sweeping a row over window j
+// with values v (the row's entries at the window columns) produces the
+// multipliers m with  m T_j = -v,  i.e.  m = v W_j  with  W_j = -T_j^{-1}.
+// T_j depends only on the pivot rows, so W_j is built ONCE per matrix
+// (k_win_build, one warp per window) instead of being re-derived by a serial
+// 32-step solve in every C row; a C row then gets all 32 multipliers from one
+// 32x32 vector-matrix product (independent lanes, no serial chain, every warp
+// computes them itself: no barrier between solve and apply), and the active
+// pivots' tails are applied by the whole CTA as one flat list of 4-entry
+// groups (all loads of a window in flight at once).  One CTA barrier per
+// non-empty window.  The multipliers equal the column-by-column sweep's, so
+// D' is bit-identical with k_sweep<0> / k_sweep_blk.
+// ---------------------------------------------------------------------------
+static constexpr int WB_WARPS = 4;
+__global__ void __launch_bounds__(32 * WB_WARPS) k_win_build(Fp fp, const u32* __restrict__ col,
+                                                             const u32* __restrict__ val, u32 N,
+                                                             const uint4* __restrict__ desc,
+                                                             const u32* __restrict__ abits,
+                                                             const u32* __restrict__ acols,
+                                                             const u32* __restrict__ apos, u32 nA, u32 nwin,
+                                                             u32* __restrict__ winW, u32* __restrict__ winC,
+                                                             uint2* __restrict__ winD, u32* __restrict__ gcursor) {
+  __shared__ u32 sT[WB_WARPS][32][33];  // T[r][t] (Montgomery): pivot r's entry at window column t (r < t)
+  __shared__ u32 sC[WB_WARPS][32];      // window columns
+  __shared__ u32 sA[WB_WARPS][32][33];  // sA[u][s]: lane s's working vector
+  __shared__ u32 sM[WB_WARPS][32];      // nonzero pattern of T's row r
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const u32 j = blockIdx.x * WB_WARPS + warp;
+  if (j >= nwin) return;
+  const unsigned FULL = 0xffffffffu;
+  const u32 base = j * 32;
+  const u32 nw = min(32u, nA - base);
+  const u32 cw = (u32)lane < nw ? __ldg(acols + base + lane) : N;
+  const uint4 d = (u32)lane < nw ? __ldg(desc + cw) : make_uint4(0, 0, 1, NONE);
+  winC[base + lane] = cw;
+  {
+    // packed-tail slots: ceil(len / 4) groups of 4 entries per pivot, the
+    // window's groups reserved with one atomicAdd (any placement works: the
+    // sweep only follows winD)
+    const u32 ng = (d.y - d.x + 3) >> 2;
+    u32 x = ng;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const u32 y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    u32 gb = 0;
+    if (lane == 31) gb = atomicAdd(gcursor, x);
+    gb = __shfl_sync(0xffffffffu, gb, 31);
+    winD[base + lane] = make_uint2(gb + x - ng, gb + x);
+  }
+  sC[warp][lane] = cw;
+  const u32 clast = __shfl_sync(FULL, cw, nw - 1);
+  for (int r = 0; r < 32; ++r) sT[warp][r][lane] = 0;
+  sM[warp][lane] = 0;
+  __syncwarp();
+  auto place = [&](u32 r, u32 cc, u32 v) {
+    if (cc <= clast && ((abits[cc >> 5] >> (cc & 31)) & 1u)) {
+      u32 lo = 0, hi = 32;  // position of cc among the window columns
+      while (lo + 1 < hi) {
+        const u32 mid = (lo + hi) >> 1;
+        if (sC[warp][mid] <= cc) lo = mid; else hi = mid;
+      }
+      sT[warp][r][lo] = fp.to_mont(v);
+      atomicOr(&sM[warp][r], 1u << lo);
+    }
+  };
+  // in-window entries: the first 32 tail entries of 8 pivots per round (all
+  // loads in flight), the rare longer in-window prefix continued afterwards
+  for (u32 r0 = 0; r0 < nw; r0 += 8) {
+    u32 cc[8], vv[8];
+#pragma unroll
+    for (int h = 0; h < 8; ++h) {
+      const u32 r = r0 + h;
+      const u32 x = __shfl_sync(FULL, d.x, r & 31), y = __shfl_sync(FULL, d.y, r & 31);
+      const u32 k = x + lane;
+      const bool ok = r < nw && k < y;
+      cc[h] = ok ? __ldg(col + k) : 0xFFFFFFFFu;
+      vv[h] = ok ? __ldg(val + k) : 0u;
+    }
+#pragma unroll
+    for (int h = 0; h < 8; ++h) {
+      const u32 r = r0 + h;
+      place(r, cc[h], vv[h]);
+      if (r < nw && __shfl_sync(FULL, cc[h], 31) <= clast) {
+        const u32 x = __shfl_sync(FULL, d.x, r), y = __shfl_sync(FULL, d.y, r);
+        for (u32 k0 = x + 32; k0 < y; k0 += 32) {
+          const u32 k = k0 + lane;
+          const u32 c2 = k < y ? __ldg(col + k) : 0xFFFFFFFFu;
+          place(r, c2, k < y ? __ldg(val + k) : 0u);
+          if (__shfl_sync(FULL, c2, 31) > clast) break;
+        }
+      }
+    }
+  }
+  __syncwarp();
+  // lane s solves x T = e_s right-looking (Montgomery domain), its vector in
+  // shared memory (sA[u][s], conflict free; a rolled loop keeps the code in
+  // the instruction cache): x_t = a_t / lead_t, then a_u -= x_t T[t][u]
+  const u32 ilm_l = fp.to_mont(d.z);
+  const u32 one_m = fp.to_mont(1u);
+  for (int u = 0; u < 32; ++u) sA[warp][u][lane] = lane == u ? one_m : 0u;
+  __syncwarp();
+  for (int t = 0; t < 32; ++t) {
+    const u32 xt = fp.mont_mul(sA[warp][t][lane], __shfl_sync(FULL, ilm_l, t));
+    sA[warp][t][lane] = xt;
+    for (u32 mk = sM[warp][t]; mk; mk &= mk - 1) {  // the nonzeros of row t only
+      const int u = __ffs(mk) - 1;
+      sA[warp][u][lane] = fp.sub(sA[warp][u][lane], fp.mont_mul(xt, sT[warp][t][u]));
+    }
+  }
+  __syncwarp();
+  // W[s][t] = -x^{(s)}_t times R^2: mont_mul(v_s, W[s][t]) summed over s is
+  // the multiplier m_t in Montgomery form
+  for (u32 s = 0; s < 32; ++s) {
+    const u32 xm = (s < nw && (u32)lane < nw) ? sA[warp][lane][s] : 0u;
+    winW[(size_t)j * 1024 + s * 32 + lane] = fp.to_mont(fp.neg(xm));
+  }
+}
+
+// Packed pivot tails for k_sweep_win: one warp per A column copies its pivot
+// row's tail into its reserved 4-entry groups; PK: (col << 16 | val) in one
+// u32 (N < 2^16, p < 2^16), else (col, val) pairs.  Padding entries point at
+// the dummy accumulator slot N with value 0.
+template <bool PK>
+__global__ void __launch_bounds__(256) k_tail_copy(const u32* __restrict__ col, const u32* __restrict__ val, u32 N,
+                                                   const uint4* __restrict__ desc, const u32* __restrict__ winC,
+                                                   const uint2* __restrict__ winD, u32 nA,
+                                                   typename std::conditional<PK, u32, uint2>::type* __restrict__ tails) {
+  const int lane = threadIdx.x & 31;
+  const u32 a = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (a >= nA) return;
+  const uint4 d = __ldg(desc + __ldg(winC + a));
+  const uint2 g = __ldg(winD + a);
+  const u32 len = d.y - d.x, n4 = 4 * (g.y - g.x);
+  for (u32 k0 = 0; k0 < n4; k0 += 128) {
+    u32 cc[4], vv[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const u32 k = k0 + q * 32 + lane;
+      cc[q] = k < len ? __ldg(col + d.x + k) : N;
+      vv[q] = k < len ? __ldg(val + d.x + k) : 0u;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const u32 k = k0 + q * 32 + lane;
+      if (k < n4) {
+        if constexpr (PK) tails[(size_t)4 * g.x + k] = (cc[q] << 16) | vv[q];
+        else tails[(size_t)4 * g.x + k] = make_uint2(cc[q], vv[q]);
+      }
+    }
+  }
+}
+
+template <bool PK>
+__global__ void __launch_bounds__(256) k_sweep_win(Fp fp, u32 mu, const u32* __restrict__ rp,
+                                                   const u32* __restrict__ col, const u32* __restrict__ val, u32 N,
+                                                   const u32* __restrict__ rows, u32 nrows,
+                                                   const u32* __restrict__ abits_g, const u32* __restrict__ winW,
+                                                   const u32* __restrict__ winC, const uint2* __restrict__ winD,
+                                                   const uint4* __restrict__ tails,
+                                                   u32* __restrict__ Dp, u32 K, const u32* __restrict__ nonA,
+                                                   unsigned long long* __restrict__ stats) {
+  extern __shared__ __align__(16) u32 smem[];
+  constexpr int NWARP = 8;
+  constexpr int H = 2;  // 32-group spans per warp in flight
+  const u32 nwords = (N + 31) / 32;
+  u32* abits = smem;
+  u32* apre = smem + nwords;  // A columns before word w
+  u32* acc = smem + ((2 * nwords + 3) & ~3u);  // N + 1 slots (slot N absorbs padding)
+  __shared__ u32 s_act[NWARP][32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const u32 p = fp.p;
+  auto red = [&](u32 v) -> u32 {  // v mod p for v < 2^32 (Barrett, mu = floor(2^32 / p))
+    const u32 r = v - __umulhi(v, mu) * p;
+    return r >= p ? r - p : r;
+  };
+  for (u32 w = tid; w < nwords; w += blockDim.x) abits[w] = abits_g[w];
+  __syncthreads();
+  if (warp == 0) {
+    u32 run = 0;
+    for (u32 w0 = 0; w0 < nwords; w0 += 32) {
+      const u32 w = w0 + lane;
+      const u32 c = w < nwords ? __popc(abits[w]) : 0u;
+      u32 x = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const u32 y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (w < nwords) apre[w] = run + x - c;
+      run += __shfl_sync(0xffffffffu, x, 31);
+    }
+  }
+  __syncthreads();
+  unsigned long long n_piv = 0, n_tail = 0;
+  for (u32 rr = blockIdx.x; rr < nrows; rr += gridDim.x) {
+    const u32 i = rows[rr];
+    const u32 s = rp[i], e = rp[i + 1];
+    const u32 lead = col[s];
+    for (u32 c = lead + tid; c <= N; c += blockDim.x) acc[c] = 0;
+    __syncthreads();
+    for (u32 k = s + tid; k < e; k += blockDim.x) acc[col[k]] = val[k];
+    __syncthreads();
+    u32 from = lead;
+    while (true) {
+      // next nonzero A column >= from (every warp, same answer)
+      u32 c = N;
+      for (u32 c0 = from & ~31u; c0 < N; c0 += 32) {
+        const u32 cc = c0 + lane;
+        const bool hit = cc >= from && cc < N && ((abits[cc >> 5] >> (cc & 31)) & 1u) && red(acc[cc]) != 0;
+        const unsigned b = __ballot_sync(0xffffffffu, hit);
+        if (b) {
+          c = c0 + __ffs(b) - 1;
+          break;
+        }
+      }
+      if (c >= N) break;
+      const u32 j = (apre[c >> 5] + __popc(abits[c >> 5] & ((1u << (c & 31)) - 1u))) >> 5;
+      const u32 cw = __ldg(winC + j * 32 + lane);
+      const uint2 dd = __ldg(winD + j * 32 + lane);
+      const u32* W = winW + (size_t)j * 1024 + lane;
+      u32 wv[32];
+#pragma unroll
+      for (int q = 0; q < 32; ++q) wv[q] = __ldg(W + q * 32);
+      const u32 v = (cw < N && cw >= lead) ? red(acc[cw]) : 0u;
+      // multipliers of the window's 32 pivots: m = v W (lane t holds m_t)
+      u32 m = 0;
+#pragma unroll
+      for (int q = 0; q < 32; ++q) m = fp.add(m, fp.mont_mul(__shfl_sync(0xffffffffu, v, q), wv[q]));
+      // standard-domain multiplier and its Shoup constant floor(ms 2^32 / p):
+      // ms * x mod p is then x*ms - umulhi(x, msh)*p, in [0, 2p)
+      const u32 ms = fp.mont_mul(m, 1u);
+      const u32 msh = ms ? (u32)(((unsigned long long)ms << 32) / p) : 0u;
+      const u32 ng = ms ? dd.y - dd.x : 0u;
+      u32 x = ng;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const u32 y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      const u32 tot = __shfl_sync(0xffffffffu, x, 31);
+      const u32 off = x - ng;
+      const unsigned act = __ballot_sync(0xffffffffu, ng != 0);
+      if (ng) s_act[warp][__popc(act & lanemask_lt())] = lane;
+      if (warp == 0) {
+        u32 tl = ng;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) tl += __shfl_xor_sync(0xffffffffu, tl, o);
+        if (lane == 0) {
+          n_piv += __popc(act);
+          n_tail += 4ull * tl;
+        }
+      }
+      __syncwarp();
+      // apply: the active pivots' groups as one flat list [0, tot); warp w
+      // takes spans of 32 consecutive groups, lane L group a0 + L; the pivot
+      // owning a group from ballots over the pivots' offsets (no search)
+      for (u32 b0 = 0; b0 < tot; b0 += 256 * H) {
+        uint4 ev[H][PK ? 1 : 2];
+        u32 mss[H], mhs[H];
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+          const u32 a0 = b0 + 256 * h + 32 * warp;  // warp-uniform
+          const u32 a = a0 + lane;
+          mss[h] = 0;
+          mhs[h] = 0;
+          if (a0 < tot) {
+            const int k0 = __popc(__ballot_sync(0xffffffffu, ng && off <= a0)) - 1;
+            unsigned sm = __ballot_sync(0xffffffffu, ng && off > a0 && off < a0 + 32);
+            int cnt = 0;
+            while (sm) {
+              const int t = __ffs(sm) - 1;
+              sm &= sm - 1;
+              cnt += a >= __shfl_sync(0xffffffffu, off, t);
+            }
+            const int t = s_act[warp][min(k0 + cnt, 31)];
+            const u32 offt = __shfl_sync(0xffffffffu, off, t);
+            const u32 g0 = __shfl_sync(0xffffffffu, dd.x, t);
+            const u32 mt = __shfl_sync(0xffffffffu, ms, t), mh = __shfl_sync(0xffffffffu, msh, t);
+            if (a < tot) {
+              const size_t g = (size_t)g0 + (a - offt);
+              if constexpr (PK) {
+                ev[h][0] = __ldg(tails + g);
+              } else {
+                ev[h][0] = __ldg(tails + 2 * g);
+                ev[h][1] = __ldg(tails + 2 * g + 1);
+              }
+              mss[h] = mt;
+              mhs[h] = mh;
+            }
+          }
+        }
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+          if (!mss[h]) continue;
+          u32 cc[4], vv[4];
+          if constexpr (PK) {
+            const u32 w4[4] = {ev[h][0].x, ev[h][0].y, ev[h][0].z, ev[h][0].w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              cc[q] = w4[q] >> 16;
+              vv[q] = w4[q] & 0xFFFFu;
+            }
+          } else {
+            cc[0] = ev[h][0].x; vv[0] = ev[h][0].y; cc[1] = ev[h][0].z; vv[1] = ev[h][0].w;
+            cc[2] = ev[h][1].x; vv[2] = ev[h][1].y; cc[3] = ev[h][1].z; vv[3] = ev[h][1].w;
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            atomicAdd(acc + cc[q], vv[q] * mss[h] - __umulhi(vv[q], mhs[h]) * p);
+        }
+      }
+      __syncthreads();
+      from = __reduce_max_sync(0xffffffffu, cw < N ? cw : 0u) + 1;
+    }
+    u32* out = Dp + (size_t)rr * K;
+    for (u32 q = tid; q < K; q += blockDim.x) {
+      const u32 cc = nonA[q];
+      out[q] = cc >= lead ? red(acc[cc]) : 0u;
+    }
+    __syncthreads();
+  }
+  if (stats && tid == 0 && n_piv) {
+    atomicAdd(stats, n_piv);
+    atomicAdd(stats + 1, n_tail);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // E2, warp per row: one warp sweeps one C row with its own shared-memory
 // accumulator, so a pivot application needs no CTA barrier (only __syncwarp).
 // The pivot tail is loaded SWW_UNR entries per lane at a time — all loads in
@@ -909,6 +1245,130 @@ __global__ void __launch_bounds__(256) k_dense_forward_cta(Fp fp, u32* Dp, u32 R
   }
 }
 
+// E3a (shared-memory rows): one CTA per SM holds a contiguous block of D'
+// rows in shared memory for the whole elimination.  Per pivot: every CTA
+// publishes its best candidate row (min (lead, row)) to a per-CTA slot in
+// global memory and bids for it with one 64-bit atomicMin; ONE grid barrier;
+// every CTA stages the winning row from its owner's slot (L2) into shared
+// memory and updates its rows leading at that column all at once,
+// row <- a*row - b*pivot with a = the pivot's lead, b = the row's entry (a
+// nonzero scaling keeps the row space, so no inverse on the critical path),
+// tracking each row's new lead in the same pass.  Pivot rows are frozen and
+// written back to D' (the echelon basis k_dense_piv_info / k_dense_back read).
+static constexpr int DS_THREADS = 512;
+static constexpr int DS_MAXROWS = 64;
+__global__ void __launch_bounds__(DS_THREADS) k_dense_fwd_smem(Fp fp, u32* __restrict__ Dp, u32 R, u32 K, u32 rpc,
+                                                               unsigned long long* __restrict__ cand,
+                                                               u32* __restrict__ slots, u32* __restrict__ piv_of_col) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) u32 smem[];
+  constexpr int NW = DS_THREADS / 32;
+  const unsigned FULL = 0xffffffffu;
+  const u32 Kp = (K + 3) & ~3u;
+  u32* prow = smem;       // [Kp] the current pivot row
+  u32* rows = smem + Kp;  // [rpc][Kp] this CTA's rows
+  __shared__ u32 s_lead[DS_MAXROWS];
+  __shared__ uint8_t s_used[DS_MAXROWS];
+  __shared__ u32 s_red[NW][DS_MAXROWS];
+  __shared__ unsigned long long s_cand;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const u32 lo = blockIdx.x * rpc;
+  const u32 nr = lo < R ? min(rpc, R - lo) : 0u;
+  for (u32 r = 0; r < nr; ++r)
+    for (u32 q = tid; q < K; q += DS_THREADS) rows[(size_t)r * Kp + q] = Dp[(size_t)(lo + r) * K + q];
+  __syncthreads();
+  for (u32 r = 0; r < nr; ++r) {
+    u32 f = K;
+    for (u32 q = tid; q < K; q += DS_THREADS)
+      if (rows[(size_t)r * Kp + q]) {
+        f = q;
+        break;
+      }
+    f = __reduce_min_sync(FULL, f);
+    if (lane == 0) s_red[warp][r] = f;
+  }
+  __syncthreads();
+  if (tid < (int)nr) {
+    u32 m = K;
+    for (int w = 0; w < NW; ++w) m = min(m, s_red[w][tid]);
+    s_lead[tid] = m;
+    s_used[tid] = 0;
+  }
+  __syncthreads();
+  for (u32 step = 0;; ++step) {
+    if (warp == 0) {
+      unsigned long long m = ~0ull;
+      for (u32 r = lane; r < nr; r += 32)
+        if (!s_used[r] && s_lead[r] < K) m = min(m, ((unsigned long long)s_lead[r] << 32) | (lo + r));
+#pragma unroll
+      for (int o = 16; o; o >>= 1) m = min(m, __shfl_xor_sync(FULL, m, o));
+      if (lane == 0) s_cand = m;
+    }
+    __syncthreads();
+    const unsigned long long mine = s_cand;
+    if (mine != ~0ull) {
+      const u32 r = (u32)(mine & 0xFFFFFFFFull) - lo, l = (u32)(mine >> 32);
+      u32* slot = slots + (size_t)blockIdx.x * Kp;
+      for (u32 q = l + tid; q < K; q += DS_THREADS) __stcg(slot + q, rows[(size_t)r * Kp + q]);
+      __syncthreads();
+      if (tid == 0) atomicMin(cand + step, mine);
+    }
+    grid.sync();
+    const unsigned long long win = __ldcg(cand + step);
+    if (win == ~0ull) break;
+    const u32 c = (u32)(win >> 32), pr = (u32)(win & 0xFFFFFFFFull);
+    const u32 owner = pr / rpc;
+    const u32* oslot = slots + (size_t)owner * Kp;
+    for (u32 q = c + tid; q < K; q += DS_THREADS) prow[q] = __ldcg(oslot + q);
+    if (owner == blockIdx.x) {
+      for (u32 q = c + tid; q < K; q += DS_THREADS) Dp[(size_t)pr * K + q] = rows[(size_t)(pr - lo) * Kp + q];
+      if (tid == 0) {
+        s_used[pr - lo] = 1;
+        piv_of_col[c] = pr;
+      }
+    }
+    __syncthreads();
+    const u32 am = fp.to_mont(prow[c]);
+    bool any = false;
+    for (u32 r = 0; r < nr; ++r) {
+      if (s_used[r] || s_lead[r] != c) continue;
+      any = true;
+      u32* row = rows + (size_t)r * Kp;
+      const u32 bm = fp.to_mont(fp.neg(row[c]));
+      u32 f = K;
+      for (u32 q0 = c + 1 + tid; q0 < K; q0 += 4 * DS_THREADS) {
+        u32 xv[4], pv[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const u32 q = q0 + h * DS_THREADS;
+          xv[h] = q < K ? row[q] : 0u;
+          pv[h] = q < K ? prow[q] : 0u;
+        }
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const u32 q = q0 + h * DS_THREADS;
+          if (q < K) {
+            const u32 nv = fp.add(fp.mont_mul(am, xv[h]), fp.mont_mul(bm, pv[h]));
+            row[q] = nv;
+            if (nv && f == K) f = q;
+          }
+        }
+      }
+      f = __reduce_min_sync(FULL, f);
+      if (lane == 0) s_red[warp][r] = f;
+    }
+    if (any) {
+      __syncthreads();
+      if (tid < (int)nr && !s_used[tid] && s_lead[tid] == c) {
+        u32 m = K;
+        for (int w = 0; w < NW; ++w) m = min(m, s_red[w][tid]);
+        s_lead[tid] = m;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // E3a (rounds): every live row whose leading column has no pivot claims it
 // (lowest row index wins, one atomicMin per row) and computes the inverse of
 // its own lead; then every other live row is reduced by the pivot of its
@@ -1152,6 +1612,64 @@ static void launch_sweep(Ctx* c, const Fp& fp, f4b_echelon* E, const u32* rows, 
   static const char* sweep_env = getenv("F4B_SWEEP");
   static const bool cta_sweep = sweep_env && !strcmp(sweep_env, "cta");
   static const bool warp_sweep = sweep_env && !strcmp(sweep_env, "warp");
+  static const bool blk_sweep = sweep_env && !strcmp(sweep_env, "blk");
+  if (MODE == 0 && !cta_sweep && !warp_sweep && !blk_sweep && E->nA > 0) {
+    // fixed windows with precomputed block inverses (k_win_build + k_sweep_win)
+    const size_t nwords = (N + 31) / 32;
+    const size_t smem = (size_t)((2 * nwords + 3) & ~(size_t)3) * 4 + (size_t)(N + 1) * 4;
+    // lazily reduced u32 accumulator: initial value + one product in [0, 2p)
+    // per applied pivot
+    if ((unsigned long long)c->p * (2ull * (unsigned long long)E->nA + 2) < (1ull << 32) && smem <= 180 * 1024) {
+      const bool pk = N < 65535u && c->p < 65536u;
+      static bool wattr = false;
+      if (!wattr) {
+        check_cuda(cudaFuncSetAttribute(k_sweep_win<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
+                   "attr");
+        check_cuda(cudaFuncSetAttribute(k_sweep_win<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
+                   "attr");
+        wattr = true;
+      }
+      const u32 nA = (u32)E->nA, nwin = (nA + 31) / 32;
+      const size_t groups = (size_t)(E->M + 4 * (long long)nA) / 4 + 8;
+      DBuf wW, wC, wD, wT, gcur;
+      ensure(c, wW, (size_t)nwin * 1024 * sizeof(u32));
+      ensure(c, wC, (size_t)nwin * 32 * sizeof(u32));
+      ensure(c, wD, (size_t)nwin * 32 * sizeof(uint2));
+      ensure(c, wT, groups * (pk ? 16 : 32));
+      ensure(c, gcur, 16);
+      check_cuda(cudaMemsetAsync(gcur.p, 0, 4, c->stream), "memset");
+      F4B_LAUNCH(c, k_win_build, nb(nwin, WB_WARPS), 32 * WB_WARPS, 0, fp, E->col, E->val, N, E->desc.as<uint4>(),
+                 E->abits.as<u32>(), E->acols.as<u32>(), E->apos.as<u32>(), nA, nwin, wW.as<u32>(), wC.as<u32>(),
+                 wD.as<uint2>(), gcur.as<u32>());
+      if (pk)
+        F4B_LAUNCH(c, k_tail_copy<true>, nb(nA, 8), 256, 0, E->col, E->val, N, E->desc.as<uint4>(), wC.as<u32>(),
+                   wD.as<uint2>(), nA, wT.as<u32>());
+      else
+        F4B_LAUNCH(c, k_tail_copy<false>, nb(nA, 8), 256, 0, E->col, E->val, N, E->desc.as<uint4>(), wC.as<u32>(),
+                   wD.as<uint2>(), nA, wT.as<uint2>());
+      int per_sm = 0;
+      check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pk ? k_sweep_win<true> : k_sweep_win<false>,
+                                                               256, smem),
+                 "occupancy");
+      per_sm = std::max(1, per_sm);
+      const int grid = (int)std::max<long long>(1, std::min<long long>(nrows, (long long)c->num_sms * per_sm));
+      const u32 mu = (u32)((1ull << 32) / c->p);
+      if (pk)
+        F4B_LAUNCH(c, k_sweep_win<true>, grid, 256, smem, fp, mu, E->rp, E->col, E->val, N, rows, nrows,
+                   E->abits.as<u32>(), wW.as<u32>(), wC.as<u32>(), wD.as<uint2>(), wT.as<uint4>(), Dp, K,
+                   E->nonA.as<u32>(), stats);
+      else
+        F4B_LAUNCH(c, k_sweep_win<false>, grid, 256, smem, fp, mu, E->rp, E->col, E->val, N, rows, nrows,
+                   E->abits.as<u32>(), wW.as<u32>(), wC.as<u32>(), wD.as<uint2>(), wT.as<uint4>(), Dp, K,
+                   E->nonA.as<u32>(), stats);
+      release(c, wW);
+      release(c, wC);
+      release(c, wD);
+      release(c, wT);
+      release(c, gcur);
+      return;
+    }
+  }
   if (MODE == 0 && !cta_sweep && !warp_sweep) {
     // blocked sweep: lazily reduced u32 accumulator needs p * (nA + 1) < 2^32
     const size_t bitmap = (size_t)((((N + 31) / 32) + 3) & ~3u) * 4;
@@ -1303,6 +1821,31 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
     check_cuda(cudaMemsetAsync(E->stats.p, 0, 16, c->stream), "memset");
     launch_sweep<0>(c, fp, E, crows.as<u32>(), (u32)R, Dp.as<u32>(), (u32)K, nullptr, 0, nullptr, nullptr, nullptr, 0,
                     nullptr, nullptr, nullptr, err, E->stats.as<unsigned long long>());
+    static const bool dp_stats = getenv("F4B_DP_STATS") != nullptr;
+    if (dp_stats) {  // diagnostic: shape of D' after the sweep (host copy)
+      std::vector<u32> h((size_t)R * K);
+      check_cuda(cudaMemcpyAsync(h.data(), Dp.p, h.size() * 4, cudaMemcpyDeviceToHost, c->stream), "d2h");
+      check_cuda(cudaStreamSynchronize(c->stream), "sync");
+      long long nz_rows = 0, nnz = 0;
+      std::vector<int> leads;
+      for (long long i = 0; i < R; ++i) {
+        long long l = -1, cnt = 0;
+        for (long long q = 0; q < K; ++q)
+          if (h[(size_t)i * K + q]) {
+            if (l < 0) l = q;
+            ++cnt;
+          }
+        if (l >= 0) {
+          ++nz_rows;
+          leads.push_back((int)l);
+        }
+        nnz += cnt;
+      }
+      std::sort(leads.begin(), leads.end());
+      long long distinct = std::unique(leads.begin(), leads.end()) - leads.begin();
+      fprintf(stderr, "[dp] R=%lld K=%lld nonzero_rows=%lld distinct_leads=%lld density=%.3f\n", R, K, nz_rows,
+              distinct, R * K ? (double)nnz / (double)(R * K) : 0.0);
+    }
     // E3a: cooperative forward elimination
     ensure(c, used, (size_t)R + 16);
     ensure(c, pofc, (size_t)K * sizeof(u32));
@@ -1356,7 +1899,36 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
         cudaGetLastError();
       }
     }
-    // default: CTA-cooperative per-pivot kernel when every CTA's row range fits
+    // default: rows resident in shared memory (k_dense_fwd_smem) when every
+    // SM's row block fits
+    static const char* dense_env = getenv("F4B_DENSE");
+    if (!done_cluster && !dense_env) {
+      const size_t Kp = (size_t)((K + 3) & ~3ll);
+      const long long rpc = (R + c->num_sms - 1) / c->num_sms;
+      const size_t smem_ds = (size_t)(rpc + 1) * Kp * 4;
+      if (rpc <= DS_MAXROWS && smem_ds <= 200 * 1024) {
+        static bool ds_attr = false;
+        if (!ds_attr) {
+          check_cuda(cudaFuncSetAttribute(k_dense_fwd_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
+                     "attr");
+          ds_attr = true;
+        }
+        const int GD = (int)((R + rpc - 1) / rpc);
+        DBuf slots;
+        ensure(c, slots, (size_t)GD * Kp * sizeof(u32));
+        u32 rpcu = (u32)rpc;
+        u32* slotp = slots.as<u32>();
+        void* args4[] = {&fp, &dpp, &Ru, &Ku, &rpcu, &candp, &slotp, &pofcp};
+        {
+          ProfScope ps(c, "k_dense_fwd_smem");
+          check_cuda(cudaLaunchCooperativeKernel((void*)k_dense_fwd_smem, GD, DS_THREADS, args4, smem_ds, c->stream),
+                     "k_dense_fwd_smem");
+        }
+        release(c, slots);
+        done_cluster = true;
+      }
+    }
+    // CTA-cooperative per-pivot kernel when every CTA's row range fits
     // its shared row state
     static const bool dense_warp = getenv("F4B_DENSE") && !strcmp(getenv("F4B_DENSE"), "warp");
     int bpc = 0;

@@ -14,8 +14,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("report")
     ap.add_argument("--top", type=int, default=30)
+    ap.add_argument("--kernel", default="", help="kernel name regex (ncu --kernel-name regex:...)")
     args = ap.parse_args()
-    out = subprocess.run(["ncu", "-i", args.report, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+    flt = ["--kernel-name", "regex:" + args.kernel, "--launch-count", "1"] if args.kernel else []
+    out = subprocess.run(["ncu", "-i", args.report, *flt, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     lines = []  # (samples, file, line, src, stall breakdown)

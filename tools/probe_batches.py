@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--full", action="store_true")
     ap.add_argument("--brief", action="store_true", help="one short line per batch (symbolic time vs kernel time)")
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--batches", default="", help="comma-separated batch indices (overrides --top)")
     ap.add_argument("--profile-region", action="store_true",
                     help="wrap the last replay of each batch in cudaProfilerStart/Stop (ncu --profile-from-start off)")
     args = ap.parse_args()
@@ -32,6 +33,8 @@ def main():
     ring, st, batches, setup = bench.capture_workload()
     eng = Engine.for_ring(ring)
     order = sorted(range(len(batches)), key=lambda i: -batches[i]["M"])[: args.top]
+    if args.batches:
+        order = [int(x) for x in args.batches.split(",")]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     for i in order:
         b = batches[i]
