@@ -15,9 +15,10 @@
  *    the reference exception classes (pkg/src/fpgb/errors.py).
  *  - Arrays named h_* / passed as `const T*` without "device" in the comment
  *    are HOST pointers.  Device memory is owned by the context and obtained
- *    through the registered allocator (the Python host registers one backed
- *    by the PyTorch caching allocator); with a NULL allocator cudaMalloc is
- *    used.
+ *    through the registered allocator when one is given; with a NULL
+ *    allocator (the Python host's default) from a per-context stream-ordered
+ *    cudaMemPool (cudaMallocFromPoolAsync / cudaFreeAsync on the context
+ *    stream, memory retained by the pool).
  *  - All work is issued on the stream set with f4b_ctx_set_stream (default
  *    stream 0).  One context per (device, ring); calls on one context are not
  *    thread-safe.

@@ -1,8 +1,9 @@
 """ctypes binding of ``libf4b200.so`` (C ABI in ``include/f4b200.h``).
 
-PyTorch supplies device memory: the context registers an allocator callback
-that hands out ``torch.empty(..., dtype=uint8, device='cuda')`` blocks from
-the caching allocator (and drops them on free), and kernels run on
+Device memory comes from the library's own stream-ordered pool (a
+``cudaMemPool`` per context; ``F4B_TORCH_ALLOC=1`` registers an allocator
+callback that hands out ``torch.empty(..., dtype=uint8)`` blocks from the
+PyTorch caching allocator instead), and kernels run on
 ``torch.cuda.current_stream()``.  There is no CPU fallback: without the
 built library or without a CUDA device every engine call raises
 ``DeviceError``.
@@ -134,8 +135,15 @@ class Context:
         def _free(p_, _user):
             self._blocks.pop(p_, None)
 
-        self._alloc_cb = ALLOC_FN(_alloc)
-        self._free_cb = FREE_FN(_free)
+        # Default: the library's own stream-ordered memory pool (no host
+        # callback per device buffer).  F4B_TORCH_ALLOC=1 routes every device
+        # buffer through the PyTorch caching allocator instead.
+        if os.environ.get("F4B_TORCH_ALLOC"):
+            self._alloc_cb = ALLOC_FN(_alloc)
+            self._free_cb = FREE_FN(_free)
+        else:
+            self._alloc_cb = ALLOC_FN()
+            self._free_cb = FREE_FN()
         h = C.c_void_p()
         with torch.cuda.device(dev):
             code = self.lib.f4b_ctx_create(device, p, n_vars, order_code, self._alloc_cb, self._free_cb, None,

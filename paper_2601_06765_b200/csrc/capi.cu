@@ -35,6 +35,8 @@ static void* raw_alloc(Ctx* c, size_t bytes) {
   if (c->alloc) {
     p = c->alloc(bytes, c->user);
     if (!p) fail(F4B_ERR_OOM, "device allocation of " + std::to_string(bytes) + " bytes failed");
+  } else if (c->mempool) {
+    check_cuda(cudaMallocFromPoolAsync(&p, bytes, c->mempool, c->stream), "cudaMallocFromPoolAsync");
   } else {
     check_cuda(cudaMalloc(&p, bytes), "cudaMalloc");
   }
@@ -44,6 +46,7 @@ static void* raw_alloc(Ctx* c, size_t bytes) {
 static void raw_free(Ctx* c, void* p) {
   if (!p) return;
   if (c->dfree) c->dfree(p, c->user);
+  else if (c->mempool) cudaFreeAsync(p, c->stream);
   else cudaFree(p);
 }
 
@@ -281,6 +284,15 @@ int f4b_ctx_create(int device, uint32_t p, int n_vars, int order, f4b_alloc_fn a
     c->pprime = (uint32_t)(0u - x);
     c->r2 = (uint32_t)(((unsigned __int128)1 << 64) % p);
     check_cuda(cudaMallocHost((void**)&c->h_stat, 4096), "pinned");
+    if (!alloc) {
+      cudaMemPoolProps props = {};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = device;
+      check_cuda(cudaMemPoolCreate(&c->mempool, &props), "cudaMemPoolCreate");
+      uint64_t keep = UINT64_MAX;
+      check_cuda(cudaMemPoolSetAttribute(c->mempool, cudaMemPoolAttrReleaseThreshold, &keep), "mempool attr");
+    }
     c->basis.h_off.push_back(0);
   } catch (const Error& e) {
     delete h;
@@ -305,6 +317,10 @@ int f4b_ctx_destroy(f4b_ctx* h) {
   if (c->h_stage) cudaFreeHost(c->h_stage);
   if (c->h_stat) cudaFreeHost(c->h_stat);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+  if (c->mempool) {
+    cudaStreamSynchronize(c->stream);
+    cudaMemPoolDestroy(c->mempool);
+  }
   delete h;
   return F4B_OK;
 }

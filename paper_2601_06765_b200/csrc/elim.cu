@@ -62,6 +62,7 @@ struct f4b_echelon {
   f4b::DBuf d_off, d_len;        // u32 [rankD] (nonpivot rows, ascending lead)
   f4b::DBuf cursor;              // u64
   f4b::DBuf stats;               // u64 [2] sweep work counters
+  f4b::DBuf rdev;                // u32 rank(D') written by k_dense_post
   unsigned long long sweep_pivots = 0, sweep_tail_nnz = 0;
   size_t pool_cap = 0;
   long long pivot_nnz = 0, nonpivot_nnz = 0;
@@ -1306,9 +1307,12 @@ __global__ void __launch_bounds__(DS_THREADS) k_dense_fwd_smem(Fp fp, u32* __res
     }
     __syncthreads();
     const unsigned long long mine = s_cand;
+    // slots are double-buffered by step parity: a CTA publishes step s+1's
+    // candidate while slower CTAs may still copy step s's pivot row
+    const u32 par = step & 1;
     if (mine != ~0ull) {
       const u32 r = (u32)(mine & 0xFFFFFFFFull) - lo, l = (u32)(mine >> 32);
-      u32* slot = slots + (size_t)blockIdx.x * Kp;
+      u32* slot = slots + ((size_t)par * gridDim.x + blockIdx.x) * Kp;
       for (u32 q = l + tid; q < K; q += DS_THREADS) __stcg(slot + q, rows[(size_t)r * Kp + q]);
       __syncthreads();
       if (tid == 0) atomicMin(cand + step, mine);
@@ -1318,7 +1322,7 @@ __global__ void __launch_bounds__(DS_THREADS) k_dense_fwd_smem(Fp fp, u32* __res
     if (win == ~0ull) break;
     const u32 c = (u32)(win >> 32), pr = (u32)(win & 0xFFFFFFFFull);
     const u32 owner = pr / rpc;
-    const u32* oslot = slots + (size_t)owner * Kp;
+    const u32* oslot = slots + ((size_t)par * gridDim.x + owner) * Kp;
     for (u32 q = c + tid; q < K; q += DS_THREADS) prow[q] = __ldcg(oslot + q);
     if (owner == blockIdx.x) {
       for (u32 q = c + tid; q < K; q += DS_THREADS) Dp[(size_t)pr * K + q] = rows[(size_t)(pr - lo) * Kp + q];
@@ -1499,10 +1503,11 @@ __global__ void __launch_bounds__(1024) k_dense_forward_cluster(Fp fp, u32* Dp, 
 // E3b: back-substitution -> RREF(D') rows (dense), one CTA per pivot.
 __global__ void __launch_bounds__(SW_THREADS) k_dense_back(Fp fp, const u32* __restrict__ Dp, u32 K,
                                                             const u32* __restrict__ dpiv, const u32* __restrict__ dprow,
-                                                            u32 rankD, const u32* __restrict__ pbits_g,
+                                                            const u32* __restrict__ rankD_p, const u32* __restrict__ pbits_g,
                                                             const u32* __restrict__ pinv, const u32* __restrict__ prow_of,
                                                             u32* __restrict__ Rd, u32* __restrict__ gacc) {
   extern __shared__ u32 smem[];
+  const u32 rankD = *rankD_p;
   const u32 nwords = (K + 31) / 32;
   u32* pbits = smem;
   u32* acc = gacc ? gacc + (size_t)blockIdx.x * K : smem + nwords;
@@ -1569,14 +1574,43 @@ __global__ void k_dense_piv_info(Fp fp, const u32* __restrict__ Dp, u32 K, const
   }
 }
 
+// E3b: pivots of D' in one CTA: pivot flags, their exclusive scan, the pivot
+// lists (column, row), the inverse leads, the pivot bitmap and rank(D') —
+// all on the device, no host read before the back-substitution.
+__global__ void __launch_bounds__(1024) k_dense_post(Fp fp, const u32* __restrict__ Dp, u32 K,
+                                                     const u32* __restrict__ pofc, u32* __restrict__ pinv,
+                                                     u32* __restrict__ dpiv, u32* __restrict__ dprow,
+                                                     u32* __restrict__ pbits, u32* __restrict__ rankD_out) {
+  __shared__ u32 red[33];
+  u32 base = 0;
+  for (u32 q0 = 0; q0 < K; q0 += blockDim.x) {
+    const u32 q = q0 + threadIdx.x;
+    const u32 pr = q < K ? pofc[q] : NONE;
+    const bool f = pr != NONE;
+    if (q < K) pinv[q] = f ? fp.inv(Dp[(size_t)pr * K + q]) : 0u;
+    const unsigned bm = __ballot_sync(0xffffffffu, f);
+    if ((threadIdx.x & 31) == 0 && q < K) pbits[q >> 5] = bm;
+    u32 tot;
+    const u32 pre = block_scan_flag(f ? 1u : 0u, red, &tot);
+    if (f) {
+      dpiv[base + pre] = q;
+      dprow[base + pre] = pr;
+    }
+    base += tot;
+  }
+  if (threadIdx.x == 0) *rankD_out = base;
+}
+
 // E3c: emit RREF(D') rows as sparse rows over the global columns
-__global__ void __launch_bounds__(SW_THREADS) k_emit_dense(const u32* __restrict__ Rd, u32 K, u32 rankD,
+__global__ void __launch_bounds__(SW_THREADS) k_emit_dense(const u32* __restrict__ Rd, u32 K,
+                                                            const u32* __restrict__ rankD_p,
                                                             const u32* __restrict__ dpiv, const u32* __restrict__ nonA,
                                                             u32* __restrict__ pcol, u32* __restrict__ pval, size_t cap,
                                                             unsigned long long* cursor, u32* s_off, u32* s_len,
                                                             u32* err) {
   __shared__ u32 red[33];
   __shared__ u32 sh[2];
+  const u32 rankD = *rankD_p;
   for (u32 k = blockIdx.x; k < rankD; k += gridDim.x) {
     emit_row(Rd + (size_t)k * K, dpiv[k], K, nonA, pcol, pval, cap, cursor, s_off + k, s_len + k, err, red, sh);
     __syncthreads();
@@ -1853,7 +1887,7 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
     ensure(c, lead, (size_t)R * sizeof(u32));
     check_cuda(cudaMemsetAsync(cand.p, 0xFF, (std::min(R, K) + 2) * sizeof(unsigned long long), c->stream), "memset");
     check_cuda(cudaMemsetAsync(used.p, 0, R, c->stream), "memset");
-    F4B_LAUNCH(c, k_fill_u32, nb(K, 256), 256, 0, pofc.as<u32>(), K, NONE);
+    check_cuda(cudaMemsetAsync(pofc.p, 0xFF, (size_t)K * sizeof(u32), c->stream), "memset");
     int bps = 0;
     check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_dense_forward, 256, 0), "occupancy");
     int G = (int)std::min<long long>((long long)c->num_sms * std::max(1, std::min(bps, 2)), std::max<long long>(R, 1));
@@ -1915,7 +1949,7 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
         }
         const int GD = (int)((R + rpc - 1) / rpc);
         DBuf slots;
-        ensure(c, slots, (size_t)GD * Kp * sizeof(u32));
+        ensure(c, slots, (size_t)2 * GD * Kp * sizeof(u32));
         u32 rpcu = (u32)rpc;
         u32* slotp = slots.as<u32>();
         void* args4[] = {&fp, &dpp, &Ru, &Ku, &rpcu, &candp, &slotp, &pofcp};
@@ -1975,24 +2009,18 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
       ProfScope ps(c, "k_dense_forward");
       check_cuda(cudaLaunchCooperativeKernel((void*)k_dense_forward, G, 256, args, 0, c->stream), "k_dense_forward");
     }
-    // pivots of D'
-    ensure(c, c->flags, (size_t)K + 32);
-    ensure(c, c->tmp_u32a, (size_t)(K + 2) * sizeof(u32));
-    F4B_LAUNCH(c, k_dense_pivots, nb(K, 256), 256, 0, pofc.as<u32>(), (u32)K, c->flags.as<uint8_t>());
-    exclusive_scan_flags(c, c->flags.as<uint8_t>(), c->tmp_u32a.as<u32>(), K);
-    E->rankD = read_u32(c, c->tmp_u32a.as<u32>() + K);
+    // pivots of D' (k_dense_post: one CTA, rank(D') stays on the device)
+    const long long rmax = std::max<long long>(1, std::min(R, K));
     DBuf pinv, dprow, pbits;
     ensure(c, pinv, (size_t)K * sizeof(u32));
-    ensure(c, E->dpiv, (size_t)std::max<long long>(E->rankD, 1) * sizeof(u32));
-    ensure(c, dprow, (size_t)std::max<long long>(E->rankD, 1) * sizeof(u32));
+    ensure(c, E->dpiv, (size_t)rmax * sizeof(u32));
+    ensure(c, dprow, (size_t)rmax * sizeof(u32));
     ensure(c, pbits, (size_t)((K + 31) / 32 + 1) * sizeof(u32));
-    F4B_LAUNCH(c, k_dense_piv_info, nb(K, 256), 256, 0, fp, Dp.as<u32>(), (u32)K, pofc.as<u32>(), pinv.as<u32>(),
-                                                         c->flags.as<uint8_t>(), c->tmp_u32a.as<u32>(), E->dpiv.as<u32>(),
-                                                         dprow.as<u32>());
-    F4B_LAUNCH(c, k_bits, nb((K + 31) / 32, 256), 256, 0, c->flags.as<uint8_t>(), K, pbits.as<u32>());
-    check_cuda(cudaGetLastError(), "k_dense_piv_info");
-    if (E->rankD) {
-      ensure(c, E->Rd, (size_t)E->rankD * K * sizeof(u32));
+    ensure(c, E->rdev, 16);
+    F4B_LAUNCH(c, k_dense_post, 1, 1024, 0, fp, Dp.as<u32>(), (u32)K, pofc.as<u32>(), pinv.as<u32>(),
+               E->dpiv.as<u32>(), dprow.as<u32>(), pbits.as<u32>(), E->rdev.as<u32>());
+    ensure(c, E->Rd, (size_t)rmax * K * sizeof(u32));
+    {
       size_t smem2 = (size_t)((K + 31) / 32) * 4 + (size_t)K * 4;
       DBuf gacc2;
       const bool gl2 = smem2 > 200 * 1024;  // accumulator in HBM for very wide blocks
@@ -2003,16 +2031,19 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
                    "attr");
         attr1 = true;
       }
-      int g2 = sweep_grid(c, smem2, E->rankD);
+      int g2 = sweep_grid(c, smem2, rmax);
       if (gl2) ensure(c, gacc2, (size_t)g2 * K * sizeof(u32));
       F4B_LAUNCH(c, k_dense_back, g2, SW_THREADS, smem2, fp, Dp.as<u32>(), (u32)K, E->dpiv.as<u32>(), dprow.as<u32>(),
-                 (u32)E->rankD, pbits.as<u32>(), pinv.as<u32>(), pofc.as<u32>(), E->Rd.as<u32>(),
+                 E->rdev.as<u32>(), pbits.as<u32>(), pinv.as<u32>(), pofc.as<u32>(), E->Rd.as<u32>(),
                  gl2 ? gacc2.as<u32>() : nullptr);
       release(c, gacc2);
     }
     release(c, pinv);
     release(c, dprow);
     release(c, pbits);
+  } else {
+    ensure(c, E->rdev, 16);
+    check_cuda(cudaMemsetAsync(E->rdev.p, 0, 4, c->stream), "memset");
   }
   release(c, Dp);
   release(c, cand);
@@ -2020,38 +2051,48 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
   release(c, pofc);
   release(c, lead);
   release(c, crows);
-  // E3c: emit the nonpivot rows (RREF(D'))
-  const long long rankD = E->rankD;
-  ensure(c, E->d_off, (size_t)std::max<long long>(rankD, 1) * sizeof(u32));
-  ensure(c, E->d_len, (size_t)std::max<long long>(rankD, 1) * sizeof(u32));
+  // E3c: emit the nonpivot rows (RREF(D')); sizes from rank(D') <= min(R, K)
+  // so nothing waits for the host; one read-back of (rank, pool use, error
+  // flag, sweep counters) at the end
+  const long long rmax = (R > 0 && K > 0) ? std::max<long long>(1, std::min(R, K)) : 1;
+  ensure(c, E->d_off, (size_t)rmax * sizeof(u32));
+  ensure(c, E->d_len, (size_t)rmax * sizeof(u32));
   ensure(c, E->cursor, 16);
   if (E->pool_cap == 0) {
-    E->pool_cap = (size_t)std::max<long long>(rankD * K + 2 * (long long)E->nA * 64 + 4096, 1 << 20);
+    E->pool_cap = (size_t)std::max<long long>(((R > 0 && K > 0) ? rmax * K : 0) + 2 * (long long)E->nA * 64 + 4096,
+                                              1 << 20);
   }
+  struct Tail {
+    unsigned long long used_pool, st[2];
+    u32 rankD, err;
+  };
+  Tail* ht = reinterpret_cast<Tail*>(c->h_stat);
   for (int attempt = 0; attempt < 8; ++attempt) {
     ensure(c, E->pool_col, E->pool_cap * sizeof(u32));
     ensure(c, E->pool_val, E->pool_cap * sizeof(u32));
     check_cuda(cudaMemsetAsync(E->cursor.p, 0, 8, c->stream), "memset");
     check_cuda(cudaMemsetAsync(err, 0, 4, c->stream), "memset");
-    if (rankD) {
-      int g = (int)std::min<long long>(rankD, (long long)c->num_sms * 4);
-      F4B_LAUNCH(c, k_emit_dense, g, SW_THREADS, 0, E->Rd.as<u32>(), (u32)K, (u32)rankD, E->dpiv.as<u32>(),
-                                                     E->nonA.as<u32>(), E->pool_col.as<u32>(), E->pool_val.as<u32>(),
-                                                     E->pool_cap, E->cursor.as<unsigned long long>(), E->d_off.as<u32>(),
-                                                     E->d_len.as<u32>(), err);
+    if (R > 0 && K > 0) {
+      int g = (int)std::min<long long>(rmax, (long long)c->num_sms * 4);
+      F4B_LAUNCH(c, k_emit_dense, g, SW_THREADS, 0, E->Rd.as<u32>(), (u32)K, E->rdev.as<u32>(), E->dpiv.as<u32>(),
+                 E->nonA.as<u32>(), E->pool_col.as<u32>(), E->pool_val.as<u32>(), E->pool_cap,
+                 E->cursor.as<unsigned long long>(), E->d_off.as<u32>(), E->d_len.as<u32>(), err);
       check_cuda(cudaGetLastError(), "k_emit_dense");
     }
-    u32 e = read_u32(c, err);
-    if (!(e & DEVERR_CAPACITY)) break;
+    ht->st[0] = ht->st[1] = 0;
+    check_cuda(cudaMemcpyAsync(&ht->used_pool, E->cursor.p, 8, cudaMemcpyDeviceToHost, c->stream), "d2h");
+    if (E->stats.p) check_cuda(cudaMemcpyAsync(ht->st, E->stats.p, 16, cudaMemcpyDeviceToHost, c->stream), "d2h");
+    check_cuda(cudaMemcpyAsync(&ht->rankD, E->rdev.p, 4, cudaMemcpyDeviceToHost, c->stream), "d2h");
+    check_cuda(cudaMemcpyAsync(&ht->err, err, 4, cudaMemcpyDeviceToHost, c->stream), "d2h");
+    check_cuda(cudaStreamSynchronize(c->stream), "sync");
+    if (!(ht->err & DEVERR_CAPACITY)) break;
     E->pool_cap *= 2;
   }
-  unsigned long long used_pool = 0, st2[2] = {0, 0};
-  check_cuda(cudaMemcpyAsync(&used_pool, E->cursor.p, 8, cudaMemcpyDeviceToHost, c->stream), "d2h");
-  if (E->stats.p) check_cuda(cudaMemcpyAsync(st2, E->stats.p, 16, cudaMemcpyDeviceToHost, c->stream), "d2h");
-  check_cuda(cudaStreamSynchronize(c->stream), "sync");
-  E->sweep_pivots = st2[0];
-  E->sweep_tail_nnz = st2[1];
-  E->nonpivot_nnz = (long long)used_pool;
+  E->rankD = ht->rankD;
+  const long long rankD = E->rankD;
+  E->sweep_pivots = ht->st[0];
+  E->sweep_tail_nnz = ht->st[1];
+  E->nonpivot_nnz = (long long)ht->used_pool;
   check_cuda(cudaEventRecord(ev1, c->stream), "event");
   check_cuda(cudaEventSynchronize(ev1), "event sync");
   float ms = 0;

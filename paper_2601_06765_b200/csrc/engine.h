@@ -71,6 +71,10 @@ struct Ctx {
   f4b_alloc_fn alloc = nullptr;
   f4b_free_fn dfree = nullptr;
   void* user = nullptr;
+  // without a registered allocator: a per-context stream-ordered pool
+  // (cudaMallocFromPoolAsync, memory retained by the pool: no device
+  // synchronisation and no host callback per buffer)
+  cudaMemPool_t mempool = nullptr;
   cudaStream_t stream = 0;
   int num_sms = 148;
   std::string last_error;
