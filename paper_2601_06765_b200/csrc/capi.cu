@@ -316,6 +316,7 @@ int f4b_ctx_destroy(f4b_ctx* h) {
   pool_flush(c);
   if (c->h_stage) cudaFreeHost(c->h_stage);
   if (c->h_stat) cudaFreeHost(c->h_stat);
+  if (c->h_app) cudaFreeHost(c->h_app);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   if (c->mempool) {
     cudaStreamSynchronize(c->stream);
@@ -532,36 +533,50 @@ int f4b_basis_append_wide(f4b_ctx* h, int64_t n_polys, const int64_t* lengths, c
   int64_t* d_l = reinterpret_cast<int64_t*>(rp + b_e + b_c);
   long long* d_p = reinterpret_cast<long long*>(rp + b_e + b_c + b_l);
   uint32_t* d_bad = reinterpret_cast<uint32_t*>(rp + b_e + b_c + b_l + b_p);
+  // page-locked staging: [lengths | prefix | tail offset] up, [LM | max exps | flag] down
+  const size_t np1 = (size_t)std::max<long long>(n_polys, 1);
+  const size_t o_len = 0, o_pre = o_len + np1 * 8, o_tail = o_pre + (size_t)(n_polys + 1) * 8,
+               o_lm = o_tail + 16, o_mx = o_lm + ((np1 * n * 2 + 15) & ~(size_t)15),
+               o_bad = o_mx + ((np1 * n * 2 + 15) & ~(size_t)15), app_bytes = o_bad + 16;
+  if (c->h_app_cap < app_bytes) {
+    if (c->h_app) cudaFreeHost(c->h_app);
+    c->h_app = nullptr;
+    c->h_app_cap = 0;
+    const size_t cap = std::max<size_t>(app_bytes + app_bytes / 2, 1 << 16);
+    check_cuda(cudaHostAlloc(&c->h_app, cap, cudaHostAllocDefault), "cudaHostAlloc app");
+    c->h_app_cap = cap;
+  }
+  unsigned char* ha = static_cast<unsigned char*>(c->h_app);
+  if (n_polys) {
+    memcpy(ha + o_len, lengths, (size_t)n_polys * 8);
+    memcpy(ha + o_pre, pre.data(), (size_t)(n_polys + 1) * 8);
+  }
+  *reinterpret_cast<u32*>(ha + o_tail) = (u32)T1;  // the basis end offset off[P1]
   check_cuda(cudaMemsetAsync(d_bad, 0, 4, c->stream), "memset");
   if (T) {
     check_cuda(cudaMemcpyAsync(d_e, exps, b_e, cudaMemcpyHostToDevice, c->stream), "h2d exps");
     check_cuda(cudaMemcpyAsync(d_c, coeffs, b_c, cudaMemcpyHostToDevice, c->stream), "h2d coeffs");
   }
-  if (n_polys) {
-    check_cuda(cudaMemcpyAsync(d_l, lengths, (size_t)n_polys * 8, cudaMemcpyHostToDevice, c->stream), "h2d lens");
-    check_cuda(cudaMemcpyAsync(d_p, pre.data(), b_p, cudaMemcpyHostToDevice, c->stream), "h2d pre");
-  }
+  if (n_polys)
+    check_cuda(cudaMemcpyAsync(d_l, ha + o_len, o_tail - o_len, cudaMemcpyHostToDevice, c->stream), "h2d lens+pre");
   if (T) {
     const int g = (int)std::min<long long>((T + 255) / 256, (long long)c->num_sms * 8);
     F4B_LAUNCH(c, k_narrow_terms, g, 256, 0, d_e, d_c, T, n, c->p, B.exps.as<u16>() + T0 * n, B.coeff.as<u32>() + T0,
                d_bad);
   }
-  std::vector<uint16_t> hlm((size_t)std::max<long long>(n_polys, 1) * n), hmx((size_t)std::max<long long>(n_polys, 1) * n);
   if (n_polys) {
     F4B_LAUNCH(c, k_poly_meta, (int)((n_polys * 32 + 255) / 256), 256, 0, B.exps.as<u16>() + T0 * n, d_l, n_polys, T0,
                n, B.off.as<u32>() + P0, B.len.as<u32>() + P0, B.lmexp.as<u16>() + P0 * n,
                B.maxe.as<u16>() + P0 * n, d_p);
-    check_cuda(cudaMemcpyAsync(hlm.data(), B.lmexp.as<u16>() + P0 * n, (size_t)n_polys * n * 2, cudaMemcpyDeviceToHost,
+    check_cuda(cudaMemcpyAsync(ha + o_lm, B.lmexp.as<u16>() + P0 * n, (size_t)n_polys * n * 2, cudaMemcpyDeviceToHost,
                                c->stream), "d2h lm");
-    check_cuda(cudaMemcpyAsync(hmx.data(), B.maxe.as<u16>() + P0 * n, (size_t)n_polys * n * 2, cudaMemcpyDeviceToHost,
+    check_cuda(cudaMemcpyAsync(ha + o_mx, B.maxe.as<u16>() + P0 * n, (size_t)n_polys * n * 2, cudaMemcpyDeviceToHost,
                                c->stream), "d2h maxe");
   }
-  // the basis end offset (off[P1]) for kernels reading off[i + 1]
-  const u32 tail_off = (u32)T1;
-  check_cuda(cudaMemcpyAsync(B.off.as<u32>() + P1, &tail_off, 4, cudaMemcpyHostToDevice, c->stream), "h2d off");
-  uint32_t bad = 0;
-  check_cuda(cudaMemcpyAsync(&bad, d_bad, 4, cudaMemcpyDeviceToHost, c->stream), "d2h");
+  check_cuda(cudaMemcpyAsync(B.off.as<u32>() + P1, ha + o_tail, 4, cudaMemcpyHostToDevice, c->stream), "h2d off");
+  check_cuda(cudaMemcpyAsync(ha + o_bad, d_bad, 4, cudaMemcpyDeviceToHost, c->stream), "d2h");
   check_cuda(cudaStreamSynchronize(c->stream), "sync");
+  const uint32_t bad = *reinterpret_cast<u32*>(ha + o_bad);
   release(c, raw);
   if (bad & 1u) fail(F4B_ERR_LANE_OVERFLOW, "exponent does not fit a 16-bit lane");
   if (bad & 2u) fail(F4B_ERR_PROPERTY, "basis coefficient outside [1, p)");
@@ -569,8 +584,10 @@ int f4b_basis_append_wide(f4b_ctx* h, int64_t n_polys, const int64_t* lengths, c
     B.h_len.push_back(lengths[i]);
     B.h_off.push_back(B.h_off.back() + lengths[i]);
   }
-  B.h_lm.insert(B.h_lm.end(), hlm.begin(), hlm.begin() + (size_t)n_polys * n);
-  B.h_maxe.insert(B.h_maxe.end(), hmx.begin(), hmx.begin() + (size_t)n_polys * n);
+  const uint16_t* hlm = reinterpret_cast<const uint16_t*>(ha + o_lm);
+  const uint16_t* hmx = reinterpret_cast<const uint16_t*>(ha + o_mx);
+  B.h_lm.insert(B.h_lm.end(), hlm, hlm + (size_t)n_polys * n);
+  B.h_maxe.insert(B.h_maxe.end(), hmx, hmx + (size_t)n_polys * n);
   B.n_terms = T1;
   B.n_polys = (int)P1;
   API_END

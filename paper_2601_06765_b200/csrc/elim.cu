@@ -1574,6 +1574,264 @@ __global__ void k_dense_piv_info(Fp fp, const u32* __restrict__ Dp, u32 K, const
   }
 }
 
+// ---------------------------------------------------------------------------
+// E3 (chunked RREF): RREF(D') with the basis kept fully reduced at all times.
+//
+// A row is reduced by a basis in reduced echelon form in ONE step: its
+// coefficients are its own entries at the basis' pivot columns
+// (x <- x - sum_j x[piv_j] B_j), so that step is a parallel product, not a
+// pivot-by-pivot chain.  Rows are taken from a queue in chunks of CH:
+//   A  (all CTAs) reduce the chunk's rows by the basis, one CTA per row
+//   B  (CTA 0)    RREF of the ≤ CH residual rows in shared memory (one warp
+//                 per row; the only sequential pivot loop left); the new
+//                 rows are appended to the basis
+//   C  (all CTAs) the old basis rows reduced by the new rows (RREF again)
+// A chunk that adds no pivot switches to a bulk step: every remaining row is
+// reduced at once and only the nonzero residuals stay queued (the rank of D'
+// concentrates in its first rows; a few late pivots come back through the
+// compacted queue).  RREF is unique, so the rows equal the reference's.  At
+// the end the basis is emitted in ascending pivot order (Rd, dpiv, rank).
+// ---------------------------------------------------------------------------
+struct RrefState {
+  u32 rho, rho_old, nnew, qh, qn, mode, done, pad;
+};
+static constexpr int RR_THREADS = 1024;
+static constexpr int RR_MAXCH = 32;
+template <bool SMALLP>
+__global__ void __launch_bounds__(RR_THREADS, 1) k_dense_rref(Fp fp, u32* __restrict__ Dp, u32 R, u32 K, u32 CH,
+                                                           u32* __restrict__ Bm, u32* __restrict__ bpiv,
+                                                           u32* __restrict__ queue, RrefState* __restrict__ st,
+                                                           u32* __restrict__ Rd, u32* __restrict__ dpiv,
+                                                           u32* __restrict__ rank_out, u32* __restrict__ colpiv) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) u32 smem[];
+  const unsigned FULL = 0xffffffffu;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const u32 G = gridDim.x;
+  const u32 p = fp.p;
+  __shared__ u32 s_nz, s_piv, s_cnt, s_lead[RR_MAXCH], s_used[RR_MAXCH], s_npiv[RR_MAXCH], s_nrow[RR_MAXCH];
+  __shared__ u32 red[33];
+  // x <- x - sum_{j<nb} x[piv(j)] * Brow(j), over all K columns, one CTA;
+  // coefficients gathered into shared memory first (nonzero ones only)
+  u32* s_cj = smem;             // [K] coefficient values (compacted)
+  u32* s_jj = smem + K;         // [K] their basis row indices
+  auto reduce_row = [&](u32* x, u32 j0, u32 nb) {
+    if (tid == 0) s_nz = 0;
+    __syncthreads();
+    for (u32 j = tid; j < nb; j += blockDim.x) {
+      const u32 v = __ldcg(x + __ldcg(bpiv + j0 + j));
+      if (v) {
+        const u32 s = atomicAdd(&s_nz, 1u);
+        s_cj[s] = SMALLP ? v : fp.to_mont(v);
+        s_jj[s] = j0 + j;
+      }
+    }
+    __syncthreads();
+    const u32 nz = s_nz;
+    if (nz) {
+      for (u32 q = tid; q < K; q += blockDim.x) {
+        if (SMALLP) {
+          unsigned long long acc = 0;
+          u32 t = 0;
+          for (; t + 4 <= nz; t += 4) {
+            acc += (unsigned long long)s_cj[t] * __ldcg(Bm + (size_t)s_jj[t] * K + q);
+            acc += (unsigned long long)s_cj[t + 1] * __ldcg(Bm + (size_t)s_jj[t + 1] * K + q);
+            acc += (unsigned long long)s_cj[t + 2] * __ldcg(Bm + (size_t)s_jj[t + 2] * K + q);
+            acc += (unsigned long long)s_cj[t + 3] * __ldcg(Bm + (size_t)s_jj[t + 3] * K + q);
+          }
+          for (; t < nz; ++t) acc += (unsigned long long)s_cj[t] * __ldcg(Bm + (size_t)s_jj[t] * K + q);
+          const u32 a = (u32)(acc % p);
+          x[q] = fp.sub(__ldcg(x + q), a);
+        } else {
+          u32 a = 0;
+          for (u32 t = 0; t < nz; ++t) a = fp.add(a, fp.mont_mul(s_cj[t], __ldcg(Bm + (size_t)s_jj[t] * K + q)));
+          x[q] = fp.sub(__ldcg(x + q), a);
+        }
+      }
+    }
+    __syncthreads();
+  };
+  if (blockIdx.x == 0 && tid == 0) {
+    st->rho = st->rho_old = st->nnew = 0;
+    st->qh = 0;
+    st->qn = R;
+    st->mode = 0;
+    st->done = 0;
+  }
+  for (u32 i = blockIdx.x * blockDim.x + tid; i < R; i += G * blockDim.x) queue[i] = i;
+  grid.sync();
+  while (true) {
+    const u32 qh = __ldcg(&st->qh), qn = __ldcg(&st->qn), rho = __ldcg(&st->rho), mode = __ldcg(&st->mode);
+    if (qh >= qn) break;
+    const u32 cnt = mode ? qn - qh : min(CH, qn - qh);
+    // A: reduce the taken rows by the basis
+    if (rho)
+      for (u32 k = blockIdx.x; k < cnt; k += G) reduce_row(Dp + (size_t)__ldcg(queue + qh + k) * K, 0, rho);
+    grid.sync();
+    if (mode) {
+      // bulk step: keep the nonzero residuals queued (CTA 0, in order)
+      if (blockIdx.x == 0) {
+        u32 outn = 0;
+        for (u32 k0 = 0; k0 < cnt; k0 += blockDim.x / 32) {
+          const u32 k = k0 + warp;
+          bool nzr = false;
+          u32 row = 0;
+          if (k < cnt) {
+            row = __ldcg(queue + qh + k);
+            const u32* x = Dp + (size_t)row * K;
+            bool any = false;
+            for (u32 b0 = 0; b0 < K && !any; b0 += 32) any = __any_sync(FULL, b0 + lane < K && __ldcg(x + b0 + lane) != 0);
+            nzr = any;
+          }
+          // order-preserving compaction of the warps' rows
+          if (lane == 0) s_used[warp] = nzr ? 1u : 0u;
+          __syncthreads();
+          u32 pre = 0, tot = 0;
+          for (u32 w = 0; w < blockDim.x / 32; ++w) {
+            if (w < (u32)warp) pre += s_used[w];
+            tot += s_used[w];
+          }
+          __syncthreads();
+          if (lane == 0 && nzr) queue[outn + pre] = row;  // outn + pre <= qh + k: never ahead of a pending read
+          outn += tot;
+          __syncthreads();
+        }
+        if (tid == 0) {
+          st->qh = 0;
+          st->qn = outn;
+          st->mode = 0;
+        }
+      }
+      grid.sync();
+      continue;
+    }
+    // B: RREF of the chunk's residual rows in shared memory (CTA 0)
+    if (blockIdx.x == 0) {
+      u32* X = smem;  // [CH][K]
+      for (u32 w = 0; w < cnt; ++w) {
+        const u32* x = Dp + (size_t)__ldcg(queue + qh + w) * K;
+        for (u32 q = tid; q < K; q += blockDim.x) X[(size_t)w * K + q] = __ldcg(x + q);
+      }
+      __syncthreads();
+      if ((u32)warp < cnt) {
+        const u32* x = X + (size_t)warp * K;
+        u32 l = K;
+        for (u32 b0 = 0; b0 < K; b0 += 32) {
+          const unsigned m = __ballot_sync(FULL, b0 + lane < K && x[b0 + lane] != 0);
+          if (m) {
+            l = b0 + __ffs(m) - 1;
+            break;
+          }
+        }
+        if (lane == 0) {
+          s_lead[warp] = l;
+          s_used[warp] = 0;
+        }
+      }
+      if (tid == 0) s_cnt = 0;
+      __syncthreads();
+      while (true) {
+        if (warp == 0) {
+          unsigned long long m = ~0ull;
+          if ((u32)lane < cnt && !s_used[lane] && s_lead[lane] < K)
+            m = ((unsigned long long)s_lead[lane] << 32) | (u32)lane;
+#pragma unroll
+          for (int o = 16; o; o >>= 1) m = min(m, __shfl_xor_sync(FULL, m, o));
+          if (lane == 0) s_piv = m == ~0ull ? NONE : (u32)(m & 0xFFFFFFFFull);
+        }
+        __syncthreads();
+        const u32 pw = s_piv;
+        if (pw == NONE) break;
+        const u32 c = s_lead[pw];
+        u32* prw = X + (size_t)pw * K;
+        if (warp == (int)pw) {
+          const u32 inv = fp.to_mont(fp.inv(prw[c]));
+          for (u32 q = c + lane; q < K; q += 32) prw[q] = fp.mont_mul(prw[q], inv);
+          if (lane == 0) {
+            s_used[pw] = 1;
+            s_npiv[s_cnt] = c;
+            s_nrow[s_cnt] = pw;
+            s_cnt = s_cnt + 1;
+          }
+        }
+        __syncthreads();
+        if ((u32)warp < cnt && warp != (int)pw) {
+          u32* x = X + (size_t)warp * K;
+          const u32 f = x[c];
+          if (f) {
+            const u32 fm = fp.to_mont(p - f);
+            for (u32 q = c + 1 + lane; q < K; q += 32) x[q] = fp.add(x[q], fp.mont_mul(fm, prw[q]));
+            __syncwarp();
+            if (lane == 0) x[c] = 0;
+            __syncwarp();
+            if (!s_used[warp]) {
+              u32 l = K;
+              for (u32 b0 = (c + 1) & ~31u; b0 < K; b0 += 32) {
+                const u32 q = b0 + lane;
+                const unsigned m = __ballot_sync(FULL, q > c && q < K && x[q] != 0);
+                if (m) {
+                  l = b0 + __ffs(m) - 1;
+                  break;
+                }
+              }
+              if (lane == 0) s_lead[warp] = l;
+            }
+          }
+        }
+        __syncthreads();
+      }
+      const u32 nn = s_cnt;
+      for (u32 k = 0; k < nn; ++k) {
+        const u32* src = X + (size_t)s_nrow[k] * K;
+        u32* dst = Bm + (size_t)(rho + k) * K;
+        for (u32 q = tid; q < K; q += blockDim.x) dst[q] = src[q];
+      }
+      if (tid < (int)nn) {
+        bpiv[rho + tid] = s_npiv[tid];
+        colpiv[s_npiv[tid]] = rho + tid;
+      }
+      if (tid == 0) {
+        st->rho_old = rho;
+        st->rho = rho + nn;
+        st->nnew = nn;
+        st->qh = qh + cnt;
+        st->mode = nn ? 0u : 1u;
+      }
+    }
+    grid.sync();
+    // C: the old basis rows reduced by the new rows (keeps the basis RREF)
+    {
+      const u32 nn = __ldcg(&st->nnew), ro = __ldcg(&st->rho_old);
+      if (nn && ro)
+        for (u32 i = blockIdx.x; i < ro; i += G) reduce_row(Bm + (size_t)i * K, ro, nn);
+    }
+    grid.sync();
+  }
+  // emit: basis rows in ascending pivot order (CTA 0 orders, all copy)
+  const u32 rho = __ldcg(&st->rho);
+  if (blockIdx.x == 0) {
+    u32 base = 0;
+    for (u32 q0 = 0; q0 < K; q0 += blockDim.x) {
+      const u32 q = q0 + tid;
+      const u32 j = q < K ? __ldcg(colpiv + q) : NONE;
+      u32 tot;
+      const u32 pre = block_scan_flag(j != NONE ? 1u : 0u, red, &tot);
+      if (j != NONE) {
+        dpiv[base + pre] = q;
+        queue[base + pre] = j;  // queue reused: position -> basis row
+      }
+      base += tot;
+    }
+    if (tid == 0) *rank_out = rho;
+  }
+  grid.sync();
+  for (u32 k = blockIdx.x; k < rho; k += G) {
+    const u32* src = Bm + (size_t)__ldcg(queue + k) * K;
+    u32* dst = Rd + (size_t)k * K;
+    for (u32 q = tid; q < K; q += blockDim.x) dst[q] = __ldcg(src + q);
+  }
+}
+
 // E3b: pivots of D' in one CTA: pivot flags, their exclusive scan, the pivot
 // lists (column, row), the inverse leads, the pivot bitmap and rank(D') —
 // all on the device, no host read before the back-substitution.
@@ -1879,7 +2137,91 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
       long long distinct = std::unique(leads.begin(), leads.end()) - leads.begin();
       fprintf(stderr, "[dp] R=%lld K=%lld nonzero_rows=%lld distinct_leads=%lld density=%.3f\n", R, K, nz_rows,
               distinct, R * K ? (double)nnz / (double)(R * K) : 0.0);
+      if (getenv("F4B_DP_PROFILE") && R * K <= (1ll << 24)) {
+        // rank profile: rows in order, incremental RREF basis (host, diagnostic)
+        const unsigned long long P = c->p;
+        std::vector<std::vector<unsigned long long>> basis;
+        std::vector<long long> bpiv, newat;
+        for (long long i = 0; i < R; ++i) {
+          std::vector<unsigned long long> x(h.begin() + i * K, h.begin() + (i + 1) * K);
+          for (size_t b = 0; b < basis.size(); ++b) {
+            const unsigned long long f = x[bpiv[b]];
+            if (!f) continue;
+            for (long long q = 0; q < K; ++q) x[q] = (x[q] + (P - f) * basis[b][q]) % P;
+          }
+          long long l = -1;
+          for (long long q = 0; q < K; ++q)
+            if (x[q]) { l = q; break; }
+          if (l < 0) continue;
+          unsigned long long inv = 1, bb = x[l], e = P - 2;
+          while (e) { if (e & 1) inv = inv * bb % P; bb = bb * bb % P; e >>= 1; }
+          for (auto& v : x) v = v * inv % P;
+          for (size_t b = 0; b < basis.size(); ++b) {
+            const unsigned long long f = basis[b][l];
+            if (!f) continue;
+            for (long long q = 0; q < K; ++q) basis[b][q] = (basis[b][q] + (P - f) * x[q]) % P;
+          }
+          basis.push_back(x);
+          bpiv.push_back(l);
+          newat.push_back(i);
+        }
+        fprintf(stderr, "[dp]   rank=%zu new pivots at rows:", basis.size());
+        for (size_t k = 0; k < newat.size(); k += std::max<size_t>(1, newat.size() / 16)) fprintf(stderr, " %lld", newat[k]);
+        if (!newat.empty()) fprintf(stderr, " last=%lld", newat.back());
+        fprintf(stderr, "\n");
+      }
     }
+    // E3 alternative (opt-in, F4B_DENSE=rref): chunked RREF with a fully
+    // reduced basis (k_dense_rref).  Measured slower than the per-pivot path
+    // on cyclic-8 (18.7 vs 10.4 ms per replay step): the rank of D' arrives
+    // at ~1 pivot per 15 rows, so almost every 27-row chunk pays its three
+    // grid barriers and a latency-bound row reduction for ~2 pivots.
+    const long long CHr = std::min<long long>(RR_MAXCH, (195ll * 1024) / (4 * std::max<long long>(K, 1)));
+    static const bool rref_on = getenv("F4B_DENSE") && !strcmp(getenv("F4B_DENSE"), "rref");
+    if (rref_on && CHr >= 8 && R < (1ll << 31) && K < (1ll << 30)) {
+      const long long rmax = std::max<long long>(1, std::min(R, K));
+      const size_t smem_r = (size_t)std::max<long long>(2 * K, CHr * K) * 4;
+      static bool rr_attr = false;
+      if (!rr_attr) {
+        check_cuda(cudaFuncSetAttribute(k_dense_rref<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
+                   "attr");
+        check_cuda(cudaFuncSetAttribute(k_dense_rref<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
+                   "attr");
+        rr_attr = true;
+      }
+      DBuf Bm, bp, qu, stt, colp;
+      ensure(c, Bm, (size_t)rmax * K * sizeof(u32));
+      ensure(c, bp, (size_t)rmax * sizeof(u32));
+      ensure(c, qu, (size_t)(std::max(R, K) + 16) * sizeof(u32));
+      ensure(c, stt, sizeof(RrefState) + 16);
+      ensure(c, colp, (size_t)K * sizeof(u32));
+      check_cuda(cudaMemsetAsync(colp.p, 0xFF, (size_t)K * sizeof(u32), c->stream), "memset");
+      ensure(c, E->Rd, (size_t)rmax * K * sizeof(u32));
+      ensure(c, E->dpiv, (size_t)rmax * sizeof(u32));
+      ensure(c, E->rdev, 16);
+      fp = make_fp(c);
+      u32* dpp = Dp.as<u32>();
+      u32 Ru = (u32)R, Ku = (u32)K, CHu = (u32)CHr;
+      u32* bmp = Bm.as<u32>();
+      u32* bpp = bp.as<u32>();
+      u32* qp = qu.as<u32>();
+      RrefState* sp = reinterpret_cast<RrefState*>(stt.p);
+      u32* rdp = E->Rd.as<u32>();
+      u32* dpivp = E->dpiv.as<u32>();
+      u32* rkp = E->rdev.as<u32>();
+      u32* colpp = colp.as<u32>();
+      void* args[] = {&fp, &dpp, &Ru, &Ku, &CHu, &bmp, &bpp, &qp, &sp, &rdp, &dpivp, &rkp, &colpp};
+      {
+        ProfScope ps(c, "k_dense_rref");
+        const void* kf = c->p < 65536u ? (const void*)k_dense_rref<true> : (const void*)k_dense_rref<false>;
+        check_cuda(cudaLaunchCooperativeKernel(kf, c->num_sms, RR_THREADS, args, smem_r, c->stream), "k_dense_rref");
+      }
+      release(c, Bm);
+      release(c, bp);
+      release(c, qu);
+      release(c, stt);
+      release(c, colp);
+    } else {
     // E3a: cooperative forward elimination
     ensure(c, used, (size_t)R + 16);
     ensure(c, pofc, (size_t)K * sizeof(u32));
@@ -2041,6 +2383,7 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
     release(c, pinv);
     release(c, dprow);
     release(c, pbits);
+    }
   } else {
     ensure(c, E->rdev, 16);
     check_cuda(cudaMemsetAsync(E->rdev.p, 0, 4, c->stream), "memset");

@@ -75,6 +75,10 @@ struct Ctx {
   // (cudaMallocFromPoolAsync, memory retained by the pool: no device
   // synchronisation and no host callback per buffer)
   cudaMemPool_t mempool = nullptr;
+  // page-locked staging of f4b_basis_append* (lengths / prefix up, LM and
+  // max-exponent rows + error flag down: async copies, one sync per call)
+  void* h_app = nullptr;
+  size_t h_app_cap = 0;
   cudaStream_t stream = 0;
   int num_sms = 148;
   std::string last_error;

@@ -2504,7 +2504,9 @@ static void compile_rank_fused(Ctx* c, const KeyFmt& f, int D, long long r0, con
   static const int bps_max = getenv("F4B_LOOP_BPS") ? atoi(getenv("F4B_LOOP_BPS")) : 2;
   // every SM, even for small batches: fewer CTAs measured slower (the closure
   // rounds' search and ranking spread over all warps)
-  const int G = c->num_sms * std::max(1, std::min(bps_cached, bps_max));
+  static const int g_env = getenv("F4B_FBSP_G") ? atoi(getenv("F4B_FBSP_G")) : 0;
+  const int G_full = c->num_sms * std::max(1, std::min(bps_cached, bps_max));
+  const int G = g_env > 0 ? std::min(g_env, G_full) : G_full;
   const size_t W = (size_t)G * (CL_THREADS / 32);
   ensure(c, c->loop_scratch, (2 * W + 16) * sizeof(u32));
   // presence maps dict | done | newbits: zero on entry (kept zero by the

@@ -11,6 +11,8 @@ host copies are materialized only when a caller touches them.
 from __future__ import annotations
 
 import enum
+import itertools
+import operator
 import hashlib
 from dataclasses import dataclass, field
 
@@ -206,6 +208,10 @@ def _empty_plan(ring: Ring) -> LayoutPlan:
                       {"dict_build_ns": 0, "row_assemble_ns": 0})
 
 
+_get_basis_index = operator.attrgetter("basis_index")
+_get_shift = operator.attrgetter("shift")
+
+
 def compile_batch(rows, basis: SoaPolySet, closure: Closure = Closure.ONE_STEP_REDUCTION,
                   policy: ExecPolicy = DEFAULT_POLICY, candidates=None) -> LayoutPlan:
     """Compile a deterministic row list into a layout plan on the GPU.
@@ -224,10 +230,11 @@ def compile_batch(rows, basis: SoaPolySet, closure: Closure = Closure.ONE_STEP_R
     eng = Engine.for_ring(ring)
     eng.sync_basis(basis)
     n = ring.n_vars
-    rb = np.fromiter((r.basis_index for r in rows), dtype=np.int64, count=len(rows))
+    rb = np.fromiter(map(_get_basis_index, rows), dtype=np.int64, count=len(rows))
     if rb.min() < 0 or rb.max() >= len(basis):
         raise IndexError("row references a basis index out of range")
-    sh = np.asarray([r.shift for r in rows], dtype=np.int64).reshape(len(rows), n)
+    sh = np.fromiter(itertools.chain.from_iterable(map(_get_shift, rows)), dtype=np.int64,
+                     count=len(rows) * n).reshape(len(rows), n)
     # compare by value: callers may pass the reference's own Closure enum
     one_step = getattr(closure, "value", closure) == Closure.ONE_STEP_REDUCTION.value
     dev = eng.compile(rb, sh, one_step,

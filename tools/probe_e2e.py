@@ -1,13 +1,17 @@
 """Where the end-to-end (host-buffer) time of bench.py's e2e leg goes.
 
 Replays every cyclic-8 batch through the public API exactly like bench.py's
-e2e loop (fresh device basis per batch) and splits the wall time into basis
-upload, compile_batch and the LayoutPlan downloads.  Diagnostic only.
+e2e loop (empty device basis per step, page-locked basis streams, the basis
+grown batch by batch) and splits the wall time into: basis upload
+(sync_basis), row-list conversion, the compile call, and the LayoutPlan
+downloads.  Diagnostic only.
 """
 
 import os
 import sys
 import time
+
+import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -18,46 +22,52 @@ import bench  # noqa: E402
 def main():
     import torch
 
-    from paper_2601_06765_b200.engine import Engine
+    from paper_2601_06765_b200.engine import Engine, host_empty
     from paper_2601_06765_b200.polynomials import SoaPolySet
-    from paper_2601_06765_b200.symbolic import compile_batch
+    from paper_2601_06765_b200.symbolic import DICT_CAP
 
     ring, st, batches, _ = bench.capture_workload()
     eng = Engine.for_ring(ring)
     final = st.soa()
-    acc = {}
-    M = 0
-    import cProfile
-    import pstats
 
-    prof = cProfile.Profile()
+    def pinned(a):
+        out = host_empty(a.shape, a.dtype)
+        out[...] = a
+        return out
+
+    f_key, f_coeff, f_exps = pinned(final.mon_key), pinned(final.coeff), pinned(final.exps)
+    n = ring.n_vars
     for rep in range(3):
-        acc = {k: 0.0 for k in ("compile", "rowptr_col_val", "dict_keys")}
+        acc = dict.fromkeys(("sync_basis", "rows", "compile", "row_ptr_col_val", "dict_keys"), 0.0)
         M = 0
+        torch.cuda.synchronize()
+        t_all = time.perf_counter()
         eng.clear_basis()
-        if rep == 2:
-            prof.enable()
         for b in batches:
             nb_, nt = b["n_basis"], b["n_terms"]
-            soa = SoaPolySet(ring, final.mon_key[:nt], final.coeff[:nt], final.offset[:nb_ + 1],
-                             final.length[:nb_], final.exps[:nt])
+            soa = SoaPolySet(ring, f_key[:nt], f_coeff[:nt], final.offset[:nb_ + 1], final.length[:nb_],
+                             f_exps[:nt])
+            t0 = time.perf_counter()
+            eng.sync_basis(soa)
+            t1 = time.perf_counter()
+            rows = b["rows"]
+            rb = np.fromiter((r.basis_index for r in rows), dtype=np.int64, count=len(rows))
+            sh = np.asarray([r.shift for r in rows], dtype=np.int64).reshape(len(rows), n)
             t2 = time.perf_counter()
-            plan = compile_batch(b["rows"], soa)
+            dev = eng.compile(rb, sh, True, None, DICT_CAP)
             t3 = time.perf_counter()
-            rp, ci, va = plan.row_ptr, plan.col_ind, plan.val
+            got = dev.download(arrays=True, dict_exps=False, closure=False)
+            t4 = time.perf_counter()
+            dk = dev.download_ref_keys(ring.n_key_words)
             t5 = time.perf_counter()
-            dk = plan.dict_keys
-            t6 = time.perf_counter()
-            acc["compile"] += t3 - t2
-            acc["rowptr_col_val"] += t5 - t3
-            acc["dict_keys"] += t6 - t5
+            for k, v in zip(acc, (t1 - t0, t2 - t1, t3 - t2, t4 - t3, t5 - t4)):
+                acc[k] += v
             M += b["M"]
-            del rp, ci, va, dk
-        if rep == 2:
-            prof.disable()
-    tot = sum(acc.values())
-    print({k: round(v * 1e3, 2) for k, v in acc.items()}, "total_ms", round(tot * 1e3, 2), "nnz/s", M / tot)
-    pstats.Stats(prof).sort_stats("cumulative").print_stats(25)
+            del got, dk, dev
+        torch.cuda.synchronize()
+        tot = time.perf_counter() - t_all
+        print({k: round(v * 1e3, 2) for k, v in acc.items()}, "total_ms", round(tot * 1e3, 2), "nnz/s",
+              round(M / tot), flush=True)
 
 
 if __name__ == "__main__":
