@@ -808,6 +808,7 @@ __global__ void __launch_bounds__(256) k_sweep_win(Fp fp, u32 mu, const u32* __r
   u32* apre = smem + nwords;  // A columns before word w
   u32* acc = smem + ((2 * nwords + 3) & ~3u);  // N + 1 slots (slot N absorbs padding)
   __shared__ u32 s_act[NWARP][32];
+  __shared__ u32 s_ms[32], s_msh[32], s_ng[32], s_g0[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const u32 p = fp.p;
   auto red = [&](u32 v) -> u32 {  // v mod p for v < 2^32 (Barrett, mu = floor(2^32 / p))
@@ -858,20 +859,33 @@ __global__ void __launch_bounds__(256) k_sweep_win(Fp fp, u32 mu, const u32* __r
       const u32 j = (apre[c >> 5] + __popc(abits[c >> 5] & ((1u << (c & 31)) - 1u))) >> 5;
       const u32 cw = __ldg(winC + j * 32 + lane);
       const uint2 dd = __ldg(winD + j * 32 + lane);
-      const u32* W = winW + (size_t)j * 1024 + lane;
-      u32 wv[32];
-#pragma unroll
-      for (int q = 0; q < 32; ++q) wv[q] = __ldg(W + q * 32);
       const u32 v = (cw < N && cw >= lead) ? red(acc[cw]) : 0u;
-      // multipliers of the window's 32 pivots: m = v W (lane t holds m_t)
-      u32 m = 0;
+      // multipliers m = v W, split over the 8 warps: warp w owns pivots
+      // t = 4w .. 4w+3 (lane s contributes v_s W[s][t], one 16-byte load),
+      // warp sums, then Shoup constants and group counts into shared memory
+      {
+        const uint4 w4 = __ldg(reinterpret_cast<const uint4*>(winW + (size_t)j * 1024 + lane * 32) + warp);
+        u32 part[4] = {v ? fp.mont_mul(v, w4.x) : 0u, v ? fp.mont_mul(v, w4.y) : 0u, v ? fp.mont_mul(v, w4.z) : 0u,
+                       v ? fp.mont_mul(v, w4.w) : 0u};
 #pragma unroll
-      for (int q = 0; q < 32; ++q) m = fp.add(m, fp.mont_mul(__shfl_sync(0xffffffffu, v, q), wv[q]));
-      // standard-domain multiplier and its Shoup constant floor(ms 2^32 / p):
-      // ms * x mod p is then x*ms - umulhi(x, msh)*p, in [0, 2p)
-      const u32 ms = fp.mont_mul(m, 1u);
-      const u32 msh = ms ? (u32)(((unsigned long long)ms << 32) / p) : 0u;
-      const u32 ng = ms ? dd.y - dd.x : 0u;
+        for (int o = 16; o; o >>= 1)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) part[i] = fp.add(part[i], __shfl_xor_sync(0xffffffffu, part[i], o));
+        const u32 t = 4 * warp + (lane & 3);
+        const uint2 dt = make_uint2(__shfl_sync(0xffffffffu, dd.x, t), __shfl_sync(0xffffffffu, dd.y, t));
+        if (lane < 4) {
+          const u32 mt = lane == 0 ? part[0] : lane == 1 ? part[1] : lane == 2 ? part[2] : part[3];
+          // standard-domain multiplier and its Shoup constant floor(ms 2^32 / p):
+          // ms * x mod p is then x*ms - umulhi(x, msh)*p, in [0, 2p)
+          const u32 ms = fp.mont_mul(mt, 1u);
+          s_ms[t] = ms;
+          s_msh[t] = ms ? (u32)(((unsigned long long)ms << 32) / p) : 0u;
+          s_ng[t] = ms ? dt.y - dt.x : 0u;
+          s_g0[t] = dt.x;
+        }
+      }
+      __syncthreads();
+      const u32 ng = s_ng[lane], ms = s_ms[lane], msh = s_msh[lane];
       u32 x = ng;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -882,15 +896,11 @@ __global__ void __launch_bounds__(256) k_sweep_win(Fp fp, u32 mu, const u32* __r
       const u32 off = x - ng;
       const unsigned act = __ballot_sync(0xffffffffu, ng != 0);
       if (ng) s_act[warp][__popc(act & lanemask_lt())] = lane;
-      if (warp == 0) {
-        u32 tl = ng;
-#pragma unroll
-        for (int o = 16; o; o >>= 1) tl += __shfl_xor_sync(0xffffffffu, tl, o);
-        if (lane == 0) {
-          n_piv += __popc(act);
-          n_tail += 4ull * tl;
-        }
+      if (warp == 0 && lane == 0) {
+        n_piv += __popc(act);
+        n_tail += 4ull * tot;
       }
+      const uint2 dd_g = make_uint2(s_g0[lane], 0u);
       __syncwarp();
       // apply: the active pivots' groups as one flat list [0, tot); warp w
       // takes spans of 32 consecutive groups, lane L group a0 + L; the pivot
@@ -915,7 +925,7 @@ __global__ void __launch_bounds__(256) k_sweep_win(Fp fp, u32 mu, const u32* __r
             }
             const int t = s_act[warp][min(k0 + cnt, 31)];
             const u32 offt = __shfl_sync(0xffffffffu, off, t);
-            const u32 g0 = __shfl_sync(0xffffffffu, dd.x, t);
+            const u32 g0 = __shfl_sync(0xffffffffu, dd_g.x, t);
             const u32 mt = __shfl_sync(0xffffffffu, ms, t), mh = __shfl_sync(0xffffffffu, msh, t);
             if (a < tot) {
               const size_t g = (size_t)g0 + (a - offt);
