@@ -276,11 +276,19 @@ def kernel_bytes(name, b, pinfo, einfo):
         return M * (8 * KW + 4) + 8 * M
     if name.startswith(("k_rank_fill", "k_tile_dict")):
         return M * 8 * KW
+    if "k_sweep_win" in name:
+        # packed pivot tails (4-byte col|val entries in 4-entry groups when
+        # N < 2^16 and p < 2^16, else 8-byte pairs), streamed once per applied
+        # pivot; the C rows read once, D' written once
+        c_nnz = int(C * M / max(1, b["r"]))
+        entry = 4 if "<true>" in name else 8
+        return entry * einfo["sweep_tail_nnz"] + 8 * c_nnz + 4 * C * K
     if "k_sweep" in name:
         # C-row share of the nonzeros: |C| rows of mean length M / r
         c_nnz = int(C * M / max(1, b["r"]))
         return 8 * einfo["sweep_tail_nnz"] + 16 * einfo["sweep_pivots"] + 8 * c_nnz + 4 * C * K
-    if name == "k_dense_forward":
+    if name in ("k_dense_forward", "k_dense_fwd_smem", "k_dense_forward_cta"):
+        # D' read into the row state and the pivot rows written back once
         return 8 * C * K
     return None
 
@@ -306,9 +314,13 @@ def roofline_for(kprof, records, peak, peak_src, want):
         out = {"bound": "hbm", "kernel": name, "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                "traffic": None, "launches": cnt, "avg_launch_us": ns / cnt / 1e3, "peak_source": peak_src,
                "share_of_step": ns / total, "algorithmic_bytes_per_launch": tot / cnt}
-        if "k_sweep" in name:
-            out["note"] = ("pivot-row stream is L2-resident (rows reused by every C row); blocked sweep: "
-                           "3 CTA barriers per 32-A-column window, shared-atomic tail application")
+        if "k_sweep_win" in name:
+            out["note"] = ("pivot tails packed once per matrix and L2-resident (reused by every C row); fixed "
+                           "32-A-column windows with precomputed block inverses: multipliers from one 32x32 "
+                           "product, two CTA barriers per non-empty window, shared-atomic tail application")
+        elif name.startswith("k_dense_fwd"):
+            out["note"] = ("latency-bound: one grid barrier per pivot of D' (byte model counts D' once; the "
+                           "per-pivot row updates stay in shared memory)")
         return out
     return None
 

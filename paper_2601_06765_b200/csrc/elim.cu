@@ -2290,7 +2290,9 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
     static const char* dense_env = getenv("F4B_DENSE");
     if (!done_cluster && !dense_env) {
       const size_t Kp = (size_t)((K + 3) & ~3ll);
-      const long long rpc = (R + c->num_sms - 1) / c->num_sms;
+      static const int ds_cps = getenv("F4B_DS_CPS") ? atoi(getenv("F4B_DS_CPS")) : 1;
+      const long long gmax = (long long)c->num_sms * std::max(1, ds_cps);
+      const long long rpc = (R + gmax - 1) / gmax;
       const size_t smem_ds = (size_t)(rpc + 1) * Kp * 4;
       if (rpc <= DS_MAXROWS && smem_ds <= 200 * 1024) {
         static bool ds_attr = false;
