@@ -333,6 +333,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--no-katsura11", action="store_true",
+                    help="skip the full Katsura-11 run reported next to the line (rank 0, after the timed region)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -492,6 +494,29 @@ def main():
                         "compile_batch, LayoutPlan arrays D2H (page-locked); wall clock incl. Python API")}
         eng.clear_basis()
 
+    # the other north-star system: the full Katsura-11 / F_32003 computation
+    # (the reference cannot finish it: its step 4 alone takes 1,556 s on one
+    # core).  Katsura-11 has 2^11 solutions, so the reduced basis must leave
+    # exactly 2048 standard monomials; steps 3-4 are pinned to the reference
+    # by tests/test_gpu_parity.py::test_large_step_replay.
+    k11 = None
+    if rank == 0 and not args.no_katsura11:
+        from paper_2601_06765_b200.groebner import f4_groebner as _f4
+        from paper_2601_06765_b200.systems import format_system, gen_katsura
+
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        from full_run import standard_monomials
+
+        kring, kpolys = gen_katsura(11, 32003)
+        t0 = time.perf_counter()
+        kgb = _f4(kpolys, kring)
+        k11 = {"system": "Katsura-11 / F_32003, grevlex, full F4 + device interreduction",
+               "wall_s": round(time.perf_counter() - t0, 3), "gb_size": len(kgb),
+               "standard_monomials": standard_monomials([f.lm() for f in kgb], kring.n_vars),
+               "expected_standard_monomials": 2 ** 11,
+               "sha256": __import__("hashlib").sha256(format_system(kring, kgb).encode()).hexdigest(),
+               "reference": "does not finish (SURVEY.md 6.2: step 4 alone 1,556 s)"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         s = cpu_sample()
@@ -514,7 +539,7 @@ def main():
             "roofline": roof, "roofline_symbolic": roof_sym, "cpu_baseline": cpu, "e2e": e2e,
             "clocks": clk.summary(),
             "gpu_launches": launches1 - launches0, "wall_ms_per_step": 1000 * wall / args.steps,
-            "setup_s": round(setup_s, 2), "full_run": full_run, "kernels_top": kernels,
+            "setup_s": round(setup_s, 2), "full_run": full_run, "full_run_katsura11": k11, "kernels_top": kernels,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -5,6 +5,7 @@ Tolerance: none — everything is exact integer arithmetic mod p, so every
 comparison is byte equality (plan_to_text / RREF digests / arrays)."""
 
 import hashlib
+import os
 
 import numpy as np
 import pytest
@@ -392,6 +393,25 @@ def test_full_run_final_basis_matches_reference(cuda, name, gen, args):
     ref = load_golden(name)
     assert len(gb) == ref["gb_size"]
     assert hashlib.sha256(format_system(ring, gb).encode()).hexdigest() == ref["final_sha256"]
+
+
+@pytest.mark.parametrize("n", [8, 10, 11])
+def test_katsura_full_run_staircase(cuda, n):
+    """Katsura-n is zero-dimensional with 2^n solutions, so its reduced grevlex
+    basis leaves exactly 2^n standard monomials.  Katsura-11 is a north-star
+    system the reference cannot finish (its step 4 alone takes 1,556 s on one
+    core); its steps 3-4 are pinned by test_large_step_replay, the
+    whole run by this count.  Katsura-8 also matches the reference digest."""
+    import sys
+
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    from full_run import standard_monomials
+
+    ring, polys = gen_katsura(n, 32003)
+    gb = f4_groebner(polys, ring)
+    assert standard_monomials([f.lm() for f in gb], ring.n_vars) == 2 ** n
+    if n == 8:
+        assert hashlib.sha256(format_system(ring, gb).encode()).hexdigest() == load_golden("katsura8_p32003")["final_sha256"]
 
 
 @pytest.mark.parametrize("shape", [(37, 37), (53, 29)])
