@@ -86,6 +86,14 @@ int f4b_basis_append(f4b_ctx* ctx, int64_t n_polys, const int64_t* lengths,
  * exponents run on the device; page-locked host buffers copy at full rate. */
 int f4b_basis_append_wide(f4b_ctx* ctx, int64_t n_polys, const int64_t* lengths,
                           const int64_t* exps, const uint64_t* coeffs);
+/* Same, without waiting for the device: the host-side completion (range-check
+ * result, LM / max-exponent mirrors) happens in the next call that needs the
+ * basis (f4b_compile_batch, f4b_basis_*), which then reports a range error of
+ * this append (the basis is left as it was).  The caller's host buffers must
+ * stay valid until that call.  f4b_basis_sync completes it explicitly. */
+int f4b_basis_append_wide_async(f4b_ctx* ctx, int64_t n_polys, const int64_t* lengths,
+                                const int64_t* exps, const uint64_t* coeffs);
+int f4b_basis_sync(f4b_ctx* ctx);
 int f4b_basis_size(const f4b_ctx* ctx, int64_t* n_polys, int64_t* n_terms);
 
 typedef struct {

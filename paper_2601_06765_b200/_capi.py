@@ -61,6 +61,8 @@ SIGNATURES = {
     "f4b_basis_clear": (C.c_int, [C.c_void_p]),
     "f4b_basis_append": (C.c_int, [C.c_void_p, C.c_int64, i64p, u16p, u32p]),
     "f4b_basis_append_wide": (C.c_int, [C.c_void_p, C.c_int64, i64p, i64p, u64p]),
+    "f4b_basis_append_wide_async": (C.c_int, [C.c_void_p, C.c_int64, i64p, i64p, u64p]),
+    "f4b_basis_sync": (C.c_int, [C.c_void_p]),
     "f4b_basis_size": (C.c_int, [C.c_void_p, i64p, i64p]),
     "f4b_compile_batch": (C.c_int, [C.c_void_p, C.c_int64, i32p, u16p, C.c_int, i32p, C.c_int64, C.c_int64,
                                     C.POINTER(C.c_void_p)]),

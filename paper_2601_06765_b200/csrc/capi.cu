@@ -381,6 +381,11 @@ const char* f4b_ctx_last_error(const f4b_ctx* h) { return h ? h->c.last_error.c_
 
 int f4b_basis_clear(f4b_ctx* h) {
   if (!h) return F4B_ERR_PRECONDITION;
+  if (h->c.pend.active) {  // a pending append is discarded with the basis
+    h->c.pend.active = false;
+    cudaStreamSynchronize(h->c.stream);
+    release(&h->c, h->c.pend.raw);
+  }
   Basis& B = h->c.basis;
   B.n_polys = 0;
   B.n_terms = 0;
@@ -399,6 +404,7 @@ int f4b_basis_append(f4b_ctx* h, int64_t n_polys, const int64_t* lengths, const 
   if (!h) return F4B_ERR_PRECONDITION;
   API_BEGIN(&h->c)
   Ctx* c = _c;
+  basis_finish(c);
   Basis& B = c->basis;
   const int n = c->n_vars;
   if (n_polys < 0) fail(F4B_ERR_PRECONDITION, "negative polynomial count");
@@ -500,11 +506,12 @@ __global__ void k_poly_meta(const uint16_t* __restrict__ e16, const int64_t* __r
   }
 }
 
-int f4b_basis_append_wide(f4b_ctx* h, int64_t n_polys, const int64_t* lengths, const int64_t* exps,
-                          const uint64_t* coeffs) {
-  if (!h) return F4B_ERR_PRECONDITION;
-  API_BEGIN(&h->c)
-  Ctx* c = _c;
+// Issue an append of the reference's int64 / uint64 streams (narrowing,
+// range checks, LM / max exponents on the device) without waiting: the host
+// mirrors and the error flag are completed by basis_finish.
+static void basis_append_wide_issue(Ctx* c, int64_t n_polys, const int64_t* lengths, const int64_t* exps,
+                                    const uint64_t* coeffs) {
+  basis_finish(c);  // the staging block is reused
   Basis& B = c->basis;
   const int n = c->n_vars;
   if (n_polys < 0) fail(F4B_ERR_PRECONDITION, "negative polynomial count");
@@ -523,7 +530,8 @@ int f4b_basis_append_wide(f4b_ctx* h, int64_t n_polys, const int64_t* lengths, c
   ensure_keep(c, B.lmexp, (size_t)(P1 + 1) * n * sizeof(u16));
   ensure_keep(c, B.maxe, (size_t)(P1 + 1) * n * sizeof(u16));
   // raw streams -> device staging -> narrowed basis streams
-  DBuf raw;
+  Ctx::PendingAppend& pa = c->pend;
+  DBuf& raw = pa.raw;
   const size_t b_e = (size_t)T * n * 8, b_c = (size_t)T * 8, b_l = (size_t)std::max<long long>(n_polys, 1) * 8,
                b_p = (size_t)(n_polys + 1) * 8;
   ensure(c, raw, b_e + b_c + b_l + b_p + 64);
@@ -575,26 +583,71 @@ int f4b_basis_append_wide(f4b_ctx* h, int64_t n_polys, const int64_t* lengths, c
   }
   check_cuda(cudaMemcpyAsync(B.off.as<u32>() + P1, ha + o_tail, 4, cudaMemcpyHostToDevice, c->stream), "h2d off");
   check_cuda(cudaMemcpyAsync(ha + o_bad, d_bad, 4, cudaMemcpyDeviceToHost, c->stream), "d2h");
+  pa.active = true;
+  pa.n_polys = n_polys;
+  pa.T1 = T1;
+  pa.P1 = P1;
+  pa.o_lm = o_lm;
+  pa.o_mx = o_mx;
+  pa.o_bad = o_bad;
+  pa.lengths.assign(lengths, lengths + n_polys);
+}
+
+static void basis_finish_impl(Ctx* c) {
+  Ctx::PendingAppend& pa = c->pend;
+  if (!pa.active) return;
+  pa.active = false;
   check_cuda(cudaStreamSynchronize(c->stream), "sync");
-  const uint32_t bad = *reinterpret_cast<u32*>(ha + o_bad);
-  release(c, raw);
+  Basis& B = c->basis;
+  const int n = c->n_vars;
+  const unsigned char* ha = static_cast<const unsigned char*>(c->h_app);
+  const uint32_t bad = *reinterpret_cast<const u32*>(ha + pa.o_bad);
+  release(c, pa.raw);
+  // a rejected append leaves the basis as it was (n_terms / n_polys not advanced)
   if (bad & 1u) fail(F4B_ERR_LANE_OVERFLOW, "exponent does not fit a 16-bit lane");
   if (bad & 2u) fail(F4B_ERR_PROPERTY, "basis coefficient outside [1, p)");
-  for (long long i = 0; i < n_polys; ++i) {
-    B.h_len.push_back(lengths[i]);
-    B.h_off.push_back(B.h_off.back() + lengths[i]);
+  for (long long i = 0; i < pa.n_polys; ++i) {
+    B.h_len.push_back(pa.lengths[i]);
+    B.h_off.push_back(B.h_off.back() + pa.lengths[i]);
   }
-  const uint16_t* hlm = reinterpret_cast<const uint16_t*>(ha + o_lm);
-  const uint16_t* hmx = reinterpret_cast<const uint16_t*>(ha + o_mx);
-  B.h_lm.insert(B.h_lm.end(), hlm, hlm + (size_t)n_polys * n);
-  B.h_maxe.insert(B.h_maxe.end(), hmx, hmx + (size_t)n_polys * n);
-  B.n_terms = T1;
-  B.n_polys = (int)P1;
+  const uint16_t* hlm = reinterpret_cast<const uint16_t*>(ha + pa.o_lm);
+  const uint16_t* hmx = reinterpret_cast<const uint16_t*>(ha + pa.o_mx);
+  B.h_lm.insert(B.h_lm.end(), hlm, hlm + (size_t)pa.n_polys * n);
+  B.h_maxe.insert(B.h_maxe.end(), hmx, hmx + (size_t)pa.n_polys * n);
+  B.n_terms = pa.T1;
+  B.n_polys = (int)pa.P1;
+}
+
+int f4b_basis_append_wide(f4b_ctx* h, int64_t n_polys, const int64_t* lengths, const int64_t* exps,
+                          const uint64_t* coeffs) {
+  if (!h) return F4B_ERR_PRECONDITION;
+  API_BEGIN(&h->c)
+  basis_append_wide_issue(_c, n_polys, lengths, exps, coeffs);
+  basis_finish(_c);
+  API_END
+}
+
+int f4b_basis_append_wide_async(f4b_ctx* h, int64_t n_polys, const int64_t* lengths, const int64_t* exps,
+                                const uint64_t* coeffs) {
+  if (!h) return F4B_ERR_PRECONDITION;
+  API_BEGIN(&h->c)
+  basis_append_wide_issue(_c, n_polys, lengths, exps, coeffs);
+  API_END
+}
+
+int f4b_basis_sync(f4b_ctx* h) {
+  if (!h) return F4B_ERR_PRECONDITION;
+  API_BEGIN(&h->c)
+  basis_finish(_c);
   API_END
 }
 
 int f4b_basis_size(const f4b_ctx* h, int64_t* n_polys, int64_t* n_terms) {
   if (!h) return F4B_ERR_PRECONDITION;
+  if (h->c.pend.active) {
+    const int code = f4b_basis_sync(const_cast<f4b_ctx*>(h));
+    if (code) return code;
+  }
   if (n_polys) *n_polys = h->c.basis.n_polys;
   if (n_terms) *n_terms = h->c.basis.n_terms;
   return F4B_OK;
@@ -609,6 +662,7 @@ int f4b_compile_batch(f4b_ctx* h, int64_t n_rows, const int32_t* row_basis, cons
   pl->ctx = &h->c;
   API_BEGIN(&h->c)
   try {
+    basis_finish(_c);
     compile_batch(_c, n_rows, row_basis, row_shift, closure, candidates, n_candidates, dict_cap, pl);
   } catch (...) {
     plan_release(pl);
@@ -657,10 +711,16 @@ int f4b_plan_download(const f4b_plan* pl, int64_t* row_ptr, int64_t* col_ind, ui
     if (w_row) F4B_LAUNCH(c, k_widen_u32, g, 256, 0, pl->row_ptr.as<u32>(), w_row, wp);
     if (w_col) F4B_LAUNCH(c, k_widen_u32, g, 256, 0, pl->col_ind.as<u32>(), w_col, wp + w_row);
     if (w_val) F4B_LAUNCH(c, k_widen_u32, g, 256, 0, pl->val.as<u32>(), w_val, wp + w_row + w_col);
-    if (w_row) check_cuda(cudaMemcpyAsync(row_ptr, wp, w_row * 8, cudaMemcpyDeviceToHost, c->stream), "d2h");
-    if (w_col) check_cuda(cudaMemcpyAsync(col_ind, wp + w_row, w_col * 8, cudaMemcpyDeviceToHost, c->stream), "d2h");
-    if (w_val)
-      check_cuda(cudaMemcpyAsync(val, wp + w_row + w_col, w_val * 8, cudaMemcpyDeviceToHost, c->stream), "d2h");
+    const bool contiguous = w_row && w_col && w_val && col_ind == row_ptr + w_row &&
+                            reinterpret_cast<int64_t*>(val) == col_ind + w_col;
+    if (contiguous) {  // one host block (the Python host allocates it so): one copy
+      check_cuda(cudaMemcpyAsync(row_ptr, wp, (w_row + w_col + w_val) * 8, cudaMemcpyDeviceToHost, c->stream), "d2h");
+    } else {
+      if (w_row) check_cuda(cudaMemcpyAsync(row_ptr, wp, w_row * 8, cudaMemcpyDeviceToHost, c->stream), "d2h");
+      if (w_col) check_cuda(cudaMemcpyAsync(col_ind, wp + w_row, w_col * 8, cudaMemcpyDeviceToHost, c->stream), "d2h");
+      if (w_val)
+        check_cuda(cudaMemcpyAsync(val, wp + w_row + w_col, w_val * 8, cudaMemcpyDeviceToHost, c->stream), "d2h");
+    }
   }
   if (dict_exps && N)
     check_cuda(cudaMemcpyAsync(dict_exps, pl->dict_exps.p, N * n * sizeof(u16), cudaMemcpyDeviceToHost, c->stream), "d2h");
@@ -831,3 +891,5 @@ int f4b_spmm(f4b_ctx* h, int64_t n_rows, int64_t n_cols, const int64_t* row_ptr,
 }
 
 }  // extern "C"
+
+void f4b::basis_finish(Ctx* c) { basis_finish_impl(c); }

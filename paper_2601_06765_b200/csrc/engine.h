@@ -30,6 +30,7 @@ struct Error {
 void ensure(Ctx* c, DBuf& b, size_t bytes);  // grow-only; contents not preserved
 void ensure_keep(Ctx* c, DBuf& b, size_t bytes);  // grow-only; contents preserved
 void release(Ctx* c, DBuf& b);
+void basis_finish(Ctx* c);  // completes a pending asynchronous basis append
 void pool_flush(Ctx* c);
 void check_cuda(cudaError_t e, const char* what);  // throws Error{F4B_ERR_CUDA}
 [[noreturn]] void fail(int code, const std::string& msg);
@@ -79,6 +80,15 @@ struct Ctx {
   // max-exponent rows + error flag down: async copies, one sync per call)
   void* h_app = nullptr;
   size_t h_app_cap = 0;
+  // an f4b_basis_append_wide_async whose host side (range-check flag, LM and
+  // max-exponent mirrors) is completed by the next call that needs it
+  struct PendingAppend {
+    bool active = false;
+    long long n_polys = 0, T1 = 0, P1 = 0;
+    size_t o_lm = 0, o_mx = 0, o_bad = 0;
+    std::vector<int64_t> lengths;
+    DBuf raw;
+  } pend;
   cudaStream_t stream = 0;
   int num_sms = 148;
   std::string last_error;

@@ -73,9 +73,11 @@ class DevicePlan:
         r, M, N, ncl = (self.info[k] for k in ("r", "M", "N", "n_closure_rows"))
         out = {}
         if arrays:
-            out["row_ptr"] = host_empty(r + 1, np.int64)
-            out["col_ind"] = host_empty(M, np.int64)
-            out["val"] = host_empty(M, np.uint64)
+            # one page-locked block, three views: the library copies it in one go
+            blk = host_empty(r + 1 + 2 * M, np.int64)
+            out["row_ptr"] = blk[:r + 1]
+            out["col_ind"] = blk[r + 1:r + 1 + M]
+            out["val"] = blk[r + 1 + M:].view(np.uint64)
         if dict_exps:
             out["dict_exps"] = np.empty((N, n), dtype=np.uint16)
         if closure:
@@ -242,7 +244,11 @@ class Engine:
         self._reset_mirror()
         self.generation += 1
 
-    def append_polys(self, lengths, exps, coeffs):
+    def append_polys(self, lengths, exps, coeffs, defer: bool = False):
+        """Append polynomials to the device basis.  With ``defer`` (the
+        reference-format int64 / uint64 streams only) the call returns without
+        waiting for the device; range errors then surface from the next
+        compile (the caller keeps ``exps`` / ``coeffs`` alive until then)."""
         lengths = np.ascontiguousarray(lengths, dtype=np.int64)
         exps = np.asarray(exps)
         coeffs = np.asarray(coeffs)
@@ -251,9 +257,11 @@ class Engine:
             # the reference's SoaPolySet streams as they are: narrowing, range
             # checks and per-polynomial metadata on the device
             self.ctx.sync_stream()
-            self.ctx.check(self.lib.f4b_basis_append_wide(self.ctx.h, len(lengths), ptr(lengths, C.c_int64),
-                                                          ptr(exps, C.c_int64), ptr(coeffs, C.c_uint64)),
-                           "basis append")
+            fn = self.lib.f4b_basis_append_wide_async if defer else self.lib.f4b_basis_append_wide
+            self.ctx.check(fn(self.ctx.h, len(lengths), ptr(lengths, C.c_int64), ptr(exps, C.c_int64),
+                              ptr(coeffs, C.c_uint64)), "basis append")
+            if defer:
+                self._deferred = (lengths, exps, coeffs)  # host buffers read by the pending copy
             self._lens = np.concatenate([self._lens, lengths])
             if len(coeffs):
                 self._chunks.append((self._T, exps, coeffs))
@@ -307,7 +315,7 @@ class Engine:
             self.clear_basis()
         n_dev, T_dev = self.n_polys, self._T
         if len(soa) > n_dev:
-            self.append_polys(soa.length[n_dev:], soa.exps[T_dev:], soa.coeff[T_dev:])
+            self.append_polys(soa.length[n_dev:], soa.exps[T_dev:], soa.coeff[T_dev:], defer=True)
         self._src = self._buffers(soa)
         self._src_refs = (soa.exps, soa.coeff)
         soa._f4b_token = self.token
@@ -326,6 +334,11 @@ class Engine:
             self.ctx.h, len(rb), ptr(rb, C.c_int32), ptr(sh, C.c_uint16), 1 if closure else 0,
             ptr(cand, C.c_int32) if cand is not None else None, 0 if cand is None else len(cand),
             int(dict_cap), C.byref(h))
+        self._deferred = None
+        if code:
+            # a failed compile may also carry the error of a deferred append:
+            # forget the device basis mirror so the next sync re-uploads it
+            self.clear_basis()
         self.ctx.check(code, "compile_batch")
         return DevicePlan(self, h)
 
