@@ -163,6 +163,13 @@ int f4b_spmm(f4b_ctx* ctx, int64_t n_rows, int64_t n_cols, const int64_t* row_pt
              const int64_t* col_ind, const uint64_t* val, const uint64_t* X, int64_t b,
              uint64_t* Y);
 
+/* berlekamp_massey (sparselin.py:377-413) for b sequences of length len
+ * (seqs [b][len] u64 residues) side by side, one CTA per sequence: polys
+ * [b][len + 1] receives each minimal polynomial ascending and monic
+ * (reversed connection polynomial, the reference's return value) in its first
+ * degrees[j] + 1 entries. */
+int f4b_bm(f4b_ctx* ctx, const uint64_t* seqs, int64_t len, int64_t b, uint64_t* polys, int64_t* degrees);
+
 /* Device-resident black-box operator for Block Wiedemann (sparselin.py:450-548):
  * B = A (square, normal = 0) or B = AᵀA (normal = 1, Aᵀ built once).  The CSR
  * stays in HBM across applications; vectors are host [dim][b] u64 residues. */

@@ -20,3 +20,4 @@ product code path.  The product (``paper_2601_06765_b200``) never imports it.
 
 from .fbsp import compile_batch_arrays, plan_text, plan_sha256  # noqa: F401
 from .psge import psge_arrays, rref_sha256  # noqa: F401
+from .wiedemann import berlekamp_massey  # noqa: F401,E402

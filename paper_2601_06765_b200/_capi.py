@@ -63,6 +63,7 @@ SIGNATURES = {
     "f4b_basis_append_wide": (C.c_int, [C.c_void_p, C.c_int64, i64p, i64p, u64p]),
     "f4b_basis_append_wide_async": (C.c_int, [C.c_void_p, C.c_int64, i64p, i64p, u64p]),
     "f4b_basis_sync": (C.c_int, [C.c_void_p]),
+    "f4b_bm": (C.c_int, [C.c_void_p, u64p, C.c_int64, C.c_int64, u64p, i64p]),
     "f4b_basis_size": (C.c_int, [C.c_void_p, i64p, i64p]),
     "f4b_compile_batch": (C.c_int, [C.c_void_p, C.c_int64, i32p, u16p, C.c_int, i32p, C.c_int64, C.c_int64,
                                     C.POINTER(C.c_void_p)]),

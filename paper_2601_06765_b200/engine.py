@@ -371,6 +371,18 @@ class Engine:
                                               C.byref(h)), "operator")
         return DeviceOperator(self, h, int(n_cols))
 
+    def bm(self, seqs):
+        """Berlekamp–Massey of the columns of ``seqs`` ([len][b]) on the
+        device; returns one ascending monic minimal polynomial per column."""
+        S = np.ascontiguousarray(np.asarray(seqs, dtype=np.uint64).T)  # [b][len]
+        b, n = S.shape
+        polys = np.zeros((b, n + 1), dtype=np.uint64)
+        degs = np.zeros(b, dtype=np.int64)
+        self.ctx.sync_stream()
+        self.ctx.check(self.lib.f4b_bm(self.ctx.h, ptr(S, C.c_uint64), int(n), int(b), ptr(polys, C.c_uint64),
+                                       ptr(degs, C.c_int64)), "berlekamp_massey")
+        return [[int(x) for x in polys[j, :degs[j] + 1]] for j in range(b)]
+
     def spmm(self, n_rows, n_cols, row_ptr, col_ind, val, X):
         X = np.ascontiguousarray(X, dtype=np.uint64)
         b = X.shape[1]

@@ -414,6 +414,35 @@ def test_katsura_full_run_staircase(cuda, n):
         assert hashlib.sha256(format_system(ring, gb).encode()).hexdigest() == load_golden("katsura8_p32003")["final_sha256"]
 
 
+def test_berlekamp_massey_device_matches_reference(cuda):
+    """k_bm (csrc/bm.cu) against the real reference's Berlekamp–Massey outputs
+    (tests/golden/bm_golden.json.gz), one sequence at a time through the
+    public berlekamp_massey and batched per prime through Engine.bm; plus long
+    Krylov-length sequences against the oracle restatement."""
+    import gzip
+    import json
+
+    from paper_2601_06765_b200.sparselin import _engine_for, berlekamp_massey
+
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "bm_golden.json.gz")
+    with gzip.open(path, "rt") as fh:
+        cases = json.load(fh)["cases"]
+    for c in cases:
+        assert berlekamp_massey(c["seq"], FieldModulus(c["p"])) == c["poly"]
+    by_len = {}
+    for c in cases:
+        by_len.setdefault((c["p"], len(c["seq"])), []).append(c)
+    for (p, n), group in by_len.items():
+        seqs = np.array([c["seq"] for c in group], dtype=np.uint64).T
+        assert _engine_for(FieldModulus(p)).bm(seqs) == [c["poly"] for c in group]
+    rng = np.random.default_rng(5)
+    for p in (31, 32003):
+        long = rng.integers(0, p, (3000, 2), dtype=np.uint64)
+        got = _engine_for(FieldModulus(p)).bm(long)
+        for j in range(2):
+            assert got[j] == oracle.berlekamp_massey(long[:, j].tolist(), p)
+
+
 @pytest.mark.parametrize("shape", [(37, 37), (53, 29)])
 def test_resident_operator_matches_numpy(cuda, shape):
     """f4b_op_*: Krylov projections, Horner evaluation and the power loop of

@@ -97,3 +97,19 @@ def test_oracle_psge_panel_width_invariance():
     digests = {oracle.rref_sha256(*(lambda e: (e["pivot_rows"], e["nonpivot_rows"]))(
         oracle.psge_arrays(30, 25, rp, cols, mat[rows, cols].astype(np.uint64), p, w))) for w in (1, 4, 64, 256)}
     assert len(digests) == 1
+
+
+def test_oracle_berlekamp_massey_matches_reference_golden():
+    """oracle.berlekamp_massey against the real reference's outputs
+    (tests/golden/make_bm_golden.py: worked examples, LFSRs, random and
+    Krylov-projection sequences over five primes)."""
+    import gzip
+    import json
+    import os
+
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "bm_golden.json.gz")
+    with gzip.open(path, "rt") as fh:
+        cases = json.load(fh)["cases"]
+    assert len(cases) > 60
+    for c in cases:
+        assert oracle.berlekamp_massey(c["seq"], c["p"]) == c["poly"]
