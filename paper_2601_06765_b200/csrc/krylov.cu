@@ -56,6 +56,71 @@ __global__ void k_op_apply(Fp fp, const u32* __restrict__ rp, const u32* __restr
   }
 }
 
+// b = 4 (the reference's block width): one pass over the row's nonzeros for
+// all four columns (one 16-byte gather of X per nonzero), products summed
+// lazily in u64 (SMALLP: p < 2^16, raw products < 2^32; else exact residues
+// < 2^31) with a single reduction mod p per output after the warp sum.
+template <bool SMALLP>
+__global__ void k_op_apply4(Fp fp, const u32* __restrict__ rp, const u32* __restrict__ col,
+                            const u32* __restrict__ val, long long r, const uint4* __restrict__ X,
+                            uint4* __restrict__ Y, u32 cmul, const uint4* __restrict__ Z,
+                            const uint4* __restrict__ U, unsigned long long* __restrict__ proj) {
+  const long long row = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x & 31;
+  if (row >= r) return;
+  const u32 s = rp[row], e = rp[row + 1];
+  unsigned long long a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+  auto term = [&](u32 v, const uint4& x) {
+    if (SMALLP) {
+      a0 += (unsigned long long)v * x.x;
+      a1 += (unsigned long long)v * x.y;
+      a2 += (unsigned long long)v * x.z;
+      a3 += (unsigned long long)v * x.w;
+    } else {
+      const u32 vm = fp.to_mont(v);
+      a0 += fp.mont_mul(vm, x.x);
+      a1 += fp.mont_mul(vm, x.y);
+      a2 += fp.mont_mul(vm, x.z);
+      a3 += fp.mont_mul(vm, x.w);
+    }
+  };
+  u32 k = s + lane;
+  for (; k + 32 < e; k += 64) {
+    const u32 c0 = __ldg(col + k), c1 = __ldg(col + k + 32);
+    const u32 v0 = __ldg(val + k), v1 = __ldg(val + k + 32);
+    const uint4 x0 = __ldg(X + c0), x1 = __ldg(X + c1);
+    term(v0, x0);
+    term(v1, x1);
+  }
+  if (k < e) term(__ldg(val + k), __ldg(X + __ldg(col + k)));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+    a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+    a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+    a3 += __shfl_xor_sync(0xffffffffu, a3, o);
+  }
+  if (lane == 0) {
+    const u32 p = fp.p;
+    uint4 y = make_uint4((u32)(a0 % p), (u32)(a1 % p), (u32)(a2 % p), (u32)(a3 % p));
+    if (Z) {
+      const uint4 z = Z[row];
+      y.x = fp.add(y.x, fp.mul(cmul, z.x));
+      y.y = fp.add(y.y, fp.mul(cmul, z.y));
+      y.z = fp.add(y.z, fp.mul(cmul, z.z));
+      y.w = fp.add(y.w, fp.mul(cmul, z.w));
+    }
+    Y[row] = y;
+    if (proj) {
+      const uint4 u = U[row], x = X[row];
+      atomicAdd(proj + 0, (unsigned long long)fp.mul(u.x, x.x));
+      atomicAdd(proj + 1, (unsigned long long)fp.mul(u.y, x.y));
+      atomicAdd(proj + 2, (unsigned long long)fp.mul(u.z, x.z));
+      atomicAdd(proj + 3, (unsigned long long)fp.mul(u.w, x.w));
+    }
+  }
+}
+
 // acc[j] += Σ_i U[i][j] X[i][j] (when the projection cannot ride on the apply)
 __global__ void k_op_proj(Fp fp, const u32* __restrict__ U, const u32* __restrict__ X, long long n, int b,
                           unsigned long long* __restrict__ proj) {
@@ -99,25 +164,38 @@ static void upload_csr(Ctx* c, long long r, const int64_t* rp, const int64_t* co
 }
 
 // W_out = B W_in (+ cmul * Z); proj (optional) += U · W_in
+static void apply_rows(Ctx* c, const Fp& fp, const u32* rp, const u32* col, const u32* val, long long r,
+                       const u32* X, int b, u32* Y, u32 cmul, const u32* Z, const u32* U, unsigned long long* proj) {
+  const int grid = (int)((r * 32 + 255) / 256);
+  if (b == 4) {
+    const uint4 *X4 = reinterpret_cast<const uint4*>(X), *Z4 = reinterpret_cast<const uint4*>(Z),
+                *U4 = reinterpret_cast<const uint4*>(U);
+    uint4* Y4 = reinterpret_cast<uint4*>(Y);
+    if (c->p < 65536u)
+      F4B_LAUNCH(c, k_op_apply4<true>, grid, 256, 0, fp, rp, col, val, r, X4, Y4, cmul, Z4, U4, proj);
+    else
+      F4B_LAUNCH(c, k_op_apply4<false>, grid, 256, 0, fp, rp, col, val, r, X4, Y4, cmul, Z4, U4, proj);
+  } else {
+    F4B_LAUNCH(c, k_op_apply, grid, 256, 0, fp, rp, col, val, r, X, b, Y, cmul, Z, U, proj);
+  }
+}
+
 static void op_apply_dev(f4b_op* op, const u32* Win, u32* Wout, int b, u32 cmul, const u32* Z, const u32* U,
                          unsigned long long* proj) {
   Ctx* c = op->ctx;
   Fp fp = make_fp_pub(c);
   if (!op->normal) {
     const long long r = op->n_rows;
-    F4B_LAUNCH(c, k_op_apply, (int)((r * 32 + 255) / 256), 256, 0, fp, op->rp.as<u32>(), op->col.as<u32>(),
-               op->val.as<u32>(), r, Win, b, Wout, cmul, Z, U, proj);
+    apply_rows(c, fp, op->rp.as<u32>(), op->col.as<u32>(), op->val.as<u32>(), r, Win, b, Wout, cmul, Z, U, proj);
   } else {
     // T = A W (n_rows), W' = Aᵀ T (dim); the projection of W rides on the second pass
     const long long r = op->n_rows, d = op->dim;
-    F4B_LAUNCH(c, k_op_apply, (int)((r * 32 + 255) / 256), 256, 0, fp, op->rp.as<u32>(), op->col.as<u32>(),
-               op->val.as<u32>(), r, Win, b, op->t.as<u32>(), 0u, (const u32*)nullptr, (const u32*)nullptr,
-               (unsigned long long*)nullptr);
+    apply_rows(c, fp, op->rp.as<u32>(), op->col.as<u32>(), op->val.as<u32>(), r, Win, b, op->t.as<u32>(), 0u,
+               nullptr, nullptr, nullptr);
     if (proj)
       F4B_LAUNCH(c, k_op_proj, (int)std::min<long long>((d + 255) / 256, c->num_sms * 4), 256, 0, fp, U, Win, d, b, proj);
-    F4B_LAUNCH(c, k_op_apply, (int)((d * 32 + 255) / 256), 256, 0, fp, op->trp.as<u32>(), op->tcol.as<u32>(),
-               op->tval.as<u32>(), d, op->t.as<u32>(), b, Wout, cmul, Z, (const u32*)nullptr,
-               (unsigned long long*)nullptr);
+    apply_rows(c, fp, op->trp.as<u32>(), op->tcol.as<u32>(), op->tval.as<u32>(), d, op->t.as<u32>(), b, Wout, cmul, Z,
+               nullptr, nullptr);
   }
 }
 
