@@ -797,7 +797,7 @@ __global__ void __launch_bounds__(256) k_sweep_win(Fp fp, u32 mu, const u32* __r
                                                    const u32* __restrict__ rows, u32 nrows,
                                                    const u32* __restrict__ abits_g, const u32* __restrict__ winW,
                                                    const u32* __restrict__ winC, const uint2* __restrict__ winD,
-                                                   const uint4* __restrict__ tails,
+                                                   u32 nwin, const uint4* __restrict__ tails,
                                                    u32* __restrict__ Dp, u32 K, const u32* __restrict__ nonA,
                                                    unsigned long long* __restrict__ stats) {
   extern __shared__ __align__(16) u32 smem[];
@@ -843,6 +843,9 @@ __global__ void __launch_bounds__(256) k_sweep_win(Fp fp, u32 mu, const u32* __r
     for (u32 k = s + tid; k < e; k += blockDim.x) acc[col[k]] = val[k];
     __syncthreads();
     u32 from = lead;
+    u32 pj = 0xFFFFFFFFu, pcw = 0;
+    uint2 pdd = make_uint2(0, 0);
+    uint4 pw4 = make_uint4(0, 0, 0, 0);
     while (true) {
       // next nonzero A column >= from (every warp, same answer)
       u32 c = N;
@@ -857,14 +860,35 @@ __global__ void __launch_bounds__(256) k_sweep_win(Fp fp, u32 mu, const u32* __r
       }
       if (c >= N) break;
       const u32 j = (apre[c >> 5] + __popc(abits[c >> 5] & ((1u << (c & 31)) - 1u))) >> 5;
-      const u32 cw = __ldg(winC + j * 32 + lane);
-      const uint2 dd = __ldg(winD + j * 32 + lane);
+      // this window's columns, tail groups and block-inverse slice: from the
+      // registers if the previous window prefetched them (the usual case:
+      // consecutive windows), then the next window's are prefetched so their
+      // L2 latency hides behind this window's product and tail application
+      u32 cw;
+      uint2 dd;
+      uint4 w4;
+      if (j == pj) {
+        cw = pcw;
+        dd = pdd;
+        w4 = pw4;
+      } else {
+        cw = __ldg(winC + j * 32 + lane);
+        dd = __ldg(winD + j * 32 + lane);
+        w4 = __ldg(reinterpret_cast<const uint4*>(winW + (size_t)j * 1024 + lane * 32) + warp);
+      }
+      if (j + 1 < nwin) {
+        pj = j + 1;
+        pcw = __ldg(winC + pj * 32 + lane);
+        pdd = __ldg(winD + pj * 32 + lane);
+        pw4 = __ldg(reinterpret_cast<const uint4*>(winW + (size_t)pj * 1024 + lane * 32) + warp);
+      } else {
+        pj = 0xFFFFFFFFu;
+      }
       const u32 v = (cw < N && cw >= lead) ? red(acc[cw]) : 0u;
       // multipliers m = v W, split over the 8 warps: warp w owns pivots
       // t = 4w .. 4w+3 (lane s contributes v_s W[s][t], one 16-byte load),
       // warp sums, then Shoup constants and group counts into shared memory
       {
-        const uint4 w4 = __ldg(reinterpret_cast<const uint4*>(winW + (size_t)j * 1024 + lane * 32) + warp);
         u32 part[4] = {v ? fp.mont_mul(v, w4.x) : 0u, v ? fp.mont_mul(v, w4.y) : 0u, v ? fp.mont_mul(v, w4.z) : 0u,
                        v ? fp.mont_mul(v, w4.w) : 0u};
 #pragma unroll
@@ -1958,11 +1982,11 @@ static void launch_sweep(Ctx* c, const Fp& fp, f4b_echelon* E, const u32* rows, 
       const u32 mu = (u32)((1ull << 32) / c->p);
       if (pk)
         F4B_LAUNCH(c, k_sweep_win<true>, grid, 256, smem, fp, mu, E->rp, E->col, E->val, N, rows, nrows,
-                   E->abits.as<u32>(), wW.as<u32>(), wC.as<u32>(), wD.as<uint2>(), wT.as<uint4>(), Dp, K,
+                   E->abits.as<u32>(), wW.as<u32>(), wC.as<u32>(), wD.as<uint2>(), nwin, wT.as<uint4>(), Dp, K,
                    E->nonA.as<u32>(), stats);
       else
         F4B_LAUNCH(c, k_sweep_win<false>, grid, 256, smem, fp, mu, E->rp, E->col, E->val, N, rows, nrows,
-                   E->abits.as<u32>(), wW.as<u32>(), wC.as<u32>(), wD.as<uint2>(), wT.as<uint4>(), Dp, K,
+                   E->abits.as<u32>(), wW.as<u32>(), wC.as<u32>(), wD.as<uint2>(), nwin, wT.as<uint4>(), Dp, K,
                    E->nonA.as<u32>(), stats);
       release(c, wW);
       release(c, wC);

@@ -152,7 +152,7 @@ def _oracle_rref(mat, p):
     return e, oracle.rref_sha256(e["pivot_rows"], e["nonpivot_rows"])
 
 
-@pytest.mark.parametrize("p", [7, 101, 32003, 65521, 2147483629])
+@pytest.mark.parametrize("p", [7, 101, 32003, 65521, 1048573, 2147483629])
 @pytest.mark.parametrize("density", [0.01, 0.05, 0.2, 0.6])
 def test_psge_random_against_oracle(cuda, p, density):
     m = FieldModulus(p)
@@ -167,6 +167,23 @@ def test_psge_random_against_oracle(cuda, p, density):
         assert ech.rank == e["rank"] and ech.zero_row_count == e["zero_row_count"]
         assert ech.pivot_cols == e["pivot_cols"]
         assert _rref_digest(ech) == want
+
+
+@pytest.mark.parametrize("p", [32003, 1048573])
+def test_psge_many_windows_against_oracle(cuda, p):
+    """Hundreds of C rows over several 32-column A windows: the windowed
+    sweep (packed tails for p < 2^16, (col, val) pairs above) and the D'
+    stage against the oracle."""
+    m = FieldModulus(p)
+    rng = np.random.default_rng(p % 1009)
+    r, c = 420, 360
+    mat = _random_sparse(rng, r, c, 0.04, p)
+    mat[rng.integers(0, r, r // 4)] = mat[rng.integers(0, r, r // 4)]
+    e, want = _oracle_rref(mat, p)
+    ech = psge_reduce(csr_from_dense(mat, m))
+    assert ech.rank == e["rank"] and ech.zero_row_count == e["zero_row_count"]
+    assert ech.pivot_cols == e["pivot_cols"]
+    assert _rref_digest(ech) == want
 
 
 def test_psge_zero_and_empty(cuda):
