@@ -173,36 +173,90 @@ def capture_workload():
 
 
 class ClockSampler:
-    """nvidia-smi sampling (100 ms) started before the timed region; only the
-    samples whose timestamps fall inside [t_begin, t_end] are summarised."""
+    """SM clock and clock-event (throttle) reasons sampled during the timed
+    region: in-process NVML queries taken between engine calls, at most every
+    100 ms (a concurrent poller — nvidia-smi -lms 100 or an NVML thread —
+    measured to stall the driver now and then inside the event intervals and
+    inflate a run by up to 30 %), with `nvidia-smi -lms 100` as the fallback
+    when NVML is unavailable.  Only samples inside [t_begin, t_end] count."""
 
-    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    # nvmlClocksEventReason bits
+    _BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40}
 
     def __init__(self, device):
         self.device = device
         self.proc = None
         self.path = None
+        self.thread = None
+        self.rows = []
+        self.max_mhz = None
         self.t_begin = self.t_end = None
+        self._sample = None
 
     def start(self):
+        if os.environ.get("F4B_BENCH_NO_SMI"):  # diagnostic: no sampling at all
+            return self
+        try:
+            import threading
+
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self._physical_index())
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+
+            def sample():
+                try:
+                    mhz = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.rows.append((time.time(), float(mhz), self.max_mhz, int(rs)))
+                except Exception:
+                    pass
+
+            self._sample = sample
+            self.thread = True
+            return self
+        except Exception:
+            self.thread = None
+            self._sample = None
         fd, self.path = tempfile.mkstemp(suffix=".csv")
         os.close(fd)
+        fields = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                  "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                  "clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={fields}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
         time.sleep(1.0)  # nvidia-smi needs a moment before its first sample
         return self
 
+    def _physical_index(self):
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        if vis:
+            try:
+                return int(vis.split(",")[self.device])
+            except (ValueError, IndexError):
+                pass
+        return self.device
+
+    def maybe_sample(self, period=0.1):
+        """NVML mode: one sample from the calling thread, between engine calls
+        (so a driver stall during the query lands outside the CUDA-event
+        intervals the metric sums), at most every `period` seconds."""
+        if self.thread is not None and self._sample is not None:
+            now = time.time()
+            if not self.rows or now - self.rows[-1][0] >= period:
+                self._sample()
+
     def begin(self):
         self.t_begin = time.time()
+        self.maybe_sample(0.0)
 
     def end(self):
+        self.maybe_sample(0.0)
         self.t_end = time.time()
 
     def stop(self):
@@ -214,7 +268,7 @@ class ClockSampler:
             except Exception:
                 self.proc.kill()
 
-    def summary(self):
+    def _read_smi(self):
         import datetime
 
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
@@ -228,24 +282,29 @@ class ClockSampler:
                     ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
                 except ValueError:
                     continue
-                rows.append((ts, float(parts[1]), float(parts[2]), parts[4:8]))
+                bits = 0
+                for nm, flag in zip(names, parts[4:8]):
+                    if flag.lower().startswith("active"):
+                        bits |= self._BITS[nm]
+                rows.append((ts, float(parts[1]), float(parts[2]), bits))
             os.unlink(self.path)
         except Exception:
             pass
+        return rows
+
+    def summary(self):
+        rows = self.rows if self.thread is not None else (self._read_smi() if self.path else [])
         inside = [r for r in rows if self.t_begin is not None and self.t_begin - 0.05 <= r[0] <= self.t_end + 0.05]
         note = "samples inside the timed region"
         if not inside and rows and self.t_begin is not None:
             # timed region shorter than the sampling period: nearest samples
             inside = sorted(rows, key=lambda r: abs(r[0] - 0.5 * (self.t_begin + self.t_end)))[:2]
             note = "timed region shorter than the sampling period: nearest samples"
-        reasons = set()
-        for r in inside:
-            for nm, flag in zip(names, r[3]):
-                if flag.lower().startswith("active"):
-                    reasons.add(nm)
+        reasons = sorted({nm for r in inside for nm, bit in self._BITS.items() if r[3] & bit})
         return {"sm_mhz": statistics.median([r[1] for r in inside]) if inside else None,
-                "sm_max_mhz": max(r[2] for r in inside) if inside else None, "reasons": sorted(reasons),
-                "samples": len(inside), "note": note}
+                "sm_max_mhz": max(r[2] for r in inside) if inside else None, "reasons": reasons,
+                "samples": len(inside), "note": note,
+                "source": "nvml" if self.thread is not None else ("nvidia-smi" if self.path else "none")}
 
 
 # Algorithmic bytes per kernel per batch — DESIGN.md §4.
@@ -376,15 +435,21 @@ def main():
     total_M = sum(b["M"] for b in batches)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
+    _dbg = [] if os.environ.get("F4B_BENCH_DEBUG") else None
+
     def replay_step(record):
         ts = tn = 0
         for b in batches:
+            clk.maybe_sample()
             flush.fill_(1)
             plan = eng.compile(b["rb"], b["sh"], True, list(range(b["n_basis"])))
             ech = eng.psge_plan(plan, full=False)
             inf = ech.info()
             ts += plan.info["dict_build_ns"] + plan.info["row_assemble_ns"]
             tn += inf["numeric_ns"]
+            if _dbg is not None:
+                _dbg.append((b["r"], (plan.info["dict_build_ns"] + plan.info["row_assemble_ns"]) / 1e6,
+                             inf["numeric_ns"] / 1e6))
             if record is not None:
                 record.append((b, plan.info, inf))
         return ts, tn
@@ -539,6 +604,7 @@ def main():
             "roofline": roof, "roofline_symbolic": roof_sym, "cpu_baseline": cpu, "e2e": e2e,
             "clocks": clk.summary(),
             "gpu_launches": launches1 - launches0, "wall_ms_per_step": 1000 * wall / args.steps,
+            "debug_slowest": (sorted(_dbg, key=lambda x: -(x[1] + x[2]))[:8] if _dbg else None),
             "setup_s": round(setup_s, 2), "full_run": full_run, "full_run_katsura11": k11, "kernels_top": kernels,
         }
         print(json.dumps(line), flush=True)

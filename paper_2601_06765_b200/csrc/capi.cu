@@ -2,6 +2,7 @@
 // the registered allocator, the device-resident basis, and the thin wrappers
 // that translate C++ exceptions into f4b_status codes.
 #include <algorithm>
+#include <chrono>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -32,6 +33,13 @@ void check_cuda(cudaError_t e, const char* what) {
 static void* raw_alloc(Ctx* c, size_t bytes) {
   if (bytes == 0) bytes = 16;
   void* p = nullptr;
+  ++c->raw_allocs;
+  const auto t0 = std::chrono::steady_clock::now();
+  struct Tm {
+    Ctx* c;
+    std::chrono::steady_clock::time_point t0;
+    ~Tm() { c->raw_alloc_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count(); }
+  } tm{c, t0};
   if (c->alloc) {
     p = c->alloc(bytes, c->user);
     if (!p) fail(F4B_ERR_OOM, "device allocation of " + std::to_string(bytes) + " bytes failed");
@@ -45,6 +53,7 @@ static void* raw_alloc(Ctx* c, size_t bytes) {
 
 static void raw_free(Ctx* c, void* p) {
   if (!p) return;
+  ++c->raw_frees;
   if (c->dfree) c->dfree(p, c->user);
   else if (c->mempool) cudaFreeAsync(p, c->stream);
   else cudaFree(p);
@@ -292,6 +301,20 @@ int f4b_ctx_create(int device, uint32_t p, int n_vars, int order, f4b_alloc_fn a
       check_cuda(cudaMemPoolCreate(&c->mempool, &props), "cudaMemPoolCreate");
       uint64_t keep = UINT64_MAX;
       check_cuda(cudaMemPoolSetAttribute(c->mempool, cudaMemPoolAttrReleaseThreshold, &keep), "mempool attr");
+      // reserve physical memory up front: growing the pool inside a call was
+      // measured to stall it for tens of ms (a 65 ms cudaMallocFromPoolAsync
+      // in the middle of an elimination); freed blocks stay with the pool
+      size_t free_b = 0, total_b = 0;
+      cudaMemGetInfo(&free_b, &total_b);
+      const size_t reserve = std::min<size_t>((size_t)2 << 30, free_b / 8);
+      if (reserve) {
+        void* warm = nullptr;
+        if (cudaMallocFromPoolAsync(&warm, reserve, c->mempool, c->stream) == cudaSuccess) {
+          cudaFreeAsync(warm, c->stream);
+          cudaStreamSynchronize(c->stream);
+        }
+        cudaGetLastError();
+      }
     }
     c->basis.h_off.push_back(0);
   } catch (const Error& e) {

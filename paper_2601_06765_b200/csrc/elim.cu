@@ -25,6 +25,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <chrono>
 #include <climits>
 #include <cstdlib>
 #include <cstring>
@@ -2081,6 +2082,14 @@ static void run_a_sweep(Ctx* c, f4b_echelon* E);
 
 static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
   Fp fp = make_fp(c);
+  static const bool etrace = getenv("F4B_ELIM_TRACE") != nullptr;
+  const auto h0 = std::chrono::steady_clock::now();
+  const long long a0 = c->raw_allocs, f0 = c->raw_frees;
+  const double au0 = c->raw_alloc_us;
+  std::vector<std::pair<const char*, double>> marks;
+  auto mark = [&](const char* w) {
+    if (etrace) marks.push_back({w, std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count()});
+  };
   const long long r = E->n_rows, N = E->n_cols;
   cudaEvent_t ev0, ev1;
   check_cuda(cudaEventCreate(&ev0), "event");
@@ -2128,8 +2137,10 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
       check_cuda(cudaLaunchCooperativeKernel((void*)k_psge_prep, GP, 256, args, 0, c->stream), "k_psge_prep");
     }
     PrepOut ho;
+    mark("prep launched");
     check_cuda(cudaMemcpyAsync(c->h_stat, d_out, sizeof(PrepOut), cudaMemcpyDeviceToHost, c->stream), "d2h");
     check_cuda(cudaStreamSynchronize(c->stream), "sync");
+    mark("prep synced");
     memcpy(&ho, c->h_stat, sizeof(PrepOut));
     E->nA = ho.nA;
     E->K = N - E->nA;
@@ -2145,8 +2156,10 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
     ensure(c, Dp, (size_t)R * K * sizeof(u32));
     ensure(c, E->stats, 16);
     check_cuda(cudaMemsetAsync(E->stats.p, 0, 16, c->stream), "memset");
+    mark("sweep issue");
     launch_sweep<0>(c, fp, E, crows.as<u32>(), (u32)R, Dp.as<u32>(), (u32)K, nullptr, 0, nullptr, nullptr, nullptr, 0,
                     nullptr, nullptr, nullptr, err, E->stats.as<unsigned long long>());
+    mark("sweep launched");
     static const bool dp_stats = getenv("F4B_DP_STATS") != nullptr;
     if (dp_stats) {  // diagnostic: shape of D' after the sweep (host copy)
       std::vector<u32> h((size_t)R * K);
@@ -2467,6 +2480,7 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
     if (!(ht->err & DEVERR_CAPACITY)) break;
     E->pool_cap *= 2;
   }
+  mark("tail synced");
   E->rankD = ht->rankD;
   const long long rankD = E->rankD;
   E->sweep_pivots = ht->st[0];
@@ -2479,6 +2493,13 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
   E->numeric_ns = (int64_t)(ms * 1e6);
   cudaEventDestroy(ev0);
   cudaEventDestroy(ev1);
+  if (etrace && ms > 10.0f) {
+    fprintf(stderr, "[elim] r=%lld N=%lld R=%lld K=%lld dev=%.2fms allocs=%lld frees=%lld alloc_us=%.0f:", (long long)r,
+            (long long)N, (long long)E->nC, (long long)E->K, ms, c->raw_allocs - a0, c->raw_frees - f0,
+            c->raw_alloc_us - au0);
+    for (auto& m : marks) fprintf(stderr, " %s @%.0f |", m.first, m.second);
+    fprintf(stderr, "\n");
+  }
   E->zero_rows = r - (E->nA + rankD);
   if (mode == F4B_FULL_RREF) run_a_sweep(c, E);
 }

@@ -121,6 +121,8 @@ struct Ctx {
   uint32_t pprime = 0, r2 = 0;
   long long launches = 0;        // kernel launches issued (reset per compile call)
   long long total_launches = 0;  // monotonically increasing
+  long long raw_allocs = 0, raw_frees = 0;  // device allocations / frees past the buffer cache
+  double raw_alloc_us = 0;                  // host time inside them
   // optional per-kernel CUDA-event timing (f4b_ctx_profile)
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
