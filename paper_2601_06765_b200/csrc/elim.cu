@@ -1867,6 +1867,383 @@ __global__ void __launch_bounds__(RR_THREADS, 1) k_dense_rref(Fp fp, u32* __rest
   }
 }
 
+// ---------------------------------------------------------------------------
+// E3 (default): RREF(D') in pivot BLOCKS.
+//
+// Invariant: every live D' row is reduced by the basis B (kept in RREF), i.e.
+// it is zero at every pivot column of B.  One iteration:
+//   1 (all CTAs)  every live row offers itself (one atomicAdd); the first NP
+//                 offers form the candidate block P.
+//   2 (CTA 0)     Gaussian elimination of P restricted to a window of DB_W
+//                 columns from its smallest lead (shared memory, one warp per
+//                 row, one CTA barrier per pivot) finds the pivot columns L
+//                 and the subset S of P's rows they come from; T = P[S, L] is
+//                 invertible, T^-1 by a Gauss-Jordan sweep in shared memory,
+//                 and T^-1·P[S] = RREF(span P[S]).  grid barrier.
+//   3 (all CTAs)  with m = x[L]·T^-1 every live row and every old basis row
+//                 is reduced in ONE product x <- x - m·P[S] (no pivot chain),
+//                 the new basis rows T^-1·P[S] are written, new leads found
+//                 in the same pass.  S's rows are consumed.
+// D' has few distinct leading columns, but its live rows are nearly
+// independent modulo B, so a block yields ~NP pivots: two grid barriers per
+// block instead of one per pivot (k_dense_fwd_smem), no back-substitution
+// (k_dense_back: B is reduced all along), and the full-width work is spread
+// over the grid.  The RREF is unique, so the rows equal the reference's
+// (sparselin.py:337-349).
+// ---------------------------------------------------------------------------
+struct DblkState {
+  u32 cnt, np, rho, rho_old, iters, t2_us, t3_us, pad;  // t*_us: CTA 0 phase times (trace)
+};
+F4B_DEV unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+static constexpr int DB_THREADS = 512;
+static constexpr int DB_NP = 32;  // max rows per block (one per lane of the selection warp)
+static constexpr int DB_W = 128;  // window of the pivot search
+static constexpr int DB_G = 8;    // rows per apply group
+template <bool SMALLP>
+__global__ void __launch_bounds__(DB_THREADS) k_dense_blk(Fp fp, u32* __restrict__ Dp, u32 R, u32 K, u32 rpc, u32 maxt,
+                                                          u32* __restrict__ lead, u32* __restrict__ cand,
+                                                          u32* __restrict__ Bm, u32* __restrict__ colpiv,
+                                                          u32* __restrict__ gwin, u32* __restrict__ gT,
+                                                          DblkState* __restrict__ st, u32* __restrict__ Rd,
+                                                          u32* __restrict__ dpiv, u32* __restrict__ rank_out,
+                                                          u32* __restrict__ order) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) u32 smem[];
+  constexpr int NW = DB_THREADS / 32;
+  const unsigned FULL = 0xffffffffu;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const u32 G = gridDim.x, bid = blockIdx.x;
+  const u32 p = fp.p;
+  __shared__ u32 s_T[DB_NP][DB_NP + 1];  // CTA 0: Y (-> T^-1); all: T^-1 of the block
+  __shared__ u32 s_U[DB_NP][DB_NP + 33];  // CTA 0: pivot rows at L | Z
+  __shared__ u32 s_dinv[DB_NP], s_crow[DB_NP], s_rl[DB_NP];
+  __shared__ u32 s_wrow[DB_NP], s_wcol[DB_NP];
+  __shared__ u32 s_red[33];
+  __shared__ u32 s_lm[NW][DB_G];
+  __shared__ u32 s_nt, s_na, s_piv, s_np, s_c0;
+  // CTA 0 phase 2: the block's window | Z, aliasing the phase-3 arrays
+  u32(*s_X)[DB_W + 32] = reinterpret_cast<u32(*)[DB_W + 32]>(smem);
+  u32* s_c = smem;                    // [maxt][DB_NP] coefficients
+  u32* s_task = smem + maxt * DB_NP;  // [maxt] kind<<30 | index
+  u32* s_act = s_task + maxt;         // [maxt] active task list
+  u32* s_lead = s_act + maxt;         // [rpc] leads of this CTA's rows
+  const u32 lo = bid * rpc;
+  const u32 nr = lo < R ? min(rpc, R - lo) : 0u;
+  auto prod = [&](u32 c, u32 v) -> u64 { return SMALLP ? (u64)c * v : (u64)fp.mont_mul(c, v); };
+  auto red64 = [&](u64 a) -> u32 { return (u32)(a % p); };
+  auto offer = [&](u32 row) {
+    const u32 s = atomicAdd(&st->cnt, 1u);
+    if (s < (u32)DB_NP) cand[s] = row;
+  };
+  u32* s_f = s_lead + rpc;  // [maxt] first nonzero column of each task
+  u32 ro = 0;
+  auto task_row = [&](u32 td) -> u32* {
+    const u32 kind = td >> 30, idx = td & 0x3FFFFFFFu;
+    return kind == 0 ? Dp + (size_t)(lo + idx) * K : Bm + (size_t)(kind == 1 ? idx : ro + idx) * K;
+  };
+  // prologue: leads of this CTA's rows (contiguous in D'), first offers
+  for (u32 r = tid; r < nr; r += DB_THREADS) s_lead[r] = K;
+  __syncthreads();
+  {
+    const u32* x0 = Dp + (size_t)lo * K;
+    const u32 tot = nr * K;  // host: rpc * K < 2^32
+    for (u32 e0 = tid; e0 < tot; e0 += 8 * DB_THREADS) {
+      u32 v[8];
+#pragma unroll
+      for (int h = 0; h < 8; ++h) {
+        const u32 e = e0 + h * DB_THREADS;
+        v[h] = e < tot ? __ldcg(x0 + e) : 0u;
+      }
+#pragma unroll
+      for (int h = 0; h < 8; ++h) {
+        if (v[h]) {
+          const u32 e = e0 + h * DB_THREADS, r = e / K, q = e - r * K;
+          if (q < s_lead[r]) atomicMin(&s_lead[r], q);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (u32 r = tid; r < nr; r += DB_THREADS) {
+    lead[lo + r] = s_lead[r];
+    if (s_lead[r] < K) offer(lo + r);
+  }
+  unsigned long long t2 = 0, t3 = 0, tm = 0;
+  while (true) {
+    grid.sync();  // offers complete, every row of this iteration final
+    if (bid == 0 && tid == 0) tm = gtimer();
+    if (bid == 0) {
+      // 2a: the candidates' window [c0, c0 + DB_W) in shared memory, each
+      // row augmented with its coefficient vector over the candidates (Z)
+      const u32 nc = min(__ldcg(&st->cnt), (u32)DB_NP);
+      const u32 rho = st->rho;
+      if (warp == 0) {
+        u32 row = 0, l = K;
+        if ((u32)lane < nc) {
+          row = __ldcg(cand + lane);
+          l = __ldcg(lead + row);
+        }
+        s_crow[lane] = row;
+        const u32 c0 = __reduce_min_sync(FULL, l);
+        if (lane == 0) {
+          s_c0 = c0;
+          s_np = 0;
+        }
+      }
+      __syncthreads();
+      const u32 c0 = s_c0;
+      for (u32 w = warp; w < nc; w += NW) {
+        const u32* src = Dp + (size_t)s_crow[w] * K + c0;
+        u32 v[DB_W / 32];
+#pragma unroll
+        for (int h = 0; h < DB_W / 32; ++h) {
+          const u32 q = lane + 32 * h;
+          v[h] = c0 + q < K ? __ldcg(src + q) : 0u;
+        }
+        u32 l = DB_W;
+#pragma unroll
+        for (int h = DB_W / 32 - 1; h >= 0; --h) {
+          s_X[w][lane + 32 * h] = v[h];
+          const unsigned bm = __ballot_sync(FULL, v[h] != 0);
+          if (bm) l = 32 * h + __ffs(bm) - 1;
+        }
+        s_X[w][DB_W + lane] = (u32)lane == w ? 1u : 0u;
+        if (lane == 0) s_rl[w] = l;
+      }
+      __syncthreads();
+      // 2b: forward elimination inside the window (row scaling, no inverses)
+      while (true) {
+        unsigned long long m = ~0ull;
+        if ((u32)lane < nc && s_rl[lane] < (u32)DB_W) m = ((unsigned long long)s_rl[lane] << 32) | (u32)lane;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) m = min(m, __shfl_xor_sync(FULL, m, o));
+        if (m == ~0ull) break;
+        const u32 pw = (u32)(m & 0xFFFFFFFFull), c = (u32)(m >> 32);
+        __syncthreads();  // every warp has read s_rl
+        if (tid == 0) {
+          s_wrow[s_np] = pw;  // candidate slot for now
+          s_wcol[s_np] = c;   // window column for now
+          s_np = s_np + 1;
+          s_rl[pw] = DB_W + 1;  // used
+        }
+        const u32* prw = s_X[pw];
+        const u32 a = fp.to_mont(prw[c]);
+        for (u32 w = warp; w < nc; w += NW) {
+          if (w == pw || s_rl[w] != c) continue;  // rows leading right of c are zero at c
+          u32* x = s_X[w];
+          const u32 bm = fp.to_mont(fp.neg(x[c]));
+          u32 l = DB_W;
+#pragma unroll
+          for (int h = DB_W / 32; h >= 0; --h) {  // h = DB_W/32: the coefficients
+            const u32 q = lane + 32 * h;
+            u32 v = 0;
+            if (q > c) {
+              v = fp.add(fp.mont_mul(a, x[q]), fp.mont_mul(bm, prw[q]));
+              x[q] = v;
+            } else if (q == c) {
+              x[q] = 0;
+            }
+            if (h < DB_W / 32) {
+              const unsigned b = __ballot_sync(FULL, v != 0);
+              if (b) l = 32 * h + __ffs(b) - 1;
+            }
+          }
+          if (lane == 0) s_rl[w] = l;
+        }
+        __syncthreads();
+      }
+      // 2c: back-elimination over the pivot columns and the coefficients
+      // (one warp per pivot row): E[:, L] becomes diagonal, then Z / diag =
+      // T^-1 expressed over the candidate slots
+      const u32 np = s_np;
+      for (u32 e = tid; e < np * (DB_NP + 32); e += DB_THREADS) {
+        const u32 i = e / (DB_NP + 32), k = e % (DB_NP + 32);
+        const u32* x = s_X[s_wrow[i]];
+        s_U[i][k] = k < DB_NP ? (k < np ? x[s_wcol[k]] : 0u) : x[DB_W + (k - DB_NP)];
+      }
+      __syncthreads();
+      for (int j = (int)np - 1; j > 0; --j) {
+        const u32 a = fp.to_mont(s_U[j][j]);
+        for (u32 i = warp; i < (u32)j; i += NW) {
+          const u32 f = s_U[i][j];
+          __syncwarp();
+          if (f) {
+            const u32 bm = fp.to_mont(fp.neg(f));
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const u32 k = lane + 32 * h;
+              if (k >= i) s_U[i][k] = fp.add(fp.mont_mul(a, s_U[i][k]), fp.mont_mul(bm, s_U[j][k]));
+            }
+          }
+        }
+        __syncthreads();
+      }
+      if (tid < (int)np) s_dinv[tid] = fp.to_mont(fp.inv(s_U[tid][tid]));
+      __syncthreads();
+      // T^-1[i][j] = Z_i[slot of S_j] / d_i
+      for (u32 e = tid; e < np * np; e += DB_THREADS) {
+        const u32 i = e / np, j = e % np;
+        const u32 v = fp.mont_mul(s_dinv[i], s_U[i][DB_NP + s_wrow[j]]);
+        gT[i * DB_NP + j] = SMALLP ? v : fp.to_mont(v);
+      }
+      if (tid < (int)np) {
+        const u32 row = s_crow[s_wrow[tid]], col = c0 + s_wcol[tid];
+        gwin[tid] = row;
+        gwin[DB_NP + tid] = col;
+        colpiv[col] = rho + tid;
+        lead[row] = K + 1;  // consumed: spans new basis rows
+      }
+      if (tid == 0) {
+        st->np = np;
+        st->rho_old = rho;
+        st->rho = rho + np;
+        st->cnt = 0;
+        st->iters += 1;
+      }
+    }
+    if (bid == 0 && tid == 0) {
+      const unsigned long long t = gtimer();
+      t2 += t - tm;
+      tm = t;
+    }
+    grid.sync();
+    const u32 np = __ldcg(&st->np);
+    ro = __ldcg(&st->rho_old);
+    if (np == 0) break;
+    // 3: tasks of this CTA
+    for (u32 e = tid; e < np * np; e += DB_THREADS) {
+      const u32 k = e / np, j = e % np;
+      s_T[k][j] = __ldcg(gT + k * DB_NP + j);
+    }
+    if (tid < (int)np) {
+      s_wrow[tid] = __ldcg(gwin + tid);
+      s_wcol[tid] = __ldcg(gwin + DB_NP + tid);
+    }
+    for (u32 r = tid; r < nr; r += DB_THREADS) s_lead[r] = __ldcg(lead + lo + r);
+    __syncthreads();
+    if (tid == 0) {
+      u32 nt = 0;
+      for (u32 r = 0; r < nr; ++r)
+        if (s_lead[r] < K) s_task[nt++] = r;  // kind 0: live D' row
+      for (u32 i = bid; i < ro; i += G) s_task[nt++] = (1u << 30) | i;  // kind 1: old basis row
+      for (u32 k = (bid + G - ro % G) % G; k < np; k += G) s_task[nt++] = (2u << 30) | k;  // kind 2: new basis row
+      s_nt = nt;
+      s_na = 0;
+    }
+    __syncthreads();
+    const u32 nt = s_nt;
+    // coefficients, one warp per task: m = x[L]·T^-1 (kind 2: row k of T^-1)
+    for (u32 t = warp; t < nt; t += NW) {
+      const u32 td = s_task[t], kind = td >> 30, idx = td & 0x3FFFFFFFu;
+      u32 m = 0;
+      if (kind == 2) {
+        m = (u32)lane < np ? s_T[idx][lane] : 0u;
+      } else {
+        const u32* x = kind == 0 ? Dp + (size_t)(lo + idx) * K : Bm + (size_t)idx * K;
+        const u32 xl = (u32)lane < np ? __ldcg(x + s_wcol[lane]) : 0u;
+        u64 acc = 0;
+        for (u32 k = 0; k < np; ++k) {
+          const u32 xk = __shfl_sync(FULL, xl, k);
+          if (xk && (u32)lane < np) acc += prod(s_T[k][lane], xk);
+        }
+        m = red64(acc);
+        if (!SMALLP && m) m = fp.to_mont(m);
+      }
+      s_c[t * DB_NP + lane] = m;
+      if (__ballot_sync(FULL, m != 0) && lane == 0) s_act[atomicAdd(&s_na, 1u)] = t;
+    }
+    __syncthreads();
+    const u32 na = s_na;
+    // one pass over the columns: the block's np rows are loaded once per
+    // column (one L2 round trip) and applied to every active task
+    for (u32 t = tid; t < nt; t += DB_THREADS) s_f[t] = K;
+    __syncthreads();
+    for (u32 q = tid; q < K; q += DB_THREADS) {
+      u32 pv[DB_NP];
+#pragma unroll
+      for (int j = 0; j < DB_NP; ++j) pv[j] = (u32)j < np ? __ldcg(Dp + (size_t)s_wrow[j] * K + q) : 0u;
+      for (u32 g0 = 0; g0 < na; g0 += DB_G) {
+        const u32 ng = min((u32)DB_G, na - g0);
+        u32 xb[DB_G];
+        u64 acc[DB_G];
+#pragma unroll
+        for (int r = 0; r < DB_G; ++r) {
+          acc[r] = 0;
+          xb[r] = 0;
+          if ((u32)r < ng) {
+            const u32 td = s_task[s_act[g0 + r]];
+            if ((td >> 30) != 2) xb[r] = __ldcg(task_row(td) + q);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < DB_NP; ++j) {
+          if (pv[j]) {
+#pragma unroll
+            for (int r = 0; r < DB_G; ++r)
+              if ((u32)r < ng) acc[r] += prod(s_c[s_act[g0 + r] * DB_NP + j], pv[j]);
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < DB_G; ++r) {
+          if ((u32)r < ng) {
+            const u32 t = s_act[g0 + r], td = s_task[t];
+            const u32 sres = red64(acc[r]);
+            const u32 v = (td >> 30) == 2 ? sres : fp.sub(xb[r], sres);
+            task_row(td)[q] = v;
+            if (v && q < s_f[t]) atomicMin(&s_f[t], q);
+          }
+        }
+      }
+    }
+    __syncthreads();
+    for (u32 a = tid; a < na; a += DB_THREADS) {
+      const u32 t = s_act[a], td = s_task[t];
+      if ((td >> 30) == 0) s_lead[td & 0x3FFFFFFFu] = s_f[t];
+    }
+    __syncthreads();
+    if (bid == 0 && tid == 0) t3 += gtimer() - tm;
+    // 1 (next iteration): offers of the live rows
+    for (u32 r = tid; r < nr; r += DB_THREADS) {
+      const u32 l = s_lead[r];
+      if (l <= K) {  // K + 1 = consumed
+        lead[lo + r] = l;
+        if (l < K) offer(lo + r);
+      }
+    }
+  }
+  // emit: basis rows in ascending pivot order
+  const u32 rho = __ldcg(&st->rho);
+  if (bid == 0) {
+    if (tid == 0) {
+      st->t2_us = (u32)(t2 / 1000);
+      st->t3_us = (u32)(t3 / 1000);
+    }
+    u32 base = 0;
+    for (u32 q0 = 0; q0 < K; q0 += DB_THREADS) {
+      const u32 q = q0 + tid;
+      const u32 j = q < K ? __ldcg(colpiv + q) : NONE;
+      u32 tot;
+      const u32 pre = block_scan_flag(j != NONE ? 1u : 0u, s_red, &tot);
+      if (j != NONE) {
+        dpiv[base + pre] = q;
+        order[base + pre] = j;
+      }
+      base += tot;
+    }
+    if (tid == 0) *rank_out = rho;
+  }
+  grid.sync();
+  for (u32 k = bid; k < rho; k += G) {
+    const u32* src = Bm + (size_t)__ldcg(order + k) * K;
+    u32* dst = Rd + (size_t)k * K;
+    for (u32 q = tid; q < K; q += DB_THREADS) dst[q] = __ldcg(src + q);
+  }
+}
+
 // E3b: pivots of D' in one CTA: pivot flags, their exclusive scan, the pivot
 // lists (column, row), the inverse leads, the pivot bitmap and rank(D') —
 // all on the device, no host read before the back-substitution.
@@ -2225,7 +2602,77 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
     // grid barriers and a latency-bound row reduction for ~2 pivots.
     const long long CHr = std::min<long long>(RR_MAXCH, (195ll * 1024) / (4 * std::max<long long>(K, 1)));
     static const bool rref_on = getenv("F4B_DENSE") && !strcmp(getenv("F4B_DENSE"), "rref");
-    if (rref_on && CHr >= 8 && R < (1ll << 31) && K < (1ll << 30)) {
+    // default E3: pivot blocks of distinct leads (k_dense_blk); F4B_DENSE=<any>
+    // keeps the measured alternatives below
+    static const char* dense_sel = getenv("F4B_DENSE");
+    bool blk_done = false;
+    if (!dense_sel && R > 0 && K > 0 && R < (1ll << 30) && K < (1ll << 30)) {
+      static int blk_occ = -1;
+      static bool blk_attr = false;
+      if (!blk_attr) {
+        check_cuda(cudaFuncSetAttribute(k_dense_blk<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024),
+                   "attr");
+        check_cuda(cudaFuncSetAttribute(k_dense_blk<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024),
+                   "attr");
+        blk_attr = true;
+      }
+      const long long rmaxb = std::max<long long>(1, std::min(R, K));
+      long long rpc = std::max<long long>(2, (R + c->num_sms - 1) / c->num_sms);
+      long long G = (R + rpc - 1) / rpc;
+      const long long maxt = rpc + (rmaxb + G - 1) / G;
+      const long long Kp = (K + 3) & ~3ll;
+      const long long maxt3 = maxt + (DB_NP + G - 1) / G;
+      const size_t smem_b = (size_t)std::max<long long>(DB_NP * (DB_W + 32), maxt3 * (DB_NP + 3) + rpc) * 4;
+      (void)Kp;
+      if (blk_occ < 0) {
+        int o = 0;
+        check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_dense_blk<false>, DB_THREADS, 160 * 1024),
+                   "occupancy");
+        blk_occ = o;
+      }
+      if (blk_occ >= 1 && G <= c->num_sms && smem_b <= 160 * 1024 && rpc * K < (1ll << 32)) {
+        DBuf Bm, colp, lead_b, cand_b, gl, gT, stt, ordr;
+        ensure(c, Bm, (size_t)rmaxb * K * sizeof(u32));
+        ensure(c, colp, (size_t)K * sizeof(u32));
+        ensure(c, lead_b, (size_t)R * sizeof(u32));
+        ensure(c, cand_b, DB_NP * sizeof(u32));
+        ensure(c, gl, 2 * DB_NP * sizeof(u32));
+        ensure(c, gT, DB_NP * DB_NP * sizeof(u32));
+        ensure(c, stt, sizeof(DblkState));
+        ensure(c, ordr, (size_t)rmaxb * sizeof(u32));
+        ensure(c, E->Rd, (size_t)rmaxb * K * sizeof(u32));
+        ensure(c, E->dpiv, (size_t)rmaxb * sizeof(u32));
+        ensure(c, E->rdev, 16);
+        check_cuda(cudaMemsetAsync(colp.p, 0xFF, (size_t)K * sizeof(u32), c->stream), "memset");
+        check_cuda(cudaMemsetAsync(stt.p, 0, sizeof(DblkState), c->stream), "memset");
+        fp = make_fp(c);
+        u32* dpp = Dp.as<u32>();
+        u32 Ru = (u32)R, Ku = (u32)K, rpcu = (u32)rpc, maxtu = (u32)maxt3;
+        u32 *leadp = lead_b.as<u32>(), *candp2 = cand_b.as<u32>(), *bmp = Bm.as<u32>(), *colpp = colp.as<u32>();
+        u32 *glp = gl.as<u32>(), *gTp = gT.as<u32>(), *rdp = E->Rd.as<u32>(), *dpivp = E->dpiv.as<u32>();
+        u32 *rkp = E->rdev.as<u32>(), *ordp = ordr.as<u32>();
+        DblkState* sp = reinterpret_cast<DblkState*>(stt.p);
+        void* argsb[] = {&fp, &dpp, &Ru, &Ku, &rpcu, &maxtu, &leadp, &candp2, &bmp, &colpp, &glp, &gTp, &sp, &rdp,
+                         &dpivp, &rkp, &ordp};
+        {
+          ProfScope ps(c, "k_dense_blk");
+          const void* kf = c->p < 65536u ? (const void*)k_dense_blk<true> : (const void*)k_dense_blk<false>;
+          check_cuda(cudaLaunchCooperativeKernel(kf, (int)G, DB_THREADS, argsb, smem_b, c->stream), "k_dense_blk");
+        }
+        static const bool btrace = getenv("F4B_BLK_TRACE") != nullptr;
+        if (btrace) {
+          DblkState hs;
+          check_cuda(cudaMemcpyAsync(&hs, stt.p, sizeof(hs), cudaMemcpyDeviceToHost, c->stream), "d2h");
+          check_cuda(cudaStreamSynchronize(c->stream), "sync");
+          fprintf(stderr, "[blk] R=%lld K=%lld G=%lld rpc=%lld rank=%u iters=%u t2=%uus t3=%uus\n",
+                  (long long)R, (long long)K, (long long)G, (long long)rpc, hs.rho, hs.iters, hs.t2_us, hs.t3_us);
+        }
+        for (DBuf* b : {&Bm, &colp, &lead_b, &cand_b, &gl, &gT, &stt, &ordr}) release(c, *b);
+        blk_done = true;
+      }
+    }
+    if (blk_done) {
+    } else if (rref_on && CHr >= 8 && R < (1ll << 31) && K < (1ll << 30)) {
       const long long rmax = std::max<long long>(1, std::min(R, K));
       const size_t smem_r = (size_t)std::max<long long>(2 * K, CHr * K) * 4;
       static bool rr_attr = false;
@@ -2325,7 +2772,7 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
     // default: rows resident in shared memory (k_dense_fwd_smem) when every
     // SM's row block fits
     static const char* dense_env = getenv("F4B_DENSE");
-    if (!done_cluster && !dense_env) {
+    if (!done_cluster && (!dense_env || !strcmp(dense_env, "smem"))) {
       const size_t Kp = (size_t)((K + 3) & ~3ll);
       static const int ds_cps = getenv("F4B_DS_CPS") ? atoi(getenv("F4B_DS_CPS")) : 1;
       const long long gmax = (long long)c->num_sms * std::max(1, ds_cps);
