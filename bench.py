@@ -320,6 +320,7 @@ class ClockSampler:
 #                                  (pivot rows are reused across C rows, so
 #                                  this stream is L2-served, not HBM)
 #   k_dense_forward              : read + write D' once       8|C|K
+#   k_dense_blk                  : D' read + RREF(D') written 4|C|K + 4 rank(D') K
 SYMBOLIC = ("k_fbsp", "k_rank_", "k_tile_dict", "k_join_gen", "k_os_", "k_small_sort", "k_unique_absent",
             "k_closure", "k_new_rows", "k_merge_corank", "k_rows0", "k_encode_basis", "k_mark_leads", "k_front0",
             "k_dict_exps")
@@ -346,6 +347,10 @@ def kernel_bytes(name, b, pinfo, einfo):
         # C-row share of the nonzeros: |C| rows of mean length M / r
         c_nnz = int(C * M / max(1, b["r"]))
         return 8 * einfo["sweep_tail_nnz"] + 16 * einfo["sweep_pivots"] + 8 * c_nnz + 4 * C * K
+    if name.startswith("k_dense_blk"):
+        # compulsory: D' read once, RREF(D') written once (the per-block
+        # products re-read L2-resident rows and are not credited)
+        return 4 * C * K + 4 * einfo["n_nonpivot_rows"] * K
     if name in ("k_dense_forward", "k_dense_fwd_smem", "k_dense_forward_cta"):
         # D' read into the row state and the pivot rows written back once
         return 8 * C * K
@@ -377,6 +382,9 @@ def roofline_for(kprof, records, peak, peak_src, want):
             out["note"] = ("pivot tails packed once per matrix and L2-resident (reused by every C row); fixed "
                            "32-A-column windows with precomputed block inverses: multipliers from one 32x32 "
                            "product, two CTA barriers per non-empty window, shared-atomic tail application")
+        elif name.startswith("k_dense_blk"):
+            out["note"] = ("latency-bound: RREF(D') in pivot blocks, two grid barriers per block of up to 32 "
+                           "pivots; byte model counts D' read and RREF(D') written once")
         elif name.startswith("k_dense_fwd"):
             out["note"] = ("latency-bound: one grid barrier per pivot of D' (byte model counts D' once; the "
                            "per-pivot row updates stay in shared memory)")

@@ -1892,7 +1892,7 @@ __global__ void __launch_bounds__(RR_THREADS, 1) k_dense_rref(Fp fp, u32* __rest
 // (sparselin.py:337-349).
 // ---------------------------------------------------------------------------
 struct DblkState {
-  u32 cnt, np, rho, rho_old, iters, t2_us, t3_us, pad;  // t*_us: CTA 0 phase times (trace)
+  u32 cnt, np, rho, rho_old, iters, t2_us, t3_us, t3a_us;  // t*_us: CTA 0 phase times (trace)
 };
 F4B_DEV unsigned long long gtimer() {
   unsigned long long t;
@@ -1933,8 +1933,18 @@ __global__ void __launch_bounds__(DB_THREADS) k_dense_blk(Fp fp, u32* __restrict
   u32* s_lead = s_act + maxt;         // [rpc] leads of this CTA's rows
   const u32 lo = bid * rpc;
   const u32 nr = lo < R ? min(rpc, R - lo) : 0u;
+  // coefficients are held in Montgomery form c' = c R.  SMALLP (p < 2^16):
+  // raw products c' v summed in 64 bits (< 32 p^2 < p 2^32) and one REDC
+  // give sum c v mod p; otherwise Montgomery products and one modulo.
   auto prod = [&](u32 c, u32 v) -> u64 { return SMALLP ? (u64)c * v : (u64)fp.mont_mul(c, v); };
-  auto red64 = [&](u64 a) -> u32 { return (u32)(a % p); };
+  auto red64 = [&](u64 a) -> u32 {
+    if (SMALLP) {
+      const u32 m = (u32)a * fp.pprime;
+      const u64 u = (a + (u64)m * p) >> 32;
+      return (u32)(u >= p ? u - p : u);
+    }
+    return (u32)(a % p);
+  };
   auto offer = [&](u32 row) {
     const u32 s = atomicAdd(&st->cnt, 1u);
     if (s < (u32)DB_NP) cand[s] = row;
@@ -1972,7 +1982,7 @@ __global__ void __launch_bounds__(DB_THREADS) k_dense_blk(Fp fp, u32* __restrict
     lead[lo + r] = s_lead[r];
     if (s_lead[r] < K) offer(lo + r);
   }
-  unsigned long long t2 = 0, t3 = 0, tm = 0;
+  unsigned long long t2 = 0, t3 = 0, t3a = 0, tm = 0;
   while (true) {
     grid.sync();  // offers complete, every row of this iteration final
     if (bid == 0 && tid == 0) tm = gtimer();
@@ -2088,7 +2098,7 @@ __global__ void __launch_bounds__(DB_THREADS) k_dense_blk(Fp fp, u32* __restrict
       for (u32 e = tid; e < np * np; e += DB_THREADS) {
         const u32 i = e / np, j = e % np;
         const u32 v = fp.mont_mul(s_dinv[i], s_U[i][DB_NP + s_wrow[j]]);
-        gT[i * DB_NP + j] = SMALLP ? v : fp.to_mont(v);
+        gT[i * DB_NP + j] = fp.to_mont(v);
       }
       if (tid < (int)np) {
         const u32 row = s_crow[s_wrow[tid]], col = c0 + s_wcol[tid];
@@ -2151,13 +2161,14 @@ __global__ void __launch_bounds__(DB_THREADS) k_dense_blk(Fp fp, u32* __restrict
           if (xk && (u32)lane < np) acc += prod(s_T[k][lane], xk);
         }
         m = red64(acc);
-        if (!SMALLP && m) m = fp.to_mont(m);
+        if (m) m = fp.to_mont(m);
       }
       s_c[t * DB_NP + lane] = m;
       if (__ballot_sync(FULL, m != 0) && lane == 0) s_act[atomicAdd(&s_na, 1u)] = t;
     }
     __syncthreads();
     const u32 na = s_na;
+    if (bid == 0 && tid == 0) t3a += gtimer() - tm;
     // one pass over the columns: the block's np rows are loaded once per
     // column (one L2 round trip) and applied to every active task
     for (u32 t = tid; t < nt; t += DB_THREADS) s_f[t] = K;
@@ -2180,11 +2191,18 @@ __global__ void __launch_bounds__(DB_THREADS) k_dense_blk(Fp fp, u32* __restrict
           }
         }
 #pragma unroll
-        for (int j = 0; j < DB_NP; ++j) {
-          if (pv[j]) {
+        for (int r = 0; r < DB_G; ++r) {
+          if ((u32)r < ng) {
+            // coefficients past np are zero (lanes >= np wrote 0)
+            const uint4* cr = reinterpret_cast<const uint4*>(s_c + s_act[g0 + r] * DB_NP);
+            u64 a = 0;
 #pragma unroll
-            for (int r = 0; r < DB_G; ++r)
-              if ((u32)r < ng) acc[r] += prod(s_c[s_act[g0 + r] * DB_NP + j], pv[j]);
+            for (int j4 = 0; j4 < DB_NP / 4; ++j4) {
+              const uint4 cv = cr[j4];
+              a += prod(cv.x, pv[4 * j4]) + prod(cv.y, pv[4 * j4 + 1]) + prod(cv.z, pv[4 * j4 + 2]) +
+                   prod(cv.w, pv[4 * j4 + 3]);
+            }
+            acc[r] = a;
           }
         }
 #pragma unroll
@@ -2221,6 +2239,7 @@ __global__ void __launch_bounds__(DB_THREADS) k_dense_blk(Fp fp, u32* __restrict
     if (tid == 0) {
       st->t2_us = (u32)(t2 / 1000);
       st->t3_us = (u32)(t3 / 1000);
+      st->t3a_us = (u32)(t3a / 1000);
     }
     u32 base = 0;
     for (u32 q0 = 0; q0 < K; q0 += DB_THREADS) {
@@ -2664,8 +2683,9 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
           DblkState hs;
           check_cuda(cudaMemcpyAsync(&hs, stt.p, sizeof(hs), cudaMemcpyDeviceToHost, c->stream), "d2h");
           check_cuda(cudaStreamSynchronize(c->stream), "sync");
-          fprintf(stderr, "[blk] R=%lld K=%lld G=%lld rpc=%lld rank=%u iters=%u t2=%uus t3=%uus\n",
-                  (long long)R, (long long)K, (long long)G, (long long)rpc, hs.rho, hs.iters, hs.t2_us, hs.t3_us);
+          fprintf(stderr, "[blk] R=%lld K=%lld G=%lld rpc=%lld rank=%u iters=%u t2=%uus t3=%uus (setup %uus)\n",
+                  (long long)R, (long long)K, (long long)G, (long long)rpc, hs.rho, hs.iters, hs.t2_us, hs.t3_us,
+                  hs.t3a_us);
         }
         for (DBuf* b : {&Bm, &colp, &lead_b, &cand_b, &gl, &gT, &stt, &ordr}) release(c, *b);
         blk_done = true;
