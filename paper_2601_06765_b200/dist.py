@@ -13,7 +13,12 @@ What shards and how:
   (``allgather_arrays``) and merged redundantly on every rank
   (``merge_key_runs``) into the identical global dictionary; concatenating
   the per-rank CSR slices in rank order reproduces the global CSR
-  (``concat_csr``).
+  (``concat_csr``);
+* Block Wiedemann on G ranks (§8e): the b block columns of each round are
+  dealt round-robin (``shard_round_robin``); every rank runs its columns'
+  Krylov sequences, Berlekamp-Massey and generator evaluations on its own
+  resident operator, and only the candidate kernel vectors are all-gathered
+  once per round (``sparselin._kernel_rounds``).
 
 Everything here is compute-agnostic host logic; the per-rank compute is the
 CUDA engine (``engine.Engine``) on that rank's device.
@@ -38,6 +43,17 @@ def rank_info() -> RankInfo:
     """RANK / WORLD_SIZE / LOCAL_RANK as set by torch.distributed.run."""
     return RankInfo(int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
                     int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def active_world() -> tuple:
+    """(rank, world) of the initialised default process group, else (0, 1)."""
+    try:
+        import torch.distributed as dist
+    except ImportError:  # pragma: no cover
+        return 0, 1
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_rank(), dist.get_world_size()
+    return 0, 1
 
 
 def init(backend: str | None = None):

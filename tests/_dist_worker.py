@@ -54,3 +54,85 @@ def run(rank, world, port, snap_name, step, out_dir):
         fh.write(f"{int(ok)} {lo} {hi} {len(gdict)} {len(full['dict_keys'])}\n")
     dist.barrier()
     dist.destroy_process_group()
+
+
+class NumpyKrylovOperator:
+    """Test stand-in for the device operator (engine.DeviceOperator): B = A
+    (square) or AᵀA, dense NumPy mod p, with the reference loop semantics
+    (sparselin.py:482-528).  Test infrastructure only: it lets the multi-rank
+    Block Wiedemann control flow run on CPU ranks."""
+
+    def __init__(self, A, p):
+        self.A = np.asarray(A, dtype=np.uint64)
+        self.p = np.uint64(p)
+        self.square = self.A.shape[0] == self.A.shape[1]
+        self.dim = self.A.shape[1]
+
+    def apply(self, X):
+        Y = self.A @ X % self.p
+        return Y if self.square else self.A.T @ Y % self.p
+
+    def krylov(self, U, V, steps):
+        W = np.array(V, dtype=np.uint64)
+        out = np.empty((steps, W.shape[1]), dtype=np.uint64)
+        for k in range(steps):
+            out[k] = (U * W % self.p).sum(axis=0, dtype=np.uint64) % self.p
+            W = self.apply(W)
+        return out
+
+    def horner(self, g, v):
+        v = np.asarray(v, dtype=np.uint64).reshape(-1, 1)
+        acc = np.uint64(g[-1]) * v % self.p
+        for c in list(g[:-1])[::-1]:
+            acc = (self.apply(acc) + np.uint64(c) * v) % self.p
+        return acc[:, 0]
+
+    def power_until_zero(self, v, max_steps):
+        acc = np.asarray(v, dtype=np.uint64).reshape(-1, 1)
+        taken = 0
+        for _ in range(max_steps):
+            nxt = self.apply(acc)
+            if (nxt == 0).all():
+                break
+            acc = nxt
+            taken += 1
+        return acc[:, 0], taken
+
+
+def wiedemann_case(p=31, seed=7):
+    """A rank-deficient 40 x 30 matrix (rank 20) over F_p."""
+    rng = np.random.default_rng(seed)
+    L = rng.integers(0, p, (40, 20), dtype=np.uint64)
+    R = rng.integers(0, p, (20, 30), dtype=np.uint64)
+    return L @ R % np.uint64(p)
+
+
+def wiedemann_rounds(A, p, rank, world, seed=3, target=6):
+    import oracle
+    from paper_2601_06765_b200.sparselin import _kernel_rounds
+
+    op = NumpyKrylovOperator(A, p)
+
+    def bm(seqs):
+        return [oracle.berlekamp_massey(seqs[:, k].tolist(), p) for k in range(seqs.shape[1])]
+
+    def check(w):
+        return not (A @ w % np.uint64(p)).any()
+
+    return _kernel_rounds(op, bm, check, A.shape[1], p, seed, 4, target, 12, 3, rank, world)
+
+
+def run_wiedemann(rank, world, port, out_dir):
+    os.environ.update(RANK=str(rank), WORLD_SIZE=str(world), LOCAL_RANK=str(rank), MASTER_ADDR="127.0.0.1",
+                      MASTER_PORT=str(port))
+    from paper_2601_06765_b200 import dist as pdist
+
+    info = pdist.init("gloo")
+    assert pdist.active_world() == (rank, world) == (info.rank, info.world)
+    p = 31
+    vectors, trail = wiedemann_rounds(wiedemann_case(p), p, rank, world)
+    np.save(os.path.join(out_dir, f"wied_rank{rank}.npy"), np.array(vectors, dtype=np.uint64))
+    import torch.distributed as dist
+
+    dist.barrier()
+    dist.destroy_process_group()

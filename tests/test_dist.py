@@ -59,3 +59,24 @@ def test_fbsp_join_world2_gloo(tmp_path, snap, step):
     for r in range(world):
         ok, lo, hi, n, nfull = (tmp_path / f"rank{r}.txt").read_text().split()
         assert ok == "1", f"rank {r}: distributed plan differs (rows {lo}:{hi}, N {n} vs {nfull})"
+
+
+def test_block_wiedemann_columns_world2_gloo(tmp_path):
+    """§8e Block Wiedemann: the b block columns dealt over 2 ranks, candidates
+    all-gathered once per round; every rank ends with the single-rank
+    vectors, in the same order, all in ker(A)."""
+    import torch.multiprocessing as mp
+
+    import _dist_worker
+
+    p = 31
+    A = _dist_worker.wiedemann_case(p)
+    single, _ = _dist_worker.wiedemann_rounds(A, p, 0, 1)
+    assert single, "expected kernel vectors"
+    for w in single:
+        assert not (A @ w % np.uint64(p)).any()
+    world = 2
+    mp.spawn(_dist_worker.run_wiedemann, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    for r in range(world):
+        got = np.load(tmp_path / f"wied_rank{r}.npy")
+        assert np.array_equal(got, np.array(single, dtype=np.uint64))
