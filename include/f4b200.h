@@ -163,6 +163,26 @@ int f4b_spmm(f4b_ctx* ctx, int64_t n_rows, int64_t n_cols, const int64_t* row_pt
              const int64_t* col_ind, const uint64_t* val, const uint64_t* X, int64_t b,
              uint64_t* Y);
 
+/* ---- isolated primitives of the reference microbenchmarks (bench.py:244-300) ----
+ * DEVICE pointers (e.g. torch tensors); synchronous on the context stream.
+ *
+ * f4b_dict_build replaces radix_sort + unique_sorted (bulk.py:86-124, :135-150)
+ * as called by microbench("dict_build") (bench.py:253-256): keys [n][words]
+ * (words in {1,2}, every word < 2^key_bits) -> ascending unique keys in
+ * out [n_unique][words] (out must hold n keys). */
+int f4b_dict_build(f4b_ctx* ctx, const uint64_t* keys, int64_t n, int words, int key_bits,
+                   uint64_t* out, int64_t* n_unique);
+/* f4b_join_index replaces merge_join_index (bulk.py:207-241), microbench
+ * ("row_assemble") (bench.py:278-282): pos[i] = index of keys[i] in the ascending
+ * dictionary dict [n_dict][words] (words 1..4); F4B_ERR_MISSING_KEY on a miss. */
+int f4b_join_index(f4b_ctx* ctx, const uint64_t* dict, int64_t n_dict, const uint64_t* keys,
+                   int64_t n, int words, int64_t* pos);
+/* f4b_mod_fma: out = (acc + a b) mod p (fp.py:335-400 KernelArith lazy
+ * multiply-add; microbench("mod_fma"), bench.py:293-300); 3 <= p < 2^31,
+ * inputs < p, 16-byte aligned buffers. */
+int f4b_mod_fma(f4b_ctx* ctx, uint32_t p, const uint64_t* a, const uint64_t* b,
+                const uint64_t* acc, int64_t n, uint64_t* out);
+
 /* berlekamp_massey (sparselin.py:377-413) for b sequences of length len
  * (seqs [b][len] u64 residues) side by side, one CTA per sequence: polys
  * [b][len + 1] receives each minimal polynomial ascending and monic

@@ -87,6 +87,10 @@ SIGNATURES = {
     "f4b_echelon_pivot_cols": (C.c_int, [C.c_void_p, i64p]),
     "f4b_echelon_free": (C.c_int, [C.c_void_p]),
     "f4b_spmm": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, i64p, i64p, u64p, u64p, C.c_int64, u64p]),
+    "f4b_dict_build": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_void_p, i64p]),
+    "f4b_join_index": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int, C.c_void_p]),
+    "f4b_mod_fma": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
+                              C.c_void_p]),
 }
 
 

@@ -913,6 +913,30 @@ int f4b_spmm(f4b_ctx* h, int64_t n_rows, int64_t n_cols, const int64_t* row_ptr,
   API_END
 }
 
+int f4b_dict_build(f4b_ctx* h, const uint64_t* keys, int64_t n, int words, int key_bits, uint64_t* out,
+                   int64_t* n_unique) {
+  if (!h || !n_unique) return F4B_ERR_PRECONDITION;
+  API_BEGIN(&h->c)
+  *n_unique = dict_build(_c, keys, n, words, key_bits, out);
+  API_END
+}
+
+int f4b_join_index(f4b_ctx* h, const uint64_t* dict, int64_t n_dict, const uint64_t* keys, int64_t n, int words,
+                   int64_t* pos) {
+  if (!h) return F4B_ERR_PRECONDITION;
+  API_BEGIN(&h->c)
+  join_index(_c, dict, n_dict, keys, n, words, pos);
+  API_END
+}
+
+int f4b_mod_fma(f4b_ctx* h, uint32_t p, const uint64_t* a, const uint64_t* b, const uint64_t* acc, int64_t n,
+                uint64_t* out) {
+  if (!h) return F4B_ERR_PRECONDITION;
+  API_BEGIN(&h->c)
+  mod_fma(_c, p, a, b, acc, n, out);
+  API_END
+}
+
 }  // extern "C"
 
 void f4b::basis_finish(Ctx* c) { basis_finish_impl(c); }

@@ -206,4 +206,10 @@ void echelon_release(f4b_echelon* E);
 void echelon_pivot_cols(const f4b_echelon* E, int64_t* cols);
 void spmm(Ctx* c, long long r, long long N, const int64_t* rp, const int64_t* col, const uint64_t* val,
           const uint64_t* X, long long b, uint64_t* Y);
+// micro.cu: the reference microbenchmark primitives on device buffers
+long long dict_build(Ctx* c, const uint64_t* keys, long long n, int words, int key_bits, uint64_t* out);
+void join_index(Ctx* c, const uint64_t* dict, long long nd, const uint64_t* keys, long long n, int words,
+                int64_t* pos);
+void mod_fma(Ctx* c, uint32_t p, const uint64_t* a, const uint64_t* b, const uint64_t* acc, long long n,
+             uint64_t* out);
 }  // namespace f4b

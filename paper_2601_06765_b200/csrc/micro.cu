@@ -1,0 +1,182 @@
+// The three isolated primitives of the reference's microbenchmarks
+// (reference src/bench.py:244-300 `microbench`), on device-resident buffers:
+//
+//   f4b_dict_build  radix_sort + unique_sorted of W-word keys
+//                   (bulk.py:86-124, :135-150): the words are packed into one
+//                   order-isomorphic device key of W * key_bits bits (reference
+//                   keys are 48-bit words, bench.py:237-241), sorted with the
+//                   one-sweep LSD radix sort of radix.cu (W * key_bits / 8
+//                   passes instead of the reference's 8 W), uniqued and
+//                   unpacked back to W words.
+//   f4b_join_index  merge_join_index (bulk.py:207-241): position of each key in
+//                   an ascending dictionary, MissingKeyError on a miss.
+//   f4b_mod_fma     acc + a b mod p, the KernelArith lazy multiply-add
+//                   (fp.py:335-400), here with a 64-bit Barrett reduction.
+//
+// All three are HBM-bound streams; the roofline is the copy bandwidth.
+#include "common.cuh"
+#include "engine.h"
+
+namespace f4b {
+
+static constexpr int MB_THREADS = 256;
+
+// Pack W <= 2 words of `kb` significant bits into one Key<2> (big-endian
+// words): value = w0 * 2^kb + w1 (W = 2) or w0 (W = 1, stored in w[1]).
+__global__ void __launch_bounds__(MB_THREADS) k_mb_pack(const u64* __restrict__ in, long long n, int words, int kb,
+                                                        u64* __restrict__ out, u32* __restrict__ err) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const u64 lim = kb >= 64 ? ~0ull : ((1ull << kb) - 1);
+  bool bad = false;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    u64 hi = 0, lo;
+    if (words == 2) {
+      const ulonglong2 v = __ldcs(reinterpret_cast<const ulonglong2*>(in) + i);
+      bad |= (v.x > lim) | (v.y > lim);
+      lo = kb >= 64 ? v.y : (v.y | (v.x << kb));
+      hi = kb >= 64 ? v.x : (kb == 0 ? 0 : (v.x >> (64 - kb)));
+    } else {
+      lo = __ldcs(in + i);
+      bad |= lo > lim;
+    }
+    __stcs(reinterpret_cast<ulonglong2*>(out) + i, make_ulonglong2(hi, lo));
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(err, 1u);
+}
+
+__global__ void __launch_bounds__(MB_THREADS) k_mb_unpack(const u64* __restrict__ in, const u32* __restrict__ d_n,
+                                                          int words, int kb, u64* __restrict__ out) {
+  const long long n = *d_n;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const u64 lim = kb >= 64 ? ~0ull : ((1ull << kb) - 1);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const ulonglong2 v = reinterpret_cast<const ulonglong2*>(in)[i];
+    if (words == 2) {
+      const u64 w1 = v.y & lim;
+      const u64 w0 = kb >= 64 ? v.x : ((v.y >> kb) | (kb == 0 ? 0 : (v.x << (64 - kb))));
+      reinterpret_cast<ulonglong2*>(out)[i] = make_ulonglong2(w0, w1);
+    } else {
+      out[i] = v.y;
+    }
+  }
+}
+
+// Lower bound of each query in an ascending W-word dictionary.  Queries of a
+// warp are usually close in key order (row segments are sorted), so the
+// upper levels of the search are shared L1/L2 hits.
+template <int KW>
+__global__ void __launch_bounds__(MB_THREADS) k_mb_join(const u64* __restrict__ dict, u32 nd,
+                                                        const u64* __restrict__ q, long long n,
+                                                        long long* __restrict__ pos, u32* __restrict__ err) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  bool miss = false;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    Key<KW> k;
+#pragma unroll
+    for (int j = 0; j < KW; ++j) k.w[j] = __ldcs(q + i * KW + j);
+    u32 lo = 0, hi = nd;
+    while (lo < hi) {
+      const u32 mid = (lo + hi) >> 1;
+      Key<KW> m;
+#pragma unroll
+      for (int j = 0; j < KW; ++j) m.w[j] = __ldg(dict + (size_t)mid * KW + j);
+      if (key_lt<KW>(m, k)) lo = mid + 1; else hi = mid;
+    }
+    bool hit = lo < nd;
+    if (hit) {
+#pragma unroll
+      for (int j = 0; j < KW; ++j) hit &= __ldg(dict + (size_t)lo * KW + j) == k.w[j];
+    }
+    miss |= !hit;
+    __stcs(pos + i, (long long)lo);
+  }
+  if (__any_sync(0xffffffffu, miss) && (threadIdx.x & 31) == 0) atomicOr(err, 1u);
+}
+
+// out = (acc + a b) mod p, p < 2^31, inputs < 2^31 (a b + acc < 2^63).
+// Barrett with mu = floor((2^64 - 1) / p): the quotient estimate is short by
+// at most 2.
+F4B_DEV u64 mb_reduce(u64 x, u64 p, u64 mu) {
+  u64 r = x - __umul64hi(x, mu) * p;
+  r = r >= p ? r - p : r;
+  return r >= p ? r - p : r;
+}
+
+__global__ void __launch_bounds__(MB_THREADS) k_mb_fma(const u64* __restrict__ a, const u64* __restrict__ b,
+                                                       const u64* __restrict__ acc, long long n, u64 p, u64 mu,
+                                                       u64* __restrict__ out) {
+  const long long n2 = n / 2;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const ulonglong2* a2 = reinterpret_cast<const ulonglong2*>(a);
+  const ulonglong2* b2 = reinterpret_cast<const ulonglong2*>(b);
+  const ulonglong2* c2 = reinterpret_cast<const ulonglong2*>(acc);
+  ulonglong2* o2 = reinterpret_cast<ulonglong2*>(out);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += stride) {
+    const ulonglong2 x = __ldcs(a2 + i), y = __ldcs(b2 + i), z = __ldcs(c2 + i);
+    __stcs(o2 + i, make_ulonglong2(mb_reduce(z.x + x.x * y.x, p, mu), mb_reduce(z.y + x.y * y.y, p, mu)));
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0)
+    out[n - 1] = mb_reduce(acc[n - 1] + a[n - 1] * b[n - 1], p, mu);
+}
+
+static unsigned mb_grid(Ctx* c, long long n) {
+  const long long want = (n + MB_THREADS - 1) / MB_THREADS;
+  return (unsigned)std::max<long long>(1, std::min<long long>(want, (long long)c->num_sms * 8));
+}
+
+long long dict_build(Ctx* c, const uint64_t* keys, long long n, int words, int key_bits, uint64_t* out) {
+  if (n < 0 || n >= (1ll << 32) - 2 || (words != 1 && words != 2) || key_bits < 1 || key_bits > 64)
+    fail(F4B_ERR_PRECONDITION, "dict_build: 0 <= n < 2^32 - 2, words in {1, 2}, 1 <= key_bits <= 64");
+  if (n == 0) return 0;
+  DBuf packed, uniq, flags;
+  ensure(c, packed, (size_t)n * 16);
+  ensure(c, uniq, (size_t)(n + 1) * 16);
+  ensure(c, flags, 16);
+  u32* err = flags.as<u32>();
+  u32* d_count = err + 1;
+  memset_async(c, err, 0, 8);
+  F4B_LAUNCH(c, k_mb_pack, mb_grid(c, n), MB_THREADS, 0, keys, n, words, key_bits, packed.as<u64>(), err);
+  sort_unique(c, 2, packed.as<u64>(), nullptr, (u32)n, words * key_bits, nullptr, nullptr, uniq.as<u64>(), d_count);
+  F4B_LAUNCH(c, k_mb_unpack, mb_grid(c, n), MB_THREADS, 0, uniq.as<u64>(), d_count, words, key_bits, out);
+  const u32 bad = read_u32(c, err);
+  const long long nu = read_u32(c, d_count);
+  release(c, packed);
+  release(c, uniq);
+  release(c, flags);
+  if (bad) fail(F4B_ERR_PRECONDITION, "dict_build: a key word has more than key_bits significant bits");
+  return nu;
+}
+
+void join_index(Ctx* c, const uint64_t* dict, long long nd, const uint64_t* keys, long long n, int words,
+                int64_t* pos) {
+  if (n < 0 || nd < 0 || nd >= (1ll << 32) - 1 || words < 1 || words > 4)
+    fail(F4B_ERR_PRECONDITION, "join_index: bad sizes");
+  if (n == 0) return;
+  DBuf flags;
+  ensure(c, flags, 16);
+  u32* err = flags.as<u32>();
+  memset_async(c, err, 0, 4);
+  const unsigned g = mb_grid(c, n);
+  long long* p = reinterpret_cast<long long*>(pos);
+  switch (words) {
+    case 1: F4B_LAUNCH(c, k_mb_join<1>, g, MB_THREADS, 0, dict, (u32)nd, keys, n, p, err); break;
+    case 2: F4B_LAUNCH(c, k_mb_join<2>, g, MB_THREADS, 0, dict, (u32)nd, keys, n, p, err); break;
+    case 3: F4B_LAUNCH(c, k_mb_join<3>, g, MB_THREADS, 0, dict, (u32)nd, keys, n, p, err); break;
+    default: F4B_LAUNCH(c, k_mb_join<4>, g, MB_THREADS, 0, dict, (u32)nd, keys, n, p, err); break;
+  }
+  const u32 miss = read_u32(c, err);
+  release(c, flags);
+  if (miss) fail(F4B_ERR_MISSING_KEY, "join_index: a key is absent from the dictionary");
+}
+
+void mod_fma(Ctx* c, uint32_t p, const uint64_t* a, const uint64_t* b, const uint64_t* acc, long long n,
+             uint64_t* out) {
+  if (n < 0 || p < 3 || p >= (1u << 31)) fail(F4B_ERR_PRECONDITION, "mod_fma: 3 <= p < 2^31");
+  if (n == 0) return;
+  if (((uintptr_t)a | (uintptr_t)b | (uintptr_t)acc | (uintptr_t)out) & 15)
+    fail(F4B_ERR_PRECONDITION, "mod_fma: buffers must be 16-byte aligned");
+  const u64 mu = ~0ull / p;
+  F4B_LAUNCH(c, k_mb_fma, mb_grid(c, (n + 1) / 2), MB_THREADS, 0, a, b, acc, n, (u64)p, mu, out);
+}
+
+}  // namespace f4b

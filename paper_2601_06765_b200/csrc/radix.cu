@@ -22,11 +22,17 @@ namespace f4b {
 
 static constexpr int OS_THREADS = 256;
 static constexpr int OS_WARPS = OS_THREADS / 32;
+static constexpr int OS_MAX_PASSES = 16;  // 128-bit keys; tickets[32]: one per pass + the unique kernel's
 
 template <int KW>
 struct OsItems {
   static constexpr int value = KW >= 4 ? 4 : (KW == 2 ? 8 : 16);
 };
+
+// tiles of at most 32 KB of keys are reordered in shared memory before the
+// scatter (static shared memory stays under 48 KB)
+template <int KW>
+constexpr bool OS_STAGED = (size_t)KW * 8 * OS_THREADS * OsItems<KW>::value <= 32768;
 
 template <int KW>
 struct SmallCfg {  // single-CTA sort: 512 threads
@@ -43,10 +49,10 @@ F4B_DEV bool skip_large(u32 n, u32 small_cap) { return small_cap && n <= small_c
 template <int KW>
 __global__ void __launch_bounds__(OS_THREADS) k_os_hist(const u64* __restrict__ in, const u32* d_n, u32 n_host,
                                                         int npass, u32* __restrict__ hist, u32 small_cap) {
-  __shared__ u32 h[8][256];
+  __shared__ u32 h[OS_MAX_PASSES][256];
   const u32 n = dev_n(d_n, n_host);
   if (skip_large(n, small_cap)) return;
-  for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) (&h[0][0])[i] = 0;
+  for (int i = threadIdx.x; i < npass * 256; i += blockDim.x) (&h[0][0])[i] = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31;
   for (long long base = (long long)blockIdx.x * blockDim.x; base < n; base += (long long)gridDim.x * blockDim.x) {
@@ -76,6 +82,8 @@ __global__ void __launch_bounds__(OS_THREADS) k_os_pass(const u64* __restrict__ 
   constexpr int TILE = OS_THREADS * ITEMS;
   __shared__ u32 wh[OS_WARPS][256];
   __shared__ u32 gbase[256];
+  __shared__ u32 s_toff[OS_STAGED<KW> ? 256 : 1];
+  __shared__ Key<KW> s_keys[OS_STAGED<KW> ? TILE : 1];
   __shared__ u32 ws[33];
   __shared__ u32 s_tile;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -142,12 +150,35 @@ __global__ void __launch_bounds__(OS_THREADS) k_os_pass(const u64* __restrict__ 
       atomicExch(st + (size_t)tile * 256, LB_PRE | (excl + run));
     }
     gbase[d] += excl;
+    if constexpr (OS_STAGED<KW>) {
+      // tile-local digit offsets: the tile is reordered by digit in shared
+      // memory, then written out in consecutive runs per digit (coalesced
+      // stores instead of one 8/16-byte scatter per key)
+      u32 tot;
+      const u32 toff = block_scan_excl(run, ws, &tot);
+      s_toff[d] = toff;
+      gbase[d] -= toff;  // global position = gbase[d] + tile-local position
+    }
   }
   __syncthreads();
+  if constexpr (OS_STAGED<KW>) {
 #pragma unroll
-  for (int it = 0; it < ITEMS; ++it) {
-    const long long idx = wbase + it * 32 + lane;
-    if (idx < n) key_store<KW>(out, (long long)gbase[dig[it]] + wh[warp][dig[it]] + rank[it], k[it]);
+    for (int it = 0; it < ITEMS; ++it) {
+      const long long idx = wbase + it * 32 + lane;
+      if (idx < n) s_keys[s_toff[dig[it]] + wh[warp][dig[it]] + rank[it]] = k[it];
+    }
+    __syncthreads();
+    const u32 tile_n = (u32)min((long long)TILE, (long long)n - (long long)tile * TILE);
+    for (u32 i = threadIdx.x; i < tile_n; i += OS_THREADS) {
+      const Key<KW> kk = s_keys[i];
+      key_store<KW>(out, (long long)gbase[key_digit<KW>(kk, bit)] + i, kk);
+    }
+  } else {
+#pragma unroll
+    for (int it = 0; it < ITEMS; ++it) {
+      const long long idx = wbase + it * 32 + lane;
+      if (idx < n) key_store<KW>(out, (long long)gbase[dig[it]] + wh[warp][dig[it]] + rank[it], k[it]);
+    }
   }
 }
 
@@ -260,14 +291,15 @@ static void sort_unique_t(Ctx* c, const u64* in, const u32* d_n, u32 n_max, int 
   const u32 small_cap = d_n ? (u32)SmallCfg<KW>::CAP : 0u;
   constexpr int TILE = OS_THREADS * OsItems<KW>::value;
   const int npass = (bits + 7) / 8;
+  if (npass > OS_MAX_PASSES || bits > 64 * KW) fail(F4B_ERR_PRECONDITION, "sort_unique: too many key bits");
   const u32 tiles = (n_max + TILE - 1) / TILE;
   const u32 utiles = (n_max + OS_THREADS * 8 - 1) / (OS_THREADS * 8);
-  // scratch: hist[npass*256] | tickets[16] | status[npass*tiles*256] | ustatus[utiles]
-  const size_t words = (size_t)npass * 256 + 16 + (size_t)npass * tiles * 256 + utiles + 16;
+  // scratch: hist[npass*256] | tickets[32] | status[npass*tiles*256] | ustatus[utiles]
+  const size_t words = (size_t)npass * 256 + 32 + (size_t)npass * tiles * 256 + utiles + 16;
   ensure(c, c->sort_hist, words * 4);
   u32* hist = c->sort_hist.as<u32>();
   u32* tickets = hist + npass * 256;
-  u32* status = tickets + 16;
+  u32* status = tickets + 32;
   u32* ustatus = status + (size_t)npass * tiles * 256;
   check_cuda(cudaMemsetAsync(hist, 0, words * 4, c->stream), "memset sort scratch");
   ensure(c, c->sort_a, (size_t)(n_max + 1) * KW * 8);
@@ -283,7 +315,7 @@ static void sort_unique_t(Ctx* c, const u64* in, const u32* d_n, u32 n_max, int 
     src = dst;
   }
   F4B_LAUNCH(c, k_unique_absent<KW>, utiles, OS_THREADS, 0, src, d_n, n_max, dict, d_ndict, out, ustatus,
-             tickets + 15, d_count, small_cap);
+             tickets + 31, d_count, small_cap);
 }
 
 void sort_unique(Ctx* c, int KW, const uint64_t* in, const uint32_t* d_n, uint32_t n_max, int bits,
