@@ -400,6 +400,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--no-micro", action="store_true", help="skip the primitive microbenchmarks")
     ap.add_argument("--no-katsura11", action="store_true",
                     help="skip the full Katsura-11 run reported next to the line (rank 0, after the timed region)")
     args = ap.parse_args()
@@ -590,6 +591,23 @@ def main():
                "sha256": __import__("hashlib").sha256(format_system(kring, kgb).encode()).hexdigest(),
                "reference": "does not finish (SURVEY.md 6.2: step 4 alone 1,556 s)"}
 
+    # kernel capability at large M: the reference's own microbenchmarks
+    # (fpgb.bench.microbench, SURVEY.md §8d "synthetic dict_build") on the
+    # device primitives, inputs resident in HBM (larger than L2)
+    micro = None
+    if rank == 0 and not args.no_micro:
+        from paper_2601_06765_b200.bench import microbench
+
+        micro = []
+        for kind, size, dup in (("dict_build", 1 << 24, 0.5), ("dict_build", 1 << 24, 0.99),
+                                ("row_assemble", 1 << 24, 0.0), ("mod_fma", 1 << 26, 0.0)):
+            m = microbench(kind, size, dup, seed=0)
+            keep = ("kind", "size", "duplicate_rate", "unique_out", "radix_passes", "keys_per_s", "joins_per_s",
+                    "updates_per_s.barrett", "algorithmic_bytes", "hbm_frac", "hbm_frac_per_pass")
+            ent = {k: m[k] for k in keep if k in m}
+            ent["us"] = round(m.get("elapsed_ns", m.get("elapsed_ns.barrett", 0)) / 1e3, 1)
+            micro.append(ent)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         s = cpu_sample()
@@ -614,6 +632,7 @@ def main():
             "gpu_launches": launches1 - launches0, "wall_ms_per_step": 1000 * wall / args.steps,
             "debug_slowest": (sorted(_dbg, key=lambda x: -(x[1] + x[2]))[:8] if _dbg else None),
             "setup_s": round(setup_s, 2), "full_run": full_run, "full_run_katsura11": k11, "kernels_top": kernels,
+            "microbench": micro,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -83,7 +83,13 @@ F4B_HD Key<KW> key_sub(const Key<KW>& a, const Key<KW>& b) {
 // 8-bit digit at bit offset `bit` counted from the least significant end.
 template <int KW>
 F4B_HD u32 key_digit(const Key<KW>& k, int bit) {
-  return (u32)((k.w[KW - 1 - (bit >> 6)] >> (bit & 63)) & 0xFFu);
+  // select the word without a dynamic index (a runtime k.w[...] index puts the
+  // key array in local memory)
+  const int wsel = KW - 1 - (bit >> 6);
+  u64 w = k.w[0];
+#pragma unroll
+  for (int j = 1; j < KW; ++j) w = (j == wsel) ? k.w[j] : w;
+  return (u32)((w >> (bit & 63)) & 0xFFu);
 }
 
 template <int KW>
