@@ -132,6 +132,7 @@ def microbench(kind: str, size: int, duplicate_rate: float = 0.5, seed: int = 0,
 
     if size < 1:
         raise PreconditionError("size must be >= 1")
+    _ctx(device)  # DeviceError without a GPU or the library: no CPU fallback
     rng = np.random.default_rng(seed)
     peak = hbm_peak_gbs()
     out = {"kind": kind, "size": size, "seed": seed, "device": "cuda"}

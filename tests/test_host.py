@@ -200,3 +200,24 @@ def test_compat_shim_rebinds_reference_names():
     assert g.csr_from_plan is sparselin.csr_from_plan
     compat.uninstall(fake)
     assert (g.compile_batch, g.csr_from_plan, g.psge_reduce) == (1, 2, 3)
+
+
+def test_microbench_host_logic_and_no_cpu_fallback():
+    """The microbench inputs follow the reference generator (bench.py:237-241:
+    pool of round(size*(1-dup)) 48-bit keys, uniform picks) and the host check
+    equals np.unique; without a GPU the device primitives raise (no fallback)."""
+    import numpy as np
+
+    from paper_2601_06765_b200 import bench as mb
+    from paper_2601_06765_b200.errors import DeviceError
+
+    k = mb._synth_keys(np.random.default_rng(5), 10_000, 0.9)
+    assert k.shape == (10_000, 2) and k.dtype == np.uint64 and int(k.max()) < 1 << 48
+    assert len(np.unique(k, axis=0)) <= 1000
+    assert np.array_equal(mb._host_unique(k), np.unique(k, axis=0))
+    assert len(mb._synth_keys(np.random.default_rng(1), 5000, 1.0)) == 5000
+    import torch
+
+    if not torch.cuda.is_available():
+        with pytest.raises(DeviceError):
+            mb.microbench("mod_fma", 16)
