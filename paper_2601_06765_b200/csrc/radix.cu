@@ -136,13 +136,25 @@ __global__ void __launch_bounds__(OS_THREADS, KW == 1 ? 3 : (OS_STAGED<KW> ? 4 :
       atomicExch(st, LB_PRE | run);
     } else {
       atomicExch(st + (size_t)tile * 256, LB_AGG | run);
+      // look back 4 predecessors per round trip (independent loads in
+      // flight); a not-yet-published one is polled again
       long long j = (long long)tile - 1;
-      while (j >= 0) {
-        const u32 s = ld_volatile(st + (size_t)j * 256);
-        if ((s & ~LB_VAL) == 0) continue;
-        excl += s & LB_VAL;
-        if ((s & ~LB_VAL) == LB_PRE) break;
-        --j;
+      bool done = false;
+      while (!done) {
+        u32 sv[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) sv[q] = j - q >= 0 ? ld_volatile(st + (size_t)(j - q) * 256) : LB_PRE;
+        int q = 0;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          if (done || q < t) continue;
+          const u32 flag = sv[t] & ~LB_VAL;
+          if (flag == 0) continue;  // not published: poll again from j - t
+          excl += sv[t] & LB_VAL;
+          q = t + 1;
+          done = flag == LB_PRE;
+        }
+        j -= q;
       }
       __threadfence();
       atomicExch(st + (size_t)tile * 256, LB_PRE | (excl + run));
