@@ -61,14 +61,26 @@ F4B_DEV u32 lookback_prefix(u32* status, u32 tile, u32 count) {
     return 0;
   }
   atomicExch(status + tile, LB_AGG | count);
+  // 4 predecessors per round trip (independent loads in flight); one not
+  // yet published is polled again
   u32 excl = 0;
   long long j = (long long)tile - 1;
-  while (j >= 0) {
-    u32 s = ld_volatile(status + j);
-    if ((s & ~LB_VAL) == 0) continue;  // not ready yet: spin
-    excl += s & LB_VAL;
-    if ((s & ~LB_VAL) == LB_PRE) break;
-    --j;
+  bool done = false;
+  while (!done) {
+    u32 sv[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) sv[q] = j - q >= 0 ? ld_volatile(status + (j - q)) : LB_PRE;
+    int q = 0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      if (done || q < t) continue;
+      const u32 flag = sv[t] & ~LB_VAL;
+      if (flag == 0) continue;
+      excl += sv[t] & LB_VAL;
+      q = t + 1;
+      done = flag == LB_PRE;
+    }
+    j -= q;
   }
   __threadfence();
   atomicExch(status + tile, LB_PRE | (excl + count));

@@ -22,6 +22,7 @@ namespace f4b {
 
 static constexpr int OS_THREADS = 256;
 static constexpr int OS_WARPS = OS_THREADS / 32;
+static constexpr int OS_LB = 4;  // look-back window (status loads per round trip)
 static constexpr int OS_MAX_PASSES = 16;  // 128-bit keys; tickets[32]: one per pass + the unique kernel's
 
 template <int KW>
@@ -136,17 +137,17 @@ __global__ void __launch_bounds__(OS_THREADS, KW == 1 ? 3 : (OS_STAGED<KW> ? 4 :
       atomicExch(st, LB_PRE | run);
     } else {
       atomicExch(st + (size_t)tile * 256, LB_AGG | run);
-      // look back 4 predecessors per round trip (independent loads in
+      // look back OS_LB predecessors per round trip (independent loads in
       // flight); a not-yet-published one is polled again
       long long j = (long long)tile - 1;
       bool done = false;
       while (!done) {
-        u32 sv[4];
+        u32 sv[OS_LB];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) sv[q] = j - q >= 0 ? ld_volatile(st + (size_t)(j - q) * 256) : LB_PRE;
+        for (int q = 0; q < OS_LB; ++q) sv[q] = j - q >= 0 ? ld_volatile(st + (size_t)(j - q) * 256) : LB_PRE;
         int q = 0;
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
+        for (int t = 0; t < OS_LB; ++t) {
           if (done || q < t) continue;
           const u32 flag = sv[t] & ~LB_VAL;
           if (flag == 0) continue;  // not published: poll again from j - t
