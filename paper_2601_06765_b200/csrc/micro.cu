@@ -2,7 +2,9 @@
 // (reference src/bench.py:244-300 `microbench`), on device-resident buffers:
 //
 //   f4b_dict_build  radix_sort + unique_sorted of W-word keys
-//                   (bulk.py:86-124, :135-150): the words are packed into one
+//                   (bulk.py:86-124, :135-150): an L2-resident hash table
+//                   drops the duplicates first (when the distinct keys fit),
+//                   the words are packed into one
 //                   order-isomorphic device key of W * key_bits bits (reference
 //                   keys are 48-bit words, bench.py:237-241), sorted with the
 //                   one-sweep LSD radix sort of radix.cu (W * key_bits / 8
@@ -14,6 +16,9 @@
 //                   (fp.py:335-400), here with a 64-bit Barrett reduction.
 //
 // All three are HBM-bound streams; the roofline is the copy bandwidth.
+#include <cstdlib>
+
+#include "block.cuh"
 #include "common.cuh"
 #include "engine.h"
 
@@ -59,6 +64,78 @@ __global__ void __launch_bounds__(MB_THREADS) k_mb_unpack(const u64* __restrict_
       out[i] = v.y;
     }
   }
+}
+
+// Duplicate filter in front of the sort (dict_build): every key is inserted
+// into an open-addressing table of packed 128-bit keys small enough to stay
+// in L2 (<= 64 MB); the first inserter of a key appends it to a compact list,
+// so only the distinct keys go through the radix sort.  Keys are packed on the
+// fly (no separate pack pass).  More distinct keys than `limit` -> overflow
+// flag, the caller falls back to sorting every key.
+static constexpr int HB_LOG_MAX = 22;
+using u128 = unsigned __int128;
+
+F4B_DEV u32 mb_hash(u64 hi, u64 lo, int logc) {
+  const u64 h = (lo * 0x9E3779B97F4A7C15ull) ^ (hi * 0xC2B2AE3D27D4EB4Full) ^ (lo >> 29);
+  return (u32)((h * 0xBF58476D1CE4E5B9ull) >> (64 - logc));
+}
+
+__global__ void __launch_bounds__(MB_THREADS) k_mb_hash_insert(const u64* __restrict__ in, long long n, int words,
+                                                               int kb, u128* __restrict__ table, int logc, u32 limit,
+                                                               u64* __restrict__ uniq, u32* __restrict__ d_count,
+                                                               u32* __restrict__ err) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const u64 lim = kb >= 64 ? ~0ull : ((1ull << kb) - 1);  // W = 2 implies kb < 64 here
+  const u32 mask = (1u << logc) - 1;
+  const u128 EMPTY = ~(u128)0;
+  const int lane = threadIdx.x & 31;
+  bool bad = false;
+  const long long n_round = (n + 31) / 32 * 32;  // whole warps iterate together (ballots)
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n_round; i += stride) {
+    // overflow: the caller sorts everything (warp-uniform exit: ballots below)
+    if (__shfl_sync(0xffffffffu, lane == 0 ? ld_volatile(err) : 0u, 0) & 2u) break;
+    bool ins = false;
+    u64 hi = 0, lo = 0;
+    if (i < n) {
+      if (words == 2) {
+        const ulonglong2 v = __ldcs(reinterpret_cast<const ulonglong2*>(in) + i);
+        bad |= (v.x > lim) | (v.y > lim);
+        lo = v.y | (v.x << kb);
+        hi = v.x >> (64 - kb);
+      } else {
+        lo = __ldcs(in + i);
+        bad |= lo > lim;
+      }
+      const u128 key = ((u128)hi << 64) | lo;
+      u32 h = mb_hash(hi, lo, logc);
+      for (;;) {
+        const ulonglong2 c2 = __ldcg(reinterpret_cast<const ulonglong2*>(table) + h);
+        const u128 cur = ((u128)c2.y << 64) | c2.x;
+        if (cur == key) break;
+        if (cur == EMPTY) {
+          const u128 old = atomicCAS(table + h, EMPTY, key);
+          if (old == EMPTY) {
+            ins = true;
+            break;
+          }
+          if (old == key) break;
+        }
+        h = (h + 1) & mask;
+      }
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, ins);
+    if (m) {
+      u32 base = 0;
+      if (lane == __ffs(m) - 1) base = atomicAdd(d_count, (u32)__popc(m));
+      base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+      if (ins) {
+        const u32 o = base + __popc(m & lanemask_lt());
+        if (o < limit) reinterpret_cast<ulonglong2*>(uniq)[o] = make_ulonglong2(hi, lo);
+      }
+      if (lane == 0 && base + __popc(m) > limit) atomicOr(err, 2u);
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(err, 1u);
 }
 
 // Lower bound of each query in an ascending W-word dictionary.  Queries of a
@@ -129,21 +206,56 @@ long long dict_build(Ctx* c, const uint64_t* keys, long long n, int words, int k
     fail(F4B_ERR_PRECONDITION, "dict_build: 0 <= n < 2^32 - 2, words in {1, 2}, 1 <= key_bits <= 64");
   if (n == 0) return 0;
   DBuf packed, uniq, flags;
-  ensure(c, packed, (size_t)n * 16);
-  ensure(c, uniq, (size_t)(n + 1) * 16);
   ensure(c, flags, 16);
   u32* err = flags.as<u32>();
   u32* d_count = err + 1;
-  memset_async(c, err, 0, 8);
-  F4B_LAUNCH(c, k_mb_pack, mb_grid(c, n), MB_THREADS, 0, keys, n, words, key_bits, packed.as<u64>(), err);
-  sort_unique(c, 2, packed.as<u64>(), nullptr, (u32)n, words * key_bits, nullptr, nullptr, uniq.as<u64>(), d_count);
+  u32* d_hcount = err + 2;
+  memset_async(c, err, 0, 12);
+  // duplicate filter first (distinct keys expected <= half the L2-sized
+  // table); packed keys with all 128 bits significant would collide with the
+  // empty-slot marker, so they always take the full sort
+  bool filtered = false;
+  static const bool no_filter = getenv("F4B_DICT_NOHASH") != nullptr;
+  if (!no_filter && words * key_bits < 128) {
+    int logc = 10;
+    while (logc < HB_LOG_MAX && (1ll << logc) < 2 * n) ++logc;
+    const u32 limit = 1u << (logc - 1);
+    DBuf table;
+    ensure(c, table, (size_t)16 << logc);
+    ensure(c, packed, (size_t)limit * 16);
+    memset_async(c, table.p, 0xFF, (size_t)16 << logc);
+    F4B_LAUNCH(c, k_mb_hash_insert, mb_grid(c, n), MB_THREADS, 0, keys, n, words, key_bits, table.as<u128>(), logc,
+               limit, packed.as<u64>(), d_hcount, err);
+    const u32 e = read_u32(c, err);
+    release(c, table);
+    if (e & 1u) {
+      release(c, packed);
+      release(c, flags);
+      fail(F4B_ERR_PRECONDITION, "dict_build: a key word has more than key_bits significant bits");
+    }
+    if (!(e & 2u)) {
+      const u32 nd = read_u32(c, d_hcount);
+      ensure(c, uniq, (size_t)(nd + 1) * 16);
+      sort_unique(c, 2, packed.as<u64>(), nullptr, nd, words * key_bits, nullptr, nullptr, uniq.as<u64>(), d_count);
+      filtered = true;
+    } else {
+      memset_async(c, err, 0, 12);
+    }
+  }
+  if (!filtered) {
+    ensure(c, packed, (size_t)n * 16);
+    ensure(c, uniq, (size_t)(n + 1) * 16);
+    F4B_LAUNCH(c, k_mb_pack, mb_grid(c, n), MB_THREADS, 0, keys, n, words, key_bits, packed.as<u64>(), err);
+    sort_unique(c, 2, packed.as<u64>(), nullptr, (u32)n, words * key_bits, nullptr, nullptr, uniq.as<u64>(),
+                d_count);
+  }
   F4B_LAUNCH(c, k_mb_unpack, mb_grid(c, n), MB_THREADS, 0, uniq.as<u64>(), d_count, words, key_bits, out);
   const u32 bad = read_u32(c, err);
   const long long nu = read_u32(c, d_count);
   release(c, packed);
   release(c, uniq);
   release(c, flags);
-  if (bad) fail(F4B_ERR_PRECONDITION, "dict_build: a key word has more than key_bits significant bits");
+  if (bad & 1u) fail(F4B_ERR_PRECONDITION, "dict_build: a key word has more than key_bits significant bits");
   return nu;
 }
 

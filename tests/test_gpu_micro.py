@@ -76,3 +76,18 @@ def test_mod_fma_odd_lengths(n):
     a[0] = b[0] = c[0] = p - 1
     got = _host(mod_fma(p, _dev(a), _dev(b), _dev(c)))
     assert np.array_equal(got, (c + a * b) % np.uint64(p))
+
+
+@pytest.mark.parametrize("size,dup", [(5_000_000, 0.3), (3_000_000, 0.999)])
+def test_dict_build_filter_and_fallback(size, dup):
+    # 3.5 M distinct keys overflow the 2^22-slot duplicate filter (full sort);
+    # 3,000 distinct keys go through the filter
+    microbench("dict_build", size, duplicate_rate=dup, seed=7, reps=1)
+
+
+def test_dict_build_filter_off_matches(monkeypatch):
+    rng = np.random.default_rng(11)
+    keys = rng.integers(0, 1 << 20, (200_000, 2), dtype=np.uint64)
+    keys[::3] = keys[5]
+    got = _host(dict_build(_dev(keys), words=2, key_bits=20)).reshape(-1, 2)
+    assert np.array_equal(got, np.unique(keys, axis=0))
