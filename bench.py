@@ -603,7 +603,7 @@ def main():
                                 ("row_assemble", 1 << 24, 0.0), ("mod_fma", 1 << 26, 0.0)):
             m = microbench(kind, size, dup, seed=0)
             keep = ("kind", "size", "duplicate_rate", "unique_out", "radix_passes", "keys_per_s", "joins_per_s",
-                    "updates_per_s.barrett", "algorithmic_bytes", "hbm_frac", "hbm_frac_per_pass")
+                    "updates_per_s.barrett", "algorithmic_bytes", "hbm_frac", "dict_path", "hbm_frac_streamed")
             ent = {k: m[k] for k in keep if k in m}
             ent["us"] = round(m.get("elapsed_ns", m.get("elapsed_ns.barrett", 0)) / 1e3, 1)
             micro.append(ent)

@@ -145,6 +145,15 @@ def microbench(kind: str, size: int, duplicate_rate: float = 0.5, seed: int = 0,
         dt = _time(torch, lambda: dict_build(kd, device=device), reps)
         nbytes = keys.nbytes + uniq.nbytes  # read every key once, write the dictionary once
         passes = -(-2 * KEY_BITS // 8)
+        # micro.cu: the duplicate filter (2^logc slots, logc = min(22, ceil
+        # log2 2n)) is kept when the distinct keys fit half of it
+        logc = min(22, max(10, int(np.ceil(np.log2(2 * size)))))
+        if len(uniq) <= 1 << (logc - 1):
+            path = "hash-filter + sort of the distinct keys"
+            streamed = keys.nbytes + 2 * (passes + 1) * uniq.nbytes + uniq.nbytes
+        else:
+            path = "full sort (distinct keys overflow the filter)"
+            streamed = keys.nbytes + 2 * (passes + 2) * keys.nbytes + uniq.nbytes
         out.update(
             duplicate_rate=duplicate_rate,
             unique_out=len(uniq),
@@ -156,7 +165,8 @@ def microbench(kind: str, size: int, duplicate_rate: float = 0.5, seed: int = 0,
             elapsed_ns=dt,
             algorithmic_bytes=nbytes,
             hbm_frac=nbytes / max(dt, 1) / peak,
-            hbm_frac_per_pass=(nbytes + 2 * (passes + 1) * keys.nbytes) / max(dt, 1) / peak,
+            dict_path=path,
+            hbm_frac_streamed=streamed / max(dt, 1) / peak,
         )
     elif kind == "row_assemble":
         dic = _host_unique(_synth_keys(rng, size, 0.0))

@@ -91,48 +91,68 @@ __global__ void __launch_bounds__(MB_THREADS) k_mb_hash_insert(const u64* __rest
   const int lane = threadIdx.x & 31;
   bool bad = false;
   const long long n_round = (n + 31) / 32 * 32;  // whole warps iterate together (ballots)
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n_round; i += stride) {
+  constexpr int HB_ITEMS = 4;  // keys per thread per iteration: four table probes in flight
+  for (long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; i0 < n_round; i0 += HB_ITEMS * stride) {
     // overflow: the caller sorts everything (warp-uniform exit: ballots below)
     if (__shfl_sync(0xffffffffu, lane == 0 ? ld_volatile(err) : 0u, 0) & 2u) break;
-    bool ins = false;
-    u64 hi = 0, lo = 0;
-    if (i < n) {
-      if (words == 2) {
-        const ulonglong2 v = __ldcs(reinterpret_cast<const ulonglong2*>(in) + i);
-        bad |= (v.x > lim) | (v.y > lim);
-        lo = v.y | (v.x << kb);
-        hi = v.x >> (64 - kb);
-      } else {
-        lo = __ldcs(in + i);
-        bad |= lo > lim;
-      }
-      const u128 key = ((u128)hi << 64) | lo;
-      u32 h = mb_hash(hi, lo, logc);
-      for (;;) {
-        const ulonglong2 c2 = __ldcg(reinterpret_cast<const ulonglong2*>(table) + h);
-        const u128 cur = ((u128)c2.y << 64) | c2.x;
-        if (cur == key) break;
-        if (cur == EMPTY) {
-          const u128 old = atomicCAS(table + h, EMPTY, key);
-          if (old == EMPTY) {
-            ins = true;
-            break;
-          }
-          if (old == key) break;
+    u64 hi[HB_ITEMS], lo[HB_ITEMS];
+    u32 h[HB_ITEMS];
+    ulonglong2 cur[HB_ITEMS];
+#pragma unroll
+    for (int k = 0; k < HB_ITEMS; ++k) {
+      const long long i = i0 + k * stride;
+      hi[k] = 0;
+      lo[k] = 0;
+      if (i < n) {
+        if (words == 2) {
+          const ulonglong2 v = __ldcs(reinterpret_cast<const ulonglong2*>(in) + i);
+          bad |= (v.x > lim) | (v.y > lim);
+          lo[k] = v.y | (v.x << kb);
+          hi[k] = v.x >> (64 - kb);
+        } else {
+          lo[k] = __ldcs(in + i);
+          bad |= lo[k] > lim;
         }
-        h = (h + 1) & mask;
       }
     }
-    const unsigned m = __ballot_sync(0xffffffffu, ins);
-    if (m) {
-      u32 base = 0;
-      if (lane == __ffs(m) - 1) base = atomicAdd(d_count, (u32)__popc(m));
-      base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
-      if (ins) {
-        const u32 o = base + __popc(m & lanemask_lt());
-        if (o < limit) reinterpret_cast<ulonglong2*>(uniq)[o] = make_ulonglong2(hi, lo);
+#pragma unroll
+    for (int k = 0; k < HB_ITEMS; ++k) {
+      h[k] = mb_hash(hi[k], lo[k], logc);
+      if (i0 + k * stride < n) cur[k] = __ldcg(reinterpret_cast<const ulonglong2*>(table) + h[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < HB_ITEMS; ++k) {
+      bool ins = false;
+      if (i0 + k * stride < n) {
+        const u128 key = ((u128)hi[k] << 64) | lo[k];
+        u32 hh = h[k];
+        u128 c = ((u128)cur[k].y << 64) | cur[k].x;
+        for (;;) {
+          if (c == key) break;
+          if (c == EMPTY) {
+            const u128 old = atomicCAS(table + hh, EMPTY, key);
+            if (old == EMPTY) {
+              ins = true;
+              break;
+            }
+            if (old == key) break;
+          }
+          hh = (hh + 1) & mask;
+          const ulonglong2 c2 = __ldcg(reinterpret_cast<const ulonglong2*>(table) + hh);
+          c = ((u128)c2.y << 64) | c2.x;
+        }
       }
-      if (lane == 0 && base + __popc(m) > limit) atomicOr(err, 2u);
+      const unsigned m = __ballot_sync(0xffffffffu, ins);
+      if (m) {
+        u32 base = 0;
+        if (lane == __ffs(m) - 1) base = atomicAdd(d_count, (u32)__popc(m));
+        base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+        if (ins) {
+          const u32 o = base + __popc(m & lanemask_lt());
+          if (o < limit) reinterpret_cast<ulonglong2*>(uniq)[o] = make_ulonglong2(hi[k], lo[k]);
+        }
+        if (lane == 0 && base + __popc(m) > limit) atomicOr(err, 2u);
+      }
     }
   }
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(err, 1u);
