@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(MB_THREADS) k_mb_unpack(const u64* __restrict_
 // so only the distinct keys go through the radix sort.  Keys are packed on the
 // fly (no separate pack pass).  More distinct keys than `limit` -> overflow
 // flag, the caller falls back to sorting every key.
-static constexpr int HB_LOG_MAX = 22;
+static constexpr int HB_LOG_MAX = 22;  // 64 MB table: L2 resident (2^25 measured: 16M keys at 50% duplicates 3.9 -> 3.4 ms, at 99% 0.46 -> 0.73 ms)
 using u128 = unsigned __int128;
 
 F4B_DEV u32 mb_hash(u64 hi, u64 lo, int logc) {
