@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(MB_THREADS) k_mb_hash_insert(const u64* __rest
   const int lane = threadIdx.x & 31;
   bool bad = false;
   const long long n_round = (n + 31) / 32 * 32;  // whole warps iterate together (ballots)
-  constexpr int HB_ITEMS = 4;  // keys per thread per iteration: four table probes in flight
+  constexpr int HB_ITEMS = 4;  // keys per thread per iteration: four table probes in flight (8: 98 registers, 168 -> 245 us)
   for (long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; i0 < n_round; i0 += HB_ITEMS * stride) {
     // overflow: the caller sorts everything (warp-uniform exit: ballots below)
     if (__shfl_sync(0xffffffffu, lane == 0 ? ld_volatile(err) : 0u, 0) & 2u) break;
