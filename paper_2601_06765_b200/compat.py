@@ -13,7 +13,9 @@ typing (rows with .shift/.basis_index/.role/.provenance, a SoaPolySet with
 .ring/.exps/.coeff/.length/.offset) and return objects with the attributes
 the reference reads (LayoutPlan .counters/.timings_ns/.dict_keys/.row_meta,
 EchelonResult .nonpivot_rows/.pivot_rows/.rank/.zero_row_count/
-.fill_generated).  `uninstall(fpgb)` restores the originals.
+.fill_generated).  `fpgb.bench.microbench` (and the CLI's copy) become the
+GPU microbenchmarks of `paper_2601_06765_b200.bench`.  `uninstall(fpgb)`
+restores the originals.
 """
 
 from __future__ import annotations
@@ -29,17 +31,28 @@ def _ring_adapter(ring):
     return ring
 
 
+# microbench (reference bench.py:244-312) is looked up in fpgb.bench and, by
+# the CLI, in fpgb.cli (imported by name at cli.py:17)
+MICRO_MODULES = ("bench", "cli")
+
+
 def install(fpgb_pkg) -> None:
+    from . import bench
+
     g = fpgb_pkg.groebner
     for name in PATCHED:
-        _SAVED.setdefault(name, getattr(g, name))
+        _SAVED.setdefault(("groebner", name), getattr(g, name))
     g.compile_batch = symbolic.compile_batch
     g.csr_from_plan = sparselin.csr_from_plan
     g.psge_reduce = sparselin.psge_reduce
+    for mod in MICRO_MODULES:
+        m = getattr(fpgb_pkg, mod, None)
+        if m is not None and hasattr(m, "microbench"):
+            _SAVED.setdefault((mod, "microbench"), m.microbench)
+            m.microbench = bench.microbench
 
 
 def uninstall(fpgb_pkg) -> None:
-    g = fpgb_pkg.groebner
-    for name, fn in _SAVED.items():
-        setattr(g, name, fn)
+    for (mod, name), fn in _SAVED.items():
+        setattr(getattr(fpgb_pkg, mod), name, fn)
     _SAVED.clear()
