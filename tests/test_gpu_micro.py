@@ -91,3 +91,16 @@ def test_dict_build_filter_off_matches(monkeypatch):
     keys[::3] = keys[5]
     got = _host(dict_build(_dev(keys), words=2, key_bits=20)).reshape(-1, 2)
     assert np.array_equal(got, np.unique(keys, axis=0))
+
+
+@pytest.mark.parametrize("words", [1, 2, 3, 4])
+def test_join_index_unsorted_queries(words):
+    # the warp narrows its search to [lb(min query), lb(max query)]: correct
+    # for queries in any order, including keys in the middle and the extremes
+    rng = np.random.default_rng(words)
+    keys = rng.integers(0, 1 << 40, (100_000, words), dtype=np.uint64)
+    dic = np.unique(keys, axis=0)
+    q = dic[rng.integers(0, len(dic), 77_777)]
+    q[0], q[-1] = dic[0], dic[-1]
+    got = join_index(_dev(dic), _dev(q)).cpu().numpy()
+    assert np.array_equal(dic[got], q)
