@@ -164,7 +164,8 @@ __global__ void __launch_bounds__(MB_THREADS) k_mb_hash_insert(const u64* __rest
 // warp are usually close in key order (row segments are sorted), so the
 // upper levels of the search are shared L1/L2 hits.  (Narrowing each warp's
 // range to [lb(min query), lb(max query)] first was measured 2x slower at 16M
-// queries: the kernel is bound by the dependent-load chain, not by requests.)
+// queries: the kernel is bound by the dependent-load chain, not by requests;
+// four branch-free searches in lockstep per thread: 1.8x slower as well.)
 template <int KW>
 __global__ void __launch_bounds__(MB_THREADS) k_mb_join(const u64* __restrict__ dict, u32 nd,
                                                         const u64* __restrict__ q, long long n,
