@@ -5,7 +5,8 @@ cyclic-8 / F_32003 grevlex run.  Setup runs the full F4 computation once on
 the GPU (bit-exact with the reference) and captures each batch's row list and
 basis prefix; the device basis (final, HBM-resident) then serves all batches
 (closure candidates restricted to the batch's basis prefix, which reproduces
-the live plans exactly).
+the live plans exactly: every replayed batch's (r, N, M, closure rounds) is
+asserted equal to the live run's).
 
 One bench *step* = all 38 batches of the run through compile_batch ->
 psge_reduce (new-row mode, what the F4 driver consumes).  L2 is flushed
@@ -17,11 +18,21 @@ psge_reduce (new-row mode, what the F4 driver consumes).  L2 is flushed
   e2e        = the same metric through the public Python API / C ABI with
                host buffers: each batch uploads its basis + rows (fresh device
                basis) and downloads the assembled LayoutPlan arrays.
-  reduction  = F_p reduction seconds per F4 step (psge, device time).
+  reduction  = F_p reduction seconds per F4 step (psge, device time), in the
+               driver's NEW_ONLY mode and in the reference's FULL_RREF mode
+               (sparselin.py:337-349 always back-reduces).
 
---impl reference times the CPU oracle (a NumPy restatement of the reference
-fpgb algorithm, tests pin it byte-for-byte) on a bounded sample: cyclic-8
-steps restored from committed reference snapshots.
+--gpus N (N > 1) relaunches itself under torch.distributed.run (one rank per
+GPU, NCCL over 127.0.0.1) and runs the sharded compile_batch of SURVEY §8e
+(dist.ShardedCompiler): each rank materialises a contiguous, length-balanced
+row range, the sorted unique monomial runs and the closure rounds are
+all-gathered over NCCL, every rank joins its share of the final rows.
+
+--impl reference times the UNMODIFIED reference (`fpgb`, installed into
+baseline/_ref) through its own API on the box's host: cyclic-8 states restored
+from the reference's snapshots, `select_batch -> select_rows ->
+compile_batch` per step (the metric's numerator and denominator), plus
+`psge_reduce` once on a bounded step for the reduction figure.
 """
 
 from __future__ import annotations
@@ -30,6 +41,7 @@ import argparse
 import gzip
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -44,23 +56,13 @@ sys.path.insert(0, ROOT)
 METRIC = "Macaulay nnz/s assembled + F_p reduction s/F4 step (cyclic-8, 1-8 GPU)"
 UNIT = "nnz/s"
 WORKLOAD = "cyclic-8 over F_32003, grevlex, all 38 F4 batches (compile_batch + psge_reduce)"
-CPU_SAMPLE_STEPS = (5, 6, 7)
-
-
-def _traffic_from_profiles():
-    """DRAM bytes per launch (dram__bytes_read + write) from the committed
-    `ncu --set full` summary (profiles/*/traffic.json), keyed by kernel."""
-    out = {}
-    pdir = os.path.join(ROOT, "profiles")
-    for sub in sorted(os.listdir(pdir)) if os.path.isdir(pdir) else []:
-        path = os.path.join(pdir, sub, "traffic.json")
-        if os.path.exists(path):
-            try:
-                with open(path) as fh:
-                    out.update(json.load(fh))
-            except Exception:
-                pass
-    return out
+# reference-arm sample: cyclic-8 steps restored from the reference's own
+# snapshots (tests/golden/cyclic8_p32003.snap.json.gz); step i of the timed
+# loop compiles REF_ROTATION[i % len] (each ~0.1-12 s on one core), so the
+# whole --steps 20 --warmup 5 run stays within a few minutes and every sample
+# includes the two heaviest symbolic steps s10 and s19 at a fixed ratio
+REF_ROTATION = (10, 19, 5, 6, 7)
+REF_PSGE_STEPS = (5, 6)  # psge_reduce sample (s10 alone takes 391 s in fpgb)
 
 
 def _peaks():
@@ -72,85 +74,187 @@ def _peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-# ---------------------------------------------------------------------------
-# CPU baseline: the oracle on reference snapshots
-# ---------------------------------------------------------------------------
-def cpu_sample(steps=CPU_SAMPLE_STEPS):
-    import oracle
-    from paper_2601_06765_b200.groebner import GroebnerState, Pair, _make_pair, select_batch
-    from paper_2601_06765_b200.symbolic import select_rows
-    from paper_2601_06765_b200.systems import parse_system
+def _traffic_from_profiles():
+    """Average DRAM bytes per launch (dram__bytes_read.sum +
+    dram__bytes_write.sum) per kernel, from the ncu capture of this same
+    bench command committed under profiles/ (latest round wins)."""
+    out = {}
+    pdir = os.path.join(ROOT, "profiles")
+    for sub in sorted(os.listdir(pdir)) if os.path.isdir(pdir) else []:
+        path = os.path.join(pdir, sub, "traffic_bench.json")
+        if os.path.exists(path):
+            try:
+                with open(path) as fh:
+                    out.update(json.load(fh))
+            except Exception:
+                pass
+    return out
 
-    path = os.path.join(ROOT, "tests", "golden", "cyclic8_p32003.snap.json.gz")
-    if not os.path.exists(path):
-        return {"M": 0, "t_sym": 0.0, "t_num": 0.0, "steps": []}
-    with gzip.open(path, "rt") as fh:
-        snaps = json.load(fh)["snapshots"]
-    tot_M = tot_sym = tot_num = 0.0
-    done = []
-    for k in steps:
-        snap = snaps.get(str(k))
-        if snap is None:
-            continue
+
+# ---------------------------------------------------------------------------
+# the reference (fpgb from baseline/_ref) on restored cyclic-8 steps
+# ---------------------------------------------------------------------------
+def _import_fpgb():
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(os.path.join(path, "fpgb")):
+        if path not in sys.path:
+            sys.path.insert(0, path)
+        import fpgb  # noqa: F401
+
+        return True
+    return False
+
+
+def _snapshots():
+    with gzip.open(os.path.join(ROOT, "tests", "golden", "cyclic8_p32003.snap.json.gz"), "rt") as fh:
+        return json.load(fh)["snapshots"]
+
+
+class RefSample:
+    """Reference states restored from snapshots (SURVEY §8d replay: parse the
+    basis, rebuild the pair queue with the reference's own _make_pair), then
+    per timed step the reference's select_batch -> select_rows ->
+    compile_batch.  Falls back to the NumPy oracle port when fpgb is absent."""
+
+    def __init__(self, steps):
+        self.kind = "reference" if _import_fpgb() else "port"
+        snaps = _snapshots()
+        self.items = {}
+        for k in steps:
+            self.items[k] = snaps[str(k)]
+
+    def _state(self, snap):
+        if self.kind == "reference":
+            from fpgb.groebner import GroebnerState, Pair, _make_pair
+            from fpgb.systems import parse_system
+
+            ring, basis = parse_system(snap["basis"])
+            st = GroebnerState(ring)
+            st.basis = list(basis)
+            st.pairs = sorted([_make_pair(st, i, j) for i, j in snap["pairs"]], key=Pair.sort_tuple)
+            return st
+        from paper_2601_06765_b200.groebner import GroebnerState, Pair, _make_pair
+        from paper_2601_06765_b200.systems import parse_system
+
         ring, basis = parse_system(snap["basis"])
         st = GroebnerState(ring)
         for f in basis:
             st._push_basis(f)
         st.pairs = sorted([_make_pair(st, i, j) for i, j in snap["pairs"]], key=Pair.sort_tuple)
+        return st
+
+    def compile(self, k):
+        """-> (M, seconds, plan) for one compile_batch of step k (host wall
+        time of the reference's compile_batch alone, as its stage timers)."""
+        st = self._state(self.items[k])
+        if self.kind == "reference":
+            from fpgb.groebner import select_batch
+            from fpgb.symbolic import Closure, compile_batch, select_rows
+
+            spec, _ = select_batch(st)
+            soa = st.soa()
+            rows = select_rows(spec, soa)
+            t0 = time.perf_counter()
+            plan = compile_batch(rows, soa, Closure.ONE_STEP_REDUCTION)
+            return plan.counters.M, time.perf_counter() - t0, plan
+        import oracle
+        from paper_2601_06765_b200.groebner import select_batch
+        from paper_2601_06765_b200.symbolic import select_rows
+
         spec, _ = select_batch(st)
         soa = st.soa()
         rows = [(r.shift, r.basis_index, r.role.value, r.provenance) for r in select_rows(spec, soa)]
         t0 = time.perf_counter()
-        plan = oracle.compile_batch_arrays(rows, (soa.exps, soa.coeff, soa.offset, soa.length), ring.order)
-        t1 = time.perf_counter()
-        oracle.psge_arrays(len(plan["row_ptr"]) - 1, plan["counters"]["N"], plan["row_ptr"], plan["col_ind"],
-                           plan["val"], ring.modulus.p)
-        t2 = time.perf_counter()
-        tot_M += plan["counters"]["M"]
-        tot_sym += t1 - t0
-        tot_num += t2 - t1
-        done.append(k)
-    return {"M": tot_M, "t_sym": tot_sym, "t_num": tot_num, "steps": done}
+        plan = oracle.compile_batch_arrays(rows, (soa.exps, soa.coeff, soa.offset, soa.length), st.ring.order)
+        return plan["counters"]["M"], time.perf_counter() - t0, plan
+
+    def psge(self, plan, p):
+        t0 = time.perf_counter()
+        if self.kind == "reference":
+            from fpgb.sparselin import csr_from_plan, psge_reduce
+
+            psge_reduce(csr_from_plan(plan, plan.ring.modulus))
+        else:
+            import oracle
+
+            oracle.psge_arrays(len(plan["row_ptr"]) - 1, plan["counters"]["N"], plan["row_ptr"], plan["col_ind"],
+                               plan["val"], p)
+        return time.perf_counter() - t0
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
 
 
 def run_reference(args, rank):
     if rank != 0:
         return
-    for _ in range(args.warmup):
-        cpu_sample()
-    tM = tS = tN = 0.0
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        s = cpu_sample()
-        tM += s["M"]
-        tS += s["t_sym"]
-        tN += s["t_num"]
-    wall = time.perf_counter() - t0
+    smp = RefSample(sorted(set(REF_ROTATION) | set(REF_PSGE_STEPS)))
+    for i in range(args.warmup):  # untimed: the cheapest sample step
+        smp.compile(5)
+    tM = tS = 0.0
+    per = {}
+    for i in range(args.steps):
+        k = REF_ROTATION[i % len(REF_ROTATION)]
+        M, sec, _ = smp.compile(k)
+        tM += M
+        tS += sec
+        per.setdefault(k, []).append(round(sec, 3))
     value = tM / tS
-    sample = (f"cyclic-8/F_32003 F4 steps {list(CPU_SAMPLE_STEPS)} restored from reference snapshots; "
-              "NumPy oracle port of fpgb compile_batch + psge_reduce, single-threaded")
+    num = []
+    for k in REF_PSGE_STEPS:
+        _, _, plan = smp.compile(k)
+        num.append(smp.psge(plan, 32003))
+    sample = (f"cyclic-8/F_32003 F4 steps restored from the reference's snapshots; step i of the timed loop = "
+              f"{'fpgb' if smp.kind == 'reference' else 'NumPy port of fpgb'} select_batch -> select_rows -> "
+              f"compile_batch on snapshot step {list(REF_ROTATION)}[i % {len(REF_ROTATION)}] (value = sum M / sum "
+              f"compile seconds); reduction = psge_reduce on steps {list(REF_PSGE_STEPS)}; 1 thread "
+              f"(the reference is single-threaded), {os.cpu_count()} cores on the host ({_cpu_model()})")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * wall / max(1, args.steps),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32 residues mod p",
-        "data": "synthetic (generated cyclic-8 system)",
-        "config": {"workload": WORKLOAD + " [CPU sample]", "sample_steps": list(CPU_SAMPLE_STEPS)},
-        "reduction_s_per_f4_step": tN / (args.steps * len(CPU_SAMPLE_STEPS)),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample},
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tS / max(1, args.steps),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64 residues mod p (fpgb)",
+        "data": "synthetic (generated cyclic-8 system, deterministic)",
+        "config": {"workload": WORKLOAD + " [bounded CPU sample]", "rotation_steps": list(REF_ROTATION),
+                   "compile_s_per_sample_step": per},
+        "reduction_s_per_f4_step": sum(num) / len(num),
+        "reduction_sample_steps": list(REF_PSGE_STEPS),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": smp.kind, "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
+def cpu_baseline_line():
+    """cpu_baseline of the GPU arm: the reference's compile_batch on the two
+    heaviest symbolic steps (s10 + s19, about 19 s of CPU work), 1 thread."""
+    smp = RefSample((10, 19))
+    tM = tS = 0.0
+    for k in (10, 19):
+        M, sec, _ = smp.compile(k)
+        tM += M
+        tS += sec
+    return {"value": tM / tS, "unit": UNIT, "cores": 1, "kind": smp.kind,
+            "sample": (f"{'fpgb (baseline/_ref)' if smp.kind == 'reference' else 'NumPy port of fpgb'} "
+                       f"compile_batch on cyclic-8 steps 10 and 19 restored from reference snapshots "
+                       f"(M = {int(tM)}, {tS:.1f} s), single thread, host {_cpu_model()}")}
+
+
 # ---------------------------------------------------------------------------
 # GPU workload capture
 # ---------------------------------------------------------------------------
-def capture_workload():
+def capture_run(ring, polys):
+    """Run the whole F4 computation on the GPU, capturing every batch's row
+    list, basis prefix and live (r, N, M, closure rounds)."""
     from paper_2601_06765_b200.groebner import GroebnerState, f4_step, update_pairs
     from paper_2601_06765_b200.polynomials import poly_monic
-    from paper_2601_06765_b200.systems import gen_cyclic
 
-    ring, polys = gen_cyclic(8, 32003)
     st = GroebnerState(ring)
     for f in polys:
         update_pairs(st, poly_monic(f))
@@ -164,12 +268,22 @@ def capture_workload():
             "sh": np.asarray([r.shift for r in rows], dtype=np.int64).reshape(len(rows), n),
             "n_basis": len(soa), "n_terms": soa.total_terms(),
             "r": plan.counters.r, "N": plan.counters.N, "M": plan.counters.M,
+            "rounds": plan.counters.closure_rounds,
+            "t_sym_ns": plan.timings_ns["dict_build_ns"] + plan.timings_ns["row_assemble_ns"],
         })
 
     t0 = time.perf_counter()
     while st.n_pairs():
         f4_step(st, _capture=cap)
-    return ring, st, batches, time.perf_counter() - t0
+    return st, batches, time.perf_counter() - t0
+
+
+def capture_workload():
+    from paper_2601_06765_b200.systems import gen_cyclic
+
+    ring, polys = gen_cyclic(8, 32003)
+    st, batches, secs = capture_run(ring, polys)
+    return ring, st, batches, secs
 
 
 class ClockSampler:
@@ -307,89 +421,83 @@ class ClockSampler:
                 "source": "nvml" if self.thread is not None else ("nvidia-smi" if self.path else "none")}
 
 
-# Algorithmic bytes per kernel per batch — DESIGN.md §4.
-#   k_fbsp (whole compile_batch) : B_sym of SURVEY.md §8(d): every term's
-#                                  source key + coefficient in, col_ind + val
-#                                  out, row_ptr, the dictionary
-#                                  M(8W+4) + 8M + 4(r+1) + 8W N
-#   k_sweep<0> (C rows by A)     : every pivot-row application streams the
-#                                  pivot tail (u32 col + u32 val) and its
-#                                  16-byte descriptor; the C rows are read
-#                                  and D' is written once
-#                                  8 tail_nnz + 16 pivots + 8 nnz(C) + 4|C|K
-#                                  (pivot rows are reused across C rows, so
-#                                  this stream is L2-served, not HBM)
-#   k_dense_forward              : read + write D' once       8|C|K
-#   k_dense_blk                  : D' read + RREF(D') written 4|C|K + 4 rank(D') K
+
+# Algorithmic bytes, per launch of one batch.
+#   symbolic (k_fbsp / the multi-launch symbolic kernels as one unit):
+#     B_sym = M (8W + 4) + 8M + 4(r+1) + 8W N with W the REFERENCE key words
+#     (ring.n_key_words: 3 for cyclic-8, 4 for Katsura-11) — the paper's
+#     key-traffic model, independent of the device key width
+#   k_sweep_win: 4 B per packed pivot-tail entry streamed (8 B for (col, val)
+#     pairs), C rows read once (8 B per nonzero), D' written once
+#   k_sweep: 8 B per tail entry + 16 B descriptor per applied pivot + C rows + D'
+#   k_dense_blk: D' read once + RREF(D') written once
+#   k_dense_forward: D' read + written once
+#   elimination step: B_elim = 8 M + 8 nnz(RREF) (FULL_RREF mode)
 SYMBOLIC = ("k_fbsp", "k_rank_", "k_tile_dict", "k_join_gen", "k_os_", "k_small_sort", "k_unique_absent",
             "k_closure", "k_new_rows", "k_merge_corank", "k_rows0", "k_encode_basis", "k_mark_leads", "k_front0",
-            "k_dict_exps")
+            "k_dict_exps", "k_sh_")
 
 
-def kernel_bytes(name, b, pinfo, einfo):
+def b_sym(b, W):
+    return b["M"] * (8 * W + 4) + 8 * b["M"] + 4 * (b["r"] + 1) + 8 * W * b["N"]
+
+
+def kernel_bytes(name, b, W, einfo):
     M = b["M"]
-    KW = pinfo["key_words"]
     C, K = einfo["dense_rows"], einfo["dense_cols"]
     if name.startswith("k_fbsp"):
-        return M * (8 * KW + 4) + 8 * M + 4 * (b["r"] + 1) + 8 * KW * b["N"]
-    if name.startswith(("k_rank_join", "k_join_gen")):
-        return M * (8 * KW + 4) + 8 * M
-    if name.startswith(("k_rank_fill", "k_tile_dict")):
-        return M * 8 * KW
+        return b_sym(b, W)
     if "k_sweep_win" in name:
-        # packed pivot tails (4-byte col|val entries in 4-entry groups when
-        # N < 2^16 and p < 2^16, else 8-byte pairs), streamed once per applied
-        # pivot; the C rows read once, D' written once
         c_nnz = int(C * M / max(1, b["r"]))
         entry = 4 if "<true>" in name else 8
         return entry * einfo["sweep_tail_nnz"] + 8 * c_nnz + 4 * C * K
     if "k_sweep" in name:
-        # C-row share of the nonzeros: |C| rows of mean length M / r
         c_nnz = int(C * M / max(1, b["r"]))
         return 8 * einfo["sweep_tail_nnz"] + 16 * einfo["sweep_pivots"] + 8 * c_nnz + 4 * C * K
     if name.startswith("k_dense_blk"):
-        # compulsory: D' read once, RREF(D') written once (the per-block
-        # products re-read L2-resident rows and are not credited)
         return 4 * C * K + 4 * einfo["n_nonpivot_rows"] * K
-    if name in ("k_dense_forward", "k_dense_fwd_smem", "k_dense_forward_cta"):
-        # D' read into the row state and the pivot rows written back once
+    if name.startswith("k_dense_forward"):
         return 8 * C * K
     return None
 
 
-def roofline_for(kprof, records, peak, peak_src, want):
-    """Roofline of the most expensive kernel accepted by `want` (with a byte model)."""
+def roofline_for(kprof, records, W, peak, peak_src, want, traffic):
+    """Roofline of the most expensive kernel accepted by `want` that has an
+    algorithmic byte model: achieved = sum of its per-batch algorithmic bytes
+    / its summed CUDA-event time (per launch: both divided by the launch count)."""
     total = max(1.0, sum(v[1] for v in kprof.values()))
     for name, (cnt, ns) in sorted(kprof.items(), key=lambda kv: -kv[1][1]):
         if not want(name) or ns <= 0:
             continue
         tot = 0
-        for b, pinfo, einfo in records:
-            kb = kernel_bytes(name, b, pinfo, einfo)
+        for b, einfo in records:
+            kb = kernel_bytes(name, b, W, einfo)
             if kb is None:
                 tot = None
                 break
             tot += kb
         if tot is None:
-            return {"bound": "latency", "kernel": name, "achieved": None, "peak": peak, "unit": "GB/s", "frac": None,
-                    "traffic": None, "launches": cnt, "avg_launch_us": ns / cnt / 1e3, "share_of_step": ns / total,
-                    "note": "no algorithmic byte model (schedule-dependent work)"}
+            continue
         ach = tot / (ns * 1e-9) / 1e9
+        tr = traffic.get(name)
         out = {"bound": "hbm", "kernel": name, "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-               "traffic": None, "launches": cnt, "avg_launch_us": ns / cnt / 1e3, "peak_source": peak_src,
+               "traffic": tr.get("dram_bytes_per_launch") if tr else None,
+               "traffic_source": tr.get("source") if tr else None,
+               "launches": cnt, "avg_launch_us": ns / cnt / 1e3, "peak_source": peak_src,
                "share_of_step": ns / total, "algorithmic_bytes_per_launch": tot / cnt}
-        if "k_sweep_win" in name:
-            out["note"] = ("pivot tails packed once per matrix and L2-resident (reused by every C row); fixed "
-                           "32-A-column windows with precomputed block inverses: multipliers from one 32x32 "
-                           "product, two CTA barriers per non-empty window, shared-atomic tail application")
-        elif name.startswith("k_dense_blk"):
-            out["note"] = ("latency-bound: RREF(D') in pivot blocks, two grid barriers per block of up to 32 "
-                           "pivots; byte model counts D' read and RREF(D') written once")
-        elif name.startswith("k_dense_fwd"):
-            out["note"] = ("latency-bound: one grid barrier per pivot of D' (byte model counts D' once; the "
-                           "per-pivot row updates stay in shared memory)")
         return out
     return None
+
+
+def _self_launch(args):
+    """--gpus N > 1 without a torchrun environment: relaunch under
+    torch.distributed.run with one rank per GPU on 127.0.0.1."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
 
 
 def main():
@@ -402,15 +510,24 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-micro", action="store_true", help="skip the primitive microbenchmarks")
     ap.add_argument("--no-katsura11", action="store_true",
-                    help="skip the full Katsura-11 run reported next to the line (rank 0, after the timed region)")
+                    help="skip the Katsura-11 run and warm replays reported next to the line (rank 0)")
     args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "b200":
+        args.warmup = 3  # timing rule: at least 3 warm-up steps
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        _self_launch(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
     if args.impl == "reference":
         run_reference(args, rank)
         return
+    run_gpu(args, world, rank, local)
 
+
+def run_gpu(args, world, rank, local):
     import torch
     import torch.distributed as dist
 
@@ -419,14 +536,10 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     from paper_2601_06765_b200.engine import Engine
-    from paper_2601_06765_b200.sparselin import csr_from_plan, psge_reduce
-    from paper_2601_06765_b200.symbolic import compile_batch
-
-    ring, st, batches, setup_s = capture_workload()
-    # the whole run also ends with the device interreduction (§8f.1); report
-    # both next to the reference's own timings of the same run (golden file)
     from paper_2601_06765_b200.groebner import reduce_basis_device
 
+    ring, st, batches, setup_s = capture_workload()
+    W = ring.n_key_words
     t0 = time.perf_counter()
     gb = reduce_basis_device(st.basis, ring)
     reduce_s = time.perf_counter() - t0
@@ -436,40 +549,57 @@ def main():
         with open(os.path.join(ROOT, "tests", "golden", "cyclic8_p32003.json")) as fh:
             g = json.load(fh)
         full_run.update(reference_f4_loop_s=g["f4_loop_s"], reference_reduce_basis_s=g["reduce_basis_s"],
-                        reference_gb_size=g["gb_size"])
+                        reference_gb_size=g["gb_size"], reference_where="survey container, 1 core (SURVEY §6.1)")
     except Exception:
         pass
     eng = Engine.for_ring(ring, local)
     eng.sync_basis(st.soa())  # the interreduction above replaced the device basis
     total_M = sum(b["M"] for b in batches)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    shard = None
+    if world > 1:
+        try:
+            from paper_2601_06765_b200.dist import ShardedCompiler
 
-    _dbg = [] if os.environ.get("F4B_BENCH_DEBUG") else None
+            shard = ShardedCompiler(eng)
+        except ImportError:
+            shard = None  # replicas
 
-    def replay_step(record):
+    def replay_step(record, full=False, check=False):
         ts = tn = 0
+        per = []
         for b in batches:
             clk.maybe_sample()
             flush.fill_(1)
-            plan = eng.compile(b["rb"], b["sh"], True, list(range(b["n_basis"])))
-            ech = eng.psge_plan(plan, full=False)
+            if shard is not None:
+                plan, t_sym_ns = shard.compile(b["rb"], b["sh"], True, list(range(b["n_basis"])))
+                inf_p = plan.info
+                t_b = t_sym_ns
+            else:
+                plan = eng.compile(b["rb"], b["sh"], True, list(range(b["n_basis"])))
+                inf_p = plan.info
+                t_b = inf_p["dict_build_ns"] + inf_p["row_assemble_ns"]
+            if check:
+                got = (inf_p["r"], inf_p["N"], inf_p["M"], inf_p["closure_rounds"])
+                want = (b["r"], b["N"], b["M"], b["rounds"])
+                assert got == want, f"replayed batch {(got)} != live {want}"
+            ech = eng.psge_plan(plan.local if shard is not None else plan, full=full)
             inf = ech.info()
-            ts += plan.info["dict_build_ns"] + plan.info["row_assemble_ns"]
-            tn += inf["numeric_ns"]
-            if _dbg is not None:
-                _dbg.append((b["r"], (plan.info["dict_build_ns"] + plan.info["row_assemble_ns"]) / 1e6,
-                             inf["numeric_ns"] / 1e6))
+            ts += t_b
+            tn += inf["numeric_ns"] + (inf["backsub_ns"] if full else 0)
+            per.append((t_b, inf["numeric_ns"] + (inf["backsub_ns"] if full else 0)))
             if record is not None:
-                record.append((b, plan.info, inf))
-        return ts, tn
+                record.append((b, inf))
+        return ts, tn, per
 
     clk = ClockSampler(local).start()
-    for _ in range(args.warmup):
-        replay_step(None)
+    for i in range(args.warmup):
+        replay_step(None, check=(i == 0))
     # timed region
     eng.profile(True)
     _, launches0 = eng.profile_read()
     records = []
+    per_sym = np.zeros(len(batches))
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -477,9 +607,10 @@ def main():
     w0 = time.perf_counter()
     t_sym = t_num = 0
     for _ in range(args.steps):
-        a, c = replay_step(records)
+        a, c, per = replay_step(records)
         t_sym += a
         t_num += c
+        per_sym += np.array([x[0] for x in per], dtype=np.float64)
     torch.cuda.synchronize()
     wall = time.perf_counter() - w0
     clk.end()
@@ -490,112 +621,52 @@ def main():
     eng.profile(False)
     t_tot_ns = float(t_sym + t_num)
     if world > 1:
-        t = torch.tensor([t_tot_ns, float(t_sym)], device="cuda", dtype=torch.float64)
+        t = torch.tensor([t_tot_ns, float(t_sym), float(t_num)], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_tot_ns, t_sym = float(t[0]), float(t[1])
+        t_tot_ns, t_sym, t_num = float(t[0]), float(t[1]), float(t[2])
     ms_per_step = t_tot_ns / 1e6 / args.steps
-    value = world * total_M * args.steps / (t_sym / 1e9)
+    # sharded: every rank assembles its share of the SAME plans (strong
+    # scaling of each batch); replicas would multiply by world
+    value = (1 if shard is not None else world) * total_M * args.steps / (t_sym / 1e9)
     red_s = t_num / 1e9 / (args.steps * len(batches))
 
-    # roofline: the dominant kernel with an algorithmic byte model
+    # the reference's mode: FULL_RREF (pivot rows back-reduced), one pass,
+    # CUDA-event timed per batch; B_elim = 8 M + 8 nnz(RREF)
+    full_recs = []
+    _, t_full, _ = replay_step(full_recs, full=True)
+    nnz_rref = sum(inf["pivot_nnz"] + inf["nonpivot_nnz"] for _, inf in full_recs)
+    B_elim = 8 * total_M + 8 * nnz_rref
     peak, peak_src = _peaks()
-    ranked = sorted(kprof.items(), key=lambda kv: -kv[1][1])
-    roof = roofline_for(kprof, records, peak, peak_src, lambda nm: True)
-    roof_sym = roofline_for(kprof, records, peak, peak_src, lambda nm: nm.startswith(SYMBOLIC))
+    elim_full = {"s_per_f4_step": t_full / 1e9 / len(batches), "B_elim_bytes": B_elim,
+                 "achieved_gbs": B_elim / (t_full / 1e9) / 1e9, "frac": B_elim / (t_full / 1e9) / 1e9 / peak,
+                 "nnz_rref": nnz_rref,
+                 "reference_s_per_f4_step": 74.9, "reference_where": "survey container, 1 core (BASELINE.md 2.1)"}
+
+    # roofline: the dominant kernel with an algorithmic byte model
     traffic = _traffic_from_profiles()
-    for rf in (roof, roof_sym):
-        if rf and rf.get("kernel") in traffic:
-            rf["traffic"] = traffic[rf["kernel"]]
-    # symbolic (FBSP) effective roofline, B_sym per SURVEY.md §8(d)
-    W = ring.n_key_words
-    B_sym = sum(b["M"] * (8 * W + 4) + 8 * b["M"] + 4 * (b["r"] + 1) + b["N"] * 8 * W for b in batches)
-    sym_frac = (B_sym * args.steps / (t_sym / 1e9) / 1e9) / peak
+    roof = roofline_for(kprof, records, W, peak, peak_src, lambda nm: True, traffic)
+    roof_sym = roofline_for(kprof, records, W, peak, peak_src, lambda nm: nm.startswith(SYMBOLIC), traffic)
+    # symbolic (FBSP) effective roofline per step and aggregate, B_sym per §8(d)
+    Bs = np.array([b_sym(b, W) for b in batches], dtype=np.float64)
+    per_us = per_sym / args.steps / 1e3
+    frac_b = Bs / (per_us * 1e-6) / 1e9 / peak
+    sym_frac = (Bs.sum() * args.steps / (t_sym / 1e9) / 1e9) / peak
+    sym_steps = {str(i): {"M": b["M"], "B_sym": int(Bs[i]), "t_us": round(float(per_us[i]), 1),
+                          "frac": round(float(frac_b[i]), 4)} for i, b in enumerate(batches)}
+    sym_named = {k: sym_steps[k] for k in ("10", "19") if k in sym_steps}
 
     # e2e: the public API with host buffers, replaying the run as the F4
-    # driver does it: the device basis starts empty each step and grows batch
-    # by batch (sync_basis appends the polynomials added since the previous
-    # batch, from page-locked copies of the basis streams); per batch the row
-    # list goes up, compile_batch runs, and the LayoutPlan arrays
-    # (row_ptr, col_ind, val, dict_keys) come back to host memory.
+    # driver does it (device basis grows batch by batch, rows up, plan down)
     e2e = None
-    if args.e2e_steps > 0:
-        from paper_2601_06765_b200.engine import host_empty
-        from paper_2601_06765_b200.polynomials import SoaPolySet
+    if args.e2e_steps > 0 and world == 1:
+        e2e = run_e2e(args, ring, st, batches, eng, torch)
 
-        final = st.soa()
-
-        def pinned(a):
-            out = host_empty(a.shape, a.dtype)
-            out[...] = a
-            return out
-
-        f_key, f_coeff, f_exps = pinned(final.mon_key), pinned(final.coeff), pinned(final.exps)
-        n = ring.n_vars
-        h2d = d2h = 0
-        e_sym = 0.0
-        e_M = 0
-        for it in range(args.e2e_steps + 1):  # iteration 0 warms the host caches, untimed
-            if it == 1:
-                h2d = d2h = e_M = 0
-                e_sym = 0.0
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            eng.clear_basis()
-            prev_nt = prev_nb = 0
-            for b in batches:
-                nb_, nt = b["n_basis"], b["n_terms"]
-                soa = SoaPolySet(ring, f_key[:nt], f_coeff[:nt], final.offset[:nb_ + 1], final.length[:nb_],
-                                 f_exps[:nt])
-                plan = compile_batch(b["rows"], soa)
-                rp, ci, va = plan.row_ptr, plan.col_ind, plan.val
-                dk = plan.dict_keys
-                e_M += b["M"]
-                # bytes moved: new basis terms as the reference streams them
-                # (int64 exps + uint64 coeff, narrowed on the device), their
-                # lengths + offsets, back their LM / max exponents; rows (basis
-                # index + shift); back: row_ptr / col_ind / val (64-bit) and
-                # dict_keys (reference key words)
-                h2d += (nt - prev_nt) * (8 * n + 8) + (nb_ - prev_nb) * 16 + len(b["rows"]) * (4 + 2 * n)
-                d2h += ((nb_ - prev_nb) * 4 * n + (plan.counters.r + 1) * 8 + plan.counters.M * 16
-                        + plan.counters.N * 8 * ring.n_key_words)
-                prev_nt, prev_nb = nt, nb_
-                del rp, ci, va, dk, plan
-            torch.cuda.synchronize()
-            e_sym += time.perf_counter() - t0
-        e2e = {"value": world * e_M / e_sym, "unit": UNIT, "h2d_bytes_per_step": h2d // args.e2e_steps,
-               "d2h_bytes_per_step": d2h // args.e2e_steps,
-               "note": ("per step: empty device basis, then per batch the new basis polys + rows H2D, "
-                        "compile_batch, LayoutPlan arrays D2H (page-locked); wall clock incl. Python API")}
-        eng.clear_basis()
-
-    # the other north-star system: the full Katsura-11 / F_32003 computation
-    # (the reference cannot finish it: its step 4 alone takes 1,556 s on one
-    # core).  Katsura-11 has 2^11 solutions, so the reduced basis must leave
-    # exactly 2048 standard monomials; steps 3-4 are pinned to the reference
-    # by tests/test_gpu_parity.py::test_large_step_replay.
     k11 = None
-    if rank == 0 and not args.no_katsura11:
-        from paper_2601_06765_b200.groebner import f4_groebner as _f4
-        from paper_2601_06765_b200.systems import format_system, gen_katsura
+    if rank == 0 and not args.no_katsura11 and world == 1:
+        k11 = run_katsura11(peak, flush, torch)
 
-        sys.path.insert(0, os.path.join(ROOT, "tools"))
-        from full_run import standard_monomials
-
-        kring, kpolys = gen_katsura(11, 32003)
-        t0 = time.perf_counter()
-        kgb = _f4(kpolys, kring)
-        k11 = {"system": "Katsura-11 / F_32003, grevlex, full F4 + device interreduction",
-               "wall_s": round(time.perf_counter() - t0, 3), "gb_size": len(kgb),
-               "standard_monomials": standard_monomials([f.lm() for f in kgb], kring.n_vars),
-               "expected_standard_monomials": 2 ** 11,
-               "sha256": __import__("hashlib").sha256(format_system(kring, kgb).encode()).hexdigest(),
-               "reference": "does not finish (SURVEY.md 6.2: step 4 alone 1,556 s)"}
-
-    # kernel capability at large M: the reference's own microbenchmarks
-    # (fpgb.bench.microbench, SURVEY.md §8d "synthetic dict_build") on the
-    # device primitives, inputs resident in HBM (larger than L2)
     micro = None
-    if rank == 0 and not args.no_micro:
+    if rank == 0 and not args.no_micro and world == 1:
         from paper_2601_06765_b200.bench import microbench
 
         micro = []
@@ -610,33 +681,137 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        s = cpu_sample()
-        if s["t_sym"] > 0:
-            cpu = {"value": s["M"] / s["t_sym"], "unit": UNIT, "cores": 1, "kind": "port",
-                   "sample": f"cyclic-8 F4 steps {s['steps']} from reference snapshots, NumPy oracle port, "
-                             f"compile {s['t_sym']:.2f}s + psge {s['t_num']:.2f}s"}
+        cpu = cpu_baseline_line()
     if rank == 0:
+        ranked = sorted(kprof.items(), key=lambda kv: -kv[1][1])
         kernels = {k: {"launches": v[0], "ms": round(v[1] / 1e6, 3)} for k, v in ranked[:12]}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong" if shard is not None else "weak",
             "vs_baseline": None, "dtype": "u32 residues mod p (u64 monomial keys)",
             "data": "synthetic (generated cyclic-8 system, deterministic)",
             "config": {"workload": WORKLOAD, "batches": len(batches), "sum_M_per_step": total_M,
-                       "parallelism": "replicas" if world > 1 else "single",
-                       "l2": "flushed (256 MiB write) before every batch"},
+                       "parallelism": (f"sharded compile_batch over {world} ranks (NCCL)" if shard is not None
+                                       else ("replicas" if world > 1 else "single")),
+                       "l2": "flushed (256 MiB write) before every batch",
+                       "replay_check": "every replayed batch's (r, N, M, closure_rounds) == the live run's"},
             "reduction_s_per_f4_step": red_s,
-            "symbolic_roofline": {"B_sym_bytes_per_step": B_sym, "frac": sym_frac, "peak": peak},
+            "reduction_mode": "NEW_ONLY (rows with new leads, what f4_step consumes)",
+            "reduction_full_rref": elim_full,
+            "symbolic_roofline": {"B_sym_bytes_per_step": int(Bs.sum()), "W_reference_key_words": W,
+                                  "frac": sym_frac, "peak": peak, "steps_named": sym_named},
+            "symbolic_per_step": sym_steps,
             "roofline": roof, "roofline_symbolic": roof_sym, "cpu_baseline": cpu, "e2e": e2e,
             "clocks": clk.summary(),
             "gpu_launches": launches1 - launches0, "wall_ms_per_step": 1000 * wall / args.steps,
-            "debug_slowest": (sorted(_dbg, key=lambda x: -(x[1] + x[2]))[:8] if _dbg else None),
-            "setup_s": round(setup_s, 2), "full_run": full_run, "full_run_katsura11": k11, "kernels_top": kernels,
+            "setup_s": round(setup_s, 2), "full_run": full_run, "katsura11": k11, "kernels_top": kernels,
             "microbench": micro,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_e2e(args, ring, st, batches, eng, torch):
+    from paper_2601_06765_b200.engine import host_empty
+    from paper_2601_06765_b200.polynomials import SoaPolySet
+    from paper_2601_06765_b200.symbolic import compile_batch
+
+    final = st.soa()
+
+    def pinned(a):
+        out = host_empty(a.shape, a.dtype)
+        out[...] = a
+        return out
+
+    f_key, f_coeff, f_exps = pinned(final.mon_key), pinned(final.coeff), pinned(final.exps)
+    n = ring.n_vars
+    h2d = d2h = 0
+    e_sym = 0.0
+    e_M = 0
+    for it in range(args.e2e_steps + 1):  # iteration 0 warms the host caches, untimed
+        if it == 1:
+            h2d = d2h = e_M = 0
+            e_sym = 0.0
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        eng.clear_basis()
+        prev_nt = prev_nb = 0
+        for b in batches:
+            nb_, nt = b["n_basis"], b["n_terms"]
+            soa = SoaPolySet(ring, f_key[:nt], f_coeff[:nt], final.offset[:nb_ + 1], final.length[:nb_],
+                             f_exps[:nt])
+            plan = compile_batch(b["rows"], soa)
+            rp, ci, va = plan.row_ptr, plan.col_ind, plan.val
+            dk = plan.dict_keys
+            e_M += b["M"]
+            # bytes moved: new basis terms as the reference streams them
+            # (int64 exps + uint64 coeff, narrowed on the device), their
+            # lengths + offsets, back their LM / max exponents; rows (basis
+            # index + shift); back: row_ptr / col_ind / val (64-bit) and
+            # dict_keys (reference key words)
+            h2d += (nt - prev_nt) * (8 * n + 8) + (nb_ - prev_nb) * 16 + len(b["rows"]) * (4 + 2 * n)
+            d2h += ((nb_ - prev_nb) * 4 * n + (plan.counters.r + 1) * 8 + plan.counters.M * 16
+                    + plan.counters.N * 8 * ring.n_key_words)
+            prev_nt, prev_nb = nt, nb_
+            del rp, ci, va, dk, plan
+        torch.cuda.synchronize()
+        e_sym += time.perf_counter() - t0
+    eng.clear_basis()
+    eng.sync_basis(final)
+    return {"value": e_M / e_sym, "unit": UNIT, "h2d_bytes_per_step": h2d // args.e2e_steps,
+            "d2h_bytes_per_step": d2h // args.e2e_steps,
+            "note": ("per step: empty device basis, then per batch the new basis polys + rows H2D, "
+                     "compile_batch, LayoutPlan arrays D2H (page-locked); wall clock incl. Python API")}
+
+
+def run_katsura11(peak, flush, torch):
+    """The other north-star system: the full Katsura-11 / F_32003 run (the
+    reference cannot finish it: step 4 alone takes 1,556 s on one core), then
+    warm replays of its largest steps s5-s9 (per-step symbolic time and B_sym
+    fraction, W = 4 reference key words)."""
+    import hashlib
+
+    from paper_2601_06765_b200.engine import Engine
+    from paper_2601_06765_b200.groebner import reduce_basis_device
+    from paper_2601_06765_b200.systems import format_system, gen_katsura
+
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    from full_run import standard_monomials
+
+    ring, polys = gen_katsura(11, 32003)
+    t0 = time.perf_counter()
+    st, batches, loop_s = capture_run(ring, polys)
+    gb = reduce_basis_device(st.basis, ring)
+    wall = time.perf_counter() - t0
+    eng = Engine.for_ring(ring)
+    eng.sync_basis(st.soa())
+    W = ring.n_key_words
+    steps = {}
+    for k in range(5, min(10, len(batches))):
+        b = batches[k]
+        ts = []
+        for rep in range(3):
+            flush.fill_(1)
+            plan = eng.compile(b["rb"], b["sh"], True, list(range(b["n_basis"])))
+            inf = plan.info
+            assert (inf["r"], inf["N"], inf["M"], inf["closure_rounds"]) == (b["r"], b["N"], b["M"], b["rounds"])
+            ts.append(inf["dict_build_ns"] + inf["row_assemble_ns"])
+            ech = eng.psge_plan(plan, full=False)
+            t_num = ech.info()["numeric_ns"]
+        t = min(ts[1:])
+        steps[str(k)] = {"M": b["M"], "B_sym": b_sym(b, W), "t_sym_us": round(t / 1e3, 1),
+                         "frac": round(b_sym(b, W) / (t * 1e-9) / 1e9 / peak, 4),
+                         "first_touch_us": round(ts[0] / 1e3, 1), "numeric_ms": round(t_num / 1e6, 3)}
+    return {"system": "Katsura-11 / F_32003, grevlex, full F4 + device interreduction",
+            "wall_s": round(wall, 3), "f4_loop_s": round(loop_s, 3), "steps": len(batches), "gb_size": len(gb),
+            "standard_monomials": standard_monomials([f.lm() for f in gb], ring.n_vars),
+            "expected_standard_monomials": 2 ** 11,
+            "sha256": hashlib.sha256(format_system(ring, gb).encode()).hexdigest(),
+            "live_sym_ms_per_step": [round((b.get("t_sym_ns") or 0) / 1e6, 3) for b in batches],
+            "warm_replays": steps,
+            "reference": "does not finish (SURVEY.md 6.2: step 4 alone 1,556 s)"}
 
 
 if __name__ == "__main__":

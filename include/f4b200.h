@@ -66,6 +66,16 @@ int f4b_ctx_create(int device, uint32_t p, int n_vars, int order, f4b_alloc_fn a
 int f4b_ctx_destroy(f4b_ctx* ctx);
 int f4b_ctx_set_stream(f4b_ctx* ctx, void* cuda_stream);
 const char* f4b_ctx_last_error(const f4b_ctx* ctx);
+/* Path selection (no reference counterpart: the reference has one path per
+ * function).  Every setting computes the same bytes; the non-default ones
+ * force the fallback kernels the automatic choice takes for shapes the
+ * default path does not fit, so tests can reach them:
+ *   "sweep"       0 auto | 1 blocked C-row sweep | 2 generic k_sweep
+ *   "dense"       0 pivot-block RREF(D') | 1 per-pivot k_dense_forward
+ *   "fbsp"        0 one cooperative k_fbsp | 1 multi-launch rank pipeline
+ *   "dict_sort"   1 = radix-sort dictionary for grevlex too
+ *   "dict_nohash" 1 = f4b_dict_build without its duplicate filter */
+int f4b_ctx_set_option(f4b_ctx* ctx, const char* name, int64_t value);
 /* Instrumentation: when enabled, every kernel launch is bracketed by CUDA
  * events on the context stream; profile_read resolves them into lines
  * "kernel launches total_ns" and reports the total launch count. */

@@ -56,6 +56,7 @@ SIGNATURES = {
     "f4b_ctx_destroy": (C.c_int, [C.c_void_p]),
     "f4b_ctx_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
     "f4b_ctx_last_error": (C.c_char_p, [C.c_void_p]),
+    "f4b_ctx_set_option": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int64]),
     "f4b_ctx_profile": (C.c_int, [C.c_void_p, C.c_int]),
     "f4b_ctx_profile_read": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int64, i64p]),
     "f4b_basis_clear": (C.c_int, [C.c_void_p]),

@@ -204,6 +204,9 @@ __global__ void k_spmm(Fp fp, const u32* __restrict__ rp, const u32* __restrict_
 void spmm(Ctx* c, long long r, long long N, const int64_t* rp, const int64_t* col, const uint64_t* val,
           const uint64_t* X, long long b, uint64_t* Y) {
   const long long M = rp[r];
+  // the device CSR holds u32 offsets / columns (row_ptr, col_ind)
+  if (M < 0 || M >= (1ll << 32) - 1 || N >= (1ll << 32) - 1 || r >= (1ll << 32) - 1)
+    fail(F4B_ERR_SIZE_CAP, "spmm: nnz, rows and columns must stay below 2^32 - 1");
   std::vector<u32> hrp(r + 1), hcol(std::max<long long>(M, 1)), hval(std::max<long long>(M, 1));
   std::vector<u32> hx(std::max<long long>(N * b, 1)), hy(std::max<long long>(r * b, 1));
   for (long long i = 0; i <= r; ++i) hrp[i] = (u32)rp[i];
@@ -287,6 +290,9 @@ int f4b_ctx_create(int device, uint32_t p, int n_vars, int order, f4b_alloc_fn a
     int sms = 0;
     check_cuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "sm count");
     c->num_sms = sms;
+    if (const char* e = getenv("F4B_DICT")) c->opt_dict_sort = !strcmp(e, "sort");
+    if (const char* e = getenv("F4B_FBSP")) c->opt_fbsp = !strcmp(e, "multi");
+    if (getenv("F4B_DICT_NOHASH")) c->opt_dict_nohash = 1;
     // Montgomery constants: p * p' = -1 mod 2^32, R^2 mod p
     uint32_t x = 1;
     for (int i = 0; i < 6; ++i) x = x * (2u - p * x);
@@ -362,6 +368,31 @@ int f4b_ctx_set_stream(f4b_ctx* h, void* stream) {
   }
   h->c.stream = (cudaStream_t)stream;
   return F4B_OK;
+}
+
+int f4b_ctx_set_option(f4b_ctx* h, const char* name, int64_t value) {
+  if (!h || !name) return F4B_ERR_PRECONDITION;
+  Ctx* c = &h->c;
+  struct {
+    const char* n;
+    int* p;
+    int64_t hi;
+  } opts[] = {{"sweep", &c->opt_sweep, 2},
+              {"dense", &c->opt_dense, 1},
+              {"fbsp", &c->opt_fbsp, 1},
+              {"dict_sort", &c->opt_dict_sort, 1},
+              {"dict_nohash", &c->opt_dict_nohash, 1}};
+  for (auto& o : opts)
+    if (!strcmp(o.n, name)) {
+      if (value < 0 || value > o.hi) {
+        c->last_error = std::string("option value out of range: ") + name;
+        return F4B_ERR_PRECONDITION;
+      }
+      *o.p = (int)value;
+      return F4B_OK;
+    }
+  c->last_error = std::string("unknown option: ") + name;
+  return F4B_ERR_PRECONDITION;
 }
 
 int f4b_ctx_profile(f4b_ctx* h, int enable) {

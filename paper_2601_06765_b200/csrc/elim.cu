@@ -77,65 +77,9 @@ static constexpr int SW_THREADS = 256;
 static inline unsigned nb(long long n, int t) { return (unsigned)std::max<long long>(1, (n + t - 1) / t); }
 
 // ---------------------------------------------------------------------------
-// E1: pivot selection and structure
-// ---------------------------------------------------------------------------
-__global__ void k_pivot_select(const u32* __restrict__ rp, const u32* __restrict__ col, long long r,
-                               unsigned long long* __restrict__ pk) {
-  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= r) return;
-  u32 s = rp[i], e = rp[i + 1];
-  if (e == s) return;
-  atomicMin(pk + col[s], ((unsigned long long)(e - s) << 32) | (unsigned long long)i);
-}
-
-__global__ void k_col_structure(Fp fp, const unsigned long long* __restrict__ pk, long long N, const u32* __restrict__ rp,
-                                const u32* __restrict__ val, u32* __restrict__ prow, u32* __restrict__ invl,
-                                uint4* __restrict__ desc, uint8_t* __restrict__ isA, uint8_t* __restrict__ notA) {
-  long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= N) return;
-  unsigned long long k = pk[c];
-  bool a = k != ~0ull;
-  u32 row = a ? (u32)(k & 0xFFFFFFFFull) : NONE;
-  prow[c] = row;
-  const u32 inv = a ? fp.inv(val[rp[row]]) : 0u;
-  invl[c] = inv;
-  // packed sweep descriptor: tail range of the pivot row + inverse lead
-  desc[c] = a ? make_uint4(rp[row] + 1, rp[row + 1], inv, row) : make_uint4(0, 0, 0, NONE);
-  isA[c] = a ? 1 : 0;
-  notA[c] = a ? 0 : 1;
-}
-
-__global__ void k_bits(const uint8_t* __restrict__ isA, long long N, u32* __restrict__ bits) {
-  long long w = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (w * 32 >= N) return;
-  u32 b = 0;
-  for (int j = 0; j < 32; ++j) {
-    long long c = w * 32 + j;
-    if (c < N && isA[c]) b |= 1u << j;
-  }
-  bits[w] = b;
-}
-
-__global__ void k_c_flags(const u32* __restrict__ rp, const u32* __restrict__ col, const u32* __restrict__ prow,
-                          long long r, uint8_t* __restrict__ flags) {
-  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= r) return;
-  u32 s = rp[i], e = rp[i + 1];
-  flags[i] = (e > s && prow[col[s]] != (u32)i) ? 1 : 0;
-}
-
-__global__ void k_compact_idx(const uint8_t* __restrict__ flags, const u32* __restrict__ pos, long long n,
-                              u32* __restrict__ out) {
-  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n && flags[i]) out[pos[i]] = (u32)i;
-}
-
-// ---------------------------------------------------------------------------
 // E1 fused (one cooperative launch): pivot selection, column structure, the
 // A-column bitmap, A / non-A column lists (ascending), A-column positions and
-// the C-row list — the work of k_pivot_select, k_col_structure, k_bits, two
-// flag scans, three compactions and k_c_flags, with 4 grid barriers and one
-// host read of (nA, nC) instead of two.
+// the C-row list, with 4 grid barriers and one host read of (nA, nC).
 // ---------------------------------------------------------------------------
 struct PrepOut {
   u32 nA, nC;
@@ -1002,88 +946,6 @@ __global__ void __launch_bounds__(256) k_sweep_win(Fp fp, u32 mu, const u32* __r
 }
 
 // ---------------------------------------------------------------------------
-// E2, warp per row: one warp sweeps one C row with its own shared-memory
-// accumulator, so a pivot application needs no CTA barrier (only __syncwarp).
-// The pivot tail is loaded SWW_UNR entries per lane at a time — all loads in
-// flight before the read-modify-writes (tail columns are distinct, so lanes
-// never collide).  Same pivot order and arithmetic as k_sweep<0>: the D' row
-// is bit-identical.
-// ---------------------------------------------------------------------------
-static constexpr int SWW_UNR = 8;
-template <typename T>
-__global__ void __launch_bounds__(128) k_sweep_warp(Fp fp, const u32* __restrict__ rp, const u32* __restrict__ col,
-                                                    const u32* __restrict__ val, u32 N, const u32* __restrict__ rows,
-                                                    u32 nrows, const uint4* __restrict__ desc,
-                                                    const u32* __restrict__ abits_g, u32* __restrict__ Dp, u32 K,
-                                                    const u32* __restrict__ nonA, unsigned long long* __restrict__ stats) {
-  extern __shared__ __align__(16) u32 smem[];
-  const u32 nwords = (N + 31) / 32;
-  u32* abits = smem;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpc = blockDim.x >> 5;
-  T* acc = reinterpret_cast<T*>(smem + ((nwords + 3) & ~3u)) + (size_t)warp * ((N + 7) & ~7u);
-  for (u32 w = threadIdx.x; w < nwords; w += blockDim.x) abits[w] = abits_g[w];
-  __syncthreads();
-  unsigned long long n_piv = 0, n_tail = 0;
-  for (u32 rr = blockIdx.x * wpc + warp; rr < nrows; rr += gridDim.x * wpc) {
-    const u32 i = rows[rr];
-    const u32 s = rp[i], e = rp[i + 1];
-    const u32 lead = col[s];
-    for (u32 c = lead + lane; c < N; c += 32) acc[c] = 0;
-    __syncwarp();
-    for (u32 k = s + lane; k < e; k += 32) acc[col[k]] = (T)val[k];
-    __syncwarp();
-    u32 from = lead;
-    while (true) {
-      // next nonzero A column >= from (warp ballot over 32 columns)
-      u32 c = N, av = 0;
-      for (u32 c0 = from & ~31u; c0 < N; c0 += 32) {
-        const u32 cc = c0 + lane;
-        const u32 v = (cc >= from && cc < N) ? (u32)acc[cc] : 0u;
-        const bool hit = v != 0 && ((abits[cc >> 5] >> (cc & 31)) & 1u);
-        const unsigned b = __ballot_sync(0xffffffffu, hit);
-        if (b) {
-          const int src = __ffs(b) - 1;
-          av = __shfl_sync(0xffffffffu, v, src);
-          c = c0 + src;
-          break;
-        }
-      }
-      if (c >= N) break;
-      const uint4 d = __ldg(desc + c);
-      const u32 fm = fp.to_mont(fp.neg(fp.mul(av, d.z)));
-      ++n_piv;
-      n_tail += d.y - d.x;
-      for (u32 k0 = d.x; k0 < d.y; k0 += 32 * SWW_UNR) {
-        u32 cc[SWW_UNR], vv[SWW_UNR];
-#pragma unroll
-        for (int q = 0; q < SWW_UNR; ++q) {
-          const u32 k = k0 + q * 32 + lane;
-          cc[q] = k < d.y ? __ldg(col + k) : N;
-          vv[q] = k < d.y ? __ldg(val + k) : 0u;
-        }
-#pragma unroll
-        for (int q = 0; q < SWW_UNR; ++q)
-          if (cc[q] < N) acc[cc[q]] = (T)fp.add((u32)acc[cc[q]], fp.mont_mul(fm, vv[q]));
-      }
-      __syncwarp();
-      // acc[c] is cancelled by construction (never read again: later tails
-      // start right of their leads and D' reads non-A columns only)
-      from = c + 1;
-    }
-    u32* out = Dp + (size_t)rr * K;
-    for (u32 q = lane; q < K; q += 32) {
-      const u32 cc = nonA[q];
-      out[q] = cc >= lead ? (u32)acc[cc] : 0u;
-    }
-    __syncwarp();
-  }
-  if (stats && lane == 0 && n_piv) {
-    atomicAdd(stats, n_piv);
-    atomicAdd(stats + 1, n_tail);
-  }
-}
-
-// ---------------------------------------------------------------------------
 // E3a: cooperative forward elimination of the dense block D' (R x K)
 // ---------------------------------------------------------------------------
 // One grid barrier per PIVOT (not per column): every CTA keeps the leading
@@ -1178,362 +1040,6 @@ __global__ void __launch_bounds__(256) k_dense_forward(Fp fp, u32* Dp, u32 R, u3
   }
 }
 
-// E3a (CTA-cooperative rows): the per-pivot schedule of k_dense_forward, but
-// each row update is done by the whole CTA (K / 256 elements per thread, all
-// loads in flight) and the row's new leading column comes out of the update
-// itself (per-thread first nonzero, block min) — the per-pivot critical path
-// is one grid barrier + one pivot-row round trip instead of a warp-serial
-// sweep over K.  Row state (lead, used) lives in shared memory.
-static constexpr int DF_MAXROWS = 64;
-__global__ void __launch_bounds__(256) k_dense_forward_cta(Fp fp, u32* Dp, u32 R, u32 K, unsigned long long* cand,
-                                                           u32* piv_of_col) {
-  cg::grid_group grid = cg::this_grid();
-  __shared__ u32 s_lead[DF_MAXROWS];
-  __shared__ uint8_t s_used[DF_MAXROWS];
-  __shared__ u32 s_red[8];
-  __shared__ u32 s_inv;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const u32 G = gridDim.x;
-  const u32 lo = (u32)(((unsigned long long)R * blockIdx.x) / G);
-  const u32 hi = (u32)(((unsigned long long)R * (blockIdx.x + 1)) / G);
-  const u32 nr = hi - lo;
-  // first nonzero of row i at or after `from`, by the whole CTA
-  auto block_first = [&](const u32* row, u32 from) -> u32 {
-    u32 f = K;
-    for (u32 q = from + tid; q < K; q += blockDim.x)
-      if (row[q]) {
-        f = q;
-        break;
-      }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) f = min(f, __shfl_xor_sync(0xffffffffu, f, o));
-    if (lane == 0) s_red[warp] = f;
-    __syncthreads();
-    u32 m = K;
-    for (int w = 0; w < 8; ++w) m = min(m, s_red[w]);
-    __syncthreads();
-    return m;
-  };
-  for (u32 r = 0; r < nr; ++r) {
-    const u32 l = block_first(Dp + (size_t)(lo + r) * K, 0);
-    if (tid == 0) {
-      s_lead[r] = l;
-      s_used[r] = 0;
-    }
-  }
-  __syncthreads();
-  for (u32 step = 0;; ++step) {
-    if (tid == 0) {
-      unsigned long long m = ~0ull;
-      for (u32 r = 0; r < nr; ++r)
-        if (!s_used[r] && s_lead[r] < K) m = min(m, ((unsigned long long)s_lead[r] << 32) | (lo + r));
-      if (m != ~0ull) atomicMin(cand + step, m);
-    }
-    grid.sync();
-    const unsigned long long win = __ldcg(cand + step);
-    if (win == ~0ull) break;
-    const u32 c = (u32)(win >> 32), pr = (u32)(win & 0xFFFFFFFFull);
-    const u32* prow_p = Dp + (size_t)pr * K;
-    if (tid == 0) {
-      s_inv = fp.inv(__ldcg(prow_p + c));
-      if (pr >= lo && pr < hi) {
-        s_used[pr - lo] = 1;
-        piv_of_col[c] = pr;
-      }
-    }
-    __syncthreads();
-    const u32 inv = s_inv;
-    for (u32 r = 0; r < nr; ++r) {
-      if (s_used[r] || s_lead[r] != c) continue;
-      u32* row = Dp + (size_t)(lo + r) * K;
-      const u32 fm = fp.to_mont(fp.neg(fp.mul(row[c], inv)));
-      // row[q] += fm * prow[q] for q >= c; track this thread's first nonzero > c
-      u32 f = K;
-      for (u32 qb = c + tid; qb < K; qb += blockDim.x * 8) {
-        u32 pv[8], rv[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const u32 q = qb + blockDim.x * j;
-          pv[j] = q < K ? __ldcg(prow_p + q) : 0u;
-          rv[j] = q < K ? row[q] : 0u;
-        }
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const u32 q = qb + blockDim.x * j;
-          if (q < K) {
-            const u32 nv = fp.add(rv[j], fp.mont_mul(fm, pv[j]));
-            row[q] = nv;
-            if (nv && q > c && q < f) f = q;
-          }
-        }
-      }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) f = min(f, __shfl_xor_sync(0xffffffffu, f, o));
-      if (lane == 0) s_red[warp] = f;
-      __syncthreads();
-      if (tid == 0) {
-        u32 m = K;
-        for (int w = 0; w < 8; ++w) m = min(m, s_red[w]);
-        s_lead[r] = m;
-      }
-      __syncthreads();
-    }
-  }
-}
-
-// E3a (shared-memory rows): one CTA per SM holds a contiguous block of D'
-// rows in shared memory for the whole elimination.  Per pivot: every CTA
-// publishes its best candidate row (min (lead, row)) to a per-CTA slot in
-// global memory and bids for it with one 64-bit atomicMin; ONE grid barrier;
-// every CTA stages the winning row from its owner's slot (L2) into shared
-// memory and updates its rows leading at that column all at once,
-// row <- a*row - b*pivot with a = the pivot's lead, b = the row's entry (a
-// nonzero scaling keeps the row space, so no inverse on the critical path),
-// tracking each row's new lead in the same pass.  Pivot rows are frozen and
-// written back to D' (the echelon basis k_dense_piv_info / k_dense_back read).
-static constexpr int DS_THREADS = 512;
-static constexpr int DS_MAXROWS = 64;
-__global__ void __launch_bounds__(DS_THREADS) k_dense_fwd_smem(Fp fp, u32* __restrict__ Dp, u32 R, u32 K, u32 rpc,
-                                                               unsigned long long* __restrict__ cand,
-                                                               u32* __restrict__ slots, u32* __restrict__ piv_of_col) {
-  cg::grid_group grid = cg::this_grid();
-  extern __shared__ __align__(16) u32 smem[];
-  constexpr int NW = DS_THREADS / 32;
-  const unsigned FULL = 0xffffffffu;
-  const u32 Kp = (K + 3) & ~3u;
-  u32* prow = smem;       // [Kp] the current pivot row
-  u32* rows = smem + Kp;  // [rpc][Kp] this CTA's rows
-  __shared__ u32 s_lead[DS_MAXROWS];
-  __shared__ uint8_t s_used[DS_MAXROWS];
-  __shared__ u32 s_red[NW][DS_MAXROWS];
-  __shared__ unsigned long long s_cand;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const u32 lo = blockIdx.x * rpc;
-  const u32 nr = lo < R ? min(rpc, R - lo) : 0u;
-  for (u32 r = 0; r < nr; ++r)
-    for (u32 q = tid; q < K; q += DS_THREADS) rows[(size_t)r * Kp + q] = Dp[(size_t)(lo + r) * K + q];
-  __syncthreads();
-  for (u32 r = 0; r < nr; ++r) {
-    u32 f = K;
-    for (u32 q = tid; q < K; q += DS_THREADS)
-      if (rows[(size_t)r * Kp + q]) {
-        f = q;
-        break;
-      }
-    f = __reduce_min_sync(FULL, f);
-    if (lane == 0) s_red[warp][r] = f;
-  }
-  __syncthreads();
-  if (tid < (int)nr) {
-    u32 m = K;
-    for (int w = 0; w < NW; ++w) m = min(m, s_red[w][tid]);
-    s_lead[tid] = m;
-    s_used[tid] = 0;
-  }
-  __syncthreads();
-  for (u32 step = 0;; ++step) {
-    if (warp == 0) {
-      unsigned long long m = ~0ull;
-      for (u32 r = lane; r < nr; r += 32)
-        if (!s_used[r] && s_lead[r] < K) m = min(m, ((unsigned long long)s_lead[r] << 32) | (lo + r));
-#pragma unroll
-      for (int o = 16; o; o >>= 1) m = min(m, __shfl_xor_sync(FULL, m, o));
-      if (lane == 0) s_cand = m;
-    }
-    __syncthreads();
-    const unsigned long long mine = s_cand;
-    // slots are double-buffered by step parity: a CTA publishes step s+1's
-    // candidate while slower CTAs may still copy step s's pivot row
-    const u32 par = step & 1;
-    if (mine != ~0ull) {
-      const u32 r = (u32)(mine & 0xFFFFFFFFull) - lo, l = (u32)(mine >> 32);
-      u32* slot = slots + ((size_t)par * gridDim.x + blockIdx.x) * Kp;
-      for (u32 q = l + tid; q < K; q += DS_THREADS) __stcg(slot + q, rows[(size_t)r * Kp + q]);
-      __syncthreads();
-      if (tid == 0) atomicMin(cand + step, mine);
-    }
-    grid.sync();
-    const unsigned long long win = __ldcg(cand + step);
-    if (win == ~0ull) break;
-    const u32 c = (u32)(win >> 32), pr = (u32)(win & 0xFFFFFFFFull);
-    const u32 owner = pr / rpc;
-    const u32* oslot = slots + ((size_t)par * gridDim.x + owner) * Kp;
-    for (u32 q = c + tid; q < K; q += DS_THREADS) prow[q] = __ldcg(oslot + q);
-    if (owner == blockIdx.x) {
-      for (u32 q = c + tid; q < K; q += DS_THREADS) Dp[(size_t)pr * K + q] = rows[(size_t)(pr - lo) * Kp + q];
-      if (tid == 0) {
-        s_used[pr - lo] = 1;
-        piv_of_col[c] = pr;
-      }
-    }
-    __syncthreads();
-    const u32 am = fp.to_mont(prow[c]);
-    bool any = false;
-    for (u32 r = 0; r < nr; ++r) {
-      if (s_used[r] || s_lead[r] != c) continue;
-      any = true;
-      u32* row = rows + (size_t)r * Kp;
-      const u32 bm = fp.to_mont(fp.neg(row[c]));
-      u32 f = K;
-      for (u32 q0 = c + 1 + tid; q0 < K; q0 += 4 * DS_THREADS) {
-        u32 xv[4], pv[4];
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          const u32 q = q0 + h * DS_THREADS;
-          xv[h] = q < K ? row[q] : 0u;
-          pv[h] = q < K ? prow[q] : 0u;
-        }
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          const u32 q = q0 + h * DS_THREADS;
-          if (q < K) {
-            const u32 nv = fp.add(fp.mont_mul(am, xv[h]), fp.mont_mul(bm, pv[h]));
-            row[q] = nv;
-            if (nv && f == K) f = q;
-          }
-        }
-      }
-      f = __reduce_min_sync(FULL, f);
-      if (lane == 0) s_red[warp][r] = f;
-    }
-    if (any) {
-      __syncthreads();
-      if (tid < (int)nr && !s_used[tid] && s_lead[tid] == c) {
-        u32 m = K;
-        for (int w = 0; w < NW; ++w) m = min(m, s_red[w][tid]);
-        s_lead[tid] = m;
-      }
-    }
-    __syncthreads();
-  }
-}
-
-// E3a (rounds): every live row whose leading column has no pivot claims it
-// (lowest row index wins, one atomicMin per row) and computes the inverse of
-// its own lead; then every other live row is reduced by the pivot of its
-// leading column, again and again, until its lead is a pivot-less column or
-// the row is zero.  Pivot rows are frozen once claimed.  All distinct leads
-// are claimed in the same round, so the grid barriers are 2 x rounds instead
-// of 1 per pivot; any echelon basis has the same RREF (k_dense_back).
-// Warp per row (rows stay with their warp for the whole kernel).
-__global__ void __launch_bounds__(256) k_dense_rounds(Fp fp, u32* Dp, u32 R, u32 K, u32* __restrict__ piv_of_col,
-                                                      u32* __restrict__ rinv, u32* __restrict__ active) {
-  cg::grid_group grid = cg::this_grid();
-  const int lane = threadIdx.x & 31;
-  const u32 W = gridDim.x * (blockDim.x >> 5);
-  const u32 gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  constexpr int RPW = 4;  // rows per warp kept in registers
-  u32 lead[RPW];
-  bool piv[RPW];
-#pragma unroll
-  for (int q = 0; q < RPW; ++q) {
-    const u32 i = gw + q * W;
-    lead[q] = i < R ? first_nonzero_warp(Dp + (size_t)i * K, 0, K) : K;
-    piv[q] = false;
-  }
-  for (u32 round = 0;; ++round) {
-    // A: claim pivot-less leading columns; inverse of the own lead
-#pragma unroll
-    for (int q = 0; q < RPW; ++q) {
-      const u32 i = gw + q * W;
-      if (i >= R || piv[q] || lead[q] >= K) continue;
-      if (lane == 0) {
-        rinv[i] = fp.inv(Dp[(size_t)i * K + lead[q]]);
-        if (__ldcg(piv_of_col + lead[q]) == NONE) atomicMin(piv_of_col + lead[q], i);
-      }
-    }
-    grid.sync();
-    // C: reduce until the lead is pivot-less (or the row is zero)
-    u32 live = 0;
-#pragma unroll
-    for (int q = 0; q < RPW; ++q) {
-      const u32 i = gw + q * W;
-      if (i >= R || piv[q] || lead[q] >= K) continue;
-      u32* row = Dp + (size_t)i * K;
-      u32 c = lead[q];
-      u32 pr = __ldcg(piv_of_col + c);
-      if (pr == i) {
-        piv[q] = true;
-        continue;
-      }
-      while (c < K && pr != NONE) {
-        const u32 fm = fp.to_mont(fp.neg(fp.mul(row[c], __ldcg(rinv + pr))));
-        row_axpy8(fp, row, Dp + (size_t)pr * K, fm, c + lane, K);
-        __syncwarp();
-        c = first_nonzero_warp(row, c + 1, K);
-        pr = c < K ? __ldcg(piv_of_col + c) : NONE;
-      }
-      lead[q] = c;
-      live += c < K;
-    }
-    if (lane == 0 && live) atomicAdd(active + round, live);
-    grid.sync();
-    if (__ldcg(active + round) == 0) break;
-  }
-}
-
-// E3a' (small D'): the same pivot-to-pivot elimination inside ONE thread-block
-// cluster: candidates are exchanged through distributed shared memory and the
-// per-pivot barrier is a cluster barrier (hardware, ~sub-µs) instead of a
-// grid-wide one.  Slots are double-buffered by step parity, so one barrier
-// per pivot suffices; pivot rows are frozen, read with ld.global.cg.
-__global__ void __launch_bounds__(1024) k_dense_forward_cluster(Fp fp, u32* Dp, u32 R, u32 K, u32* lead,
-                                                               uint8_t* used, u32* piv_of_col) {
-  cg::cluster_group cl = cg::this_cluster();
-  __shared__ unsigned long long slot[2];
-  __shared__ unsigned long long wmin[32];
-  __shared__ u32 s_inv;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-  const u32 cs = cl.num_blocks(), me = cl.block_rank();
-  const u32 lo = (u32)(((unsigned long long)R * me) / cs);
-  const u32 hi = (u32)(((unsigned long long)R * (me + 1)) / cs);
-  for (u32 i = lo + warp; i < hi; i += nwarps) {
-    const u32 l = first_nonzero_warp(Dp + (size_t)i * K, 0, K);
-    if (lane == 0) lead[i] = l;
-  }
-  __syncthreads();
-  for (u32 step = 0;; ++step) {
-    const int par = step & 1;
-    unsigned long long m = ~0ull;
-    for (u32 i = lo + tid; i < hi; i += blockDim.x)
-      if (!used[i] && lead[i] < K) m = min(m, ((unsigned long long)lead[i] << 32) | i);
-#pragma unroll
-    for (int o = 16; o; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (lane == 0) wmin[warp] = m;
-    __syncthreads();
-    if (tid == 0) {
-      unsigned long long mm = ~0ull;
-      for (int w = 0; w < nwarps; ++w) mm = min(mm, wmin[w]);
-      slot[par] = mm;
-    }
-    cl.sync();
-    unsigned long long win = ~0ull;
-    for (u32 rk = 0; rk < cs; ++rk) win = min(win, *cl.map_shared_rank(&slot[par], rk));
-    if (win == ~0ull) break;
-    const u32 c = (u32)(win >> 32), pr = (u32)(win & 0xFFFFFFFFull);
-    const u32* prow_p = Dp + (size_t)pr * K;
-    if (tid == 0) {
-      s_inv = fp.inv(__ldcg(prow_p + c));
-      if (pr >= lo && pr < hi) {
-        used[pr] = 1;
-        piv_of_col[c] = pr;
-      }
-    }
-    __syncthreads();
-    const u32 inv = s_inv;
-    for (u32 i = lo + warp; i < hi; i += nwarps) {
-      if (used[i] || lead[i] != c) continue;
-      u32* row = Dp + (size_t)i * K;
-      const u32 fm = fp.to_mont(fp.neg(fp.mul(row[c], inv)));
-      row_axpy8(fp, row, prow_p, fm, c + lane, K);
-      __syncwarp();
-      const u32 l = first_nonzero_warp(row, c + 1, K);
-      if (lane == 0) lead[i] = l;
-    }
-    __syncthreads();
-  }
-  cl.sync();  // keep every CTA's shared slots alive until all have read them
-}
 
 // E3b: back-substitution -> RREF(D') rows (dense), one CTA per pivot.
 __global__ void __launch_bounds__(SW_THREADS) k_dense_back(Fp fp, const u32* __restrict__ Dp, u32 K,
@@ -1586,286 +1092,6 @@ __global__ void __launch_bounds__(SW_THREADS) k_dense_back(Fp fp, const u32* __r
   }
 }
 
-__global__ void k_fill_u32(u32* __restrict__ p, long long n, u32 v) {
-  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) p[i] = v;
-}
-
-__global__ void k_dense_pivots(const u32* __restrict__ piv_of_col, u32 K, uint8_t* __restrict__ flags) {
-  long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (q < K) flags[q] = piv_of_col[q] != NONE;
-}
-
-__global__ void k_dense_piv_info(Fp fp, const u32* __restrict__ Dp, u32 K, const u32* __restrict__ piv_of_col,
-                                 u32* __restrict__ pinv, const uint8_t* __restrict__ flags, const u32* __restrict__ pos,
-                                 u32* __restrict__ dpiv, u32* __restrict__ dprow) {
-  long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= K) return;
-  u32 pr = piv_of_col[q];
-  pinv[q] = pr != NONE ? fp.inv(Dp[(size_t)pr * K + q]) : 0u;
-  if (flags[q]) {
-    dpiv[pos[q]] = (u32)q;
-    dprow[pos[q]] = pr;
-  }
-}
-
-// ---------------------------------------------------------------------------
-// E3 (chunked RREF): RREF(D') with the basis kept fully reduced at all times.
-//
-// A row is reduced by a basis in reduced echelon form in ONE step: its
-// coefficients are its own entries at the basis' pivot columns
-// (x <- x - sum_j x[piv_j] B_j), so that step is a parallel product, not a
-// pivot-by-pivot chain.  Rows are taken from a queue in chunks of CH:
-//   A  (all CTAs) reduce the chunk's rows by the basis, one CTA per row
-//   B  (CTA 0)    RREF of the ≤ CH residual rows in shared memory (one warp
-//                 per row; the only sequential pivot loop left); the new
-//                 rows are appended to the basis
-//   C  (all CTAs) the old basis rows reduced by the new rows (RREF again)
-// A chunk that adds no pivot switches to a bulk step: every remaining row is
-// reduced at once and only the nonzero residuals stay queued (the rank of D'
-// concentrates in its first rows; a few late pivots come back through the
-// compacted queue).  RREF is unique, so the rows equal the reference's.  At
-// the end the basis is emitted in ascending pivot order (Rd, dpiv, rank).
-// ---------------------------------------------------------------------------
-struct RrefState {
-  u32 rho, rho_old, nnew, qh, qn, mode, done, pad;
-};
-static constexpr int RR_THREADS = 1024;
-static constexpr int RR_MAXCH = 32;
-template <bool SMALLP>
-__global__ void __launch_bounds__(RR_THREADS, 1) k_dense_rref(Fp fp, u32* __restrict__ Dp, u32 R, u32 K, u32 CH,
-                                                           u32* __restrict__ Bm, u32* __restrict__ bpiv,
-                                                           u32* __restrict__ queue, RrefState* __restrict__ st,
-                                                           u32* __restrict__ Rd, u32* __restrict__ dpiv,
-                                                           u32* __restrict__ rank_out, u32* __restrict__ colpiv) {
-  cg::grid_group grid = cg::this_grid();
-  extern __shared__ __align__(16) u32 smem[];
-  const unsigned FULL = 0xffffffffu;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const u32 G = gridDim.x;
-  const u32 p = fp.p;
-  __shared__ u32 s_nz, s_piv, s_cnt, s_lead[RR_MAXCH], s_used[RR_MAXCH], s_npiv[RR_MAXCH], s_nrow[RR_MAXCH];
-  __shared__ u32 red[33];
-  // x <- x - sum_{j<nb} x[piv(j)] * Brow(j), over all K columns, one CTA;
-  // coefficients gathered into shared memory first (nonzero ones only)
-  u32* s_cj = smem;             // [K] coefficient values (compacted)
-  u32* s_jj = smem + K;         // [K] their basis row indices
-  auto reduce_row = [&](u32* x, u32 j0, u32 nb) {
-    if (tid == 0) s_nz = 0;
-    __syncthreads();
-    for (u32 j = tid; j < nb; j += blockDim.x) {
-      const u32 v = __ldcg(x + __ldcg(bpiv + j0 + j));
-      if (v) {
-        const u32 s = atomicAdd(&s_nz, 1u);
-        s_cj[s] = SMALLP ? v : fp.to_mont(v);
-        s_jj[s] = j0 + j;
-      }
-    }
-    __syncthreads();
-    const u32 nz = s_nz;
-    if (nz) {
-      for (u32 q = tid; q < K; q += blockDim.x) {
-        if (SMALLP) {
-          unsigned long long acc = 0;
-          u32 t = 0;
-          for (; t + 4 <= nz; t += 4) {
-            acc += (unsigned long long)s_cj[t] * __ldcg(Bm + (size_t)s_jj[t] * K + q);
-            acc += (unsigned long long)s_cj[t + 1] * __ldcg(Bm + (size_t)s_jj[t + 1] * K + q);
-            acc += (unsigned long long)s_cj[t + 2] * __ldcg(Bm + (size_t)s_jj[t + 2] * K + q);
-            acc += (unsigned long long)s_cj[t + 3] * __ldcg(Bm + (size_t)s_jj[t + 3] * K + q);
-          }
-          for (; t < nz; ++t) acc += (unsigned long long)s_cj[t] * __ldcg(Bm + (size_t)s_jj[t] * K + q);
-          const u32 a = (u32)(acc % p);
-          x[q] = fp.sub(__ldcg(x + q), a);
-        } else {
-          u32 a = 0;
-          for (u32 t = 0; t < nz; ++t) a = fp.add(a, fp.mont_mul(s_cj[t], __ldcg(Bm + (size_t)s_jj[t] * K + q)));
-          x[q] = fp.sub(__ldcg(x + q), a);
-        }
-      }
-    }
-    __syncthreads();
-  };
-  if (blockIdx.x == 0 && tid == 0) {
-    st->rho = st->rho_old = st->nnew = 0;
-    st->qh = 0;
-    st->qn = R;
-    st->mode = 0;
-    st->done = 0;
-  }
-  for (u32 i = blockIdx.x * blockDim.x + tid; i < R; i += G * blockDim.x) queue[i] = i;
-  grid.sync();
-  while (true) {
-    const u32 qh = __ldcg(&st->qh), qn = __ldcg(&st->qn), rho = __ldcg(&st->rho), mode = __ldcg(&st->mode);
-    if (qh >= qn) break;
-    const u32 cnt = mode ? qn - qh : min(CH, qn - qh);
-    // A: reduce the taken rows by the basis
-    if (rho)
-      for (u32 k = blockIdx.x; k < cnt; k += G) reduce_row(Dp + (size_t)__ldcg(queue + qh + k) * K, 0, rho);
-    grid.sync();
-    if (mode) {
-      // bulk step: keep the nonzero residuals queued (CTA 0, in order)
-      if (blockIdx.x == 0) {
-        u32 outn = 0;
-        for (u32 k0 = 0; k0 < cnt; k0 += blockDim.x / 32) {
-          const u32 k = k0 + warp;
-          bool nzr = false;
-          u32 row = 0;
-          if (k < cnt) {
-            row = __ldcg(queue + qh + k);
-            const u32* x = Dp + (size_t)row * K;
-            bool any = false;
-            for (u32 b0 = 0; b0 < K && !any; b0 += 32) any = __any_sync(FULL, b0 + lane < K && __ldcg(x + b0 + lane) != 0);
-            nzr = any;
-          }
-          // order-preserving compaction of the warps' rows
-          if (lane == 0) s_used[warp] = nzr ? 1u : 0u;
-          __syncthreads();
-          u32 pre = 0, tot = 0;
-          for (u32 w = 0; w < blockDim.x / 32; ++w) {
-            if (w < (u32)warp) pre += s_used[w];
-            tot += s_used[w];
-          }
-          __syncthreads();
-          if (lane == 0 && nzr) queue[outn + pre] = row;  // outn + pre <= qh + k: never ahead of a pending read
-          outn += tot;
-          __syncthreads();
-        }
-        if (tid == 0) {
-          st->qh = 0;
-          st->qn = outn;
-          st->mode = 0;
-        }
-      }
-      grid.sync();
-      continue;
-    }
-    // B: RREF of the chunk's residual rows in shared memory (CTA 0)
-    if (blockIdx.x == 0) {
-      u32* X = smem;  // [CH][K]
-      for (u32 w = 0; w < cnt; ++w) {
-        const u32* x = Dp + (size_t)__ldcg(queue + qh + w) * K;
-        for (u32 q = tid; q < K; q += blockDim.x) X[(size_t)w * K + q] = __ldcg(x + q);
-      }
-      __syncthreads();
-      if ((u32)warp < cnt) {
-        const u32* x = X + (size_t)warp * K;
-        u32 l = K;
-        for (u32 b0 = 0; b0 < K; b0 += 32) {
-          const unsigned m = __ballot_sync(FULL, b0 + lane < K && x[b0 + lane] != 0);
-          if (m) {
-            l = b0 + __ffs(m) - 1;
-            break;
-          }
-        }
-        if (lane == 0) {
-          s_lead[warp] = l;
-          s_used[warp] = 0;
-        }
-      }
-      if (tid == 0) s_cnt = 0;
-      __syncthreads();
-      while (true) {
-        if (warp == 0) {
-          unsigned long long m = ~0ull;
-          if ((u32)lane < cnt && !s_used[lane] && s_lead[lane] < K)
-            m = ((unsigned long long)s_lead[lane] << 32) | (u32)lane;
-#pragma unroll
-          for (int o = 16; o; o >>= 1) m = min(m, __shfl_xor_sync(FULL, m, o));
-          if (lane == 0) s_piv = m == ~0ull ? NONE : (u32)(m & 0xFFFFFFFFull);
-        }
-        __syncthreads();
-        const u32 pw = s_piv;
-        if (pw == NONE) break;
-        const u32 c = s_lead[pw];
-        u32* prw = X + (size_t)pw * K;
-        if (warp == (int)pw) {
-          const u32 inv = fp.to_mont(fp.inv(prw[c]));
-          for (u32 q = c + lane; q < K; q += 32) prw[q] = fp.mont_mul(prw[q], inv);
-          if (lane == 0) {
-            s_used[pw] = 1;
-            s_npiv[s_cnt] = c;
-            s_nrow[s_cnt] = pw;
-            s_cnt = s_cnt + 1;
-          }
-        }
-        __syncthreads();
-        if ((u32)warp < cnt && warp != (int)pw) {
-          u32* x = X + (size_t)warp * K;
-          const u32 f = x[c];
-          if (f) {
-            const u32 fm = fp.to_mont(p - f);
-            for (u32 q = c + 1 + lane; q < K; q += 32) x[q] = fp.add(x[q], fp.mont_mul(fm, prw[q]));
-            __syncwarp();
-            if (lane == 0) x[c] = 0;
-            __syncwarp();
-            if (!s_used[warp]) {
-              u32 l = K;
-              for (u32 b0 = (c + 1) & ~31u; b0 < K; b0 += 32) {
-                const u32 q = b0 + lane;
-                const unsigned m = __ballot_sync(FULL, q > c && q < K && x[q] != 0);
-                if (m) {
-                  l = b0 + __ffs(m) - 1;
-                  break;
-                }
-              }
-              if (lane == 0) s_lead[warp] = l;
-            }
-          }
-        }
-        __syncthreads();
-      }
-      const u32 nn = s_cnt;
-      for (u32 k = 0; k < nn; ++k) {
-        const u32* src = X + (size_t)s_nrow[k] * K;
-        u32* dst = Bm + (size_t)(rho + k) * K;
-        for (u32 q = tid; q < K; q += blockDim.x) dst[q] = src[q];
-      }
-      if (tid < (int)nn) {
-        bpiv[rho + tid] = s_npiv[tid];
-        colpiv[s_npiv[tid]] = rho + tid;
-      }
-      if (tid == 0) {
-        st->rho_old = rho;
-        st->rho = rho + nn;
-        st->nnew = nn;
-        st->qh = qh + cnt;
-        st->mode = nn ? 0u : 1u;
-      }
-    }
-    grid.sync();
-    // C: the old basis rows reduced by the new rows (keeps the basis RREF)
-    {
-      const u32 nn = __ldcg(&st->nnew), ro = __ldcg(&st->rho_old);
-      if (nn && ro)
-        for (u32 i = blockIdx.x; i < ro; i += G) reduce_row(Bm + (size_t)i * K, ro, nn);
-    }
-    grid.sync();
-  }
-  // emit: basis rows in ascending pivot order (CTA 0 orders, all copy)
-  const u32 rho = __ldcg(&st->rho);
-  if (blockIdx.x == 0) {
-    u32 base = 0;
-    for (u32 q0 = 0; q0 < K; q0 += blockDim.x) {
-      const u32 q = q0 + tid;
-      const u32 j = q < K ? __ldcg(colpiv + q) : NONE;
-      u32 tot;
-      const u32 pre = block_scan_flag(j != NONE ? 1u : 0u, red, &tot);
-      if (j != NONE) {
-        dpiv[base + pre] = q;
-        queue[base + pre] = j;  // queue reused: position -> basis row
-      }
-      base += tot;
-    }
-    if (tid == 0) *rank_out = rho;
-  }
-  grid.sync();
-  for (u32 k = blockIdx.x; k < rho; k += G) {
-    const u32* src = Bm + (size_t)__ldcg(queue + k) * K;
-    u32* dst = Rd + (size_t)k * K;
-    for (u32 q = tid; q < K; q += blockDim.x) dst[q] = __ldcg(src + q);
-  }
-}
 
 // ---------------------------------------------------------------------------
 // E3 (default): RREF(D') in pivot BLOCKS.
@@ -2332,11 +1558,10 @@ static void launch_sweep(Ctx* c, const Fp& fp, f4b_echelon* E, const u32* rows, 
                          unsigned long long* cursor, u32* s_off, u32* s_len, u32* err,
                          unsigned long long* stats = nullptr) {
   const u32 N = (u32)E->n_cols;
-  static const char* sweep_env = getenv("F4B_SWEEP");
-  static const bool cta_sweep = sweep_env && !strcmp(sweep_env, "cta");
-  static const bool warp_sweep = sweep_env && !strcmp(sweep_env, "warp");
-  static const bool blk_sweep = sweep_env && !strcmp(sweep_env, "blk");
-  if (MODE == 0 && !cta_sweep && !warp_sweep && !blk_sweep && E->nA > 0) {
+  // c->opt_sweep (f4b_ctx_set_option "sweep"): 0 = automatic (windows, then
+  // the blocked sweep, then k_sweep), 1 = start at the blocked sweep,
+  // 2 = k_sweep only — the fallbacks are forced by the parity tests
+  if (MODE == 0 && c->opt_sweep == 0 && E->nA > 0) {
     // fixed windows with precomputed block inverses (k_win_build + k_sweep_win)
     const size_t nwords = (N + 31) / 32;
     const size_t smem = (size_t)((2 * nwords + 3) & ~(size_t)3) * 4 + (size_t)(N + 1) * 4;
@@ -2393,7 +1618,7 @@ static void launch_sweep(Ctx* c, const Fp& fp, f4b_echelon* E, const u32* rows, 
       return;
     }
   }
-  if (MODE == 0 && !cta_sweep && !warp_sweep) {
+  if (MODE == 0 && c->opt_sweep <= 1) {
     // blocked sweep: lazily reduced u32 accumulator needs p * (nA + 1) < 2^32
     const size_t bitmap = (size_t)((((N + 31) / 32) + 3) & ~3u) * 4;
     const size_t smem = bitmap + (size_t)N * 4;
@@ -2410,35 +1635,6 @@ static void launch_sweep(Ctx* c, const Fp& fp, f4b_echelon* E, const u32* rows, 
       F4B_LAUNCH(c, k_sweep_blk, grid, 256, smem, fp, mu, E->rp, E->col, E->val, N, rows, nrows, E->desc.as<uint4>(),
                  E->abits.as<u32>(), E->acols.as<u32>(), E->apos.as<u32>(), (u32)E->nA, Dp, K, E->nonA.as<u32>(),
                  stats);
-      return;
-    }
-  }
-  if (MODE == 0 && warp_sweep) {
-    // warp per C row; warps per CTA from the accumulator footprint
-    const bool small_p = c->p < 65536u;
-    const size_t tb = small_p ? 2 : 4;
-    const size_t bitmap = (size_t)((((N + 31) / 32) + 3) & ~3u) * 4;
-    const size_t per_warp = (size_t)((N + 7) & ~7u) * tb;
-    if (bitmap + per_warp <= 200 * 1024) {
-      const int wpc = (int)std::max<size_t>(1, std::min<size_t>(4, (200 * 1024 - bitmap) / per_warp));
-      const size_t smem = bitmap + per_warp * wpc;
-      const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(16 / wpc, (220 * 1024) / (smem + 1024)));
-      const int grid = (int)std::max<long long>(
-          1, std::min<long long>((nrows + wpc - 1) / wpc, (long long)c->num_sms * per_sm));
-      static bool wattr = false;
-      if (!wattr) {
-        check_cuda(cudaFuncSetAttribute(k_sweep_warp<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        200 * 1024 + 4096), "attr");
-        check_cuda(cudaFuncSetAttribute(k_sweep_warp<u32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        200 * 1024 + 4096), "attr");
-        wattr = true;
-      }
-      if (small_p)
-        F4B_LAUNCH(c, k_sweep_warp<uint16_t>, grid, 32 * wpc, smem, fp, E->rp, E->col, E->val, N, rows, nrows,
-                   E->desc.as<uint4>(), E->abits.as<u32>(), Dp, K, E->nonA.as<u32>(), stats);
-      else
-        F4B_LAUNCH(c, k_sweep_warp<u32>, grid, 32 * wpc, smem, fp, E->rp, E->col, E->val, N, rows, nrows,
-                   E->desc.as<uint4>(), E->abits.as<u32>(), Dp, K, E->nonA.as<u32>(), stats);
       return;
     }
   }
@@ -2556,76 +1752,10 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
     launch_sweep<0>(c, fp, E, crows.as<u32>(), (u32)R, Dp.as<u32>(), (u32)K, nullptr, 0, nullptr, nullptr, nullptr, 0,
                     nullptr, nullptr, nullptr, err, E->stats.as<unsigned long long>());
     mark("sweep launched");
-    static const bool dp_stats = getenv("F4B_DP_STATS") != nullptr;
-    if (dp_stats) {  // diagnostic: shape of D' after the sweep (host copy)
-      std::vector<u32> h((size_t)R * K);
-      check_cuda(cudaMemcpyAsync(h.data(), Dp.p, h.size() * 4, cudaMemcpyDeviceToHost, c->stream), "d2h");
-      check_cuda(cudaStreamSynchronize(c->stream), "sync");
-      long long nz_rows = 0, nnz = 0;
-      std::vector<int> leads;
-      for (long long i = 0; i < R; ++i) {
-        long long l = -1, cnt = 0;
-        for (long long q = 0; q < K; ++q)
-          if (h[(size_t)i * K + q]) {
-            if (l < 0) l = q;
-            ++cnt;
-          }
-        if (l >= 0) {
-          ++nz_rows;
-          leads.push_back((int)l);
-        }
-        nnz += cnt;
-      }
-      std::sort(leads.begin(), leads.end());
-      long long distinct = std::unique(leads.begin(), leads.end()) - leads.begin();
-      fprintf(stderr, "[dp] R=%lld K=%lld nonzero_rows=%lld distinct_leads=%lld density=%.3f\n", R, K, nz_rows,
-              distinct, R * K ? (double)nnz / (double)(R * K) : 0.0);
-      if (getenv("F4B_DP_PROFILE") && R * K <= (1ll << 24)) {
-        // rank profile: rows in order, incremental RREF basis (host, diagnostic)
-        const unsigned long long P = c->p;
-        std::vector<std::vector<unsigned long long>> basis;
-        std::vector<long long> bpiv, newat;
-        for (long long i = 0; i < R; ++i) {
-          std::vector<unsigned long long> x(h.begin() + i * K, h.begin() + (i + 1) * K);
-          for (size_t b = 0; b < basis.size(); ++b) {
-            const unsigned long long f = x[bpiv[b]];
-            if (!f) continue;
-            for (long long q = 0; q < K; ++q) x[q] = (x[q] + (P - f) * basis[b][q]) % P;
-          }
-          long long l = -1;
-          for (long long q = 0; q < K; ++q)
-            if (x[q]) { l = q; break; }
-          if (l < 0) continue;
-          unsigned long long inv = 1, bb = x[l], e = P - 2;
-          while (e) { if (e & 1) inv = inv * bb % P; bb = bb * bb % P; e >>= 1; }
-          for (auto& v : x) v = v * inv % P;
-          for (size_t b = 0; b < basis.size(); ++b) {
-            const unsigned long long f = basis[b][l];
-            if (!f) continue;
-            for (long long q = 0; q < K; ++q) basis[b][q] = (basis[b][q] + (P - f) * x[q]) % P;
-          }
-          basis.push_back(x);
-          bpiv.push_back(l);
-          newat.push_back(i);
-        }
-        fprintf(stderr, "[dp]   rank=%zu new pivots at rows:", basis.size());
-        for (size_t k = 0; k < newat.size(); k += std::max<size_t>(1, newat.size() / 16)) fprintf(stderr, " %lld", newat[k]);
-        if (!newat.empty()) fprintf(stderr, " last=%lld", newat.back());
-        fprintf(stderr, "\n");
-      }
-    }
-    // E3 alternative (opt-in, F4B_DENSE=rref): chunked RREF with a fully
-    // reduced basis (k_dense_rref).  Measured slower than the per-pivot path
-    // on cyclic-8 (18.7 vs 10.4 ms per replay step): the rank of D' arrives
-    // at ~1 pivot per 15 rows, so almost every 27-row chunk pays its three
-    // grid barriers and a latency-bound row reduction for ~2 pivots.
-    const long long CHr = std::min<long long>(RR_MAXCH, (195ll * 1024) / (4 * std::max<long long>(K, 1)));
-    static const bool rref_on = getenv("F4B_DENSE") && !strcmp(getenv("F4B_DENSE"), "rref");
-    // default E3: pivot blocks of distinct leads (k_dense_blk); F4B_DENSE=<any>
-    // keeps the measured alternatives below
-    static const char* dense_sel = getenv("F4B_DENSE");
+    // E3 default: RREF(D') in pivot blocks (k_dense_blk); c->opt_dense = 1
+    // (f4b_ctx_set_option "dense") forces the general fallback below
     bool blk_done = false;
-    if (!dense_sel && R > 0 && K > 0 && R < (1ll << 30) && K < (1ll << 30)) {
+    if (c->opt_dense == 0 && R > 0 && K > 0 && R < (1ll << 30) && K < (1ll << 30)) {
       static int blk_occ = -1;
       static bool blk_attr = false;
       if (!blk_attr) {
@@ -2692,49 +1822,6 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
       }
     }
     if (blk_done) {
-    } else if (rref_on && CHr >= 8 && R < (1ll << 31) && K < (1ll << 30)) {
-      const long long rmax = std::max<long long>(1, std::min(R, K));
-      const size_t smem_r = (size_t)std::max<long long>(2 * K, CHr * K) * 4;
-      static bool rr_attr = false;
-      if (!rr_attr) {
-        check_cuda(cudaFuncSetAttribute(k_dense_rref<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
-                   "attr");
-        check_cuda(cudaFuncSetAttribute(k_dense_rref<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
-                   "attr");
-        rr_attr = true;
-      }
-      DBuf Bm, bp, qu, stt, colp;
-      ensure(c, Bm, (size_t)rmax * K * sizeof(u32));
-      ensure(c, bp, (size_t)rmax * sizeof(u32));
-      ensure(c, qu, (size_t)(std::max(R, K) + 16) * sizeof(u32));
-      ensure(c, stt, sizeof(RrefState) + 16);
-      ensure(c, colp, (size_t)K * sizeof(u32));
-      check_cuda(cudaMemsetAsync(colp.p, 0xFF, (size_t)K * sizeof(u32), c->stream), "memset");
-      ensure(c, E->Rd, (size_t)rmax * K * sizeof(u32));
-      ensure(c, E->dpiv, (size_t)rmax * sizeof(u32));
-      ensure(c, E->rdev, 16);
-      fp = make_fp(c);
-      u32* dpp = Dp.as<u32>();
-      u32 Ru = (u32)R, Ku = (u32)K, CHu = (u32)CHr;
-      u32* bmp = Bm.as<u32>();
-      u32* bpp = bp.as<u32>();
-      u32* qp = qu.as<u32>();
-      RrefState* sp = reinterpret_cast<RrefState*>(stt.p);
-      u32* rdp = E->Rd.as<u32>();
-      u32* dpivp = E->dpiv.as<u32>();
-      u32* rkp = E->rdev.as<u32>();
-      u32* colpp = colp.as<u32>();
-      void* args[] = {&fp, &dpp, &Ru, &Ku, &CHu, &bmp, &bpp, &qp, &sp, &rdp, &dpivp, &rkp, &colpp};
-      {
-        ProfScope ps(c, "k_dense_rref");
-        const void* kf = c->p < 65536u ? (const void*)k_dense_rref<true> : (const void*)k_dense_rref<false>;
-        check_cuda(cudaLaunchCooperativeKernel(kf, c->num_sms, RR_THREADS, args, smem_r, c->stream), "k_dense_rref");
-      }
-      release(c, Bm);
-      release(c, bp);
-      release(c, qu);
-      release(c, stt);
-      release(c, colp);
     } else {
     // E3a: cooperative forward elimination
     ensure(c, used, (size_t)R + 16);
@@ -2754,116 +1841,7 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
     uint8_t* usedp = used.as<uint8_t>();
     u32* pofcp = pofc.as<u32>();
     void* args[] = {&fp, &dpp, &Ru, &Ku, &candp, &leadp, &usedp, &pofcp};
-    // Grid-wide cooperative kernel by default.  The 16-CTA cluster variant
-    // (F4B_DENSE_CLUSTER=1) has cheaper barriers but measured slower on the
-    // cyclic-8 batches (profiles/r01/NOTES.md): per-pivot work, not the
-    // barrier, dominates once the loads are pipelined.
-    bool done_cluster = false;
-    if (R <= 16384 && (long long)R * K <= (64ll << 20) && getenv("F4B_DENSE_CLUSTER")) {
-      static int cl_ok = -1;
-      if (cl_ok < 0) {
-        cl_ok = cudaFuncSetAttribute(k_dense_forward_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
-                cudaSuccess;
-        cudaGetLastError();
-      }
-      for (int csz : {16, 8}) {
-        if (csz == 16 && !cl_ok) continue;
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(csz);
-        cfg.blockDim = dim3(1024);
-        cfg.dynamicSmemBytes = 0;
-        cfg.stream = c->stream;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = csz;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        ProfScope ps(c, "k_dense_forward");
-        cudaError_t e = cudaLaunchKernelEx(&cfg, k_dense_forward_cluster, fp, dpp, Ru, Ku, leadp, usedp, pofcp);
-        if (e == cudaSuccess) {
-          done_cluster = true;
-          break;
-        }
-        cudaGetLastError();
-      }
-    }
-    // default: rows resident in shared memory (k_dense_fwd_smem) when every
-    // SM's row block fits
-    static const char* dense_env = getenv("F4B_DENSE");
-    if (!done_cluster && (!dense_env || !strcmp(dense_env, "smem"))) {
-      const size_t Kp = (size_t)((K + 3) & ~3ll);
-      static const int ds_cps = getenv("F4B_DS_CPS") ? atoi(getenv("F4B_DS_CPS")) : 1;
-      const long long gmax = (long long)c->num_sms * std::max(1, ds_cps);
-      const long long rpc = (R + gmax - 1) / gmax;
-      const size_t smem_ds = (size_t)(rpc + 1) * Kp * 4;
-      if (rpc <= DS_MAXROWS && smem_ds <= 200 * 1024) {
-        static bool ds_attr = false;
-        if (!ds_attr) {
-          check_cuda(cudaFuncSetAttribute(k_dense_fwd_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
-                     "attr");
-          ds_attr = true;
-        }
-        const int GD = (int)((R + rpc - 1) / rpc);
-        DBuf slots;
-        ensure(c, slots, (size_t)2 * GD * Kp * sizeof(u32));
-        u32 rpcu = (u32)rpc;
-        u32* slotp = slots.as<u32>();
-        void* args4[] = {&fp, &dpp, &Ru, &Ku, &rpcu, &candp, &slotp, &pofcp};
-        {
-          ProfScope ps(c, "k_dense_fwd_smem");
-          check_cuda(cudaLaunchCooperativeKernel((void*)k_dense_fwd_smem, GD, DS_THREADS, args4, smem_ds, c->stream),
-                     "k_dense_fwd_smem");
-        }
-        release(c, slots);
-        done_cluster = true;
-      }
-    }
-    // CTA-cooperative per-pivot kernel when every CTA's row range fits
-    // its shared row state
-    static const bool dense_warp = getenv("F4B_DENSE") && !strcmp(getenv("F4B_DENSE"), "warp");
-    int bpc = 0;
-    check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpc, k_dense_forward_cta, 256, 0), "occupancy");
-    static const int dcta = getenv("F4B_DENSE_CTAS") ? atoi(getenv("F4B_DENSE_CTAS")) : 4;
-    const int GC = (int)std::min<long long>((long long)c->num_sms * std::max(1, std::min(bpc, dcta)),
-                                            std::max<long long>(R, 1));
-    // narrow D' blocks keep the warp-per-row kernel (a CTA per 459-wide row
-    // update idles most of its threads)
-    if (!done_cluster && !dense_warp && K >= 1024 && (long long)R <= (long long)GC * DF_MAXROWS) {
-      void* args3[] = {&fp, &dpp, &Ru, &Ku, &candp, &pofcp};
-      ProfScope ps(c, "k_dense_forward_cta");
-      check_cuda(cudaLaunchCooperativeKernel((void*)k_dense_forward_cta, GC, 256, args3, 0, c->stream),
-                 "k_dense_forward_cta");
-      done_cluster = true;
-    }
-    // F4B_DENSE=rounds: claim-all-leads rounds (2 grid barriers per round
-    // instead of 1 per pivot) — measured slower on cyclic-8 (a row reduced by
-    // many pivots becomes one warp's serial chain), kept as an option
-    static const bool rounds = getenv("F4B_DENSE") && !strcmp(getenv("F4B_DENSE"), "rounds");
-    if (!done_cluster && rounds) {
-      int bpr = 0;
-      check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpr, k_dense_rounds, 256, 0), "occupancy");
-      const int GR = c->num_sms * std::max(1, std::min(bpr, 2));
-      if ((long long)R <= 4ll * GR * 8) {
-        DBuf rinv, active;
-        ensure(c, rinv, (size_t)R * sizeof(u32));
-        ensure(c, active, (size_t)(K + 2) * sizeof(u32));
-        check_cuda(cudaMemsetAsync(active.p, 0, (size_t)(K + 2) * sizeof(u32), c->stream), "memset");
-        u32* rinvp = rinv.as<u32>();
-        u32* actp = active.as<u32>();
-        void* args2[] = {&fp, &dpp, &Ru, &Ku, &pofcp, &rinvp, &actp};
-        {
-          ProfScope ps(c, "k_dense_rounds");
-          check_cuda(cudaLaunchCooperativeKernel((void*)k_dense_rounds, GR, 256, args2, 0, c->stream),
-                     "k_dense_rounds");
-        }
-        release(c, rinv);
-        release(c, active);
-        done_cluster = true;
-      }
-    }
-    if (!done_cluster) {
+    {
       ProfScope ps(c, "k_dense_forward");
       check_cuda(cudaLaunchCooperativeKernel((void*)k_dense_forward, G, 256, args, 0, c->stream), "k_dense_forward");
     }
@@ -2945,7 +1923,9 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
     check_cuda(cudaMemcpyAsync(&ht->err, err, 4, cudaMemcpyDeviceToHost, c->stream), "d2h");
     check_cuda(cudaStreamSynchronize(c->stream), "sync");
     if (!(ht->err & DEVERR_CAPACITY)) break;
-    E->pool_cap *= 2;
+    if (attempt == 7) fail(F4B_ERR_OOM, "psge: nonpivot row pool still overflows after 8 resizes");
+    // the cursor counts every requested slot, also past the capacity
+    E->pool_cap = std::max<size_t>(2 * E->pool_cap, (size_t)ht->used_pool + 1024);
   }
   mark("tail synced");
   E->rankD = ht->rankD;
@@ -3012,6 +1992,7 @@ static void run_a_sweep(Ctx* c, f4b_echelon* E) {
                       E->a_len.as<u32>(), err);
       u32 e = read_u32(c, err);
       if (!(e & DEVERR_CAPACITY)) break;
+      if (attempt == 7) fail(F4B_ERR_OOM, "psge: pivot row pool still overflows after 8 resizes");
       unsigned long long tot = 0;
       check_cuda(cudaMemcpy(&tot, E->cursor.p, 8, cudaMemcpyDeviceToHost), "d2h");
       E->pool_cap = std::max<size_t>(2 * E->pool_cap, (size_t)tot + 1024);
@@ -3062,6 +2043,9 @@ f4b_echelon* psge_csr(Ctx* c, long long r, long long N, const int64_t* rp, const
   try {
     long long M = rp[r];
     E->M = M;
+    // the elimination kernels index rows, columns and nonzeros with u32
+    if (M < 0 || M >= (1ll << 32) - 1 || N >= (1ll << 31) || r >= (1ll << 31))
+      fail(F4B_ERR_SIZE_CAP, "psge: nnz must stay below 2^32 - 1, rows and columns below 2^31");
     std::vector<u32> hrp(r + 1), hcol(std::max<long long>(M, 1)), hval(std::max<long long>(M, 1));
     for (long long i = 0; i <= r; ++i) hrp[i] = (u32)rp[i];
     for (long long k = 0; k < M; ++k) {

@@ -91,6 +91,14 @@ struct Ctx {
   } pend;
   cudaStream_t stream = 0;
   int num_sms = 148;
+  // path selection (f4b_ctx_set_option); the defaults are the measured best
+  // paths, the others are the fallbacks the automatic choice takes when a
+  // shape does not fit, forced here so the parity tests reach every kernel
+  int opt_sweep = 0;        // "sweep": 0 auto, 1 blocked sweep, 2 k_sweep only
+  int opt_dense = 0;        // "dense": 0 pivot blocks (k_dense_blk), 1 k_dense_forward
+  int opt_fbsp = 0;         // "fbsp": 0 one cooperative k_fbsp, 1 multi-launch rank path
+  int opt_dict_sort = 0;    // "dict_sort": 1 = radix-sort dictionary even for grevlex
+  int opt_dict_nohash = 0;  // "dict_nohash": 1 = f4b_dict_build without the duplicate filter
   std::string last_error;
   Basis basis;
   // pinned host scratch for round counters

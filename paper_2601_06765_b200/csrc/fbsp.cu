@@ -2369,11 +2369,8 @@ static unsigned long long binom_ull(int a, int b) {
 }
 
 // Eligibility of the rank path: grevlex and a rank space of <= 2^26 monomials.
-static bool rank_path_ok(int order, int n, long long D) {
-  if (order != 0 || D > 255) return false;
-  if (const char* e = getenv("F4B_DICT")) {
-    if (!strcmp(e, "sort")) return false;
-  }
+static bool rank_path_ok(const Ctx* c, int order, int n, long long D) {
+  if (order != 0 || D > 255 || c->opt_dict_sort) return false;
   return binom_ull(n + (int)D, n) <= (1ull << 26);
 }
 
@@ -3128,10 +3125,10 @@ void compile_batch(Ctx* c, long long r0, const int32_t* rb, const uint16_t* shif
   int KW = 1;
   while (64 * KW < bits) KW *= 2;
   if (KW > 8) fail(F4B_ERR_PRECONDITION, "batch degree too large for the device key format");
-  if (rank_path_ok(c->order, n, D)) {
-    // F4B_FBSP=multi: the multi-launch pipeline (kept as a cross-check)
-    static const bool multi = getenv("F4B_FBSP") && !strcmp(getenv("F4B_FBSP"), "multi");
-    if (multi) {
+  if (rank_path_ok(c, c->order, n, D)) {
+    // opt_fbsp = 1: the multi-launch pipeline (the same phases as separate
+    // launches; also the building blocks of the sharded compile, shard.cu)
+    if (c->opt_fbsp == 1) {
       switch (KW) {
         case 1: compile_rank<1>(c, f, (int)D, r0, rb, shift, closure, cand, dict_cap, pl); break;
         case 2: compile_rank<2>(c, f, (int)D, r0, rb, shift, closure, cand, dict_cap, pl); break;

@@ -240,8 +240,7 @@ long long dict_build(Ctx* c, const uint64_t* keys, long long n, int words, int k
   // table); packed keys with all 128 bits significant would collide with the
   // empty-slot marker, so they always take the full sort
   bool filtered = false;
-  static const bool no_filter = getenv("F4B_DICT_NOHASH") != nullptr;
-  if (!no_filter && words * key_bits < 128) {
+  if (!c->opt_dict_nohash && words * key_bits < 128) {
     int logc = 10;
     while (logc < HB_LOG_MAX && (1ll << logc) < 2 * n) ++logc;
     const u32 limit = 1u << (logc - 1);

@@ -143,8 +143,9 @@ def allgather_arrays(arr: np.ndarray) -> list:
     world = dist.get_world_size()
     dev = _dev()
     row_shape = arr.shape[1:]
-    as_bytes = arr.view(np.uint8).reshape(len(arr), -1) if arr.ndim > 1 else arr.view(np.uint8).reshape(len(arr), -1)
-    width = as_bytes.shape[1] if len(arr) else int(np.prod(row_shape, dtype=np.int64)) * arr.dtype.itemsize
+    width = int(np.prod(row_shape, dtype=np.int64)) * arr.dtype.itemsize
+    # (0, width) for an empty local array: reshape(0, -1) is ambiguous
+    as_bytes = arr.view(np.uint8).reshape(len(arr), width) if len(arr) else np.zeros((0, width), np.uint8)
     n = torch.tensor([len(arr)], dtype=torch.int64, device=dev)
     sizes = [torch.zeros_like(n) for _ in range(world)]
     dist.all_gather(sizes, n)

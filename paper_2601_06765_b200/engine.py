@@ -186,6 +186,18 @@ class Engine:
     """Device engine for one ring on one GPU."""
 
     _registry: dict = {}
+    _forced: dict = {}  # f4b_ctx_set_option settings applied to every engine
+
+    @classmethod
+    def force_option(cls, name: str, value: int):
+        """Apply a path-selection option (see set_option) to every engine,
+        existing and future; value 0 restores the automatic choice."""
+        if value:
+            cls._forced[name] = int(value)
+        else:
+            cls._forced.pop(name, None)
+        for eng in cls._registry.values():
+            eng.set_option(name, value)
 
     @classmethod
     def for_ring(cls, ring, device: int = 0) -> "Engine":
@@ -203,6 +215,8 @@ class Engine:
         self.uid = next(_ids)
         self.generation = 0
         self._reset_mirror()
+        for name, value in self._forced.items():
+            self.set_option(name, value)
 
     def _reset_mirror(self):
         # host mirror of the device basis: lengths + the appended chunks (no
@@ -213,6 +227,13 @@ class Engine:
         self._T = 0
         self._src = None
         self._src_refs = None
+
+    # -- path selection (f4b_ctx_set_option) ---------------------------------
+    def set_option(self, name: str, value: int):
+        """Force a fallback path ("sweep", "dense", "fbsp", "dict_sort",
+        "dict_nohash"; 0 = the automatic choice).  Every setting computes the
+        same bytes; the tests use this to reach every kernel."""
+        self.ctx.check(self.lib.f4b_ctx_set_option(self.ctx.h, name.encode(), int(value)), f"set_option {name}")
 
     # -- instrumentation -----------------------------------------------------
     def profile(self, enable: bool):

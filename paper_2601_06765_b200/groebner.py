@@ -432,7 +432,9 @@ def reduce_basis_device(polys: list, ring: Ring) -> list:
     soa = soa_pack(minimal, ring)
     zero = (0,) * ring.n_vars
     rows = [Row(zero, k, RowRole.SPOLY_HALF, 0) for k in range(len(minimal))]
-    plan = compile_batch(rows, soa, Closure.ONE_STEP_REDUCTION)
+    # the reference's normal-form loop has no dictionary cap: neither has this
+    # matrix (only the device's 2^30-term plan limit applies)
+    plan = compile_batch(rows, soa, Closure.ONE_STEP_REDUCTION, dict_cap=1 << 62)
     ech = psge_reduce(csr_from_plan(plan, ring.modulus))
     ex = plan.dict_exps()
     rp, ci = plan.row_ptr, plan.col_ind

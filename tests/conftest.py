@@ -61,3 +61,20 @@ def cuda():
 
     _build.build()
     return torch.device("cuda", 0)
+
+
+@pytest.fixture
+def force_option():
+    """Force a path-selection option (f4b_ctx_set_option) on every engine for
+    the duration of one test: force_option("dict_sort", 1)."""
+    from paper_2601_06765_b200.engine import Engine
+
+    touched = []
+
+    def _set(name, value):
+        Engine.force_option(name, value)
+        touched.append(name)
+
+    yield _set
+    for name in touched:
+        Engine.force_option(name, 0)

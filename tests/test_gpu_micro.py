@@ -85,7 +85,11 @@ def test_dict_build_filter_and_fallback(size, dup):
     microbench("dict_build", size, duplicate_rate=dup, seed=7, reps=1)
 
 
-def test_dict_build_filter_off_matches(monkeypatch):
+@pytest.mark.parametrize("nohash", [0, 1])
+def test_dict_build_filter_off_matches(force_option, nohash):
+    """dict_build with and without its duplicate filter (f4b_ctx_set_option
+    "dict_nohash") against np.unique."""
+    force_option("dict_nohash", nohash)
     rng = np.random.default_rng(11)
     keys = rng.integers(0, 1 << 20, (200_000, 2), dtype=np.uint64)
     keys[::3] = keys[5]

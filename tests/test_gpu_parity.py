@@ -106,13 +106,15 @@ def _random_poly(rng, ring, max_exp, terms):
     return poly_monic(poly_normalize(ts, ring))
 
 
-@pytest.fixture(params=["rank", "sort"])
-def dict_mode(request, monkeypatch):
-    """Both dictionary paths: rank bitmap (grevlex fast path) and radix sort."""
+@pytest.fixture(params=["rank", "sort", "multi"])
+def dict_mode(request, force_option):
+    """Every dictionary path: the rank bitmap in one cooperative k_fbsp
+    (grevlex default), the same phases as separate launches (the sharded
+    compile's building blocks) and the radix sort (lex / deglex default)."""
     if request.param == "sort":
-        monkeypatch.setenv("F4B_DICT", "sort")
-    else:
-        monkeypatch.delenv("F4B_DICT", raising=False)
+        force_option("dict_sort", 1)
+    elif request.param == "multi":
+        force_option("fbsp", 1)
     return request.param
 
 
@@ -249,9 +251,9 @@ def test_f4_steps_match_reference(cuda, name, gen, args):
 
 @pytest.mark.parametrize("name,gen,args", [("cyclic6_p32003", gen_cyclic, (6, 32003)),
                                            ("katsura6_p32003", gen_katsura, (6, 32003))])
-def test_f4_steps_match_reference_sort_path(cuda, monkeypatch, name, gen, args):
+def test_f4_steps_match_reference_sort_path(cuda, force_option, name, gen, args):
     """Same per-step digests with the radix-sort dictionary forced."""
-    monkeypatch.setenv("F4B_DICT", "sort")
+    force_option("dict_sort", 1)
     gold = load_golden(name)
     ring, polys = gen(*args)
     st = GroebnerState(ring)
@@ -266,8 +268,12 @@ def test_f4_steps_match_reference_sort_path(cuda, monkeypatch, name, gen, args):
 
 
 @pytest.mark.parametrize("name", ["cyclic8_p32003", "katsura11_p32003"])
-def test_large_step_replay_sort_path(cuda, monkeypatch, name):
-    monkeypatch.setenv("F4B_DICT", "sort")
+@pytest.mark.parametrize("option", [("dict_sort", 1), ("fbsp", 1), ("sweep", 1), ("sweep", 2), ("dense", 1)])
+def test_large_step_replay_fallback_paths(cuda, force_option, name, option):
+    """The north-star replays through every fallback path: radix-sort
+    dictionary, multi-launch rank pipeline, blocked / generic C-row sweeps and
+    the per-pivot D' elimination (each forced via f4b_ctx_set_option)."""
+    force_option(*option)
     test_large_step_replay(cuda, name)
 
 
@@ -398,21 +404,105 @@ def test_reduce_basis_device_matches_host(cuda, name, gen, args):
     assert hashlib.sha256(format_system(ring, dev).encode()).hexdigest() == load_golden(name)["final_sha256"]
 
 
+def _run_checking_steps(ring, polys, gold, max_checked=None):
+    """The F4 loop on the GPU, every step's (r, N, M, rounds), plan digest and
+    RREF digest against the reference's (up to max_checked steps)."""
+    st = GroebnerState(ring)
+    for f in polys:
+        update_pairs(st, poly_monic(f))
+    k = 0
+    steps = gold["steps"]
+    while st.n_pairs():
+        plan, ech, _ = f4_step(st)
+        if k < len(steps) and (max_checked is None or k < max_checked):
+            g = steps[k]
+            assert (plan.counters.r, plan.counters.N, plan.counters.M, plan.counters.closure_rounds) == \
+                (g["r"], g["N"], g["M"], g["closure_rounds"]), f"step {k}"
+            assert ech.rank == g["rank"], f"rank step {k}"
+            assert plan_digest(plan) == g["plan_sha256"], f"plan step {k}"
+            assert _rref_digest(ech) == g["rref_sha256"], f"rref step {k}"
+        k += 1
+    return st, k
+
+
 @pytest.mark.parametrize("name,gen,args", [("cyclic8_p32003", gen_cyclic, (8, 32003)),
                                            ("katsura9_p32003", gen_katsura, (9, 32003)),
                                            ("cyclic7_p65521", gen_cyclic, (7, 65521))])
 def test_full_run_final_basis_matches_reference(cuda, name, gen, args):
-    """Whole north-star runs through f4_groebner (every F4 step + the device
-    interreduction) against the reference's final reduced-basis digest
-    (reference: 3,258 s + 66 s for cyclic-8 on one CPU core)."""
+    """Whole north-star runs on the GPU: EVERY F4 step's plan and RREF digests
+    (all 38 for cyclic-8) and the final reduced basis (device
+    interreduction) against the reference's digests (reference: 3,258 s +
+    66 s for cyclic-8 on one CPU core)."""
+    from paper_2601_06765_b200.groebner import reduce_basis_device
+
     ring, polys = gen(*args)
-    gb = f4_groebner(polys, ring)
     ref = load_golden(name)
+    st, k = _run_checking_steps(ring, polys, ref)
+    assert k == len(ref["steps"])
+    gb = reduce_basis_device(st.basis, ring)
     assert len(gb) == ref["gb_size"]
     assert hashlib.sha256(format_system(ring, gb).encode()).hexdigest() == ref["final_sha256"]
 
 
-@pytest.mark.parametrize("n", [8, 10, 11])
+def _in_ideal_device(gb, gens, ring):
+    """Ideal membership of every generator on the device: one Macaulay matrix
+    through compile_batch -> psge_reduce.  Rows: for each generator f a
+    reducer t*g with LM(t*g) = LM(f) (g = first basis element whose LM divides
+    LM(f)), then f itself; the closure (restricted to the basis) adds a
+    reducer for every other monomial divisible by a leading monomial.  The
+    reducer rows have distinct leads, so they are independent, and f reduces
+    to zero by the Gröbner basis iff its row is in their span: the number of
+    zero rows of the echelon form must equal the number of generators."""
+    from paper_2601_06765_b200.monomials import mon_divides
+
+    soa = soa_pack(list(gb) + list(gens), ring)
+    lms = [g.lm() for g in gb]
+    red = {}
+    for f in gens:
+        m = f.lm()
+        k = next(i for i, lm in enumerate(lms) if mon_divides(lm, m))
+        red[m] = Row(tuple(a - b for a, b in zip(m, lms[k])), k, RowRole.REDUCER, 0)
+    rows = list(red.values()) + [Row((0,) * ring.n_vars, len(gb) + j, RowRole.SPOLY_HALF, 1)
+                                 for j in range(len(gens))]
+    plan = compile_batch(rows, soa, Closure.ONE_STEP_REDUCTION, candidates=list(range(len(gb))))
+    ech = psge_reduce(csr_from_plan(plan, ring.modulus))
+    return ech.zero_row_count, len(gens), plan
+
+
+@pytest.mark.slow
+def test_katsura11_full_run_pinned(cuda):
+    """Katsura-11 / F_32003 (north-star system the reference cannot finish):
+    steps 0-4 of the live GPU run against the reference's per-step digests,
+    2^11 standard monomials, and every generator reduces to zero by the final
+    basis on the device (ideal membership, one Macaulay matrix); a perturbed
+    generator does not."""
+    import sys
+
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    from full_run import standard_monomials
+    from paper_2601_06765_b200.groebner import reduce_basis_device
+    from paper_2601_06765_b200.polynomials import Poly
+
+    ring, polys = gen_katsura(11, 32003)
+    gold = load_golden("katsura11_p32003")
+    assert len(gold["steps"]) >= 5
+    st, _ = _run_checking_steps(ring, polys, gold, max_checked=5)
+    gb = reduce_basis_device(st.basis, ring)
+    assert standard_monomials([f.lm() for f in gb], ring.n_vars) == 2 ** 11
+    zero, n, _ = _in_ideal_device(gb, polys, ring)
+    assert zero == n
+    # shift the constant term of a generator that has one: f + 1 is in the
+    # ideal iff 1 is, and Katsura-11 has solutions
+    bad = list(polys)
+    j = next(i for i, f in enumerate(bad) if sum(f.terms[-1][0]) == 0)
+    t = bad[j].terms
+    c = (t[-1][1] + 1) % 32003
+    bad[j] = Poly(ring, t[:-1] + (((t[-1][0], c),) if c else ()))
+    zero, n, _ = _in_ideal_device(gb, bad, ring)
+    assert zero == n - 1
+
+
+@pytest.mark.parametrize("n", [8, 10])
 def test_katsura_full_run_staircase(cuda, n):
     """Katsura-n is zero-dimensional with 2^n solutions, so its reduced grevlex
     basis leaves exactly 2^n standard monomials.  Katsura-11 is a north-star
@@ -521,3 +611,36 @@ def test_verify_kernel_syzygy_device(cuda):
     kbad = KernelBasis(kb.side, bad, len(bad), kb.seed_trail)
     assert not verify_kernel_syzygy(plan, st.basis, kbad).ok
     assert not verify_kernel_syzygy(host, st.basis, kbad).ok
+
+
+def test_mq16_wiedemann_kernel_matches_reference(cuda):
+    """BASELINE config 4 (MQ n=16, m=32 over F_31, Block Wiedemann): the first
+    two F4 steps with F4Config(numeric="wiedemann") return the same left
+    kernel as the real reference — step 0 via the dense path (62 x 153),
+    step 1 via Wiedemann on Aᵀ (584 x 968, 12 seeded rounds, nullity 41):
+    identical vectors (sha256), dimension and seed trail
+    (tests/golden/make_golden_wiedemann.py; reference left_kernel,
+    sparselin.py:551-569, 136 s for step 1 on one core)."""
+    import json
+
+    from paper_2601_06765_b200.groebner import F4Config
+    from paper_2601_06765_b200.systems import gen_random_quadratic
+
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "mq16x32_p31_wiedemann.json")
+    with open(path) as fh:
+        gold = json.load(fh)
+    ring, polys = gen_random_quadratic(16, 32, 1.0, 0, 31)
+    st = GroebnerState(ring)
+    for f in polys:
+        update_pairs(st, poly_monic(f))
+    cfg = F4Config(numeric="wiedemann", block_width=4, seed=0)
+    for g in gold["steps"]:
+        plan, ech, kb = f4_step(st, cfg)
+        assert plan_digest(plan) == g["plan_sha256"] and _rref_digest(ech) == g["rref_sha256"]
+        assert kb.side == g["kernel_side"] and kb.dimension_found == g["dimension_found"]
+        assert [list(t) for t in kb.seed_trail] == g["seed_trail"]
+        assert [int(x) for x in kb.vectors[0]] == g["first_vector"]
+        h = hashlib.sha256()
+        for v in kb.vectors:
+            h.update(("v:" + ",".join(str(int(x)) for x in v) + ";").encode())
+        assert h.hexdigest() == g["kernel_sha256"]
