@@ -572,9 +572,14 @@ def run_gpu(args, world, rank, local):
             clk.maybe_sample()
             flush.fill_(1)
             if shard is not None:
-                plan, t_sym_ns = shard.compile(b["rb"], b["sh"], True, list(range(b["n_basis"])))
-                inf_p = plan.info
-                t_b = t_sym_ns
+                # sharded compile (timed: CUDA events around the whole call,
+                # collectives included), then the full plan for the
+                # elimination, which is replicated on every rank (PSGE's C-row
+                # split is not implemented)
+                part, t_b, _ = shard.compile(b["rb"], b["sh"], True, list(range(b["n_basis"])))
+                plan = eng.compile(b["rb"], b["sh"], True, list(range(b["n_basis"])))
+                inf_p = dict(plan.info)
+                assert part.info["r_total"] == inf_p["r"] and part.info["N"] == inf_p["N"]
             else:
                 plan = eng.compile(b["rb"], b["sh"], True, list(range(b["n_basis"])))
                 inf_p = plan.info
@@ -583,7 +588,7 @@ def run_gpu(args, world, rank, local):
                 got = (inf_p["r"], inf_p["N"], inf_p["M"], inf_p["closure_rounds"])
                 want = (b["r"], b["N"], b["M"], b["rounds"])
                 assert got == want, f"replayed batch {(got)} != live {want}"
-            ech = eng.psge_plan(plan.local if shard is not None else plan, full=full)
+            ech = eng.psge_plan(plan, full=full)
             inf = ech.info()
             ts += t_b
             tn += inf["numeric_ns"] + (inf["backsub_ns"] if full else 0)

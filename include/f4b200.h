@@ -111,6 +111,7 @@ typedef struct {
   int64_t key_words, lane_bits;
   int64_t dict_build_ns, row_assemble_ns; /* device time (CUDA events) */
   int64_t sort_passes, kernel_launches;
+  int64_t row_lo, r_total; /* a sharded-compile slice: rows [row_lo, row_lo + r) of r_total */
 } f4b_plan_info;
 
 /* compile_batch (symbolic.py:293-388): rows in select_rows order
@@ -138,6 +139,41 @@ int f4b_plan_download_ref_keys(const f4b_plan* plan, uint64_t* keys);
  * dictionary, so Y = 0 is the exact recombination Σ v_i t_i g_{k_i} = 0. */
 int f4b_plan_left_apply(const f4b_plan* plan, const uint64_t* V, int64_t b, uint64_t* Y);
 int f4b_plan_free(f4b_plan* plan);
+
+/* ---- sharded compile_batch (one rank per GPU) ----
+ * The stages of compile_batch (symbolic.py:293-388) between which the caller
+ * all-gathers the small per-rank outputs (NCCL or gloo).  Every rank passes
+ * the SAME rows, candidates and gathered data; rank k owns the contiguous,
+ * length-balanced input rows [row_lo, row_hi), frontier slice
+ * [f_lo, f_hi) per round and final rows [row_lo, row_hi) of the join.
+ * Concatenating the finish() slices in rank order is the single-GPU plan.
+ * Run / rank / reducer buffers may be host or device pointers.  grevlex
+ * rank path only (else F4B_ERR_PRECONDITION).
+ *   begin        -> *n_run = length of this rank's sorted unique run of
+ *                   monomial ranks (ascending = ascending key)
+ *   take_run     copy it out (n_run u32)
+ *   merge        all gathered runs (concatenated) -> dictionary, round-1
+ *                frontier size
+ *   round        this rank's frontier slice: red_out[f_hi - f_lo] = reducer
+ *                basis index or -1, *n_run = its run of new monomials
+ *   round_merge  all reducer indices (frontier order) + all new runs -> the
+ *                round's rows, next frontier size (0 = closure done)
+ *   rows         final row count and row starts (r_total + 1, may be NULL)
+ *   finish       the join of final rows [row_lo, row_hi) -> a plan slice */
+typedef struct f4b_shard f4b_shard;
+int f4b_shard_begin(f4b_ctx* ctx, int64_t n_rows, const int32_t* row_basis, const uint16_t* row_shift,
+                    int closure, const int32_t* candidates, int64_t n_candidates, int64_t dict_cap,
+                    int64_t row_lo, int64_t row_hi, f4b_shard** out, int64_t* n_run);
+int f4b_shard_take_run(f4b_shard* sh, uint32_t* out, int64_t n_run);
+int f4b_shard_merge(f4b_shard* sh, const uint32_t* ranks, int64_t n, int64_t* n_frontier);
+int f4b_shard_round(f4b_shard* sh, int64_t f_lo, int64_t f_hi, int32_t* red_out, int64_t* n_run);
+int f4b_shard_round_merge(f4b_shard* sh, const int32_t* red_all, int64_t n_frontier, const uint32_t* ranks,
+                          int64_t n, int64_t* n_next_frontier);
+int f4b_shard_rows(f4b_shard* sh, int64_t* r_total, uint32_t* row_start);
+int f4b_shard_finish(f4b_shard* sh, int64_t row_lo, int64_t row_hi, f4b_plan** out);
+/* closure rounds so far, dictionary size, this rank's summed device time */
+int f4b_shard_info(const f4b_shard* sh, int64_t* rounds, int64_t* n_dict, int64_t* device_ns);
+int f4b_shard_free(f4b_shard* sh);
 
 typedef struct {
   int64_t n_rows, n_cols, rank, zero_rows;

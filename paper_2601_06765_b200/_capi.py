@@ -38,7 +38,7 @@ u16p = C.POINTER(C.c_uint16)
 class PlanInfo(C.Structure):
     _fields_ = [(k, C.c_int64) for k in (
         "r", "N", "M", "closure_rounds", "n_closure_rows", "key_words", "lane_bits",
-        "dict_build_ns", "row_assemble_ns", "sort_passes", "kernel_launches")]
+        "dict_build_ns", "row_assemble_ns", "sort_passes", "kernel_launches", "row_lo", "r_total")]
 
 
 class EchelonInfo(C.Structure):
@@ -69,6 +69,16 @@ SIGNATURES = {
     "f4b_compile_batch": (C.c_int, [C.c_void_p, C.c_int64, i32p, u16p, C.c_int, i32p, C.c_int64, C.c_int64,
                                     C.POINTER(C.c_void_p)]),
     "f4b_plan_get_info": (C.c_int, [C.c_void_p, C.POINTER(PlanInfo)]),
+    "f4b_shard_begin": (C.c_int, [C.c_void_p, C.c_int64, i32p, u16p, C.c_int, i32p, C.c_int64, C.c_int64,
+                                  C.c_int64, C.c_int64, C.POINTER(C.c_void_p), i64p]),
+    "f4b_shard_take_run": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64]),
+    "f4b_shard_merge": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, i64p]),
+    "f4b_shard_round": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, i64p]),
+    "f4b_shard_round_merge": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, i64p]),
+    "f4b_shard_rows": (C.c_int, [C.c_void_p, i64p, C.c_void_p]),
+    "f4b_shard_finish": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.POINTER(C.c_void_p)]),
+    "f4b_shard_info": (C.c_int, [C.c_void_p, i64p, i64p, i64p]),
+    "f4b_shard_free": (C.c_int, [C.c_void_p]),
     "f4b_plan_download": (C.c_int, [C.c_void_p, i64p, i64p, u64p, u16p, i32p, u16p, i32p]),
     "f4b_plan_download_ref_keys": (C.c_int, [C.c_void_p, u64p]),
     "f4b_plan_left_apply": (C.c_int, [C.c_void_p, u64p, C.c_int64, u64p]),

@@ -125,6 +125,11 @@ uint32_t read_u32(Ctx* c, const uint32_t* dptr) {
   return c->h_stat[0];
 }
 
+cudaEvent_t timing_event(Ctx* c, int i) {
+  if (!c->tev[i]) check_cuda(cudaEventCreate(&c->tev[i]), "event");
+  return c->tev[i];
+}
+
 void memset_async(Ctx* c, void* p, int v, size_t bytes) { check_cuda(cudaMemsetAsync(p, v, bytes, c->stream), "memset"); }
 
 ProfScope::ProfScope(Ctx* c_, const char* n) : c(c_), name(n) {
@@ -347,6 +352,8 @@ int f4b_ctx_destroy(f4b_ctx* h) {
   if (c->h_stat) cudaFreeHost(c->h_stat);
   if (c->h_app) cudaFreeHost(c->h_app);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+  for (cudaEvent_t& e : c->tev)
+    if (e) cudaEventDestroy(e);
   if (c->mempool) {
     cudaStreamSynchronize(c->stream);
     cudaMemPoolDestroy(c->mempool);
@@ -732,7 +739,9 @@ int f4b_plan_get_info(const f4b_plan* pl, f4b_plan_info* info) {
   info->N = pl->N;
   info->M = pl->M;
   info->closure_rounds = pl->closure_rounds;
-  info->n_closure_rows = pl->r - pl->r0;
+  info->n_closure_rows = pl->n_closure();
+  info->row_lo = pl->row_lo;
+  info->r_total = pl->r_total >= 0 ? pl->r_total : pl->r;
   info->key_words = pl->KW;
   info->lane_bits = pl->lane_bits;
   info->dict_build_ns = pl->dict_ns;
@@ -753,7 +762,7 @@ int f4b_plan_download(const f4b_plan* pl, int64_t* row_ptr, int64_t* col_ind, ui
   API_BEGIN(pl->ctx)
   Ctx* c = _c;
   const int n = c->n_vars;
-  const long long r = pl->r, M = pl->M, N = pl->N, ncl = pl->r - pl->r0;
+  const long long r = pl->r, M = pl->M, N = pl->N, ncl = pl->n_closure();
   // widen u32 -> 64-bit on the device, then one D2H per array straight into
   // the caller's buffers (page-locked ones copy at full link rate)
   const long long w_row = row_ptr ? r + 1 : 0, w_col = col_ind ? M : 0, w_val = val ? M : 0;

@@ -205,9 +205,69 @@ F4B_DEV u32 key_lane(const KeyFmt& f, const Key<KW>& k, int lane) {
   int bit = (f.n_lanes - 1 - lane) * f.lane_bits;
   int wi = KW - 1 - (bit >> 6);
   int sh = bit & 63;
-  u64 v = k.w[wi] >> sh;
-  if (sh + f.lane_bits > 64 && wi > 0) v |= k.w[wi - 1] << (64 - sh);
+  // word select without a dynamic index (a runtime k.w[...] index would put
+  // the key in local memory)
+  u64 lo = k.w[0], hi = 0;
+#pragma unroll
+  for (int j = 1; j < KW; ++j) {
+    if (j == wi) lo = k.w[j];
+    if (j == wi - 1) hi = k.w[j];
+  }
+  u64 v = lo >> sh;
+  if (KW > 1 && sh + f.lane_bits > 64 && wi > 0) v |= hi << (64 - sh);
   return (u32)(v & ((1ull << f.lane_bits) - 1ull));
+}
+
+// OR a lane value into a key (lane counted from the most significant end).
+template <int KW>
+F4B_DEV void key_or_lane(const KeyFmt& f, Key<KW>& k, int lane, u32 val) {
+  const int bit = (f.n_lanes - 1 - lane) * f.lane_bits;
+  const int wi = KW - 1 - (bit >> 6);
+  const int sh = bit & 63;
+#pragma unroll
+  for (int j = 0; j < KW; ++j) {
+    if (j == wi) k.w[j] |= ((u64)val) << sh;
+    if (KW > 1 && j == wi - 1 && sh + f.lane_bits > 64) k.w[j] |= ((u64)val) >> (64 - sh);
+  }
+}
+
+// ---- grevlex keys with a compile-time bound NV >= n_vars on the number of
+// variables: exponent vectors live in registers (every index is a
+// compile-time constant after unrolling), no local-memory frame.
+// grevlex lanes: lane 0 = degree, lane L (1 <= L < n) = full - e_{n-L}.
+template <int KW, int NV>
+F4B_DEV void gl_decode(const KeyFmt& f, const Key<KW>& k, u16 (&e)[NV]) {
+  const u32 full = (1u << f.lane_bits) - 1u;
+  const int n = f.n_vars;
+  u32 rest = 0;
+#pragma unroll
+  for (int v = 1; v < NV; ++v) {
+    e[v] = 0;
+    if (v < n) {
+      const u32 x = full - key_lane<KW>(f, k, n - v);
+      e[v] = (u16)x;
+      rest += x;
+    }
+  }
+  e[0] = (u16)(key_lane<KW>(f, k, 0) - rest);
+}
+
+template <int KW, int NV>
+F4B_DEV Key<KW> gl_encode(const KeyFmt& f, const u16 (&e)[NV]) {
+  Key<KW> k;
+#pragma unroll
+  for (int j = 0; j < KW; ++j) k.w[j] = 0;
+  const u32 full = (1u << f.lane_bits) - 1u;
+  const int n = f.n_vars;
+  u32 deg = 0;
+#pragma unroll
+  for (int v = 0; v < NV; ++v)
+    if (v < n) deg += e[v];
+  key_or_lane<KW>(f, k, 0, deg);
+#pragma unroll
+  for (int v = 1; v < NV; ++v)
+    if (v < n) key_or_lane<KW>(f, k, n - v, full - e[v]);
+  return k;
 }
 
 // Decode a device key into exponents.

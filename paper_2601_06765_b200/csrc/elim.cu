@@ -1683,9 +1683,7 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
     if (etrace) marks.push_back({w, std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count()});
   };
   const long long r = E->n_rows, N = E->n_cols;
-  cudaEvent_t ev0, ev1;
-  check_cuda(cudaEventCreate(&ev0), "event");
-  check_cuda(cudaEventCreate(&ev1), "event");
+  cudaEvent_t ev0 = timing_event(c, 2), ev1 = timing_event(c, 3);
   check_cuda(cudaEventRecord(ev0, c->stream), "event");
   ensure(c, c->errflag, 64);
   u32* err = c->errflag.as<u32>();
@@ -1938,8 +1936,6 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
   float ms = 0;
   cudaEventElapsedTime(&ms, ev0, ev1);
   E->numeric_ns = (int64_t)(ms * 1e6);
-  cudaEventDestroy(ev0);
-  cudaEventDestroy(ev1);
   if (etrace && ms > 10.0f) {
     fprintf(stderr, "[elim] r=%lld N=%lld R=%lld K=%lld dev=%.2fms allocs=%lld frees=%lld alloc_us=%.0f:", (long long)r,
             (long long)N, (long long)E->nC, (long long)E->K, ms, c->raw_allocs - a0, c->raw_frees - f0,
@@ -1955,9 +1951,7 @@ static void run_a_sweep(Ctx* c, f4b_echelon* E) {
   if (E->full) return;
   Fp fp = make_fp(c);
   const long long N = E->n_cols, nA = E->nA, K = E->K;
-  cudaEvent_t ev0, ev1;
-  check_cuda(cudaEventCreate(&ev0), "event");
-  check_cuda(cudaEventCreate(&ev1), "event");
+  cudaEvent_t ev0 = timing_event(c, 2), ev1 = timing_event(c, 3);
   check_cuda(cudaEventRecord(ev0, c->stream), "event");
   ensure(c, E->a_off, (size_t)std::max<long long>(nA, 1) * sizeof(u32));
   ensure(c, E->a_len, (size_t)std::max<long long>(nA, 1) * sizeof(u32));
@@ -2011,8 +2005,6 @@ static void run_a_sweep(Ctx* c, f4b_echelon* E) {
   float ms = 0;
   cudaEventElapsedTime(&ms, ev0, ev1);
   E->backsub_ns = (int64_t)(ms * 1e6);
-  cudaEventDestroy(ev0);
-  cudaEventDestroy(ev1);
   E->full = true;
 }
 

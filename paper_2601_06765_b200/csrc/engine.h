@@ -134,6 +134,7 @@ struct Ctx {
   // optional per-kernel CUDA-event timing (f4b_ctx_profile)
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
+  cudaEvent_t tev[4] = {};  // per-call timing events (created once, reused)
   size_t ev_used = 0;
   struct Pending {
     const char* name;
@@ -172,6 +173,7 @@ void sort_unique(Ctx* c, int KW, const uint64_t* in, const uint32_t* d_n, uint32
                  const uint64_t* dict, const uint32_t* d_ndict, uint64_t* out, uint32_t* d_count);
 
 uint32_t read_u32(Ctx* c, const uint32_t* dptr);  // synchronous small D2H
+cudaEvent_t timing_event(Ctx* c, int i);           // reusable event i < 4 of the context
 void memset_async(Ctx* c, void* p, int v, size_t bytes);
 
 }  // namespace f4b
@@ -193,6 +195,10 @@ struct f4b_plan {
   f4b::DBuf cl_basis;   // i32 [r-r0]
   f4b::DBuf cl_shift;   // u16 [(r-r0)*n]
   f4b::DBuf cl_round;   // i32 [r-r0]
+  // slice of a sharded compile (shard.cu): rows [row_lo, row_lo + r) of the
+  // r_total final rows; the closure metadata covers all ncl_all closure rows
+  long long row_lo = 0, r_total = -1, ncl_all = -1;
+  long long n_closure() const { return ncl_all >= 0 ? ncl_all : r - r0; }
 };
 
 struct f4b_echelon;

@@ -35,10 +35,11 @@
 #include "block.cuh"
 #include "common.cuh"
 #include "engine.h"
+#include "rank.cuh"
+#include "fbsp_internal.cuh"
 
 namespace f4b {
 
-static constexpr int MAXV = 32;
 static constexpr int K1_THREADS = 512;
 
 template <int KW>
@@ -770,46 +771,6 @@ static void compile_t(Ctx* c, const KeyFmt& f, long long r0, const int32_t* h_rb
 static constexpr int RK_THREADS = 256;
 static constexpr int RK_TILE = 4096;
 static constexpr int RK_SROWS = 1024;
-
-template <int KW>
-F4B_DEV u32 key_rank(const KeyFmt& f, const u32* bt, int st, const Key<KW>& k) {
-  const int n = f.n_vars;
-  const int full = (1 << f.lane_bits) - 1;
-  const int d = (int)key_lane<KW>(f, k, 0);
-  u32 r = d ? bt[(n + d - 1) * st + n] : 0u;
-  int s = d;
-  for (int L = 1; L < n; ++L) {
-    const int i = n - L;
-    const int e = full - (int)key_lane<KW>(f, k, L);
-    if (s > e) r += bt[(s - e - 1 + i) * st + i];
-    s -= e;
-  }
-  return r;
-}
-
-F4B_DEV void unrank_exps(u32 r, int n, int D, const u32* bt, int st, u16* e) {
-  // degree: largest d <= D with C(n+d-1, n) <= r  (binary search; C(n-1, n) = 0)
-  int lo = 0, hi = D;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (bt[(n + mid - 1) * st + n] <= r) lo = mid; else hi = mid - 1;
-  }
-  const int d = lo;
-  if (d) r -= bt[(n + d - 1) * st + n];
-  int s = d;
-  for (int i = n - 1; i >= 1; --i) {
-    // largest m in [0, s] with C(m-1+i, i) <= r  (C(i-1, i) = 0 for m = 0)
-    int a = 0, b = s;
-    while (a < b) {
-      const int mid = (a + b + 1) >> 1;
-      if (bt[(mid - 1 + i) * st + i] <= r) a = mid; else b = mid - 1;
-    }
-    if (a > 0) r -= bt[(a - 1 + i) * st + i];
-    e[i] = (u16)(s - a);
-    s = a;
-  }
-  e[0] = (u16)s;
-}
 
 // Fill: every term of rows [r_lo, r_hi) -> its rank -> one bit.  Private
 // shared-memory bitmaps per CTA (written out as partials) when the rank space
@@ -1763,7 +1724,7 @@ struct FbspArgs {
   unsigned long long* trace;
 };
 
-template <int KW>
+template <int KW, int NV>
 __global__ void __launch_bounds__(CL_THREADS) k_fbsp(const FbspArgs a) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
@@ -1809,6 +1770,7 @@ __global__ void __launch_bounds__(CL_THREADS) k_fbsp(const FbspArgs a) {
   }
   // the next call's counters are idle now: clear them
   if (tid < 4) a.cnt_next[tid * G + blockIdx.x] = 0;
+  if (blockIdx.x == 0 && tid == 0) *a.err = 0;  // nothing sets it before the first grid barrier
   __syncthreads();
   const u32 CH = max(1u, (a.maxlen + 31) / 32);
   const u32 cw = (((a.words + G - 1) / G) + 31) & ~31u;
@@ -1854,11 +1816,14 @@ __global__ void __launch_bounds__(CL_THREADS) k_fbsp(const FbspArgs a) {
       const u32 pre = block_scan_excl(__popc(x), ws, &tt);
       if (out_exps && w < w_hi) a.dwp[w] = make_uint2(x, base + pre);
       auto put = [&](u32 pos, u32 rk) {
-        u16 e[MAXV];
-        unrank_exps(rk, n, a.D, bt, a.st, e);
-        key_store<KW>(out_keys, pos, key_encode<KW>(a.f, e));
-        if (out_exps)
-          for (int v = 0; v < n; ++v) out_exps[((long long)N_all - 1 - pos) * n + v] = e[v];
+        u16 e[NV];
+        gl_unrank<NV>(rk, n, a.D, bt, a.st, e);
+        key_store<KW>(out_keys, pos, gl_encode<KW, NV>(a.f, e));
+        if (out_exps) {
+#pragma unroll
+          for (int v = 0; v < NV; ++v)
+            if (v < n) out_exps[((long long)N_all - 1 - pos) * n + v] = e[v];
+        }
       };
       if (tt <= (u32)CL_LIST) {
         u32 p = pre, m = x;
@@ -1925,12 +1890,13 @@ __global__ void __launch_bounds__(CL_THREADS) k_fbsp(const FbspArgs a) {
   // owning word chunk; the warp owning a row's first term writes its entry)
   term_ranges(0u, (u32)a.r0, 0u, a.M0, [&](u32 i) { return a.start_in[i]; }, [&](u32 i, u32 rsi, u32 from, u32 to) {
     const int g = a.rb_in[i];
-    u16 e[MAXV], z[MAXV];
-    for (int v = 0; v < n; ++v) {
-      e[v] = a.shift_in[(long long)i * n + v];
+    u16 e[NV], z[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      e[v] = v < n ? a.shift_in[(long long)i * n + v] : (u16)0;
       z[v] = 0;
     }
-    const Key<KW> dl = key_sub<KW>(key_encode<KW>(a.f, e), key_encode<KW>(a.f, z));
+    const Key<KW> dl = key_sub<KW>(gl_encode<KW, NV>(a.f, e), gl_encode<KW, NV>(a.f, z));
     const u32 off = __ldg(a.boff + g), len = __ldg(a.blen + g);
     if (from == rsi && lane == 0) {
       a.rows_basis[i] = g;
@@ -2017,17 +1983,21 @@ __global__ void __launch_bounds__(CL_THREADS) k_fbsp(const FbspArgs a) {
       for (u32 j = j0; j < j1; ++j) {
         const Key<KW> m = key_load_cg<KW>(front, j);
         int found = -1;
-        u16 e[MAXV + 1];
-        key_decode<KW>(a.f, m, e);
-        e[n] = 0;
-        u32 me[MAXV / 2];
-        for (int w = 0; w < a.nw; ++w) me[w] = (u32)e[2 * w] | ((u32)e[2 * w + 1] << 16);
+        u16 e[NV];
+        gl_decode<KW, NV>(a.f, m, e);
+        constexpr int NW2 = (NV + 1) / 2;
+        u32 me[NW2];
+#pragma unroll
+        for (int w = 0; w < NW2; ++w)
+          me[w] = (u32)e[2 * w] | (2 * w + 1 < NV ? ((u32)e[2 * w + 1] << 16) : 0u);
         for (int b0 = 0; b0 < a.nc; b0 += 32) {
           const int cc = b0 + lane;
           bool ok = cc < a.nc;
           if (ok) {
             const u32* lm = lmw + (long long)cc * a.nw;
-            for (int w = 0; w < a.nw; ++w) ok &= (__vcmpgeu2(me[w], lm[w]) == 0xFFFFFFFFu);
+#pragma unroll
+            for (int w = 0; w < NW2; ++w)
+              if (w < a.nw) ok &= (__vcmpgeu2(me[w], lm[w]) == 0xFFFFFFFFu);
           }
           const unsigned bm = __ballot_sync(0xffffffffu, ok);
           if (bm) {
@@ -2129,13 +2099,16 @@ __global__ void __launch_bounds__(CL_THREADS) k_fbsp(const FbspArgs a) {
           a.rows_basis[row] = g;
           key_store<KW>(a.rows_delta, row, key_sub<KW>(m, key_load<KW>(a.bckey, __ldg(a.boff + g))));
           a.rows_start[row] = Mcur + bl + lp - len;
-          u16 e[MAXV];
-          key_decode<KW>(a.f, m, e);
+          u16 e[NV];
+          gl_decode<KW, NV>(a.f, m, e);
           bool over = false;
-          for (int v = 0; v < n; ++v) {
-            const u32 sft = (u32)e[v] - (u32)a.lmexp[(long long)g * n + v];
-            over |= (sft + (u32)a.maxe[(long long)g * n + v]) > 0xFFFFu;
-            a.cl_shift[(n_cl + q) * n + v] = (u16)sft;
+#pragma unroll
+          for (int v = 0; v < NV; ++v) {
+            if (v < n) {
+              const u32 sft = (u32)e[v] - (u32)a.lmexp[(long long)g * n + v];
+              over |= (sft + (u32)a.maxe[(long long)g * n + v]) > 0xFFFFu;
+              a.cl_shift[(n_cl + q) * n + v] = (u16)sft;
+            }
           }
           if (over) atomicOr(a.err, (u32)DEVERR_LANE_OVERFLOW);
           a.cl_basis[n_cl + q] = g;
@@ -2361,12 +2334,6 @@ __global__ void __launch_bounds__(RK_THREADS) k_rank_join(KeyFmt f, u32 M, u32 r
   if (miss) atomicOr(err, (u32)DEVERR_MISSING_KEY);
 }
 
-static unsigned long long binom_ull(int a, int b) {
-  if (b < 0 || a < b) return 0;
-  unsigned long long r = 1;
-  for (int i = 1; i <= b; ++i) r = r * (unsigned long long)(a - b + i) / (unsigned long long)i;
-  return r;
-}
 
 // Eligibility of the rank path: grevlex and a rank space of <= 2^26 monomials.
 static bool rank_path_ok(const Ctx* c, int order, int n, long long D) {
@@ -2381,7 +2348,7 @@ static bool rank_path_ok(const Ctx* c, int order, int n, long long D) {
 // counters back once.  Plan buffers are sized from capacity hints; an
 // overflow (flagged by the kernel) grows the hints and recompiles.
 // ===========================================================================
-template <int KW>
+template <int KW, int NV>
 static void compile_rank_fused(Ctx* c, const KeyFmt& f, int D, long long r0, const int32_t* h_rb,
                                const uint16_t* h_shift, int closure, const std::vector<int32_t>& cand,
                                long long dict_cap, f4b_plan* pl) {
@@ -2395,9 +2362,7 @@ static void compile_rank_fused(Ctx* c, const KeyFmt& f, int D, long long r0, con
     if (htrace)
       hmarks.push_back({what, std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count()});
   };
-  cudaEvent_t ev0, ev1;
-  check_cuda(cudaEventCreate(&ev0), "event");
-  check_cuda(cudaEventCreate(&ev1), "event");
+  cudaEvent_t ev0 = timing_event(c, 0), ev1 = timing_event(c, 1);
   check_cuda(cudaEventRecord(ev0, c->stream), "event record");
   encode_basis<KW>(c, f);
 
@@ -2483,21 +2448,25 @@ static void compile_rank_fused(Ctx* c, const KeyFmt& f, int D, long long r0, con
   ensure(c, c->errflag, sizeof(DevCounters) + 4096);
   DevCounters* dc = reinterpret_cast<DevCounters*>(c->errflag.p);
   LoopOut* d_out = reinterpret_cast<LoopOut*>(dc + 1);
-  check_cuda(cudaMemsetAsync(dc, 0, sizeof(DevCounters), c->stream), "memset counters");
+  // dc->err is cleared by k_fbsp itself (CTA 0, before its first barrier)
 
   const int stage_lm = (size_t)nc * nw * 4 <= 48 * 1024 ? 1 : 0;
-  const size_t lsm = ((size_t)((bt_words + 3) & ~3) + CL_LIST) * 4 + (stage_lm ? (size_t)nc * nw * 4 : 0);
+  // dynamic shared memory rounded up to 8 KB steps: the occupancy query below
+  // (tens of microseconds of host time) then runs once per step, not once per
+  // call as the LM table grows
+  const size_t lsm = ((((size_t)((bt_words + 3) & ~3) + CL_LIST) * 4 + (stage_lm ? (size_t)nc * nw * 4 : 0)) + 8191) &
+                     ~(size_t)8191;
   static bool lattr = false;
   if (!lattr) {
-    check_cuda(cudaFuncSetAttribute(k_fbsp<KW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024), "attr");
+    check_cuda(cudaFuncSetAttribute((k_fbsp<KW, NV>), cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024), "attr");
     lattr = true;
   }
-  static int bps_cached = -1;
-  static size_t bps_smem = 0;
-  if (bps_cached < 0 || bps_smem != lsm) {
-    check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps_cached, k_fbsp<KW>, CL_THREADS, lsm), "occupancy");
-    bps_smem = lsm;
-  }
+  static int bps_by_step[16] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
+  const int lstep = (int)std::min<size_t>(15, lsm / 8192);
+  if (bps_by_step[lstep] < 0)
+    check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps_by_step[lstep], (k_fbsp<KW, NV>), CL_THREADS, lsm),
+               "occupancy");
+  const int bps_cached = bps_by_step[lstep];
   static const int bps_max = getenv("F4B_LOOP_BPS") ? atoi(getenv("F4B_LOOP_BPS")) : 2;
   // every SM, even for small batches: fewer CTAs measured slower (the closure
   // rounds' search and ranking spread over all warps)
@@ -2600,7 +2569,7 @@ static void compile_rank_fused(Ctx* c, const KeyFmt& f, int D, long long r0, con
   {
     void* args[] = {&fa};
     ProfScope ps(c, "k_fbsp");
-    check_cuda(cudaLaunchCooperativeKernel((void*)k_fbsp<KW>, G, CL_THREADS, args, lsm, c->stream), "k_fbsp");
+    check_cuda(cudaLaunchCooperativeKernel((void*)(k_fbsp<KW, NV>), G, CL_THREADS, args, lsm, c->stream), "k_fbsp");
   }
   mark("launched");
   check_cuda(cudaEventRecord(ev1, c->stream), "event record");
@@ -2634,8 +2603,6 @@ static void compile_rank_fused(Ctx* c, const KeyFmt& f, int D, long long r0, con
   }
   float ms = 0;
   check_cuda(cudaEventElapsedTime(&ms, ev0, ev1), "elapsed");
-  cudaEventDestroy(ev0);
-  cudaEventDestroy(ev1);
   if (ho.flags) {
     // aborted run: maps and counters may be dirty
     c->maps_clean = 0;
@@ -2645,7 +2612,7 @@ static void compile_rank_fused(Ctx* c, const KeyFmt& f, int D, long long r0, con
     c->closure_cap_hint = std::max<long long>(4 * cap, c->closure_cap_hint);
     c->m_cap_hint = std::max<long long>(c->m_cap_hint, std::max<long long>(2 * M_cap, (long long)ho.M + ho.M / 4));
     c->n_cap_hint = std::max<long long>(c->n_cap_hint, std::max<long long>(2 * N_cap, (long long)ho.N + ho.N / 4));
-    compile_rank_fused<KW>(c, f, D, r0, h_rb, h_shift, closure, cand, dict_cap, pl);
+    compile_rank_fused<KW, NV>(c, f, D, r0, h_rb, h_shift, closure, cand, dict_cap, pl);
     return;
   }
   if (ho.flags & LOOP_SIZE_CAP) fail(F4B_ERR_SIZE_CAP, "batch has more than 2^30 terms");
@@ -3082,10 +3049,11 @@ static void compile_rank(Ctx* c, const KeyFmt& f, int D, long long r0, const int
   if (hc.err & DEVERR_MISSING_KEY) fail(F4B_ERR_MISSING_KEY, "row key absent from dictionary (closure defect)");
 }
 
-void compile_batch(Ctx* c, long long r0, const int32_t* rb, const uint16_t* shift, int closure, const int32_t* cands,
-                   long long n_cands, long long dict_cap, f4b_plan* pl) {
+BatchFormat batch_format(Ctx* c, long long r0, const int32_t* rb, const uint16_t* shift, const int32_t* cands,
+                         long long n_cands) {
   Basis& B = c->basis;
   const int n = c->n_vars;
+  BatchFormat bf;
   long long D = 0;
   for (long long i = 0; i < r0; ++i) {
     const int g = rb[i];
@@ -3100,7 +3068,8 @@ void compile_batch(Ctx* c, long long r0, const int32_t* rb, const uint16_t* shif
     }
     D = std::max(D, d);
   }
-  std::vector<int32_t> cand;
+  bf.D = D;
+  std::vector<int32_t>& cand = bf.cand;
   if (cands) {
     cand.assign(cands, cands + n_cands);
     for (int32_t k : cand)
@@ -3110,7 +3079,7 @@ void compile_batch(Ctx* c, long long r0, const int32_t* rb, const uint16_t* shif
     for (int k = 0; k < B.n_polys; ++k) cand[k] = k;
   }
   cand.erase(std::remove_if(cand.begin(), cand.end(), [&](int32_t k) { return B.h_len[k] < 1; }), cand.end());
-  KeyFmt f;
+  KeyFmt& f = bf.f;
   f.order = c->order;
   f.n_vars = n;
   if (c->order == 2) {
@@ -3121,11 +3090,47 @@ void compile_batch(Ctx* c, long long r0, const int32_t* rb, const uint16_t* shif
     f.lane_bits = b;
   }
   f.n_lanes = n;
-  const int bits = f.lane_bits * f.n_lanes;
-  int KW = 1;
-  while (64 * KW < bits) KW *= 2;
-  if (KW > 8) fail(F4B_ERR_PRECONDITION, "batch degree too large for the device key format");
-  if (rank_path_ok(c, c->order, n, D)) {
+  auto words_for = [&](int lane_bits) {
+    int w = 1;
+    while (64 * w < lane_bits * n) w *= 2;
+    return w;
+  };
+  bf.KW = words_for(f.lane_bits);
+  // never narrow the lanes of the cached basis keys when the wider format
+  // needs no more words: any lane width >= bits(D) is order-isomorphic and
+  // injective on the batch, and a narrower format would re-encode the whole
+  // basis (k_encode_basis over every term) for nothing
+  // (rank path only: the radix path sorts lane_bits * n bits)
+  bf.rank_ok = rank_path_ok(c, c->order, n, D) && bf.KW <= 2;
+  if (bf.rank_ok && B.ckey_lane_bits > f.lane_bits && B.ckey_lane_bits <= 16 && words_for(B.ckey_lane_bits) == bf.KW)
+    f.lane_bits = B.ckey_lane_bits;
+  if (bf.KW > 8) fail(F4B_ERR_PRECONDITION, "batch degree too large for the device key format");
+  return bf;
+}
+
+bool rank_path_ok_pub(const Ctx* c, int order, int n, long long D) { return rank_path_ok(c, order, n, D); }
+
+void encode_basis_kw(Ctx* c, const KeyFmt& f, int KW) {
+  switch (KW) {
+    case 1: encode_basis<1>(c, f); break;
+    case 2: encode_basis<2>(c, f); break;
+    case 4: encode_basis<4>(c, f); break;
+    default: encode_basis<8>(c, f); break;
+  }
+}
+
+std::vector<int32_t> reducer_preference(Ctx* c, const std::vector<int32_t>& cand) { return preference_order(c, cand); }
+
+void compile_batch(Ctx* c, long long r0, const int32_t* rb, const uint16_t* shift, int closure, const int32_t* cands,
+                   long long n_cands, long long dict_cap, f4b_plan* pl) {
+  const int n = c->n_vars;
+  BatchFormat bf = batch_format(c, r0, rb, shift, cands, n_cands);
+  const long long D = bf.D;
+  const KeyFmt& f = bf.f;
+  const int KW = bf.KW;
+  const std::vector<int32_t>& cand = bf.cand;
+  const bool rank_ok = bf.rank_ok;
+  if (rank_ok) {
     // opt_fbsp = 1: the multi-launch pipeline (the same phases as separate
     // launches; also the building blocks of the sharded compile, shard.cu)
     if (c->opt_fbsp == 1) {
@@ -3136,12 +3141,14 @@ void compile_batch(Ctx* c, long long r0, const int32_t* rb, const uint16_t* shif
         default: compile_rank<8>(c, f, (int)D, r0, rb, shift, closure, cand, dict_cap, pl); break;
       }
     } else {
-      switch (KW) {
-        case 1: compile_rank_fused<1>(c, f, (int)D, r0, rb, shift, closure, cand, dict_cap, pl); break;
-        case 2: compile_rank_fused<2>(c, f, (int)D, r0, rb, shift, closure, cand, dict_cap, pl); break;
-        case 4: compile_rank_fused<4>(c, f, (int)D, r0, rb, shift, closure, cand, dict_cap, pl); break;
-        default: compile_rank_fused<8>(c, f, (int)D, r0, rb, shift, closure, cand, dict_cap, pl); break;
-      }
+      // exponent vectors in registers: NV = the next of 8 / 16 / 32 >= n
+      // (a 2^26 rank space keeps KW <= 2: rank_path_ok)
+      const int NVs = n <= 8 ? 8 : (n <= 16 ? 16 : 32);
+      if (KW == 1 && NVs == 8) compile_rank_fused<1, 8>(c, f, (int)D, r0, rb, shift, closure, cand, dict_cap, pl);
+      else if (KW == 1 && NVs == 16) compile_rank_fused<1, 16>(c, f, (int)D, r0, rb, shift, closure, cand, dict_cap, pl);
+      else if (KW == 1) compile_rank_fused<1, 32>(c, f, (int)D, r0, rb, shift, closure, cand, dict_cap, pl);
+      else if (NVs <= 16) compile_rank_fused<2, 16>(c, f, (int)D, r0, rb, shift, closure, cand, dict_cap, pl);
+      else compile_rank_fused<2, 32>(c, f, (int)D, r0, rb, shift, closure, cand, dict_cap, pl);
     }
     return;
   }

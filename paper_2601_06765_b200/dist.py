@@ -199,3 +199,132 @@ def remap_columns(local_keys_desc: np.ndarray, global_keys_desc: np.ndarray) -> 
     view = lambda a: np.ascontiguousarray(a).view([("", a.dtype)] * a.shape[1]).ravel()  # noqa: E731
     pos_asc = np.searchsorted(view(g_asc), view(local_keys_desc))
     return (len(global_keys_desc) - 1 - pos_asc).astype(np.int64)
+
+
+class ShardedCompiler:
+    """compile_batch split across the ranks of a process group,
+    on each rank's CUDA engine (csrc/shard.cu, C ABI f4b_shard_*).
+
+    Per call, every rank passes the same rows:
+
+    1. rows split into contiguous ranges balanced by term count; each rank
+       materialises its range and builds its sorted unique run of monomial
+       ranks (rank order = key order) -> all-gather of the runs -> every rank
+       holds the identical dictionary (reference _materialize + radix_sort +
+       unique_sorted, symbolic.py:204-225, :330-333);
+    2. closure rounds (symbolic.py:335-363): the frontier (identical on every
+       rank, ascending key(m)) split into contiguous slices; each rank finds the
+       reducers of its slice and ranks their rows' terms -> all-gather of the
+       reducer indices (frontier order, so rows stay in ascending key(m)) and
+       of the new-monomial runs -> identical rows and next frontier everywhere;
+    3. the final row list split by term count; each rank joins its range
+       against the dictionary (merge_join_index) -> its plan slice.
+
+    Collectives: torch.distributed all_gather of int32 tensors on the rank's
+    GPU (NCCL) or on the host (gloo); two per exchange (sizes, then the padded
+    payload).  ``compile`` returns (DevicePlan slice, device ns of the whole
+    call incl. collectives, stats).  Concatenating the slices of all ranks in
+    rank order is the single-GPU plan byte for byte."""
+
+    def __init__(self, engine, group=None):
+        import torch
+        import torch.distributed as dist
+
+        self.eng = engine
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        nccl = dist.get_backend(group) == "nccl"
+        self.dev = torch.device("cuda", torch.cuda.current_device()) if nccl else torch.device("cpu")
+        self.exchanges = 0
+        self.bytes = 0
+
+    def _allgather(self, t):
+        """Variable-length all-gather of a 1-D int32 tensor -> concatenation
+        in rank order."""
+        import torch
+        import torch.distributed as dist
+
+        n = torch.tensor([t.numel()], dtype=torch.int64, device=self.dev)
+        sizes = [torch.empty_like(n) for _ in range(self.world)]
+        dist.all_gather(sizes, n, group=self.group)
+        sizes = [int(x) for x in sizes]
+        cap = max(1, max(sizes))
+        buf = torch.zeros(cap, dtype=torch.int32, device=self.dev)
+        if t.numel():
+            buf[: t.numel()] = t
+        outs = [torch.empty(cap, dtype=torch.int32, device=self.dev) for _ in range(self.world)]
+        dist.all_gather(outs, buf, group=self.group)
+        self.exchanges += 1
+        self.bytes += 4 * sum(sizes)
+        return torch.cat([o[:s] for o, s in zip(outs, sizes)]) if sum(sizes) else buf[:0]
+
+    def _take_run(self, h, n):
+        import torch
+
+        run = torch.empty(int(n), dtype=torch.int32, device=self.dev)
+        if n:
+            self.eng.ctx.check(self.eng.lib.f4b_shard_take_run(h, C_ptr(run), int(n)), "shard take_run")
+        return run
+
+    def compile(self, row_basis, row_shift, closure: bool = True, candidates=None, dict_cap=10**6):
+        import ctypes as C
+
+        import torch
+
+        from .engine import DevicePlan, ptr
+
+        eng = self.eng
+        lib, ctx = eng.lib, eng.ctx
+        rb = np.ascontiguousarray(row_basis, dtype=np.int32)
+        sh = np.ascontiguousarray(np.asarray(row_shift), dtype=np.uint16).reshape(len(rb), eng.n_vars)
+        cand = None if candidates is None else np.ascontiguousarray(candidates, dtype=np.int32)
+        ctx.sync_stream()
+        stream = torch.cuda.current_stream()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        lens = eng.basis_lengths()[rb]
+        lo, hi = balanced_ranges(lens, self.world)[self.rank]
+        h = C.c_void_p()
+        nrun = C.c_int64()
+        ctx.check(lib.f4b_shard_begin(ctx.h, len(rb), ptr(rb, C.c_int32), ptr(sh, C.c_uint16), 1 if closure else 0,
+                                      ptr(cand, C.c_int32) if cand is not None else None,
+                                      0 if cand is None else len(cand), int(dict_cap), lo, hi, C.byref(h),
+                                      C.byref(nrun)), "shard begin")
+        try:
+            runs = self._allgather(self._take_run(h, nrun.value))
+            nf = C.c_int64()
+            ctx.check(lib.f4b_shard_merge(h, C_ptr(runs), runs.numel(), C.byref(nf)), "shard merge")
+            rounds = 0
+            while nf.value > 0:
+                per = -(-nf.value // self.world)
+                f_lo, f_hi = min(nf.value, self.rank * per), min(nf.value, (self.rank + 1) * per)
+                red = torch.empty(max(f_hi - f_lo, 0), dtype=torch.int32, device=self.dev)
+                ctx.check(lib.f4b_shard_round(h, f_lo, f_hi, C_ptr(red), C.byref(nrun)), "shard round")
+                run = self._take_run(h, nrun.value)
+                red_all = self._allgather(red)
+                runs = self._allgather(run)
+                ctx.check(lib.f4b_shard_round_merge(h, C_ptr(red_all), nf.value, C_ptr(runs), runs.numel(),
+                                                    C.byref(nf)), "shard round merge")
+                rounds += 1
+            r_total = C.c_int64()
+            ctx.check(lib.f4b_shard_rows(h, C.byref(r_total), None), "shard rows")
+            starts = np.empty(r_total.value + 1, dtype=np.uint32)
+            ctx.check(lib.f4b_shard_rows(h, C.byref(r_total), starts.ctypes.data_as(C.c_void_p)), "shard rows")
+            lo2, hi2 = balanced_ranges(np.diff(starts.astype(np.int64)), self.world)[self.rank]
+            ph = C.c_void_p()
+            ctx.check(lib.f4b_shard_finish(h, lo2, hi2, C.byref(ph)), "shard finish")
+            plan = DevicePlan(eng, ph)
+        finally:
+            lib.f4b_shard_free(h)
+        ev1.record(stream)
+        ev1.synchronize()
+        ns = int(ev0.elapsed_time(ev1) * 1e6)
+        return plan, ns, {"rows": (lo2, hi2), "input_rows": (lo, hi), "exchange_rounds": rounds}
+
+
+def C_ptr(t):
+    """Raw data pointer of a torch tensor (host or device) for the C ABI."""
+    import ctypes as C
+
+    return C.c_void_p(t.data_ptr()) if t.numel() else None

@@ -260,6 +260,10 @@ class Engine:
     def n_polys(self) -> int:
         return len(self._lens)
 
+    def basis_lengths(self) -> np.ndarray:
+        """Term counts of the device basis polynomials (host mirror)."""
+        return self._lens
+
     def clear_basis(self):
         self.ctx.check(self.lib.f4b_basis_clear(self.ctx.h), "basis clear")
         self._reset_mirror()

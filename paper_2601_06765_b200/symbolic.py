@@ -213,7 +213,7 @@ _get_shift = operator.attrgetter("shift")
 
 
 def compile_batch(rows, basis: SoaPolySet, closure: Closure = Closure.ONE_STEP_REDUCTION,
-                  policy: ExecPolicy = DEFAULT_POLICY, candidates=None, *, dict_cap: int = DICT_CAP) -> LayoutPlan:
+                  policy: ExecPolicy = DEFAULT_POLICY, candidates=None, *, dict_cap: int | None = None) -> LayoutPlan:
     """Compile a deterministic row list into a layout plan on the GPU.
 
     Same contract as the reference (:293-388): closure rows are appended per
@@ -240,7 +240,7 @@ def compile_batch(rows, basis: SoaPolySet, closure: Closure = Closure.ONE_STEP_R
     # compare by value: callers may pass the reference's own Closure enum
     one_step = getattr(closure, "value", closure) == Closure.ONE_STEP_REDUCTION.value
     dev = eng.compile(rb, sh, one_step,
-                      None if candidates is None else list(candidates), dict_cap)
+                      None if candidates is None else list(candidates), DICT_CAP if dict_cap is None else dict_cap)
     info = dev.info
     M = info["M"]
     counters = PlanCounters(r=info["r"], N=info["N"], M=M, nnz=M, closure_rounds=info["closure_rounds"],
