@@ -139,6 +139,12 @@ int f4b_plan_download_ref_keys(const f4b_plan* plan, uint64_t* keys);
  * dictionary, so Y = 0 is the exact recombination Σ v_i t_i g_{k_i} = 0. */
 int f4b_plan_left_apply(const f4b_plan* plan, const uint64_t* V, int64_t b, uint64_t* Y);
 int f4b_plan_free(f4b_plan* plan);
+/* plan_to_text (symbolic.py:438-460) number lists formatted on the device:
+ * which = 0 row_ptr, 1 col_ind, 2 val, 3 dict_keys (reference key words, row
+ * major); decimal numbers separated by one space, no label, no newline.
+ * *length receives the byte count; the text is written when cap >= length
+ * (call with out = NULL to size the buffer). */
+int f4b_plan_text(const f4b_plan* plan, int which, char* out, int64_t cap, int64_t* length);
 
 /* ---- sharded compile_batch (one rank per GPU) ----
  * The stages of compile_batch (symbolic.py:293-388) between which the caller
@@ -202,6 +208,13 @@ int f4b_echelon_download(const f4b_echelon* ech, int which, int64_t* leads, int6
 /* pivot_cols (ascending, rank entries) — available in both modes. */
 int f4b_echelon_pivot_cols(const f4b_echelon* ech, int64_t* cols);
 int f4b_echelon_free(f4b_echelon* ech);
+
+/* csr_transpose (sparselin.py:108-121): stable counting-sort transpose on
+ * the device; host CSR in (n_rows x n_cols), host CSR out (n_cols x n_rows:
+ * t_row_ptr [n_cols + 1], t_col_ind / t_val [nnz]). */
+int f4b_csr_transpose(f4b_ctx* ctx, int64_t n_rows, int64_t n_cols, const int64_t* row_ptr,
+                      const int64_t* col_ind, const uint64_t* val, int64_t* t_row_ptr,
+                      int64_t* t_col_ind, uint64_t* t_val);
 
 /* spmm (sparselin.py:142-173): Y = A X mod p; A host CSR (n_rows x n_cols),
  * X host [n_cols][b], Y host [n_rows][b]; u64 standard residues. */

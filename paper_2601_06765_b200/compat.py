@@ -5,10 +5,11 @@
     compat.install(fpgb)          # fpgb.groebner now runs the hot path on the GPU
 
 `f4_step` (reference groebner.py:253-311) resolves `compile_batch`,
-`csr_from_plan` and `psge_reduce` from the `fpgb.groebner` module namespace
-(imported at groebner.py:32-50), so rebinding those three names routes every
-F4 step of `f4_groebner`, `run_pipeline` and `verify_instance` through the
-CUDA engine.  The GPU functions accept the reference's own objects by duck
+`csr_from_plan`, `psge_reduce` and `left_kernel` from the `fpgb.groebner`
+module namespace (imported at groebner.py:32-50), so rebinding those four
+names routes every F4 step of `f4_groebner`, `run_pipeline` and
+`verify_instance` through the CUDA engine, including the kernel-solver
+variant (`numeric="wiedemann"`, groebner.py:276-283).  The GPU functions accept the reference's own objects by duck
 typing (rows with .shift/.basis_index/.role/.provenance, a SoaPolySet with
 .ring/.exps/.coeff/.length/.offset) and return objects with the attributes
 the reference reads (LayoutPlan .counters/.timings_ns/.dict_keys/.row_meta,
@@ -23,12 +24,7 @@ from __future__ import annotations
 from . import sparselin, symbolic
 
 _SAVED: dict = {}
-PATCHED = ("compile_batch", "csr_from_plan", "psge_reduce")
-
-
-def _ring_adapter(ring):
-    """The device engine only needs p, n_vars, order and the key width."""
-    return ring
+PATCHED = ("compile_batch", "csr_from_plan", "psge_reduce", "left_kernel")
 
 
 # microbench (reference bench.py:244-312) is looked up in fpgb.bench and, by
@@ -45,6 +41,7 @@ def install(fpgb_pkg) -> None:
     g.compile_batch = symbolic.compile_batch
     g.csr_from_plan = sparselin.csr_from_plan
     g.psge_reduce = sparselin.psge_reduce
+    g.left_kernel = sparselin.left_kernel
     for mod in MICRO_MODULES:
         m = getattr(fpgb_pkg, mod, None)
         if m is not None and hasattr(m, "microbench"):

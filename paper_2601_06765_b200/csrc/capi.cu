@@ -821,6 +821,17 @@ __global__ void k_ref_keys(const uint16_t* __restrict__ ex, long long N, int n, 
   for (int q = 0; q < W; ++q) out[i * W + q] = w[q];
 }
 
+extern "C++" {
+namespace f4b {
+// reference keys of the plan dictionary (column order) into a device buffer
+void ref_keys_device(Ctx* c, const f4b_plan* pl, unsigned long long* out, int W) {
+  if (pl->N)
+    F4B_LAUNCH(c, k_ref_keys, (int)((pl->N + 255) / 256), 256, 0, pl->dict_exps.as<uint16_t>(), pl->N, c->n_vars,
+               c->order, W, out);
+}
+}  // namespace f4b
+}
+
 int f4b_plan_download_ref_keys(const f4b_plan* pl, uint64_t* keys) {
   if (!pl) return F4B_ERR_PRECONDITION;
   API_BEGIN(pl->ctx)

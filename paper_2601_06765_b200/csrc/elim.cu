@@ -1652,21 +1652,26 @@ static void launch_sweep(Ctx* c, const Fp& fp, f4b_echelon* E, const u32* rows, 
                                     200 * 1024 + 4096), "attr");
     attr = true;
   }
+  // profiled as k_sweep<MODE> (the tests check which sweep ran)
+  ProfScope ps(c, MODE ? "k_sweep<1>" : "k_sweep<0>");
   if (gl) {
     DBuf gacc;
     ensure(c, gacc, (size_t)grid * N * sizeof(u32));
-    F4B_LAUNCH(c, (k_sweep<MODE, u32>), grid, SW_THREADS, smem, fp, E->rp, E->col, E->val, N, rows, nrows,
+    k_sweep<MODE, u32><<<grid, SW_THREADS, smem, c->stream>>>(fp, E->rp, E->col, E->val, N, rows, nrows,
                E->desc.as<uint4>(), E->invl.as<u32>(), E->abits.as<u32>(), gacc.as<u32>(), Dp, K, E->nonA.as<u32>(),
                Rd, rankD, dpiv, pcol, pval, cap, cursor, s_off, s_len, err, stats);
+    check_cuda(cudaGetLastError(), "k_sweep");
     release(c, gacc);
   } else if (small_p) {
-    F4B_LAUNCH(c, (k_sweep<MODE, uint16_t>), grid, SW_THREADS, smem, fp, E->rp, E->col, E->val, N, rows, nrows,
+    k_sweep<MODE, uint16_t><<<grid, SW_THREADS, smem, c->stream>>>(fp, E->rp, E->col, E->val, N, rows, nrows,
                E->desc.as<uint4>(), E->invl.as<u32>(), E->abits.as<u32>(), (uint16_t*)nullptr, Dp, K,
                E->nonA.as<u32>(), Rd, rankD, dpiv, pcol, pval, cap, cursor, s_off, s_len, err, stats);
+    check_cuda(cudaGetLastError(), "k_sweep");
   } else {
-    F4B_LAUNCH(c, (k_sweep<MODE, u32>), grid, SW_THREADS, smem, fp, E->rp, E->col, E->val, N, rows, nrows,
+    k_sweep<MODE, u32><<<grid, SW_THREADS, smem, c->stream>>>(fp, E->rp, E->col, E->val, N, rows, nrows,
                E->desc.as<uint4>(), E->invl.as<u32>(), E->abits.as<u32>(), (u32*)nullptr, Dp, K, E->nonA.as<u32>(),
                Rd, rankD, dpiv, pcol, pval, cap, cursor, s_off, s_len, err, stats);
+    check_cuda(cudaGetLastError(), "k_sweep");
   }
 }
 

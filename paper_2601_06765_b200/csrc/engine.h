@@ -205,6 +205,7 @@ struct f4b_echelon;
 
 namespace f4b {
 void plan_release(f4b_plan* pl);
+void ref_keys_device(Ctx* c, const f4b_plan* pl, unsigned long long* out, int W);  // capi.cu
 }
 
 namespace f4b {

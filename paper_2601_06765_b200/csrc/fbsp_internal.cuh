@@ -26,4 +26,5 @@ void encode_basis_kw(Ctx* c, const KeyFmt& f, int KW);
 std::vector<int32_t> reducer_preference(Ctx* c, const std::vector<int32_t>& cand);
 bool rank_path_ok_pub(const Ctx* c, int order, int n, long long D);
 
+
 }  // namespace f4b

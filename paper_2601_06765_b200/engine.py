@@ -68,6 +68,19 @@ class DevicePlan:
                                   "plan keys")
         return out
 
+    _TEXT = {"row_ptr": 0, "col_ind": 1, "val": 2, "dict_keys": 3}
+
+    def text(self, which: str) -> bytes:
+        """One number list of plan_to_text (reference symbolic.py:438-460)
+        formatted on the device (decimal, space separated)."""
+        e = self.engine
+        n = C.c_int64()
+        code = self._TEXT[which]
+        e.ctx.check(e.lib.f4b_plan_text(self.h, code, None, 0, C.byref(n)), "plan text")
+        buf = C.create_string_buffer(max(n.value, 1))
+        e.ctx.check(e.lib.f4b_plan_text(self.h, code, buf, n.value, C.byref(n)), "plan text")
+        return buf.raw[: n.value]
+
     def download(self, arrays=True, dict_exps=True, closure=True):
         e, n = self.engine, self.engine.n_vars
         r, M, N, ncl = (self.info[k] for k in ("r", "M", "N", "n_closure_rows"))
@@ -372,6 +385,22 @@ class Engine:
         h = C.c_void_p()
         self.ctx.check(self.lib.f4b_psge_plan(self.ctx.h, plan.h, 1 if full else 0, C.byref(h)), "psge")
         return DeviceEchelon(self, h, keepalive=plan)
+
+    def csr_transpose(self, n_rows, n_cols, row_ptr, col_ind, val):
+        """Stable transpose on the device (f4b_csr_transpose) -> (row_ptr,
+        col_ind, val) of the n_cols x n_rows matrix."""
+        rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+        ci = np.ascontiguousarray(col_ind, dtype=np.int64)
+        va = np.ascontiguousarray(val, dtype=np.uint64)
+        nnz = int(rp[n_rows]) if len(rp) else 0
+        trp = np.empty(n_cols + 1, dtype=np.int64)
+        tci = np.empty(max(nnz, 1), dtype=np.int64)
+        tva = np.empty(max(nnz, 1), dtype=np.uint64)
+        self.ctx.sync_stream()
+        self.ctx.check(self.lib.f4b_csr_transpose(self.ctx.h, n_rows, n_cols, ptr(rp, C.c_int64), ptr(ci, C.c_int64),
+                                                  ptr(va, C.c_uint64), ptr(trp, C.c_int64), ptr(tci, C.c_int64),
+                                                  ptr(tva, C.c_uint64)), "csr transpose")
+        return trp, tci[:nnz], tva[:nnz]
 
     def psge_csr(self, n_rows, n_cols, row_ptr, col_ind, val, full: bool) -> DeviceEchelon:
         rp = np.ascontiguousarray(row_ptr, dtype=np.int64)

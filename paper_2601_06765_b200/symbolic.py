@@ -315,25 +315,35 @@ def plan_stats(plan: LayoutPlan) -> dict:
             "row_length_histogram": hist}
 
 
-def plan_to_text(plan: LayoutPlan) -> str:
-    """Canonical dump (reference :438-460), byte-identical."""
+def _plan_text_parts(plan: LayoutPlan):
+    """The lines of plan_to_text as byte chunks.  A device plan whose arrays
+    were never touched on the host streams its number lists from the device
+    (f4b_plan_text) instead of formatting millions of ints in
+    Python; the bytes are identical either way."""
     c = plan.counters
+    yield (f"fpgb-plan v1\np {plan.ring.modulus.p}\norder {plan.ring.order}\nvars " + " ".join(plan.ring.var_names)
+           + f"\ncounters r={c.r} N={c.N} M={c.M} nnz={c.nnz} closure_rounds={c.closure_rounds} "
+           f"keys_emitted={c.keys_emitted} keys_generated_total={c.keys_generated_total}\n").encode()
+    dev = plan.device
+    for name in ("row_ptr", "col_ind", "val", "dict_keys"):
+        yield f"{name} ".encode()
+        if dev is not None and name not in plan._host:
+            yield dev.text(name)
+        else:
+            yield " ".join(map(str, np.asarray(getattr(plan, name)).ravel().tolist())).encode()
+        yield b"\n"
     meta = " ".join(",".join([*map(str, r.shift), str(r.basis_index), str(r.role.value), str(r.provenance)])
                     for r in plan.row_meta)
-    return "\n".join([
-        "fpgb-plan v1",
-        f"p {plan.ring.modulus.p}",
-        f"order {plan.ring.order}",
-        "vars " + " ".join(plan.ring.var_names),
-        f"counters r={c.r} N={c.N} M={c.M} nnz={c.nnz} closure_rounds={c.closure_rounds} "
-        f"keys_emitted={c.keys_emitted} keys_generated_total={c.keys_generated_total}",
-        "row_ptr " + " ".join(map(str, np.asarray(plan.row_ptr).tolist())),
-        "col_ind " + " ".join(map(str, np.asarray(plan.col_ind).tolist())),
-        "val " + " ".join(map(str, np.asarray(plan.val).tolist())),
-        "dict_keys " + " ".join(map(str, np.asarray(plan.dict_keys).ravel().tolist())),
-        "row_meta " + meta,
-    ]) + "\n"
+    yield ("row_meta " + meta + "\n").encode()
+
+
+def plan_to_text(plan: LayoutPlan) -> str:
+    """Canonical dump (reference :438-460), byte-identical."""
+    return b"".join(_plan_text_parts(plan)).decode()
 
 
 def plan_digest(plan: LayoutPlan) -> str:
-    return hashlib.sha256(plan_to_text(plan).encode()).hexdigest()
+    h = hashlib.sha256()
+    for part in _plan_text_parts(plan):
+        h.update(part)
+    return h.hexdigest()

@@ -267,14 +267,27 @@ def test_f4_steps_match_reference_sort_path(cuda, force_option, name, gen, args)
         k += 1
 
 
+_FALLBACK_KERNELS = {("dict_sort", 1): "k_tile_dict", ("fbsp", 1): "k_rank_fill", ("sweep", 1): "k_sweep_blk",
+                     ("sweep", 2): "k_sweep<0", ("dense", 1): "k_dense_forward"}
+
+
 @pytest.mark.parametrize("name", ["cyclic8_p32003", "katsura11_p32003"])
-@pytest.mark.parametrize("option", [("dict_sort", 1), ("fbsp", 1), ("sweep", 1), ("sweep", 2), ("dense", 1)])
+@pytest.mark.parametrize("option", list(_FALLBACK_KERNELS))
 def test_large_step_replay_fallback_paths(cuda, force_option, name, option):
     """The north-star replays through every fallback path: radix-sort
     dictionary, multi-launch rank pipeline, blocked / generic C-row sweeps and
-    the per-pivot D' elimination (each forced via f4b_ctx_set_option)."""
+    the per-pivot D' elimination (each forced via f4b_ctx_set_option), with
+    the in-library launch profile proving the forced kernel ran."""
+    from paper_2601_06765_b200.engine import Engine
+
     force_option(*option)
+    ring, _ = state_from_snapshot(next(iter(load_snapshots(name).values())))
+    eng = Engine.for_ring(ring)
+    eng.profile(True)
     test_large_step_replay(cuda, name)
+    prof, _ = eng.profile_read()
+    eng.profile(False)
+    assert any(k.startswith(_FALLBACK_KERNELS[option]) for k in prof), sorted(prof)
 
 
 def test_f4_groebner_entry_point(cuda):
@@ -644,3 +657,59 @@ def test_mq16_wiedemann_kernel_matches_reference(cuda):
         for v in kb.vectors:
             h.update(("v:" + ",".join(str(int(x)) for x in v) + ";").encode())
         assert h.hexdigest() == g["kernel_sha256"]
+
+
+@pytest.mark.parametrize("shape,density", [((40, 30), 0.2), ((300, 1200), 0.02), ((1, 5), 1.0), ((7, 3), 0.0)])
+def test_csr_transpose_device(cuda, shape, density):
+    """f4b_csr_transpose (reference sparselin.py:108-121: stable counting-sort
+    transpose) against NumPy's stable argsort."""
+    from paper_2601_06765_b200.sparselin import csr_transpose
+
+    p = 32003
+    rng = np.random.default_rng(shape[0] * 7 + shape[1])
+    mat = _random_sparse(rng, shape[0], shape[1], density, p)
+    A = csr_from_dense(mat, FieldModulus(p))
+    T = csr_transpose(A)
+    want = csr_from_dense(np.ascontiguousarray(mat.T), FieldModulus(p))
+    assert (T.n_rows, T.n_cols) == (shape[1], shape[0])
+    assert np.array_equal(T.row_ptr, want.row_ptr) and np.array_equal(T.col_ind, want.col_ind)
+    assert np.array_equal(T.val, want.val)
+
+
+def test_plan_text_streamed_from_device(cuda):
+    """plan_to_text of a device plan streams its number lists from the device
+    (f4b_plan_text); the text equals the host formatting of the downloaded
+    arrays and the reference digest (cyclic-8 step 19, M = 2.68 M)."""
+    from paper_2601_06765_b200.symbolic import LayoutPlan
+
+    snaps = load_snapshots("cyclic8_p32003")
+    gold = load_golden("cyclic8_p32003")
+    ring, st = state_from_snapshot(snaps[19])
+    spec, _ = select_batch(st)
+    soa = st.soa()
+    plan = compile_batch(select_rows(spec, soa), soa, Closure.ONE_STEP_REDUCTION)
+    dev_text = plan_to_text(plan)
+    host = LayoutPlan(ring, plan.row_ptr, plan.col_ind, plan.val, plan.dict_keys, plan.row_meta, plan.counters)
+    assert dev_text == plan_to_text(host)
+    assert hashlib.sha256(dev_text.encode()).hexdigest() == gold["steps"][19]["plan_sha256"]
+
+
+def test_snapshot_resume_gpu(cuda, tmp_path):
+    """A binary state snapshot taken mid-run (snapshot.py) resumes the GPU F4
+    loop to the reference's final reduced basis (cyclic-6)."""
+    from paper_2601_06765_b200.groebner import reduce_basis_device
+    from paper_2601_06765_b200.snapshot import load_state, save_state
+
+    ring, polys = gen_cyclic(6, 32003)
+    st = GroebnerState(ring)
+    for f in polys:
+        update_pairs(st, poly_monic(f))
+    for _ in range(6):
+        f4_step(st)
+    path = str(tmp_path / "c6.f4bsnap")
+    save_state(st, path)
+    st2 = load_state(path)
+    while st2.n_pairs():
+        f4_step(st2)
+    gb = reduce_basis_device(st2.basis, ring)
+    assert hashlib.sha256(format_system(ring, gb).encode()).hexdigest() == load_golden("cyclic6_p32003")["final_sha256"]

@@ -195,15 +195,15 @@ def test_compat_shim_rebinds_reference_names():
 
     from paper_2601_06765_b200 import bench
 
-    g = types.SimpleNamespace(compile_batch=1, csr_from_plan=2, psge_reduce=3)
+    g = types.SimpleNamespace(compile_batch=1, csr_from_plan=2, psge_reduce=3, left_kernel=6)
     b, cli = types.SimpleNamespace(microbench=4), types.SimpleNamespace(microbench=5)
     fake = types.SimpleNamespace(groebner=g, bench=b, cli=cli)
     compat.install(fake)
     assert g.compile_batch is symbolic.compile_batch and g.psge_reduce is sparselin.psge_reduce
-    assert g.csr_from_plan is sparselin.csr_from_plan
+    assert g.csr_from_plan is sparselin.csr_from_plan and g.left_kernel is sparselin.left_kernel
     assert b.microbench is bench.microbench and cli.microbench is bench.microbench
     compat.uninstall(fake)
-    assert (g.compile_batch, g.csr_from_plan, g.psge_reduce) == (1, 2, 3)
+    assert (g.compile_batch, g.csr_from_plan, g.psge_reduce, g.left_kernel) == (1, 2, 3, 6)
     assert (b.microbench, cli.microbench) == (4, 5)
 
 
