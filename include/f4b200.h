@@ -208,6 +208,12 @@ int f4b_echelon_download(const f4b_echelon* ech, int which, int64_t* leads, int6
 /* pivot_cols (ascending, rank entries) — available in both modes. */
 int f4b_echelon_pivot_cols(const f4b_echelon* ech, int64_t* cols);
 int f4b_echelon_free(f4b_echelon* ech);
+/* The F4 harvest on the device (groebner.py:285-290): append
+ * the echelon's nonpivot rows (new leading monomials) to the device basis in
+ * the driver's order (ascending key(LM)), exponents gathered from the plan's
+ * dictionary (plan = the echelon's input), coefficients from the echelon —
+ * device to device, no host copy of the terms. */
+int f4b_basis_append_echelon(f4b_ctx* ctx, const f4b_plan* plan, const f4b_echelon* ech);
 
 /* csr_transpose (sparselin.py:108-121): stable counting-sort transpose on
  * the device; host CSR in (n_rows x n_cols), host CSR out (n_cols x n_rows:

@@ -99,6 +99,7 @@ SIGNATURES = {
     "f4b_echelon_download": (C.c_int, [C.c_void_p, C.c_int, i64p, i64p, i64p, u64p]),
     "f4b_echelon_pivot_cols": (C.c_int, [C.c_void_p, i64p]),
     "f4b_echelon_free": (C.c_int, [C.c_void_p]),
+    "f4b_basis_append_echelon": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "f4b_spmm": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, i64p, i64p, u64p, u64p, C.c_int64, u64p]),
     "f4b_dict_build": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_void_p, i64p]),
     "f4b_join_index": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int, C.c_void_p]),

@@ -951,6 +951,14 @@ int f4b_echelon_pivot_cols(const f4b_echelon* e, int64_t* cols) {
   return F4B_OK;
 }
 
+int f4b_basis_append_echelon(f4b_ctx* h, const f4b_plan* plan, const f4b_echelon* ech) {
+  if (!h || !plan || !ech) return F4B_ERR_PRECONDITION;
+  API_BEGIN(&h->c)
+  basis_finish(_c);
+  basis_append_echelon(_c, plan, ech);
+  API_END
+}
+
 int f4b_echelon_free(f4b_echelon* e) {
   echelon_release(e);
   return F4B_OK;

@@ -1119,6 +1119,7 @@ __global__ void __launch_bounds__(SW_THREADS) k_dense_back(Fp fp, const u32* __r
 // ---------------------------------------------------------------------------
 struct DblkState {
   u32 cnt, np, rho, rho_old, iters, t2_us, t3_us, t3a_us;  // t*_us: CTA 0 phase times (trace)
+  u32 t2a_us, t2b_us, t2c_us, pad;                         // phase 2 split: window load | forward | back + inverse
 };
 F4B_DEV unsigned long long gtimer() {
   unsigned long long t;
@@ -1208,7 +1209,7 @@ __global__ void __launch_bounds__(DB_THREADS) k_dense_blk(Fp fp, u32* __restrict
     lead[lo + r] = s_lead[r];
     if (s_lead[r] < K) offer(lo + r);
   }
-  unsigned long long t2 = 0, t3 = 0, t3a = 0, tm = 0;
+  unsigned long long t2 = 0, t3 = 0, t3a = 0, tm = 0, t2a = 0, t2b = 0, t2c = 0;
   while (true) {
     grid.sync();  // offers complete, every row of this iteration final
     if (bid == 0 && tid == 0) tm = gtimer();
@@ -1251,6 +1252,11 @@ __global__ void __launch_bounds__(DB_THREADS) k_dense_blk(Fp fp, u32* __restrict
         if (lane == 0) s_rl[w] = l;
       }
       __syncthreads();
+      unsigned long long tb0 = 0;
+      if (tid == 0) {
+        tb0 = gtimer();
+        t2a += tb0 - tm;
+      }
       // 2b: forward elimination inside the window (row scaling, no inverses)
       while (true) {
         unsigned long long m = ~0ull;
@@ -1292,6 +1298,11 @@ __global__ void __launch_bounds__(DB_THREADS) k_dense_blk(Fp fp, u32* __restrict
         }
         __syncthreads();
       }
+      if (tid == 0) {
+        const unsigned long long tc0 = gtimer();
+        t2b += tc0 - tb0;
+        tb0 = tc0;
+      }
       // 2c: back-elimination over the pivot columns and the coefficients
       // (one warp per pivot row): E[:, L] becomes diagonal, then Z / diag =
       // T^-1 expressed over the candidate slots
@@ -1320,6 +1331,7 @@ __global__ void __launch_bounds__(DB_THREADS) k_dense_blk(Fp fp, u32* __restrict
       }
       if (tid < (int)np) s_dinv[tid] = fp.to_mont(fp.inv(s_U[tid][tid]));
       __syncthreads();
+      if (tid == 0) t2c += gtimer() - tb0;
       // T^-1[i][j] = Z_i[slot of S_j] / d_i
       for (u32 e = tid; e < np * np; e += DB_THREADS) {
         const u32 i = e / np, j = e % np;
@@ -1419,11 +1431,13 @@ __global__ void __launch_bounds__(DB_THREADS) k_dense_blk(Fp fp, u32* __restrict
 #pragma unroll
         for (int r = 0; r < DB_G; ++r) {
           if ((u32)r < ng) {
-            // coefficients past np are zero (lanes >= np wrote 0)
+            // coefficients past np are zero (lanes >= np wrote 0): the
+            // groups of 4 beyond np are skipped (warp-uniform exit)
             const uint4* cr = reinterpret_cast<const uint4*>(s_c + s_act[g0 + r] * DB_NP);
             u64 a = 0;
 #pragma unroll
             for (int j4 = 0; j4 < DB_NP / 4; ++j4) {
+              if (4 * j4 >= (int)np) break;
               const uint4 cv = cr[j4];
               a += prod(cv.x, pv[4 * j4]) + prod(cv.y, pv[4 * j4 + 1]) + prod(cv.z, pv[4 * j4 + 2]) +
                    prod(cv.w, pv[4 * j4 + 3]);
@@ -1464,6 +1478,9 @@ __global__ void __launch_bounds__(DB_THREADS) k_dense_blk(Fp fp, u32* __restrict
   if (bid == 0) {
     if (tid == 0) {
       st->t2_us = (u32)(t2 / 1000);
+      st->t2a_us = (u32)(t2a / 1000);
+      st->t2b_us = (u32)(t2b / 1000);
+      st->t2c_us = (u32)(t2c / 1000);
       st->t3_us = (u32)(t3 / 1000);
       st->t3a_us = (u32)(t3a / 1000);
     }
@@ -1816,9 +1833,9 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
           DblkState hs;
           check_cuda(cudaMemcpyAsync(&hs, stt.p, sizeof(hs), cudaMemcpyDeviceToHost, c->stream), "d2h");
           check_cuda(cudaStreamSynchronize(c->stream), "sync");
-          fprintf(stderr, "[blk] R=%lld K=%lld G=%lld rpc=%lld rank=%u iters=%u t2=%uus t3=%uus (setup %uus)\n",
-                  (long long)R, (long long)K, (long long)G, (long long)rpc, hs.rho, hs.iters, hs.t2_us, hs.t3_us,
-                  hs.t3a_us);
+          fprintf(stderr, "[blk] R=%lld K=%lld G=%lld rpc=%lld rank=%u iters=%u t2=%uus (load %u fwd %u back %u) t3=%uus (setup %uus)\n",
+                  (long long)R, (long long)K, (long long)G, (long long)rpc, hs.rho, hs.iters, hs.t2_us, hs.t2a_us,
+                  hs.t2b_us, hs.t2c_us, hs.t3_us, hs.t3a_us);
         }
         for (DBuf* b : {&Bm, &colp, &lead_b, &cand_b, &gl, &gT, &stt, &ordr}) release(c, *b);
         blk_done = true;
@@ -2124,6 +2141,89 @@ void echelon_download(const f4b_echelon* E, int which, int64_t* leads, int64_t* 
     at += len[k];
     if (row_ptr) row_ptr[k + 1] = at;
   }
+}
+
+// ---------------------------------------------------------------------------
+// Harvest on the device (reference groebner.py:285-290): the
+// nonpivot rows of an echelon appended to the device basis in the driver's
+// order (ascending key(LM) = descending lead column), exponents gathered from
+// the plan dictionary by column, no host round trip of the terms.
+// ---------------------------------------------------------------------------
+__global__ void k_append_rows(const u32* __restrict__ d_off, const u32* __restrict__ d_len, u32 nnew,
+                              const u32* __restrict__ noff, const u32* __restrict__ pcol, const u32* __restrict__ pval,
+                              const u16* __restrict__ dict_exps, int n, long long T0, u16* __restrict__ exps,
+                              u32* __restrict__ coeff, u16* __restrict__ lm, u16* __restrict__ maxe) {
+  const u32 i = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);  // new polynomial (warp)
+  const int lane = threadIdx.x & 31;
+  if (i >= nnew) return;
+  const u32 k = nnew - 1 - i;  // source row: descending lead
+  const u32 so = d_off[k], L = d_len[k], to = noff[i];
+  for (u32 t = lane; t < L; t += 32) {
+    const u32 cc = pcol[so + t];
+    for (int v = 0; v < n; ++v) exps[(T0 + to + t) * n + v] = dict_exps[(size_t)cc * n + v];
+    coeff[T0 + to + t] = pval[so + t];
+  }
+  for (int v = 0; v < n; ++v) {
+    u32 mx = 0;
+    for (u32 t = lane; t < L; t += 32) mx = max(mx, (u32)dict_exps[(size_t)pcol[so + t] * n + v]);
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    if (lane == 0) {
+      maxe[(size_t)i * n + v] = (u16)mx;
+      lm[(size_t)i * n + v] = L ? dict_exps[(size_t)pcol[so] * n + v] : (u16)0;
+    }
+  }
+}
+
+void basis_append_echelon(Ctx* c, const f4b_plan* pl, const f4b_echelon* E) {
+  Basis& B = c->basis;
+  const int n = c->n_vars;
+  const long long nnew = E->rankD;
+  if (!nnew) return;
+  if (pl->ctx != c || E->ctx != c) fail(F4B_ERR_PRECONDITION, "plan / echelon of another context");
+  std::vector<u32> len(nnew);
+  check_cuda(cudaMemcpyAsync(len.data(), E->d_len.p, nnew * 4, cudaMemcpyDeviceToHost, c->stream), "d2h");
+  check_cuda(cudaStreamSynchronize(c->stream), "sync");
+  const long long T0 = B.n_terms, P0 = B.n_polys, P1 = P0 + nnew;
+  std::vector<u32> noff(nnew + 1);
+  long long T = 0;
+  for (long long i = 0; i < nnew; ++i) {
+    noff[i] = (u32)T;
+    T += len[nnew - 1 - i];
+  }
+  noff[nnew] = (u32)T;
+  const long long T1 = T0 + T;
+  if (T1 >= (1ll << 31)) fail(F4B_ERR_SIZE_CAP, "basis has more than 2^31 terms");
+  ensure_keep(c, B.exps, (size_t)(T1 + 1) * n * sizeof(u16));
+  ensure_keep(c, B.coeff, (size_t)(T1 + 1) * sizeof(u32));
+  ensure_keep(c, B.off, (size_t)(P1 + 1) * sizeof(u32));
+  ensure_keep(c, B.len, (size_t)(P1 + 1) * sizeof(u32));
+  ensure_keep(c, B.lmexp, (size_t)(P1 + 1) * n * sizeof(u16));
+  ensure_keep(c, B.maxe, (size_t)(P1 + 1) * n * sizeof(u16));
+  DBuf dno;
+  ensure(c, dno, (size_t)(nnew + 1) * 4);
+  check_cuda(cudaMemcpyAsync(dno.p, noff.data(), (nnew + 1) * 4, cudaMemcpyHostToDevice, c->stream), "h2d");
+  F4B_LAUNCH(c, k_append_rows, nb(nnew, 8), 256, 0, E->d_off.as<u32>(), E->d_len.as<u32>(), (u32)nnew, dno.as<u32>(),
+             E->pool_col.as<u32>(), E->pool_val.as<u32>(), pl->dict_exps.as<u16>(), n, T0, B.exps.as<u16>(),
+             B.coeff.as<u32>(), B.lmexp.as<u16>() + P0 * n, B.maxe.as<u16>() + P0 * n);
+  // offsets / lengths of the new polynomials; LM and max-exponent mirrors back
+  std::vector<u32> hoff(nnew + 1), hlen(nnew);
+  for (long long i = 0; i <= nnew; ++i) hoff[i] = (u32)(B.h_off.back() + noff[i]);
+  for (long long i = 0; i < nnew; ++i) hlen[i] = len[nnew - 1 - i];
+  check_cuda(cudaMemcpyAsync(B.off.as<u32>() + P0, hoff.data(), (nnew + 1) * 4, cudaMemcpyHostToDevice, c->stream), "h2d");
+  check_cuda(cudaMemcpyAsync(B.len.as<u32>() + P0, hlen.data(), nnew * 4, cudaMemcpyHostToDevice, c->stream), "h2d");
+  std::vector<uint16_t> hlm((size_t)nnew * n), hmx((size_t)nnew * n);
+  check_cuda(cudaMemcpyAsync(hlm.data(), B.lmexp.as<u16>() + P0 * n, hlm.size() * 2, cudaMemcpyDeviceToHost, c->stream), "d2h");
+  check_cuda(cudaMemcpyAsync(hmx.data(), B.maxe.as<u16>() + P0 * n, hmx.size() * 2, cudaMemcpyDeviceToHost, c->stream), "d2h");
+  check_cuda(cudaStreamSynchronize(c->stream), "sync");
+  release(c, dno);
+  for (long long i = 0; i < nnew; ++i) {
+    B.h_len.push_back(hlen[i]);
+    B.h_off.push_back(B.h_off.back() + hlen[i]);
+  }
+  B.h_lm.insert(B.h_lm.end(), hlm.begin(), hlm.end());
+  B.h_maxe.insert(B.h_maxe.end(), hmx.begin(), hmx.end());
+  B.n_polys = (int)P1;
+  B.n_terms = T1;
 }
 
 // All pivot columns, ascending: A columns merged with the D' pivots.

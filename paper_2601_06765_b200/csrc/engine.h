@@ -218,6 +218,7 @@ void echelon_complete(Ctx* c, f4b_echelon* E);
 void echelon_info(const f4b_echelon* E, f4b_echelon_info* info);
 void echelon_download(const f4b_echelon* E, int which, int64_t* leads, int64_t* row_ptr, int64_t* cols, uint64_t* vals);
 void echelon_release(f4b_echelon* E);
+void basis_append_echelon(Ctx* c, const f4b_plan* pl, const f4b_echelon* E);
 void echelon_pivot_cols(const f4b_echelon* E, int64_t* cols);
 void spmm(Ctx* c, long long r, long long N, const int64_t* rp, const int64_t* col, const uint64_t* val,
           const uint64_t* X, long long b, uint64_t* Y);

@@ -321,6 +321,22 @@ class Engine:
         self._src = None
         self.generation += 1
 
+    def append_from_echelon(self, plan: DevicePlan, ech: DeviceEchelon, lengths, exps, coeffs):
+        """The F4 harvest on the device (f4b_basis_append_echelon): the
+        echelon's nonpivot rows appended to the device basis straight from
+        the plan dictionary and the echelon pool (device to device).  The
+        host arrays (the same polynomials, which the driver already holds)
+        only extend the prefix-check mirror; nothing is uploaded."""
+        self.ctx.sync_stream()
+        self.ctx.check(self.lib.f4b_basis_append_echelon(self.ctx.h, plan.h, ech.h), "basis append (echelon)")
+        lengths = np.ascontiguousarray(lengths, dtype=np.int64)
+        self._lens = np.concatenate([self._lens, lengths])
+        if len(coeffs):
+            self._chunks.append((self._T, np.asarray(exps), np.asarray(coeffs)))
+        self._T += len(coeffs)
+        self._src = None
+        self.generation += 1
+
     @staticmethod
     def _buffers(soa):
         # (address, strides) of the streams; the arrays themselves are kept in

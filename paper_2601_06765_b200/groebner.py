@@ -331,10 +331,16 @@ def f4_step(state: GroebnerState, config: F4Config | None = None, _capture=None)
         new_ex.append(ex)
         new_cf.append(cf)
         new_len.append(len(c))
-    # keep the device basis in lockstep (no re-upload of the whole basis)
+    # keep the device basis in lockstep: the new rows go from the echelon
+    # pool to the device basis on the device (§8f.2, no upload)
     eng = Engine.for_ring(ring)
     if getattr(soa, "_f4b_token", None) == eng.token and new_len:
-        eng.append_polys(np.asarray(new_len), np.concatenate(new_ex), np.concatenate(new_cf))
+        dplan, dech = plan.device, getattr(ech, "device", None)
+        if dplan is not None and dech is not None and dplan.engine is eng and dech.engine is eng:
+            eng.append_from_echelon(dplan, dech, np.asarray(new_len), np.concatenate(new_ex),
+                                    np.concatenate(new_cf))
+        else:
+            eng.append_polys(np.asarray(new_len), np.concatenate(new_ex), np.concatenate(new_cf))
     if getattr(soa, "_f4b_token", None) is not None and soa._f4b_token[0] == eng.uid:
         state._dev_token, state._dev_n = eng.token, len(state.basis)
     state.zero_reductions += ech.zero_row_count
