@@ -736,7 +736,26 @@ __global__ void __launch_bounds__(256) k_tail_copy(const u32* __restrict__ col, 
   }
 }
 
-template <bool PK>
+// MODE 0: C rows -> D' (dense rows over the non-A columns).  MODE 1 (full
+// RREF only): the pivot rows themselves, each swept from just after its own
+// lead (the window solve gives its own and earlier pivots zero multipliers),
+// then reduced in one step by RREF(D') (one coefficient per D' pivot),
+// made monic and emitted as sparse rows — the back-reduction of
+// sparselin.py:337-349 with the same window machinery as the C rows.
+struct SweepOut {
+  const u32* invl;
+  const u32* Rd;
+  u32 rankD;
+  const u32* dpiv;
+  u32* pcol;
+  u32* pval;
+  size_t cap;
+  unsigned long long* cursor;
+  u32* s_off;
+  u32* s_len;
+  u32* err;
+};
+template <bool PK, int MODE>
 __global__ void __launch_bounds__(256) k_sweep_win(Fp fp, u32 mu, const u32* __restrict__ rp,
                                                    const u32* __restrict__ col, const u32* __restrict__ val, u32 N,
                                                    const u32* __restrict__ rows, u32 nrows,
@@ -744,7 +763,7 @@ __global__ void __launch_bounds__(256) k_sweep_win(Fp fp, u32 mu, const u32* __r
                                                    const u32* __restrict__ winC, const uint2* __restrict__ winD,
                                                    u32 nwin, const uint4* __restrict__ tails,
                                                    u32* __restrict__ Dp, u32 K, const u32* __restrict__ nonA,
-                                                   unsigned long long* __restrict__ stats) {
+                                                   unsigned long long* __restrict__ stats, const SweepOut so) {
   extern __shared__ __align__(16) u32 smem[];
   constexpr int NWARP = 8;
   constexpr int H = 2;  // 32-group spans per warp in flight
@@ -754,6 +773,7 @@ __global__ void __launch_bounds__(256) k_sweep_win(Fp fp, u32 mu, const u32* __r
   u32* acc = smem + ((2 * nwords + 3) & ~3u);  // N + 1 slots (slot N absorbs padding)
   __shared__ u32 s_act[NWARP][32];
   __shared__ u32 s_ms[32], s_msh[32], s_ng[32], s_g0[32];
+  __shared__ u32 s_cn, s_ck[MODE == 1 ? 256 : 1], s_cv[MODE == 1 ? 256 : 1], s_red[33], s_sh[4];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const u32 p = fp.p;
   auto red = [&](u32 v) -> u32 {  // v mod p for v < 2^32 (Barrett, mu = floor(2^32 / p))
@@ -787,7 +807,7 @@ __global__ void __launch_bounds__(256) k_sweep_win(Fp fp, u32 mu, const u32* __r
     __syncthreads();
     for (u32 k = s + tid; k < e; k += blockDim.x) acc[col[k]] = val[k];
     __syncthreads();
-    u32 from = lead;
+    u32 from = MODE == 1 ? lead + 1 : lead;
     u32 pj = 0xFFFFFFFFu, pcw = 0;
     uint2 pdd = make_uint2(0, 0);
     uint4 pw4 = make_uint4(0, 0, 0, 0);
@@ -829,7 +849,7 @@ __global__ void __launch_bounds__(256) k_sweep_win(Fp fp, u32 mu, const u32* __r
       } else {
         pj = 0xFFFFFFFFu;
       }
-      const u32 v = (cw < N && cw >= lead) ? red(acc[cw]) : 0u;
+      const u32 v = (cw < N && (MODE == 1 ? cw > lead : cw >= lead)) ? red(acc[cw]) : 0u;
       // multipliers m = v W, split over the 8 warps: warp w owns pivots
       // t = 4w .. 4w+3 (lane s contributes v_s W[s][t], one 16-byte load),
       // warp sums, then Shoup constants and group counts into shared memory
@@ -932,12 +952,57 @@ __global__ void __launch_bounds__(256) k_sweep_win(Fp fp, u32 mu, const u32* __r
       __syncthreads();
       from = __reduce_max_sync(0xffffffffu, cw < N ? cw : 0u) + 1;
     }
-    u32* out = Dp + (size_t)rr * K;
-    for (u32 q = tid; q < K; q += blockDim.x) {
-      const u32 cc = nonA[q];
-      out[q] = cc >= lead ? red(acc[cc]) : 0u;
+    if (MODE == 0) {
+      u32* out = Dp + (size_t)rr * K;
+      for (u32 q = tid; q < K; q += blockDim.x) {
+        const u32 cc = nonA[q];
+        out[q] = cc >= lead ? red(acc[cc]) : 0u;
+      }
+      __syncthreads();
+    } else {
+      // reduce right of the lead (the lazy sums), then one step by RREF(D'):
+      // x <- x - sum_k x[D' pivot k] R_k (R in reduced echelon form)
+      // (the A columns right of the lead are eliminated: the window sweep
+      // leaves stale partial sums there, which are cleared, not read)
+      for (u32 c2 = lead + 1 + tid; c2 < N; c2 += blockDim.x)
+        acc[c2] = ((abits[c2 >> 5] >> (c2 & 31)) & 1u) ? 0u : red(acc[c2]);
+      __syncthreads();
+      for (u32 k0 = 0; k0 < so.rankD; k0 += 256) {
+        if (tid == 0) s_cn = 0;
+        __syncthreads();
+        for (u32 k = k0 + tid; k < min(so.rankD, k0 + 256); k += blockDim.x) {
+          const u32 cc = nonA[so.dpiv[k]];
+          const u32 v = cc > lead ? acc[cc] : 0u;
+          if (v) {
+            const u32 slot = atomicAdd(&s_cn, 1u);
+            s_ck[slot] = k;
+            s_cv[slot] = fp.to_mont(fp.neg(v));
+          }
+        }
+        __syncthreads();
+        const u32 nco = s_cn;
+        if (nco)
+          for (u32 q = tid; q < K; q += blockDim.x) {
+            const u32 cc = nonA[q];
+            if (cc <= lead) continue;
+            u32 x = acc[cc];
+            for (u32 t = 0; t < nco; ++t) x = fp.add(x, fp.mont_mul(s_cv[t], __ldg(so.Rd + (size_t)s_ck[t] * K + q)));
+            acc[cc] = x;
+          }
+        __syncthreads();
+      }
+      // monic (the lead is untouched by the sweep), then the sparse row
+      const u32 inv = so.invl[lead];
+      if (tid == 0) acc[lead] = fp.mul(red(acc[lead]), inv);
+      for (u32 c2 = lead + 1 + tid; c2 < N; c2 += blockDim.x) {
+        const u32 v = acc[c2];
+        if (v) acc[c2] = fp.mul(v, inv);
+      }
+      __syncthreads();
+      emit_row<u32>(acc, lead, N, nullptr, so.pcol, so.pval, so.cap, so.cursor, so.s_off + rr, so.s_len + rr, so.err,
+                    s_red, s_sh + 1);
+      __syncthreads();
     }
-    __syncthreads();
   }
   if (stats && tid == 0 && n_piv) {
     atomicAdd(stats, n_piv);
@@ -1578,7 +1643,7 @@ static void launch_sweep(Ctx* c, const Fp& fp, f4b_echelon* E, const u32* rows, 
   // c->opt_sweep (f4b_ctx_set_option "sweep"): 0 = automatic (windows, then
   // the blocked sweep, then k_sweep), 1 = start at the blocked sweep,
   // 2 = k_sweep only — the fallbacks are forced by the parity tests
-  if (MODE == 0 && c->opt_sweep == 0 && E->nA > 0) {
+  if (c->opt_sweep == 0 && E->nA > 0) {
     // fixed windows with precomputed block inverses (k_win_build + k_sweep_win)
     const size_t nwords = (N + 31) / 32;
     const size_t smem = (size_t)((2 * nwords + 3) & ~(size_t)3) * 4 + (size_t)(N + 1) * 4;
@@ -1588,9 +1653,9 @@ static void launch_sweep(Ctx* c, const Fp& fp, f4b_echelon* E, const u32* rows, 
       const bool pk = N < 65535u && c->p < 65536u;
       static bool wattr = false;
       if (!wattr) {
-        check_cuda(cudaFuncSetAttribute(k_sweep_win<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
+        check_cuda(cudaFuncSetAttribute(k_sweep_win<true, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
                    "attr");
-        check_cuda(cudaFuncSetAttribute(k_sweep_win<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
+        check_cuda(cudaFuncSetAttribute(k_sweep_win<false, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
                    "attr");
         wattr = true;
       }
@@ -1613,20 +1678,26 @@ static void launch_sweep(Ctx* c, const Fp& fp, f4b_echelon* E, const u32* rows, 
         F4B_LAUNCH(c, k_tail_copy<false>, nb(nA, 8), 256, 0, E->col, E->val, N, E->desc.as<uint4>(), wC.as<u32>(),
                    wD.as<uint2>(), nA, wT.as<uint2>());
       int per_sm = 0;
-      check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pk ? k_sweep_win<true> : k_sweep_win<false>,
-                                                               256, smem),
+      check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                     &per_sm, pk ? k_sweep_win<true, MODE> : k_sweep_win<false, MODE>, 256, smem),
                  "occupancy");
       per_sm = std::max(1, per_sm);
       const int grid = (int)std::max<long long>(1, std::min<long long>(nrows, (long long)c->num_sms * per_sm));
       const u32 mu = (u32)((1ull << 32) / c->p);
-      if (pk)
-        F4B_LAUNCH(c, k_sweep_win<true>, grid, 256, smem, fp, mu, E->rp, E->col, E->val, N, rows, nrows,
+      SweepOut so{E->invl.as<u32>(), Rd, rankD, dpiv, pcol, pval, cap, cursor, s_off, s_len, err};
+      {
+        ProfScope ps(c, pk ? (MODE ? "k_sweep_win<true,1>" : "k_sweep_win<true>")
+                           : (MODE ? "k_sweep_win<false,1>" : "k_sweep_win<false>"));
+        if (pk)
+          k_sweep_win<true, MODE><<<grid, 256, smem, c->stream>>>(fp, mu, E->rp, E->col, E->val, N, rows, nrows,
                    E->abits.as<u32>(), wW.as<u32>(), wC.as<u32>(), wD.as<uint2>(), nwin, wT.as<uint4>(), Dp, K,
-                   E->nonA.as<u32>(), stats);
-      else
-        F4B_LAUNCH(c, k_sweep_win<false>, grid, 256, smem, fp, mu, E->rp, E->col, E->val, N, rows, nrows,
+                   E->nonA.as<u32>(), stats, so);
+        else
+          k_sweep_win<false, MODE><<<grid, 256, smem, c->stream>>>(fp, mu, E->rp, E->col, E->val, N, rows, nrows,
                    E->abits.as<u32>(), wW.as<u32>(), wC.as<u32>(), wD.as<uint2>(), nwin, wT.as<uint4>(), Dp, K,
-                   E->nonA.as<u32>(), stats);
+                   E->nonA.as<u32>(), stats, so);
+        check_cuda(cudaGetLastError(), "k_sweep_win");
+      }
       release(c, wW);
       release(c, wC);
       release(c, wD);
