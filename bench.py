@@ -531,9 +531,16 @@ def run_gpu(args, world, rank, local):
     import torch
     import torch.distributed as dist
 
+    # one rank per GPU; F4B_DIST_BACKEND=gloo (test only) lets several ranks
+    # share the GPUs of a smaller box, exchanging through the host
+    backend = os.environ.get("F4B_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     from paper_2601_06765_b200.engine import Engine
     from paper_2601_06765_b200.groebner import reduce_basis_device
@@ -626,7 +633,8 @@ def run_gpu(args, world, rank, local):
     eng.profile(False)
     t_tot_ns = float(t_sym + t_num)
     if world > 1:
-        t = torch.tensor([t_tot_ns, float(t_sym), float(t_num)], device="cuda", dtype=torch.float64)
+        t = torch.tensor([t_tot_ns, float(t_sym), float(t_num)], dtype=torch.float64,
+                         device="cuda" if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_tot_ns, t_sym, t_num = float(t[0]), float(t[1]), float(t[2])
     ms_per_step = t_tot_ns / 1e6 / args.steps
@@ -697,7 +705,7 @@ def run_gpu(args, world, rank, local):
             "vs_baseline": None, "dtype": "u32 residues mod p (u64 monomial keys)",
             "data": "synthetic (generated cyclic-8 system, deterministic)",
             "config": {"workload": WORKLOAD, "batches": len(batches), "sum_M_per_step": total_M,
-                       "parallelism": (f"sharded compile_batch over {world} ranks (NCCL)" if shard is not None
+                       "parallelism": (f"sharded compile_batch over {world} ranks ({backend})" if shard is not None
                                        else ("replicas" if world > 1 else "single")),
                        "l2": "flushed (256 MiB write) before every batch",
                        "replay_check": "every replayed batch's (r, N, M, closure_rounds) == the live run's"},

@@ -1185,6 +1185,7 @@ __global__ void __launch_bounds__(SW_THREADS) k_dense_back(Fp fp, const u32* __r
 struct DblkState {
   u32 cnt, np, rho, rho_old, iters, t2_us, t3_us, t3a_us;  // t*_us: CTA 0 phase times (trace)
   u32 t2a_us, t2b_us, t2c_us, pad;                         // phase 2 split: window load | forward | back + inverse
+  u32 offers, distinct;                                    // trace: offers and distinct offered leads, summed over blocks
 };
 F4B_DEV unsigned long long gtimer() {
   unsigned long long t;
@@ -1202,7 +1203,7 @@ __global__ void __launch_bounds__(DB_THREADS) k_dense_blk(Fp fp, u32* __restrict
                                                           u32* __restrict__ gwin, u32* __restrict__ gT,
                                                           DblkState* __restrict__ st, u32* __restrict__ Rd,
                                                           u32* __restrict__ dpiv, u32* __restrict__ rank_out,
-                                                          u32* __restrict__ order) {
+                                                          u32* __restrict__ order, u32* __restrict__ dflag) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) u32 smem[];
   constexpr int NW = DB_THREADS / 32;
@@ -1237,9 +1238,14 @@ __global__ void __launch_bounds__(DB_THREADS) k_dense_blk(Fp fp, u32* __restrict
     }
     return (u32)(a % p);
   };
-  auto offer = [&](u32 row) {
+  u32 it_no = 1;  // block number (trace: distinct offered leads per block)
+  auto offer = [&](u32 row, u32 l) {
     const u32 s = atomicAdd(&st->cnt, 1u);
     if (s < (u32)DB_NP) cand[s] = row;
+    if (dflag) {
+      atomicAdd(&st->offers, 1u);
+      if (atomicMax(dflag + l, it_no) < it_no) atomicAdd(&st->distinct, 1u);
+    }
   };
   u32* s_f = s_lead + rpc;  // [maxt] first nonzero column of each task
   u32 ro = 0;
@@ -1272,7 +1278,7 @@ __global__ void __launch_bounds__(DB_THREADS) k_dense_blk(Fp fp, u32* __restrict
   __syncthreads();
   for (u32 r = tid; r < nr; r += DB_THREADS) {
     lead[lo + r] = s_lead[r];
-    if (s_lead[r] < K) offer(lo + r);
+    if (s_lead[r] < K) offer(lo + r, s_lead[r]);
   }
   unsigned long long t2 = 0, t3 = 0, t3a = 0, tm = 0, t2a = 0, t2b = 0, t2c = 0;
   while (true) {
@@ -1530,11 +1536,12 @@ __global__ void __launch_bounds__(DB_THREADS) k_dense_blk(Fp fp, u32* __restrict
     __syncthreads();
     if (bid == 0 && tid == 0) t3 += gtimer() - tm;
     // 1 (next iteration): offers of the live rows
+    ++it_no;
     for (u32 r = tid; r < nr; r += DB_THREADS) {
       const u32 l = s_lead[r];
       if (l <= K) {  // K + 1 = consumed
         lead[lo + r] = l;
-        if (l < K) offer(lo + r);
+        if (l < K) offer(lo + r, l);
       }
     }
   }
@@ -1892,21 +1899,29 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
         u32 *glp = gl.as<u32>(), *gTp = gT.as<u32>(), *rdp = E->Rd.as<u32>(), *dpivp = E->dpiv.as<u32>();
         u32 *rkp = E->rdev.as<u32>(), *ordp = ordr.as<u32>();
         DblkState* sp = reinterpret_cast<DblkState*>(stt.p);
+        static const bool btrace = getenv("F4B_BLK_TRACE") != nullptr;
+        DBuf dfl;
+        u32* dflp = nullptr;
+        if (btrace) {
+          ensure(c, dfl, (size_t)K * sizeof(u32));
+          check_cuda(cudaMemsetAsync(dfl.p, 0, (size_t)K * sizeof(u32), c->stream), "memset");
+          dflp = dfl.as<u32>();
+        }
         void* argsb[] = {&fp, &dpp, &Ru, &Ku, &rpcu, &maxtu, &leadp, &candp2, &bmp, &colpp, &glp, &gTp, &sp, &rdp,
-                         &dpivp, &rkp, &ordp};
+                         &dpivp, &rkp, &ordp, &dflp};
         {
           ProfScope ps(c, "k_dense_blk");
           const void* kf = c->p < 65536u ? (const void*)k_dense_blk<true> : (const void*)k_dense_blk<false>;
           check_cuda(cudaLaunchCooperativeKernel(kf, (int)G, DB_THREADS, argsb, smem_b, c->stream), "k_dense_blk");
         }
-        static const bool btrace = getenv("F4B_BLK_TRACE") != nullptr;
         if (btrace) {
+          release(c, dfl);
           DblkState hs;
           check_cuda(cudaMemcpyAsync(&hs, stt.p, sizeof(hs), cudaMemcpyDeviceToHost, c->stream), "d2h");
           check_cuda(cudaStreamSynchronize(c->stream), "sync");
-          fprintf(stderr, "[blk] R=%lld K=%lld G=%lld rpc=%lld rank=%u iters=%u t2=%uus (load %u fwd %u back %u) t3=%uus (setup %uus)\n",
+          fprintf(stderr, "[blk] R=%lld K=%lld G=%lld rpc=%lld rank=%u iters=%u t2=%uus (load %u fwd %u back %u) t3=%uus (setup %uus) offers=%u distinct=%u\n",
                   (long long)R, (long long)K, (long long)G, (long long)rpc, hs.rho, hs.iters, hs.t2_us, hs.t2a_us,
-                  hs.t2b_us, hs.t2c_us, hs.t3_us, hs.t3a_us);
+                  hs.t2b_us, hs.t2c_us, hs.t3_us, hs.t3a_us, hs.offers, hs.distinct);
         }
         for (DBuf* b : {&Bm, &colp, &lead_b, &cand_b, &gl, &gT, &stt, &ordr}) release(c, *b);
         blk_done = true;

@@ -39,6 +39,12 @@ def host_empty(shape, dtype):
 _ids = itertools.count(1)
 
 
+def _current_device() -> int:
+    import torch
+
+    return torch.cuda.current_device() if torch.cuda.is_available() else 0
+
+
 class DevicePlan:
     """Handle of an ``f4b_plan`` (device CSR + dictionary + closure rows)."""
 
@@ -213,7 +219,11 @@ class Engine:
             eng.set_option(name, value)
 
     @classmethod
-    def for_ring(cls, ring, device: int = 0) -> "Engine":
+    def for_ring(cls, ring, device: int | None = None) -> "Engine":
+        """The engine of ``ring`` on ``device`` (default: the current CUDA
+        device, so one process per GPU under torchrun uses its own GPU)."""
+        if device is None:
+            device = _current_device()
         key = (device, ring.modulus.p, ring.n_vars, ring.order)
         eng = cls._registry.get(key)
         if eng is None:
