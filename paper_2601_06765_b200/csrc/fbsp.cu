@@ -1805,43 +1805,23 @@ __global__ void __launch_bounds__(CL_THREADS) k_fbsp(const FbspArgs a) {
     i0 = g < ng ? min(nitems, g * per) : nitems;
     i1 = g < ng ? min(nitems, i0 + per) : nitems;
   };
-  // set bits of getx(w) over this CTA's chunk, ascending from `base`: keys to
-  // out_keys[pos]; with out_exps also exponents to out_exps[N_all-1-pos]
-  // (column order) and the word prefix to dwp
-  auto emit_chunk = [&](auto getx, u32 base, u64* out_keys, u16* out_exps, u32 N_all) {
+  // set bits of getx(w) over this CTA's chunk, ascending from `base`: their
+  // RANKS to out[pos] (a u32 list; the frontier consumers and the final
+  // dictionary pass unrank them, balanced over the grid) and, with dwp, the
+  // word prefix for the join.  One store per monomial: a chunk owning most of
+  // the dictionary no longer serialises the unranking.
+  auto emit_chunk = [&](auto getx, u32 base, u32* out, bool with_dwp, u32 stride) {
     for (u32 w0 = w_lo; w0 < w_hi; w0 += blockDim.x) {
       const u32 w = w0 + tid;
       const u32 x = w < w_hi ? getx(w) : 0u;
       u32 tt;
       const u32 pre = block_scan_excl(__popc(x), ws, &tt);
-      if (out_exps && w < w_hi) a.dwp[w] = make_uint2(x, base + pre);
-      auto put = [&](u32 pos, u32 rk) {
-        u16 e[NV];
-        gl_unrank<NV>(rk, n, a.D, bt, a.st, e);
-        key_store<KW>(out_keys, pos, gl_encode<KW, NV>(a.f, e));
-        if (out_exps) {
-#pragma unroll
-          for (int v = 0; v < NV; ++v)
-            if (v < n) out_exps[((long long)N_all - 1 - pos) * n + v] = e[v];
-        }
-      };
-      if (tt <= (u32)CL_LIST) {
-        u32 p = pre, m = x;
-        while (m) {
-          const int b = __ffs(m) - 1;
-          m &= m - 1;
-          list[p++] = w * 32 + b;
-        }
-        __syncthreads();
-        for (u32 q = tid; q < tt; q += blockDim.x) put(base + q, list[q]);
-        __syncthreads();
-      } else {
-        u32 p = base + pre, m = x;
-        while (m) {
-          const int b = __ffs(m) - 1;
-          m &= m - 1;
-          put(p++, w * 32 + b);
-        }
+      if (with_dwp && w < w_hi) a.dwp[w] = make_uint2(x, base + pre);
+      u32 p = base + pre, m = x;
+      while (m) {
+        const int b = __ffs(m) - 1;
+        m &= m - 1;
+        out[(size_t)(p++) * stride] = w * 32 + b;
       }
       base += tt;
     }
@@ -1949,7 +1929,7 @@ __global__ void __launch_bounds__(CL_THREADS) k_fbsp(const FbspArgs a) {
           const u32 d = __ldcg(a.dict + w), dn = __ldcg(a.done + w);
           if (dn) a.done[w] = 0;
           return d & ~dn;
-        }, base, a.front0, nullptr, 0u);
+        }, base, reinterpret_cast<u32*>(a.front0), false, 1u);
       }
       grid.sync();
     }
@@ -1960,8 +1940,8 @@ __global__ void __launch_bounds__(CL_THREADS) k_fbsp(const FbspArgs a) {
   u32 Mcur = a.M0;
   int sel = 0;
   while (!flags && nf > 0 && a.nc > 0) {
-    const u64* front = sel ? a.front1 : a.front0;
-    u64* fnext = sel ? a.front0 : a.front1;
+    const u32* front = reinterpret_cast<const u32*>(sel ? a.front1 : a.front0);  // ranks, ascending
+    u32* fnext = reinterpret_cast<u32*>(sel ? a.front0 : a.front1);
     u32* cur = (rounds & 1) ? cnt_b : cnt_a;
     u32* nxt = (rounds & 1) ? cnt_a : cnt_b;
     const bool tr = a.trace && t0th && rounds < 64;
@@ -1981,10 +1961,10 @@ __global__ void __launch_bounds__(CL_THREADS) k_fbsp(const FbspArgs a) {
     {
       u32 cn = 0, cl = 0;
       for (u32 j = j0; j < j1; ++j) {
-        const Key<KW> m = key_load_cg<KW>(front, j);
         int found = -1;
         u16 e[NV];
-        gl_decode<KW, NV>(a.f, m, e);
+        gl_unrank<NV>(__ldcg(front + j), n, a.D, bt, a.st, e);
+        const Key<KW> m = gl_encode<KW, NV>(a.f, e);
         constexpr int NW2 = (NV + 1) / 2;
         u32 me[NW2];
 #pragma unroll
@@ -2095,12 +2075,12 @@ __global__ void __launch_bounds__(CL_THREADS) k_fbsp(const FbspArgs a) {
         if (g >= 0) {
           const long long q = (long long)bn + __popc(bm & lanemask_lt());
           const long long row = r + q;
-          const Key<KW> m = key_load_cg<KW>(front, j);
+          u16 e[NV];
+          gl_unrank<NV>(__ldcg(front + j), n, a.D, bt, a.st, e);
+          const Key<KW> m = gl_encode<KW, NV>(a.f, e);
           a.rows_basis[row] = g;
           key_store<KW>(a.rows_delta, row, key_sub<KW>(m, key_load<KW>(a.bckey, __ldg(a.boff + g))));
           a.rows_start[row] = Mcur + bl + lp - len;
-          u16 e[NV];
-          gl_decode<KW, NV>(a.f, m, e);
           bool over = false;
 #pragma unroll
           for (int v = 0; v < NV; ++v) {
@@ -2167,7 +2147,7 @@ __global__ void __launch_bounds__(CL_THREADS) k_fbsp(const FbspArgs a) {
       a.dict[w] = d | nb;
       a.newbits[w] = 0;
       return nb & ~d;
-    }, base, fnext, nullptr, 0u);
+    }, base, fnext, false, 1u);
     if (tid == 0) {
       dcount[blockIdx.x] += __ldcg(cur + blockIdx.x);
       nxt[blockIdx.x] = 0;
@@ -2189,13 +2169,27 @@ __global__ void __launch_bounds__(CL_THREADS) k_fbsp(const FbspArgs a) {
     // ---- P3: final dictionary (the map is cleared behind us)
     u32 base, tot;
     cta_bases([&](u32 b) { return __ldcg(dcount + b); }, base, tot);
+    // ranks of the final dictionary parked in the first word of each
+    // dict_out slot; the same thread turns slot i into the key below
+    u32* drank = reinterpret_cast<u32*>(a.dict_out);
     emit_chunk([&](u32 w) {
       const u32 d = __ldcg(a.dict + w);
       if (d) a.dict[w] = 0;
       return d;
-    }, base, a.dict_out, a.dict_exps, N);
+    }, base, drank, true, 2u * KW);
     grid.sync();
     stamp(387);
+    // final dictionary: keys ascending, exponents in column order (grid-stride,
+    // every thread of the grid)
+    for (u32 i = blockIdx.x * blockDim.x + tid; i < N; i += G * blockDim.x) {
+      const u32 rk = __ldcg(drank + (size_t)i * 2 * KW);
+      u16 e[NV];
+      gl_unrank<NV>(rk, n, a.D, bt, a.st, e);
+      key_store<KW>(a.dict_out, i, gl_encode<KW, NV>(a.f, e));
+#pragma unroll
+      for (int v = 0; v < NV; ++v)
+        if (v < n) a.dict_exps[((long long)N - 1 - i) * n + v] = e[v];
+    }
     // ---- P4: join: col = N - 1 - (prefix[rank >> 5] + popc(word & below))
     bool miss = false;
     term_ranges(0u, (u32)r, 0u, Mcur, [&](u32 i) { return __ldcg(a.rows_start + i); },

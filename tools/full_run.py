@@ -57,6 +57,8 @@ def main():
     ap.add_argument("--p", type=int, default=32003)
     ap.add_argument("--max-steps", type=int, default=10**6)
     ap.add_argument("--numeric", default="psge", choices=["psge", "wiedemann"])
+    ap.add_argument("--profile-step", type=int, default=-1,
+                    help="wrap that step in cudaProfilerStart/Stop (ncu --profile-from-start off)")
     args = ap.parse_args()
     from paper_2601_06765_b200.groebner import F4Config, GroebnerState, f4_step, reduce_basis_device, update_pairs
     from paper_2601_06765_b200.polynomials import poly_monic
@@ -77,7 +79,15 @@ def main():
     tot_sym = tot_num = 0.0
     while st.n_pairs() and k < args.max_steps:
         ts = time.perf_counter()
+        if k == args.profile_step:
+            import torch
+
+            torch.cuda.synchronize()
+            torch.cuda.profiler.start()
         plan, ech, _ = f4_step(st, cfg)
+        if k == args.profile_step:
+            torch.cuda.synchronize()
+            torch.cuda.profiler.stop()
         c = plan.counters
         sym = (plan.timings_ns["dict_build_ns"] + plan.timings_ns["row_assemble_ns"]) / 1e6
         num = ech.timings().get("numeric_ns", 0) / 1e6
