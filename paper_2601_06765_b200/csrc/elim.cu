@@ -766,7 +766,7 @@ __global__ void __launch_bounds__(256) k_sweep_win(Fp fp, u32 mu, const u32* __r
                                                    unsigned long long* __restrict__ stats, const SweepOut so) {
   extern __shared__ __align__(16) u32 smem[];
   constexpr int NWARP = 8;
-  constexpr int H = 2;  // 32-group spans per warp in flight
+  constexpr int H = 4;  // 32-group spans per warp in flight
   const u32 nwords = (N + 31) / 32;
   u32* abits = smem;
   u32* apre = smem + nwords;  // A columns before word w
