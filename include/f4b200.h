@@ -74,7 +74,7 @@ const char* f4b_ctx_last_error(const f4b_ctx* ctx);
  *   "dense"       0 pivot-block RREF(D') | 1 per-pivot k_dense_forward
  *   "fbsp"        0 one cooperative k_fbsp | 1 multi-launch rank pipeline
  *   "dict_sort"   1 = radix-sort dictionary for grevlex too
- *   "dict_nohash" 1 = f4b_dict_build without its duplicate filter */
+ *   "dict_lsd"    1 = f4b_dict_build sorts every key (LSD), no MSD buckets */
 int f4b_ctx_set_option(f4b_ctx* ctx, const char* name, int64_t value);
 /* Instrumentation: when enabled, every kernel launch is bracketed by CUDA
  * events on the context stream; profile_read resolves them into lines
@@ -145,6 +145,18 @@ int f4b_plan_free(f4b_plan* plan);
  * *length receives the byte count; the text is written when cap >= length
  * (call with out = NULL to size the buffer). */
 int f4b_plan_text(const f4b_plan* plan, int which, char* out, int64_t cap, int64_t* length);
+
+/* LayoutPlan.validate (symbolic.py:125-163, called by compile_batch at
+ * :383-387) on the device buffers: row_ptr tiles [0, M), rows nonempty with
+ * strictly ascending in-range columns, values nonzero (and < p), dictionary
+ * strictly descending in the ring order.  F4B_ERR_PROPERTY with the
+ * reference's message on the first violation in its check order;
+ * *violation (optional) = -1 or the encoded (kind << 40 | index). */
+int f4b_plan_validate(const f4b_plan* plan, int64_t* violation);
+
+/* fault injection for validation tests: plan row_ptr (0) / col_ind (1) /
+ * val (2) entry `index` := value (device write, synchronous). */
+int f4b_plan_poke(f4b_plan* plan, int which, int64_t index, uint32_t value);
 
 /* ---- sharded compile_batch (one rank per GPU) ----
  * The stages of compile_batch (symbolic.py:293-388) between which the caller

@@ -82,6 +82,8 @@ SIGNATURES = {
     "f4b_plan_download": (C.c_int, [C.c_void_p, i64p, i64p, u64p, u16p, i32p, u16p, i32p]),
     "f4b_plan_download_ref_keys": (C.c_int, [C.c_void_p, u64p]),
     "f4b_plan_text": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, i64p]),
+    "f4b_plan_validate": (C.c_int, [C.c_void_p, i64p]),
+    "f4b_plan_poke": (C.c_int, [C.c_void_p, C.c_int, C.c_int64, C.c_uint32]),
     "f4b_csr_transpose": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, i64p, i64p, u64p, i64p, i64p, u64p]),
     "f4b_plan_left_apply": (C.c_int, [C.c_void_p, u64p, C.c_int64, u64p]),
     "f4b_op_create": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, i64p, i64p, u64p, C.c_int, C.POINTER(C.c_void_p)]),

@@ -145,14 +145,15 @@ def microbench(kind: str, size: int, duplicate_rate: float = 0.5, seed: int = 0,
         dt = _time(torch, lambda: dict_build(kd, device=device), reps)
         nbytes = keys.nbytes + uniq.nbytes  # read every key once, write the dictionary once
         passes = -(-2 * KEY_BITS // 8)
-        # micro.cu: the duplicate filter (2^logc slots, logc = min(22, ceil
-        # log2 2n)) is kept when the distinct keys fit half of it
-        logc = min(22, max(10, int(np.ceil(np.log2(2 * size)))))
-        if len(uniq) <= 1 << (logc - 1):
-            path = "hash-filter + sort of the distinct keys"
-            streamed = keys.nbytes + 2 * (passes + 1) * uniq.nbytes + uniq.nbytes
+        # micro.cu: up to 2^24 + 2^22 keys take the MSD bucket path (read 4x:
+        # top-bit scan, histogram, scatter, bucket sort; write the packed keys
+        # once and the dictionary once); larger inputs the one-sweep LSD sort
+        if size <= (1 << 24) + (1 << 22):
+            path = "MSD buckets (one global scatter, sub-buckets sorted in shared memory)"
+            streamed = 4 * keys.nbytes + keys.nbytes + uniq.nbytes
+            passes = 1
         else:
-            path = "full sort (distinct keys overflow the filter)"
+            path = "LSD one-sweep sort of every key"
             streamed = keys.nbytes + 2 * (passes + 2) * keys.nbytes + uniq.nbytes
         out.update(
             duplicate_rate=duplicate_rate,

@@ -55,12 +55,14 @@ F4B_DEV u32 ld_volatile(const u32* p) {
 
 // Decoupled look-back for one counter per tile.  Called by ONE thread.
 // status[] zero-initialised; returns the exclusive prefix of `count`.
-F4B_DEV u32 lookback_prefix(u32* status, u32 tile, u32 count) {
-  if (tile == 0) {
-    atomicExch(status, LB_PRE | count);
-    return 0;
-  }
-  atomicExch(status + tile, LB_AGG | count);
+// lb_publish (the tile's aggregate) and lb_resolve (the wait for the
+// predecessors) may be split so the caller works in between.
+F4B_DEV void lb_publish(u32* status, u32 tile, u32 count) {
+  atomicExch(status + tile, (tile == 0 ? LB_PRE : LB_AGG) | count);
+}
+
+F4B_DEV u32 lb_resolve(u32* status, u32 tile, u32 count) {
+  if (tile == 0) return 0;
   // 4 predecessors per round trip (independent loads in flight); one not
   // yet published is polled again
   u32 excl = 0;
@@ -85,6 +87,11 @@ F4B_DEV u32 lookback_prefix(u32* status, u32 tile, u32 count) {
   __threadfence();
   atomicExch(status + tile, LB_PRE | (excl + count));
   return excl;
+}
+
+F4B_DEV u32 lookback_prefix(u32* status, u32 tile, u32 count) {
+  lb_publish(status, tile, count);
+  return lb_resolve(status, tile, count);
 }
 
 // Stable LSD radix sort of n (<= cap) keys in shared memory, low `bits` bits.

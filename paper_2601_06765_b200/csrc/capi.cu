@@ -297,7 +297,7 @@ int f4b_ctx_create(int device, uint32_t p, int n_vars, int order, f4b_alloc_fn a
     c->num_sms = sms;
     if (const char* e = getenv("F4B_DICT")) c->opt_dict_sort = !strcmp(e, "sort");
     if (const char* e = getenv("F4B_FBSP")) c->opt_fbsp = !strcmp(e, "multi");
-    if (getenv("F4B_DICT_NOHASH")) c->opt_dict_nohash = 1;
+    if (getenv("F4B_DICT_LSD")) c->opt_dict_lsd = 1;
     // Montgomery constants: p * p' = -1 mod 2^32, R^2 mod p
     uint32_t x = 1;
     for (int i = 0; i < 6; ++i) x = x * (2u - p * x);
@@ -388,7 +388,7 @@ int f4b_ctx_set_option(f4b_ctx* h, const char* name, int64_t value) {
               {"dense", &c->opt_dense, 1},
               {"fbsp", &c->opt_fbsp, 1},
               {"dict_sort", &c->opt_dict_sort, 1},
-              {"dict_nohash", &c->opt_dict_nohash, 1}};
+              {"dict_lsd", &c->opt_dict_lsd, 1}};
   for (auto& o : opts)
     if (!strcmp(o.n, name)) {
       if (value < 0 || value > o.hi) {

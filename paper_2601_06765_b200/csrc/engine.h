@@ -98,7 +98,7 @@ struct Ctx {
   int opt_dense = 0;        // "dense": 0 pivot blocks (k_dense_blk), 1 k_dense_forward
   int opt_fbsp = 0;         // "fbsp": 0 one cooperative k_fbsp, 1 multi-launch rank path
   int opt_dict_sort = 0;    // "dict_sort": 1 = radix-sort dictionary even for grevlex
-  int opt_dict_nohash = 0;  // "dict_nohash": 1 = f4b_dict_build without the duplicate filter
+  int opt_dict_lsd = 0;  // "dict_lsd": 1 = f4b_dict_build sorts every key (LSD), no MSD bucket pass
   std::string last_error;
   Basis basis;
   // pinned host scratch for round counters

@@ -12,8 +12,15 @@
 //                      unique, so sort == stable order), column counts ->
 //                      scan -> row_ptr of the transpose, values found by a
 //                      binary search in the source row.
+//   f4b_plan_validate  LayoutPlan.validate (reference symbolic.py:125-163) on
+//                      the device buffers: one pass over rows, terms and
+//                      dictionary entries; the first violation in the
+//                      reference's check order wins (atomicMin of
+//                      reason << 40 | index), so the message names the same
+//                      row the host check would.
 #include <algorithm>
 #include <cstring>
+#include <string>
 
 #include "common.cuh"
 #include "engine.h"
@@ -107,6 +114,78 @@ __global__ void k_u32_to_i64(const u32* __restrict__ in, long long n, long long*
   if (i < n) out[i] = in[i];
 }
 
+
+// violation keys, ordered like the reference's checks (symbolic.py:133-154):
+// tiling, negative segment, then per row (empty, ascending, range), zero
+// value, dictionary order; an unreduced value (>= p, never produced by a
+// compile) is reported last
+enum : unsigned long long {
+  V_TILE = 1ull << 40,
+  V_NEG = 2ull << 40,
+  V_ROW = 3ull << 40,  // | row * 4 + {0 empty, 1 ascending, 2 range}
+  V_ZERO = 4ull << 40,
+  V_DICT = 5ull << 40,
+  V_UNRED = 6ull << 40,
+};
+
+F4B_DEV long long row_of(const u32* __restrict__ rp, long long r, long long t) {
+  long long lo = 0, hi = r;  // rp[lo] <= t < rp[hi]
+  while (lo + 1 < hi) {
+    const long long mid = (lo + hi) >> 1;
+    if ((long long)rp[mid] <= t) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// key(a) > key(b) in the ring order (monomials.py:131-148 key layout):
+// grevlex (0) / deglex (1) by degree first; then grevlex by the reversed
+// complemented exponents, deglex and lex (2) by the exponents
+F4B_DEV bool mono_gt(const uint16_t* a, const uint16_t* b, int n, int order) {
+  if (order != 2) {
+    u32 da = 0, db = 0;
+    for (int v = 0; v < n; ++v) {
+      da += a[v];
+      db += b[v];
+    }
+    if (da != db) return da > db;
+  }
+  for (int l = 0; l < n; ++l) {
+    const u32 x = order == 0 ? 0xFFFFu - a[n - 1 - l] : a[l];
+    const u32 y = order == 0 ? 0xFFFFu - b[n - 1 - l] : b[l];
+    if (x != y) return x > y;
+  }
+  return false;
+}
+
+__global__ void k_validate(const u32* __restrict__ rp, long long r, const u32* __restrict__ col,
+                           const u32* __restrict__ val, long long M, long long N, u32 p,
+                           const uint16_t* __restrict__ dex, int n, int order, unsigned long long* __restrict__ flag) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long f = ~0ull;
+  if (t0 == 0 && (rp[0] != 0 || (long long)rp[r] != M)) f = V_TILE;
+  for (long long i = t0; i < r; i += stride) {
+    const u32 a = rp[i], b = rp[i + 1];
+    if (b < a) f = min(f, V_NEG | (unsigned long long)i);
+    else if (b == a) f = min(f, V_ROW | (unsigned long long)(i * 4));
+  }
+  for (long long t = t0; t < M; t += stride) {
+    const u32 c = col[t], v = val[t];
+    if (v == 0) f = min(f, V_ZERO | (unsigned long long)t);
+    else if (v >= p) f = min(f, V_UNRED | (unsigned long long)t);
+    const bool range = (long long)c >= N;
+    const bool desc = t + 1 < M && col[t + 1] <= c;
+    if (range || desc) {
+      const long long i = row_of(rp, r, t);
+      if (range) f = min(f, V_ROW | (unsigned long long)(i * 4 + 2));
+      if (desc && (long long)rp[i + 1] != t + 1) f = min(f, V_ROW | (unsigned long long)(i * 4 + 1));
+    }
+  }
+  for (long long k = t0; k + 1 < N; k += stride)
+    if (!mono_gt(dex + k * n, dex + (k + 1) * n, n, order)) f = min(f, V_DICT | (unsigned long long)k);
+  if (f != ~0ull) atomicMin(flag, f);
+}
+
 }  // namespace f4b
 
 using namespace f4b;
@@ -132,6 +211,65 @@ int f4b_plan_text(const f4b_plan* pl, int which, char* out, int64_t cap, int64_t
       }
     }
     *length = tot;
+  } catch (const Error& e) {
+    c->last_error = e.msg;
+    return e.code;
+  }
+  return F4B_OK;
+}
+
+int f4b_plan_validate(const f4b_plan* pl, int64_t* violation) {
+  if (!pl) return F4B_ERR_PRECONDITION;
+  Ctx* c = pl->ctx;
+  try {
+    DBuf fl;
+    ensure(c, fl, 8);
+    check_cuda(cudaMemsetAsync(fl.p, 0xFF, 8, c->stream), "memset");
+    const long long work = std::max({pl->r, pl->M, pl->N, 1ll});
+    const unsigned g = (unsigned)std::min<long long>(nbi(work, 256), 148ll * 8);
+    F4B_LAUNCH(c, k_validate, g, 256, 0, pl->row_ptr.as<u32>(), pl->r, pl->col_ind.as<u32>(), pl->val.as<u32>(),
+               pl->M, pl->N, c->p, pl->dict_exps.as<uint16_t>(), c->n_vars, c->order, fl.as<unsigned long long>());
+    unsigned long long f = 0;
+    check_cuda(cudaMemcpyAsync(&f, fl.p, 8, cudaMemcpyDeviceToHost, c->stream), "d2h");
+    check_cuda(cudaStreamSynchronize(c->stream), "sync");
+    release(c, fl);
+    if (violation) *violation = f == ~0ull ? -1 : (int64_t)f;
+    if (f != ~0ull) {
+      const unsigned long long kind = f >> 40, idx = f & ((1ull << 40) - 1);
+      const long long row = pl->row_lo + (long long)(idx >> 2);
+      std::string m;
+      switch (kind) {
+        case 1: m = "row_ptr does not tile the value stream"; break;
+        case 2: m = "negative row segment length"; break;
+        case 3:
+          m = (idx & 3) == 0 ? "empty row " + std::to_string(row) + " (basis members are nonzero)"
+              : (idx & 3) == 1 ? "row " + std::to_string(row) + " columns not strictly ascending"
+                               : "row " + std::to_string(row) + " column out of range";
+          break;
+        case 4: m = "zero value stored in plan"; break;
+        case 5: m = "dictionary keys not strictly descending"; break;
+        default: m = "value not reduced mod p at term " + std::to_string(idx); break;
+      }
+      fail(F4B_ERR_PROPERTY, m);
+    }
+  } catch (const Error& e) {
+    c->last_error = e.msg;
+    return e.code;
+  }
+  return F4B_OK;
+}
+
+// fault injection for the validation tests: overwrite one u32 entry of the
+// plan's row_ptr (0), col_ind (1) or val (2) on the device
+int f4b_plan_poke(f4b_plan* pl, int which, int64_t index, uint32_t value) {
+  if (!pl || which < 0 || which > 2 || index < 0) return F4B_ERR_PRECONDITION;
+  const long long len = which == 0 ? pl->r + 1 : pl->M;
+  if (index >= len) return F4B_ERR_PRECONDITION;
+  Ctx* c = pl->ctx;
+  u32* base = (which == 0 ? pl->row_ptr : which == 1 ? pl->col_ind : pl->val).as<u32>();
+  try {
+    check_cuda(cudaMemcpyAsync(base + index, &value, 4, cudaMemcpyHostToDevice, c->stream), "h2d");
+    check_cuda(cudaStreamSynchronize(c->stream), "sync");
   } catch (const Error& e) {
     c->last_error = e.msg;
     return e.code;

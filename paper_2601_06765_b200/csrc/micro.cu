@@ -2,14 +2,15 @@
 // (reference src/bench.py:244-300 `microbench`), on device-resident buffers:
 //
 //   f4b_dict_build  radix_sort + unique_sorted of W-word keys
-//                   (bulk.py:86-124, :135-150): an L2-resident hash table
-//                   drops the duplicates first (when the distinct keys fit),
-//                   the words are packed into one
-//                   order-isomorphic device key of W * key_bits bits (reference
-//                   keys are 48-bit words, bench.py:237-241), sorted with the
-//                   one-sweep LSD radix sort of radix.cu (W * key_bits / 8
-//                   passes instead of the reference's 8 W), uniqued and
-//                   unpacked back to W words.
+//                   (bulk.py:86-124, :135-150): the words are packed into
+//                   one order-isomorphic 128-bit key (reference keys are
+//                   48-bit words, bench.py:237-241); an MSD bucket pass
+//                   (one global scatter by the top varying bits, then
+//                   sub-buckets of ~1 key sorted and deduplicated in shared
+//                   memory, written in order through a decoupled look-back)
+//                   replaces the reference's 8 W LSD passes.  Skewed inputs
+//                   that overflow a bucket take the one-sweep LSD radix sort
+//                   of radix.cu (W * key_bits / 8 passes) + unique.
 //   f4b_join_index  merge_join_index (bulk.py:207-241): position of each key in
 //                   an ascending dictionary, MissingKeyError on a miss.
 //   f4b_mod_fma     acc + a b mod p, the KernelArith lazy multiply-add
@@ -68,96 +69,260 @@ __global__ void __launch_bounds__(MB_THREADS) k_mb_unpack(const u64* __restrict_
   }
 }
 
-// Duplicate filter in front of the sort (dict_build): every key is inserted
-// into an open-addressing table of packed 128-bit keys small enough to stay
-// in L2 (<= 64 MB); the first inserter of a key appends it to a compact list,
-// so only the distinct keys go through the radix sort.  Keys are packed on the
-// fly (no separate pack pass).  More distinct keys than `limit` -> overflow
-// flag, the caller falls back to sorting every key.
-static constexpr int HB_LOG_MAX = 22;  // 64 MB table: L2 resident (2^25 measured: 16M keys at 50% duplicates 3.9 -> 3.4 ms, at 99% 0.46 -> 0.73 ms)
+// MSD bucket path of dict_build (no hash table: the reference spec rejects
+// atomic hash tables; the result is the sorted unique run
+// whatever order keys land in a bucket):
+//   k_msd_diff    OR of (key XOR key[0]) -> the highest bit where keys differ
+//                 (`top`); bits above it are common and carry no order
+//   k_msd_hist    bucket sizes of the D1-bit digit just below top
+//                 (shared-memory histograms summed into global counts)
+//   scan          -> bucket starts
+//   k_msd_scatter packed 128-bit keys appended to their buckets (one global
+//                 cursor per bucket)
+//   k_msd_bucket  one CTA per bucket: keys to registers, scattered in shared
+//                 memory by the next D2 bits into sub-buckets of ~1 key,
+//                 first occurrences found and ranked inside their
+//                 sub-bucket, written back sorted to the front of the
+//                 bucket's range; distinct count per bucket
+//   scan          -> output offsets (a decoupled look-back chaining the
+//                 buckets was measured 30 % of the bucket kernel in barrier
+//                 waits: a bucket's predecessor is still sorting)
+//   k_msd_compact one warp per bucket: distinct keys unpacked to W words
+// A bucket above MSD_CAP keys or a sub-bucket above MSD_SUBLEN keys sets err
+// bit 2 and the caller sorts every key with the LSD path instead (skewed
+// inputs: only the speed changes).
 using u128 = unsigned __int128;
+static constexpr int MSD_THREADS = 512;
+static constexpr int MSD_BT = 256;       // k_msd_bucket: 4 CTAs per SM
+static constexpr int MSD_CAP = 2048;     // keys per bucket in shared memory (~512 expected)
+static constexpr int MSD_D2 = 11;        // sub-bucket digit bits (2048 sub-buckets)
+static constexpr int MSD_SUBLEN = 1024;  // keys per sub-bucket (~1 expected)
 
-F4B_DEV u32 mb_hash(u64 hi, u64 lo, int logc) {
-  const u64 h = (lo * 0x9E3779B97F4A7C15ull) ^ (hi * 0xC2B2AE3D27D4EB4Full) ^ (lo >> 29);
-  return (u32)((h * 0xBF58476D1CE4E5B9ull) >> (64 - logc));
+F4B_DEV u128 msd_pack(const u64* __restrict__ in, long long i, int words, int kb, u64 lim, bool& bad) {
+  if (words == 2) {
+    const ulonglong2 v = __ldcs(reinterpret_cast<const ulonglong2*>(in) + i);
+    bad |= (v.x > lim) | (v.y > lim);
+    return ((u128)v.x << kb) | (u128)v.y;
+  }
+  const u64 w = __ldcs(in + i);
+  bad |= w > lim;
+  return (u128)w;
 }
 
-__global__ void __launch_bounds__(MB_THREADS) k_mb_hash_insert(const u64* __restrict__ in, long long n, int words,
-                                                               int kb, u128* __restrict__ table, int logc, u32 limit,
-                                                               u64* __restrict__ uniq, u32* __restrict__ d_count,
-                                                               u32* __restrict__ err) {
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  const u64 lim = kb >= 64 ? ~0ull : ((1ull << kb) - 1);  // W = 2 implies kb < 64 here
-  const u32 mask = (1u << logc) - 1;
-  const u128 EMPTY = ~(u128)0;
-  const int lane = threadIdx.x & 31;
+F4B_DEV int msd_top(const u64* diff) {  // bits below and including the highest differing bit
+  return diff[0] ? 128 - __clzll((long long)diff[0]) : (diff[1] ? 64 - __clzll((long long)diff[1]) : 0);
+}
+
+__global__ void __launch_bounds__(MB_THREADS) k_msd_diff(const u64* __restrict__ in, long long n, int words, int kb,
+                                                         u64* __restrict__ diff, u32* __restrict__ err) {
+  const u64 lim = kb >= 64 ? ~0ull : ((1ull << kb) - 1);
   bool bad = false;
-  const long long n_round = (n + 31) / 32 * 32;  // whole warps iterate together (ballots)
-  constexpr int HB_ITEMS = 4;  // keys per thread per iteration: four table probes in flight (8: 98 registers, 168 -> 245 us)
-  for (long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; i0 < n_round; i0 += HB_ITEMS * stride) {
-    // overflow: the caller sorts everything (warp-uniform exit: ballots below)
-    if (__shfl_sync(0xffffffffu, lane == 0 ? ld_volatile(err) : 0u, 0) & 2u) break;
-    u64 hi[HB_ITEMS], lo[HB_ITEMS];
-    u32 h[HB_ITEMS];
-    ulonglong2 cur[HB_ITEMS];
+  const u128 k0 = msd_pack(in, 0, words, kb, lim, bad);
+  u128 acc = 0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    acc |= msd_pack(in, i, words, kb, lim, bad) ^ k0;
+  u64 hi = (u64)(acc >> 64), lo = (u64)acc;
 #pragma unroll
-    for (int k = 0; k < HB_ITEMS; ++k) {
-      const long long i = i0 + k * stride;
-      hi[k] = 0;
-      lo[k] = 0;
-      if (i < n) {
-        if (words == 2) {
-          const ulonglong2 v = __ldcs(reinterpret_cast<const ulonglong2*>(in) + i);
-          bad |= (v.x > lim) | (v.y > lim);
-          lo[k] = v.y | (v.x << kb);
-          hi[k] = v.x >> (64 - kb);
-        } else {
-          lo[k] = __ldcs(in + i);
-          bad |= lo[k] > lim;
-        }
-      }
-    }
+  for (int o = 16; o; o >>= 1) {
+    hi |= __shfl_xor_sync(0xffffffffu, hi, o);
+    lo |= __shfl_xor_sync(0xffffffffu, lo, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (hi) atomicOr(reinterpret_cast<unsigned long long*>(diff), (unsigned long long)hi);
+    if (lo) atomicOr(reinterpret_cast<unsigned long long*>(diff) + 1, (unsigned long long)lo);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(err, 1u);
+}
+
+F4B_DEV u32 msd_digit(u128 v, int shift, int bits) { return (u32)(v >> shift) & ((1u << bits) - 1u); }
+
+// bucket sizes: shared-memory histogram per CTA, summed into C[nb]
+__global__ void __launch_bounds__(MSD_THREADS) k_msd_hist(const u64* __restrict__ in, long long n, int words, int kb,
+                                                          int d1, const u64* __restrict__ diff, u32* __restrict__ C) {
+  extern __shared__ u32 h[];
+  const int nb = 1 << d1;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const int s1 = max(msd_top(diff) - d1, 0);
+  bool bad = false;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    atomicAdd(h + msd_digit(msd_pack(in, i, words, kb, ~0ull, bad), s1, d1), 1u);
+  __syncthreads();
+  for (int d = threadIdx.x; d < nb; d += blockDim.x)
+    if (h[d]) atomicAdd(C + d, h[d]);
+}
+
+// keys appended to their bucket through one global cursor per bucket: all
+// CTAs extend the same bucket tails at the same time, so the 16-byte stores
+// fill whole sectors while they are L2-resident (per-CTA ranges were measured
+// 2.7x DRAM read amplification from partial-sector write-backs)
+__global__ void __launch_bounds__(MSD_THREADS) k_msd_scatter(const u64* __restrict__ in, long long n, int words,
+                                                             int kb, int d1, const u64* __restrict__ diff,
+                                                             u32* __restrict__ cur, u128* __restrict__ out) {
+  const int s1 = max(msd_top(diff) - d1, 0);
+  bool bad = false;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  // four keys per thread per iteration: loads and cursor atomics in flight
+  for (long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += 4 * stride) {
+    u128 v[4];
+    u32 o[4];
 #pragma unroll
-    for (int k = 0; k < HB_ITEMS; ++k) {
-      h[k] = mb_hash(hi[k], lo[k], logc);
-      if (i0 + k * stride < n) cur[k] = __ldcg(reinterpret_cast<const ulonglong2*>(table) + h[k]);
-    }
+    for (int k = 0; k < 4; ++k)
+      if (i0 + k * stride < n) v[k] = msd_pack(in, i0 + k * stride, words, kb, ~0ull, bad);
 #pragma unroll
-    for (int k = 0; k < HB_ITEMS; ++k) {
-      bool ins = false;
-      if (i0 + k * stride < n) {
-        const u128 key = ((u128)hi[k] << 64) | lo[k];
-        u32 hh = h[k];
-        u128 c = ((u128)cur[k].y << 64) | cur[k].x;
-        for (;;) {
-          if (c == key) break;
-          if (c == EMPTY) {
-            const u128 old = atomicCAS(table + hh, EMPTY, key);
-            if (old == EMPTY) {
-              ins = true;
-              break;
-            }
-            if (old == key) break;
-          }
-          hh = (hh + 1) & mask;
-          const ulonglong2 c2 = __ldcg(reinterpret_cast<const ulonglong2*>(table) + hh);
-          c = ((u128)c2.y << 64) | c2.x;
-        }
-      }
-      const unsigned m = __ballot_sync(0xffffffffu, ins);
-      if (m) {
-        u32 base = 0;
-        if (lane == __ffs(m) - 1) base = atomicAdd(d_count, (u32)__popc(m));
-        base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
-        if (ins) {
-          const u32 o = base + __popc(m & lanemask_lt());
-          if (o < limit) reinterpret_cast<ulonglong2*>(uniq)[o] = make_ulonglong2(hi[k], lo[k]);
-        }
-        if (lane == 0 && base + __popc(m) > limit) atomicOr(err, 2u);
-      }
+    for (int k = 0; k < 4; ++k)
+      if (i0 + k * stride < n) o[k] = atomicAdd(cur + msd_digit(v[k], s1, d1), 1u);
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (i0 + k * stride < n) out[o[k]] = v[k];
+  }
+}
+
+// One bucket per CTA:
+//   keys -> registers, sub-bucket histogram, scan, scatter into B (shared);
+//   phase 1: a key is the first occurrence of its value when no earlier key
+//            of its sub-bucket equals it (copies stop at the first compare);
+//   phase 2: a first occurrence's rank = number of first occurrences of its
+//            sub-bucket below it -> output slot.
+// Work per sub-bucket is O(len * distinct); a sub-bucket above MSD_SUBLEN
+// keys or a bucket above MSD_CAP keys flags the LSD fallback.
+__global__ void __launch_bounds__(MSD_BT, 4) k_msd_bucket(u128* __restrict__ keys, const u32* __restrict__ O, int d1,
+                                                          const u64* __restrict__ diff, u32* __restrict__ Dc,
+                                                          u32* __restrict__ err) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int NS = 1 << MSD_D2, PER = NS / MSD_BT, KPT = MSD_CAP / MSD_BT;
+  u128* B = reinterpret_cast<u128*>(smem);
+  u32* C = reinterpret_cast<u32*>(B + MSD_CAP);  // [NS] counts -> cursors -> sub-bucket ends
+  u32* D = C + NS;                               // [NS] distinct counts -> output offsets
+  u32* F = D + NS;                               // [MSD_CAP / 32] first-occurrence bits
+  __shared__ u32 ws[33];
+  __shared__ u32 s_bad;
+  if (threadIdx.x == 0) s_bad = 0;
+  for (int j = threadIdx.x; j < NS; j += blockDim.x) C[j] = D[j] = 0;
+  for (int j = threadIdx.x; j < MSD_CAP / 32; j += blockDim.x) F[j] = 0;
+  __syncthreads();
+  const u32 tile = blockIdx.x;
+  const u32 base = O[tile], size = O[tile + 1] - base;
+  const bool over = size > (u32)MSD_CAP;
+  const int s1 = max(msd_top(diff) - d1, 0), s2 = max(s1 - MSD_D2, 0);
+  u128 v[KPT];
+  u32 dg[KPT], pos[KPT];
+#pragma unroll
+  for (int k = 0; k < KPT; ++k) {
+    const u32 i = threadIdx.x + k * MSD_BT;
+    dg[k] = NS;
+    if (!over && i < size) {
+      v[k] = keys[base + i];
+      dg[k] = msd_digit(v[k], s2, MSD_D2);
     }
   }
-  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(err, 1u);
+#pragma unroll
+  for (int k = 0; k < KPT; ++k)
+    if (dg[k] < NS) atomicAdd(C + dg[k], 1u);
+  __syncthreads();
+  u32 loc[PER], sum = 0;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    loc[q] = C[threadIdx.x * PER + q];
+    sum += loc[q];
+    if (loc[q] > (u32)MSD_SUBLEN) s_bad = 1;
+  }
+  u32 tot;
+  u32 run = block_scan_excl(sum, ws, &tot);
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    C[threadIdx.x * PER + q] = run;
+    run += loc[q];
+  }
+  __syncthreads();
+  const bool bad = over || s_bad;
+  if (!bad) {
+#pragma unroll
+    for (int k = 0; k < KPT; ++k)
+      if (dg[k] < NS) {
+        pos[k] = atomicAdd(C + dg[k], 1u);
+        B[pos[k]] = v[k];
+      }
+  }
+  __syncthreads();  // C[j] = end of sub-bucket j = start of j + 1
+  u32 first = 0;
+  if (!bad) {
+#pragma unroll
+    for (int k = 0; k < KPT; ++k)
+      if (dg[k] < NS) {
+        const u32 st = dg[k] ? C[dg[k] - 1] : 0u;
+        const u128 x = B[pos[k]];  // keys are re-read from shared memory: registers stay < 64
+        bool f = true;
+        for (u32 u = st; u < pos[k]; ++u)
+          if (B[u] == x) {
+            f = false;
+            break;
+          }
+        if (f) {
+          first |= 1u << k;
+          atomicAdd(D + dg[k], 1u);
+          atomicOr(F + (pos[k] >> 5), 1u << (pos[k] & 31));
+        }
+      }
+  }
+  __syncthreads();
+  sum = 0;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    loc[q] = D[threadIdx.x * PER + q];
+    sum += loc[q];
+  }
+  u32 dtot;
+  run = block_scan_excl(sum, ws, &dtot);
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    D[threadIdx.x * PER + q] = run;
+    run += loc[q];
+  }
+  if (threadIdx.x == 0) {
+    if (bad) atomicOr(err, 2u);
+    Dc[tile] = bad ? 0u : dtot;
+  }
+  __syncthreads();
+  if (bad) return;
+  // first occurrences, ranked, overwrite the front of the bucket's own range
+  // (the keys are all in shared memory by now)
+  u128 ranked[KPT];
+  u32 loff[KPT];
+#pragma unroll
+  for (int k = 0; k < KPT; ++k)
+    if (first & (1u << k)) {
+      const u32 st = dg[k] ? C[dg[k] - 1] : 0u, en = C[dg[k]];
+      const u128 x = B[pos[k]];
+      u32 rank = 0;
+      for (u32 u = st; u < en; ++u) rank += ((F[u >> 5] >> (u & 31)) & 1u) && B[u] < x;
+      loff[k] = D[dg[k]] + rank;
+      ranked[k] = x;
+    }
+  __syncthreads();  // every key of the bucket read (registers / shared) before the overwrite
+#pragma unroll
+  for (int k = 0; k < KPT; ++k)
+    if (first & (1u << k)) keys[base + loff[k]] = ranked[k];
+}
+
+// distinct keys of bucket b (front of its range) -> out[Doff[b] ...],
+// unpacked to W words; one warp per bucket
+__global__ void __launch_bounds__(MB_THREADS) k_msd_compact(const u128* __restrict__ keys, const u32* __restrict__ O,
+                                                            const u32* __restrict__ Dc, const u32* __restrict__ Doff,
+                                                            int nb, int words, int kb, u64* __restrict__ out) {
+  const int b = (int)(((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  if (b >= nb) return;
+  const u32 base = O[b], cnt = Dc[b], o = Doff[b];
+  const u64 lim = kb >= 64 ? ~0ull : ((1ull << kb) - 1);
+  for (u32 i = lane; i < cnt; i += 32) {
+    const u128 x = keys[base + i];
+    if (words == 2)
+      reinterpret_cast<ulonglong2*>(out)[o + i] = make_ulonglong2((u64)(x >> kb), (u64)x & lim);
+    else
+      out[o + i] = (u64)x;
+  }
 }
 
 // Lower bound of each query in an ascending W-word dictionary.  Queries of a
@@ -231,66 +396,60 @@ long long dict_build(Ctx* c, const uint64_t* keys, long long n, int words, int k
     fail(F4B_ERR_PRECONDITION, "dict_build: 0 <= n < 2^32 - 2, words in {1, 2}, 1 <= key_bits <= 64");
   if (n == 0) return 0;
   DBuf packed, uniq, flags;
-  ensure(c, flags, 16);
+  ensure(c, flags, 32);
   u32* err = flags.as<u32>();
   u32* d_count = err + 1;
-  u32* d_hcount = err + 2;
-  memset_async(c, err, 0, 12);
-  // duplicate filter first (distinct keys expected <= half the L2-sized
-  // table); packed keys with all 128 bits significant would collide with the
-  // empty-slot marker, so they always take the full sort
-  bool filtered = false;
-  if (!c->opt_dict_nohash && words * key_bits < 128) {
-    int logc = 10;
-    while (logc < HB_LOG_MAX && (1ll << logc) < 2 * n) ++logc;
-    const u32 limit = 1u << (logc - 1);
-    DBuf table;
-    ensure(c, table, (size_t)16 << logc);
-    ensure(c, packed, (size_t)limit * 16);
-    memset_async(c, table.p, 0xFF, (size_t)16 << logc);
-    // a leading sample first: if its distinct count extrapolates (uniform
-    // picks from a pool of P keys: d = P (1 - e^{-S/P})) to more distinct keys
-    // than the table takes, skip the filter instead of running into the
-    // overflow (measured 0.27 ms wasted at 16M keys / 50 % duplicates).  Only
-    // the speed depends on this guess; the result never does.
-    const long long S = std::min<long long>(n, 1ll << 18);
-    F4B_LAUNCH(c, k_mb_hash_insert, mb_grid(c, S), MB_THREADS, 0, keys, S, words, key_bits, table.as<u128>(), logc,
-               limit, packed.as<u64>(), d_hcount, err);
-    bool give_up = false;
-    if (S < n) {
-      const double d = (double)read_u32(c, d_hcount);
-      double P = 1e18;  // all distinct: unbounded pool
-      if (d < (double)S) {  // solve P (1 - exp(-S/P)) = d by bisection on log P
-        double lo = std::log(std::max(d, 1.0)), hi = std::log(1e18);
-        for (int it = 0; it < 80; ++it) {
-          const double mid = 0.5 * (lo + hi), Pm = std::exp(mid);
-          if (Pm * -std::expm1(-(double)S / Pm) < d) lo = mid; else hi = mid;
-        }
-        P = std::exp(0.5 * (lo + hi));
-      }
-      const double n_est = P * -std::expm1(-(double)n / P);
-      give_up = n_est > 0.9 * (double)limit;
-      if (!give_up)
-        F4B_LAUNCH(c, k_mb_hash_insert, mb_grid(c, n - S), MB_THREADS, 0, keys + (size_t)S * words, n - S, words,
-                   key_bits, table.as<u128>(), logc, limit, packed.as<u64>(), d_hcount, err);
-    }
-    const u32 e = read_u32(c, err) | (give_up ? 2u : 0u);
-    release(c, table);
+  memset_async(c, err, 0, 32);
+  // MSD bucket path (see above); D1 puts ~1K keys in a bucket
+  bool done = false;
+  if (!c->opt_dict_lsd && n <= (1ll << 24) + (1ll << 22)) {
+    int d1 = 0;  // ~512 keys per bucket: 100 copies of ~5 distinct keys still fit MSD_CAP
+    while (d1 < 15 && ((long long)512 << d1) < n) ++d1;
+    const int nb = 1 << d1;
+    const int G = std::max(1, std::min(c->num_sms * 2, (int)((n + 4095) / 4096)));
+    DBuf H, O, st;
+    ensure(c, H, (size_t)nb * 4 + 4);
+    ensure(c, O, (size_t)(nb + 1) * 4);
+    ensure(c, st, (size_t)nb * 4 + 8);
+    ensure(c, packed, (size_t)n * 16);
+    u64* diff = reinterpret_cast<u64*>(err + 4);  // 16-byte aligned: err + 4 .. + 7
+    memset_async(c, st.p, 0, (size_t)nb * 4 + 8);
+    memset_async(c, H.p, 0, (size_t)nb * 4 + 4);
+    F4B_LAUNCH(c, k_msd_diff, mb_grid(c, n), MB_THREADS, 0, keys, n, words, key_bits, diff, err);
+    const size_t hs = (size_t)nb * 4;
+    check_cuda(cudaFuncSetAttribute(k_msd_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hs), "smem");
+    F4B_LAUNCH(c, k_msd_hist, G, MSD_THREADS, hs, keys, n, words, key_bits, d1, diff, H.as<u32>());
+    exclusive_scan_u32(c, H.as<u32>(), O.as<u32>(), (long long)nb);
+    check_cuda(cudaMemcpyAsync(H.p, O.p, (size_t)nb * 4, cudaMemcpyDeviceToDevice, c->stream), "d2d");
+    F4B_LAUNCH(c, k_msd_scatter, mb_grid(c, n), MB_THREADS, 0, keys, n, words, key_bits, d1, diff, H.as<u32>(),
+               packed.as<u128>());
+    const size_t bs = (size_t)MSD_CAP * 16 + (size_t)(2 << MSD_D2) * 4 + MSD_CAP / 8;
+    check_cuda(cudaFuncSetAttribute(k_msd_bucket, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bs), "smem");
+    u32* Dc = st.as<u32>();  // [nb + 1] distinct per bucket -> (H) offsets
+    F4B_LAUNCH(c, k_msd_bucket, nb, MSD_BT, bs, packed.as<u128>(), O.as<u32>(), d1, diff, Dc, err);
+    exclusive_scan_u32(c, Dc, H.as<u32>(), (long long)nb);
+    F4B_LAUNCH(c, k_msd_compact, (unsigned)((nb * 32ll + MB_THREADS - 1) / MB_THREADS), MB_THREADS, 0,
+               packed.as<u128>(), O.as<u32>(), Dc, H.as<u32>(), nb, words, key_bits, out);
+    check_cuda(cudaMemcpyAsync(d_count, H.as<u32>() + nb, 4, cudaMemcpyDeviceToDevice, c->stream), "d2d");
+    const u32 e = read_u32(c, err);
+    release(c, H);
+    release(c, O);
+    release(c, st);
     if (e & 1u) {
       release(c, packed);
       release(c, flags);
       fail(F4B_ERR_PRECONDITION, "dict_build: a key word has more than key_bits significant bits");
     }
-    if (!(e & 2u)) {
-      const u32 nd = read_u32(c, d_hcount);
-      ensure(c, uniq, (size_t)(nd + 1) * 16);
-      sort_unique(c, 2, packed.as<u64>(), nullptr, nd, words * key_bits, nullptr, nullptr, uniq.as<u64>(), d_count);
-      filtered = true;
-    } else {
-      memset_async(c, err, 0, 12);
-    }
+    done = !(e & 2u);
+    if (!done) memset_async(c, err, 0, 8);
   }
-  if (!filtered) {
+  if (done) {
+    const long long nu = read_u32(c, d_count);
+    release(c, packed);
+    release(c, flags);
+    return nu;
+  }
+  {
     ensure(c, packed, (size_t)n * 16);
     ensure(c, uniq, (size_t)(n + 1) * 16);
     F4B_LAUNCH(c, k_mb_pack, mb_grid(c, n), MB_THREADS, 0, keys, n, words, key_bits, packed.as<u64>(), err);

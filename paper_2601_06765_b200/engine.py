@@ -74,6 +74,16 @@ class DevicePlan:
                                   "plan keys")
         return out
 
+    def validate(self):
+        """LayoutPlan.validate (reference symbolic.py:125-163) on the device
+        buffers (f4b_plan_validate); PropertyViolationError on failure."""
+        self.engine.ctx.check(self.engine.lib.f4b_plan_validate(self.h, None), "validate")
+
+    def poke(self, which: str, index: int, value: int):
+        """Fault injection for tests: overwrite one device entry."""
+        code = {"row_ptr": 0, "col_ind": 1, "val": 2}[which]
+        self.engine.ctx.check(self.engine.lib.f4b_plan_poke(self.h, code, index, value), "poke")
+
     _TEXT = {"row_ptr": 0, "col_ind": 1, "val": 2, "dict_keys": 3}
 
     def text(self, which: str) -> bytes:
@@ -254,7 +264,7 @@ class Engine:
     # -- path selection (f4b_ctx_set_option) ---------------------------------
     def set_option(self, name: str, value: int):
         """Force a fallback path ("sweep", "dense", "fbsp", "dict_sort",
-        "dict_nohash"; 0 = the automatic choice).  Every setting computes the
+        "dict_lsd"; 0 = the automatic choice).  Every setting computes the
         same bytes; the tests use this to reach every kernel."""
         self.ctx.check(self.lib.f4b_ctx_set_option(self.ctx.h, name.encode(), int(value)), f"set_option {name}")
 

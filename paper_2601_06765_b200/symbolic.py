@@ -143,8 +143,19 @@ class LayoutPlan:
         return self.counters.N if self.device is not None else len(self.dict_keys)
 
     def validate(self):
-        """Structural invariants (reference :125-163); PropertyViolationError."""
+        """Structural invariants (reference :125-163); PropertyViolationError.
+
+        A device plan is checked where it lives (f4b_plan_validate: one
+        kernel over rows, terms and dictionary entries); the counters on
+        the host.
+        """
         c = self.counters
+        if self.device is not None:
+            self.device.validate()
+            if not (c.r == self.device.info["r"] and c.N == self.device.info["N"] and c.M == self.device.info["M"]
+                    and c.nnz == c.M and c.keys_emitted == c.M and c.keys_generated_total >= c.M):
+                raise PropertyViolationError(f"counters inconsistent: {c}")
+            return
         rp, ci, va, dk = self.row_ptr, self.col_ind, self.val, self.dict_keys
         if not (rp[0] == 0 and rp[-1] == len(ci) == len(va)):
             raise PropertyViolationError("row_ptr does not tile the value stream")
@@ -163,8 +174,10 @@ class LayoutPlan:
             if bad.any():
                 row = int(np.searchsorted(rp, np.flatnonzero(bad)[0] + 1, side="right") - 1)
                 raise PropertyViolationError(f"row {row} columns not strictly ascending")
-            if ci.min() < 0 or ci.max() >= len(dk):
-                raise PropertyViolationError("column out of range")
+            oob = (ci < 0) | (ci >= len(dk))
+            if oob.any():
+                row = int(np.searchsorted(rp, np.flatnonzero(oob)[0], side="right") - 1)
+                raise PropertyViolationError(f"row {row} column out of range")
         if len(va) and (va == 0).any():
             raise PropertyViolationError("zero value stored in plan")
         if len(dk) > 1 and not (key_cmp_rows(dk[:-1], dk[1:]) == 1).all():
@@ -246,7 +259,9 @@ def compile_batch(rows, basis: SoaPolySet, closure: Closure = Closure.ONE_STEP_R
     counters = PlanCounters(r=info["r"], N=info["N"], M=M, nnz=M, closure_rounds=info["closure_rounds"],
                             keys_emitted=M, keys_generated_total=M)
     timings = {"dict_build_ns": info["dict_build_ns"], "row_assemble_ns": info["row_assemble_ns"]}
-    return LayoutPlan(ring, counters=counters, timings_ns=timings, device=dev, input_rows=rows)
+    plan = LayoutPlan(ring, counters=counters, timings_ns=timings, device=dev, input_rows=rows)
+    plan.validate()  # reference :383-387, on the device
+    return plan
 
 
 def closure_expand(dict_keys_desc: np.ndarray, basis: SoaPolySet, done=None, candidates=None,

@@ -694,6 +694,61 @@ def test_plan_text_streamed_from_device(cuda):
     assert hashlib.sha256(dev_text.encode()).hexdigest() == gold["steps"][19]["plan_sha256"]
 
 
+@pytest.mark.parametrize("which,fault", [
+    ("none", None),
+    ("col_desc", "columns not strictly ascending"),
+    ("col_range", "column out of range"),
+    ("val_zero", "zero value stored in plan"),
+    ("row_empty", "(basis members are nonzero)"),
+    ("row_tile", "row_ptr does not tile the value stream"),
+])
+def test_device_validate_matches_host(cuda, which, fault):
+    """compile_batch validates device plans on the device (f4b_plan_validate,
+    reference symbolic.py:125-163 / :383-387); an injected fault raises the
+    same PropertyViolationError message the host check gives on the same
+    (downloaded, equally corrupted) arrays."""
+    from paper_2601_06765_b200.symbolic import LayoutPlan
+
+    snaps = load_snapshots("cyclic8_p32003")
+    ring, st = state_from_snapshot(snaps[10])
+    spec, _ = select_batch(st)
+    soa = st.soa()
+    plan = compile_batch(select_rows(spec, soa), soa, Closure.ONE_STEP_REDUCTION)  # validated inside
+    rp, ci, va = plan.row_ptr.copy(), plan.col_ind.copy(), plan.val.copy()
+    r, N = plan.n_rows, plan.n_cols
+    i = r // 3  # a row in the middle, > 1 term
+    while rp[i + 1] - rp[i] < 2:
+        i += 1
+    a = int(rp[i])
+    if which == "col_desc":
+        plan.device.poke("col_ind", a + 1, int(ci[a]))
+        ci[a + 1] = ci[a]
+    elif which == "col_range":
+        last = int(rp[i + 1]) - 1
+        plan.device.poke("col_ind", last, N)
+        ci[last] = N
+    elif which == "val_zero":
+        plan.device.poke("val", a + 1, 0)
+        va[a + 1] = 0
+    elif which == "row_empty":
+        plan.device.poke("row_ptr", i + 1, a)
+        rp[i + 1] = a
+    elif which == "row_tile":
+        plan.device.poke("row_ptr", r, int(rp[r]) - 1)
+        rp[r] -= 1
+    host = LayoutPlan(ring, rp, ci, va, plan.dict_keys, plan.row_meta, plan.counters)
+    if fault is None:
+        plan.validate()
+        host.validate()
+        return
+    with pytest.raises(errors.PropertyViolationError) as dev_err:
+        plan.validate()
+    with pytest.raises(errors.PropertyViolationError) as host_err:
+        host.validate()
+    assert fault in str(dev_err.value)
+    assert str(host_err.value) in str(dev_err.value)
+
+
 def test_snapshot_resume_gpu(cuda, tmp_path):
     """A binary state snapshot taken mid-run (snapshot.py) resumes the GPU F4
     loop to the reference's final reduced basis (cyclic-6)."""
