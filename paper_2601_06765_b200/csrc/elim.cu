@@ -595,128 +595,37 @@ __global__ void __launch_bounds__(256) k_sweep_blk(Fp fp, u32 mu, const u32* __r
 // non-empty window.  The multipliers equal the column-by-column sweep's, so
 // D' is bit-identical with k_sweep<0> / k_sweep_blk.
 // ---------------------------------------------------------------------------
-static constexpr int WB_WARPS = 4;
-__global__ void __launch_bounds__(32 * WB_WARPS) k_win_build(Fp fp, const u32* __restrict__ col,
-                                                             const u32* __restrict__ val, u32 N,
-                                                             const uint4* __restrict__ desc,
-                                                             const u32* __restrict__ abits,
-                                                             const u32* __restrict__ acols,
-                                                             const u32* __restrict__ apos, u32 nA, u32 nwin,
-                                                             u32* __restrict__ winW, u32* __restrict__ winC,
-                                                             uint2* __restrict__ winD, u32* __restrict__ gcursor) {
-  __shared__ u32 sT[WB_WARPS][32][33];  // T[r][t] (Montgomery): pivot r's entry at window column t (r < t)
-  __shared__ u32 sC[WB_WARPS][32];      // window columns
-  __shared__ u32 sA[WB_WARPS][32][33];  // sA[u][s]: lane s's working vector
-  __shared__ u32 sM[WB_WARPS][32];      // nonzero pattern of T's row r
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const u32 j = blockIdx.x * WB_WARPS + warp;
-  if (j >= nwin) return;
-  const unsigned FULL = 0xffffffffu;
-  const u32 base = j * 32;
-  const u32 nw = min(32u, nA - base);
-  const u32 cw = (u32)lane < nw ? __ldg(acols + base + lane) : N;
-  const uint4 d = (u32)lane < nw ? __ldg(desc + cw) : make_uint4(0, 0, 1, NONE);
-  winC[base + lane] = cw;
-  {
-    // packed-tail slots: ceil(len / 4) groups of 4 entries per pivot, the
-    // window's groups reserved with one atomicAdd (any placement works: the
-    // sweep only follows winD)
-    const u32 ng = (d.y - d.x + 3) >> 2;
-    u32 x = ng;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const u32 y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    u32 gb = 0;
-    if (lane == 31) gb = atomicAdd(gcursor, x);
-    gb = __shfl_sync(0xffffffffu, gb, 31);
-    winD[base + lane] = make_uint2(gb + x - ng, gb + x);
-  }
-  sC[warp][lane] = cw;
-  const u32 clast = __shfl_sync(FULL, cw, nw - 1);
-  for (int r = 0; r < 32; ++r) sT[warp][r][lane] = 0;
-  sM[warp][lane] = 0;
-  __syncwarp();
-  auto place = [&](u32 r, u32 cc, u32 v) {
-    if (cc <= clast && ((abits[cc >> 5] >> (cc & 31)) & 1u)) {
-      u32 lo = 0, hi = 32;  // position of cc among the window columns
-      while (lo + 1 < hi) {
-        const u32 mid = (lo + hi) >> 1;
-        if (sC[warp][mid] <= cc) lo = mid; else hi = mid;
-      }
-      sT[warp][r][lo] = fp.to_mont(v);
-      atomicOr(&sM[warp][r], 1u << lo);
-    }
-  };
-  // in-window entries: the first 32 tail entries of 8 pivots per round (all
-  // loads in flight), the rare longer in-window prefix continued afterwards
-  for (u32 r0 = 0; r0 < nw; r0 += 8) {
-    u32 cc[8], vv[8];
-#pragma unroll
-    for (int h = 0; h < 8; ++h) {
-      const u32 r = r0 + h;
-      const u32 x = __shfl_sync(FULL, d.x, r & 31), y = __shfl_sync(FULL, d.y, r & 31);
-      const u32 k = x + lane;
-      const bool ok = r < nw && k < y;
-      cc[h] = ok ? __ldg(col + k) : 0xFFFFFFFFu;
-      vv[h] = ok ? __ldg(val + k) : 0u;
-    }
-#pragma unroll
-    for (int h = 0; h < 8; ++h) {
-      const u32 r = r0 + h;
-      place(r, cc[h], vv[h]);
-      if (r < nw && __shfl_sync(FULL, cc[h], 31) <= clast) {
-        const u32 x = __shfl_sync(FULL, d.x, r), y = __shfl_sync(FULL, d.y, r);
-        for (u32 k0 = x + 32; k0 < y; k0 += 32) {
-          const u32 k = k0 + lane;
-          const u32 c2 = k < y ? __ldg(col + k) : 0xFFFFFFFFu;
-          place(r, c2, k < y ? __ldg(val + k) : 0u);
-          if (__shfl_sync(FULL, c2, 31) > clast) break;
-        }
-      }
-    }
-  }
-  __syncwarp();
-  // lane s solves x T = e_s right-looking (Montgomery domain), its vector in
-  // shared memory (sA[u][s], conflict free; a rolled loop keeps the code in
-  // the instruction cache): x_t = a_t / lead_t, then a_u -= x_t T[t][u]
-  const u32 ilm_l = fp.to_mont(d.z);
-  const u32 one_m = fp.to_mont(1u);
-  for (int u = 0; u < 32; ++u) sA[warp][u][lane] = lane == u ? one_m : 0u;
-  __syncwarp();
-  for (int t = 0; t < 32; ++t) {
-    const u32 xt = fp.mont_mul(sA[warp][t][lane], __shfl_sync(FULL, ilm_l, t));
-    sA[warp][t][lane] = xt;
-    for (u32 mk = sM[warp][t]; mk; mk &= mk - 1) {  // the nonzeros of row t only
-      const int u = __ffs(mk) - 1;
-      sA[warp][u][lane] = fp.sub(sA[warp][u][lane], fp.mont_mul(xt, sT[warp][t][u]));
-    }
-  }
-  __syncwarp();
-  // W[s][t] = -x^{(s)}_t times R^2: mont_mul(v_s, W[s][t]) summed over s is
-  // the multiplier m_t in Montgomery form
-  for (u32 s = 0; s < 32; ++s) {
-    const u32 xm = (s < nw && (u32)lane < nw) ? sA[warp][lane][s] : 0u;
-    winW[(size_t)j * 1024 + s * 32 + lane] = fp.to_mont(fp.neg(xm));
-  }
-}
-
-// Packed pivot tails for k_sweep_win: one warp per A column copies its pivot
-// row's tail into its reserved 4-entry groups; PK: (col << 16 | val) in one
-// u32 (N < 2^16, p < 2^16), else (col, val) pairs.  Padding entries point at
-// the dummy accumulator slot N with value 0.
+// k_tail_copy: one warp per A column (pivot a = 32 j + t of window j) walks
+// its pivot row's tail once, coalesced: reserves ceil(len / 4) packed groups
+// (winD[a]; any placement works, the sweep follows winD), copies the tail
+// into them (PK: (col << 16 | val) in one u32 when N, p < 2^16, else
+// (col, val) pairs; padding points at the dummy accumulator slot N with value
+// 0), and scatters the tail's in-window entries (A columns of window j, a
+// prefix of the tail) into the window's dense block T_j (Montgomery) and its
+// row masks.  k_win_build then only solves: the in-window prefixes were a
+// serial chain of dependent L2 loads per pivot there (~30 us per launch).
 template <bool PK>
-__global__ void __launch_bounds__(256) k_tail_copy(const u32* __restrict__ col, const u32* __restrict__ val, u32 N,
-                                                   const uint4* __restrict__ desc, const u32* __restrict__ winC,
-                                                   const uint2* __restrict__ winD, u32 nA,
+__global__ void __launch_bounds__(256) k_tail_copy(Fp fp, const u32* __restrict__ col, const u32* __restrict__ val,
+                                                   u32 N, const uint4* __restrict__ desc,
+                                                   const u32* __restrict__ abits, const u32* __restrict__ acols,
+                                                   const u32* __restrict__ apos, const u32* __restrict__ pnA, u32 nA,
+                                                   uint2* __restrict__ winD, u32* __restrict__ gcursor,
+                                                   u32* __restrict__ winT, u32* __restrict__ winM,
                                                    typename std::conditional<PK, u32, uint2>::type* __restrict__ tails) {
   const int lane = threadIdx.x & 31;
   const u32 a = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (pnA) nA = *pnA;  // enqueued before the host knows nA (grid sized by N)
   if (a >= nA) return;
-  const uint4 d = __ldg(desc + __ldg(winC + a));
-  const uint2 g = __ldg(winD + a);
-  const u32 len = d.y - d.x, n4 = 4 * (g.y - g.x);
+  const u32 j = a >> 5, t = a & 31;
+  const u32 cw = __ldg(acols + a);
+  const u32 clast = __ldg(acols + min(32 * j + 31, nA - 1));
+  const uint4 d = __ldg(desc + cw);
+  const u32 len = d.y - d.x, ng = (len + 3) >> 2, n4 = 4 * ng;
+  u32 g0 = 0;
+  if (lane == 0) g0 = atomicAdd(gcursor, ng);
+  g0 = __shfl_sync(0xffffffffu, g0, 0);
+  if (lane == 0) winD[a] = make_uint2(g0, g0 + ng);
+  u32 mask = 0;
   for (u32 k0 = 0; k0 < n4; k0 += 128) {
     u32 cc[4], vv[4];
 #pragma unroll
@@ -729,10 +638,84 @@ __global__ void __launch_bounds__(256) k_tail_copy(const u32* __restrict__ col, 
     for (int q = 0; q < 4; ++q) {
       const u32 k = k0 + q * 32 + lane;
       if (k < n4) {
-        if constexpr (PK) tails[(size_t)4 * g.x + k] = (cc[q] << 16) | vv[q];
-        else tails[(size_t)4 * g.x + k] = make_uint2(cc[q], vv[q]);
+        if constexpr (PK) tails[(size_t)4 * g0 + k] = (cc[q] << 16) | vv[q];
+        else tails[(size_t)4 * g0 + k] = make_uint2(cc[q], vv[q]);
+      }
+      if (cc[q] <= clast && ((__ldg(abits + (cc[q] >> 5)) >> (cc[q] & 31)) & 1u)) {
+        const u32 u = __ldg(apos + cc[q]) - 32 * j;
+        winT[(size_t)j * 1024 + t * 32 + u] = fp.to_mont(vv[q]);
+        mask |= 1u << u;
       }
     }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mask |= __shfl_xor_sync(0xffffffffu, mask, o);
+  if (lane == 0) winM[a] = mask;
+}
+
+// Block inverses W_j = -T_j^{-1} (one warp per window, T_j from k_tail_copy):
+// lane s solves x T = e_s right-looking (Montgomery domain), its vector in
+// shared memory (sA[u][s], conflict free; a rolled loop keeps the code in the
+// instruction cache): x_t = a_t / lead_t, then a_u -= x_t T[t][u].
+static constexpr int WB_WARPS = 4;
+__global__ void __launch_bounds__(32 * WB_WARPS) k_win_build(Fp fp, u32 N, const uint4* __restrict__ desc,
+                                                             const u32* __restrict__ acols,
+                                                             const u32* __restrict__ pnA, u32 nA,
+                                                             const u32* __restrict__ winT,
+                                                             const u32* __restrict__ winM, u32* __restrict__ winW,
+                                                             u32* __restrict__ winC) {
+  __shared__ u32 sT[WB_WARPS][32][33];  // T[r][t] (Montgomery): pivot r's entry at window column t (r < t)
+  __shared__ u32 sA[WB_WARPS][32][33];  // sA[u][s]: lane s's working vector
+  __shared__ u32 sM[WB_WARPS][32];      // nonzero pattern of T's row r
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const u32 j = blockIdx.x * WB_WARPS + warp;
+  if (pnA) nA = *pnA;
+  const u32 nwin = (nA + 31) / 32;
+  if (j >= nwin) return;
+  const unsigned FULL = 0xffffffffu;
+  const u32 base = j * 32;
+  const u32 nw = min(32u, nA - base);
+  const u32 cw = (u32)lane < nw ? __ldg(acols + base + lane) : N;
+  const uint4 d = (u32)lane < nw ? __ldg(desc + cw) : make_uint4(0, 0, 1, NONE);
+  winC[base + lane] = cw;
+  sM[warp][lane] = (u32)lane < nw ? __ldg(winM + base + lane) : 0u;
+#pragma unroll 8
+  for (int r = 0; r < 32; ++r) sT[warp][r][lane] = __ldg(winT + (size_t)j * 1024 + r * 32 + lane);
+  __syncwarp();
+  const u32 ilm_l = fp.to_mont(d.z);
+  const u32 one_m = fp.to_mont(1u);
+  for (int u = 0; u < 32; ++u) sA[warp][u][lane] = lane == u ? one_m : 0u;
+  __syncwarp();
+  for (int t = 0; t < 32; ++t) {
+    const u32 xt = fp.mont_mul(sA[warp][t][lane], __shfl_sync(FULL, ilm_l, t));
+    sA[warp][t][lane] = xt;
+    // the nonzeros of row t only, four independent updates in flight
+    for (u32 mk = sM[warp][t]; mk;) {
+      int u[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        u[q] = mk ? __ffs(mk) - 1 : -1;
+        mk &= mk - 1;
+      }
+      u32 a4[4], t4[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (u[q] >= 0) {
+          a4[q] = sA[warp][u[q]][lane];
+          t4[q] = sT[warp][t][u[q]];
+        }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (u[q] >= 0) sA[warp][u[q]][lane] = fp.sub(a4[q], fp.mont_mul(xt, t4[q]));
+    }
+  }
+  __syncwarp();
+  // W[s][t] = -x^{(s)}_t times R^2: mont_mul(v_s, W[s][t]) summed over s is
+  // the multiplier m_t in Montgomery form
+#pragma unroll 8
+  for (u32 s = 0; s < 32; ++s) {
+    const u32 xm = (s < nw && (u32)lane < nw) ? sA[warp][lane][s] : 0u;
+    winW[(size_t)j * 1024 + s * 32 + lane] = fp.to_mont(fp.neg(xm));
   }
 }
 
@@ -755,8 +738,8 @@ struct SweepOut {
   u32* s_len;
   u32* err;
 };
-template <bool PK, int MODE>
-__global__ void __launch_bounds__(256) k_sweep_win(Fp fp, u32 mu, const u32* __restrict__ rp,
+template <bool PK, int MODE, int H = 4, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) k_sweep_win(Fp fp, u32 mu, const u32* __restrict__ rp,
                                                    const u32* __restrict__ col, const u32* __restrict__ val, u32 N,
                                                    const u32* __restrict__ rows, u32 nrows,
                                                    const u32* __restrict__ abits_g, const u32* __restrict__ winW,
@@ -765,8 +748,7 @@ __global__ void __launch_bounds__(256) k_sweep_win(Fp fp, u32 mu, const u32* __r
                                                    u32* __restrict__ Dp, u32 K, const u32* __restrict__ nonA,
                                                    unsigned long long* __restrict__ stats, const SweepOut so) {
   extern __shared__ __align__(16) u32 smem[];
-  constexpr int NWARP = 8;
-  constexpr int H = 4;  // 32-group spans per warp in flight
+  constexpr int NWARP = 8;  // H: 32-group spans per warp in flight
   const u32 nwords = (N + 31) / 32;
   u32* abits = smem;
   u32* apre = smem + nwords;  // A columns before word w
@@ -1186,6 +1168,7 @@ struct DblkState {
   u32 cnt, np, rho, rho_old, iters, t2_us, t3_us, t3a_us;  // t*_us: CTA 0 phase times (trace)
   u32 t2a_us, t2b_us, t2c_us, pad;                         // phase 2 split: window load | forward | back + inverse
   u32 offers, distinct;                                    // trace: offers and distinct offered leads, summed over blocks
+  u32 fc1, fc2, fc3, fcn;  // trace: forward loop kilocycles (min + barrier | update | barrier), iterations
 };
 F4B_DEV unsigned long long gtimer() {
   unsigned long long t;
@@ -1211,9 +1194,11 @@ __global__ void __launch_bounds__(DB_THREADS) k_dense_blk(Fp fp, u32* __restrict
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const u32 G = gridDim.x, bid = blockIdx.x;
   const u32 p = fp.p;
+  const bool tiny = p < 32768u;                          // 2 p^2 < 2^31
+  const u32 mu32 = (u32)(0x100000000ull / p);            // Barrett constant
   __shared__ u32 s_T[DB_NP][DB_NP + 1];  // CTA 0: Y (-> T^-1); all: T^-1 of the block
   __shared__ u32 s_U[DB_NP][DB_NP + 33];  // CTA 0: pivot rows at L | Z
-  __shared__ u32 s_dinv[DB_NP], s_crow[DB_NP], s_rl[DB_NP];
+  __shared__ u32 s_crow[DB_NP], s_rl[DB_NP];
   __shared__ u32 s_wrow[DB_NP], s_wcol[DB_NP];
   __shared__ u32 s_red[33];
   __shared__ u32 s_lm[NW][DB_G];
@@ -1328,15 +1313,23 @@ __global__ void __launch_bounds__(DB_THREADS) k_dense_blk(Fp fp, u32* __restrict
         tb0 = gtimer();
         t2a += tb0 - tm;
       }
-      // 2b: forward elimination inside the window (row scaling, no inverses)
+      // 2b: forward elimination inside the window (row scaling, no inverses);
+      // the pivot is the lowest candidate of the smallest lead (one 32-bit
+      // warp min), each warp updates its two rows interleaved
+      __shared__ unsigned long long s_upd;
+      unsigned long long fa = 0, fb = 0, fc = 0, fn = 0, ft0 = 0;
       while (true) {
-        unsigned long long m = ~0ull;
-        if ((u32)lane < nc && s_rl[lane] < (u32)DB_W) m = ((unsigned long long)s_rl[lane] << 32) | (u32)lane;
-#pragma unroll
-        for (int o = 16; o; o >>= 1) m = min(m, __shfl_xor_sync(FULL, m, o));
-        if (m == ~0ull) break;
-        const u32 pw = (u32)(m & 0xFFFFFFFFull), c = (u32)(m >> 32);
+        if (dflag && tid == 0) {
+          ft0 = clock64();
+          s_upd = 0;
+        }
+        const u32 key = ((u32)lane < nc && s_rl[lane] < (u32)DB_W) ? (s_rl[lane] << 5) | (u32)lane : 0xFFFFFFFFu;
+        const u32 m = __reduce_min_sync(FULL, key);
+        if (m == 0xFFFFFFFFu) break;
+        const u32 pw = m & 31u, c = m >> 5;
         __syncthreads();  // every warp has read s_rl
+        unsigned long long ft1 = 0;
+        if (dflag && tid == 0) ft1 = clock64();
         if (tid == 0) {
           s_wrow[s_np] = pw;  // candidate slot for now
           s_wcol[s_np] = c;   // window column for now
@@ -1344,70 +1337,114 @@ __global__ void __launch_bounds__(DB_THREADS) k_dense_blk(Fp fp, u32* __restrict
           s_rl[pw] = DB_W + 1;  // used
         }
         const u32* prw = s_X[pw];
-        const u32 a = fp.to_mont(prw[c]);
-        for (u32 w = warp; w < nc; w += NW) {
-          if (w == pw || s_rl[w] != c) continue;  // rows leading right of c are zero at c
-          u32* x = s_X[w];
-          const u32 bm = fp.to_mont(fp.neg(x[c]));
-          u32 l = DB_W;
+        static_assert(DB_NP == 2 * NW, "two candidate rows per warp");
+        const u32 wa = warp, wb = warp + NW;
+        const bool ua = wa < nc && wa != pw && s_rl[wa] == c;  // rows leading right of c are zero at c
+        const bool ub = wb < nc && wb != pw && s_rl[wb] == c;
+        if (ua || ub) {
+          u32* xa = s_X[wa];
+          u32* xb = s_X[wb];
+          // x <- a x - x[c] prow: p < 2^15 sums both raw products in 32 bits
+          // and reduces once (Barrett); otherwise Montgomery products
+          const u32 a = tiny ? prw[c] : fp.to_mont(prw[c]);
+          const u32 ba = ua ? (tiny ? p - xa[c] : fp.to_mont(fp.neg(xa[c]))) : 0u;
+          const u32 bb = ub ? (tiny ? p - xb[c] : fp.to_mont(fp.neg(xb[c]))) : 0u;
+          auto comb = [&](u32 m1, u32 x1, u32 m2, u32 x2) -> u32 {
+            if (tiny) {
+              const u32 t = m1 * x1 + m2 * x2;  // < 2 p^2 < 2^31
+              const u32 r = t - __umulhi(t, mu32) * p;
+              return r >= p ? r - p : r;
+            }
+            return fp.add(fp.mont_mul(m1, x1), fp.mont_mul(m2, x2));
+          };
+          u32 la = DB_W, lb = DB_W;
 #pragma unroll
           for (int h = DB_W / 32; h >= 0; --h) {  // h = DB_W/32: the coefficients
+            if (h < DB_W / 32 && 32 * h + 31 < (int)c) continue;  // left of c: zero in both rows
             const u32 q = lane + 32 * h;
-            u32 v = 0;
+            const u32 pq = prw[q];
+            u32 va = 0, vb = 0;
             if (q > c) {
-              v = fp.add(fp.mont_mul(a, x[q]), fp.mont_mul(bm, prw[q]));
-              x[q] = v;
+              if (ua) {
+                va = comb(a, xa[q], ba, pq);
+                xa[q] = va;
+              }
+              if (ub) {
+                vb = comb(a, xb[q], bb, pq);
+                xb[q] = vb;
+              }
             } else if (q == c) {
-              x[q] = 0;
+              if (ua) xa[q] = 0;
+              if (ub) xb[q] = 0;
             }
             if (h < DB_W / 32) {
-              const unsigned b = __ballot_sync(FULL, v != 0);
-              if (b) l = 32 * h + __ffs(b) - 1;
+              const unsigned b1 = __ballot_sync(FULL, va != 0), b2 = __ballot_sync(FULL, vb != 0);
+              if (b1) la = 32 * h + __ffs(b1) - 1;
+              if (b2) lb = 32 * h + __ffs(b2) - 1;
             }
           }
-          if (lane == 0) s_rl[w] = l;
+          if (lane == 0) {
+            if (ua) s_rl[wa] = la;
+            if (ub) s_rl[wb] = lb;
+          }
         }
+        if (dflag && lane == 0) atomicMax(&s_upd, (unsigned long long)clock64());
         __syncthreads();
+        if (dflag && tid == 0) {
+          const unsigned long long ft3 = clock64(), fu = max(s_upd, ft1);
+          fa += ft1 - ft0;
+          fb += fu - ft1;
+          fc += ft3 - fu;
+          fn += 1;
+        }
+      }
+      if (dflag && tid == 0) {
+        st->fc1 += (u32)(fa / 1000);
+        st->fc2 += (u32)(fb / 1000);
+        st->fc3 += (u32)(fc / 1000);
+        st->fcn += (u32)fn;
       }
       if (tid == 0) {
         const unsigned long long tc0 = gtimer();
         t2b += tc0 - tb0;
         tb0 = tc0;
       }
-      // 2c: back-elimination over the pivot columns and the coefficients
-      // (one warp per pivot row): E[:, L] becomes diagonal, then Z / diag =
-      // T^-1 expressed over the candidate slots
+      // 2c: Y = U_L^-1 Z by back-substitution on the coefficient vectors (U_L
+      // = the pivot rows at the pivot columns, upper triangular; Z their
+      // expressions over the candidate slots): one warp, lane = slot, no CTA
+      // barrier per pivot.  Y's rows have the identity at L: T^-1 = Y[:, S].
       const u32 np = s_np;
       for (u32 e = tid; e < np * (DB_NP + 32); e += DB_THREADS) {
         const u32 i = e / (DB_NP + 32), k = e % (DB_NP + 32);
         const u32* x = s_X[s_wrow[i]];
-        s_U[i][k] = k < DB_NP ? (k < np ? x[s_wcol[k]] : 0u) : x[DB_W + (k - DB_NP)];
+        s_U[i][k] = k < DB_NP ? (k < np ? fp.to_mont(x[s_wcol[k]]) : 0u) : x[DB_W + (k - DB_NP)];
       }
       __syncthreads();
-      for (int j = (int)np - 1; j > 0; --j) {
-        const u32 a = fp.to_mont(s_U[j][j]);
-        for (u32 i = warp; i < (u32)j; i += NW) {
-          const u32 f = s_U[i][j];
-          __syncwarp();
-          if (f) {
-            const u32 bm = fp.to_mont(fp.neg(f));
+      if (warp == 0) {
+        const u32 dl = (u32)lane < np ? fp.to_mont(fp.inv(fp.mont_mul(s_U[lane][lane], 1u))) : 0u;
+        for (int i = (int)np - 1; i >= 0; --i) {
+          const u32 y = fp.mont_mul(__shfl_sync(FULL, dl, i), s_U[i][DB_NP + lane]);
+          s_U[i][DB_NP + lane] = y;
+          int r = 0;
+          for (; r + 4 <= i; r += 4) {  // four independent updates in flight
+            u32 z[4], u[4];
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const u32 k = lane + 32 * h;
-              if (k >= i) s_U[i][k] = fp.add(fp.mont_mul(a, s_U[i][k]), fp.mont_mul(bm, s_U[j][k]));
+            for (int q = 0; q < 4; ++q) {
+              z[q] = s_U[r + q][DB_NP + lane];
+              u[q] = s_U[r + q][i];
             }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) s_U[r + q][DB_NP + lane] = fp.sub(z[q], fp.mont_mul(u[q], y));
           }
+          for (; r < i; ++r) s_U[r][DB_NP + lane] = fp.sub(s_U[r][DB_NP + lane], fp.mont_mul(s_U[r][i], y));
         }
-        __syncthreads();
       }
-      if (tid < (int)np) s_dinv[tid] = fp.to_mont(fp.inv(s_U[tid][tid]));
       __syncthreads();
       if (tid == 0) t2c += gtimer() - tb0;
-      // T^-1[i][j] = Z_i[slot of S_j] / d_i
+      // T^-1[i][j] = Y_i[slot of S_j]
       for (u32 e = tid; e < np * np; e += DB_THREADS) {
         const u32 i = e / np, j = e % np;
-        const u32 v = fp.mont_mul(s_dinv[i], s_U[i][DB_NP + s_wrow[j]]);
-        gT[i * DB_NP + j] = fp.to_mont(v);
+        gT[i * DB_NP + j] = fp.to_mont(s_U[i][DB_NP + s_wrow[j]]);
       }
       if (tid < (int)np) {
         const u32 row = s_crow[s_wrow[tid]], col = c0 + s_wcol[tid];
@@ -1641,78 +1678,101 @@ static int sweep_grid(Ctx* c, size_t smem, long long rows) {
 
 // k_sweep<MODE, T>: u16 accumulators when p < 2^16 and the row fits shared
 // memory, u32 in shared memory otherwise, u32 in HBM for very wide matrices.
+// Window tables of k_sweep_win (k_tail_copy + k_win_build), enqueued either
+// with the host's nA or, right behind k_psge_prep, with nA read on the device
+// and the grids sized by N (the host then learns (nA, nC) while these run).
+struct WinPrep {
+  bool ok = false, pk = false;
+  DBuf wW, wC, wD, wT, gcur, wTm, wM;
+};
+static bool win_eligible(Ctx* c, u32 N, long long nA_bound) {
+  const size_t nwords = (N + 31) / 32;
+  const size_t smem = (size_t)((2 * nwords + 3) & ~(size_t)3) * 4 + (size_t)(N + 1) * 4;
+  // lazily reduced u32 accumulator: initial value + one product in [0, 2p)
+  // per applied pivot
+  return c->opt_sweep == 0 && nA_bound > 0 &&
+         (unsigned long long)c->p * (2ull * (unsigned long long)nA_bound + 2) < (1ull << 32) && smem <= 180 * 1024;
+}
+static void win_prepare(Ctx* c, const Fp& fp, f4b_echelon* E, const u32* d_nA, u32 nA_bound, WinPrep& w) {
+  const u32 N = (u32)E->n_cols;
+  w.pk = N < 65535u && c->p < 65536u;
+  const u32 nwin = (nA_bound + 31) / 32;
+  const size_t groups = (size_t)(E->M + 4 * (long long)nA_bound) / 4 + 8;
+  ensure(c, w.wW, (size_t)nwin * 1024 * sizeof(u32));
+  ensure(c, w.wC, (size_t)nwin * 32 * sizeof(u32));
+  ensure(c, w.wD, (size_t)nwin * 32 * sizeof(uint2));
+  ensure(c, w.wT, groups * (w.pk ? 16 : 32));
+  ensure(c, w.wTm, (size_t)nwin * 1024 * sizeof(u32));
+  ensure(c, w.wM, (size_t)nwin * 32 * sizeof(u32));
+  ensure(c, w.gcur, 16);
+  check_cuda(cudaMemsetAsync(w.gcur.p, 0, 4, c->stream), "memset");
+  check_cuda(cudaMemsetAsync(w.wTm.p, 0, (size_t)nwin * 1024 * sizeof(u32), c->stream), "memset");
+  if (w.pk)
+    F4B_LAUNCH(c, k_tail_copy<true>, nb(nA_bound, 8), 256, 0, fp, E->col, E->val, N, E->desc.as<uint4>(),
+               E->abits.as<u32>(), E->acols.as<u32>(), E->apos.as<u32>(), d_nA, nA_bound, w.wD.as<uint2>(),
+               w.gcur.as<u32>(), w.wTm.as<u32>(), w.wM.as<u32>(), w.wT.as<u32>());
+  else
+    F4B_LAUNCH(c, k_tail_copy<false>, nb(nA_bound, 8), 256, 0, fp, E->col, E->val, N, E->desc.as<uint4>(),
+               E->abits.as<u32>(), E->acols.as<u32>(), E->apos.as<u32>(), d_nA, nA_bound, w.wD.as<uint2>(),
+               w.gcur.as<u32>(), w.wTm.as<u32>(), w.wM.as<u32>(), w.wT.as<uint2>());
+  F4B_LAUNCH(c, k_win_build, nb(nwin, WB_WARPS), 32 * WB_WARPS, 0, fp, N, E->desc.as<uint4>(), E->acols.as<u32>(),
+             d_nA, nA_bound, w.wTm.as<u32>(), w.wM.as<u32>(), w.wW.as<u32>(), w.wC.as<u32>());
+  w.ok = true;
+}
+static void win_release(Ctx* c, WinPrep& w) {
+  for (DBuf* b : {&w.wW, &w.wC, &w.wD, &w.wT, &w.gcur, &w.wTm, &w.wM}) release(c, *b);
+  w.ok = false;
+}
+
+// k_sweep<MODE, T>: u16 accumulators when p < 2^16 and the row fits shared
+// memory, u32 in shared memory otherwise, u32 in HBM for very wide matrices.
 template <int MODE>
 static void launch_sweep(Ctx* c, const Fp& fp, f4b_echelon* E, const u32* rows, u32 nrows, u32* Dp, u32 K,
                          const u32* Rd, u32 rankD, const u32* dpiv, u32* pcol, u32* pval, size_t cap,
                          unsigned long long* cursor, u32* s_off, u32* s_len, u32* err,
-                         unsigned long long* stats = nullptr) {
+                         unsigned long long* stats = nullptr, WinPrep* pre = nullptr) {
   const u32 N = (u32)E->n_cols;
   // c->opt_sweep (f4b_ctx_set_option "sweep"): 0 = automatic (windows, then
   // the blocked sweep, then k_sweep), 1 = start at the blocked sweep,
   // 2 = k_sweep only — the fallbacks are forced by the parity tests
-  if (c->opt_sweep == 0 && E->nA > 0) {
+  if (win_eligible(c, N, E->nA)) {
     // fixed windows with precomputed block inverses (k_win_build + k_sweep_win)
     const size_t nwords = (N + 31) / 32;
     const size_t smem = (size_t)((2 * nwords + 3) & ~(size_t)3) * 4 + (size_t)(N + 1) * 4;
-    // lazily reduced u32 accumulator: initial value + one product in [0, 2p)
-    // per applied pivot
-    if ((unsigned long long)c->p * (2ull * (unsigned long long)E->nA + 2) < (1ull << 32) && smem <= 180 * 1024) {
-      const bool pk = N < 65535u && c->p < 65536u;
-      static bool wattr = false;
-      if (!wattr) {
-        check_cuda(cudaFuncSetAttribute(k_sweep_win<true, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
-                   "attr");
-        check_cuda(cudaFuncSetAttribute(k_sweep_win<false, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
-                   "attr");
-        wattr = true;
-      }
-      const u32 nA = (u32)E->nA, nwin = (nA + 31) / 32;
-      const size_t groups = (size_t)(E->M + 4 * (long long)nA) / 4 + 8;
-      DBuf wW, wC, wD, wT, gcur;
-      ensure(c, wW, (size_t)nwin * 1024 * sizeof(u32));
-      ensure(c, wC, (size_t)nwin * 32 * sizeof(u32));
-      ensure(c, wD, (size_t)nwin * 32 * sizeof(uint2));
-      ensure(c, wT, groups * (pk ? 16 : 32));
-      ensure(c, gcur, 16);
-      check_cuda(cudaMemsetAsync(gcur.p, 0, 4, c->stream), "memset");
-      F4B_LAUNCH(c, k_win_build, nb(nwin, WB_WARPS), 32 * WB_WARPS, 0, fp, E->col, E->val, N, E->desc.as<uint4>(),
-                 E->abits.as<u32>(), E->acols.as<u32>(), E->apos.as<u32>(), nA, nwin, wW.as<u32>(), wC.as<u32>(),
-                 wD.as<uint2>(), gcur.as<u32>());
-      if (pk)
-        F4B_LAUNCH(c, k_tail_copy<true>, nb(nA, 8), 256, 0, E->col, E->val, N, E->desc.as<uint4>(), wC.as<u32>(),
-                   wD.as<uint2>(), nA, wT.as<u32>());
-      else
-        F4B_LAUNCH(c, k_tail_copy<false>, nb(nA, 8), 256, 0, E->col, E->val, N, E->desc.as<uint4>(), wC.as<u32>(),
-                   wD.as<uint2>(), nA, wT.as<uint2>());
-      int per_sm = 0;
-      check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                     &per_sm, pk ? k_sweep_win<true, MODE> : k_sweep_win<false, MODE>, 256, smem),
-                 "occupancy");
-      per_sm = std::max(1, per_sm);
-      const int grid = (int)std::max<long long>(1, std::min<long long>(nrows, (long long)c->num_sms * per_sm));
-      const u32 mu = (u32)((1ull << 32) / c->p);
-      SweepOut so{E->invl.as<u32>(), Rd, rankD, dpiv, pcol, pval, cap, cursor, s_off, s_len, err};
-      {
-        ProfScope ps(c, pk ? (MODE ? "k_sweep_win<true,1>" : "k_sweep_win<true>")
-                           : (MODE ? "k_sweep_win<false,1>" : "k_sweep_win<false>"));
-        if (pk)
-          k_sweep_win<true, MODE><<<grid, 256, smem, c->stream>>>(fp, mu, E->rp, E->col, E->val, N, rows, nrows,
-                   E->abits.as<u32>(), wW.as<u32>(), wC.as<u32>(), wD.as<uint2>(), nwin, wT.as<uint4>(), Dp, K,
-                   E->nonA.as<u32>(), stats, so);
-        else
-          k_sweep_win<false, MODE><<<grid, 256, smem, c->stream>>>(fp, mu, E->rp, E->col, E->val, N, rows, nrows,
-                   E->abits.as<u32>(), wW.as<u32>(), wC.as<u32>(), wD.as<uint2>(), nwin, wT.as<uint4>(), Dp, K,
-                   E->nonA.as<u32>(), stats, so);
-        check_cuda(cudaGetLastError(), "k_sweep_win");
-      }
-      release(c, wW);
-      release(c, wC);
-      release(c, wD);
-      release(c, wT);
-      release(c, gcur);
-      return;
+    WinPrep local;
+    WinPrep& w = pre && pre->ok ? *pre : local;
+    if (!w.ok) win_prepare(c, fp, E, nullptr, (u32)E->nA, w);
+    const bool pk = w.pk;
+    const void* kf = pk ? (const void*)k_sweep_win<true, MODE> : (const void*)k_sweep_win<false, MODE>;
+    static int per_sm_c[2] = {-1, -1};
+    static size_t smem_c[2] = {0, 0};
+    if (per_sm_c[pk] < 0 || smem_c[pk] != smem) {  // occupancy query once per (kernel, N)
+      check_cuda(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "attr");
+      check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_c[pk], kf, 256, smem), "occupancy");
+      smem_c[pk] = smem;
     }
+    const int per_sm = std::max(1, per_sm_c[pk]);
+    const int grid = (int)std::max<long long>(1, std::min<long long>(nrows, (long long)c->num_sms * per_sm));
+    const u32 mu = (u32)((1ull << 32) / c->p);
+    const u32 nwin = (u32)((E->nA + 31) / 32);
+    SweepOut so{E->invl.as<u32>(), Rd, rankD, dpiv, pcol, pval, cap, cursor, s_off, s_len, err};
+    {
+      ProfScope ps(c, pk ? (MODE ? "k_sweep_win<true,1>" : "k_sweep_win<true>")
+                         : (MODE ? "k_sweep_win<false,1>" : "k_sweep_win<false>"));
+      if (pk)
+        k_sweep_win<true, MODE><<<grid, 256, smem, c->stream>>>(fp, mu, E->rp, E->col, E->val, N, rows, nrows,
+                 E->abits.as<u32>(), w.wW.as<u32>(), w.wC.as<u32>(), w.wD.as<uint2>(), nwin, w.wT.as<uint4>(), Dp, K,
+                 E->nonA.as<u32>(), stats, so);
+      else
+        k_sweep_win<false, MODE><<<grid, 256, smem, c->stream>>>(fp, mu, E->rp, E->col, E->val, N, rows, nrows,
+                 E->abits.as<u32>(), w.wW.as<u32>(), w.wC.as<u32>(), w.wD.as<uint2>(), nwin, w.wT.as<uint4>(), Dp, K,
+                 E->nonA.as<u32>(), stats, so);
+      check_cuda(cudaGetLastError(), "k_sweep_win");
+    }
+    win_release(c, w);
+    return;
   }
+  if (pre && pre->ok) win_release(c, *pre);
   if (MODE == 0 && c->opt_sweep <= 1) {
     // blocked sweep: lazily reduced u32 accumulator needs p * (nA + 1) < 2^32
     const size_t bitmap = (size_t)((((N + 31) / 32) + 3) & ~3u) * 4;
@@ -1772,6 +1832,19 @@ static void launch_sweep(Ctx* c, const Fp& fp, f4b_echelon* E, const u32* rows, 
 
 static void run_a_sweep(Ctx* c, f4b_echelon* E);
 
+// psge tail record (pool use, sweep counters, rank(D'), error flags) written
+// by one thread into page-locked host memory (UVA)
+__global__ void k_tail_gather(const unsigned long long* cursor, const unsigned long long* stats, const u32* rdev,
+                              const u32* err, unsigned long long* out) {
+  if (threadIdx.x != 0) return;
+  volatile unsigned long long* o = out;
+  o[0] = *cursor;
+  o[1] = stats ? stats[0] : 0ull;
+  o[2] = stats ? stats[1] : 0ull;
+  o[3] = (unsigned long long)*rdev | ((unsigned long long)*err << 32);
+  __threadfence_system();
+}
+
 static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
   Fp fp = make_fp(c);
   static const bool etrace = getenv("F4B_ELIM_TRACE") != nullptr;
@@ -1779,16 +1852,26 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
   const long long a0 = c->raw_allocs, f0 = c->raw_frees;
   const double au0 = c->raw_alloc_us;
   std::vector<std::pair<const char*, double>> marks;
+  // trace: host marks plus a device event per mark (device gaps = host work)
+  static cudaEvent_t tev[12] = {};
+  int ntev = 0;
   auto mark = [&](const char* w) {
-    if (etrace) marks.push_back({w, std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count()});
+    if (!etrace) return;
+    marks.push_back({w, std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count()});
+    if (ntev < 12) {
+      if (!tev[ntev]) cudaEventCreate(&tev[ntev]);
+      cudaEventRecord(tev[ntev++], c->stream);
+    }
   };
   const long long r = E->n_rows, N = E->n_cols;
   cudaEvent_t ev0 = timing_event(c, 2), ev1 = timing_event(c, 3);
   check_cuda(cudaEventRecord(ev0, c->stream), "event");
+  mark("start");
   ensure(c, c->errflag, 64);
   u32* err = c->errflag.as<u32>();
   check_cuda(cudaMemsetAsync(err, 0, 4, c->stream), "memset");
   const long long Nn = std::max<long long>(N, 1);
+  WinPrep wpre;  // window tables queued behind k_psge_prep (see win_prepare)
   // E1: one cooperative launch (k_psge_prep) and one read of (nA, nC)
   DBuf pk, crows, pcnt;
   ensure(c, pk, Nn * sizeof(unsigned long long));
@@ -1803,6 +1886,8 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
   {
     static int bpp = -1;
     if (bpp < 0) check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpp, k_psge_prep, 256, 0), "occupancy");
+    // every SM (a grid sized by the batch, ~2K rows per CTA, was measured
+    // slower: 0.9 -> 1.2 ms of k_psge_prep per cyclic-8 step)
     const int GP = c->num_sms * std::max(1, std::min(bpp, 2));
     ensure(c, pcnt, (size_t)GP * sizeof(u32) + sizeof(PrepOut) + 16);
     PrepOut* d_out = reinterpret_cast<PrepOut*>(pcnt.as<u32>() + GP);
@@ -1829,7 +1914,13 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
     PrepOut ho;
     mark("prep launched");
     check_cuda(cudaMemcpyAsync(c->h_stat, d_out, sizeof(PrepOut), cudaMemcpyDeviceToHost, c->stream), "d2h");
-    check_cuda(cudaStreamSynchronize(c->stream), "sync");
+    cudaEvent_t evp = timing_event(c, 0);
+    check_cuda(cudaEventRecord(evp, c->stream), "event");
+    // the window tables need only the device's nA: queued now, they run
+    // while the host waits for (nA, nC)
+    const long long nA_bound = std::min(r, N);
+    if (win_eligible(c, (u32)N, nA_bound)) win_prepare(c, fp, E, &d_out->nA, (u32)nA_bound, wpre);
+    check_cuda(cudaEventSynchronize(evp), "sync");
     mark("prep synced");
     memcpy(&ho, c->h_stat, sizeof(PrepOut));
     E->nA = ho.nA;
@@ -1848,7 +1939,7 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
     check_cuda(cudaMemsetAsync(E->stats.p, 0, 16, c->stream), "memset");
     mark("sweep issue");
     launch_sweep<0>(c, fp, E, crows.as<u32>(), (u32)R, Dp.as<u32>(), (u32)K, nullptr, 0, nullptr, nullptr, nullptr, 0,
-                    nullptr, nullptr, nullptr, err, E->stats.as<unsigned long long>());
+                    nullptr, nullptr, nullptr, err, E->stats.as<unsigned long long>(), &wpre);
     mark("sweep launched");
     // E3 default: RREF(D') in pivot blocks (k_dense_blk); c->opt_dense = 1
     // (f4b_ctx_set_option "dense") forces the general fallback below
@@ -1912,16 +2003,18 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
         {
           ProfScope ps(c, "k_dense_blk");
           const void* kf = c->p < 65536u ? (const void*)k_dense_blk<true> : (const void*)k_dense_blk<false>;
+          mark("dense issue");
           check_cuda(cudaLaunchCooperativeKernel(kf, (int)G, DB_THREADS, argsb, smem_b, c->stream), "k_dense_blk");
+          mark("dense launched");
         }
         if (btrace) {
           release(c, dfl);
           DblkState hs;
           check_cuda(cudaMemcpyAsync(&hs, stt.p, sizeof(hs), cudaMemcpyDeviceToHost, c->stream), "d2h");
           check_cuda(cudaStreamSynchronize(c->stream), "sync");
-          fprintf(stderr, "[blk] R=%lld K=%lld G=%lld rpc=%lld rank=%u iters=%u t2=%uus (load %u fwd %u back %u) t3=%uus (setup %uus) offers=%u distinct=%u\n",
+          fprintf(stderr, "[blk] R=%lld K=%lld G=%lld rpc=%lld rank=%u iters=%u t2=%uus (load %u fwd %u back %u) t3=%uus (setup %uus) offers=%u distinct=%u fwd_kcyc(min+bar %u upd %u bar %u n %u)\n",
                   (long long)R, (long long)K, (long long)G, (long long)rpc, hs.rho, hs.iters, hs.t2_us, hs.t2a_us,
-                  hs.t2b_us, hs.t2c_us, hs.t3_us, hs.t3a_us, hs.offers, hs.distinct);
+                  hs.t2b_us, hs.t2c_us, hs.t3_us, hs.t3a_us, hs.offers, hs.distinct, hs.fc1, hs.fc2, hs.fc3, hs.fcn);
         }
         for (DBuf* b : {&Bm, &colp, &lead_b, &cand_b, &gl, &gT, &stt, &ordr}) release(c, *b);
         blk_done = true;
@@ -1988,6 +2081,7 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
     ensure(c, E->rdev, 16);
     check_cuda(cudaMemsetAsync(E->rdev.p, 0, 4, c->stream), "memset");
   }
+  if (wpre.ok) win_release(c, wpre);  // no sweep (R = 0 or K = 0)
   release(c, Dp);
   release(c, cand);
   release(c, used);
@@ -2022,11 +2116,11 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
                  E->cursor.as<unsigned long long>(), E->d_off.as<u32>(), E->d_len.as<u32>(), err);
       check_cuda(cudaGetLastError(), "k_emit_dense");
     }
-    ht->st[0] = ht->st[1] = 0;
-    check_cuda(cudaMemcpyAsync(&ht->used_pool, E->cursor.p, 8, cudaMemcpyDeviceToHost, c->stream), "d2h");
-    if (E->stats.p) check_cuda(cudaMemcpyAsync(ht->st, E->stats.p, 16, cudaMemcpyDeviceToHost, c->stream), "d2h");
-    check_cuda(cudaMemcpyAsync(&ht->rankD, E->rdev.p, 4, cudaMemcpyDeviceToHost, c->stream), "d2h");
-    check_cuda(cudaMemcpyAsync(&ht->err, err, 4, cudaMemcpyDeviceToHost, c->stream), "d2h");
+    // one tiny kernel stores (pool use, sweep counters, rank, error) straight
+    // into the page-locked host block (4 D2H copies before)
+    F4B_LAUNCH(c, k_tail_gather, 1, 32, 0, E->cursor.as<unsigned long long>(),
+               E->stats.p ? E->stats.as<unsigned long long>() : nullptr, E->rdev.as<u32>(), err,
+               reinterpret_cast<unsigned long long*>(ht));
     check_cuda(cudaStreamSynchronize(c->stream), "sync");
     if (!(ht->err & DEVERR_CAPACITY)) break;
     if (attempt == 7) fail(F4B_ERR_OOM, "psge: nonpivot row pool still overflows after 8 resizes");
@@ -2044,11 +2138,16 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
   float ms = 0;
   cudaEventElapsedTime(&ms, ev0, ev1);
   E->numeric_ns = (int64_t)(ms * 1e6);
-  if (etrace && ms > 10.0f) {
+  static const float etrace_ms = etrace ? (float)atof(getenv("F4B_ELIM_TRACE")) : 0.f;  // print above this device time
+  if (etrace && ms > etrace_ms) {
     fprintf(stderr, "[elim] r=%lld N=%lld R=%lld K=%lld dev=%.2fms allocs=%lld frees=%lld alloc_us=%.0f:", (long long)r,
             (long long)N, (long long)E->nC, (long long)E->K, ms, c->raw_allocs - a0, c->raw_frees - f0,
             c->raw_alloc_us - au0);
-    for (auto& m : marks) fprintf(stderr, " %s @%.0f |", m.first, m.second);
+    for (size_t i = 0; i < marks.size(); ++i) {
+      float dm = 0;
+      if (i > 0 && (int)i < ntev) cudaEventElapsedTime(&dm, tev[i - 1], tev[i]);
+      fprintf(stderr, " %s @%.0f (dev +%.0fus) |", marks[i].first, marks[i].second, dm * 1e3);
+    }
     fprintf(stderr, "\n");
   }
   E->zero_rows = r - (E->nA + rankD);
