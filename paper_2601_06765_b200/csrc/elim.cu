@@ -737,9 +737,10 @@ struct SweepOut {
   u32* s_off;
   u32* s_len;
   u32* err;
+  unsigned long long* tr;  // trace (F4B_SWEEP_TRACE): rows, windows, misses, cycles find | mult | apply | out
 };
-template <bool PK, int MODE, int H = 4, int MINB = 1>
-__global__ void __launch_bounds__(256, MINB) k_sweep_win(Fp fp, u32 mu, const u32* __restrict__ rp,
+template <bool PK, int MODE, bool TR = false>
+__global__ void __launch_bounds__(256) k_sweep_win(Fp fp, u32 mu, const u32* __restrict__ rp,
                                                    const u32* __restrict__ col, const u32* __restrict__ val, u32 N,
                                                    const u32* __restrict__ rows, u32 nrows,
                                                    const u32* __restrict__ abits_g, const u32* __restrict__ winW,
@@ -748,7 +749,8 @@ __global__ void __launch_bounds__(256, MINB) k_sweep_win(Fp fp, u32 mu, const u3
                                                    u32* __restrict__ Dp, u32 K, const u32* __restrict__ nonA,
                                                    unsigned long long* __restrict__ stats, const SweepOut so) {
   extern __shared__ __align__(16) u32 smem[];
-  constexpr int NWARP = 8;  // H: 32-group spans per warp in flight
+  constexpr int NWARP = 8;
+  constexpr int H = 4;  // 32-group spans per warp in flight
   const u32 nwords = (N + 31) / 32;
   u32* abits = smem;
   u32* apre = smem + nwords;  // A columns before word w
@@ -762,6 +764,7 @@ __global__ void __launch_bounds__(256, MINB) k_sweep_win(Fp fp, u32 mu, const u3
     const u32 r = v - __umulhi(v, mu) * p;
     return r >= p ? r - p : r;
   };
+  const unsigned long long pinv64 = ~0ull / p;  // Shoup constants below without a 64-bit division
   for (u32 w = tid; w < nwords; w += blockDim.x) abits[w] = abits_g[w];
   __syncthreads();
   if (warp == 0) {
@@ -790,23 +793,38 @@ __global__ void __launch_bounds__(256, MINB) k_sweep_win(Fp fp, u32 mu, const u3
     for (u32 k = s + tid; k < e; k += blockDim.x) acc[col[k]] = val[k];
     __syncthreads();
     u32 from = MODE == 1 ? lead + 1 : lead;
+    unsigned long long tq0 = 0, tw = 0, tmiss = 0, tcf = 0, tcm = 0, tca = 0, tcfind = 0, tcv = 0, tqf = 0;
+    const bool trc = TR && so.tr && tid == 0;  // TR: trace build only (the counters cost registers)
+    if (trc) tq0 = clock64();
     u32 pj = 0xFFFFFFFFu, pcw = 0;
     uint2 pdd = make_uint2(0, 0);
     uint4 pw4 = make_uint4(0, 0, 0, 0);
     while (true) {
       // next nonzero A column >= from (every warp, same answer)
+      // (128 columns per step: four independent ballots, then the first hit)
       u32 c = N;
-      for (u32 c0 = from & ~31u; c0 < N; c0 += 32) {
-        const u32 cc = c0 + lane;
-        const bool hit = cc >= from && cc < N && ((abits[cc >> 5] >> (cc & 31)) & 1u) && red(acc[cc]) != 0;
-        const unsigned b = __ballot_sync(0xffffffffu, hit);
-        if (b) {
-          c = c0 + __ffs(b) - 1;
+      for (u32 c0 = from & ~31u; c0 < N; c0 += 128) {
+        unsigned b[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const u32 cc = c0 + 32 * q + lane;
+          const bool hit = cc >= from && cc < N && ((abits[cc >> 5] >> (cc & 31)) & 1u) && red(acc[cc]) != 0;
+          b[q] = __ballot_sync(0xffffffffu, hit);
+        }
+        if (b[0] | b[1] | b[2] | b[3]) {
+          const int q = b[0] ? 0 : b[1] ? 1 : b[2] ? 2 : 3;
+          c = c0 + 32 * q + __ffs(q == 0 ? b[0] : q == 1 ? b[1] : q == 2 ? b[2] : b[3]) - 1;
           break;
         }
       }
       if (c >= N) break;
       const u32 j = (apre[c >> 5] + __popc(abits[c >> 5] & ((1u << (c & 31)) - 1u))) >> 5;
+      if (trc) {
+        ++tw;
+        tmiss += j != pj;
+        tqf = clock64();
+        tcfind += tqf - tq0;
+      }
       // this window's columns, tail groups and block-inverse slice: from the
       // registers if the previous window prefetched them (the usual case:
       // consecutive windows), then the next window's are prefetched so their
@@ -832,6 +850,11 @@ __global__ void __launch_bounds__(256, MINB) k_sweep_win(Fp fp, u32 mu, const u3
         pj = 0xFFFFFFFFu;
       }
       const u32 v = (cw < N && (MODE == 1 ? cw > lead : cw >= lead)) ? red(acc[cw]) : 0u;
+      if (trc) {
+        const u32 vv = v;
+        asm volatile("" ::"r"(vv), "r"(w4.x), "r"(dd.x));  // v, window data ready
+        tcv += clock64() - tqf;
+      }
       // multipliers m = v W, split over the 8 warps: warp w owns pivots
       // t = 4w .. 4w+3 (lane s contributes v_s W[s][t], one 16-byte load),
       // warp sums, then Shoup constants and group counts into shared memory
@@ -850,12 +873,31 @@ __global__ void __launch_bounds__(256, MINB) k_sweep_win(Fp fp, u32 mu, const u3
           // ms * x mod p is then x*ms - umulhi(x, msh)*p, in [0, 2p)
           const u32 ms = fp.mont_mul(mt, 1u);
           s_ms[t] = ms;
-          s_msh[t] = ms ? (u32)(((unsigned long long)ms << 32) / p) : 0u;
+          // floor(ms 2^32 / p) from the 64-bit reciprocal (no division):
+          // the estimate is short by at most one
+          u32 q = 0;
+          if (ms) {
+            const unsigned long long X = (unsigned long long)ms << 32;
+            unsigned long long qe = __umul64hi(X, pinv64);
+            if (X - qe * p >= p) ++qe;
+            q = (u32)qe;
+          }
+          s_msh[t] = q;
           s_ng[t] = ms ? dt.y - dt.x : 0u;
           s_g0[t] = dt.x;
         }
       }
+      unsigned long long tq1 = 0;
+      if (trc) {
+        tq1 = clock64();
+        tcf += tq1 - tq0;  // find + window data + multipliers (this thread)
+      }
       __syncthreads();
+      if (trc) {
+        const unsigned long long tq2 = clock64();
+        tcm += tq2 - tq1;  // barrier after the multipliers
+        tq0 = tq2;
+      }
       const u32 ng = s_ng[lane], ms = s_ms[lane], msh = s_msh[lane];
       u32 x = ng;
 #pragma unroll
@@ -932,7 +974,23 @@ __global__ void __launch_bounds__(256, MINB) k_sweep_win(Fp fp, u32 mu, const u3
         }
       }
       __syncthreads();
+      if (trc) {
+        const unsigned long long tq3 = clock64();
+        tca += tq3 - tq0;  // apply + barrier
+        tq0 = tq3;
+      }
       from = __reduce_max_sync(0xffffffffu, cw < N ? cw : 0u) + 1;
+    }
+    if (trc) {
+      atomicAdd(so.tr + 0, 1ull);
+      atomicAdd(so.tr + 1, tw);
+      atomicAdd(so.tr + 2, tmiss);
+      atomicAdd(so.tr + 3, tcf);
+      atomicAdd(so.tr + 4, tcm);
+      atomicAdd(so.tr + 5, tca);
+      atomicAdd(so.tr + 6, clock64() - tq0);
+      atomicAdd(so.tr + 7, tcfind);
+      atomicAdd(so.tr + 8, tcv);
     }
     if (MODE == 0) {
       u32* out = Dp + (size_t)rr * K;
@@ -1755,11 +1813,22 @@ static void launch_sweep(Ctx* c, const Fp& fp, f4b_echelon* E, const u32* rows, 
     const int grid = (int)std::max<long long>(1, std::min<long long>(nrows, (long long)c->num_sms * per_sm));
     const u32 mu = (u32)((1ull << 32) / c->p);
     const u32 nwin = (u32)((E->nA + 31) / 32);
-    SweepOut so{E->invl.as<u32>(), Rd, rankD, dpiv, pcol, pval, cap, cursor, s_off, s_len, err};
+    static const bool strace = getenv("F4B_SWEEP_TRACE") != nullptr;
+    DBuf trb;
+    if (strace) {
+      ensure(c, trb, 128);
+      check_cuda(cudaMemsetAsync(trb.p, 0, 128, c->stream), "memset");
+    }
+    SweepOut so{E->invl.as<u32>(), Rd, rankD, dpiv, pcol, pval, cap, cursor, s_off, s_len, err,
+                strace ? trb.as<unsigned long long>() : nullptr};
     {
       ProfScope ps(c, pk ? (MODE ? "k_sweep_win<true,1>" : "k_sweep_win<true>")
                          : (MODE ? "k_sweep_win<false,1>" : "k_sweep_win<false>"));
-      if (pk)
+      if (pk && strace && MODE == 0)
+        k_sweep_win<true, MODE, true><<<grid, 256, smem, c->stream>>>(fp, mu, E->rp, E->col, E->val, N, rows, nrows,
+                 E->abits.as<u32>(), w.wW.as<u32>(), w.wC.as<u32>(), w.wD.as<uint2>(), nwin, w.wT.as<uint4>(), Dp, K,
+                 E->nonA.as<u32>(), stats, so);
+      else if (pk)
         k_sweep_win<true, MODE><<<grid, 256, smem, c->stream>>>(fp, mu, E->rp, E->col, E->val, N, rows, nrows,
                  E->abits.as<u32>(), w.wW.as<u32>(), w.wC.as<u32>(), w.wD.as<uint2>(), nwin, w.wT.as<uint4>(), Dp, K,
                  E->nonA.as<u32>(), stats, so);
@@ -1768,6 +1837,16 @@ static void launch_sweep(Ctx* c, const Fp& fp, f4b_echelon* E, const u32* rows, 
                  E->abits.as<u32>(), w.wW.as<u32>(), w.wC.as<u32>(), w.wD.as<uint2>(), nwin, w.wT.as<uint4>(), Dp, K,
                  E->nonA.as<u32>(), stats, so);
       check_cuda(cudaGetLastError(), "k_sweep_win");
+    }
+    if (strace) {
+      unsigned long long h[16];
+      check_cuda(cudaMemcpyAsync(h, trb.p, 128, cudaMemcpyDeviceToHost, c->stream), "d2h");
+      check_cuda(cudaStreamSynchronize(c->stream), "sync");
+      const double rows = (double)std::max(1ull, h[0]), wins = (double)std::max(1ull, h[1]);
+      fprintf(stderr, "[sweep%d] rows=%llu N=%u nA=%lld grid=%d windows/row=%.1f miss=%.2f cyc/window: find+mult %.0f (find %.0f v %.0f) bar %.0f apply+bar %.0f | tail/row %.0f\n",
+              MODE, h[0], N, (long long)E->nA, grid, wins / rows, h[2] / wins, h[3] / wins, h[7] / wins, h[8] / wins,
+              h[4] / wins, h[5] / wins, h[6] / rows);
+      release(c, trb);
     }
     win_release(c, w);
     return;
