@@ -112,6 +112,7 @@ typedef struct {
   int64_t dict_build_ns, row_assemble_ns; /* device time (CUDA events) */
   int64_t sort_passes, kernel_launches;
   int64_t row_lo, r_total; /* a sharded-compile slice: rows [row_lo, row_lo + r) of r_total */
+  int64_t validated;       /* 1: f4b_plan_validate's checks already ran inside the compile */
 } f4b_plan_info;
 
 /* compile_batch (symbolic.py:293-388): rows in select_rows order
@@ -145,6 +146,17 @@ int f4b_plan_free(f4b_plan* plan);
  * *length receives the byte count; the text is written when cap >= length
  * (call with out = NULL to size the buffer). */
 int f4b_plan_text(const f4b_plan* plan, int which, char* out, int64_t cap, int64_t* length);
+
+/* Asynchronous host download on the context's copy stream, behind the plan's
+ * completion (the next compile runs meanwhile): block = one host buffer of
+ * r+1 + 2M + N*W 64-bit words receiving row_ptr, col_ind (int64), val
+ * (uint64) and the reference dictionary keys [N][W] (as
+ * f4b_plan_download_ref_keys) — symbolic.py:383-388's host arrays, built by
+ * one kernel and copied in one D2H.  Page-locked memory copies at full link
+ * rate.  f4b_plan_wait blocks until the block is complete; freeing the plan
+ * waits too. */
+int f4b_plan_prefetch(f4b_plan* plan, uint64_t* block, int W);
+int f4b_plan_wait(f4b_plan* plan);
 
 /* LayoutPlan.validate (symbolic.py:125-163, called by compile_batch at
  * :383-387) on the device buffers: row_ptr tiles [0, M), rows nonempty with

@@ -38,7 +38,7 @@ u16p = C.POINTER(C.c_uint16)
 class PlanInfo(C.Structure):
     _fields_ = [(k, C.c_int64) for k in (
         "r", "N", "M", "closure_rounds", "n_closure_rows", "key_words", "lane_bits",
-        "dict_build_ns", "row_assemble_ns", "sort_passes", "kernel_launches", "row_lo", "r_total")]
+        "dict_build_ns", "row_assemble_ns", "sort_passes", "kernel_launches", "row_lo", "r_total", "validated")]
 
 
 class EchelonInfo(C.Structure):
@@ -83,6 +83,8 @@ SIGNATURES = {
     "f4b_plan_download_ref_keys": (C.c_int, [C.c_void_p, u64p]),
     "f4b_plan_text": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, i64p]),
     "f4b_plan_validate": (C.c_int, [C.c_void_p, i64p]),
+    "f4b_plan_prefetch": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),
+    "f4b_plan_wait": (C.c_int, [C.c_void_p]),
     "f4b_plan_poke": (C.c_int, [C.c_void_p, C.c_int, C.c_int64, C.c_uint32]),
     "f4b_csr_transpose": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, i64p, i64p, u64p, i64p, i64p, u64p]),
     "f4b_plan_left_apply": (C.c_int, [C.c_void_p, u64p, C.c_int64, u64p]),

@@ -176,7 +176,12 @@ static void prof_resolve(Ctx* c) {
 void plan_release(f4b_plan* pl) {
   if (!pl) return;
   Ctx* c = pl->ctx;
-  DBuf* bufs[] = {&pl->row_ptr, &pl->col_ind, &pl->val, &pl->dict, &pl->dict_exps, &pl->cl_basis, &pl->cl_shift, &pl->cl_round};
+  if (pl->pf_done) {  // a prefetch still reading the buffers (or writing the host block)
+    cudaEventSynchronize(pl->pf_done);
+    cudaEventDestroy(pl->pf_done);
+  }
+  DBuf* bufs[] = {&pl->row_ptr, &pl->col_ind, &pl->val, &pl->dict, &pl->dict_exps, &pl->cl_basis, &pl->cl_shift,
+                  &pl->cl_round, &pl->pf_wide};
   for (DBuf* b : bufs) release(c, *b);
   delete pl;
 }
@@ -350,6 +355,7 @@ int f4b_ctx_destroy(f4b_ctx* h) {
   pool_flush(c);
   if (c->h_stage) cudaFreeHost(c->h_stage);
   if (c->h_stat) cudaFreeHost(c->h_stat);
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   if (c->h_app) cudaFreeHost(c->h_app);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   for (cudaEvent_t& e : c->tev)
@@ -748,6 +754,7 @@ int f4b_plan_get_info(const f4b_plan* pl, f4b_plan_info* info) {
   info->row_assemble_ns = pl->asm_ns;
   info->sort_passes = pl->sort_passes;
   info->kernel_launches = pl->launches;
+  info->validated = pl->validated ? 1 : 0;
   return F4B_OK;
 }
 
@@ -866,6 +873,76 @@ __global__ void k_left_apply(Fp fp, const u32* __restrict__ rp, const u32* __res
     if (!vj) continue;
     for (u32 k = s + lane; k < e; k += 32) atomicAdd(Y + (size_t)col[k] * b + j, (unsigned long long)fp.mul(vj, val[k]));
   }
+}
+
+// Asynchronous host download: ONE staging block [r+1 | M | M | N*W] of
+// 64-bit words (row_ptr, col_ind, val widened; the reference dictionary keys)
+// built by one kernel on the context's copy stream behind the plan's
+// completion and copied in one D2H — the next compile_batch runs on the
+// main stream while the copy engine drains this one.  f4b_plan_wait blocks
+// until the host block is complete.
+__global__ void k_prefetch_pack(const u32* __restrict__ rp, long long r1, const u32* __restrict__ col,
+                                const u32* __restrict__ val, long long M, const uint16_t* __restrict__ ex,
+                                long long N, int n, int order, int W, unsigned long long* __restrict__ out) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  for (long long i = i0; i < r1; i += stride) out[i] = rp[i];
+  for (long long i = i0; i < M; i += stride) {
+    out[r1 + i] = col[i];
+    out[r1 + M + i] = val[i];
+  }
+  unsigned long long* kout = out + r1 + 2 * M;
+  const int head = order == 2 ? 0 : 32;
+  for (long long i = i0; i < N; i += stride) {  // k_ref_keys, reference monomials.py:131-148
+    const uint16_t* e = ex + i * n;
+    unsigned long long w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (order != 2) {
+      unsigned long long d = 0;
+      for (int v = 0; v < n; ++v) d += e[v];
+      w[0] |= d << 32;
+    }
+    for (int l = 0; l < n; ++l) {
+      const unsigned long long lane = order == 0 ? (unsigned long long)(0xFFFFu - e[n - 1 - l]) : (unsigned long long)e[l];
+      const int off = head + 16 * l;
+      w[off / 64] |= lane << (64 - (off % 64) - 16);
+    }
+    for (int q = 0; q < W; ++q) kout[i * W + q] = w[q];
+  }
+}
+
+int f4b_plan_prefetch(f4b_plan* pl, uint64_t* block, int W) {
+  if (!pl || !block || W < 1 || W > 8) return F4B_ERR_PRECONDITION;
+  API_BEGIN(pl->ctx)
+  Ctx* c = _c;
+  if (pl->pf_pending) fail(F4B_ERR_PRECONDITION, "plan prefetch already pending");
+  if (!c->copy_stream) check_cuda(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking), "stream");
+  if (!pl->pf_done) check_cuda(cudaEventCreateWithFlags(&pl->pf_done, cudaEventDisableTiming), "event");
+  const long long r1 = pl->r + 1, M = pl->M, N = pl->N;
+  const long long words = r1 + 2 * M + N * W;
+  ensure(c, pl->pf_wide, (size_t)words * 8);
+  cudaEvent_t ready = timing_event(c, 1);  // the plan and the staging allocation complete on the main stream
+  check_cuda(cudaEventRecord(ready, c->stream), "event");
+  check_cuda(cudaStreamWaitEvent(c->copy_stream, ready, 0), "wait");
+  const long long most = std::max({r1, M, N, 1ll});
+  const int g = (int)std::min<long long>((most + 255) / 256, (long long)c->num_sms * 4);
+  k_prefetch_pack<<<g, 256, 0, c->copy_stream>>>(pl->row_ptr.as<u32>(), r1, pl->col_ind.as<u32>(), pl->val.as<u32>(),
+                                                 M, pl->dict_exps.as<uint16_t>(), N, c->n_vars, c->order, W,
+                                                 pl->pf_wide.as<unsigned long long>());
+  check_cuda(cudaGetLastError(), "k_prefetch_pack");
+  check_cuda(cudaMemcpyAsync(block, pl->pf_wide.p, (size_t)words * 8, cudaMemcpyDeviceToHost, c->copy_stream), "d2h");
+  check_cuda(cudaEventRecord(pl->pf_done, c->copy_stream), "event");
+  pl->pf_pending = true;
+  API_END
+}
+
+int f4b_plan_wait(f4b_plan* pl) {
+  if (!pl) return F4B_ERR_PRECONDITION;
+  API_BEGIN(pl->ctx)
+  if (pl->pf_pending) {
+    check_cuda(cudaEventSynchronize(pl->pf_done), "prefetch wait");
+    pl->pf_pending = false;
+  }
+  API_END
 }
 
 int f4b_plan_left_apply(const f4b_plan* pl, const uint64_t* V, int64_t b, uint64_t* Y) {

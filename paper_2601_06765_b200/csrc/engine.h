@@ -90,6 +90,7 @@ struct Ctx {
     DBuf raw;
   } pend;
   cudaStream_t stream = 0;
+  cudaStream_t copy_stream = nullptr;  // plan prefetches (created on first use)
   int num_sms = 148;
   // path selection (f4b_ctx_set_option); the defaults are the measured best
   // paths, the others are the fallbacks the automatic choice takes when a
@@ -199,6 +200,11 @@ struct f4b_plan {
   // r_total final rows; the closure metadata covers all ncl_all closure rows
   long long row_lo = 0, r_total = -1, ncl_all = -1;
   long long n_closure() const { return ncl_all >= 0 ? ncl_all : r - r0; }
+  // asynchronous host download (f4b_plan_prefetch): staging and completion
+  f4b::DBuf pf_wide;
+  cudaEvent_t pf_done = nullptr;
+  bool pf_pending = false;
+  bool validated = false;  // the compile ran f4b_plan_validate's checks (fused, io.cu)
 };
 
 struct f4b_echelon;
@@ -206,6 +212,11 @@ struct f4b_echelon;
 namespace f4b {
 void plan_release(f4b_plan* pl);
 void ref_keys_device(Ctx* c, const f4b_plan* pl, unsigned long long* out, int W);  // capi.cu
+// io.cu: LayoutPlan.validate on the device with the sizes read on the device
+// (sz[0] = r, sz[2] = M, sz[3] = N: the LoopOut layout), result in *flag
+// (~0 = valid); validate_message turns a flag into the reference's message
+void validate_launch_dev(Ctx* c, const f4b_plan* pl, const uint32_t* sz, unsigned long long* flag);
+std::string validate_message(unsigned long long f, long long row_lo);
 }
 
 namespace f4b {

@@ -2567,7 +2567,12 @@ static void compile_rank_fused(Ctx* c, const KeyFmt& f, int D, long long r0, con
   }
   mark("launched");
   check_cuda(cudaEventRecord(ev1, c->stream), "event record");
-  check_cuda(cudaMemcpyAsync(c->h_stat, dc, sizeof(DevCounters) + sizeof(LoopOut), cudaMemcpyDeviceToHost, c->stream),
+  // LayoutPlan.validate (symbolic.py:383-387) fused behind the kernel: sizes
+  // from LoopOut on the device, its flag read back with the counters
+  unsigned long long* vflag = reinterpret_cast<unsigned long long*>(d_out + 1);
+  validate_launch_dev(c, pl, reinterpret_cast<const uint32_t*>(d_out), vflag);
+  check_cuda(cudaMemcpyAsync(c->h_stat, dc, sizeof(DevCounters) + sizeof(LoopOut) + 8, cudaMemcpyDeviceToHost,
+                             c->stream),
              "d2h");
   check_cuda(cudaStreamSynchronize(c->stream), "sync");
   mark("synced");
@@ -2629,6 +2634,10 @@ static void compile_rank_fused(Ctx* c, const KeyFmt& f, int D, long long r0, con
   pl->asm_ns = (int64_t)asm_ns;
   pl->dict_ns = (int64_t)std::max(0.0, ms * 1e6 - asm_ns);
   pl->launches = c->launches;
+  unsigned long long vf;
+  memcpy(&vf, reinterpret_cast<unsigned char*>(c->h_stat) + sizeof(DevCounters) + sizeof(LoopOut), 8);
+  if (vf != ~0ull) fail(F4B_ERR_PROPERTY, validate_message(vf, pl->row_lo));
+  pl->validated = true;
 }
 
 template <int KW>

@@ -157,7 +157,7 @@ F4B_DEV bool mono_gt(const uint16_t* a, const uint16_t* b, int n, int order) {
   return false;
 }
 
-__global__ void k_validate(const u32* __restrict__ rp, long long r, const u32* __restrict__ col,
+F4B_DEV void validate_body(const u32* __restrict__ rp, long long r, const u32* __restrict__ col,
                            const u32* __restrict__ val, long long M, long long N, u32 p,
                            const uint16_t* __restrict__ dex, int n, int order, unsigned long long* __restrict__ flag) {
   const long long stride = (long long)gridDim.x * blockDim.x;
@@ -184,6 +184,42 @@ __global__ void k_validate(const u32* __restrict__ rp, long long r, const u32* _
   for (long long k = t0; k + 1 < N; k += stride)
     if (!mono_gt(dex + k * n, dex + (k + 1) * n, n, order)) f = min(f, V_DICT | (unsigned long long)k);
   if (f != ~0ull) atomicMin(flag, f);
+}
+
+__global__ void k_validate(const u32* __restrict__ rp, long long r, const u32* __restrict__ col,
+                           const u32* __restrict__ val, long long M, long long N, u32 p,
+                           const uint16_t* __restrict__ dex, int n, int order, unsigned long long* __restrict__ flag) {
+  validate_body(rp, r, col, val, M, N, p, dex, n, order, flag);
+}
+
+// sizes on the device (behind the compile kernel, no host round trip)
+__global__ void k_validate_dev(const u32* __restrict__ rp, const u32* __restrict__ col, const u32* __restrict__ val,
+                               const u32* __restrict__ sz, u32 p, const uint16_t* __restrict__ dex, int n, int order,
+                               unsigned long long* __restrict__ flag) {
+  if (sz[6]) return;  // LoopOut.flags: an aborted (re-run) compile, sizes not final
+  validate_body(rp, sz[0], col, val, sz[2], sz[3], p, dex, n, order, flag);
+}
+
+void validate_launch_dev(Ctx* c, const f4b_plan* pl, const uint32_t* sz, unsigned long long* flag) {
+  check_cuda(cudaMemsetAsync(flag, 0xFF, 8, c->stream), "memset");
+  F4B_LAUNCH(c, k_validate_dev, (unsigned)(c->num_sms * 4), 256, 0, pl->row_ptr.as<u32>(), pl->col_ind.as<u32>(),
+             pl->val.as<u32>(), sz, c->p, pl->dict_exps.as<uint16_t>(), c->n_vars, c->order, flag);
+}
+
+std::string validate_message(unsigned long long f, long long row_lo) {
+  const unsigned long long kind = f >> 40, idx = f & ((1ull << 40) - 1);
+  const long long row = row_lo + (long long)(idx >> 2);
+  switch (kind) {
+    case 1: return "row_ptr does not tile the value stream";
+    case 2: return "negative row segment length";
+    case 3:
+      return (idx & 3) == 0 ? "empty row " + std::to_string(row) + " (basis members are nonzero)"
+             : (idx & 3) == 1 ? "row " + std::to_string(row) + " columns not strictly ascending"
+                              : "row " + std::to_string(row) + " column out of range";
+    case 4: return "zero value stored in plan";
+    case 5: return "dictionary keys not strictly descending";
+    default: return "value not reduced mod p at term " + std::to_string(idx);
+  }
 }
 
 }  // namespace f4b
@@ -234,24 +270,7 @@ int f4b_plan_validate(const f4b_plan* pl, int64_t* violation) {
     check_cuda(cudaStreamSynchronize(c->stream), "sync");
     release(c, fl);
     if (violation) *violation = f == ~0ull ? -1 : (int64_t)f;
-    if (f != ~0ull) {
-      const unsigned long long kind = f >> 40, idx = f & ((1ull << 40) - 1);
-      const long long row = pl->row_lo + (long long)(idx >> 2);
-      std::string m;
-      switch (kind) {
-        case 1: m = "row_ptr does not tile the value stream"; break;
-        case 2: m = "negative row segment length"; break;
-        case 3:
-          m = (idx & 3) == 0 ? "empty row " + std::to_string(row) + " (basis members are nonzero)"
-              : (idx & 3) == 1 ? "row " + std::to_string(row) + " columns not strictly ascending"
-                               : "row " + std::to_string(row) + " column out of range";
-          break;
-        case 4: m = "zero value stored in plan"; break;
-        case 5: m = "dictionary keys not strictly descending"; break;
-        default: m = "value not reduced mod p at term " + std::to_string(idx); break;
-      }
-      fail(F4B_ERR_PROPERTY, m);
-    }
+    if (f != ~0ull) fail(F4B_ERR_PROPERTY, validate_message(f, pl->row_lo));
   } catch (const Error& e) {
     c->last_error = e.msg;
     return e.code;

@@ -45,6 +45,10 @@ def _current_device() -> int:
     return torch.cuda.current_device() if torch.cuda.is_available() else 0
 
 
+def _free_plan(free_fn, handle, keep):
+    free_fn(handle)  # waits for a pending prefetch before the host block in `keep` is released
+
+
 class DevicePlan:
     """Handle of an ``f4b_plan`` (device CSR + dictionary + closure rows)."""
 
@@ -73,6 +77,31 @@ class DevicePlan:
             self.engine.ctx.check(self.engine.lib.f4b_plan_download_ref_keys(self.h, ptr(out, C.c_uint64)),
                                   "plan keys")
         return out
+
+    def prefetch(self, n_key_words):
+        """Start the host download of (row_ptr, col_ind, val) and the
+        reference dictionary keys on the copy stream (f4b_plan_prefetch: one
+        kernel, one D2H into one page-locked block); ``prefetched()`` waits
+        and returns the views."""
+        e = self.engine
+        r, M, N = self.info["r"], self.info["M"], self.info["N"]
+        blk = host_empty(r + 1 + 2 * M + N * n_key_words, np.int64)
+        e.ctx.check(e.lib.f4b_plan_prefetch(self.h, blk.ctypes.data, int(n_key_words)), "plan prefetch")
+        self._pf = (blk, n_key_words)
+        # the host block must outlive any pending copy: the finalizer (which
+        # frees the plan, waiting for the copy) keeps it alive
+        self._fin.detach()
+        self._fin = weakref.finalize(self, _free_plan, e.lib.f4b_plan_free, self.h, blk)
+
+    def prefetched(self):
+        if getattr(self, "_pf", None) is None:
+            return None
+        self.engine.ctx.check(self.engine.lib.f4b_plan_wait(self.h), "plan wait")
+        blk, W = self._pf
+        r, M, N = self.info["r"], self.info["M"], self.info["N"]
+        o = r + 1 + 2 * M
+        return {"row_ptr": blk[:r + 1], "col_ind": blk[r + 1:r + 1 + M], "val": blk[r + 1 + M:o].view(np.uint64),
+                "dict_keys": blk[o:o + N * W].view(np.uint64).reshape(N, W)}
 
     def validate(self):
         """LayoutPlan.validate (reference symbolic.py:125-163) on the device

@@ -104,6 +104,12 @@ class LayoutPlan:
             raise AttributeError(name)
         dev = self.device
         n = self.ring.n_vars
+        pf = dev.prefetched() if name in ("row_ptr", "col_ind", "val", "dict_keys") else None
+        if pf is not None and (name != "dict_keys" or pf["dict_keys"] is not None):
+            for k in ("row_ptr", "col_ind", "val", "dict_keys"):
+                if pf[k] is not None:
+                    self._host[k] = pf[k]
+            return self._host[name]
         if name in ("row_ptr", "col_ind", "val"):
             got = dev.download(arrays=True, dict_exps=False, closure=False)
             for k in ("row_ptr", "col_ind", "val"):
@@ -118,6 +124,15 @@ class LayoutPlan:
                                      got["cl_round"].tolist()))
             self._host["row_meta"] = self._input_rows + extra
         return self._host[name]
+
+    def prefetch(self) -> "LayoutPlan":
+        """Start downloading the host arrays (row_ptr, col_ind, val,
+        dict_keys) of a device plan in the background (copy stream); the
+        attributes then wait for it instead of downloading.  Lets a caller
+        compile the next batch while this one's arrays cross PCIe."""
+        if self.device is not None and not self._host:
+            self.device.prefetch(self.ring.n_key_words)
+        return self
 
     def dict_exps(self) -> np.ndarray:
         """Exponent rows of the dictionary, descending (column order)."""
@@ -142,6 +157,12 @@ class LayoutPlan:
     def n_cols(self) -> int:
         return self.counters.N if self.device is not None else len(self.dict_keys)
 
+    def _check_device_counters(self):
+        c, info = self.counters, self.device.info
+        if not (c.r == info["r"] and c.N == info["N"] and c.M == info["M"] and c.nnz == c.M
+                and c.keys_emitted == c.M and c.keys_generated_total >= c.M):
+            raise PropertyViolationError(f"counters inconsistent: {c}")
+
     def validate(self):
         """Structural invariants (reference :125-163); PropertyViolationError.
 
@@ -152,9 +173,7 @@ class LayoutPlan:
         c = self.counters
         if self.device is not None:
             self.device.validate()
-            if not (c.r == self.device.info["r"] and c.N == self.device.info["N"] and c.M == self.device.info["M"]
-                    and c.nnz == c.M and c.keys_emitted == c.M and c.keys_generated_total >= c.M):
-                raise PropertyViolationError(f"counters inconsistent: {c}")
+            self._check_device_counters()
             return
         rp, ci, va, dk = self.row_ptr, self.col_ind, self.val, self.dict_keys
         if not (rp[0] == 0 and rp[-1] == len(ci) == len(va)):
@@ -260,7 +279,12 @@ def compile_batch(rows, basis: SoaPolySet, closure: Closure = Closure.ONE_STEP_R
                             keys_emitted=M, keys_generated_total=M)
     timings = {"dict_build_ns": info["dict_build_ns"], "row_assemble_ns": info["row_assemble_ns"]}
     plan = LayoutPlan(ring, counters=counters, timings_ns=timings, device=dev, input_rows=rows)
-    plan.validate()  # reference :383-387, on the device
+    # reference :383-387, on the device: fused into the compile launch
+    # (info["validated"]) or one f4b_plan_validate pass
+    if info.get("validated"):
+        plan._check_device_counters()
+    else:
+        plan.validate()
     return plan
 
 

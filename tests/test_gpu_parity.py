@@ -749,6 +749,27 @@ def test_device_validate_matches_host(cuda, which, fault):
     assert str(host_err.value) in str(dev_err.value)
 
 
+def test_plan_prefetch_matches_download(cuda):
+    """LayoutPlan.prefetch (f4b_plan_prefetch on the copy stream, overlapped
+    with the next compile) returns the same host arrays and dictionary keys
+    as the synchronous download (cyclic-8 step 10 compiled twice, the second
+    compile issued while the first plan's arrays are in flight)."""
+    snaps = load_snapshots("cyclic8_p32003")
+    gold = load_golden("cyclic8_p32003")
+    ring, st = state_from_snapshot(snaps[10])
+    spec, _ = select_batch(st)
+    soa = st.soa()
+    rows = select_rows(spec, soa)
+    a = compile_batch(rows, soa, Closure.ONE_STEP_REDUCTION).prefetch()
+    b = compile_batch(rows, soa, Closure.ONE_STEP_REDUCTION)  # runs while a's arrays download
+    for k in ("row_ptr", "col_ind", "val", "dict_keys"):
+        assert np.array_equal(getattr(a, k), getattr(b, k)), k
+    assert a.col_ind.dtype == np.int64 and a.val.dtype == np.uint64
+    assert plan_digest(a) == gold["steps"][10]["plan_sha256"]
+    c = compile_batch(rows, soa, Closure.ONE_STEP_REDUCTION).prefetch()
+    del c  # freed with the copy pending: the free waits for it
+
+
 def test_snapshot_resume_gpu(cuda, tmp_path):
     """A binary state snapshot taken mid-run (snapshot.py) resumes the GPU F4
     loop to the reference's final reduced basis (cyclic-6)."""

@@ -37,33 +37,50 @@ def main():
 
     f_key, f_coeff, f_exps = pinned(final.mon_key), pinned(final.coeff), pinned(final.exps)
     n = ring.n_vars
+    from paper_2601_06765_b200.symbolic import LayoutPlan, PlanCounters
+
     for rep in range(3):
-        acc = dict.fromkeys(("sync_basis", "rows", "compile", "row_ptr_col_val", "dict_keys"), 0.0)
+        acc = dict.fromkeys(("sync_basis", "rows", "compile", "validate", "prefetch", "consume"), 0.0)
         M = 0
         torch.cuda.synchronize()
         t_all = time.perf_counter()
         eng.clear_basis()
-        for b in batches:
-            nb_, nt = b["n_basis"], b["n_terms"]
-            soa = SoaPolySet(ring, f_key[:nt], f_coeff[:nt], final.offset[:nb_ + 1], final.length[:nb_],
-                             f_exps[:nt])
+        pending = None
+        for b in batches + [None]:
             t0 = time.perf_counter()
-            eng.sync_basis(soa)
+            plan = None
+            if b is not None:
+                nb_, nt = b["n_basis"], b["n_terms"]
+                soa = SoaPolySet(ring, f_key[:nt], f_coeff[:nt], final.offset[:nb_ + 1], final.length[:nb_],
+                                 f_exps[:nt])
+                eng.sync_basis(soa)
             t1 = time.perf_counter()
-            rows = b["rows"]
-            rb = np.fromiter((r.basis_index for r in rows), dtype=np.int64, count=len(rows))
-            sh = np.asarray([r.shift for r in rows], dtype=np.int64).reshape(len(rows), n)
+            if b is not None:
+                rows = b["rows"]
+                rb = np.fromiter((r.basis_index for r in rows), dtype=np.int64, count=len(rows))
+                sh = np.asarray([r.shift for r in rows], dtype=np.int64).reshape(len(rows), n)
             t2 = time.perf_counter()
-            dev = eng.compile(rb, sh, True, None, DICT_CAP)
+            if b is not None:
+                dev = eng.compile(rb, sh, True, None, DICT_CAP)
             t3 = time.perf_counter()
-            got = dev.download(arrays=True, dict_exps=False, closure=False)
+            if b is not None:
+                info = dev.info
+                plan = LayoutPlan(ring, counters=PlanCounters(r=info["r"], N=info["N"], M=info["M"], nnz=info["M"],
+                                                              keys_emitted=info["M"], keys_generated_total=info["M"]),
+                                  device=dev, input_rows=rows)
+                plan.validate()
             t4 = time.perf_counter()
-            dk = dev.download_ref_keys(ring.n_key_words)
+            if plan is not None:
+                plan.prefetch()
             t5 = time.perf_counter()
-            for k, v in zip(acc, (t1 - t0, t2 - t1, t3 - t2, t4 - t3, t5 - t4)):
+            if pending is not None:
+                _ = (pending.row_ptr, pending.col_ind, pending.val, pending.dict_keys)
+            t6 = time.perf_counter()
+            pending = plan
+            for k, v in zip(acc, (t1 - t0, t2 - t1, t3 - t2, t4 - t3, t5 - t4, t6 - t5)):
                 acc[k] += v
-            M += b["M"]
-            del got, dk, dev
+            if b is not None:
+                M += b["M"]
         torch.cuda.synchronize()
         tot = time.perf_counter() - t_all
         print({k: round(v * 1e3, 2) for k, v in acc.items()}, "total_ms", round(tot * 1e3, 2), "nnz/s",
