@@ -597,6 +597,21 @@ def test_resident_operator_matches_numpy(cuda, shape):
         acc = (apply_b(acc) + np.uint64(cc) * v) % P
     assert np.array_equal(op.horner(g, V[:, 0]), acc[:, 0])
     assert np.array_equal(op.apply(V), apply_b(V))
+    # the power loop (stop before the first zero vector) on a nilpotent
+    # operator and on this one (which runs all max_steps)
+    N = np.triu(rng.integers(0, p, (c, c), dtype=np.uint64) * (rng.random((c, c)) < 0.3), 1)
+    Nc = csr_from_dense(N, m)
+    nop = _engine_for(m).operator(c, c, Nc.row_ptr, Nc.col_ind, Nc.val, False)
+    for o, app, steps_max in ((nop, lambda x: spmm(Nc, x), 3 * c), (op, apply_b, 7)):
+        x = V[:, 0].copy()
+        kept = 0
+        for _ in range(steps_max):
+            y = app(x.reshape(-1, 1))[:, 0]
+            if not y.any():
+                break
+            x, kept = y, kept + 1
+        got, taken = o.power_until_zero(V[:, 0], steps_max)
+        assert taken == kept and np.array_equal(got, x)
 
 
 def test_verify_kernel_syzygy_device(cuda):
