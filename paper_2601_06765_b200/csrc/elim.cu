@@ -1966,8 +1966,11 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
     static int bpp = -1;
     if (bpp < 0) check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpp, k_psge_prep, 256, 0), "occupancy");
     // every SM (a grid sized by the batch, ~2K rows per CTA, was measured
-    // slower: 0.9 -> 1.2 ms of k_psge_prep per cyclic-8 step)
-    const int GP = c->num_sms * std::max(1, std::min(bpp, 2));
+    // slower: 0.9 -> 1.2 ms of k_psge_prep per cyclic-8 step); F4B_PREP_G
+    // overrides (experiments)
+    static const int gp_env = getenv("F4B_PREP_G") ? atoi(getenv("F4B_PREP_G")) : 0;
+    const int GP = gp_env > 0 ? std::min(gp_env, c->num_sms * std::max(1, std::min(bpp, 2)))
+                              : c->num_sms * std::max(1, std::min(bpp, 2));
     ensure(c, pcnt, (size_t)GP * sizeof(u32) + sizeof(PrepOut) + 16);
     PrepOut* d_out = reinterpret_cast<PrepOut*>(pcnt.as<u32>() + GP);
     u32 ru = (u32)r, Nu = (u32)N;

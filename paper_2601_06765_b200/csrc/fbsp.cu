@@ -2462,11 +2462,13 @@ static void compile_rank_fused(Ctx* c, const KeyFmt& f, int D, long long r0, con
                "occupancy");
   const int bps_cached = bps_by_step[lstep];
   static const int bps_max = getenv("F4B_LOOP_BPS") ? atoi(getenv("F4B_LOOP_BPS")) : 2;
-  // every SM, even for small batches: fewer CTAs measured slower (the closure
-  // rounds' search and ranking spread over all warps)
+  // batches below ~150k input terms: one CTA per SM (cheaper grid barriers;
+  // measured 5-20 us faster per cyclic-8 batch up to ~400k final terms),
+  // larger ones two per SM.  Fewer than one per SM was slower (the closure
+  // rounds' search and ranking spread over all warps).
   static const int g_env = getenv("F4B_FBSP_G") ? atoi(getenv("F4B_FBSP_G")) : 0;
   const int G_full = c->num_sms * std::max(1, std::min(bps_cached, bps_max));
-  const int G = g_env > 0 ? std::min(g_env, G_full) : G_full;
+  const int G = g_env > 0 ? std::min(g_env, G_full) : (M0 < 150000u ? std::min(c->num_sms, G_full) : G_full);
   const size_t W = (size_t)G * (CL_THREADS / 32);
   ensure(c, c->loop_scratch, (2 * W + 16) * sizeof(u32));
   // presence maps dict | done | newbits: zero on entry (kept zero by the
