@@ -1227,6 +1227,7 @@ struct DblkState {
   u32 t2a_us, t2b_us, t2c_us, pad;                         // phase 2 split: window load | forward | back + inverse
   u32 offers, distinct;                                    // trace: offers and distinct offered leads, summed over blocks
   u32 fc1, fc2, fc3, fcn;  // trace: forward loop kilocycles (min + barrier | update | barrier), iterations
+  u32 q1, q2, q3;          // trace (CTA 1, us): phase-3 setup + coefficients | apply | offers
 };
 F4B_DEV unsigned long long gtimer() {
   unsigned long long t;
@@ -1237,7 +1238,11 @@ static constexpr int DB_THREADS = 512;
 static constexpr int DB_NP = 32;  // max rows per block (one per lane of the selection warp)
 static constexpr int DB_W = 128;  // window of the pivot search
 static constexpr int DB_G = 8;    // rows per apply group
-template <bool SMALLP>
+// SR: this CTA's D' rows live in shared memory for the whole kernel (phase 3
+// reads and writes them there); a row goes back to Dp only when it is one of
+// the block's first DB_NP offers — CTA 0's window and the pivot rows are read
+// from Dp, and only candidates are ever read there.
+template <bool SMALLP, bool SR>
 __global__ void __launch_bounds__(DB_THREADS) k_dense_blk(Fp fp, u32* __restrict__ Dp, u32 R, u32 K, u32 rpc, u32 maxt,
                                                           u32* __restrict__ lead, u32* __restrict__ cand,
                                                           u32* __restrict__ Bm, u32* __restrict__ colpiv,
@@ -1282,18 +1287,23 @@ __global__ void __launch_bounds__(DB_THREADS) k_dense_blk(Fp fp, u32* __restrict
     return (u32)(a % p);
   };
   u32 it_no = 1;  // block number (trace: distinct offered leads per block)
-  auto offer = [&](u32 row, u32 l) {
+  auto offer = [&](u32 row, u32 l) -> bool {
     const u32 s = atomicAdd(&st->cnt, 1u);
     if (s < (u32)DB_NP) cand[s] = row;
     if (dflag) {
       atomicAdd(&st->offers, 1u);
       if (atomicMax(dflag + l, it_no) < it_no) atomicAdd(&st->distinct, 1u);
     }
+    return s < (u32)DB_NP;
   };
   u32* s_f = s_lead + rpc;  // [maxt] first nonzero column of each task
+  // SR: [rpc][K] this CTA's rows, after the window / task area
+  u32* s_rows = smem + max((u32)(DB_NP * (DB_W + 32)), maxt * (DB_NP + 3) + rpc);
+  __shared__ u32 s_wbn, s_wb[DB_NP];  // SR: rows to write back (offered into the candidate slots)
   u32 ro = 0;
   auto task_row = [&](u32 td) -> u32* {
     const u32 kind = td >> 30, idx = td & 0x3FFFFFFFu;
+    if (SR && kind == 0) return s_rows + (size_t)idx * K;
     return kind == 0 ? Dp + (size_t)(lo + idx) * K : Bm + (size_t)(kind == 1 ? idx : ro + idx) * K;
   };
   // prologue: leads of this CTA's rows (contiguous in D'), first offers
@@ -1311,8 +1321,10 @@ __global__ void __launch_bounds__(DB_THREADS) k_dense_blk(Fp fp, u32* __restrict
       }
 #pragma unroll
       for (int h = 0; h < 8; ++h) {
+        const u32 e = e0 + h * DB_THREADS;
+        if (SR && e < tot) s_rows[e] = v[h];
         if (v[h]) {
-          const u32 e = e0 + h * DB_THREADS, r = e / K, q = e - r * K;
+          const u32 r = e / K, q = e - r * K;
           if (q < s_lead[r]) atomicMin(&s_lead[r], q);
         }
       }
@@ -1321,7 +1333,7 @@ __global__ void __launch_bounds__(DB_THREADS) k_dense_blk(Fp fp, u32* __restrict
   __syncthreads();
   for (u32 r = tid; r < nr; r += DB_THREADS) {
     lead[lo + r] = s_lead[r];
-    if (s_lead[r] < K) offer(lo + r, s_lead[r]);
+    if (s_lead[r] < K) offer(lo + r, s_lead[r]);  // Dp still holds the rows here
   }
   unsigned long long t2 = 0, t3 = 0, t3a = 0, tm = 0, t2a = 0, t2b = 0, t2c = 0;
   while (true) {
@@ -1525,6 +1537,7 @@ __global__ void __launch_bounds__(DB_THREADS) k_dense_blk(Fp fp, u32* __restrict
       tm = t;
     }
     grid.sync();
+    const unsigned long long qa = dflag && bid == 1 && tid == 0 ? gtimer() : 0ull;
     const u32 np = __ldcg(&st->np);
     ro = __ldcg(&st->rho_old);
     if (np == 0) break;
@@ -1557,8 +1570,8 @@ __global__ void __launch_bounds__(DB_THREADS) k_dense_blk(Fp fp, u32* __restrict
       if (kind == 2) {
         m = (u32)lane < np ? s_T[idx][lane] : 0u;
       } else {
-        const u32* x = kind == 0 ? Dp + (size_t)(lo + idx) * K : Bm + (size_t)idx * K;
-        const u32 xl = (u32)lane < np ? __ldcg(x + s_wcol[lane]) : 0u;
+        const u32* x = task_row(td);
+        const u32 xl = (u32)lane < np ? (SR && kind == 0 ? x[s_wcol[lane]] : __ldcg(x + s_wcol[lane])) : 0u;
         u64 acc = 0;
         for (u32 k = 0; k < np; ++k) {
           const u32 xk = __shfl_sync(FULL, xl, k);
@@ -1573,6 +1586,7 @@ __global__ void __launch_bounds__(DB_THREADS) k_dense_blk(Fp fp, u32* __restrict
     __syncthreads();
     const u32 na = s_na;
     if (bid == 0 && tid == 0) t3a += gtimer() - tm;
+    const unsigned long long qb = dflag && bid == 1 && tid == 0 ? gtimer() : 0ull;
     // one pass over the columns: the block's np rows are loaded once per
     // column (one L2 round trip) and applied to every active task
     for (u32 t = tid; t < nt; t += DB_THREADS) s_f[t] = K;
@@ -1591,7 +1605,7 @@ __global__ void __launch_bounds__(DB_THREADS) k_dense_blk(Fp fp, u32* __restrict
           xb[r] = 0;
           if ((u32)r < ng) {
             const u32 td = s_task[s_act[g0 + r]];
-            if ((td >> 30) != 2) xb[r] = __ldcg(task_row(td) + q);
+            if ((td >> 30) != 2) xb[r] = SR && (td >> 30) == 0 ? task_row(td)[q] : __ldcg(task_row(td) + q);
           }
         }
 #pragma unroll
@@ -1630,13 +1644,35 @@ __global__ void __launch_bounds__(DB_THREADS) k_dense_blk(Fp fp, u32* __restrict
     }
     __syncthreads();
     if (bid == 0 && tid == 0) t3 += gtimer() - tm;
+    const unsigned long long qc = dflag && bid == 1 && tid == 0 ? gtimer() : 0ull;
     // 1 (next iteration): offers of the live rows
     ++it_no;
+    if (SR) {
+      if (tid == 0) s_wbn = 0;
+      __syncthreads();
+    }
     for (u32 r = tid; r < nr; r += DB_THREADS) {
       const u32 l = s_lead[r];
       if (l <= K) {  // K + 1 = consumed
         lead[lo + r] = l;
-        if (l < K) offer(lo + r, l);
+        if (l < K && offer(lo + r, l) && SR) s_wb[atomicAdd(&s_wbn, 1u)] = r;
+      }
+    }
+    if (SR) {  // candidates are read from Dp (CTA 0's window, the pivot rows)
+      __syncthreads();
+      const u32 nwb = s_wbn;
+      for (u32 e = tid; e < nwb * K; e += DB_THREADS) {
+        const u32 i = e / K, q = e - i * K, r = s_wb[i];
+        Dp[(size_t)(lo + r) * K + q] = s_rows[(size_t)r * K + q];
+      }
+    }
+    if (dflag && bid == 1) {
+      __syncthreads();
+      if (tid == 0) {
+        const unsigned long long qd = gtimer();
+        atomicAdd(&st->q1, (u32)((qb - qa) / 1000));
+        atomicAdd(&st->q2, (u32)((qc - qb) / 1000));
+        atomicAdd(&st->q3, (u32)((qd - qc) / 1000));
       }
     }
   }
@@ -2030,10 +2066,9 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
       static int blk_occ = -1;
       static bool blk_attr = false;
       if (!blk_attr) {
-        check_cuda(cudaFuncSetAttribute(k_dense_blk<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024),
-                   "attr");
-        check_cuda(cudaFuncSetAttribute(k_dense_blk<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024),
-                   "attr");
+        for (const void* kf : {(const void*)k_dense_blk<true, false>, (const void*)k_dense_blk<false, false>,
+                               (const void*)k_dense_blk<true, true>, (const void*)k_dense_blk<false, true>})
+          check_cuda(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "attr");
         blk_attr = true;
       }
       const long long rmaxb = std::max<long long>(1, std::min(R, K));
@@ -2042,15 +2077,19 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
       const long long maxt = rpc + (rmaxb + G - 1) / G;
       const long long Kp = (K + 3) & ~3ll;
       const long long maxt3 = maxt + (DB_NP + G - 1) / G;
-      const size_t smem_b = (size_t)std::max<long long>(DB_NP * (DB_W + 32), maxt3 * (DB_NP + 3) + rpc) * 4;
+      size_t smem_b = (size_t)std::max<long long>(DB_NP * (DB_W + 32), maxt3 * (DB_NP + 3) + rpc) * 4;
       (void)Kp;
+      // this CTA's rows resident in shared memory when they fit
+      static const bool sr_off = getenv("F4B_DENSE_NOSR") != nullptr;  // experiments
+      const bool sr = !sr_off && smem_b + (size_t)rpc * K * 4 <= 196 * 1024;
+      if (sr) smem_b += (size_t)rpc * K * 4;
       if (blk_occ < 0) {
         int o = 0;
-        check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_dense_blk<false>, DB_THREADS, 160 * 1024),
+        check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_dense_blk<false, true>, DB_THREADS, 196 * 1024),
                    "occupancy");
         blk_occ = o;
       }
-      if (blk_occ >= 1 && G <= c->num_sms && smem_b <= 160 * 1024 && rpc * K < (1ll << 32)) {
+      if (blk_occ >= 1 && G <= c->num_sms && smem_b <= 196 * 1024 && rpc * K < (1ll << 32)) {
         DBuf Bm, colp, lead_b, cand_b, gl, gT, stt, ordr;
         ensure(c, Bm, (size_t)rmaxb * K * sizeof(u32));
         ensure(c, colp, (size_t)K * sizeof(u32));
@@ -2084,7 +2123,8 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
                          &dpivp, &rkp, &ordp, &dflp};
         {
           ProfScope ps(c, "k_dense_blk");
-          const void* kf = c->p < 65536u ? (const void*)k_dense_blk<true> : (const void*)k_dense_blk<false>;
+          const void* kf = c->p < 65536u ? (sr ? (const void*)k_dense_blk<true, true> : (const void*)k_dense_blk<true, false>)
+                                          : (sr ? (const void*)k_dense_blk<false, true> : (const void*)k_dense_blk<false, false>);
           mark("dense issue");
           check_cuda(cudaLaunchCooperativeKernel(kf, (int)G, DB_THREADS, argsb, smem_b, c->stream), "k_dense_blk");
           mark("dense launched");
@@ -2094,9 +2134,9 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
           DblkState hs;
           check_cuda(cudaMemcpyAsync(&hs, stt.p, sizeof(hs), cudaMemcpyDeviceToHost, c->stream), "d2h");
           check_cuda(cudaStreamSynchronize(c->stream), "sync");
-          fprintf(stderr, "[blk] R=%lld K=%lld G=%lld rpc=%lld rank=%u iters=%u t2=%uus (load %u fwd %u back %u) t3=%uus (setup %uus) offers=%u distinct=%u fwd_kcyc(min+bar %u upd %u bar %u n %u)\n",
+          fprintf(stderr, "[blk] R=%lld K=%lld G=%lld rpc=%lld rank=%u iters=%u t2=%uus (load %u fwd %u back %u) t3=%uus (setup %uus) offers=%u distinct=%u fwd_kcyc(min+bar %u upd %u bar %u n %u) cta1(setup+coef %u apply %u offers %u us)\n",
                   (long long)R, (long long)K, (long long)G, (long long)rpc, hs.rho, hs.iters, hs.t2_us, hs.t2a_us,
-                  hs.t2b_us, hs.t2c_us, hs.t3_us, hs.t3a_us, hs.offers, hs.distinct, hs.fc1, hs.fc2, hs.fc3, hs.fcn);
+                  hs.t2b_us, hs.t2c_us, hs.t3_us, hs.t3a_us, hs.offers, hs.distinct, hs.fc1, hs.fc2, hs.fc3, hs.fcn, hs.q1, hs.q2, hs.q3);
         }
         for (DBuf* b : {&Bm, &colp, &lead_b, &cand_b, &gl, &gT, &stt, &ordr}) release(c, *b);
         blk_done = true;
