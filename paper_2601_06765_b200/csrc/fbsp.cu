@@ -1900,7 +1900,10 @@ __global__ void __launch_bounds__(CL_THREADS) k_fbsp(const FbspArgs a) {
       }
 #pragma unroll
       for (int q = 0; q < U; ++q)
-        if (tt[q] < t_hi) rk[q] = key_rank<KW>(a.f, bt, a.st, key_add<KW>(kk[q], dl));
+        if (tt[q] < t_hi) {
+          rk[q] = key_rank<KW>(a.f, bt, a.st, key_add<KW>(kk[q], dl));
+          a.col[rsi + tt[q]] = rk[q];  // parked for the join (P4 turns it into the column)
+        }
 #pragma unroll
       for (int q = 0; q < U; ++q) dw[q] = tt[q] < t_hi ? __ldcg(a.dict + (rk[q] >> 5)) : 0xFFFFFFFFu;  // L2 filter
 #pragma unroll
@@ -2078,7 +2081,7 @@ __global__ void __launch_bounds__(CL_THREADS) k_fbsp(const FbspArgs a) {
           u16 e[NV];
           gl_unrank<NV>(__ldcg(front + j), n, a.D, bt, a.st, e);
           const Key<KW> m = gl_encode<KW, NV>(a.f, e);
-          a.rows_basis[row] = g;
+          a.rows_basis[row] = big ? g : ~g;  // ~g: ranks not parked in col (ranked in AC), the join ranks them
           key_store<KW>(a.rows_delta, row, key_sub<KW>(m, key_load<KW>(a.bckey, __ldg(a.boff + g))));
           a.rows_start[row] = Mcur + bl + lp - len;
           bool over = false;
@@ -2118,7 +2121,10 @@ __global__ void __launch_bounds__(CL_THREADS) k_fbsp(const FbspArgs a) {
           }
 #pragma unroll
           for (int q = 0; q < U; ++q)
-            if (tt[q] < t_hi) rk[q] = key_rank<KW>(a.f, bt, a.st, key_add<KW>(kk[q], dl));
+            if (tt[q] < t_hi) {
+              rk[q] = key_rank<KW>(a.f, bt, a.st, key_add<KW>(kk[q], dl));
+              if (rsi + tt[q] < a.M_cap) a.col[rsi + tt[q]] = rk[q];  // parked for the join
+            }
 #pragma unroll
           for (int q = 0; q < U; ++q)
             dw[q] = tt[q] < t_hi ? (__ldcg(a.dict + (rk[q] >> 5)) | __ldcg(a.newbits + (rk[q] >> 5))) : 0xFFFFFFFFu;
@@ -2194,7 +2200,9 @@ __global__ void __launch_bounds__(CL_THREADS) k_fbsp(const FbspArgs a) {
     bool miss = false;
     term_ranges(0u, (u32)r, 0u, Mcur, [&](u32 i) { return __ldcg(a.rows_start + i); },
                 [&](u32 i, u32 rsi, u32 from, u32 to) {
-      const int g = __ldcg(a.rows_basis + i);
+      int g = __ldcg(a.rows_basis + i);
+      const bool parked = g >= 0;  // ranks parked in col by P1 / a big round's C
+      if (!parked) g = ~g;
       const u32 off = __ldg(a.boff + g), len = __ldg(a.blen + g);
       const Key<KW> dl = key_load_cg<KW>(a.rows_delta, i);
       const u32 t_lo = from - rsi, t_hi = min(len, to - rsi);
@@ -2206,13 +2214,16 @@ __global__ void __launch_bounds__(CL_THREADS) k_fbsp(const FbspArgs a) {
         for (int q = 0; q < U; ++q) {
           tt[q] = tb + q * 32 + lane;
           if (tt[q] < t_hi) {
-            kk[q] = key_load<KW>(a.bckey, (long long)off + tt[q]);
+            if (parked) rk[q] = __ldcg(a.col + rsi + tt[q]);
+            else kk[q] = key_load<KW>(a.bckey, (long long)off + tt[q]);
             cf[q] = __ldg(a.bcoeff + off + tt[q]);
           }
         }
+        if (!parked) {
 #pragma unroll
-        for (int q = 0; q < U; ++q)
-          if (tt[q] < t_hi) rk[q] = key_rank<KW>(a.f, bt, a.st, key_add<KW>(kk[q], dl));
+          for (int q = 0; q < U; ++q)
+            if (tt[q] < t_hi) rk[q] = key_rank<KW>(a.f, bt, a.st, key_add<KW>(kk[q], dl));
+        }
 #pragma unroll
         for (int q = 0; q < U; ++q)
           if (tt[q] < t_hi) dw[q] = __ldcg(a.dwp + (rk[q] >> 5));
