@@ -72,6 +72,7 @@ const char* f4b_ctx_last_error(const f4b_ctx* ctx);
  * default path does not fit, so tests can reach them:
  *   "sweep"       0 auto | 1 blocked C-row sweep | 2 generic k_sweep
  *   "dense"       0 pivot-block RREF(D') | 1 per-pivot k_dense_forward
+ *   "dense_rows"  0 auto (a CTA's D' rows in shared memory when they fit) | 1 in HBM
  *   "fbsp"        0 one cooperative k_fbsp | 1 multi-launch rank pipeline
  *   "dict_sort"   1 = radix-sort dictionary for grevlex too
  *   "dict_lsd"    1 = f4b_dict_build sorts every key (LSD), no MSD buckets */

@@ -392,6 +392,7 @@ int f4b_ctx_set_option(f4b_ctx* h, const char* name, int64_t value) {
     int64_t hi;
   } opts[] = {{"sweep", &c->opt_sweep, 2},
               {"dense", &c->opt_dense, 1},
+              {"dense_rows", &c->opt_dense_rows, 1},
               {"fbsp", &c->opt_fbsp, 1},
               {"dict_sort", &c->opt_dict_sort, 1},
               {"dict_lsd", &c->opt_dict_lsd, 1}};

@@ -1264,8 +1264,7 @@ __global__ void __launch_bounds__(DB_THREADS) k_dense_blk(Fp fp, u32* __restrict
   __shared__ u32 s_crow[DB_NP], s_rl[DB_NP];
   __shared__ u32 s_wrow[DB_NP], s_wcol[DB_NP];
   __shared__ u32 s_red[33];
-  __shared__ u32 s_lm[NW][DB_G];
-  __shared__ u32 s_nt, s_na, s_piv, s_np, s_c0;
+  __shared__ u32 s_nt, s_na, s_np, s_c0;
   // CTA 0 phase 2: the block's window | Z, aliasing the phase-3 arrays
   u32(*s_X)[DB_W + 32] = reinterpret_cast<u32(*)[DB_W + 32]>(smem);
   u32* s_c = smem;                    // [maxt][DB_NP] coefficients
@@ -2049,7 +2048,7 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
   release(c, pcnt);
   // E2: D' = C swept over the A columns
   const long long R = E->nC, K = E->K;
-  DBuf Dp, gacc, cand, used, pofc, lead;
+  DBuf Dp, cand, used, pofc, lead;
   E->rankD = 0;
   if (R > 0 && K > 0) {
     ensure(c, Dp, (size_t)R * K * sizeof(u32));
@@ -2080,8 +2079,7 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
       size_t smem_b = (size_t)std::max<long long>(DB_NP * (DB_W + 32), maxt3 * (DB_NP + 3) + rpc) * 4;
       (void)Kp;
       // this CTA's rows resident in shared memory when they fit
-      static const bool sr_off = getenv("F4B_DENSE_NOSR") != nullptr;  // experiments
-      const bool sr = !sr_off && smem_b + (size_t)rpc * K * 4 <= 196 * 1024;
+      const bool sr = c->opt_dense_rows == 0 && smem_b + (size_t)rpc * K * 4 <= 196 * 1024;
       if (sr) smem_b += (size_t)rpc * K * 4;
       if (blk_occ < 0) {
         int o = 0;

@@ -96,6 +96,7 @@ struct Ctx {
   // paths, the others are the fallbacks the automatic choice takes when a
   // shape does not fit, forced here so the parity tests reach every kernel
   int opt_sweep = 0;        // "sweep": 0 auto, 1 blocked sweep, 2 k_sweep only
+  int opt_dense_rows = 0;   // "dense_rows": 0 auto (D' rows in shared memory when they fit), 1 always in HBM
   int opt_dense = 0;        // "dense": 0 pivot blocks (k_dense_blk), 1 k_dense_forward
   int opt_fbsp = 0;         // "fbsp": 0 one cooperative k_fbsp, 1 multi-launch rank path
   int opt_dict_sort = 0;    // "dict_sort": 1 = radix-sort dictionary even for grevlex

@@ -268,7 +268,8 @@ def test_f4_steps_match_reference_sort_path(cuda, force_option, name, gen, args)
 
 
 _FALLBACK_KERNELS = {("dict_sort", 1): "k_tile_dict", ("fbsp", 1): "k_rank_fill", ("sweep", 1): "k_sweep_blk",
-                     ("sweep", 2): "k_sweep<0", ("dense", 1): "k_dense_forward"}
+                     ("sweep", 2): "k_sweep<0", ("dense", 1): "k_dense_forward",
+                     ("dense_rows", 1): "k_dense_blk"}
 
 
 @pytest.mark.parametrize("name", ["cyclic8_p32003", "katsura11_p32003"])
