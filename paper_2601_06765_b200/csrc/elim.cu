@@ -1618,8 +1618,11 @@ __global__ void __launch_bounds__(DB_THREADS) k_dense_blk(Fp fp, u32* __restrict
             for (int j4 = 0; j4 < DB_NP / 4; ++j4) {
               if (4 * j4 >= (int)np) break;
               const uint4 cv = cr[j4];
-              a += prod(cv.x, pv[4 * j4]) + prod(cv.y, pv[4 * j4 + 1]) + prod(cv.z, pv[4 * j4 + 2]) +
-                   prod(cv.w, pv[4 * j4 + 3]);
+              if (SMALLP && tiny)  // p < 2^15: four products < 4 p^2 < 2^32 summed in 32 bits
+                a += (u64)(cv.x * pv[4 * j4] + cv.y * pv[4 * j4 + 1] + cv.z * pv[4 * j4 + 2] + cv.w * pv[4 * j4 + 3]);
+              else
+                a += prod(cv.x, pv[4 * j4]) + prod(cv.y, pv[4 * j4 + 1]) + prod(cv.z, pv[4 * j4 + 2]) +
+                     prod(cv.w, pv[4 * j4 + 3]);
             }
             acc[r] = a;
           }
