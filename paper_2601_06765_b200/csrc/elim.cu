@@ -1026,7 +1026,15 @@ __global__ void __launch_bounds__(256) k_sweep_win(Fp fp, u32 mu, const u32* __r
             const u32 cc = nonA[q];
             if (cc <= lead) continue;
             u32 x = acc[cc];
-            for (u32 t = 0; t < nco; ++t) x = fp.add(x, fp.mont_mul(s_cv[t], __ldg(so.Rd + (size_t)s_ck[t] * K + q)));
+            if (PK) {  // p < 2^16: raw Montgomery-coefficient products summed in 64 bits (< 256 p^2), one REDC
+              unsigned long long a = 0;
+              for (u32 t = 0; t < nco; ++t) a += (unsigned long long)s_cv[t] * __ldg(so.Rd + (size_t)s_ck[t] * K + q);
+              const u32 m = (u32)a * fp.pprime;
+              const unsigned long long u = (a + (unsigned long long)m * p) >> 32;
+              x = fp.add(x, (u32)(u >= p ? u - p : u));
+            } else {
+              for (u32 t = 0; t < nco; ++t) x = fp.add(x, fp.mont_mul(s_cv[t], __ldg(so.Rd + (size_t)s_ck[t] * K + q)));
+            }
             acc[cc] = x;
           }
         __syncthreads();
