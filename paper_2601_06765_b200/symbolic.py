@@ -130,7 +130,7 @@ class LayoutPlan:
         dict_keys) of a device plan in the background (copy stream); the
         attributes then wait for it instead of downloading.  Lets a caller
         compile the next batch while this one's arrays cross PCIe."""
-        if self.device is not None and not self._host:
+        if self.device is not None and not self._host and getattr(self.device, "_pf", None) is None:
             self.device.prefetch(self.ring.n_key_words)
         return self
 

@@ -782,7 +782,7 @@ def test_plan_prefetch_matches_download(cuda):
         assert np.array_equal(getattr(a, k), getattr(b, k)), k
     assert a.col_ind.dtype == np.int64 and a.val.dtype == np.uint64
     assert plan_digest(a) == gold["steps"][10]["plan_sha256"]
-    c = compile_batch(rows, soa, Closure.ONE_STEP_REDUCTION).prefetch()
+    c = compile_batch(rows, soa, Closure.ONE_STEP_REDUCTION).prefetch().prefetch()  # idempotent
     del c  # freed with the copy pending: the free waits for it
 
 
