@@ -225,6 +225,12 @@ int f4b_psge_plan(f4b_ctx* ctx, const f4b_plan* plan, int mode, f4b_echelon** ou
 int f4b_psge_csr(f4b_ctx* ctx, int64_t n_rows, int64_t n_cols, const int64_t* row_ptr,
                  const int64_t* col_ind, const uint64_t* val, int mode, f4b_echelon** out);
 int f4b_echelon_complete(f4b_ctx* ctx, f4b_echelon* ech); /* NEW_ONLY -> FULL_RREF */
+/* FULL_RREF restricted to the pivot rows led by the n given columns (the
+ * final interreduction needs only the rows led by the basis' leading
+ * monomials, groebner.py:314-332): those rows are back-reduced exactly as
+ * f4b_echelon_complete does it, the other pivot rows come back empty and
+ * f4b_echelon_info.full reports 2. */
+int f4b_echelon_complete_rows(f4b_ctx* ctx, f4b_echelon* ech, const int64_t* lead_cols, int64_t n);
 int f4b_echelon_get_info(const f4b_echelon* ech, f4b_echelon_info* info);
 /* which = 0: pivot rows, 1: nonpivot rows; rows ascending by lead column.
  * leads[k], row_ptr[k+1], cols/vals concatenated (standard residues). */

@@ -99,6 +99,7 @@ SIGNATURES = {
     "f4b_psge_csr": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, i64p, i64p, u64p, C.c_int,
                                C.POINTER(C.c_void_p)]),
     "f4b_echelon_complete": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "f4b_echelon_complete_rows": (C.c_int, [C.c_void_p, C.c_void_p, i64p, C.c_int64]),
     "f4b_echelon_get_info": (C.c_int, [C.c_void_p, C.POINTER(EchelonInfo)]),
     "f4b_echelon_download": (C.c_int, [C.c_void_p, C.c_int, i64p, i64p, i64p, u64p]),
     "f4b_echelon_pivot_cols": (C.c_int, [C.c_void_p, i64p]),

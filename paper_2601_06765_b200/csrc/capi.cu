@@ -1002,6 +1002,13 @@ int f4b_echelon_complete(f4b_ctx* h, f4b_echelon* e) {
   API_END
 }
 
+int f4b_echelon_complete_rows(f4b_ctx* h, f4b_echelon* e, const int64_t* lead_cols, int64_t n) {
+  if (!h || !e || n < 0 || (n && !lead_cols)) return F4B_ERR_PRECONDITION;
+  API_BEGIN(&h->c)
+  echelon_complete_rows(_c, e, lead_cols, n);
+  API_END
+}
+
 int f4b_echelon_get_info(const f4b_echelon* e, f4b_echelon_info* info) {
   if (!e || !info) return F4B_ERR_PRECONDITION;
   echelon_info(e, info);

@@ -43,6 +43,7 @@ struct f4b_echelon {
   long long M = 0;
   long long n_rows = 0, n_cols = 0, nA = 0, nC = 0, K = 0, rankD = 0, zero_rows = 0;
   bool full = false;
+  bool partial = false;  // only the pivot rows of chosen lead columns were back-reduced (echelon_complete_rows)
   int64_t numeric_ns = 0, backsub_ns = 0;
   // input CSR (owned if uploaded from host)
   f4b::DBuf own_rp, own_col, own_val;
@@ -1955,7 +1956,7 @@ static void launch_sweep(Ctx* c, const Fp& fp, f4b_echelon* E, const u32* rows, 
   }
 }
 
-static void run_a_sweep(Ctx* c, f4b_echelon* E);
+static void run_a_sweep(Ctx* c, f4b_echelon* E, const std::vector<char>* want = nullptr);
 
 // psge tail record (pool use, sweep counters, rank(D'), error flags) written
 // by one thread into page-locked host memory (UVA)
@@ -2285,8 +2286,21 @@ static void psge_run(Ctx* c, f4b_echelon* E, int mode) {
   if (mode == F4B_FULL_RREF) run_a_sweep(c, E);
 }
 
-static void run_a_sweep(Ctx* c, f4b_echelon* E) {
-  if (E->full) return;
+// pivot-row slots of a subset sweep scattered to their A positions
+__global__ void k_scatter_slots(const u32* __restrict__ so, const u32* __restrict__ sl, const u32* __restrict__ pos,
+                                u32 n, u32* __restrict__ off, u32* __restrict__ len) {
+  const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    off[pos[i]] = so[i];
+    len[pos[i]] = sl[i];
+  }
+}
+
+// FULL_RREF's pivot rows (sparselin.py:337-349); `want` (optional, a flag
+// per column) restricts the back-reduction to the pivot rows led by the
+// flagged columns — the others are left empty (echelon_complete_rows)
+static void run_a_sweep(Ctx* c, f4b_echelon* E, const std::vector<char>* want) {
+  if (E->full && !(E->partial && !want)) return;
   Fp fp = make_fp(c);
   const long long N = E->n_cols, nA = E->nA, K = E->K;
   cudaEvent_t ev0 = timing_event(c, 2), ev1 = timing_event(c, 3);
@@ -2303,9 +2317,25 @@ static void run_a_sweep(Ctx* c, f4b_echelon* E) {
     check_cuda(cudaMemcpyAsync(h_acols.data(), E->acols.p, nA * sizeof(u32), cudaMemcpyDeviceToHost, c->stream), "d2h");
     check_cuda(cudaMemcpyAsync(h_prow.data(), E->prow.p, N * sizeof(u32), cudaMemcpyDeviceToHost, c->stream), "d2h");
     check_cuda(cudaStreamSynchronize(c->stream), "sync");
-    std::vector<u32> h_arows(nA);
-    for (long long k = 0; k < nA; ++k) h_arows[k] = h_prow[h_acols[k]];
-    check_cuda(cudaMemcpyAsync(arows.p, h_arows.data(), nA * sizeof(u32), cudaMemcpyHostToDevice, c->stream), "h2d");
+    std::vector<u32> h_arows, h_pos;
+    h_arows.reserve(nA);
+    for (long long k = 0; k < nA; ++k)
+      if (!want || (*want)[h_acols[k]]) {
+        h_arows.push_back(h_prow[h_acols[k]]);
+        h_pos.push_back((u32)k);
+      }
+    const long long ns = (long long)h_arows.size();
+    DBuf sub, posb;
+    if (want) {  // subset: slots indexed by subset position, scattered afterwards; the rest empty
+      ensure(c, sub, (size_t)std::max<long long>(2 * ns, 1) * sizeof(u32));
+      ensure(c, posb, (size_t)std::max<long long>(ns, 1) * sizeof(u32));
+      check_cuda(cudaMemsetAsync(E->a_off.p, 0, nA * sizeof(u32), c->stream), "memset");
+      check_cuda(cudaMemsetAsync(E->a_len.p, 0, nA * sizeof(u32), c->stream), "memset");
+      if (ns) check_cuda(cudaMemcpyAsync(posb.p, h_pos.data(), ns * sizeof(u32), cudaMemcpyHostToDevice, c->stream), "h2d");
+    }
+    if (ns) check_cuda(cudaMemcpyAsync(arows.p, h_arows.data(), ns * sizeof(u32), cudaMemcpyHostToDevice, c->stream), "h2d");
+    u32* s_off = want ? sub.as<u32>() : E->a_off.as<u32>();
+    u32* s_len = want ? sub.as<u32>() + std::max<long long>(ns, 1) : E->a_len.as<u32>();
     size_t base_used = (size_t)E->nonpivot_nnz;
     for (int attempt = 0; attempt < 8; ++attempt) {
       size_t need = base_used + (size_t)std::max<long long>(2 * E->M, 1 << 20);
@@ -2318,10 +2348,10 @@ static void run_a_sweep(Ctx* c, f4b_echelon* E) {
       unsigned long long cur = base_used;
       check_cuda(cudaMemcpyAsync(E->cursor.p, &cur, 8, cudaMemcpyHostToDevice, c->stream), "h2d");
       check_cuda(cudaMemsetAsync(err, 0, 4, c->stream), "memset");
-      launch_sweep<1>(c, fp, E, arows.as<u32>(), (u32)nA, nullptr, (u32)K, E->rankD ? E->Rd.as<u32>() : nullptr,
-                      (u32)E->rankD, E->rankD ? E->dpiv.as<u32>() : nullptr, E->pool_col.as<u32>(),
-                      E->pool_val.as<u32>(), E->pool_cap, E->cursor.as<unsigned long long>(), E->a_off.as<u32>(),
-                      E->a_len.as<u32>(), err);
+      if (ns)
+        launch_sweep<1>(c, fp, E, arows.as<u32>(), (u32)ns, nullptr, (u32)K, E->rankD ? E->Rd.as<u32>() : nullptr,
+                        (u32)E->rankD, E->rankD ? E->dpiv.as<u32>() : nullptr, E->pool_col.as<u32>(),
+                        E->pool_val.as<u32>(), E->pool_cap, E->cursor.as<unsigned long long>(), s_off, s_len, err);
       u32 e = read_u32(c, err);
       if (!(e & DEVERR_CAPACITY)) break;
       if (attempt == 7) fail(F4B_ERR_OOM, "psge: pivot row pool still overflows after 8 resizes");
@@ -2335,8 +2365,13 @@ static void run_a_sweep(Ctx* c, f4b_echelon* E) {
     check_cuda(cudaMemcpyAsync(&tot, E->cursor.p, 8, cudaMemcpyDeviceToHost, c->stream), "d2h");
     check_cuda(cudaStreamSynchronize(c->stream), "sync");
     E->pivot_nnz = (long long)tot - (long long)base_used;
+    if (want && ns)
+      F4B_LAUNCH(c, k_scatter_slots, nb(ns, 256), 256, 0, sub.as<u32>(), sub.as<u32>() + std::max<long long>(ns, 1),
+                 posb.as<u32>(), (u32)ns, E->a_off.as<u32>(), E->a_len.as<u32>());
     release(c, arows);
     release(c, gacc);
+    release(c, sub);
+    release(c, posb);
   }
   check_cuda(cudaEventRecord(ev1, c->stream), "event");
   check_cuda(cudaEventSynchronize(ev1), "event sync");
@@ -2344,6 +2379,7 @@ static void run_a_sweep(Ctx* c, f4b_echelon* E) {
   cudaEventElapsedTime(&ms, ev0, ev1);
   E->backsub_ns = (int64_t)(ms * 1e6);
   E->full = true;
+  E->partial = want != nullptr;
 }
 
 f4b_echelon* psge_plan(Ctx* c, const f4b_plan* pl, int mode) {
@@ -2406,6 +2442,15 @@ f4b_echelon* psge_csr(Ctx* c, long long r, long long N, const int64_t* rp, const
 
 void echelon_complete(Ctx* c, f4b_echelon* E) { run_a_sweep(c, E); }
 
+void echelon_complete_rows(Ctx* c, f4b_echelon* E, const int64_t* lead_cols, long long n) {
+  std::vector<char> want((size_t)std::max<long long>(E->n_cols, 1), 0);
+  for (long long i = 0; i < n; ++i)
+    if (lead_cols[i] >= 0 && lead_cols[i] < E->n_cols) want[(size_t)lead_cols[i]] = 1;
+  if (E->full && !E->partial) return;  // every pivot row is already there
+  E->full = false;
+  run_a_sweep(c, E, &want);
+}
+
 void echelon_info(const f4b_echelon* E, f4b_echelon_info* info) {
   info->n_rows = E->n_rows;
   info->n_cols = E->n_cols;
@@ -2415,7 +2460,7 @@ void echelon_info(const f4b_echelon* E, f4b_echelon_info* info) {
   info->n_nonpivot_rows = E->rankD;
   info->pivot_nnz = E->pivot_nnz;
   info->nonpivot_nnz = E->nonpivot_nnz;
-  info->full = E->full ? 1 : 0;
+  info->full = E->full ? (E->partial ? 2 : 1) : 0;
   info->numeric_ns = E->numeric_ns;
   info->backsub_ns = E->backsub_ns;
   info->dense_rows = E->nC;

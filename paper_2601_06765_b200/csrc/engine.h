@@ -227,6 +227,7 @@ f4b_echelon* psge_plan(Ctx* c, const f4b_plan* pl, int mode);
 f4b_echelon* psge_csr(Ctx* c, long long r, long long N, const int64_t* rp, const int64_t* col, const uint64_t* val,
                       int mode);
 void echelon_complete(Ctx* c, f4b_echelon* E);
+void echelon_complete_rows(Ctx* c, f4b_echelon* E, const int64_t* lead_cols, long long n);
 void echelon_info(const f4b_echelon* E, f4b_echelon_info* info);
 void echelon_download(const f4b_echelon* E, int which, int64_t* leads, int64_t* row_ptr, int64_t* cols, uint64_t* vals);
 void echelon_release(f4b_echelon* E);

@@ -216,6 +216,14 @@ class DeviceEchelon:
         self.engine.ctx.sync_stream()
         self.engine.ctx.check(self.engine.lib.f4b_echelon_complete(self.engine.ctx.h, self.h), "echelon complete")
 
+    def complete_rows(self, lead_cols):
+        """Back-reduce only the pivot rows led by ``lead_cols``
+        (f4b_echelon_complete_rows); the other pivot rows stay empty."""
+        lc = np.ascontiguousarray(lead_cols, dtype=np.int64)
+        self.engine.ctx.sync_stream()
+        self.engine.ctx.check(self.engine.lib.f4b_echelon_complete_rows(self.engine.ctx.h, self.h, ptr(lc, C.c_int64),
+                                                                        len(lc)), "echelon complete rows")
+
     def pivot_cols(self):
         inf = self.info()
         out = np.empty(inf["rank"], dtype=np.int64)

@@ -420,7 +420,28 @@ def _minimal_monic(polys: list, ring: Ring) -> list:
     return minimal
 
 
-def reduce_basis_device(polys: list, ring: Ring) -> list:
+def _minimal_order(polys: list, ring: Ring) -> np.ndarray:
+    """Indices of the minimal basis (reference reduce_basis :314-332: ascending
+    sort_key(LM), keep a polynomial unless an earlier kept LM divides its LM)
+    with NumPy: divisibility is transitive, so "no earlier LM divides it"
+    decides; ties keep the first (stable order)."""
+    idx = [i for i, f in enumerate(polys) if not f.is_zero()]
+    if not idx:
+        return np.zeros(0, np.int64)
+    L = np.asarray([polys[i].lm() for i in idx], dtype=np.int64).reshape(len(idx), ring.n_vars)
+    keys = key_pack_vec(L, ring)
+    order = np.lexsort(keys.T[::-1])  # ascending key = ascending term order, stable
+    Ls = L[order]
+    kept = np.ones(len(order), dtype=bool)
+    for i0 in range(0, len(order), 256):
+        blk = Ls[i0:i0 + 256]
+        div = (Ls[None, :, :] <= blk[:, None, :]).all(axis=2)  # div[i, j]: LM_j divides LM_(i0+i)
+        div &= np.arange(len(order))[None, :] < np.arange(i0, i0 + len(blk))[:, None]
+        kept[i0:i0 + len(blk)] = ~div.any(axis=1)
+    return np.asarray(idx, dtype=np.int64)[order[kept]]
+
+
+def reduce_basis_device(polys: list, ring: Ring, soa: SoaPolySet | None = None) -> list:
     """Final interreduction of a Gröbner basis as ONE extra Macaulay matrix on
     the GPU: the minimal basis (same selection as
     reduce_basis, reference :314-332) as shift-0 rows, closed under one-step
@@ -432,24 +453,54 @@ def reduce_basis_device(polys: list, ring: Ring) -> list:
     from .polynomials import soa_pack
     from .symbolic import Row, RowRole
 
-    minimal = _minimal_monic(polys, ring)
-    if not minimal:
+    sel = _minimal_order(polys, ring)
+    if not len(sel):
         return []
-    soa = soa_pack(minimal, ring)
+    monic = all(polys[i].lc() == 1 for i in sel.tolist())
+    minimal = [polys[i] if monic else poly_monic(polys[i]) for i in sel.tolist()]
+    if soa is not None and monic and len(soa) == len(polys):
+        # the caller's flat streams (e.g. GroebnerState.soa()): gather the
+        # minimal polynomials' term ranges instead of re-packing tuples
+        off, ln = soa.offset[sel], soa.length[sel]
+        new_off = np.zeros(len(sel) + 1, dtype=np.int64)
+        np.cumsum(ln, out=new_off[1:])
+        tix = np.repeat(off - new_off[:-1], ln) + np.arange(int(new_off[-1]), dtype=np.int64)
+        soa = SoaPolySet(ring, soa.mon_key[tix], soa.coeff[tix], new_off, ln.astype(np.int64), soa.exps[tix])
+    else:
+        soa = soa_pack(minimal, ring)
     zero = (0,) * ring.n_vars
     rows = [Row(zero, k, RowRole.SPOLY_HALF, 0) for k in range(len(minimal))]
     # the reference's normal-form loop has no dictionary cap: neither has this
     # matrix (only the device's 2^30-term plan limit applies)
     plan = compile_batch(rows, soa, Closure.ONE_STEP_REDUCTION, dict_cap=1 << 62)
-    ech = psge_reduce(csr_from_plan(plan, ring.modulus))
     ex = plan.dict_exps()
-    rp, ci = plan.row_ptr, plan.col_ind
-    lead_cols = {int(ci[rp[k]]) for k in range(len(minimal))}
     out = []
-    for lead, cols, vals in ech.pivot_rows:
-        if lead in lead_cols:
-            out.append(Poly(ring, tuple((tuple(int(x) for x in ex[c]), int(v)) for c, v in zip(cols.tolist(),
-                                                                                          vals.tolist()))))
+    if plan.device is not None:
+        # only the rows led by the basis LMs are back-reduced (the closure
+        # rows are pivots for them, never output): f4b_echelon_complete_rows
+        from .engine import Engine
+
+        eng = Engine.for_ring(ring)
+        col_of = {tuple(r): c for c, r in enumerate(ex.tolist())}
+        lead_cols = np.unique(np.asarray([col_of[tuple(f.lm())] for f in minimal], dtype=np.int64))
+        ech = eng.psge_plan(plan.device, full=False)
+        ech.complete_rows(lead_cols)
+        leads, prp, cols, vals = ech.rows(0)
+        want = set(lead_cols.tolist())
+        cl, vl = cols.tolist(), vals.tolist()
+        ex_t = [tuple(r) for r in ex.tolist()]  # one tuple per column, shared by every term
+        for k, lead in enumerate(leads.tolist()):
+            if lead in want:
+                a, b = int(prp[k]), int(prp[k + 1])
+                out.append(Poly(ring, tuple(zip(map(ex_t.__getitem__, cl[a:b]), vl[a:b]))))
+    else:
+        ech = psge_reduce(csr_from_plan(plan, ring.modulus))
+        rp, ci = plan.row_ptr, plan.col_ind
+        lead_cols = {int(ci[rp[k]]) for k in range(len(minimal))}
+        for lead, cols, vals in ech.pivot_rows:
+            if lead in lead_cols:
+                out.append(Poly(ring, tuple((tuple(int(x) for x in ex[c]), int(v)) for c, v in zip(cols.tolist(),
+                                                                                              vals.tolist()))))
     out.sort(key=lambda f: ring.sort_key(f.lm()), reverse=True)
     return out
 
@@ -468,7 +519,7 @@ def f4_groebner(system: list, ring: Ring, config: F4Config | None = None) -> lis
             raise NonterminationError(f"f4 exceeded {config.max_steps} batches")
         f4_step(state, config)
         steps += 1
-    return reduce_basis_device(state.basis, ring)
+    return reduce_basis_device(state.basis, ring, state.soa())
 
 
 @dataclass

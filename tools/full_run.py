@@ -99,7 +99,7 @@ def main():
         k += 1
     loop_s = time.perf_counter() - t0
     t1 = time.perf_counter()
-    gb = reduce_basis_device(st.basis, ring) if not st.n_pairs() else []
+    gb = reduce_basis_device(st.basis, ring, st.soa()) if not st.n_pairs() else []
     red_s = time.perf_counter() - t1
     text = format_system(ring, gb) if gb else ""
     staircase = standard_monomials([f.lm() for f in gb], ring.n_vars) if gb else None
