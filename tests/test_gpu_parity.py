@@ -138,6 +138,10 @@ def test_compile_random_against_oracle(cuda, dict_mode, order, n, max_exp, p):
         for closure in (Closure.SUPPORT_ONLY, Closure.ONE_STEP_REDUCTION):
             plan = compile_batch(rows, soa, closure)
             _check_plan(plan, rows, soa, closure is Closure.ONE_STEP_REDUCTION)
+            # the copy-stream download of every dictionary path equals the synchronous one
+            pf = compile_batch(rows, soa, closure).prefetch()
+            for k in ("row_ptr", "col_ind", "val", "dict_keys"):
+                assert np.array_equal(getattr(pf, k), getattr(plan, k)), k
 
 
 # ---------------------------------------------------------------------------
@@ -784,6 +788,30 @@ def test_plan_prefetch_matches_download(cuda):
     assert plan_digest(a) == gold["steps"][10]["plan_sha256"]
     c = compile_batch(rows, soa, Closure.ONE_STEP_REDUCTION).prefetch().prefetch()  # idempotent
     del c  # freed with the copy pending: the free waits for it
+
+
+@pytest.mark.parametrize("p", [101, 32003, 2147483629])
+def test_echelon_complete_rows_subset(cuda, p):
+    """f4b_echelon_complete_rows: the pivot rows led by the chosen columns are
+    exactly the FULL_RREF ones (every other pivot row comes back empty)."""
+    m = FieldModulus(p)
+    rng = np.random.default_rng(p % 1000)
+    mat = _random_sparse(rng, 120, 160, 0.08, p)
+    full = psge_reduce(csr_from_dense(mat, m))
+    want = {lead: (c.tolist(), v.tolist()) for lead, c, v in full.pivot_rows}
+    pick = sorted(want)[::3]
+    part = psge_reduce(csr_from_dense(mat, m))
+    part.device.complete_rows(np.asarray(pick + [10**6], dtype=np.int64))  # out-of-range columns are ignored
+    assert part.device.info()["full"] == 2
+    leads, rp, cols, vals = part.device.rows(0)
+    got = {}
+    for k, lead in enumerate(leads.tolist()):
+        a, b = int(rp[k]), int(rp[k + 1])
+        if b > a:
+            got[lead] = (cols[a:b].tolist(), vals[a:b].tolist())
+    assert sorted(got) == pick
+    for lead in pick:
+        assert got[lead] == want[lead]
 
 
 def test_snapshot_resume_gpu(cuda, tmp_path):
