@@ -1498,7 +1498,24 @@ __global__ void __launch_bounds__(DB_THREADS) k_dense_blk(Fp fp, u32* __restrict
         s_U[i][k] = k < DB_NP ? (k < np ? fp.to_mont(x[s_wcol[k]]) : 0u) : x[DB_W + (k - DB_NP)];
       }
       __syncthreads();
-      if (warp == 0) {
+      if (SMALLP && warp == 0) {
+        // p < 2^16: left-looking, y_i = d_i (z_i - sum_{j>i} U_ij y_j) with
+        // the raw products summed in 64 bits (< 32 p^2 < p 2^32), one REDC
+        // per row; the loads of a row's dot product are independent
+        const u32 dl = (u32)lane < np ? fp.to_mont(fp.inv(fp.mont_mul(s_U[lane][lane], 1u))) : 0u;
+        for (int i = (int)np - 1; i >= 0; --i) {
+          u64 acc0 = 0, acc1 = 0;
+          int j = i + 1;
+          for (; j + 2 <= (int)np; j += 2) {
+            acc0 += (u64)s_U[i][j] * s_U[j][DB_NP + lane];
+            acc1 += (u64)s_U[i][j + 1] * s_U[j + 1][DB_NP + lane];
+          }
+          if (j < (int)np) acc0 += (u64)s_U[i][j] * s_U[j][DB_NP + lane];
+          s_U[i][DB_NP + lane] =
+              fp.mont_mul(__shfl_sync(FULL, dl, i), fp.sub(s_U[i][DB_NP + lane], red64(acc0 + acc1)));
+          __syncwarp();
+        }
+      } else if (warp == 0) {
         const u32 dl = (u32)lane < np ? fp.to_mont(fp.inv(fp.mont_mul(s_U[lane][lane], 1u))) : 0u;
         for (int i = (int)np - 1; i >= 0; --i) {
           const u32 y = fp.mont_mul(__shfl_sync(FULL, dl, i), s_U[i][DB_NP + lane]);
