@@ -3,7 +3,9 @@
 Every ``csrc/*.cu`` is compiled to an object in parallel, then linked into
 ``paper_2601_06765_b200/libf4b200.so``.  Flags: ``-gencode
 arch=compute_100a,code=sm_100a -O3 -lineinfo``.  Rebuilds only when a source
-or header is newer than the library.
+or header is newer than the library.  ``csrc/rowpack.c`` (host glue: the
+row-list packing of compile_batch, a CPython extension) is compiled with gcc
+into ``paper_2601_06765_b200/_rowpack*.so``.
 """
 
 from __future__ import annotations
@@ -13,6 +15,7 @@ import glob
 import os
 import subprocess
 import sys
+import sysconfig
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
@@ -42,7 +45,25 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
+ROWPACK_SRC = os.path.join(CSRC, "rowpack.c")
+ROWPACK = os.path.join(HERE, "_rowpack" + (sysconfig.get_config_var("EXT_SUFFIX") or ".so"))
+
+
+def build_rowpack(force: bool = False) -> str:
+    if not force and os.path.exists(ROWPACK) and os.path.getmtime(ROWPACK) >= os.path.getmtime(ROWPACK_SRC):
+        return ROWPACK
+    tmp = ROWPACK + ".tmp"
+    cmd = [os.environ.get("CC", "gcc"), "-O2", "-shared", "-fPIC", "-Wall", "-I", sysconfig.get_paths()["include"],
+           ROWPACK_SRC, "-o", tmp]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"gcc failed for {ROWPACK_SRC}:\n{res.stdout}\n{res.stderr}")
+    os.replace(tmp, ROWPACK)
+    return ROWPACK
+
+
 def build(force: bool = False, verbose: bool = False, extra=()) -> str:
+    build_rowpack(force)
     if not force and not _stale():
         return LIB
     os.makedirs(OBJ_DIR, exist_ok=True)

@@ -465,6 +465,8 @@ int f4b_basis_clear(f4b_ctx* h) {
   B.ckey_lane_bits = -1;
   B.lm_order.clear();
   B.lm_sorted = 0;
+  B.h_lmw.clear();
+  B.lmw_polys = 0;
   return F4B_OK;
 }
 

@@ -62,6 +62,10 @@ struct Basis {
   // order (symbolic.py:228-235), extended incrementally on append
   std::vector<int32_t> lm_order;
   int lm_sorted = 0;  // polynomials [0, lm_sorted) are merged into lm_order
+  // LMs packed two 16-bit lanes per word (the closure kernels' LM table
+  // format), polynomials [0, lmw_polys) done
+  std::vector<uint32_t> h_lmw;
+  int lmw_polys = 0;
 };
 
 struct Ctx {
@@ -115,6 +119,8 @@ struct Ctx {
   long long m_cap_hint = 0, n_cap_hint = 0;  // plan capacities of the fused FBSP kernel
   void* h_stage = nullptr;                   // page-locked H2D staging (grow-only)
   size_t h_stage_cap = 0;
+  std::vector<uint32_t> h_binom;  // binomial table of the rank path, cached per (rows, n)
+  int h_binom_rows = -1, h_binom_n = -1;
   DBuf dstage;
   // k_fbsp presence maps + chunk counters: zero between calls; the first
   // maps_clean bytes of `maps` are known to be zero

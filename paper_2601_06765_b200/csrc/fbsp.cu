@@ -2369,7 +2369,9 @@ static void compile_rank_fused(Ctx* c, const KeyFmt& f, int D, long long r0, con
   };
   cudaEvent_t ev0 = timing_event(c, 0), ev1 = timing_event(c, 1);
   check_cuda(cudaEventRecord(ev0, c->stream), "event record");
+  mark("ev0");
   encode_basis<KW>(c, f);
+  mark("encode");
 
   const int st = n + 1;
   const int rows_bt = D + n + 2;
@@ -2406,9 +2408,17 @@ static void compile_rank_fused(Ctx* c, const KeyFmt& f, int D, long long r0, con
   }
   unsigned char* hs = static_cast<unsigned char*>(c->h_stage);
   {
-    u32* hbt = reinterpret_cast<u32*>(hs + o_bt);
-    for (int x = 0; x < rows_bt; ++x)
-      for (int y = 0; y <= n; ++y) hbt[(size_t)x * st + y] = (u32)std::min<unsigned long long>(binom_ull(x, y), 0xFFFFFFFFull);
+    // binomials: cached per (rows, n) in the context
+    if (c->h_binom_rows != rows_bt || c->h_binom_n != n) {
+      c->h_binom.resize((size_t)bt_words);
+      for (int x = 0; x < rows_bt; ++x)
+        for (int y = 0; y <= n; ++y)
+          c->h_binom[(size_t)x * st + y] = (u32)std::min<unsigned long long>(binom_ull(x, y), 0xFFFFFFFFull);
+      c->h_binom_rows = rows_bt;
+      c->h_binom_n = n;
+    }
+    memcpy(hs + o_bt, c->h_binom.data(), (size_t)bt_words * 4);
+    mark("binom");
     memcpy(hs + o_rb, h_rb, (size_t)r0 * 4);
     u32* hst = reinterpret_cast<u32*>(hs + o_st);
     u32 acc = 0;
@@ -2418,12 +2428,23 @@ static void compile_rank_fused(Ctx* c, const KeyFmt& f, int D, long long r0, con
     }
     hst[r0] = acc;
     memcpy(hs + o_sh, h_shift, (size_t)r0 * n * 2);
+    // LM table in preference order, from the per-polynomial packed LMs
+    // (packed once per appended polynomial)
+    if (B.lmw_polys < B.n_polys) {
+      B.h_lmw.resize((size_t)B.n_polys * nw, 0u);
+      for (int k = B.lmw_polys; k < B.n_polys; ++k) {
+        u32* w = &B.h_lmw[(size_t)k * nw];
+        for (int v = 0; v < nw; ++v) w[v] = 0;
+        for (int v = 0; v < n; ++v) w[v / 2] |= (u32)B.h_lm[(size_t)k * n + v] << (16 * (v & 1));
+      }
+      B.lmw_polys = B.n_polys;
+    }
     u32* hlm = reinterpret_cast<u32*>(hs + o_lm);
-    memset(hlm, 0, (size_t)std::max(nc, 1) * nw * 4);
-    for (int q = 0; q < nc; ++q)
-      for (int v = 0; v < n; ++v) hlm[(size_t)q * nw + v / 2] |= (u32)B.h_lm[(size_t)pref[q] * n + v] << (16 * (v & 1));
+    if (!nc) memset(hlm, 0, (size_t)nw * 4);
+    for (int q = 0; q < nc; ++q) memcpy(hlm + (size_t)q * nw, &B.h_lmw[(size_t)pref[q] * nw], (size_t)nw * 4);
     if (nc) memcpy(hs + o_ci, pref.data(), (size_t)nc * 4);
   }
+  mark("pack");
   ensure(c, c->dstage, stage_bytes);
   check_cuda(cudaMemcpyAsync(c->dstage.p, hs, stage_bytes, cudaMemcpyHostToDevice, c->stream), "h2d stage");
   unsigned char* ds = c->dstage.as<unsigned char>();
@@ -2455,6 +2476,7 @@ static void compile_rank_fused(Ctx* c, const KeyFmt& f, int D, long long r0, con
   LoopOut* d_out = reinterpret_cast<LoopOut*>(dc + 1);
   // dc->err is cleared by k_fbsp itself (CTA 0, before its first barrier)
 
+  mark("ensure");
   const int stage_lm = (size_t)nc * nw * 4 <= 48 * 1024 ? 1 : 0;
   // dynamic shared memory rounded up to 8 KB steps: the occupancy query below
   // (tens of microseconds of host time) then runs once per step, not once per
@@ -2507,6 +2529,7 @@ static void compile_rank_fused(Ctx* c, const KeyFmt& f, int D, long long r0, con
   c->fcnt_parity ^= 1;
   ensure(c, c->dwp, (size_t)(words + 1) * sizeof(uint2));
 
+  mark("occ+maps");
   FbspArgs fa;
   memset(&fa, 0, sizeof(fa));
   fa.f = f;

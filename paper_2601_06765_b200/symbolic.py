@@ -11,15 +11,13 @@ host copies are materialized only when a caller touches them.
 from __future__ import annotations
 
 import enum
-import itertools
-import operator
 import hashlib
 from dataclasses import dataclass, field
 
 import numpy as np
 
 from .bulk import DEFAULT_POLICY, ExecPolicy
-from .errors import PropertyViolationError, UncoverableTargetError
+from .errors import DeviceError, LaneOverflowError, PropertyViolationError, UncoverableTargetError
 from .monomials import Ring, key_cmp_rows, key_pack_vec, key_unpack_vec, mon_div, mon_key_pack
 from .polynomials import Poly, SoaPolySet
 
@@ -240,8 +238,19 @@ def _empty_plan(ring: Ring) -> LayoutPlan:
                       {"dict_build_ns": 0, "row_assemble_ns": 0})
 
 
-_get_basis_index = operator.attrgetter("basis_index")
-_get_shift = operator.attrgetter("shift")
+_ROWPACK = None
+
+
+def _rowpack():
+    """The row-list packer (csrc/rowpack.c, built in-tree by _build)."""
+    global _ROWPACK
+    if _ROWPACK is None:
+        try:
+            from . import _rowpack as m
+        except ImportError as e:
+            raise DeviceError("paper_2601_06765_b200/_rowpack is not built (run __graft_entry__.build())") from e
+        _ROWPACK = m
+    return _ROWPACK
 
 
 def compile_batch(rows, basis: SoaPolySet, closure: Closure = Closure.ONE_STEP_REDUCTION,
@@ -264,11 +273,14 @@ def compile_batch(rows, basis: SoaPolySet, closure: Closure = Closure.ONE_STEP_R
     eng = Engine.for_ring(ring)
     eng.sync_basis(basis)
     n = ring.n_vars
-    rb = np.fromiter(map(_get_basis_index, rows), dtype=np.int64, count=len(rows))
-    if rb.min() < 0 or rb.max() >= len(basis):
+    # the Row list -> (int32 basis index, u16 shift lanes), walked in C
+    rb = np.empty(len(rows), dtype=np.int32)
+    sh = np.empty((len(rows), n), dtype=np.uint16)
+    bmin, bmax, lane_ok = _rowpack().pack_rows(rows, n, rb, sh)
+    if bmin < 0 or bmax >= len(basis):
         raise IndexError("row references a basis index out of range")
-    sh = np.fromiter(itertools.chain.from_iterable(map(_get_shift, rows)), dtype=np.int64,
-                     count=len(rows) * n).reshape(len(rows), n)
+    if not lane_ok:
+        raise LaneOverflowError("shift exponent does not fit a 16-bit lane")
     # compare by value: callers may pass the reference's own Closure enum
     one_step = getattr(closure, "value", closure) == Closure.ONE_STEP_REDUCTION.value
     dev = eng.compile(rb, sh, one_step,

@@ -226,3 +226,33 @@ def test_microbench_host_logic_and_no_cpu_fallback():
     if not torch.cuda.is_available():
         with pytest.raises(DeviceError):
             mb.microbench("mod_fma", 16)
+
+
+def test_row_pack_matches_python_conversion():
+    """csrc/rowpack.c (compile_batch's Row list -> int32 basis index + u16
+    shift lanes) against the plain Python conversion, and its error paths."""
+    from paper_2601_06765_b200 import _build
+    from paper_2601_06765_b200.symbolic import Row, RowRole, _rowpack
+
+    _build.build_rowpack()
+    rng = np.random.default_rng(3)
+    n = 6
+    rows = [Row(tuple(int(x) for x in rng.integers(0, 0xFFFF, n)), int(rng.integers(0, 900)), RowRole.REDUCER, i)
+            for i in range(257)]
+    rows.append(Row(tuple(np.int64(x) for x in range(n)), np.int32(7), RowRole.SPOLY_HALF, 0))  # numpy scalars
+    rb = np.empty(len(rows), np.int32)
+    sh = np.empty((len(rows), n), np.uint16)
+    bmin, bmax, ok = _rowpack().pack_rows(rows, n, rb, sh)
+    assert ok and (bmin, bmax) == (min(r.basis_index for r in rows), max(r.basis_index for r in rows))
+    assert (rb == [r.basis_index for r in rows]).all()
+    assert (sh == np.array([r.shift for r in rows], dtype=np.int64)).all()
+    # lane overflow / negative exponent / negative index are reported, not wrapped silently
+    bad = [Row((0,) * (n - 1) + (0x10000,), 1, RowRole.REDUCER, 0), Row((0,) * n, -3, RowRole.REDUCER, 0)]
+    assert _rowpack().pack_rows(bad, n, np.empty(2, np.int32), np.empty((2, n), np.uint16)) == (-3, 1, False)
+    assert _rowpack().pack_rows([Row((0, -1) + (0,) * (n - 2), 0, RowRole.REDUCER, 0)], n, np.empty(1, np.int32),
+                                np.empty((1, n), np.uint16))[2] is False
+    with pytest.raises(ValueError):  # shift of the wrong length
+        _rowpack().pack_rows([Row((1,) * (n - 1), 0, RowRole.REDUCER, 0)], n, np.empty(1, np.int32),
+                             np.empty((1, n), np.uint16))
+    with pytest.raises(ValueError):  # output too small
+        _rowpack().pack_rows(rows, n, np.empty(3, np.int32), sh)
