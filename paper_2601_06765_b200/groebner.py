@@ -18,7 +18,7 @@ from .bulk import ExecPolicy
 from .errors import NonterminationError, PreconditionError, PropertyViolationError
 from .fp import FieldModulus
 from .monomials import Ring, key_pack_vec, mon_div, mon_divides, mon_lcm
-from .polynomials import Poly, SoaPolySet, poly_add_scaled, poly_monic, poly_mul_mon
+from .polynomials import ArrayPoly, Poly, SoaPolySet, poly_add_scaled, poly_monic, poly_mul_mon
 from .sparselin import (EchelonResult, KernelBasis, KernelMode, csr_from_plan, dense_gauss, left_kernel,
                         psge_reduce)
 from .symbolic import BatchSpec, Closure, LayoutPlan, PairTarget, compile_batch, row_lead_cols, select_rows
@@ -120,9 +120,11 @@ class GroebnerState:
         if pairs:
             self.pairs = pairs
 
-    def _push_basis(self, f: Poly):
+    def _push_basis(self, f: Poly, arrays=None):
         self.basis.append(f)
-        if f.terms:
+        if arrays is not None:  # (int64 exps [len, n], uint64 coeffs): the caller's arrays of f's terms
+            ex, cf = arrays
+        elif f.terms:
             ex = np.asarray([e for e, _ in f.terms], dtype=np.int64)
             cf = np.asarray([c for _, c in f.terms], dtype=np.uint64)
         else:
@@ -204,12 +206,15 @@ def _unique_rows(a: np.ndarray):
     return uq, inv.reshape(-1)
 
 
-def update_pairs(state: GroebnerState, new_poly: Poly) -> GroebnerState:
-    """Append a monic polynomial with Gebauer–Möller pruning (reference :154-201)."""
+def update_pairs(state: GroebnerState, new_poly: Poly, *, _arrays=None) -> GroebnerState:
+    """Append a monic polynomial with Gebauer–Möller pruning (reference :154-201).
+
+    ``_arrays`` (internal, f4_step): the polynomial's terms as (int64 exps,
+    uint64 coeffs) arrays, so the host basis copy skips re-reading the tuples."""
     if new_poly.is_zero() or new_poly.lc() != 1:
         raise PreconditionError("basis members must be monic and nonzero")
     t = len(state.basis)
-    state._push_basis(new_poly)
+    state._push_basis(new_poly, _arrays)
     lm_t = np.asarray(new_poly.lm(), dtype=np.int64)
     L = state._hb.lm[:t]
     ring = state.ring
@@ -327,7 +332,8 @@ def f4_step(state: GroebnerState, config: F4Config | None = None, _capture=None)
         c = cols[rp[k]:rp[k + 1]]
         ex = exps_all[c]
         cf = vals[rp[k]:rp[k + 1]]
-        update_pairs(state, Poly(ring, tuple(zip(map(tuple, ex.tolist()), cf.tolist()))))
+        cf64 = cf.astype(np.uint64, copy=False)
+        update_pairs(state, ArrayPoly(ring, ex, cf64), _arrays=(ex, cf64))
         new_ex.append(ex)
         new_cf.append(cf)
         new_len.append(len(c))
