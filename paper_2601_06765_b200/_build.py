@@ -3,9 +3,10 @@
 Every ``csrc/*.cu`` is compiled to an object in parallel, then linked into
 ``paper_2601_06765_b200/libf4b200.so``.  Flags: ``-gencode
 arch=compute_100a,code=sm_100a -O3 -lineinfo``.  Rebuilds only when a source
-or header is newer than the library.  ``csrc/rowpack.c`` (host glue: the
-row-list packing of compile_batch, a CPython extension) is compiled with gcc
-into ``paper_2601_06765_b200/_rowpack*.so``.
+or header is newer than the library.  ``csrc/hostglue.cpp`` (host glue of the
+F4 driver: compile_batch's row-list packing and the Gebauer-Moeller criteria,
+a CPython extension) is compiled with g++ into
+``paper_2601_06765_b200/_hostglue*.so``.
 """
 
 from __future__ import annotations
@@ -45,25 +46,25 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-ROWPACK_SRC = os.path.join(CSRC, "rowpack.c")
-ROWPACK = os.path.join(HERE, "_rowpack" + (sysconfig.get_config_var("EXT_SUFFIX") or ".so"))
+HOSTGLUE_SRC = os.path.join(CSRC, "hostglue.cpp")
+HOSTGLUE = os.path.join(HERE, "_hostglue" + (sysconfig.get_config_var("EXT_SUFFIX") or ".so"))
 
 
-def build_rowpack(force: bool = False) -> str:
-    if not force and os.path.exists(ROWPACK) and os.path.getmtime(ROWPACK) >= os.path.getmtime(ROWPACK_SRC):
-        return ROWPACK
-    tmp = ROWPACK + ".tmp"
-    cmd = [os.environ.get("CC", "gcc"), "-O2", "-shared", "-fPIC", "-Wall", "-I", sysconfig.get_paths()["include"],
-           ROWPACK_SRC, "-o", tmp]
+def build_hostglue(force: bool = False) -> str:
+    if not force and os.path.exists(HOSTGLUE) and os.path.getmtime(HOSTGLUE) >= os.path.getmtime(HOSTGLUE_SRC):
+        return HOSTGLUE
+    tmp = HOSTGLUE + ".tmp"
+    cmd = [os.environ.get("CXX", "g++"), "-O2", "-std=c++17", "-shared", "-fPIC", "-Wall", "-I",
+           sysconfig.get_paths()["include"], HOSTGLUE_SRC, "-o", tmp]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
-        raise RuntimeError(f"gcc failed for {ROWPACK_SRC}:\n{res.stdout}\n{res.stderr}")
-    os.replace(tmp, ROWPACK)
-    return ROWPACK
+        raise RuntimeError(f"g++ failed for {HOSTGLUE_SRC}:\n{res.stdout}\n{res.stderr}")
+    os.replace(tmp, HOSTGLUE)
+    return HOSTGLUE
 
 
 def build(force: bool = False, verbose: bool = False, extra=()) -> str:
-    build_rowpack(force)
+    build_hostglue(force)
     if not force and not _stale():
         return LIB
     os.makedirs(OBJ_DIR, exist_ok=True)

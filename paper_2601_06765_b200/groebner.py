@@ -15,8 +15,9 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from .bulk import ExecPolicy
-from .errors import NonterminationError, PreconditionError, PropertyViolationError
+from .errors import LaneOverflowError, NonterminationError, PreconditionError, PropertyViolationError
 from .fp import FieldModulus
+from .hostglue import native
 from .monomials import Ring, key_pack_vec, mon_div, mon_divides, mon_lcm
 from .polynomials import ArrayPoly, Poly, SoaPolySet, poly_add_scaled, poly_monic, poly_mul_mon
 from .sparselin import (EchelonResult, KernelBasis, KernelMode, csr_from_plan, dense_gauss, left_kernel,
@@ -59,6 +60,7 @@ class _HostBasis:
         self.ring = ring
         n, W = ring.n_vars, ring.n_key_words
         self.T = 0
+        self.keyed = 0  # terms [0, keyed) have their reference keys (packed in soa(), once per batch of appends)
         self.exps = np.zeros((1024, n), dtype=np.int64)
         self.coeff = np.zeros(1024, dtype=np.uint64)
         self.keys = np.zeros((1024, W), dtype=np.uint64)
@@ -77,8 +79,6 @@ class _HostBasis:
                 setattr(self, name, new)
         self.exps[self.T:need] = exps
         self.coeff[self.T:need] = coeff
-        if k:
-            self.keys[self.T:need] = key_pack_vec(exps, self.ring)
         t = len(self.lengths)
         if t >= len(self.lm):
             grown = np.zeros((2 * len(self.lm), self.lm.shape[1]), dtype=np.int64)
@@ -89,6 +89,9 @@ class _HostBasis:
         self.T = need
 
     def soa(self) -> SoaPolySet:
+        if self.keyed < self.T:
+            self.keys[self.keyed:self.T] = key_pack_vec(self.exps[self.keyed:self.T], self.ring)
+            self.keyed = self.T
         lengths = np.asarray(self.lengths, dtype=np.int64)
         offset = np.zeros(len(lengths) + 1, dtype=np.int64)
         np.cumsum(lengths, out=offset[1:])
@@ -215,42 +218,25 @@ def update_pairs(state: GroebnerState, new_poly: Poly, *, _arrays=None) -> Groeb
         raise PreconditionError("basis members must be monic and nonzero")
     t = len(state.basis)
     state._push_basis(new_poly, _arrays)
-    lm_t = np.asarray(new_poly.lm(), dtype=np.int64)
-    L = state._hb.lm[:t]
+    lm_t = np.ascontiguousarray(new_poly.lm(), dtype=np.int64)
+    L = np.ascontiguousarray(state._hb.lm[:t])
     ring = state.ring
-    # new pairs (i, t): chain criterion among themselves
-    lcm = np.maximum(L, lm_t[None, :])
-    if t:
-        uq, inv = _unique_rows(lcm)
-        kept = _minimal_mask(uq)[inv]
-        kept_idx = np.flatnonzero(kept)
-        # one representative per lcm: the lowest partner index
-        _, first = np.unique(inv[kept_idx], return_index=True)
-        reps = np.sort(kept_idx[first])
-        # product criterion on the representative
-        coprime = (np.minimum(L[reps], lm_t[None, :]) == 0).all(axis=1)
-        surv = reps[~coprime]
-    else:
-        surv = np.zeros(0, dtype=np.int64)
-    # chain criterion against queued pairs
-    pl = state._plcm
-    if len(pl):
-        hit = (pl >= lm_t[None, :]).all(axis=1)
-        hit &= (np.maximum(L[state._pi], lm_t) != pl).any(axis=1)
-        hit &= (np.maximum(L[state._pj], lm_t) != pl).any(axis=1)
-        keep_old = ~hit
-    else:
-        keep_old = np.zeros(0, dtype=bool)
-    nl = lcm[surv]
-    pi = np.concatenate([state._pi[keep_old], surv])
-    pj = np.concatenate([state._pj[keep_old], np.full(len(surv), t, dtype=np.int64)])
-    plcm = np.concatenate([pl[keep_old], nl])
-    pdeg = np.concatenate([state._pdeg[keep_old], nl.sum(axis=1)])
-    pkey = np.concatenate([state._pkey[keep_old], key_pack_vec(nl, ring) if len(nl)
-                           else np.zeros((0, ring.n_key_words), np.uint64)])
-    order = np.lexsort((pj, pi) + tuple(pkey[:, w] for w in reversed(range(pkey.shape[1]))) + (pdeg,))
-    state._pi, state._pj, state._plcm = pi[order], pj[order], plcm[order]
-    state._pdeg, state._pkey = pdeg[order], pkey[order]
+    n, W = ring.n_vars, ring.n_key_words
+    # chain criterion among the new pairs (i, t) (one representative per
+    # minimal lcm, the lowest partner) + product criterion, chain criterion
+    # on the queued pairs, and the merge into the sorted queue: one call
+    # into csrc/hostglue.cpp (gm_update)
+    P = len(state._pi)
+    cap = P + t
+    o_pi, o_pj, o_pdeg = np.empty(cap, np.int64), np.empty(cap, np.int64), np.empty(cap, np.int64)
+    o_plcm, o_pkey = np.empty((cap, n), np.int64), np.empty((cap, W), np.uint64)
+    c = np.ascontiguousarray
+    m = native().gm_update(L, t, n, lm_t, int(ring.graded), int(ring.order == "grevlex"), W, c(state._pi),
+                           c(state._pj), c(state._plcm), c(state._pdeg), c(state._pkey), P, o_pi, o_pj, o_plcm,
+                           o_pdeg, o_pkey)
+    if m < 0:
+        raise LaneOverflowError("pair lcm does not fit the 16-bit lanes of the reference key")
+    state._pi, state._pj, state._plcm, state._pdeg, state._pkey = o_pi[:m], o_pj[:m], o_plcm[:m], o_pdeg[:m], o_pkey[:m]
     state._pairs_cache = None
     return state
 

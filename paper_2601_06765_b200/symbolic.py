@@ -17,7 +17,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from .bulk import DEFAULT_POLICY, ExecPolicy
-from .errors import DeviceError, LaneOverflowError, PropertyViolationError, UncoverableTargetError
+from .errors import LaneOverflowError, PropertyViolationError, UncoverableTargetError
+from .hostglue import native
 from .monomials import Ring, key_cmp_rows, key_pack_vec, key_unpack_vec, mon_div, mon_key_pack
 from .polynomials import Poly, SoaPolySet
 
@@ -211,20 +212,61 @@ def row_sort_key(row: Row, ring: Ring):
 def select_rows(spec: BatchSpec, basis: SoaPolySet) -> list:
     """Two S-pair halves per target, optional admissibility filter, then the
     deterministic order (role, pair id, key(shift), basis index)
-    (reference :166-201)."""
+    (reference :166-201).  Shifts and sort keys are computed over arrays;
+    a malformed target takes the per-row path, which raises the reference's
+    error for it."""
     ring = basis.ring
     n_basis = len(basis)
+    targets = list(spec.targets)
+    if not targets:
+        return []
+    n = ring.n_vars
+    fg = np.array([(t.fi, t.gi) for t in targets], dtype=np.int64)
+    bad = np.flatnonzero(((fg < 0) | (fg >= n_basis)).any(axis=1))
+    if len(bad):
+        raise UncoverableTargetError(f"pair {targets[int(bad[0])].pair_id} references unknown basis index")
+    try:
+        lcm = np.array([t.lcm for t in targets], dtype=np.int64)
+    except (ValueError, TypeError):
+        lcm = None
+    idx = fg.reshape(-1)
+    lead = np.asarray(basis.exps)[np.asarray(basis.offset)[idx]].astype(np.int64, copy=False)
+    if lcm is None or lcm.shape != (len(targets), n) or lead.shape != (len(idx), n) or \
+            (np.repeat(lcm, 2, axis=0) < lead).any():
+        return _select_rows_loop(spec, basis, targets)
+    shift = np.repeat(lcm, 2, axis=0) - lead
+    pid = np.repeat(np.array([t.pair_id for t in targets], dtype=np.int64), 2)
+    rows = [Row(sh, k, RowRole.SPOLY_HALF, q)
+            for sh, k, q in zip(map(tuple, shift.tolist()), idx.tolist(), pid.tolist())]
+    if spec.adm is not None:
+        keep = np.fromiter((bool(spec.adm(r.shift, r.basis_index, r.role, r.provenance)) for r in rows),
+                           dtype=bool, count=len(rows))
+        alive = set(pid[keep].tolist())
+        for tgt in targets:
+            if tgt.pair_id not in alive:
+                raise UncoverableTargetError(f"target {tgt.lcm} of pair {tgt.pair_id} has no admissible rows")
+        sel = np.flatnonzero(keep)
+        rows = [rows[i] for i in sel.tolist()]
+        shift, idx, pid = shift[sel], idx[sel], pid[sel]
+    if not rows:
+        return rows
+    # (role, pair id, key(shift), basis index); every row here is an S-half
+    keys = key_pack_vec(shift, ring)
+    order = np.lexsort((idx,) + tuple(keys[:, w] for w in reversed(range(keys.shape[1]))) + (pid,))
+    return [rows[i] for i in order.tolist()]
+
+
+def _select_rows_loop(spec: BatchSpec, basis: SoaPolySet, targets: list) -> list:
+    ring = basis.ring
     rows = []
-    for tgt in spec.targets:
-        if not (0 <= tgt.fi < n_basis and 0 <= tgt.gi < n_basis):
-            raise UncoverableTargetError(f"pair {tgt.pair_id} references unknown basis index")
+    for tgt in targets:
         for k in (tgt.fi, tgt.gi):
             lead = tuple(int(x) for x in basis.exps[int(basis.offset[k])])
             rows.append(Row(mon_div(tgt.lcm, lead), k, RowRole.SPOLY_HALF, tgt.pair_id))
     if spec.adm is not None and rows:
         kept = [r for r in rows if spec.adm(r.shift, r.basis_index, r.role, r.provenance)]
         alive = {r.provenance for r in kept}
-        for tgt in spec.targets:
+        for tgt in targets:
             if tgt.pair_id not in alive:
                 raise UncoverableTargetError(f"target {tgt.lcm} of pair {tgt.pair_id} has no admissible rows")
         rows = kept
@@ -236,21 +278,6 @@ def _empty_plan(ring: Ring) -> LayoutPlan:
     return LayoutPlan(ring, np.zeros(1, np.int64), np.zeros(0, np.int64), np.zeros(0, np.uint64),
                       np.zeros((0, ring.n_key_words), np.uint64), (), PlanCounters(),
                       {"dict_build_ns": 0, "row_assemble_ns": 0})
-
-
-_ROWPACK = None
-
-
-def _rowpack():
-    """The row-list packer (csrc/rowpack.c, built in-tree by _build)."""
-    global _ROWPACK
-    if _ROWPACK is None:
-        try:
-            from . import _rowpack as m
-        except ImportError as e:
-            raise DeviceError("paper_2601_06765_b200/_rowpack is not built (run __graft_entry__.build())") from e
-        _ROWPACK = m
-    return _ROWPACK
 
 
 def compile_batch(rows, basis: SoaPolySet, closure: Closure = Closure.ONE_STEP_REDUCTION,
@@ -276,7 +303,7 @@ def compile_batch(rows, basis: SoaPolySet, closure: Closure = Closure.ONE_STEP_R
     # the Row list -> (int32 basis index, u16 shift lanes), walked in C
     rb = np.empty(len(rows), dtype=np.int32)
     sh = np.empty((len(rows), n), dtype=np.uint16)
-    bmin, bmax, lane_ok = _rowpack().pack_rows(rows, n, rb, sh)
+    bmin, bmax, lane_ok = native().pack_rows(rows, n, rb, sh)
     if bmin < 0 or bmax >= len(basis):
         raise IndexError("row references a basis index out of range")
     if not lane_ok:

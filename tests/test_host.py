@@ -229,12 +229,14 @@ def test_microbench_host_logic_and_no_cpu_fallback():
 
 
 def test_row_pack_matches_python_conversion():
-    """csrc/rowpack.c (compile_batch's Row list -> int32 basis index + u16
-    shift lanes) against the plain Python conversion, and its error paths."""
+    """csrc/hostglue.cpp pack_rows (compile_batch's Row list -> int32 basis
+    index + u16 shift lanes) against the plain Python conversion, and its
+    error paths."""
     from paper_2601_06765_b200 import _build
-    from paper_2601_06765_b200.symbolic import Row, RowRole, _rowpack
+    from paper_2601_06765_b200.hostglue import native as _rowpack
+    from paper_2601_06765_b200.symbolic import Row, RowRole
 
-    _build.build_rowpack()
+    _build.build_hostglue()
     rng = np.random.default_rng(3)
     n = 6
     rows = [Row(tuple(int(x) for x in rng.integers(0, 0xFFFF, n)), int(rng.integers(0, 900)), RowRole.REDUCER, i)
@@ -256,3 +258,145 @@ def test_row_pack_matches_python_conversion():
                              np.empty((1, n), np.uint16))
     with pytest.raises(ValueError):  # output too small
         _rowpack().pack_rows(rows, n, np.empty(3, np.int32), sh)
+
+
+def _gm_numpy(L, lm_t, pi, pj, plcm):
+    """NumPy statement of the Gebauer–Möller criteria (reference
+    groebner.py:154-201), the checker for csrc/hostglue.cpp."""
+    from paper_2601_06765_b200.groebner import _unique_rows
+
+    t = len(L)
+    lcm = np.maximum(L, lm_t[None, :])
+    if t:
+        uq, inv = _unique_rows(lcm)
+        kept_idx = np.flatnonzero(_minimal_mask(uq)[inv])
+        _, first = np.unique(inv[kept_idx], return_index=True)
+        reps = np.sort(kept_idx[first])
+        coprime = (np.minimum(L[reps], lm_t[None, :]) == 0).all(axis=1)
+        surv = reps[~coprime]
+    else:
+        surv = np.zeros(0, dtype=np.int64)
+    if len(plcm):
+        hit = (plcm >= lm_t[None, :]).all(axis=1)
+        hit &= (np.maximum(L[pi], lm_t) != plcm).any(axis=1)
+        hit &= (np.maximum(L[pj], lm_t) != plcm).any(axis=1)
+    else:
+        hit = np.zeros(0, dtype=bool)
+    return surv, ~hit
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_gm_criteria_native_matches_numpy(seed):
+    """gm_new_pairs / gm_prune against the NumPy statement on random leading
+    monomials (small exponents: many equal lcms, divisibility chains and
+    coprime pairs), including the queued pairs a run accumulates."""
+    from paper_2601_06765_b200 import _build
+    from paper_2601_06765_b200.hostglue import native
+
+    _build.build_hostglue()
+    hg = native()
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(2, 7))
+    L = np.zeros((0, n), np.int64)
+    pi = np.zeros(0, np.int64)
+    pj = np.zeros(0, np.int64)
+    plcm = np.zeros((0, n), np.int64)
+    for t in range(120):
+        lm_t = np.ascontiguousarray(rng.integers(0, 4, n) * (rng.random(n) < 0.6), dtype=np.int64)
+        want_s, want_k = _gm_numpy(L, lm_t, pi, pj, plcm)
+        surv = np.empty(t, np.int64)
+        surv = surv[:hg.gm_new_pairs(np.ascontiguousarray(L), t, n, lm_t, surv)]
+        keep = np.ones(len(pi), np.uint8)
+        if len(pi):
+            assert hg.gm_prune(plcm, pi, pj, len(pi), np.ascontiguousarray(L), n, lm_t, keep) == int(want_k.sum())
+        assert surv.tolist() == want_s.tolist()
+        assert keep.view(bool).tolist() == want_k.tolist()
+        keep = keep.view(bool)
+        pi = np.concatenate([pi[keep], surv])
+        pj = np.concatenate([pj[keep], np.full(len(surv), t, np.int64)])
+        plcm = np.ascontiguousarray(np.concatenate([plcm[keep], np.maximum(L[surv], lm_t)]))
+        L = np.ascontiguousarray(np.concatenate([L, lm_t[None, :]]))
+        if rng.random() < 0.2 and len(pi):  # a select_batch pops a prefix
+            k = int(rng.integers(1, len(pi) + 1))
+            pi, pj, plcm = pi[k:], pj[k:], np.ascontiguousarray(plcm[k:])
+    with pytest.raises(IndexError):
+        hg.gm_prune(np.zeros((1, n), np.int64), np.array([5], np.int64), np.array([0], np.int64), 1,
+                    np.zeros((2, n), np.int64), n, np.zeros(n, np.int64), np.ones(1, np.uint8))
+
+
+def test_select_rows_arrays_match_row_loop():
+    """select_rows (shifts and keys over arrays) equals the per-row statement
+    (reference symbolic.py:166-201), with and without an admissibility filter,
+    and raises the same errors."""
+    import dataclasses
+
+    from paper_2601_06765_b200.symbolic import _select_rows_loop
+
+    for ring, polys in (gen_cyclic(6, 32003), gen_katsura(5, 32003)):
+        st = GroebnerState(ring)
+        for f in polys:
+            update_pairs(st, poly_monic(f))
+        spec, _ = select_batch(st)
+        soa = st.soa()
+        assert select_rows(spec, soa) == _select_rows_loop(spec, soa, list(spec.targets))
+        adm = dataclasses.replace(spec, adm=lambda sh, b, role, prov: (b + prov) % 3 != 0)
+        try:
+            want = _select_rows_loop(adm, soa, list(adm.targets))
+        except errors.UncoverableTargetError:
+            with pytest.raises(errors.UncoverableTargetError):
+                select_rows(adm, soa)
+        else:
+            assert select_rows(adm, soa) == want
+        t0 = spec.targets[0]
+        bad = dataclasses.replace(spec, targets=(dataclasses.replace(t0, lcm=tuple(0 for _ in t0.lcm)),))
+        with pytest.raises(errors.DivisionError):
+            select_rows(bad, soa)
+        bad = dataclasses.replace(spec, targets=(dataclasses.replace(t0, gi=len(soa)),))
+        with pytest.raises(errors.UncoverableTargetError):
+            select_rows(bad, soa)
+
+
+@pytest.mark.parametrize("order", ["grevlex", "lex", "deglex"])
+@pytest.mark.parametrize("seed", range(3))
+def test_gm_update_native_matches_numpy_queue(order, seed):
+    """gm_update (criteria + reference keys + merge into the sorted queue)
+    against the NumPy update: concatenate, key_pack_vec, lexsort on
+    (degree, key(lcm), i, j) — reference Pair.sort_tuple, groebner.py:110-116."""
+    from paper_2601_06765_b200 import _build
+    from paper_2601_06765_b200.hostglue import native
+
+    _build.build_hostglue()
+    hg = native()
+    rng = np.random.default_rng(100 + seed)
+    n = int(rng.integers(2, 7))
+    ring = Ring([f"x{i}" for i in range(n)], order, FieldModulus(32003))
+    W = ring.n_key_words
+    L = np.zeros((0, n), np.int64)
+    q = {"pi": np.zeros(0, np.int64), "pj": np.zeros(0, np.int64), "plcm": np.zeros((0, n), np.int64),
+         "pdeg": np.zeros(0, np.int64), "pkey": np.zeros((0, W), np.uint64)}
+    for t in range(100):
+        lm_t = np.ascontiguousarray(rng.integers(0, 4, n) * (rng.random(n) < 0.6), dtype=np.int64)
+        surv, keep = _gm_numpy(L, lm_t, q["pi"], q["pj"], q["plcm"])
+        nl = np.maximum(L[surv], lm_t)
+        pi = np.concatenate([q["pi"][keep], surv])
+        pj = np.concatenate([q["pj"][keep], np.full(len(surv), t, np.int64)])
+        plcm = np.concatenate([q["plcm"][keep], nl])
+        pdeg = np.concatenate([q["pdeg"][keep], nl.sum(axis=1)])
+        pkey = np.concatenate([q["pkey"][keep], key_pack_vec(nl, ring) if len(nl) else np.zeros((0, W), np.uint64)])
+        o = np.lexsort((pj, pi) + tuple(pkey[:, w] for w in reversed(range(W))) + (pdeg,))
+        want = {"pi": pi[o], "pj": pj[o], "plcm": plcm[o], "pdeg": pdeg[o], "pkey": pkey[o]}
+        P, cap = len(q["pi"]), len(q["pi"]) + t
+        out = {"pi": np.empty(cap, np.int64), "pj": np.empty(cap, np.int64), "plcm": np.empty((cap, n), np.int64),
+               "pdeg": np.empty(cap, np.int64), "pkey": np.empty((cap, W), np.uint64)}
+        c = np.ascontiguousarray
+        m = hg.gm_update(c(L), t, n, lm_t, int(ring.graded), int(order == "grevlex"), W, c(q["pi"]), c(q["pj"]),
+                         c(q["plcm"]), c(q["pdeg"]), c(q["pkey"]), P, out["pi"], out["pj"], out["plcm"],
+                         out["pdeg"], out["pkey"])
+        assert m == len(want["pi"])
+        for k in want:
+            assert np.array_equal(out[k][:m], want[k]), (t, k)
+        q = {k: c(v[:m]) for k, v in out.items()}
+        L = np.concatenate([L, lm_t[None, :]])
+        if rng.random() < 0.2 and m:
+            k = int(rng.integers(1, m + 1))
+            q = {kk: c(v[k:]) for kk, v in q.items()}

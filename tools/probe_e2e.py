@@ -24,7 +24,8 @@ def main():
 
     from paper_2601_06765_b200.engine import Engine, host_empty
     from paper_2601_06765_b200.polynomials import SoaPolySet
-    from paper_2601_06765_b200.symbolic import DICT_CAP, _rowpack
+    from paper_2601_06765_b200.hostglue import native
+    from paper_2601_06765_b200.symbolic import DICT_CAP
 
     ring, st, batches, _ = bench.capture_workload()
     eng = Engine.for_ring(ring)
@@ -60,7 +61,7 @@ def main():
                 rows = b["rows"]
                 rb = np.empty(len(rows), dtype=np.int32)
                 sh = np.empty((len(rows), n), dtype=np.uint16)
-                _rowpack().pack_rows(rows, n, rb, sh)
+                native().pack_rows(rows, n, rb, sh)
             t2 = time.perf_counter()
             if b is not None:
                 dev = eng.compile(rb, sh, True, None, DICT_CAP)
