@@ -777,12 +777,14 @@ def run_e2e(args, ring, st, batches, eng, torch):
                 consume(pending)
             pending = plan
             e_M += b["M"]
-            # bytes moved: new basis terms as the reference streams them
-            # (int64 exps + uint64 coeff, narrowed on the device), their
+            # bytes moved: new basis terms as the SoaPolySet holds them (the
+            # uint64 reference keys when W < n words, else the int64 exps,
+            # + uint64 coeff; unpacked / narrowed on the device), their
             # lengths + offsets, back their LM / max exponents; rows (basis
             # index + shift); back: row_ptr / col_ind / val (64-bit) and
             # dict_keys (reference key words)
-            h2d += (nt - prev_nt) * (8 * n + 8) + (nb_ - prev_nb) * 16 + len(b["rows"]) * (4 + 2 * n)
+            W = ring.n_key_words
+            h2d += (nt - prev_nt) * (8 * min(W, n) + 8) + (nb_ - prev_nb) * 16 + len(b["rows"]) * (4 + 2 * n)
             d2h += ((nb_ - prev_nb) * 4 * n + (plan.counters.r + 1) * 8 + plan.counters.M * 16
                     + plan.counters.N * 8 * ring.n_key_words)
             prev_nt, prev_nb = nt, nb_

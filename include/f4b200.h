@@ -104,6 +104,15 @@ int f4b_basis_append_wide(f4b_ctx* ctx, int64_t n_polys, const int64_t* lengths,
  * stay valid until that call.  f4b_basis_sync completes it explicitly. */
 int f4b_basis_append_wide_async(f4b_ctx* ctx, int64_t n_polys, const int64_t* lengths,
                                 const int64_t* exps, const uint64_t* coeffs);
+/* Same as f4b_basis_append_wide_async with the terms given by the reference
+ * keys of the SoaPolySet (mon_key [T][key_words] uint64, monomials.py
+ * mon_key_pack / key_pack_vec) instead of the int64 exponent rows: 8 W bytes
+ * per term up instead of 8 n (cyclic-8: 24 instead of 64).  The exponents are
+ * recovered from the 16-bit lanes on the device; a degree lane that differs
+ * from the lanes' sum, or nonzero padding bits, is F4B_ERR_PROPERTY (the
+ * reference's CorruptKeyError condition, key_unpack_vec). */
+int f4b_basis_append_keys_async(f4b_ctx* ctx, int64_t n_polys, const int64_t* lengths,
+                                const uint64_t* keys, int key_words, const uint64_t* coeffs);
 int f4b_basis_sync(f4b_ctx* ctx);
 int f4b_basis_size(const f4b_ctx* ctx, int64_t* n_polys, int64_t* n_terms);
 

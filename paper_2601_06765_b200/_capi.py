@@ -63,6 +63,7 @@ SIGNATURES = {
     "f4b_basis_append": (C.c_int, [C.c_void_p, C.c_int64, i64p, u16p, u32p]),
     "f4b_basis_append_wide": (C.c_int, [C.c_void_p, C.c_int64, i64p, i64p, u64p]),
     "f4b_basis_append_wide_async": (C.c_int, [C.c_void_p, C.c_int64, i64p, i64p, u64p]),
+    "f4b_basis_append_keys_async": (C.c_int, [C.c_void_p, C.c_int64, i64p, u64p, C.c_int, u64p]),
     "f4b_basis_sync": (C.c_int, [C.c_void_p]),
     "f4b_bm": (C.c_int, [C.c_void_p, u64p, C.c_int64, C.c_int64, u64p, i64p]),
     "f4b_basis_size": (C.c_int, [C.c_void_p, i64p, i64p]),

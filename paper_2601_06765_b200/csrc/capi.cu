@@ -551,6 +551,42 @@ __global__ void k_narrow_terms(const int64_t* __restrict__ e64, const uint64_t* 
   if (flags) atomicOr(bad, flags);
 }
 
+// The same from the reference keys (monomials.py mon_key_pack: MSB first,
+// [32-bit degree if graded] then one 16-bit lane per variable, grevlex lanes
+// 0xFFFF - e in reversed variable order; W words per key): exponents
+// recovered from the lanes, the degree lane checked against their sum
+// (flag 4: corrupt key) and the padding bits against zero.
+__global__ void k_narrow_keys(const uint64_t* __restrict__ keys, int W, int order, const uint64_t* __restrict__ c64,
+                              long long T, int n, uint32_t p, uint16_t* __restrict__ e16, uint32_t* __restrict__ c32,
+                              uint32_t* __restrict__ bad) {
+  uint32_t flags = 0;
+  const bool graded = order != 2, grevlex = order == 0;
+  const int head = graded ? 32 : 0;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < T; t += (long long)gridDim.x * blockDim.x) {
+    const uint64_t* k = keys + t * W;
+    uint64_t deg = 0;
+    for (int i = 0; i < n; ++i) {
+      const int off = head + 16 * i;
+      const uint32_t lane = (uint32_t)(k[off >> 6] >> (48 - (off & 63))) & 0xFFFFu;
+      const uint32_t e = grevlex ? 0xFFFFu - lane : lane;
+      e16[t * n + (grevlex ? n - 1 - i : i)] = (uint16_t)e;
+      deg += e;
+    }
+    if (graded && (k[0] >> 32) != deg) flags |= 4u;
+    const int used = head + 16 * n;  // padding bits below the last lane
+    if (used < 64 * W) {
+      const int w = used >> 6, b = used & 63;
+      if (b && (k[w] << b) != 0) flags |= 4u;
+      for (int x = w + (b ? 1 : 0); x < W; ++x)
+        if (k[x]) flags |= 4u;
+    }
+    const uint64_t cc = c64[t];
+    if (cc == 0 || cc >= p) flags |= 2u;
+    c32[t] = (uint32_t)cc;
+  }
+  if (flags) atomicOr(bad, flags);
+}
+
 // per polynomial (warp each): offset, length, LM exponents, max exponent per variable
 __global__ void k_poly_meta(const uint16_t* __restrict__ e16, const int64_t* __restrict__ lens, long long P,
                             long long T0, int n, uint32_t* __restrict__ off, uint32_t* __restrict__ len,
@@ -579,8 +615,10 @@ __global__ void k_poly_meta(const uint16_t* __restrict__ e16, const int64_t* __r
 // Issue an append of the reference's int64 / uint64 streams (narrowing,
 // range checks, LM / max exponents on the device) without waiting: the host
 // mirrors and the error flag are completed by basis_finish.
+// keys != nullptr: the terms come as reference keys (W words each) instead of
+// int64 exponent rows (exps unused).
 static void basis_append_wide_issue(Ctx* c, int64_t n_polys, const int64_t* lengths, const int64_t* exps,
-                                    const uint64_t* coeffs) {
+                                    const uint64_t* coeffs, const uint64_t* keys = nullptr, int W = 0) {
   basis_finish(c);  // the staging block is reused
   Basis& B = c->basis;
   const int n = c->n_vars;
@@ -602,7 +640,9 @@ static void basis_append_wide_issue(Ctx* c, int64_t n_polys, const int64_t* leng
   // raw streams -> device staging -> narrowed basis streams
   Ctx::PendingAppend& pa = c->pend;
   DBuf& raw = pa.raw;
-  const size_t b_e = (size_t)T * n * 8, b_c = (size_t)T * 8, b_l = (size_t)std::max<long long>(n_polys, 1) * 8,
+  if (keys && (W < 1 || W > 8 || (c->order != 2 ? 32 : 0) + 16 * n > 64 * W))
+    fail(F4B_ERR_PRECONDITION, "key words do not match the ring");
+  const size_t b_e = keys ? (size_t)T * W * 8 : (size_t)T * n * 8, b_c = (size_t)T * 8, b_l = (size_t)std::max<long long>(n_polys, 1) * 8,
                b_p = (size_t)(n_polys + 1) * 8;
   ensure(c, raw, b_e + b_c + b_l + b_p + 64);
   unsigned char* rp = raw.as<unsigned char>();
@@ -632,15 +672,20 @@ static void basis_append_wide_issue(Ctx* c, int64_t n_polys, const int64_t* leng
   *reinterpret_cast<u32*>(ha + o_tail) = (u32)T1;  // the basis end offset off[P1]
   check_cuda(cudaMemsetAsync(d_bad, 0, 4, c->stream), "memset");
   if (T) {
-    check_cuda(cudaMemcpyAsync(d_e, exps, b_e, cudaMemcpyHostToDevice, c->stream), "h2d exps");
+    check_cuda(cudaMemcpyAsync(d_e, keys ? (const void*)keys : (const void*)exps, b_e, cudaMemcpyHostToDevice,
+                               c->stream), "h2d exps");
     check_cuda(cudaMemcpyAsync(d_c, coeffs, b_c, cudaMemcpyHostToDevice, c->stream), "h2d coeffs");
   }
   if (n_polys)
     check_cuda(cudaMemcpyAsync(d_l, ha + o_len, o_tail - o_len, cudaMemcpyHostToDevice, c->stream), "h2d lens+pre");
   if (T) {
     const int g = (int)std::min<long long>((T + 255) / 256, (long long)c->num_sms * 8);
-    F4B_LAUNCH(c, k_narrow_terms, g, 256, 0, d_e, d_c, T, n, c->p, B.exps.as<u16>() + T0 * n, B.coeff.as<u32>() + T0,
-               d_bad);
+    if (keys)
+      F4B_LAUNCH(c, k_narrow_keys, g, 256, 0, reinterpret_cast<const uint64_t*>(d_e), W, c->order, d_c, T, n, c->p,
+                 B.exps.as<u16>() + T0 * n, B.coeff.as<u32>() + T0, d_bad);
+    else
+      F4B_LAUNCH(c, k_narrow_terms, g, 256, 0, d_e, d_c, T, n, c->p, B.exps.as<u16>() + T0 * n,
+                 B.coeff.as<u32>() + T0, d_bad);
   }
   if (n_polys) {
     F4B_LAUNCH(c, k_poly_meta, (int)((n_polys * 32 + 255) / 256), 256, 0, B.exps.as<u16>() + T0 * n, d_l, n_polys, T0,
@@ -676,6 +721,7 @@ static void basis_finish_impl(Ctx* c) {
   // a rejected append leaves the basis as it was (n_terms / n_polys not advanced)
   if (bad & 1u) fail(F4B_ERR_LANE_OVERFLOW, "exponent does not fit a 16-bit lane");
   if (bad & 2u) fail(F4B_ERR_PROPERTY, "basis coefficient outside [1, p)");
+  if (bad & 4u) fail(F4B_ERR_PROPERTY, "basis key lanes are internally inconsistent");
   for (long long i = 0; i < pa.n_polys; ++i) {
     B.h_len.push_back(pa.lengths[i]);
     B.h_off.push_back(B.h_off.back() + pa.lengths[i]);
@@ -702,6 +748,14 @@ int f4b_basis_append_wide_async(f4b_ctx* h, int64_t n_polys, const int64_t* leng
   if (!h) return F4B_ERR_PRECONDITION;
   API_BEGIN(&h->c)
   basis_append_wide_issue(_c, n_polys, lengths, exps, coeffs);
+  API_END
+}
+
+int f4b_basis_append_keys_async(f4b_ctx* h, int64_t n_polys, const int64_t* lengths, const uint64_t* keys,
+                                int key_words, const uint64_t* coeffs) {
+  if (!h) return F4B_ERR_PRECONDITION;
+  API_BEGIN(&h->c)
+  basis_append_wide_issue(_c, n_polys, lengths, nullptr, coeffs, keys, key_words);
   API_END
 }
 

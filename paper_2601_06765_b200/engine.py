@@ -339,14 +339,33 @@ class Engine:
         self._reset_mirror()
         self.generation += 1
 
-    def append_polys(self, lengths, exps, coeffs, defer: bool = False):
+    def append_polys(self, lengths, exps, coeffs, defer: bool = False, keys=None):
         """Append polynomials to the device basis.  With ``defer`` (the
         reference-format int64 / uint64 streams only) the call returns without
         waiting for the device; range errors then surface from the next
-        compile (the caller keeps ``exps`` / ``coeffs`` alive until then)."""
+        compile (the caller keeps ``exps`` / ``coeffs`` alive until then).
+        ``keys`` (with ``defer``): the SoaPolySet's reference keys of the same
+        terms, uploaded instead of the exponent rows (8 W instead of 8 n bytes
+        per term; the device unpacks the lanes)."""
         lengths = np.ascontiguousarray(lengths, dtype=np.int64)
         exps = np.asarray(exps)
         coeffs = np.asarray(coeffs)
+        W = ((32 if self.order != "lex" else 0) + 16 * self.n_vars + 63) // 64  # reference key words (monomials.Ring)
+        if (defer and keys is not None and keys.dtype == np.uint64 and keys.ndim == 2 and keys.shape[1] == W
+                and keys.flags.c_contiguous and coeffs.dtype == np.uint64 and coeffs.flags.c_contiguous
+                and W < self.n_vars):
+            self.ctx.sync_stream()
+            self.ctx.check(self.lib.f4b_basis_append_keys_async(self.ctx.h, len(lengths), ptr(lengths, C.c_int64),
+                                                                ptr(keys, C.c_uint64), W, ptr(coeffs, C.c_uint64)),
+                           "basis append")
+            self._deferred = (lengths, keys, coeffs)  # host buffers read by the pending copy
+            self._lens = np.concatenate([self._lens, lengths])
+            if len(coeffs):
+                self._chunks.append((self._T, exps, coeffs))
+            self._T += len(coeffs)
+            self._src = None
+            self.generation += 1
+            return
         if (exps.dtype == np.int64 and coeffs.dtype == np.uint64 and exps.ndim == 2
                 and exps.flags.c_contiguous and coeffs.flags.c_contiguous):
             # the reference's SoaPolySet streams as they are: narrowing, range
@@ -426,7 +445,8 @@ class Engine:
             self.clear_basis()
         n_dev, T_dev = self.n_polys, self._T
         if len(soa) > n_dev:
-            self.append_polys(soa.length[n_dev:], soa.exps[T_dev:], soa.coeff[T_dev:], defer=True)
+            self.append_polys(soa.length[n_dev:], soa.exps[T_dev:], soa.coeff[T_dev:], defer=True,
+                              keys=soa.mon_key[T_dev:])
         self._src = self._buffers(soa)
         self._src_refs = (soa.exps, soa.coeff)
         soa._f4b_token = self.token

@@ -403,6 +403,41 @@ def test_basis_append_wide_matches_narrow(cuda):
     eng.clear_basis()
 
 
+@pytest.mark.parametrize("order", ["grevlex", "deglex", "lex"])
+def test_basis_append_keys_matches_exps(cuda, order):
+    """f4b_basis_append_keys_async (the SoaPolySet's reference keys uploaded
+    instead of the int64 exponent rows, lanes unpacked on the device) builds
+    the same device basis as the exponent path; a corrupt key (degree lane
+    != lane sum, or nonzero padding) is PropertyViolationError."""
+    from paper_2601_06765_b200.engine import Engine
+
+    rng = np.random.default_rng(11)
+    ring = Ring(["a", "b", "c", "d", "e", "f"], order, FieldModulus(32003))
+    assert ring.n_key_words < ring.n_vars
+    polys = [_random_poly(rng, ring, 5, 12) for _ in range(9)]
+    soa = soa_pack(polys, ring)
+    rows = [Row(tuple(int(x) for x in rng.integers(0, 3, 6)), int(k), RowRole.SPOLY_HALF, 0) for k in range(9)]
+    rb, sh = np.array([r.basis_index for r in rows]), np.array([r.shift for r in rows])
+    eng = Engine.for_ring(ring)
+    got = []
+    for keys in (soa.mon_key, None):
+        eng.clear_basis()
+        eng.append_polys(soa.length, soa.exps, soa.coeff, defer=True, keys=keys)
+        got.append(eng.compile(rb, sh, True).download())
+    for k in got[0]:
+        assert np.array_equal(got[0][k], got[1][k]), k
+    bad = soa.mon_key.copy()
+    if ring.graded:
+        bad[4, 0] += np.uint64(1 << 32)  # degree lane off by one
+    else:
+        bad[4, -1] |= np.uint64(1)  # padding bit below the last lane
+    eng.clear_basis()
+    eng.append_polys(soa.length, soa.exps, soa.coeff, defer=True, keys=bad)
+    with pytest.raises(errors.PropertyViolationError):
+        eng.compile(rb, sh, True)
+    eng.clear_basis()
+
+
 @pytest.mark.parametrize("name,gen,args", [("cyclic5_p32003", gen_cyclic, (5, 32003)),
                                            ("katsura6_p32003", gen_katsura, (6, 32003))])
 def test_reduce_basis_device_matches_host(cuda, name, gen, args):
