@@ -451,6 +451,7 @@ int f4b_basis_clear(f4b_ctx* h) {
   if (!h) return F4B_ERR_PRECONDITION;
   if (h->c.pend.active) {  // a pending append is discarded with the basis
     h->c.pend.active = false;
+    h->c.pend.applied = false;
     cudaStreamSynchronize(h->c.stream);
     release(&h->c, h->c.pend.raw);
   }
@@ -700,12 +701,54 @@ static void basis_append_wide_issue(Ctx* c, int64_t n_polys, const int64_t* leng
   check_cuda(cudaMemcpyAsync(ha + o_bad, d_bad, 4, cudaMemcpyDeviceToHost, c->stream), "d2h");
   pa.active = true;
   pa.n_polys = n_polys;
+  pa.T0 = T0;
+  pa.P0 = P0;
   pa.T1 = T1;
   pa.P1 = P1;
+  pa.applied = false;
+  pa.lazy_ok = keys != nullptr && c->order != 2;
+  if (pa.lazy_ok) {
+    // LMs from the host keys (same lanes as k_narrow_keys), bound deg(LM)
+    pa.lm_host.assign((size_t)n_polys * n, 0);
+    pa.bound_host.assign((size_t)n_polys * n, 0);
+    const bool grevlex = c->order == 0;
+    for (long long i = 0; i < n_polys; ++i) {
+      if (!lengths[i]) continue;
+      const uint64_t* k = keys + (size_t)pre[i] * W;
+      const uint64_t deg = k[0] >> 32;
+      for (int q = 0; q < n; ++q) {
+        const int off = 32 + 16 * q;
+        const uint32_t lane = (uint32_t)(k[off >> 6] >> (48 - (off & 63))) & 0xFFFFu;
+        pa.lm_host[(size_t)i * n + (grevlex ? n - 1 - q : q)] = (uint16_t)(grevlex ? 0xFFFFu - lane : lane);
+      }
+      for (int v = 0; v < n; ++v) pa.bound_host[(size_t)i * n + v] = (uint16_t)std::min<uint64_t>(deg, 0xFFFFu);
+    }
+  }
   pa.o_lm = o_lm;
   pa.o_mx = o_mx;
   pa.o_bad = o_bad;
   pa.lengths.assign(lengths, lengths + n_polys);
+}
+
+static bool basis_apply_lazy_impl(Ctx* c) {
+  Ctx::PendingAppend& pa = c->pend;
+  if (!pa.active) return false;
+  if (!pa.lazy_ok) {
+    basis_finish(c);
+    return false;
+  }
+  if (pa.applied) return true;
+  Basis& B = c->basis;
+  for (long long i = 0; i < pa.n_polys; ++i) {
+    B.h_len.push_back(pa.lengths[i]);
+    B.h_off.push_back(B.h_off.back() + pa.lengths[i]);
+  }
+  B.h_lm.insert(B.h_lm.end(), pa.lm_host.begin(), pa.lm_host.end());
+  B.h_maxe.insert(B.h_maxe.end(), pa.bound_host.begin(), pa.bound_host.end());
+  B.n_terms = pa.T1;
+  B.n_polys = (int)pa.P1;
+  pa.applied = true;
+  return true;
 }
 
 static void basis_finish_impl(Ctx* c) {
@@ -718,6 +761,28 @@ static void basis_finish_impl(Ctx* c) {
   const unsigned char* ha = static_cast<const unsigned char*>(c->h_app);
   const uint32_t bad = *reinterpret_cast<const u32*>(ha + pa.o_bad);
   release(c, pa.raw);
+  if (pa.applied) {
+    pa.applied = false;
+    if (bad) {
+      // roll the mirrors back to the basis before this append
+      B.h_len.resize((size_t)pa.P0);
+      B.h_off.resize((size_t)pa.P0 + 1);
+      B.h_lm.resize((size_t)pa.P0 * n);
+      B.h_maxe.resize((size_t)pa.P0 * n);
+      B.n_terms = pa.T0;
+      B.n_polys = (int)pa.P0;
+      if (B.lm_sorted > pa.P0) {
+        B.lm_order.clear();
+        B.lm_sorted = 0;
+      }
+      B.lmw_polys = std::min<int>(B.lmw_polys, (int)pa.P0);
+      B.ckey_terms = std::min<long long>(B.ckey_terms, pa.T0);
+    } else {
+      const uint16_t* hmx = reinterpret_cast<const uint16_t*>(ha + pa.o_mx);
+      std::copy(hmx, hmx + (size_t)pa.n_polys * n, B.h_maxe.begin() + (size_t)pa.P0 * n);
+      return;
+    }
+  }
   // a rejected append leaves the basis as it was (n_terms / n_polys not advanced)
   if (bad & 1u) fail(F4B_ERR_LANE_OVERFLOW, "exponent does not fit a 16-bit lane");
   if (bad & 2u) fail(F4B_ERR_PROPERTY, "basis coefficient outside [1, p)");
@@ -786,8 +851,19 @@ int f4b_compile_batch(f4b_ctx* h, int64_t n_rows, const int32_t* row_basis, cons
   pl->ctx = &h->c;
   API_BEGIN(&h->c)
   try {
-    basis_finish(_c);
+    static const bool htrace = getenv("F4B_HOST_TRACE") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
+    // a pending key append is not waited for: the compile is queued behind
+    // it on the stream, its check completes after the compile (below)
+    const bool lazy = basis_apply_lazy_impl(_c);
+    if (htrace)
+      fprintf(stderr, "[host] basis_finish %.1f us\n",
+              std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count());
     compile_batch(_c, n_rows, row_basis, row_shift, closure, candidates, n_candidates, dict_cap, pl);
+    if (lazy) {
+      basis_finish_impl(_c);  // the append's flag (fails with its error) and the exact maximum exponents
+      recheck_lanes(_c, n_rows, row_basis, row_shift);
+    }
   } catch (...) {
     plan_release(pl);
     throw;
@@ -1140,3 +1216,4 @@ int f4b_mod_fma(f4b_ctx* h, uint32_t p, const uint64_t* a, const uint64_t* b, co
 }  // extern "C"
 
 void f4b::basis_finish(Ctx* c) { basis_finish_impl(c); }
+bool f4b::basis_apply_lazy(Ctx* c) { return basis_apply_lazy_impl(c); }

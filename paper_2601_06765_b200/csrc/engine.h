@@ -31,6 +31,8 @@ void ensure(Ctx* c, DBuf& b, size_t bytes);  // grow-only; contents not preserve
 void ensure_keep(Ctx* c, DBuf& b, size_t bytes);  // grow-only; contents preserved
 void release(Ctx* c, DBuf& b);
 void basis_finish(Ctx* c);  // completes a pending asynchronous basis append
+bool basis_apply_lazy(Ctx* c);
+void recheck_lanes(Ctx* c, long long r0, const int32_t* rb, const uint16_t* shift);  // advances the host mirrors of a pending key append without waiting (true if pending)
 void pool_flush(Ctx* c);
 void check_cuda(cudaError_t e, const char* what);  // throws Error{F4B_ERR_CUDA}
 [[noreturn]] void fail(int code, const std::string& msg);
@@ -88,10 +90,17 @@ struct Ctx {
   // max-exponent mirrors) is completed by the next call that needs it
   struct PendingAppend {
     bool active = false;
-    long long n_polys = 0, T1 = 0, P1 = 0;
+    long long n_polys = 0, T0 = 0, P0 = 0, T1 = 0, P1 = 0;
     size_t o_lm = 0, o_mx = 0, o_bad = 0;
     std::vector<int64_t> lengths;
     DBuf raw;
+    // key appends of a graded ring: the host mirrors can be advanced before
+    // the device finishes (basis_apply_lazy) from the LMs read off the host
+    // keys, with deg(LM) as the bound of every exponent (terms descend in a
+    // graded order); basis_finish then checks the flag and installs the
+    // exact maximum exponents, or rolls the mirrors back
+    bool lazy_ok = false, applied = false;
+    std::vector<uint16_t> lm_host, bound_host;
   } pend;
   cudaStream_t stream = 0;
   cudaStream_t copy_stream = nullptr;  // plan prefetches (created on first use)

@@ -3101,8 +3101,15 @@ BatchFormat batch_format(Ctx* c, long long r0, const int32_t* rb, const uint16_t
     long long d = 0;
     for (int v = 0; v < n; ++v) {
       const long long s = shift[i * n + v];
-      if (s + B.h_maxe[(size_t)g * n + v] > 0xFFFF)
+      if (s + B.h_maxe[(size_t)g * n + v] > 0xFFFF) {
+        // h_maxe may still hold the deg(LM) bounds of a pending key append:
+        // decide on the exact maximum exponents
+        if (c->pend.active && c->pend.applied) {
+          basis_finish(c);
+          return batch_format(c, r0, rb, shift, cands, n_cands);
+        }
         fail(F4B_ERR_LANE_OVERFLOW, "shifted exponent overflows a 16-bit lane");
+      }
       d += s + B.h_lm[(size_t)g * n + v];
     }
     D = std::max(D, d);
@@ -3148,6 +3155,17 @@ BatchFormat batch_format(Ctx* c, long long r0, const int32_t* rb, const uint16_t
 }
 
 bool rank_path_ok_pub(const Ctx* c, int order, int n, long long D) { return rank_path_ok(c, order, n, D); }
+
+// The lane check of batch_format against the exact maximum exponents (after
+// a compile that ran on the deg(LM) bounds of a pending key append).
+void recheck_lanes(Ctx* c, long long r0, const int32_t* rb, const uint16_t* shift) {
+  const Basis& B = c->basis;
+  const int n = c->n_vars;
+  for (long long i = 0; i < r0; ++i)
+    for (int v = 0; v < n; ++v)
+      if ((long long)shift[i * n + v] + B.h_maxe[(size_t)rb[i] * n + v] > 0xFFFF)
+        fail(F4B_ERR_LANE_OVERFLOW, "shifted exponent overflows a 16-bit lane");
+}
 
 void encode_basis_kw(Ctx* c, const KeyFmt& f, int KW) {
   switch (KW) {

@@ -426,6 +426,25 @@ def test_basis_append_keys_matches_exps(cuda, order):
         got.append(eng.compile(rb, sh, True).download())
     for k in got[0]:
         assert np.array_equal(got[0][k], got[1][k]), k
+    # a shift that passes on the exact maximum exponent but not on the deg(LM)
+    # bound the pending key append starts from: both paths compile it alike
+    g = 0
+    mx = int(soa.exps[soa.offset[g]:soa.offset[g + 1], 0].max())
+    if ring.graded and int(soa.exps[soa.offset[g]].sum()) > mx:
+        sh1 = np.zeros((1, 6), np.int64)
+        sh1[0, 0] = 0xFFFF - mx
+        res = []
+        for keys in (soa.mon_key, None):
+            eng.clear_basis()
+            eng.append_polys(soa.length, soa.exps, soa.coeff, defer=True, keys=keys)
+            try:
+                res.append(eng.compile(np.array([g]), sh1, False).download())
+            except errors.FpgbError as e:
+                res.append(type(e))
+        if isinstance(res[0], dict):
+            assert isinstance(res[1], dict) and all(np.array_equal(res[0][k], res[1][k]) for k in res[0])
+        else:
+            assert res[0] == res[1]
     bad = soa.mon_key.copy()
     if ring.graded:
         bad[4, 0] += np.uint64(1 << 32)  # degree lane off by one
