@@ -373,7 +373,60 @@ static PyObject* gm_update(PyObject* self, PyObject* args) {
   return ret;
 }
 
+/* pack_keys(exps, K, n, graded, grevlex, W, out) -> 0 | 1 (lane overflow) |
+ * 2 (degree overflow): the reference keys of K exponent rows (monomials.py
+ * key_pack_vec / mon_key_pack), out uint64 [K][W]. */
+static PyObject* pack_keys(PyObject* self, PyObject* args) {
+  (void)self;
+  Py_buffer be, bo;
+  Py_ssize_t K, n, W;
+  int graded, grevlex;
+  if (!PyArg_ParseTuple(args, "y*nniinw*", &be, &K, &n, &graded, &grevlex, &W, &bo)) return NULL;
+  PyObject* ret = NULL;
+  if (K < 0 || n < 1 || W < 1 || be.len < K * n * 8 || bo.len < K * W * 8 || (graded ? 32 : 0) + 16 * n > 64 * W) {
+    PyErr_SetString(PyExc_ValueError, "pack_keys: buffer sizes");
+  } else {
+    const int64_t* e = (const int64_t*)be.buf;
+    uint64_t* out = (uint64_t*)bo.buf;
+    const int head = graded ? 32 : 0;
+    long code = 0;
+    Py_BEGIN_ALLOW_THREADS
+    for (Py_ssize_t t = 0; t < K && !code; ++t) {
+      const int64_t* x = e + t * n;
+      uint64_t* k = out + t * W;
+      for (Py_ssize_t w = 0; w < W; ++w) k[w] = 0;
+      uint64_t deg = 0;
+      for (Py_ssize_t v = 0; v < n; ++v) {
+        if (x[v] < 0 || x[v] > 0xFFFF) {
+          code = 1;
+          break;
+        }
+        deg += (uint64_t)x[v];
+      }
+      if (code) break;
+      if (graded) {
+        if (deg >> 32) {
+          code = 2;
+          break;
+        }
+        k[0] |= deg << 32;
+      }
+      for (Py_ssize_t i = 0; i < n; ++i) {
+        const uint64_t lane = grevlex ? 0xFFFFu - (uint64_t)x[n - 1 - i] : (uint64_t)x[i];
+        const int off = head + 16 * (int)i;
+        k[off >> 6] |= lane << (48 - (off & 63));
+      }
+    }
+    Py_END_ALLOW_THREADS
+    ret = PyLong_FromLong(code);
+  }
+  PyBuffer_Release(&be);
+  PyBuffer_Release(&bo);
+  return ret;
+}
+
 static PyMethodDef methods[] = {
+    {"pack_keys", pack_keys, METH_VARARGS, "pack_keys(exps, K, n, graded, grevlex, W, out) -> 0 | 1 | 2"},
     {"pack_rows", pack_rows, METH_VARARGS, "pack_rows(rows, n, rb_int32, shift_uint16) -> (min_basis, max_basis, lane_ok)"},
     {"gm_new_pairs", gm_new_pairs, METH_VARARGS, "gm_new_pairs(L, t, n, lm, surv_out) -> count"},
     {"gm_prune", gm_prune, METH_VARARGS, "gm_prune(plcm, pi, pj, P, L, n, lm, keep_out) -> kept"},

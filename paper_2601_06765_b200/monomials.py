@@ -133,6 +133,18 @@ def key_pack_vec(exps: np.ndarray, ring: Ring) -> np.ndarray:
     exps = np.asarray(exps)
     if exps.ndim != 2 or exps.shape[1] != ring.n_vars:
         raise ArityMismatchError(f"expected shape (K, {ring.n_vars}), got {exps.shape}")
+    if len(exps) >= 4096 and exps.dtype == np.int64 and exps.flags.c_contiguous:
+        # large blocks (the host basis copy): one pass in csrc/hostglue.cpp
+        from .hostglue import native
+
+        out = np.empty((exps.shape[0], ring.n_key_words), dtype=np.uint64)
+        code = native().pack_keys(exps, exps.shape[0], ring.n_vars, int(ring.graded), int(ring.order == "grevlex"),
+                                  ring.n_key_words, out)
+        if code == 1:
+            raise LaneOverflowError("exponent does not fit a 16-bit lane")
+        if code == 2:
+            raise LaneOverflowError("total degree does not fit the 32-bit degree lane")
+        return out
     if exps.size and (exps.min() < 0 or exps.max() > _LANE_MAX):
         raise LaneOverflowError("exponent does not fit a 16-bit lane")
     e = exps.astype(np.uint64)

@@ -400,3 +400,24 @@ def test_gm_update_native_matches_numpy_queue(order, seed):
         if rng.random() < 0.2 and m:
             k = int(rng.integers(1, m + 1))
             q = {kk: c(v[k:]) for kk, v in q.items()}
+
+
+@pytest.mark.parametrize("order", ["grevlex", "deglex", "lex"])
+def test_key_pack_native_matches_numpy(order):
+    """key_pack_vec on >= 4096 int64 rows (csrc/hostglue.cpp pack_keys) equals
+    the NumPy packing of the same rows in smaller blocks; lane overflow is
+    LaneOverflowError on both."""
+    from paper_2601_06765_b200 import _build
+
+    _build.build_hostglue()
+    for n in (2, 8, 11):
+        ring = Ring([f"x{i}" for i in range(n)], order, FieldModulus(32003))
+        e = np.random.default_rng(n).integers(0, 0x10000, (9000, n)).astype(np.int64)
+        big = key_pack_vec(e, ring)
+        small = np.concatenate([key_pack_vec(e[i:i + 1000], ring) for i in range(0, len(e), 1000)])
+        assert np.array_equal(big, small)
+        for i in range(0, len(e), 997):
+            assert tuple(int(x) for x in big[i]) == mon_key_pack(tuple(int(x) for x in e[i]), ring)
+        e[1234, n - 1] = 0x10000
+        with pytest.raises(errors.LaneOverflowError):
+            key_pack_vec(e, ring)
