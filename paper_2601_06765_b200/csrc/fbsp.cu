@@ -1733,6 +1733,7 @@ __global__ void __launch_bounds__(CL_THREADS) k_fbsp(const FbspArgs a) {
   u32* list = csm + ((a.bt_words + 3) & ~3);  // 16-byte aligned
   u32* slm = list + CL_LIST;
   __shared__ u32 ws[33];
+  __shared__ u32 s_red6[CL_THREADS / 32][6];  // fused BD reductions of a small round
   __shared__ u32 s_wn[CL_THREADS / 32], s_wl[CL_THREADS / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NWARP = CL_THREADS / 32;
@@ -2029,23 +2030,45 @@ __global__ void __launch_bounds__(CL_THREADS) k_fbsp(const FbspArgs a) {
     }
     grid.sync();
     if (tr) a.trace[rounds * 6 + 1] = gtimer();
-    // ---- BD: totals, this warp's row / term bases
-    u32 R, Mk, bn, bl;
+    // ---- BD: totals, this warp's row / term bases; a small round's new
+    // monomial counts are final here too, so the CTA's frontier base comes
+    // out of the same pass (one CTA barrier for all six sums)
+    u32 R, Mk, bn, bl, base = 0, total = 0;
     {
-      u32 tn = 0, tl = 0, pn = 0, pl = 0;
+      u32 v6[6] = {0u, 0u, 0u, 0u, 0u, 0u};  // tn, tl, pn, pl, total, base
       for (u32 b = tid; b < G; b += blockDim.x) {
         const uint2 v = __ldcg(reinterpret_cast<const uint2*>(a.tilecnt) + b);
-        tn += v.x;
-        tl += v.y;
+        const u32 x = big ? 0u : __ldcg(cur + b);
+        v6[0] += v.x;
+        v6[1] += v.y;
+        v6[4] += x;
         if (b < blockIdx.x) {
-          pn += v.x;
-          pl += v.y;
+          v6[2] += v.x;
+          v6[3] += v.y;
+          v6[5] += x;
         }
       }
-      R = block_sum_u32(tn, ws);
-      Mk = block_sum_u32(tl, ws);
-      bn = block_sum_u32(pn, ws);
-      bl = block_sum_u32(pl, ws);
+#pragma unroll
+      for (int q = 0; q < 6; ++q)
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v6[q] += __shfl_xor_sync(0xffffffffu, v6[q], o);
+      if (lane == 0)
+#pragma unroll
+        for (int q = 0; q < 6; ++q) s_red6[warp][q] = v6[q];
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        u32 t = 0;
+#pragma unroll
+        for (int w = 0; w < NWARP; ++w) t += s_red6[w][q];
+        v6[q] = t;
+      }
+      R = v6[0];
+      Mk = v6[1];
+      bn = v6[2];
+      bl = v6[3];
+      total = v6[4];
+      base = v6[5];
       for (int q = 0; q < warp; ++q) {
         bn += s_wn[q];
         bl += s_wl[q];
@@ -2139,8 +2162,7 @@ __global__ void __launch_bounds__(CL_THREADS) k_fbsp(const FbspArgs a) {
       grid.sync();
       if (tr) a.trace[rounds * 6 + 3] = gtimer();
     }
-    u32 base, total;
-    cta_bases([&](u32 b) { return __ldcg(cur + b); }, base, total);
+    if (big) cta_bases([&](u32 b) { return __ldcg(cur + b); }, base, total);
     if (total > a.front_cap) {
       flags |= LOOP_OVERFLOW;
       break;
