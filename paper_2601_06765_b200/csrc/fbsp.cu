@@ -1922,10 +1922,33 @@ __global__ void __launch_bounds__(CL_THREADS) k_fbsp(const FbspArgs a) {
   // a dictionary monomial, so the chunk counts are dcount - lcount)
   u32 nf = 0, N = 0, flags = 0, rounds = 0;
   {
-    u32 base, dummy;
-    cta_bases([&](u32 b) { return __ldcg(dcount + b); }, dummy, N);
+    // N, nf and this CTA's frontier base in one pass (one CTA barrier)
+    u32 v3[3] = {0u, 0u, 0u};
+    for (u32 b = tid; b < G; b += blockDim.x) {
+      const u32 d = __ldcg(dcount + b), f = a.closure ? d - __ldcg(lcount + b) : 0u;
+      v3[0] += d;
+      v3[1] += f;
+      if (b < blockIdx.x) v3[2] += f;
+    }
+#pragma unroll
+    for (int q = 0; q < 3; ++q)
+#pragma unroll
+      for (int o = 16; o; o >>= 1) v3[q] += __shfl_xor_sync(0xffffffffu, v3[q], o);
+    if (lane == 0)
+#pragma unroll
+      for (int q = 0; q < 3; ++q) s_red6[warp][q] = v3[q];
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      u32 t = 0;
+#pragma unroll
+      for (int w = 0; w < NWARP; ++w) t += s_red6[w][q];
+      v3[q] = t;
+    }
+    N = v3[0];
+    const u32 base = v3[2];
     if (a.closure) {
-      cta_bases([&](u32 b) { return __ldcg(dcount + b) - __ldcg(lcount + b); }, base, nf);
+      nf = v3[1];
       if (nf > a.front_cap) {
         flags |= LOOP_OVERFLOW;
       } else {
