@@ -1735,6 +1735,12 @@ __global__ void __launch_bounds__(CL_THREADS) k_fbsp(const FbspArgs a) {
   __shared__ u32 ws[33];
   __shared__ u32 s_red6[CL_THREADS / 32][6];  // fused BD reductions of a small round
   __shared__ u32 s_wn[CL_THREADS / 32], s_wl[CL_THREADS / 32];
+  // a group's reducer and exponent words per frontier monomial (small rounds,
+  // up to 32 monomials per group), kept from the search for the row writer
+  constexpr bool STASH = NV <= 16;
+  constexpr int JW = STASH ? (NV + 1) / 2 : 1;
+  __shared__ int s_jf[STASH ? CL_THREADS / 32 : 1][32];
+  __shared__ u32 s_je[STASH ? CL_THREADS / 32 : 1][32][JW];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NWARP = CL_THREADS / 32;
   constexpr int U = KW <= 2 ? 4 : 2;  // 32-term chunks in flight per warp
@@ -2018,6 +2024,12 @@ __global__ void __launch_bounds__(CL_THREADS) k_fbsp(const FbspArgs a) {
             ++cn;
             cl += __ldg(a.blen + found);
           }
+          if (STASH && j1 - j0 <= 32u) {
+            if (lane == 0) s_jf[warp][j - j0] = found;
+#pragma unroll
+            for (int w = 0; w < JW; ++w)
+              if (lane == w) s_je[warp][j - j0][w] = me[w];
+          }
         }
         if (found < 0 || big) continue;
         const u32 off = __ldg(a.boff + found), len = __ldg(a.blen + found);
@@ -2109,9 +2121,10 @@ __global__ void __launch_bounds__(CL_THREADS) k_fbsp(const FbspArgs a) {
     if (t0th) a.rows_start[r + R] = Mcur + Mk;
     // B: the group's rows, in frontier order (leader warp)
     if (leader) {
+      const bool stashed = STASH && j1 - j0 <= 32u;
       for (u32 jb = j0; jb < j1; jb += 32) {
         const u32 j = jb + lane;
-        const int g = j < j1 ? __ldcg(a.red + j) : -1;
+        const int g = j < j1 ? (stashed ? s_jf[warp][lane] : __ldcg(a.red + j)) : -1;
         const u32 len = g >= 0 ? __ldg(a.blen + g) : 0u;
         const unsigned bm = __ballot_sync(0xffffffffu, g >= 0);
         u32 lp = len;
@@ -2125,7 +2138,12 @@ __global__ void __launch_bounds__(CL_THREADS) k_fbsp(const FbspArgs a) {
           const long long q = (long long)bn + __popc(bm & lanemask_lt());
           const long long row = r + q;
           u16 e[NV];
-          gl_unrank<NV>(__ldcg(front + j), n, a.D, bt, a.st, e);
+          if (stashed) {
+#pragma unroll
+            for (int v = 0; v < NV; ++v) e[v] = (u16)(s_je[warp][lane][v / 2 < JW ? v / 2 : 0] >> (16 * (v & 1)));
+          } else {
+            gl_unrank<NV>(__ldcg(front + j), n, a.D, bt, a.st, e);
+          }
           const Key<KW> m = gl_encode<KW, NV>(a.f, e);
           a.rows_basis[row] = big ? g : ~g;  // ~g: ranks not parked in col (ranked in AC), the join ranks them
           key_store<KW>(a.rows_delta, row, key_sub<KW>(m, key_load<KW>(a.bckey, __ldg(a.boff + g))));
