@@ -1741,6 +1741,8 @@ __global__ void __launch_bounds__(CL_THREADS) k_fbsp(const FbspArgs a) {
   constexpr int JW = STASH ? (NV + 1) / 2 : 1;
   __shared__ int s_jf[STASH ? CL_THREADS / 32 : 1][32];
   __shared__ u32 s_je[STASH ? CL_THREADS / 32 : 1][32][JW];
+  __shared__ u32 s_jl[STASH ? CL_THREADS / 32 : 1][32];                       // reducer length
+  __shared__ unsigned long long s_jd[STASH ? CL_THREADS / 32 : 1][32][KW];  // row key delta (small rounds)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NWARP = CL_THREADS / 32;
   constexpr int U = KW <= 2 ? 4 : 2;  // 32-term chunks in flight per warp
@@ -2025,7 +2027,10 @@ __global__ void __launch_bounds__(CL_THREADS) k_fbsp(const FbspArgs a) {
             cl += __ldg(a.blen + found);
           }
           if (STASH && j1 - j0 <= 32u) {
-            if (lane == 0) s_jf[warp][j - j0] = found;
+            if (lane == 0) {
+              s_jf[warp][j - j0] = found;
+              s_jl[warp][j - j0] = found >= 0 ? __ldg(a.blen + found) : 0u;
+            }
 #pragma unroll
             for (int w = 0; w < JW; ++w)
               if (lane == w) s_je[warp][j - j0][w] = me[w];
@@ -2034,6 +2039,9 @@ __global__ void __launch_bounds__(CL_THREADS) k_fbsp(const FbspArgs a) {
         if (found < 0 || big) continue;
         const u32 off = __ldg(a.boff + found), len = __ldg(a.blen + found);
         const Key<KW> dl = key_sub<KW>(m, key_load<KW>(a.bckey, off));
+        if (STASH && leader && lane == 0 && j1 - j0 <= 32u)
+#pragma unroll
+          for (int w = 0; w < KW; ++w) s_jd[warp][j - j0][w] = dl.w[w];
         for (u32 c = sub; c * 32 < len; c += U * k) {
           u32 tt[U], rk[U], dw[U];
           rank_chunks(off, len, dl, sub, k, c, tt, rk);
@@ -2125,7 +2133,7 @@ __global__ void __launch_bounds__(CL_THREADS) k_fbsp(const FbspArgs a) {
       for (u32 jb = j0; jb < j1; jb += 32) {
         const u32 j = jb + lane;
         const int g = j < j1 ? (stashed ? s_jf[warp][lane] : __ldcg(a.red + j)) : -1;
-        const u32 len = g >= 0 ? __ldg(a.blen + g) : 0u;
+        const u32 len = g >= 0 ? (stashed ? s_jl[warp][lane] : __ldg(a.blen + g)) : 0u;
         const unsigned bm = __ballot_sync(0xffffffffu, g >= 0);
         u32 lp = len;
 #pragma unroll
@@ -2146,7 +2154,14 @@ __global__ void __launch_bounds__(CL_THREADS) k_fbsp(const FbspArgs a) {
           }
           const Key<KW> m = gl_encode<KW, NV>(a.f, e);
           a.rows_basis[row] = big ? g : ~g;  // ~g: ranks not parked in col (ranked in AC), the join ranks them
-          key_store<KW>(a.rows_delta, row, key_sub<KW>(m, key_load<KW>(a.bckey, __ldg(a.boff + g))));
+          if (stashed && !big) {
+            Key<KW> dl;
+#pragma unroll
+            for (int w = 0; w < KW; ++w) dl.w[w] = s_jd[warp][lane][w];
+            key_store<KW>(a.rows_delta, row, dl);
+          } else {
+            key_store<KW>(a.rows_delta, row, key_sub<KW>(m, key_load<KW>(a.bckey, __ldg(a.boff + g))));
+          }
           a.rows_start[row] = Mcur + bl + lp - len;
           bool over = false;
 #pragma unroll
