@@ -2619,9 +2619,12 @@ static void compile_rank_fused(Ctx* c, const KeyFmt& f, int D, long long r0, con
   fa.nw = nw;
   fa.stage_lm = stage_lm;
   {
-    // L2 prefetch of the basis streams when they fit comfortably (126 MB L2)
+    // L2 prefetch of the whole basis stream (experiment, F4B_L2_PREFETCH=1):
+    // measured 1.7 % slower on the cyclic-8 replays (a batch touches a few
+    // reducers, the prefetch pulls every term) and neutral on Katsura-11
+    static const bool l2pf = getenv("F4B_L2_PREFETCH") != nullptr;
     const unsigned long long bytes = (unsigned long long)B.n_terms * (KW * 8 + 4);
-    fa.prefetch_terms = bytes <= (48ull << 20) && !getenv("F4B_NO_PREFETCH") ? (unsigned long long)B.n_terms : 0ull;
+    fa.prefetch_terms = l2pf && bytes <= (48ull << 20) ? (unsigned long long)B.n_terms : 0ull;
   }
   fa.words = words;
   fa.maxlen = maxlen;
