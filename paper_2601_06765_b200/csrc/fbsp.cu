@@ -1708,7 +1708,8 @@ struct FbspArgs {
   int* red;
   u32* tilecnt;  // [2 * warps]
   u32* cnt;      // [4 * G] this call: new-bit counts (two parities), dictionary and lead counts per chunk
-  u32* cnt_next; // [4 * G] the next call's set, cleared here
+  u32* cnt_next; // the next call's set, cleared here ([0, cnt_clear))
+  u32 cnt_clear;
   int* rows_basis;
   u64* rows_delta;
   u32* rows_start;
@@ -1778,7 +1779,7 @@ __global__ void __launch_bounds__(CL_THREADS) k_fbsp(const FbspArgs a) {
     lmw = slm;
   }
   // the next call's counters are idle now: clear them
-  if (tid < 4) a.cnt_next[tid * G + blockIdx.x] = 0;
+  for (u32 i = blockIdx.x * blockDim.x + tid; i < a.cnt_clear; i += G * blockDim.x) a.cnt_next[i] = 0;
   if (blockIdx.x == 0 && tid == 0) *a.err = 0;  // nothing sets it before the first grid barrier
   __syncthreads();
   const u32 CH = max(1u, (a.maxlen + 31) / 32);
@@ -2573,13 +2574,16 @@ static void compile_rank_fused(Ctx* c, const KeyFmt& f, int D, long long r0, con
                "occupancy");
   const int bps_cached = bps_by_step[lstep];
   static const int bps_max = getenv("F4B_LOOP_BPS") ? atoi(getenv("F4B_LOOP_BPS")) : 2;
-  // batches below ~150k input terms: one CTA per SM (cheaper grid barriers;
-  // measured 5-20 us faster per cyclic-8 batch up to ~400k final terms),
-  // larger ones two per SM.  Fewer than one per SM was slower (the closure
-  // rounds' search and ranking spread over all warps).
+  // two CTAs per SM when they fit.  One per SM for batches below
+  // F4B_FBSP_SMALL_M0 input terms (an experiment knob, default 0 = never):
+  // cheaper grid barriers, but over the 38 cyclic-8 batches the fixed G is
+  // 2 % faster (5000: 1.3 %, 150k: 0 %; the tiny batches lose 2-4 us each,
+  // the medium and big ones gain more).  Fewer than one per SM was slower
+  // (the closure rounds' search and ranking spread over all warps).
   static const int g_env = getenv("F4B_FBSP_G") ? atoi(getenv("F4B_FBSP_G")) : 0;
   const int G_full = c->num_sms * std::max(1, std::min(bps_cached, bps_max));
-  const int G = g_env > 0 ? std::min(g_env, G_full) : (M0 < 150000u ? std::min(c->num_sms, G_full) : G_full);
+  static const unsigned small_m0 = getenv("F4B_FBSP_SMALL_M0") ? (unsigned)atoi(getenv("F4B_FBSP_SMALL_M0")) : 0u;
+  const int G = g_env > 0 ? std::min(g_env, G_full) : (M0 < small_m0 ? std::min(c->num_sms, G_full) : G_full);
   const size_t W = (size_t)G * (CL_THREADS / 32);
   ensure(c, c->loop_scratch, (2 * W + 16) * sizeof(u32));
   // presence maps dict | done | newbits: zero on entry (kept zero by the
@@ -2596,14 +2600,18 @@ static void compile_rank_fused(Ctx* c, const KeyFmt& f, int D, long long r0, con
   u32* d_new = d_done + words;
   // chunk counters: set `parity` for this call (zero), the other set is
   // cleared by the kernel for the next call
-  if (c->fcnt_G != G || !c->fcnt.p) {
-    ensure(c, c->fcnt, (size_t)8 * G * sizeof(u32));
-    check_cuda(cudaMemsetAsync(c->fcnt.p, 0, (size_t)8 * G * sizeof(u32), c->stream), "memset counters");
-    c->fcnt_G = G;
+  // two sets of per-CTA counters at a fixed stride for any G up to the
+  // buffer's: the kernel clears the whole next set, so a change of G between
+  // calls needs no memset (only growth does)
+  const int Gset = std::max(G, 2 * c->num_sms);
+  if (c->fcnt_G < Gset || !c->fcnt.p) {
+    ensure(c, c->fcnt, (size_t)8 * Gset * sizeof(u32));
+    check_cuda(cudaMemsetAsync(c->fcnt.p, 0, (size_t)8 * Gset * sizeof(u32), c->stream), "memset counters");
+    c->fcnt_G = Gset;
     c->fcnt_parity = 0;
   }
-  u32* d_cnt = c->fcnt.as<u32>() + (size_t)4 * G * c->fcnt_parity;
-  u32* d_cnt_next = c->fcnt.as<u32>() + (size_t)4 * G * (1 - c->fcnt_parity);
+  u32* d_cnt = c->fcnt.as<u32>() + (size_t)4 * c->fcnt_G * c->fcnt_parity;
+  u32* d_cnt_next = c->fcnt.as<u32>() + (size_t)4 * c->fcnt_G * (1 - c->fcnt_parity);
   c->fcnt_parity ^= 1;
   ensure(c, c->dwp, (size_t)(words + 1) * sizeof(uint2));
 
@@ -2658,6 +2666,7 @@ static void compile_rank_fused(Ctx* c, const KeyFmt& f, int D, long long r0, con
   fa.tilecnt = c->loop_scratch.as<u32>();
   fa.cnt = d_cnt;
   fa.cnt_next = d_cnt_next;
+  fa.cnt_clear = (u32)(4 * c->fcnt_G);
   fa.rows_basis = c->rows_basis.as<int>();
   fa.rows_delta = c->rows_delta.as<u64>();
   fa.rows_start = pl->row_ptr.as<u32>();
