@@ -1710,6 +1710,7 @@ struct FbspArgs {
   u32* cnt;      // [4 * G] this call: new-bit counts (two parities), dictionary and lead counts per chunk
   u32* cnt_next; // the next call's set, cleared here ([0, cnt_clear))
   u32 cnt_clear;
+  u32 big_nf;    // frontier size from which a round ranks over balanced term ranges (0: one per warp of the grid)
   int* rows_basis;
   u64* rows_delta;
   u32* rows_start;
@@ -1988,7 +1989,7 @@ __global__ void __launch_bounds__(CL_THREADS) k_fbsp(const FbspArgs a) {
     // big rounds (nf >= W): search only here, the reducer rows' terms are
     // ranked after the rows are written, over balanced term ranges (two more
     // barriers); small rounds rank inside the search groups
-    const bool big = nf >= W;
+    const bool big = nf >= (a.big_nf ? a.big_nf : W);
     u32 k, j0, j1, sub;
     groups_of(nf, big ? 1u : CH, k, j0, j1, sub);
     const bool leader = sub == 0;
@@ -2667,6 +2668,8 @@ static void compile_rank_fused(Ctx* c, const KeyFmt& f, int D, long long r0, con
   fa.cnt = d_cnt;
   fa.cnt_next = d_cnt_next;
   fa.cnt_clear = (u32)(4 * c->fcnt_G);
+  static const int big_env = getenv("F4B_FBSP_BIG_NF") ? atoi(getenv("F4B_FBSP_BIG_NF")) : 0;  // experiment knob
+  fa.big_nf = (u32)std::max(0, big_env);
   fa.rows_basis = c->rows_basis.as<int>();
   fa.rows_delta = c->rows_delta.as<u64>();
   fa.rows_start = pl->row_ptr.as<u32>();
