@@ -1917,11 +1917,19 @@ __global__ void __launch_bounds__(CL_THREADS) k_fbsp(const FbspArgs a) {
         }
 #pragma unroll
       for (int q = 0; q < U; ++q) dw[q] = tt[q] < t_hi ? __ldcg(a.dict + (rk[q] >> 5)) : 0xFFFFFFFFu;  // L2 filter
+      // lanes whose bits fall in the same word combine them: one atomicOr
+      // per distinct word of the warp (a row's consecutive terms often share
+      // a word), the new bits counted by the lane that issued it
 #pragma unroll
       for (int q = 0; q < U; ++q) {
-        if (tt[q] >= t_hi) continue;
         const u32 w = rk[q] >> 5, bit = 1u << (rk[q] & 31);
-        if (!(dw[q] & bit) && !(atomicOr(a.dict + w, bit) & bit)) atomicAdd(dcount + w / cw, 1u);
+        const bool need = tt[q] < t_hi && !(dw[q] & bit);
+        const unsigned grp = __match_any_sync(0xffffffffu, need ? w : 0xFFFFFFFFu);
+        const u32 gb = __reduce_or_sync(grp, need ? bit : 0u);
+        if (need && lane == __ffs(grp) - 1) {
+          const u32 nb = gb & ~atomicOr(a.dict + w, gb);
+          if (nb) atomicAdd(dcount + w / cw, (u32)__popc(nb));
+        }
       }
     }
   });
