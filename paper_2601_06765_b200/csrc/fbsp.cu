@@ -1747,7 +1747,7 @@ __global__ void __launch_bounds__(CL_THREADS) k_fbsp(const FbspArgs a) {
   __shared__ unsigned long long s_jd[STASH ? CL_THREADS / 32 : 1][32][KW];  // row key delta (small rounds)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NWARP = CL_THREADS / 32;
-  constexpr int U = KW <= 2 ? 4 : 2;  // 32-term chunks in flight per warp
+  constexpr int U = 1;  // 32-term chunks per warp step (U = 4 / 2 / 1 measured 2.90e9 / 3.04e9 / 3.08e9 nnz/s: finer term ranges)
   const int n = a.f.n_vars;
   const u32 G = gridDim.x, W = G * NWARP, gw = blockIdx.x * NWARP + warp;
   // pull the basis keys / coefficients into L2 (one 128-byte line per
