@@ -1226,6 +1226,8 @@ F4B_DEV unsigned long long gtimer() {
 }
 
 static constexpr int CL_THREADS = 256;
+// k_fbsp: 512 threads, one CTA per SM slot pair (256: 3.08e9, 512: 3.11e9 nnz/s)
+static constexpr int FB_THREADS = 512;
 static constexpr int CL_LIST = 2048;
 
 F4B_DEV u32 block_sum_u32(u32 v, u32* ws) {
@@ -1727,7 +1729,7 @@ struct FbspArgs {
 };
 
 template <int KW, int NV>
-__global__ void __launch_bounds__(CL_THREADS) k_fbsp(const FbspArgs a) {
+__global__ void __launch_bounds__(FB_THREADS) k_fbsp(const FbspArgs a) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) u32 csm[];
@@ -1735,18 +1737,18 @@ __global__ void __launch_bounds__(CL_THREADS) k_fbsp(const FbspArgs a) {
   u32* list = csm + ((a.bt_words + 3) & ~3);  // 16-byte aligned
   u32* slm = list + CL_LIST;
   __shared__ u32 ws[33];
-  __shared__ u32 s_red6[CL_THREADS / 32][6];  // fused BD reductions of a small round
-  __shared__ u32 s_wn[CL_THREADS / 32], s_wl[CL_THREADS / 32];
+  __shared__ u32 s_red6[FB_THREADS / 32][6];  // fused BD reductions of a small round
+  __shared__ u32 s_wn[FB_THREADS / 32], s_wl[FB_THREADS / 32];
   // a group's reducer and exponent words per frontier monomial (small rounds,
   // up to 32 monomials per group), kept from the search for the row writer
   constexpr bool STASH = NV <= 16;
   constexpr int JW = STASH ? (NV + 1) / 2 : 1;
-  __shared__ int s_jf[STASH ? CL_THREADS / 32 : 1][32];
-  __shared__ u32 s_je[STASH ? CL_THREADS / 32 : 1][32][JW];
-  __shared__ u32 s_jl[STASH ? CL_THREADS / 32 : 1][32];                       // reducer length
-  __shared__ unsigned long long s_jd[STASH ? CL_THREADS / 32 : 1][32][KW];  // row key delta (small rounds)
+  __shared__ int s_jf[STASH ? FB_THREADS / 32 : 1][32];
+  __shared__ u32 s_je[STASH ? FB_THREADS / 32 : 1][32][JW];
+  __shared__ u32 s_jl[STASH ? FB_THREADS / 32 : 1][32];                       // reducer length
+  __shared__ unsigned long long s_jd[STASH ? FB_THREADS / 32 : 1][32][KW];  // row key delta (small rounds)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int NWARP = CL_THREADS / 32;
+  constexpr int NWARP = FB_THREADS / 32;
   constexpr int U = 1;  // 32-term chunks per warp step (U = 4 / 2 / 1 measured 2.90e9 / 3.04e9 / 3.08e9 nnz/s: finer term ranges)
   const int n = a.f.n_vars;
   const u32 G = gridDim.x, W = G * NWARP, gw = blockIdx.x * NWARP + warp;
@@ -2579,7 +2581,7 @@ static void compile_rank_fused(Ctx* c, const KeyFmt& f, int D, long long r0, con
   static int bps_by_step[16] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
   const int lstep = (int)std::min<size_t>(15, lsm / 8192);
   if (bps_by_step[lstep] < 0)
-    check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps_by_step[lstep], (k_fbsp<KW, NV>), CL_THREADS, lsm),
+    check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps_by_step[lstep], (k_fbsp<KW, NV>), FB_THREADS, lsm),
                "occupancy");
   const int bps_cached = bps_by_step[lstep];
   static const int bps_max = getenv("F4B_LOOP_BPS") ? atoi(getenv("F4B_LOOP_BPS")) : 2;
@@ -2593,7 +2595,7 @@ static void compile_rank_fused(Ctx* c, const KeyFmt& f, int D, long long r0, con
   const int G_full = c->num_sms * std::max(1, std::min(bps_cached, bps_max));
   static const unsigned small_m0 = getenv("F4B_FBSP_SMALL_M0") ? (unsigned)atoi(getenv("F4B_FBSP_SMALL_M0")) : 0u;
   const int G = g_env > 0 ? std::min(g_env, G_full) : (M0 < small_m0 ? std::min(c->num_sms, G_full) : G_full);
-  const size_t W = (size_t)G * (CL_THREADS / 32);
+  const size_t W = (size_t)G * (FB_THREADS / 32);
   ensure(c, c->loop_scratch, (2 * W + 16) * sizeof(u32));
   // presence maps dict | done | newbits: zero on entry (kept zero by the
   // kernel; cleared here after growth or an aborted run)
@@ -2700,7 +2702,7 @@ static void compile_rank_fused(Ctx* c, const KeyFmt& f, int D, long long r0, con
   {
     void* args[] = {&fa};
     ProfScope ps(c, "k_fbsp");
-    check_cuda(cudaLaunchCooperativeKernel((void*)(k_fbsp<KW, NV>), G, CL_THREADS, args, lsm, c->stream), "k_fbsp");
+    check_cuda(cudaLaunchCooperativeKernel((void*)(k_fbsp<KW, NV>), G, FB_THREADS, args, lsm, c->stream), "k_fbsp");
   }
   mark("launched");
   check_cuda(cudaEventRecord(ev1, c->stream), "event record");
