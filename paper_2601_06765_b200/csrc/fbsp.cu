@@ -2585,12 +2585,12 @@ static void compile_rank_fused(Ctx* c, const KeyFmt& f, int D, long long r0, con
                "occupancy");
   const int bps_cached = bps_by_step[lstep];
   static const int bps_max = getenv("F4B_LOOP_BPS") ? atoi(getenv("F4B_LOOP_BPS")) : 2;
-  // two CTAs per SM when they fit.  One per SM for batches below
-  // F4B_FBSP_SMALL_M0 input terms (an experiment knob, default 0 = never):
-  // cheaper grid barriers, but over the 38 cyclic-8 batches the fixed G is
-  // 2 % faster (5000: 1.3 %, 150k: 0 %; the tiny batches lose 2-4 us each,
-  // the medium and big ones gain more).  Fewer than one per SM was slower
-  // (the closure rounds' search and ranking spread over all warps).
+  // as many CTAs per SM as fit, up to F4B_LOOP_BPS (2): with FB_THREADS =
+  // 512 that is one.  F4B_FBSP_SMALL_M0 (experiment knob, default 0 = never)
+  // drops batches below that many input terms to one CTA per SM; with
+  // 256-thread CTAs this measured 2 % slower over the 38 cyclic-8 batches
+  // than two per SM for every batch.  Fewer than one per SM was slower (the
+  // closure rounds' search and ranking spread over all warps).
   static const int g_env = getenv("F4B_FBSP_G") ? atoi(getenv("F4B_FBSP_G")) : 0;
   const int G_full = c->num_sms * std::max(1, std::min(bps_cached, bps_max));
   static const unsigned small_m0 = getenv("F4B_FBSP_SMALL_M0") ? (unsigned)atoi(getenv("F4B_FBSP_SMALL_M0")) : 0u;
